@@ -1,0 +1,167 @@
+/* dbfft.h — C ABI of the B200-native DBFFT hot path.
+ *
+ * DBFFT (Lucarini & Segurado, arXiv 1905.12725; "P:<line>" = /root/reference/PAPER.md line)
+ * solves the periodic cell problem with the Fourier displacement u_hat(xi) as the unknown.
+ * This library implements, on one CUDA device (sm_100a) per process, the matrix-free operator
+ *     K u_hat = -d_hat : F( C(x) : F^-1( s_hat . u_hat ) )                 (Eq. lineqf)
+ * (symmetric gradient s_hat at small strain; full gradient g_hat at finite strain),
+ * its mixed-control augmentation, the averaged-stiffness preconditioner
+ * (Eqs. pred2/pred3), preconditioned CG and the Newton driver with per-voxel
+ * constitutive updates.  Every call returns a dbfft_status; no C++ exception crosses
+ * the ABI.  There is no CPU fallback: a call that cannot run on the GPU fails with DBFFT_E_CUDA.
+ *
+ * Conventions (SURVEY.md "Notation"; readings R1..R22 listed in DESIGN.md):
+ *  - Grid n = {n1, n2, n3} voxels (x, y, z); each n_a a power of two in [8, 512].
+ *    Cell lengths L = {L1, L2, L3} > 0.  Voxel (i,j,k) has centre ((i+1/2)L1/n1, ...).
+ *  - Frequencies (Eq. 1) in FFT-native order, xi_a(k) = 2 pi kappa / L_a with
+ *    kappa = k (k < n/2), k - n (k > n/2) and xi_a = 0 at the Nyquist index k = n/2 (R1).
+ *  - Spectra are mean-normalised (R5): u_hat = F(u)/(n1 n2 n3), so u_hat(0) = <u>.
+ *  - SPECTRAL VECTOR layout (device, complex128 = two doubles {re, im}):
+ *        [3 components][ky = 0..n2-1][kz = 0..n3-1][kx = 0..n1/2]        (kx fastest)
+ *    i.e. the half spectrum of a real field (R6).  H = (n1/2+1) n2 n3 points per component.
+ *    dbfft_spectral_layout() returns the same as shape/strides (in complex elements).
+ *    Inputs must be Hermitian-consistent on the kx = 0 and kx = n1/2 planes (true for any
+ *    spectrum of a real field); the operator uses their Hermitian part.
+ *  - REAL FIELD layout (host or device, double): [component][z][y][x] (x fastest).
+ *    Second-order tensors have 9 components, row-major (c = 3 i + j).
+ *  - Macro 3x3 quantities (targets, masks, e blocks, reports): 9 entries, row-major.
+ *  - Ownership: the ctx owns all of its device memory (cudaMalloc).  Pointers passed in are
+ *    borrowed for the duration of the call only; inputs are copied when retained.
+ *  - Streams: all device work of a ctx is issued on env->cuda_stream (a cudaStream_t, e.g.
+ *    torch.cuda.current_stream().cuda_stream) or on a ctx-owned stream if NULL.  Calls marked
+ *    (async) return before the device work completes; the others synchronise that stream.
+ *  - Distribution: env->world == 1 in this version (slab decomposition reserved).
+ */
+#ifndef DBFFT_H
+#define DBFFT_H
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dbfft_ctx_s* dbfft_ctx;
+
+typedef enum {
+  DBFFT_OK = 0,
+  DBFFT_E_INVALID_GRID = 1,  /* n_a not a power of two in [8,512], or L_a <= 0            */
+  DBFFT_E_INVALID_ARG = 2,   /* null pointer, unknown kind, phase id >= n_phases, bad parameters */
+  DBFFT_E_STATE = 3,         /* call-order violation, e.g. apply_K before set_phases             */
+  DBFFT_E_CUDA = 4,          /* CUDA error (message in dbfft_last_error)                          */
+  DBFFT_E_NCCL = 5,          /* reserved (multi-GPU)                                              */
+  DBFFT_E_OOM = 6,           /* device allocation failed                                          */
+  DBFFT_E_NOT_CONVERGED = 7, /* PCG max_cg or Newton max_newton exhausted; report filled; state
+                                rolled back to the last commit                                   */
+  DBFFT_E_BREAKDOWN = 8,     /* NaN/Inf or <p,Kp> <= 0 in PCG                                     */
+  DBFFT_E_MATERIAL = 9       /* det F <= 0 at some voxel (report.bad_voxel)                       */
+} dbfft_status;
+
+typedef enum { DBFFT_SMALL_STRAIN = 6, DBFFT_FINITE_STRAIN = 9 } dbfft_kinematics;
+
+typedef struct {
+  int32_t rank, world;   /* world must be 1 in this version                        */
+  const void* nccl_id;   /* reserved, NULL                                         */
+  void* cuda_stream;     /* cudaStream_t or NULL (ctx creates its own stream)      */
+  int32_t device;        /* CUDA device ordinal (-1: current device)               */
+} dbfft_env;
+
+/* Create a context for grid n (voxels) and cell lengths L.  (sync) */
+dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinematics,
+                          const dbfft_env* env, dbfft_ctx* out);
+dbfft_status dbfft_destroy(dbfft_ctx ctx);
+/* Last error message of ctx (NULL ctx: last creation error); valid until the next call. */
+const char* dbfft_last_error(dbfft_ctx ctx);
+/* shape[4] = {3, n2, n3, n1/2+1}; strides[4] in complex elements. */
+dbfft_status dbfft_spectral_layout(dbfft_ctx ctx, int64_t shape[4], int64_t strides[4]);
+
+/* Material laws, one record per phase ("the behavior at a point x defined by the
+ * constitutive equation of the phase occupying that point").  Parameters in p[]:
+ *   DBFFT_MAT_ISO      : p = {E, nu}                      linear isotropic   small strain
+ *   DBFFT_MAT_CUBIC    : p = {C11, C12, C44, R[9]}        cubic crystal, stiffness rotated
+ *                        C'_ijkl = R_ia R_jb R_kc R_ld C_abcd, R row-major        small strain
+ *   DBFFT_MAT_NEOHOOKE : p = {mu, kappa}                  compressible neo-Hookean (R14)   finite
+ *   DBFFT_MAT_J2       : p = {E, nu, sigma_y, n, edot0}   J2 Perzyna overstress (R16)     small
+ * Linear kinds require no state; NEOHOOKE and J2 keep per-voxel state.            */
+typedef enum {
+  DBFFT_MAT_ISO = 1,
+  DBFFT_MAT_CUBIC = 2,
+  DBFFT_MAT_NEOHOOKE = 3,
+  DBFFT_MAT_J2 = 4
+} dbfft_mat_kind;
+typedef struct { int32_t kind; double p[36]; } dbfft_material;
+
+/* Phase id per voxel ([z][y][x], uint16, host if on_device == 0 else device) and the per-phase
+ * table (host, copied).  All phases must be of one family: linear (ISO/CUBIC), NEOHOOKE (finite
+ * strain ctx) or J2.  Resets the mechanical state to the undeformed configuration.  (sync)  */
+dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t on_device,
+                              int32_t n_phases, const dbfft_material* table);
+
+/* f_hat = K u_hat with the current stiffness/tangent (positive form, R3).  u_hat, f_hat:
+ * device spectral vectors (layout above), may not alias.  Output is 0 on the null set Z.
+ * Nonlinear materials use the tangent of the last dbfft_eval_state / Newton iteration.  (async) */
+dbfft_status dbfft_apply_K(dbfft_ctx ctx, const void* u_hat, void* f_hat);
+/* Mixed-control augmented operator: the strain argument gains the macro block
+ * e_in (host, 9, row-major; used on mask entries only) and r_out (host, 9) receives
+ * P_mask <C:(F^-1(s.u) + e)> (the xi = 0 rows).  mask: host, 9 bytes, 1 = stress
+ * controlled.  With mask all 0 this equals dbfft_apply_K and r_out = 0.  (sync)               */
+dbfft_status dbfft_apply_K_aug(dbfft_ctx ctx, const uint8_t mask[9], const void* u_hat,
+                               const double e_in[9], void* f_hat, double r_out[9]);
+/* z_hat = M(xi) r_hat, M = [xi . Cbar . xi]^-1 off Z and 0 on Z (R4), Cbar the volume
+ * average of the current stiffness/tangent.  Device vectors.  (async)         */
+dbfft_status dbfft_precond(dbfft_ctx ctx, const void* r_hat, void* z_hat);
+/* Evaluate the constitutive law at the real field `field` ([9][z][y][x] doubles: eps (small
+ * strain, symmetric) or F (finite strain)), host or device, from the committed state, and
+ * install the resulting tangent for apply_K / precond (no state is committed).  dt is used by
+ * rate-dependent laws.  Linear materials: no-op.  (sync)                                    */
+dbfft_status dbfft_eval_state(dbfft_ctx ctx, const double* field, int32_t on_device, double dt);
+
+typedef struct {
+  double tol_eq;       /* PCG stop: eps_eq = ||div sigma||_L2/||<sigma>||, default 1e-10 */
+  double tol_load;     /* mixed control: ||P(<sigma> - sigma_bar)||/||<sigma>||, 1e-10  */
+  double tol_newton;   /* Newton stop: max |grad du + dF_f|, default 1e-6               */
+  int32_t max_cg;      /* default 10000                                                 */
+  int32_t max_newton;  /* default 25                                                            */
+  int32_t check_every; /* host convergence poll period in CG iterations (default 4)             */
+  int32_t precond_refresh; /* 0: mean tangent at the first Newton iterate of every increment
+                              (R12); 1: every Newton iteration                            */
+} dbfft_opts;
+dbfft_opts dbfft_default_opts(void);
+
+typedef struct {
+  int32_t converged, cg_iters, newton_iters, status;
+  double eps_eq, eps_load, max_dgrad;
+  double macro_strain[9];  /* <eps> (small strain) or <F> (finite strain), row-major          */
+  double macro_stress[9];  /* <sigma> or <P>                                                    */
+  int64_t bad_voxel;       /* first voxel with det F <= 0, else -1                              */
+  double seconds;          /* device time of the call                                          */
+} dbfft_report;
+
+/* Advance one load increment to the TOTAL target.  mask[a] = 1: component a is stress
+ * controlled (target is sigma or P); 0: strain controlled (eps or F) (IJ != ij).  Small
+ * strain targets and masks must be symmetric.  Linear materials: one PCG solve of the
+ * (augmented) system.  Nonlinear: Newton.  dt: increment duration.
+ * On success the state is committed; on failure it is rolled back.  (sync)                   */
+dbfft_status dbfft_solve_increment(dbfft_ctx ctx, const double target[9], const uint8_t mask[9],
+                                   double dt, const dbfft_opts* opts, dbfft_report* report);
+
+typedef enum {
+  DBFFT_FIELD_U = 0,        /* fluctuation displacement u~(x): 3 x N doubles          */
+  DBFFT_FIELD_STRAIN = 1,   /* eps (small) or F (finite): 9 x N doubles                        */
+  DBFFT_FIELD_STRESS = 2,   /* sigma (small) or P (finite): 9 x N doubles                      */
+  DBFFT_FIELD_U_HAT = 3     /* u~_hat, spectral vector layout (3 x H complex)                  */
+} dbfft_field;
+/* Copy a field of the committed state into `out` (host if out_on_device == 0). (sync) */
+dbfft_status dbfft_get_field(dbfft_ctx ctx, int32_t which, void* out, int32_t out_on_device);
+
+/* Per-kernel device-time accounting (CUDA events around each launch of the named pass
+ * kernels, accumulated while enabled).  names: comma-separated list written to buf. */
+dbfft_status dbfft_profile_enable(dbfft_ctx ctx, int32_t enable);
+dbfft_status dbfft_profile_read(dbfft_ctx ctx, int32_t kernel_id, double* total_ms, int64_t* launches);
+const char* dbfft_profile_name(int32_t kernel_id);
+int32_t dbfft_profile_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DBFFT_H */

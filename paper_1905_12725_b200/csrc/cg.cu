@@ -1,0 +1,432 @@
+// cg.cu — PCG vector algebra with the preconditioner applied on the fly.
+//
+// Vectors are half spectra [3][ky][kz][kx] (R6); inner products weight kx = 0 and kx = n1/2 by
+// 1 and the other kx by 2, and take Re() (the full-spectrum Hermitian product, mean-normalised
+// spectra so it equals the voxel-mean product by Parseval, R5/R7).  z = M(xi) r is never stored:
+// M(xi) = [xi.Cbar.xi]^-1 is rebuilt per point from 36 coefficients (~70 flops) in the update
+// and direction kernels (HBM-bound work, no table read).  Reductions are two-stage and
+// deterministic: per-CTA partials in a fixed grid, then one CTA sums them in a fixed order.
+#include "cg.cuh"
+
+namespace {
+
+constexpr int BLK = 256;
+constexpr int NBLK = 148 * 4;
+
+struct Pt {
+  double xx, xy, xz;
+  double w;
+  bool null;
+};
+
+DBF_DEV Pt point(const SpecGeom& g, long long i) {
+  const int kx = (int)(i % g.n1h);
+  const long long rest = i / g.n1h;
+  const int kz = (int)(rest % g.n3);
+  const int ky = (int)(rest / g.n3);
+  Pt p;
+  p.xx = __ldg(g.fq.xx + kx);
+  p.xy = __ldg(g.fq.xy + ky);
+  p.xz = __ldg(g.fq.xz + kz);
+  p.w = (kx == 0 || 2 * kx == g.n1) ? 1.0 : 2.0;
+  p.null = (p.xx == 0.0 && p.xy == 0.0 && p.xz == 0.0);
+  return p;
+}
+
+// z = A^-1 r with A = xi.Cbar.xi (symmetric 3x3), 0 on the null set Z (R4)
+DBF_DEV void apply_M(const PrecQ& Q, const Pt& p, const cplx* r, cplx* z) {
+  if (p.null) {
+    z[0] = z[1] = z[2] = make_double2(0.0, 0.0);
+    return;
+  }
+  const double q[6] = {p.xx * p.xx, p.xy * p.xy, p.xz * p.xz, p.xy * p.xz, p.xx * p.xz, p.xx * p.xy};
+  double A[6];
+#pragma unroll
+  for (int m = 0; m < 6; ++m) {
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) a = fma(Q.Q[6 * m + k], q[k], a);
+    A[m] = a;
+  }
+  // A = [[A0, A5, A4], [A5, A1, A3], [A4, A3, A2]]
+  const double c00 = A[1] * A[2] - A[3] * A[3];
+  const double c01 = A[4] * A[3] - A[5] * A[2];
+  const double c02 = A[5] * A[3] - A[1] * A[4];
+  const double c11 = A[0] * A[2] - A[4] * A[4];
+  const double c12 = A[5] * A[4] - A[0] * A[3];
+  const double c22 = A[0] * A[1] - A[5] * A[5];
+  const double id = 1.0 / (A[0] * c00 + A[5] * c01 + A[4] * c02);
+  z[0] = make_double2((c00 * r[0].x + c01 * r[1].x + c02 * r[2].x) * id, (c00 * r[0].y + c01 * r[1].y + c02 * r[2].y) * id);
+  z[1] = make_double2((c01 * r[0].x + c11 * r[1].x + c12 * r[2].x) * id, (c01 * r[0].y + c11 * r[1].y + c12 * r[2].y) * id);
+  z[2] = make_double2((c02 * r[0].x + c12 * r[1].x + c22 * r[2].x) * id, (c02 * r[0].y + c12 * r[1].y + c22 * r[2].y) * id);
+}
+
+DBF_DEV double cdot(cplx a, cplx b) { return a.x * b.x + a.y * b.y; }  // Re(conj(a) b)
+
+template <int NV>
+DBF_DEV void block_store(double (&v)[NV], double* partials) {
+  __shared__ double red[BLK / 32][NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double s = warp_sum(v[k]);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][k] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double s = 0.0;
+    for (int w = 0; w < BLK / 32; ++w) s += red[w][threadIdx.x];
+    partials[(long long)blockIdx.x * NV + threadIdx.x] = s;
+  }
+}
+
+__global__ void __launch_bounds__(BLK) k_precond(SpecGeom g, PrecQ Q, const cplx* __restrict__ r, cplx* __restrict__ z) {
+  for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < g.Hs; i += (long long)gridDim.x * BLK) {
+    Pt p = point(g, i);
+    cplx rv[3] = {__ldg(r + i), __ldg(r + g.Hs + i), __ldg(r + 2 * g.Hs + i)};
+    cplx zv[3];
+    apply_M(Q, p, rv, zv);
+    z[i] = zv[0];
+    z[g.Hs + i] = zv[1];
+    z[2 * g.Hs + i] = zv[2];
+  }
+}
+
+// p = M r ; partials (<r, p>, <r, r>)
+__global__ void __launch_bounds__(BLK) k_cg_init(SpecGeom g, PrecQ Q, const cplx* __restrict__ r, cplx* __restrict__ pv, double* partials) {
+  double acc[2] = {0.0, 0.0};
+  for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < g.Hs; i += (long long)gridDim.x * BLK) {
+    Pt p = point(g, i);
+    cplx rv[3] = {__ldg(r + i), __ldg(r + g.Hs + i), __ldg(r + 2 * g.Hs + i)};
+    cplx zv[3];
+    apply_M(Q, p, rv, zv);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      pv[c * g.Hs + i] = zv[c];
+      acc[0] += p.w * cdot(rv[c], zv[c]);
+      acc[1] += p.w * cdot(rv[c], rv[c]);
+    }
+  }
+  block_store<2>(acc, partials);
+}
+
+// x += alpha p ; r -= alpha q ; z = M r ; partials (<r, z>, <r, r>)
+__global__ void __launch_bounds__(BLK) k_cg_update(SpecGeom g, PrecQ Q, const CgDev* __restrict__ cg, cplx* __restrict__ x,
+                                                   const cplx* __restrict__ pv, cplx* __restrict__ r, const cplx* __restrict__ qv,
+                                                   double* partials) {
+  if (cg->converged | cg->breakdown) return;
+  const double alpha = cg->alpha;
+  double acc[2] = {0.0, 0.0};
+  for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < g.Hs; i += (long long)gridDim.x * BLK) {
+    Pt p = point(g, i);
+    cplx rv[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const long long j = c * g.Hs + i;
+      cplx pj = __ldg(pv + j), xj = x[j], rj = r[j], qj = __ldg(qv + j);
+      xj.x = fma(alpha, pj.x, xj.x); xj.y = fma(alpha, pj.y, xj.y);
+      rj.x = fma(-alpha, qj.x, rj.x); rj.y = fma(-alpha, qj.y, rj.y);
+      x[j] = xj;
+      r[j] = rj;
+      rv[c] = rj;
+    }
+    cplx zv[3];
+    apply_M(Q, p, rv, zv);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      acc[0] += p.w * cdot(rv[c], zv[c]);
+      acc[1] += p.w * cdot(rv[c], rv[c]);
+    }
+  }
+  block_store<2>(acc, partials);
+}
+
+// p = M r + beta p
+__global__ void __launch_bounds__(BLK) k_cg_direction(SpecGeom g, PrecQ Q, const CgDev* __restrict__ cg, cplx* __restrict__ pv,
+                                                      const cplx* __restrict__ r) {
+  if (cg->converged | cg->breakdown) return;
+  const double beta = cg->beta;
+  for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < g.Hs; i += (long long)gridDim.x * BLK) {
+    Pt p = point(g, i);
+    cplx rv[3] = {__ldg(r + i), __ldg(r + g.Hs + i), __ldg(r + 2 * g.Hs + i)};
+    cplx zv[3];
+    apply_M(Q, p, rv, zv);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const long long j = c * g.Hs + i;
+      cplx pj = pv[j];
+      pv[j] = make_double2(fma(beta, pj.x, zv[c].x), fma(beta, pj.y, zv[c].y));
+    }
+  }
+}
+
+// r = b - Ax ; partial <r, r>
+__global__ void __launch_bounds__(BLK) k_true_residual(SpecGeom g, const cplx* __restrict__ b, const cplx* __restrict__ ax,
+                                                       cplx* __restrict__ r, double* partials) {
+  double acc[1] = {0.0};
+  for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < g.Hs; i += (long long)gridDim.x * BLK) {
+    Pt p = point(g, i);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const long long j = c * g.Hs + i;
+      cplx bj = __ldg(b + j), aj = __ldg(ax + j);
+      cplx rj = make_double2(bj.x - aj.x, bj.y - aj.y);
+      r[j] = rj;
+      acc[0] += p.w * cdot(rj, rj);
+    }
+  }
+  block_store<1>(acc, partials);
+}
+
+__global__ void __launch_bounds__(BLK) k_axpy(SpecGeom g, cplx* __restrict__ y, const cplx* __restrict__ x, double a) {
+  for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < 3 * g.Hs; i += (long long)gridDim.x * BLK) {
+    cplx xv = __ldg(x + i), yv = y[i];
+    y[i] = make_double2(fma(a, xv.x, yv.x), fma(a, xv.y, yv.y));
+  }
+}
+
+// ---- single-CTA finalizers ---------------------------------------------------------------------
+// sum partials[j*nred + k] over j for k < nred into out[k] (slot 9 of nred = 10 is a max)
+DBF_DEV void cta_reduce(const double* partials, int nblk, int nred, double* out) {
+  __shared__ double red[BLK];
+  for (int k = 0; k < nred; ++k) {
+    const bool is_max = (nred == 10 && k == 9);
+    double s = 0.0;
+    for (int j = threadIdx.x; j < nblk; j += BLK) {
+      double v = partials[(long long)j * nred + k];
+      s = is_max ? fmax(s, v) : s + v;
+    }
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = BLK / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w) red[threadIdx.x] = is_max ? fmax(red[threadIdx.x], red[threadIdx.x + w]) : red[threadIdx.x] + red[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[k] = red[0];
+    __syncthreads();
+  }
+}
+
+DBF_DEV void sym9(double* m) {  // small strain: only 6 Voigt slots were accumulated
+  m[3] = m[1];
+  m[6] = m[2];
+  m[7] = m[5];
+}
+
+DBF_DEV double norm9(const double* m) {
+  double s = 0.0;
+  for (int a = 0; a < 9; ++a) s += m[a] * m[a];
+  return sqrt(s);
+}
+
+__global__ void __launch_bounds__(BLK) k_fin_init(CgDev* cg, const double* partials, int nblk) {
+  __shared__ double s[2];
+  cta_reduce(partials, nblk, 2, s);
+  if (threadIdx.x == 0) {
+    for (int a = 0; a < 9; ++a) {
+      double z = 0.0;
+      for (int b = 0; b < 9; ++b) z += cg->Minv_e[9 * a + b] * cg->re[b];
+      cg->ze[a] = z;
+    }
+    double rze = 0.0, ree = 0.0;
+    for (int a = 0; a < 9; ++a) {
+      cg->pe[a] = cg->ze[a];
+      rze += cg->re[a] * cg->ze[a];
+      ree += cg->re[a] * cg->re[a];
+    }
+    cg->rz = s[0] + rze;
+    cg->rr = s[1];
+    const double den = fmax(norm9(cg->msig), 1e-300);
+    cg->eps_eq = sqrt(s[1]) / den;
+    cg->eps_load = cg->macro ? sqrt(ree) / den : 0.0;
+    cg->converged = (cg->eps_eq <= cg->tol_eq && cg->eps_load <= cg->tol_load) ? 1 : 0;
+    if (!(cg->rz == cg->rz)) cg->breakdown = 1;
+  }
+}
+
+__global__ void __launch_bounds__(BLK) k_fin_alpha(CgDev* cg, const double* pq_part, int npq, const double* dc_part, int ndc, int nred) {
+  if (cg->converged | cg->breakdown) return;
+  __shared__ double s[1];
+  __shared__ double dc[10];
+  cta_reduce(pq_part, npq, 1, s);
+  cta_reduce(dc_part, ndc, nred, dc);
+  if (threadIdx.x == 0) {
+    for (int a = 0; a < 9; ++a) cg->dc[a] = dc[a] * cg->inv_n;
+    if (cg->sym) sym9(cg->dc);
+    double pq = s[0];
+    for (int a = 0; a < 9; ++a) {
+      cg->qe[a] = cg->mask[a] * cg->dc[a];
+      pq += cg->pe[a] * cg->qe[a];
+    }
+    cg->pq = pq;
+    if (!(pq > 0.0) || !(pq == pq)) {
+      cg->breakdown = 1;
+      return;
+    }
+    const double alpha = cg->rz / pq;
+    cg->alpha = alpha;
+    for (int a = 0; a < 9; ++a) {
+      cg->xe[a] += alpha * cg->pe[a];
+      cg->re[a] -= alpha * cg->qe[a];
+      cg->msig[a] += alpha * cg->dc[a];
+    }
+    for (int a = 0; a < 9; ++a) {
+      double z = 0.0;
+      for (int b = 0; b < 9; ++b) z += cg->Minv_e[9 * a + b] * cg->re[b];
+      cg->ze[a] = z;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(BLK) k_fin_beta(CgDev* cg, const double* partials, int nblk) {
+  if (cg->converged | cg->breakdown) return;
+  __shared__ double s[2];
+  cta_reduce(partials, nblk, 2, s);
+  if (threadIdx.x == 0) {
+    double rze = 0.0, ree = 0.0;
+    for (int a = 0; a < 9; ++a) {
+      rze += cg->re[a] * cg->ze[a];
+      ree += cg->re[a] * cg->re[a];
+    }
+    const double rz_new = s[0] + rze;
+    cg->rr = s[1];
+    cg->iters += 1;
+    const double den = fmax(norm9(cg->msig), 1e-300);
+    cg->eps_eq = sqrt(s[1]) / den;
+    cg->eps_load = cg->macro ? sqrt(ree) / den : 0.0;
+    if (!(rz_new == rz_new)) {
+      cg->breakdown = 1;
+      return;
+    }
+    if (cg->eps_eq <= cg->tol_eq && cg->eps_load <= cg->tol_load) {
+      cg->converged = 1;
+      return;
+    }
+    const double beta = rz_new / cg->rz;
+    cg->beta = beta;
+    cg->rz = rz_new;
+    for (int a = 0; a < 9; ++a) cg->pe[a] = cg->ze[a] + beta * cg->pe[a];
+    if (cg->iters >= cg->max_iter) cg->converged = 2;  // exhausted
+  }
+}
+
+// true residual: r = b - Ax already formed; msig = msig0 + <sigma(x)>; re = be - P<sigma(x)>
+__global__ void __launch_bounds__(BLK) k_fin_true(CgDev* cg, const double* rr_part, int nblk, const double* dc_part, int ndc, int nred) {
+  __shared__ double s[1];
+  __shared__ double dc[10];
+  cta_reduce(rr_part, nblk, 1, s);
+  cta_reduce(dc_part, ndc, nred, dc);
+  if (threadIdx.x == 0) {
+    for (int a = 0; a < 9; ++a) cg->dc[a] = dc[a] * cg->inv_n;
+    if (cg->sym) sym9(cg->dc);
+    double ree = 0.0;
+    for (int a = 0; a < 9; ++a) {
+      cg->msig[a] = cg->msig0[a] + cg->dc[a];
+      cg->re[a] = cg->be[a] - cg->mask[a] * cg->dc[a];
+      ree += cg->re[a] * cg->re[a];
+    }
+    const double den = fmax(norm9(cg->msig), 1e-300);
+    cg->rr = s[0];
+    cg->eps_eq = sqrt(s[0]) / den;
+    cg->eps_load = cg->macro ? sqrt(ree) / den : 0.0;
+    cg->converged = (cg->eps_eq <= cg->tol_eq && cg->eps_load <= cg->tol_load) ? 1 : 0;
+  }
+}
+
+__global__ void __launch_bounds__(BLK) k_reduce(const double* partials, int nblk, int nred, double* out) {
+  __shared__ double s[64];
+  cta_reduce(partials, nblk, nred, s);
+  if (threadIdx.x < nred) out[threadIdx.x] = s[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(BLK) k_mean_sym(const double* __restrict__ tan, int nk, long long nvox, double* partials) {
+  // partials[block][nk]; nk <= 45
+  double acc[45];
+  for (int k = 0; k < 45; ++k) acc[k] = 0.0;
+  for (long long v = (long long)blockIdx.x * BLK + threadIdx.x; v < nvox; v += (long long)gridDim.x * BLK)
+    for (int k = 0; k < nk; ++k) acc[k] += __ldg(tan + (long long)k * nvox + v);
+  __shared__ double red[BLK / 32][45];
+  for (int k = 0; k < nk; ++k) {
+    double s = warp_sum(acc[k]);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][k] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < nk) {
+    double s = 0.0;
+    for (int w = 0; w < BLK / 32; ++w) s += red[w][threadIdx.x];
+    partials[(long long)blockIdx.x * nk + threadIdx.x] = s;
+  }
+}
+
+__global__ void k_phase_hist(const uint16_t* __restrict__ ph, long long nvox, unsigned long long* counts, int nphase, int* bad) {
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < nvox; v += (long long)gridDim.x * blockDim.x) {
+    const int p = ph[v];
+    if (p >= nphase) atomicExch(bad, 1);
+    else atomicAdd(counts + p, 1ull);
+  }
+}
+
+__global__ void k_fill(double* p, long long n, double v) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) p[i] = v;
+}
+
+}  // namespace
+
+int cg_blocks() { return NBLK; }
+
+cudaError_t launch_precond(const SpecGeom& g, const PrecQ& q, const cplx* r, cplx* z, cudaStream_t s) {
+  k_precond<<<NBLK, BLK, 0, s>>>(g, q, r, z);
+  return cudaGetLastError();
+}
+cudaError_t launch_cg_init(const SpecGeom& g, const PrecQ& q, const cplx* r, cplx* p, double* partials, int nblk, cudaStream_t s) {
+  k_cg_init<<<nblk, BLK, 0, s>>>(g, q, r, p, partials);
+  return cudaGetLastError();
+}
+cudaError_t launch_cg_update(const SpecGeom& g, const PrecQ& q, CgDev* cg, cplx* x, const cplx* p, cplx* r, const cplx* qv,
+                             double* partials, int nblk, cudaStream_t s) {
+  k_cg_update<<<nblk, BLK, 0, s>>>(g, q, cg, x, p, r, qv, partials);
+  return cudaGetLastError();
+}
+cudaError_t launch_cg_direction(const SpecGeom& g, const PrecQ& q, const CgDev* cg, cplx* p, const cplx* r, cudaStream_t s) {
+  k_cg_direction<<<NBLK, BLK, 0, s>>>(g, q, cg, p, r);
+  return cudaGetLastError();
+}
+cudaError_t launch_fin_init(CgDev* cg, const double* partials, int nblk, cudaStream_t s) {
+  k_fin_init<<<1, BLK, 0, s>>>(cg, partials, nblk);
+  return cudaGetLastError();
+}
+cudaError_t launch_fin_alpha(CgDev* cg, const double* pq_part, int npq, const double* dc_part, int ndc, int nred, cudaStream_t s) {
+  k_fin_alpha<<<1, BLK, 0, s>>>(cg, pq_part, npq, dc_part, ndc, nred);
+  return cudaGetLastError();
+}
+cudaError_t launch_fin_beta(CgDev* cg, const double* partials, int nblk, cudaStream_t s) {
+  k_fin_beta<<<1, BLK, 0, s>>>(cg, partials, nblk);
+  return cudaGetLastError();
+}
+cudaError_t launch_true_residual(const SpecGeom& g, const cplx* b, const cplx* Ax, cplx* r, double* partials, int nblk, cudaStream_t s) {
+  k_true_residual<<<nblk, BLK, 0, s>>>(g, b, Ax, r, partials);
+  return cudaGetLastError();
+}
+cudaError_t launch_fin_true(CgDev* cg, const double* rr_part, int nblk, const double* dc_part, int ndc, int nred, cudaStream_t s) {
+  k_fin_true<<<1, BLK, 0, s>>>(cg, rr_part, nblk, dc_part, ndc, nred);
+  return cudaGetLastError();
+}
+cudaError_t launch_axpy(const SpecGeom& g, cplx* y, const cplx* x, double a, cudaStream_t s) {
+  k_axpy<<<NBLK, BLK, 0, s>>>(g, y, x, a);
+  return cudaGetLastError();
+}
+cudaError_t launch_reduce(const double* partials, int nblk, int nred, double* out, cudaStream_t s) {
+  k_reduce<<<1, BLK, 0, s>>>(partials, nblk, nred, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_mean_sym(const double* tan, int nk, long long nvox, double* partials, int nblk, cudaStream_t s) {
+  k_mean_sym<<<nblk, BLK, 0, s>>>(tan, nk, nvox, partials);
+  return cudaGetLastError();
+}
+cudaError_t launch_phase_hist(const uint16_t* ph, long long nvox, unsigned long long* counts, int nphase, int* bad, cudaStream_t s) {
+  k_phase_hist<<<NBLK, BLK, 0, s>>>(ph, nvox, counts, nphase, bad);
+  return cudaGetLastError();
+}
+cudaError_t launch_fill(double* p, long long n, double v, cudaStream_t s) {
+  k_fill<<<NBLK, BLK, 0, s>>>(p, n, v);
+  return cudaGetLastError();
+}

@@ -1,0 +1,48 @@
+// cg.cuh — device-resident PCG state and launchers (cg.cu).
+#pragma once
+#include "common.cuh"
+#include "passes.cuh"
+
+// Scalars of the preconditioned CG on the augmented system {u_hat | e}, kept
+// on the device so an iteration needs no host round trip; the host polls `converged`.
+struct CgDev {
+  double rz, pq, alpha, beta, rr, rz_new;
+  double eps_eq, eps_load;
+  double tol_eq, tol_load;
+  double inv_n;
+  double xe[9], re[9], pe[9], qe[9], ze[9], be[9];
+  double msig[9];      // tracked <sigma> of the current iterate (R7)
+  double msig0[9];     // <sigma> at x = 0
+  double dc[9];        // <sigma(p)> of the latest operator application
+  double mask[9];      // 1 = stress controlled
+  double Minv_e[81];   // (P Cbar P)^-1 on the stress-controlled subspace (R4), 9x9 row-major
+  int converged, breakdown, iters, sym, macro, max_iter, pad0, pad1;
+};
+
+// spectral-point preconditioner coefficients: A_m(xi) = sum_p Q[m][p] q_p(xi),
+// m over (xx,yy,zz,yz,xz,xy) of A = xi.Cbar.xi, q = (x x, y y, z z, y z, x z, x y) products.
+struct PrecQ { double Q[36]; };
+
+struct SpecGeom {
+  int n1h, n2, n3;
+  long long Hs;         // points per component
+  Freq fq;              // xy already offset to the local ky slab
+  int n1;
+};
+
+cudaError_t launch_precond(const SpecGeom& g, const PrecQ& q, const cplx* r, cplx* z, cudaStream_t s);
+cudaError_t launch_cg_init(const SpecGeom& g, const PrecQ& q, const cplx* r, cplx* p, double* partials, int nblk, cudaStream_t s);
+cudaError_t launch_cg_update(const SpecGeom& g, const PrecQ& q, CgDev* cg, cplx* x, const cplx* p, cplx* r, const cplx* qv,
+                             double* partials, int nblk, cudaStream_t s);
+cudaError_t launch_cg_direction(const SpecGeom& g, const PrecQ& q, const CgDev* cg, cplx* p, const cplx* r, cudaStream_t s);
+cudaError_t launch_fin_init(CgDev* cg, const double* partials, int nblk, cudaStream_t s);
+cudaError_t launch_fin_alpha(CgDev* cg, const double* pq_part, int npq, const double* dc_part, int ndc, int nred, cudaStream_t s);
+cudaError_t launch_fin_beta(CgDev* cg, const double* partials, int nblk, cudaStream_t s);
+cudaError_t launch_true_residual(const SpecGeom& g, const cplx* b, const cplx* Ax, cplx* r, double* partials, int nblk, cudaStream_t s);
+cudaError_t launch_fin_true(CgDev* cg, const double* rr_part, int nblk, const double* dc_part, int ndc, int nred, cudaStream_t s);
+cudaError_t launch_axpy(const SpecGeom& g, cplx* y, const cplx* x, double a, cudaStream_t s);
+cudaError_t launch_reduce(const double* partials, int nblk, int nred, double* out, cudaStream_t s);
+cudaError_t launch_mean_sym(const double* tan, int nk, long long nvox, double* partials, int nblk, cudaStream_t s);
+cudaError_t launch_phase_hist(const uint16_t* ph, long long nvox, unsigned long long* counts, int nphase, int* bad, cudaStream_t s);
+cudaError_t launch_fill(double* p, long long n, double v, cudaStream_t s);
+int cg_blocks();

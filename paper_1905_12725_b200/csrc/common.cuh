@@ -1,0 +1,175 @@
+// common.cuh — device helpers shared by the DBFFT kernels (complex fp64, in-CTA FFT).
+//
+// FFT design (B200-first): every pass FFTs along ONE axis for a batch of
+// lines held by one CTA.  A length-N transform is done by N/8 threads, each holding 8 points in
+// registers (a[s] <-> position g + s*N/8).  Stages are radix-8 (then one radix-4 or radix-2
+// stage when N is not a power of 8), Stockham order, exchanging through shared memory; the
+// first stage loads straight from global memory and the last stage's registers go straight to
+// global memory, so the fused pointwise pre/post operations (gradient, divergence, contraction)
+// touch registers only.  Twiddles come from a table of W_N = exp(-2 pi i k/N) computed on the
+// host in long double (accurate to 0.5 ulp), never from sincos recurrences.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define DBF_DEV __device__ __forceinline__
+
+typedef double2 cplx;
+
+DBF_DEV cplx cmk(double r, double i) { return make_double2(r, i); }
+DBF_DEV cplx cadd(cplx a, cplx b) { return make_double2(a.x + b.x, a.y + b.y); }
+DBF_DEV cplx csub(cplx a, cplx b) { return make_double2(a.x - b.x, a.y - b.y); }
+DBF_DEV cplx cmul(cplx a, cplx b) { return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+DBF_DEV cplx cconj(cplx a) { return make_double2(a.x, -a.y); }
+DBF_DEV cplx cscale(cplx a, double s) { return make_double2(a.x * s, a.y * s); }
+// i*s*a  (multiplication by the imaginary number i s)
+DBF_DEV cplx cimul(cplx a, double s) { return make_double2(-a.y * s, a.x * s); }
+// a + i*s*b
+DBF_DEV cplx cfma_i(cplx a, double s, cplx b) { return make_double2(a.x - s * b.y, a.y + s * b.x); }
+
+// ---------------------------------------------------------------------------------------------
+// In-register DFTs.  INV = false: exp(-2 pi i jk/R); INV = true: exp(+2 pi i jk/R).
+// ---------------------------------------------------------------------------------------------
+template <bool INV>
+DBF_DEV cplx mul_mi(cplx a) {  // forward: multiply by -i ; inverse: by +i
+  return INV ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
+
+template <bool INV>
+DBF_DEV void dft2(cplx& a, cplx& b) {
+  cplx t = a;
+  a = cadd(t, b);
+  b = csub(t, b);
+}
+
+template <bool INV>
+DBF_DEV void dft4(cplx& x0, cplx& x1, cplx& x2, cplx& x3) {
+  cplx t0 = cadd(x0, x2), t1 = csub(x0, x2);
+  cplx t2 = cadd(x1, x3), t3 = mul_mi<INV>(csub(x1, x3));
+  x0 = cadd(t0, t2);
+  x2 = csub(t0, t2);
+  x1 = cadd(t1, t3);
+  x3 = csub(t1, t3);
+}
+
+template <bool INV>
+DBF_DEV void dft8(cplx* x) {
+  const double h = 0.70710678118654752440;
+  cplx e0 = x[0], e1 = x[2], e2 = x[4], e3 = x[6];
+  cplx o0 = x[1], o1 = x[3], o2 = x[5], o3 = x[7];
+  dft4<INV>(e0, e1, e2, e3);
+  dft4<INV>(o0, o1, o2, o3);
+  // o_k *= W8^k
+  o1 = INV ? make_double2(h * (o1.x - o1.y), h * (o1.x + o1.y)) : make_double2(h * (o1.x + o1.y), h * (o1.y - o1.x));
+  o2 = mul_mi<INV>(o2);
+  o3 = INV ? make_double2(-h * (o3.x + o3.y), h * (o3.x - o3.y)) : make_double2(h * (o3.y - o3.x), -h * (o3.x + o3.y));
+  x[0] = cadd(e0, o0); x[4] = csub(e0, o0);
+  x[1] = cadd(e1, o1); x[5] = csub(e1, o1);
+  x[2] = cadd(e2, o2); x[6] = csub(e2, o2);
+  x[3] = cadd(e3, o3); x[7] = csub(e3, o3);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Stage plan: radix-8 stages, then one radix-(N / 8^k) stage if N is not a power of 8.
+// ---------------------------------------------------------------------------------------------
+template <int N>
+struct FftPlan {
+  static constexpr int log2n = (N == 8) ? 3 : (N == 16) ? 4 : (N == 32) ? 5 : (N == 64) ? 6 : (N == 128) ? 7 : (N == 256) ? 8 : (N == 512) ? 9 : (N == 1024) ? 10 : -1;
+  static_assert(log2n > 0, "unsupported FFT length");
+  static constexpr int n8 = log2n / 3;                  // number of radix-8 stages
+  static constexpr int last = 1 << (log2n - 3 * n8);    // 1, 2 or 4
+  static constexpr int nstages = n8 + (last > 1 ? 1 : 0);
+};
+
+// One Stockham stage of radix R on the register array a[8] (positions g + s*N/8), reading
+// was already done; writes outputs to smem via idx(pos).  Ns = product of previous radices.
+template <int N, int R, bool INV>
+DBF_DEV void stage_compute(cplx (&a)[8], int g, int Ns, const cplx* __restrict__ tw) {
+  constexpr int M = 8 / R;  // butterflies per thread
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int b = g + m * (N / 8);
+    const int k = b % Ns;
+    if (Ns > 1) {
+      const int step = (N / (Ns * R)) * k;
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        cplx w = __ldg(tw + r * step);
+        if (INV) w.y = -w.y;
+        a[m + M * r] = cmul(a[m + M * r], w);
+      }
+    }
+    if (R == 8) {
+      dft8<INV>(a);
+    } else if (R == 4) {
+      dft4<INV>(a[m], a[m + M], a[m + 2 * M], a[m + 3 * M]);
+    } else {
+      dft2<INV>(a[m], a[m + M]);
+    }
+  }
+}
+
+// Full in-CTA FFT.  On entry a[s] = x[g + s*N/8]; on exit a[s] = X[g + s*N/8].
+// IDX(pos) maps a line position to a shared-memory slot (column interleave or padding).
+// All threads of the CTA must call this (it contains __syncthreads()).
+template <int N, bool INV, class IDX>
+DBF_DEV void fft_cta(cplx (&a)[8], cplx* sbuf, int g, const IDX& idx, const cplx* __restrict__ tw) {
+  typedef FftPlan<N> P;
+  int Ns = 1;
+#pragma unroll
+  for (int st = 0; st < P::nstages; ++st) {
+    constexpr int dummy = 0;
+    (void)dummy;
+    const bool is_last = (st == P::nstages - 1);
+    const int R = (st < P::n8) ? 8 : P::last;
+    if (st > 0) {
+      // load a[s] = buf[g + s*N/8]
+#pragma unroll
+      for (int s = 0; s < 8; ++s) a[s] = sbuf[idx(g + s * (N / 8))];
+    }
+    if (R == 8) stage_compute<N, 8, INV>(a, g, Ns, tw);
+    else if (R == 4) stage_compute<N, 4, INV>(a, g, Ns, tw);
+    else stage_compute<N, 2, INV>(a, g, Ns, tw);
+    if (!is_last) {
+      __syncthreads();  // everyone finished reading the buffer
+      const int M = 8 / R;
+#pragma unroll
+      for (int m = 0; m < 8 / 2; ++m) {
+        if (m >= M) break;
+        const int b = g + m * (N / 8);
+        const int base = (b / Ns) * Ns * R + (b % Ns);
+        for (int r = 0; r < R; ++r) sbuf[idx(base + r * Ns)] = a[m + M * r];
+      }
+      if (M == 8) {  // unreachable (R >= 2 gives M <= 4); kept for clarity
+      }
+      __syncthreads();
+    }
+    Ns *= R;
+  }
+}
+
+// Column interleave: element (pos, column c) at pos*COLS + c.
+template <int COLS>
+struct IdxCols {
+  int c;
+  DBF_DEV int operator()(int pos) const { return pos * COLS + c; }
+};
+// One line per buffer, one pad complex per 8 (bank-conflict-free radix-8 scatter).
+struct IdxPad {
+  int base;
+  DBF_DEV int operator()(int pos) const { return base + pos + (pos >> 3); }
+};
+
+// ---------------------------------------------------------------------------------------------
+// Warp/block reductions (deterministic order).
+// ---------------------------------------------------------------------------------------------
+DBF_DEV double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+DBF_DEV double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}

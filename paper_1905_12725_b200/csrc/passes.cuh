@@ -1,0 +1,88 @@
+// passes.cuh — geometry/parameter structs shared by the pass kernels and the host driver.
+#pragma once
+#include "common.cuh"
+
+// Frequency tables (Eq. 1 with the Nyquist reading R1), device arrays.
+struct Freq {
+  const double* xx;  // [n1h]
+  const double* xy;  // [n2]
+  const double* xz;  // [n3]
+};
+
+// Column pass (FFT along z or y) geometry.  Field f, outer index o, position p, kx:
+//   addr = f*fs + o*os + (p / pchunk)*pcs + (p % pchunk)*ps + kx      (complex elements)
+// pchunk/pcs express rank-blocked layouts of a distributed transpose (pchunk = N: plain).
+struct ColGeom {
+  const cplx* in;
+  cplx* out;
+  long long in_fs, in_os, in_ps, in_pcs;
+  long long out_fs, out_os, out_ps, out_pcs;
+  int in_pchunk, out_pchunk;
+  int n1h;
+  long long ncols;   // n_outer * n1h columns
+  const cplx* tw;    // twiddles W_N[k], k < N
+  Freq fq;
+  // fused <p, out> (F3): weighted Hermitian dot with a vector in the output layout
+  const cplx* dotp;
+  double* partials;  // one double per CTA
+  int n1;            // full x length (weights: kx = 0 and n1/2 count once)
+};
+
+// Column pass kinds
+enum ColKind {
+  COL_I1S = 0,  // small strain, z inverse: u(3) -> {u_x, u_y, eps_zz, eps_xz, eps_yz}
+  COL_I1F,      // finite strain, z inverse: u(3) -> {u_i, G_iz}
+  COL_I2S,      // small strain, y inverse: 5 -> eps (Voigt 6)
+  COL_I2F,      // finite strain, y inverse: 6 -> 9 (G_ix holds u_i until the x pass)
+  COL_F2S,      // small strain, y forward: sigma (6) -> 6
+  COL_F2F,      // finite strain, y forward: 9 -> {g_i, P_iz}
+  COL_F3S,      // small strain, z forward + divergence: 6 -> f (3)
+  COL_F3F,      // finite strain, z forward + divergence: 6 -> f (3)
+  COL_ZI3,      // plain z inverse of a vector (3)
+  COL_YI3,      // plain y inverse of a vector (3)
+  COL_NKINDS
+};
+
+// X pass (lines along x: C2R -> per-voxel op -> R2C) voxel-op kinds
+enum XKind {
+  X_K_SMALL_PHASE = 0,  // sigma = C_phase : (eps + e)            (apply_K, linear)
+  X_K_SMALL_TAN,        // sigma = C_alg(x) : (eps + e)           (apply_K, J2 tangent)
+  X_K_FIN_TAN,          // dP = K(x) : (G + e)                    (apply_K, finite strain)
+  X_RHS_SMALL_PHASE,    // -sigma = -C_phase : e                  (rhs of the linear system)
+  X_CONST_FIN,          // F += G + dF; P, K (neo-Hookean); -P    (Newton residual)
+  X_CONST_J2,           // eps += G + de; J2 return map; -sigma   (Newton residual)
+  X_REAL_OUT,           // C2R only -> real fields
+  X_NKINDS
+};
+
+struct XGeom {
+  const cplx* in;       // [f][line][kx], line = z*n2 + y
+  cplx* out;
+  long long fs_in, fs_out;
+  int n1h, n1;
+  long long nlines;
+  const cplx* tw;       // twiddles W_{n1}
+  const double* xix;    // xi_x [n1h]
+  double inv_n;         // 1 / (n1 n2 n3)
+  double* partials;     // per CTA reduction outputs [grid][nred]
+  int nred;
+  // materials / state (SoA, voxel index = line*n1 + x)
+  const uint16_t* phase;
+  const double* ptable;   // per phase: 36 doubles (linear Voigt 6x6 row-major) / params
+  const double* e;        // 9 macro doubles (device) or null
+  double* tan;            // tangent SoA [21 or 45][N]
+  double* F;              // finite: F SoA [9][N]; J2: eps SoA [6][N]
+  const double* epsp_c;   // J2 committed plastic strain [6][N]
+  double* epsp_t;         // J2 trial plastic strain [6][N]
+  double dt;
+  long long nvox;
+  double* real_out;       // X_REAL_OUT: [f][N]
+  int* bad;               // first bad voxel flag (atomicMin on voxel index)
+  int has_in;             // constitutive kinds: 0 = no C2R input (uniform increment only)
+};
+
+// host launchers (passes.cu)
+cudaError_t launch_col(int kind, int N, const ColGeom& g, cudaStream_t s);
+cudaError_t launch_x(int kind, int N1, const XGeom& g, cudaStream_t s, int* grid_out);
+int x_grid(int kind, int N1, long long nlines);
+int col_grid(int N, long long ncols);

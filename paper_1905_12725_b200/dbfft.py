@@ -1,0 +1,263 @@
+"""Thin ctypes binding of libdbfft.so (include/dbfft.h).  Argument marshalling only: every
+step of the hot path runs in the CUDA kernels of csrc/.  torch provides device memory and
+streams.  There is no CPU fallback: if the extension is missing this module raises."""
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdbfft.so")
+
+# ---------------------------------------------------------------------------- C types
+
+
+class Env(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
+                ("cuda_stream", ctypes.c_void_p), ("device", ctypes.c_int32)]
+
+
+class Material(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("p", ctypes.c_double * 36)]
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("tol_eq", ctypes.c_double), ("tol_load", ctypes.c_double), ("tol_newton", ctypes.c_double),
+                ("max_cg", ctypes.c_int32), ("max_newton", ctypes.c_int32), ("check_every", ctypes.c_int32),
+                ("precond_refresh", ctypes.c_int32)]
+
+
+class Report(ctypes.Structure):
+    _fields_ = [("converged", ctypes.c_int32), ("cg_iters", ctypes.c_int32), ("newton_iters", ctypes.c_int32),
+                ("status", ctypes.c_int32), ("eps_eq", ctypes.c_double), ("eps_load", ctypes.c_double),
+                ("max_dgrad", ctypes.c_double), ("macro_strain", ctypes.c_double * 9),
+                ("macro_stress", ctypes.c_double * 9), ("bad_voxel", ctypes.c_int64), ("seconds", ctypes.c_double)]
+
+
+MAT_ISO, MAT_CUBIC, MAT_NEOHOOKE, MAT_J2 = 1, 2, 3, 4
+FIELD_U, FIELD_STRAIN, FIELD_STRESS, FIELD_U_HAT = 0, 1, 2, 3
+STATUS = {0: "OK", 1: "E_INVALID_GRID", 2: "E_INVALID_ARG", 3: "E_STATE", 4: "E_CUDA", 5: "E_NCCL", 6: "E_OOM",
+          7: "E_NOT_CONVERGED", 8: "E_BREAKDOWN", 9: "E_MATERIAL"}
+
+# every symbol declared in include/dbfft.h
+EXPORTS = ["dbfft_create", "dbfft_destroy", "dbfft_last_error", "dbfft_spectral_layout", "dbfft_set_phases",
+           "dbfft_apply_K", "dbfft_apply_K_aug", "dbfft_precond", "dbfft_eval_state", "dbfft_default_opts",
+           "dbfft_solve_increment", "dbfft_get_field", "dbfft_profile_enable", "dbfft_profile_read",
+           "dbfft_profile_name", "dbfft_profile_count"]
+
+_lib = None
+
+
+class DBFFTError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def load_library(path=LIB_PATH):
+    """Load libdbfft.so (raises if it was not built: there is no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} missing: run `python -m paper_1905_12725_b200.build` (CUDA extension required)")
+    lib = ctypes.CDLL(path)
+    P, I32, D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_double
+    lib.dbfft_create.argtypes = [ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double), I32,
+                                 ctypes.POINTER(Env), ctypes.POINTER(P)]
+    lib.dbfft_destroy.argtypes = [P]
+    lib.dbfft_last_error.argtypes = [P]
+    lib.dbfft_last_error.restype = ctypes.c_char_p
+    lib.dbfft_spectral_layout.argtypes = [P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
+    lib.dbfft_set_phases.argtypes = [P, P, I32, I32, ctypes.POINTER(Material)]
+    lib.dbfft_apply_K.argtypes = [P, P, P]
+    lib.dbfft_apply_K_aug.argtypes = [P, ctypes.POINTER(ctypes.c_uint8), P, ctypes.POINTER(D), P, ctypes.POINTER(D)]
+    lib.dbfft_precond.argtypes = [P, P, P]
+    lib.dbfft_eval_state.argtypes = [P, P, I32, D]
+    lib.dbfft_default_opts.restype = Opts
+    lib.dbfft_solve_increment.argtypes = [P, ctypes.POINTER(D), ctypes.POINTER(ctypes.c_uint8), D,
+                                          ctypes.POINTER(Opts), ctypes.POINTER(Report)]
+    lib.dbfft_get_field.argtypes = [P, I32, P, I32]
+    lib.dbfft_profile_enable.argtypes = [P, I32]
+    lib.dbfft_profile_read.argtypes = [P, I32, ctypes.POINTER(D), ctypes.POINTER(ctypes.c_int64)]
+    lib.dbfft_profile_name.argtypes = [I32]
+    lib.dbfft_profile_name.restype = ctypes.c_char_p
+    lib.dbfft_profile_count.restype = I32
+    for fn in EXPORTS:
+        getattr(lib, fn).restype = getattr(lib, fn).restype if fn in (
+            "dbfft_last_error", "dbfft_default_opts", "dbfft_profile_name", "dbfft_profile_count") else ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def material_record(m):
+    """synth.configs material dict -> dbfft_material (parameters copied, no arithmetic)."""
+    rec = Material()
+    k = m["kind"]
+    if k == "iso":
+        rec.kind, vals = MAT_ISO, [m["E"], m["nu"]]
+    elif k == "cubic":
+        rec.kind, vals = MAT_CUBIC, [m["C11"], m["C12"], m["C44"], *np.asarray(m["R"], float).ravel()]
+    elif k == "neohooke":
+        rec.kind, vals = MAT_NEOHOOKE, [m["mu"], m["kappa"]]
+    elif k == "j2":
+        rec.kind, vals = MAT_J2, [m["E"], m["nu"], m["sigma_y"], m["n"], m["edot0"]]
+    else:
+        raise ValueError(k)
+    for i, v in enumerate(vals):
+        rec.p[i] = float(v)
+    return rec
+
+
+def _dptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class DBFFT:
+    """One DBFFT context on one CUDA device (include/dbfft.h)."""
+
+    def __init__(self, n, L=(1.0, 1.0, 1.0), kinematics="small", device=0, stream=None):
+        import torch
+        self.torch = torch
+        self.lib = load_library()
+        self.n = tuple(int(v) for v in n)
+        self.kin = 6 if kinematics in ("small", 6) else 9
+        self.device = torch.device("cuda", device)
+        torch.cuda.set_device(self.device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        env = Env(0, 1, None, ctypes.c_void_p(self.stream.cuda_stream), device)
+        h = ctypes.c_void_p()
+        st = self.lib.dbfft_create((ctypes.c_int32 * 3)(*self.n), (ctypes.c_double * 3)(*L), self.kin,
+                                   ctypes.byref(env), ctypes.byref(h))
+        if st != 0:
+            raise DBFFTError(st, self.lib.dbfft_last_error(None).decode())
+        self.h = h
+        shape = (ctypes.c_int64 * 4)()
+        strides = (ctypes.c_int64 * 4)()
+        self._check(self.lib.dbfft_spectral_layout(self.h, shape, strides))
+        self.spec_shape = tuple(shape)
+
+    def _check(self, st):
+        if st != 0:
+            raise DBFFTError(st, self.lib.dbfft_last_error(self.h).decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.dbfft_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ setup
+    def set_phases(self, phase, materials):
+        recs = (Material * len(materials))(*[material_record(m) for m in materials])
+        if isinstance(phase, np.ndarray):
+            ph = np.ascontiguousarray(phase, dtype=np.uint16)
+            self._check(self.lib.dbfft_set_phases(self.h, ph.ctypes.data_as(ctypes.c_void_p), 0, len(materials), recs))
+        else:
+            ph = phase.contiguous()
+            self._check(self.lib.dbfft_set_phases(self.h, _dptr(ph), 1, len(materials), recs))
+
+    def empty_spectral(self):
+        return self.torch.empty(self.spec_shape, dtype=self.torch.complex128, device=self.device)
+
+    # ------------------------------------------------------------------ operator
+    def apply_K(self, u_hat, out=None):
+        out = self.empty_spectral() if out is None else out
+        self._check(self.lib.dbfft_apply_K(self.h, _dptr(u_hat.contiguous()), _dptr(out)))
+        return out
+
+    def apply_K_aug(self, mask, u_hat, e, out=None):
+        out = self.empty_spectral() if out is None else out
+        m = (ctypes.c_uint8 * 9)(*np.asarray(mask, np.uint8).ravel())
+        ein = (ctypes.c_double * 9)(*np.asarray(e, float).ravel())
+        rout = (ctypes.c_double * 9)()
+        self._check(self.lib.dbfft_apply_K_aug(self.h, m, _dptr(u_hat.contiguous()), ein, _dptr(out), rout))
+        return out, np.array(rout[:]).reshape(3, 3)
+
+    def precond(self, r_hat, out=None):
+        out = self.empty_spectral() if out is None else out
+        self._check(self.lib.dbfft_precond(self.h, _dptr(r_hat.contiguous()), _dptr(out)))
+        return out
+
+    def eval_state(self, field, dt=1.0):
+        if isinstance(field, np.ndarray):
+            f = np.ascontiguousarray(field, dtype=np.float64)
+            self._check(self.lib.dbfft_eval_state(self.h, f.ctypes.data_as(ctypes.c_void_p), 0, float(dt)))
+        else:
+            f = field.contiguous()
+            self._check(self.lib.dbfft_eval_state(self.h, _dptr(f), 1, float(dt)))
+
+    # ------------------------------------------------------------------ solve
+    def solve_increment(self, target, mask, dt=1.0, raise_on_error=True, **opts):
+        o = self.lib.dbfft_default_opts()
+        for k, v in opts.items():
+            setattr(o, k, v)
+        t = (ctypes.c_double * 9)(*np.asarray(target, float).ravel())
+        m = (ctypes.c_uint8 * 9)(*np.asarray(mask, np.uint8).ravel())
+        rep = Report()
+        st = self.lib.dbfft_solve_increment(self.h, t, m, float(dt), ctypes.byref(o), ctypes.byref(rep))
+        out = dict(status=STATUS.get(st, st), converged=bool(rep.converged), cg_iters=rep.cg_iters,
+                   newton_iters=rep.newton_iters, eps_eq=rep.eps_eq, eps_load=rep.eps_load,
+                   max_dgrad=rep.max_dgrad, macro_strain=np.array(rep.macro_strain[:]).reshape(3, 3),
+                   macro_stress=np.array(rep.macro_stress[:]).reshape(3, 3), bad_voxel=rep.bad_voxel,
+                   seconds=rep.seconds)
+        if st != 0 and raise_on_error:
+            raise DBFFTError(st, self.lib.dbfft_last_error(self.h).decode())
+        return out
+
+    def get_field(self, which, on_device=False):
+        n1, n2, n3 = self.n
+        N = n1 * n2 * n3
+        if which == FIELD_U_HAT:
+            out = self.empty_spectral()
+            self._check(self.lib.dbfft_get_field(self.h, which, _dptr(out), 1))
+            return out
+        ncomp = 3 if which == FIELD_U else 9
+        if on_device:
+            out = self.torch.empty((ncomp, n3, n2, n1), dtype=self.torch.float64, device=self.device)
+            self._check(self.lib.dbfft_get_field(self.h, which, _dptr(out), 1))
+            return out
+        out = np.empty((ncomp, n3, n2, n1))
+        self._check(self.lib.dbfft_get_field(self.h, which, out.ctypes.data_as(ctypes.c_void_p), 0))
+        if ncomp == 9:
+            out = out.reshape(3, 3, n3, n2, n1)
+        return out
+
+    # ------------------------------------------------------------------ profiling
+    def profile(self, enable=True):
+        self._check(self.lib.dbfft_profile_enable(self.h, int(enable)))
+
+    def profile_read(self):
+        res = {}
+        for k in range(self.lib.dbfft_profile_count()):
+            ms = ctypes.c_double()
+            n = ctypes.c_int64()
+            self._check(self.lib.dbfft_profile_read(self.h, k, ctypes.byref(ms), ctypes.byref(n)))
+            res[self.lib.dbfft_profile_name(k).decode()] = (ms.value, n.value)
+        return res
+
+
+def half_spectrum(u_real):
+    """Test/bench helper: mean-normalised half spectrum of a real [3][z][y][x] field laid out as
+    [3][ky][kz][kx] (numpy rfftn; input preparation, not part of the product path)."""
+    n3, n2, n1 = u_real.shape[1:]
+    h = np.fft.rfftn(u_real, axes=(1, 2, 3)) / (n1 * n2 * n3)   # [3][kz][ky][kx]
+    return np.ascontiguousarray(np.transpose(h, (0, 2, 1, 3)))
+
+
+def full_from_half(h, n1):
+    """Inverse of the layout of `half_spectrum`: [3][ky][kz][kx] -> full [3][kz][ky][kx] spectrum."""
+    hz = np.transpose(h, (0, 2, 1, 3))  # [3][kz][ky][kx<=n1/2]
+    n3, n2 = hz.shape[1], hz.shape[2]
+    full = np.zeros((hz.shape[0], n3, n2, n1), dtype=np.complex128)
+    full[..., : n1 // 2 + 1] = hz
+    kz = (-np.arange(n3)) % n3
+    ky = (-np.arange(n2)) % n2
+    for kx in range(n1 // 2 + 1, n1):
+        full[..., kx] = np.conj(hz[:, kz][:, :, ky][..., n1 - kx])
+    return full

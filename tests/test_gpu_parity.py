@@ -1,0 +1,237 @@
+"""GPU-vs-oracle parity through the C ABI (libdbfft.so).  Marked `gpu`.
+
+Bars (BASELINE.json north_star): single operator applications 1e-12 relative (fp64),
+macroscopic stress/strain 1e-9 relative, per-voxel fields 1e-8 relative L2 at tol 1e-10."""
+import numpy as np
+import pytest
+
+from oracle import dbfft_oracle as O
+from synth import configs, microstructure as ms
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def dbf():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1905_12725_b200 import dbfft
+    dbfft.load_library()
+    return dbfft
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.ravel(a - b)) / max(np.linalg.norm(np.ravel(b)), 1e-300))
+
+
+def to_gpu_spec(dbf, u_real):
+    return torch.from_numpy(dbf.half_spectrum(u_real)).cuda()
+
+
+def gpu_full(dbf, t, n1):
+    return dbf.full_from_half(t.cpu().numpy(), n1)
+
+
+def two_phase(n, seed, frac=0.3):
+    u = ms.SplitMix64(seed).uniform(n[0] * n[1] * n[2]).reshape(n[2], n[1], n[0])
+    return (u < frac).astype(np.uint16)
+
+
+ISO2 = [dict(kind="iso", E=1.0, nu=0.3), dict(kind="iso", E=10.0, nu=0.25)]
+GRIDS = [(8, 8, 8), (16, 8, 32), (32, 64, 16), (64, 64, 64)]
+
+
+@pytest.mark.parametrize("n", GRIDS)
+def test_apply_K_small_linear(dbf, n):
+    ph = two_phase(n, 1)
+    ctx = dbf.DBFFT(n, kinematics="small")
+    ctx.set_phases(ph, ISO2)
+    u = ms.random_field((3, n[2], n[1], n[0]), 7)
+    f = ctx.apply_K(to_gpu_spec(dbf, u))
+    torch.cuda.synchronize()
+    XI = O.frequency_grid(n)
+    ref, _ = O.apply_K(O.fft(u), O.stiffness_field(ph, ISO2), XI)
+    assert rel(gpu_full(dbf, f, n[0]), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [(8, 8, 8), (32, 16, 64)])
+def test_apply_K_cubic_polycrystal(dbf, n):
+    cfg = configs.c3(n=n[0], grains=12, seed=3) if n[0] == n[1] == n[2] else None
+    if cfg is None:
+        ph, _ = ms.voronoi(n, 12, 3)
+        R = ms.random_rotations(12, 1003)
+        mats = [dict(kind="cubic", C11=168.4, C12=121.4, C44=75.4, R=R[g]) for g in range(12)]
+    else:
+        ph, mats = cfg["phase"], cfg["materials"]
+    ctx = dbf.DBFFT(n, kinematics="small")
+    ctx.set_phases(ph, mats)
+    u = ms.random_field((3, n[2], n[1], n[0]), 8)
+    f = ctx.apply_K(to_gpu_spec(dbf, u))
+    ref, _ = O.apply_K(O.fft(u), O.stiffness_field(ph, mats), O.frequency_grid(n))
+    assert rel(gpu_full(dbf, f, n[0]), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [(8, 8, 8), (16, 32, 8), (32, 32, 32)])
+def test_apply_K_finite_neohooke(dbf, n):
+    ph = two_phase(n, 2)
+    mats = [dict(kind="neohooke", mu=1.0, kappa=2.5), dict(kind="neohooke", mu=10.0, kappa=25.0)]
+    F = np.eye(3).reshape(3, 3, 1, 1, 1) + 0.1 * ms.random_field((3, 3, n[2], n[1], n[0]), 9)
+    ctx = dbf.DBFFT(n, kinematics="finite")
+    ctx.set_phases(ph, mats)
+    ctx.eval_state(F.reshape(9, n[2], n[1], n[0]))
+    u = ms.random_field((3, n[2], n[1], n[0]), 10)
+    f = ctx.apply_K(to_gpu_spec(dbf, u))
+    mu = np.array([1.0, 10.0])[ph]
+    kap = np.array([2.5, 25.0])[ph]
+    _, K = O.neo_hookean(F, mu, kap)
+    ref, _ = O.apply_K(O.fft(u), K, O.frequency_grid(n), finite=True)
+    assert rel(gpu_full(dbf, f, n[0]), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [(8, 8, 8), (32, 16, 16)])
+def test_apply_K_j2_tangent(dbf, n):
+    ph = two_phase(n, 3, 0.5)
+    mats = [dict(kind="j2", E=2e5, nu=0.3, sigma_y=300.0, n=20.0, edot0=1e-3),
+            dict(kind="j2", E=2e5, nu=0.3, sigma_y=200.0, n=20.0, edot0=1e-3)]
+    eps = 2e-3 * np.diag([-0.5, -0.5, 1.0]).reshape(3, 3, 1, 1, 1) + 5e-4 * ms.random_field((3, 3, n[2], n[1], n[0]), 11)
+    eps = 0.5 * (eps + np.swapaxes(eps, 0, 1))
+    ctx = dbf.DBFFT(n, kinematics="small")
+    ctx.set_phases(ph, mats)
+    ctx.eval_state(eps.reshape(9, n[2], n[1], n[0]), dt=1.0)
+    u = ms.random_field((3, n[2], n[1], n[0]), 12)
+    f = ctx.apply_K(to_gpu_spec(dbf, u))
+    sy = np.array([300.0, 200.0])[ph]
+    _, C, _, dp = O.j2_perzyna(eps, np.zeros_like(eps), 2e5, 0.3, sy, 20.0, 1e-3, 1.0)
+    assert np.mean(dp > 0) > 0.2  # a real mix of plastic and elastic voxels
+    ref, _ = O.apply_K(O.fft(u), C, O.frequency_grid(n))
+    assert rel(gpu_full(dbf, f, n[0]), ref) <= 1e-12
+
+
+def test_precond_and_aug(dbf):
+    n = (16, 32, 8)
+    ph = two_phase(n, 4)
+    C = O.stiffness_field(ph, ISO2)
+    ctx = dbf.DBFFT(n, kinematics="small")
+    ctx.set_phases(ph, ISO2)
+    r = ms.random_field((3, n[2], n[1], n[0]), 13)
+    z = ctx.precond(to_gpu_spec(dbf, r))
+    XI = O.frequency_grid(n)
+    zref = O.precondition(O.fft(r), C.mean(axis=(-3, -2, -1)), XI)
+    assert rel(gpu_full(dbf, z, n[0]), zref) <= 1e-12
+    mask = np.zeros((3, 3), bool); mask[0, 0] = mask[1, 1] = mask[0, 1] = mask[1, 0] = True
+    e = np.array([[1e-3, 2e-4, 0], [2e-4, -5e-4, 0], [0, 0, 0.0]])
+    u = ms.random_field((3, n[2], n[1], n[0]), 14)
+    f, rout = ctx.apply_K_aug(mask, to_gpu_spec(dbf, u), e)
+    fref, msig = O.apply_K(O.fft(u), C, XI, e=e)
+    assert rel(gpu_full(dbf, f, n[0]), fref) <= 1e-12
+    assert np.allclose(rout, np.where(mask, msig, 0.0), rtol=1e-12, atol=1e-15 * np.abs(msig).max())
+
+
+def test_hermitian_and_null_modes_full_size(dbf):
+    """Full c4-size property test (any size): <Kv,w> = <v,Kw> and K = 0 on Z."""
+    n = (256, 256, 256)
+    cfg = configs.c4()
+    ctx = dbf.DBFFT(n, kinematics="finite")
+    ctx.set_phases(cfg["phase"], cfg["materials"])
+    g = torch.Generator(device="cuda").manual_seed(0)
+
+    def rnd():
+        x = torch.randn((3, n[2], n[1], n[0]), dtype=torch.float64, device="cuda", generator=g)
+        h = torch.fft.rfftn(x, dim=(1, 2, 3)) / x[0].numel()
+        return h.permute(0, 2, 1, 3).contiguous()
+
+    v, w = rnd(), rnd()
+    Kv, Kw = ctx.apply_K(v), ctx.apply_K(w)
+
+    def dot(a, b):
+        wgt = torch.full((n[0] // 2 + 1,), 2.0, dtype=torch.float64, device="cuda")
+        wgt[0] = 1.0; wgt[-1] = 1.0
+        return float(((a.conj() * b).real * wgt).sum())
+
+    a, b = dot(Kv, w), dot(v, Kw)
+    assert abs(a - b) <= 1e-12 * abs(a)
+    assert dot(Kv, v) > 0
+    # null set: DC and the 7 Nyquist combinations are exactly zero
+    for ky in (0, n[1] // 2):
+        for kz in (0, n[2] // 2):
+            for kx in (0, n[0] // 2):
+                assert float(Kv[:, ky, kz, kx].abs().max()) == 0.0
+
+
+# ------------------------------------------------------------------------------- solves
+
+
+def _field_rel(a, b):
+    return rel(a, b)
+
+
+def test_solve_c1(dbf):
+    cfg = configs.c1()
+    ref = O.solve_small_strain(cfg["phase"], cfg["materials"], cfg["loads"][0], tol=1e-10)
+    ctx = dbf.DBFFT(cfg["n"], kinematics="small")
+    ctx.set_phases(cfg["phase"], cfg["materials"])
+    L = cfg["loads"][0]
+    rep = ctx.solve_increment(L["target"], L["mask"])
+    assert rep["converged"]
+    assert abs(rep["cg_iters"] - ref["iters"]) <= 1
+    assert rel(rep["macro_stress"], ref["mean_sig"]) <= 1e-9
+    assert rel(ctx.get_field(dbf.FIELD_STRESS), ref["sig"]) <= 1e-8
+    assert rel(ctx.get_field(dbf.FIELD_STRAIN), ref["eps"]) <= 1e-8
+    assert rel(ctx.get_field(dbf.FIELD_U), O.displacement(ref["u_hat"])) <= 1e-8
+
+
+@pytest.mark.parametrize("n", [32, 64])
+def test_solve_c2_mixed(dbf, n):
+    cfg = configs.c2(n=n, radius_vox=6 * n // 64)
+    L = cfg["loads"][0]
+    ref = O.solve_small_strain(cfg["phase"], cfg["materials"], L, tol=1e-10)
+    ctx = dbf.DBFFT(cfg["n"], kinematics="small")
+    ctx.set_phases(cfg["phase"], cfg["materials"])
+    rep = ctx.solve_increment(L["target"], L["mask"])
+    assert rep["converged"]
+    assert rel(rep["macro_stress"], ref["mean_sig"]) <= 1e-9
+    assert rel(rep["macro_strain"], ref["mean_eps"]) <= 1e-9
+    assert rep["macro_strain"][2, 2] == pytest.approx(1e-3, rel=1e-14)
+    assert rel(ctx.get_field(dbf.FIELD_STRESS), ref["sig"]) <= 1e-8
+
+
+def test_solve_c3_twin(dbf):
+    cfg = configs.c3(n=32, grains=24)
+    L = cfg["loads"][0]
+    ref = O.solve_small_strain(cfg["phase"], cfg["materials"], L, tol=1e-10)
+    ctx = dbf.DBFFT(cfg["n"], kinematics="small")
+    ctx.set_phases(cfg["phase"], cfg["materials"])
+    rep = ctx.solve_increment(L["target"], L["mask"])
+    assert rel(rep["macro_stress"], ref["mean_sig"]) <= 1e-9
+    assert rel(ctx.get_field(dbf.FIELD_STRESS), ref["sig"]) <= 1e-8
+
+
+def test_solve_c4_twin_newton(dbf):
+    cfg = configs.c4(n=32, radius_vox=3, increments=10)
+    st = O.FiniteStrainState(cfg["n"])
+    ctx = dbf.DBFFT(cfg["n"], kinematics="finite")
+    ctx.set_phases(cfg["phase"], cfg["materials"])
+    for L in cfg["loads"][:3]:
+        ref = O.solve_finite_increment(st, cfg["phase"], cfg["materials"], L, tol=1e-10)
+        rep = ctx.solve_increment(L["target"], L["mask"])
+        assert rep["converged"] and ref["converged"]
+        assert rep["newton_iters"] == ref["newton_iters"]
+        assert rel(rep["macro_stress"], ref["mean_P"]) <= 1e-9
+        assert rel(rep["macro_strain"], ref["mean_F"]) <= 1e-9
+        assert rel(ctx.get_field(dbf.FIELD_STRAIN), ref["F"]) <= 1e-8
+        assert rel(ctx.get_field(dbf.FIELD_STRESS), ref["P"]) <= 1e-8
+
+
+def test_solve_c5_twin_j2(dbf):
+    cfg = configs.c5(n=16, grains=6, increments=4)
+    st = O.J2State(cfg["n"])
+    ctx = dbf.DBFFT(cfg["n"], kinematics="small")
+    ctx.set_phases(cfg["phase"], cfg["materials"])
+    for L in cfg["loads"]:
+        ref = O.solve_j2_increment(st, cfg["phase"], cfg["materials"], L, 1.0, tol=1e-10)
+        rep = ctx.solve_increment(L["target"], L["mask"], dt=1.0)
+        assert rep["converged"]
+        assert rel(rep["macro_stress"], ref["mean_sig"]) <= 1e-9
+        assert rel(ctx.get_field(dbf.FIELD_STRESS), ref["sig"]) <= 1e-8
