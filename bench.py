@@ -1,0 +1,348 @@
+"""bench.py — DBFFT hot-path benchmark (driver contract).
+
+Workload (BASELINE.json metric "voxel.CG-iter/s (fp64) and % HBM roofline at 256^3"):
+config c4 — 256^3 finite-strain neo-Hookean two-phase composite (1202 RSA spheres of radius
+10 voxels, vf 0.30, shear-modulus contrast 10, kappa/mu = 2.5), F_zz -> 1.10 in 10 increments,
+P_xx = P_yy = 0 (mixed control).  One step = one load increment: the constitutive update,
+residual, mean tangent and preconditioner, and Newton-PCG to tol_eq = 1e-10 / Newton 1e-6,
+i.e. every row of SURVEY 8(a).  Steps walk the increments in order (state carried over);
+after increment 10 the state is reset (inside the step that wraps).
+
+value = (voxels x PCG iterations summed over all ranks' timed steps) / max-over-ranks time.
+N > 1: independent replicas, one c4 problem per rank ("scaling": "weak"); the slab-decomposed
+multi-GPU operator is not built yet.
+
+--impl reference: the CPU oracle (oracle/dbfft_oracle.py) timed on this host, one oracle PCG
+iteration per step on c4's 128^3 twin (bounded sample).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "voxel*CG-iter/s (fp64), config c4 256^3"
+UNIT = "voxel*iter/s"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """dram read+write bytes per launch of pass_X from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_pass_x_summary.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    return None
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if self.proc is None or not os.path.exists(self.path):
+            return None
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for k, nm in enumerate(names):
+                if r[5 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+# ------------------------------------------------------------------------------------------ GPU arm
+
+
+def bytes_pass_x(n, kin=9):
+    """Algorithmic bytes of one pass_X launch: c complex half-spectrum fields in
+    and out (16 B each) plus the per-voxel tangent read (45 fp64 = 360 B/voxel at finite strain)."""
+    n1, n2, n3 = n
+    H = (n1 // 2 + 1) * n2 * n3
+    N = n1 * n2 * n3
+    return 2 * kin * 16 * H + (360 if kin == 9 else 168) * N
+
+
+def bytes_apply_K(n, kin=9):
+    """Per-axis model schedule B_op = 16 * (66 | 52) * H + tangent bytes."""
+    n1, n2, n3 = n
+    H = (n1 // 2 + 1) * n2 * n3
+    N = n1 * n2 * n3
+    return 16 * (66 if kin == 9 else 52) * H + (360 if kin == 9 else 168) * N
+
+
+def gpu_arm(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1905_12725_b200 import dbfft
+    from synth import configs
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = configs.c4(n=args.n, radius_vox=max(1, round(10 * args.n / 256)))
+    n = cfg["n"]
+    N = n[0] * n[1] * n[2]
+    stream = torch.cuda.current_stream()
+    ctx = dbfft.DBFFT(n, kinematics="finite", device=local, stream=stream)
+    ctx.set_phases(cfg["phase"], cfg["materials"])
+    loads = cfg["loads"]
+    state = {"k": 0}
+
+    def step():
+        if state["k"] == len(loads):
+            ctx.set_phases(cfg["phase"], cfg["materials"])
+            state["k"] = 0
+        L = loads[state["k"]]
+        rep = ctx.solve_increment(L["target"], L["mask"], dt=1.0, check_every=args.check_every)
+        state["k"] += 1
+        return rep
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ctx.profile(True)
+    launches0 = ctx.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    iters = 0
+    newton = 0
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            rep = step()
+            iters += rep["cg_iters"]
+            newton += rep["newton_iters"]
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches = ctx.launch_count() - launches0
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    t_local = ms / 1e3
+    tot_iters = iters
+    t_max = t_local
+    if world > 1:
+        tt = torch.tensor([t_local], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        it = torch.tensor([float(iters)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(it, op=dist.ReduceOp.SUM)
+        t_max, tot_iters = float(tt.item()), int(it.item())
+    value = N * tot_iters / t_max
+
+    # ------------------------------------------------ e2e: host inputs -> C ABI -> host result
+    e2e = None
+    if args.e2e_steps > 0:
+        torch.cuda.synchronize()
+        phase_host = np.ascontiguousarray(cfg["phase"])
+        h2d = phase_host.nbytes
+        d2h = 0
+        e_iters = 0
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            ctx.set_phases(phase_host, cfg["materials"])            # H2D of the microstructure
+            L = loads[0]
+            rep = ctx.solve_increment(L["target"], L["mask"], dt=1.0, check_every=args.check_every)
+            u = ctx.get_field(dbfft.FIELD_U)                        # D2H of the displacement field
+            d2h = u.nbytes + 9 * 2 * 8
+            e_iters += rep["cg_iters"]
+        torch.cuda.synchronize()
+        t_e2e = time.perf_counter() - t0
+        e2e = {"value": N * e_iters / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "steps": args.e2e_steps,
+               "note": "per step: set_phases from host uint16 map, solve increment 1 from the reset state, "
+                       "get_field(U) to host; wall clock around the C-ABI calls"}
+        # restore the walk state
+        ctx.set_phases(cfg["phase"], cfg["materials"])
+
+    px_ms, px_n = prof.get("pass_X", (0.0, 0))
+    peak, peak_src = measured_peaks()
+    bx = bytes_pass_x(n)
+    avg_x = px_ms / max(px_n, 1) / 1e3
+    achieved = bx / avg_x / 1e9 if px_n else None
+    # whole operator (all five passes) for context
+    op_ms = sum(prof.get(k, (0.0, 0))[0] for k in ("pass_I1", "pass_I2", "pass_X", "pass_F2", "pass_F3"))
+    n_op = max(px_n, 1)
+    op_gbs = bytes_apply_K(n) / (op_ms / n_op / 1e3) / 1e9 if px_n else None
+    total_prof = sum(v[0] for v in prof.values())
+    roofline = {"bound": "hbm", "kernel": "pass_X (x C2R + 9x9 tangent contraction + R2C)",
+                "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": ncu_traffic(),
+                "algorithmic_bytes_per_launch": bx, "avg_launch_ms": avg_x * 1e3, "launches": px_n,
+                "peak_source": peak_src, "share_of_step": (px_ms / total_prof) if total_prof else None,
+                "apply_K": {"algorithmic_bytes": bytes_apply_K(n), "avg_ms": op_ms / n_op,
+                            "achieved_GBps": op_gbs, "frac": (op_gbs / peak) if op_gbs else None}}
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"c4: {n[0]}^3 finite-strain neo-Hookean, 30% RSA spheres r=10, "
+                                  "F_zz->1.10 in 10 increments, P_xx=P_yy=0; one step = one increment",
+                      "grid": list(n), "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                      "l2": "inputs larger than L2 (working set ~15 GB per GPU)", "tol_eq": 1e-10,
+                      "tol_newton": 1e-6, "cg_iters_timed": iters, "newton_iters_timed": newton},
+           "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches),
+           "kernel_ms": {k: v[0] for k, v in prof.items()}}
+    clk_sum = clk.summary()
+    out["clocks"] = clk_sum
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(iters=2)
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------------------------------ oracle
+
+
+def oracle_setup(n=128):
+    from oracle import dbfft_oracle as O
+    from synth import configs
+    cfg = configs.c4(n=n, radius_vox=max(1, round(10 * n / 256)))
+    ph = cfg["phase"]
+    mu = np.array([m["mu"] for m in cfg["materials"]])[ph]
+    kap = np.array([m["kappa"] for m in cfg["materials"]])[ph]
+    L = cfg["loads"][0]
+    F = np.where(L["mask"], np.eye(3), L["target"]).reshape(3, 3, 1, 1, 1) * np.ones((1, 1) + ph.shape)
+    P, K = O.neo_hookean(F, mu, kap)
+    XI = O.frequency_grid(cfg["n"])
+    Kbar = K.mean(axis=(-3, -2, -1))
+    b = O.rhs_from_stress(P, XI)
+    return dict(O=O, K=K, XI=XI, Kbar=Kbar, b=b, mask=L["mask"], N=ph.size, n=cfg["n"])
+
+
+def oracle_iteration(S, p, r, rz):
+    """One PCG iteration of the oracle (apply_K + preconditioner + CG algebra), as in O.pcg."""
+    O = S["O"]
+    q, _ = O.apply_K(p, S["K"], S["XI"], finite=True)
+    alpha = rz / O.inner(p, q)
+    r = r - alpha * q
+    z = O.precondition(r, S["Kbar"], S["XI"])
+    rz_new = O.inner(r, z)
+    p = z + (rz_new / rz) * p
+    return p, r, rz_new
+
+
+def cpu_baseline(iters=2):
+    S = oracle_setup(128)
+    O = S["O"]
+    r = S["b"]
+    z = O.precondition(r, S["Kbar"], S["XI"])
+    p, rz = z, O.inner(r, z)
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        p, r, rz = oracle_iteration(S, p, r, rz)
+    t = time.perf_counter() - t0
+    return {"value": S["N"] * iters / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{iters} oracle PCG iterations (apply_K + preconditioner + CG algebra) of c4's first "
+                      f"Newton step on its 128^3 twin (same structure, r=5); numpy single-threaded FFT/einsum",
+            "seconds": t}
+
+
+def reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    S = oracle_setup(128)
+    O = S["O"]
+    r = S["b"]
+    z = O.precondition(r, S["Kbar"], S["XI"])
+    p, rz = z, O.inner(r, z)
+    for _ in range(args.warmup):
+        p, r, rz = oracle_iteration(S, p, r, rz)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        p, r, rz = oracle_iteration(S, p, r, rz)
+    t = time.perf_counter() - t0
+    v = S["N"] * args.steps / t
+    sample = ("one oracle PCG iteration per step (apply_K + preconditioner + CG algebra) on c4's 128^3 twin, "
+              "first Newton step; numpy single-threaded")
+    print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+                      "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+                      "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                      "data": "synthetic", "config": {"workload": "c4 128^3 twin (bounded oracle sample)"},
+                      "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+                      "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="dbfft", choices=["dbfft", "reference"])
+    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--check-every", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

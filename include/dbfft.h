@@ -154,11 +154,13 @@ typedef enum {
 /* Copy a field of the committed state into `out` (host if out_on_device == 0). (sync) */
 dbfft_status dbfft_get_field(dbfft_ctx ctx, int32_t which, void* out, int32_t out_on_device);
 
-/* Per-kernel device-time accounting (CUDA events around each launch of the named pass
- * kernels, accumulated while enabled).  names: comma-separated list written to buf. */
+/* Per-kernel device-time accounting: while enabled, CUDA events are recorded on the ctx stream
+ * around every kernel launch and accumulated per kernel id (names via dbfft_profile_name). */
 dbfft_status dbfft_profile_enable(dbfft_ctx ctx, int32_t enable);
 dbfft_status dbfft_profile_read(dbfft_ctx ctx, int32_t kernel_id, double* total_ms, int64_t* launches);
 const char* dbfft_profile_name(int32_t kernel_id);
+/* Number of CUDA kernels this ctx has launched since creation (always counted). */
+dbfft_status dbfft_launch_count(dbfft_ctx ctx, int64_t* count);
 int32_t dbfft_profile_count(void);
 
 #ifdef __cplusplus

@@ -83,6 +83,7 @@ struct dbfft_ctx_s {
   size_t ev_next = 0;
   double prof_ms[PK_COUNT];
   long long prof_n[PK_COUNT];
+  long long nlaunch = 0;  // kernels launched by this ctx (always counted)
 };
 
 namespace {
@@ -110,6 +111,7 @@ struct ProfScope {
   int id;
   int i0 = -1;
   ProfScope(dbfft_ctx c, int k) : ctx(c), id(k) {
+    ctx->nlaunch += 1;
     if (!ctx->prof) return;
     if (ctx->ev_next + 2 > ctx->ev_pool.size()) {
       for (int j = 0; j < 256; ++j) {
@@ -496,7 +498,10 @@ dbfft_status forward_tail(dbfft_ctx ctx, cplx* out) {
 }
 
 dbfft_status read_reduction(dbfft_ctx ctx, const double* partials, int nblk, int nred, double* host_out) {
-  CK(launch_reduce(partials, nblk, nred, ctx->red_out, ctx->stream));
+  {
+    ProfScope ps(ctx, PK_FIN);
+    CK(launch_reduce(partials, nblk, nred, ctx->red_out, ctx->stream));
+  }
   CK(cudaMemcpyAsync(ctx->h_red, ctx->red_out, sizeof(double) * nred, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   memcpy(host_out, ctx->h_red, sizeof(double) * nred);
@@ -513,7 +518,10 @@ void sym_fill(double* m) {
 dbfft_status refresh_mean_tangent(dbfft_ctx ctx) {
   const int nk = ctx->kin == 9 ? 45 : 21;
   const int nblk = cg_blocks();
-  CK(launch_mean_sym(ctx->tan, nk, ctx->N, ctx->part_misc, nblk, ctx->stream));
+  {
+    ProfScope ps(ctx, PK_OTHER);
+    CK(launch_mean_sym(ctx->tan, nk, ctx->N, ctx->part_misc, nblk, ctx->stream));
+  }
   double m[64];
   CKS(read_reduction(ctx, ctx->part_misc, nblk, nk, m));
   for (int k = 0; k < nk; ++k) m[k] /= (double)ctx->N;
@@ -581,7 +589,10 @@ dbfft_status pcg(dbfft_ctx ctx, const dbfft_opts& o, const uint8_t* mask, int* i
         ProfScope ps(ctx, PK_CGUPD);
         CK(launch_true_residual(sg, ctx->b, ctx->q, ctx->r, ctx->part_cg, nb, ctx->stream));
       }
-      CK(launch_fin_true(cg, ctx->part_cg, nb, ctx->part_x, ao.grid_x, 10, ctx->stream));
+      {
+        ProfScope ps(ctx, PK_FIN);
+        CK(launch_fin_true(cg, ctx->part_cg, nb, ctx->part_x, ao.grid_x, 10, ctx->stream));
+      }
       CK(cudaMemcpyAsync(ctx->h_cg, cg, sizeof(CgDev), cudaMemcpyDeviceToHost, ctx->stream));
       CK(cudaStreamSynchronize(ctx->stream));
       if (ctx->h_cg->converged == 1 || restarts > 20) {
@@ -590,8 +601,14 @@ dbfft_status pcg(dbfft_ctx ctx, const dbfft_opts& o, const uint8_t* mask, int* i
       }
       // restart from the true residual: z = M r, p = z
       ++restarts;
-      CK(launch_cg_init(sg, ctx->prec, ctx->r, ctx->p, ctx->part_cg, nb, ctx->stream));
-      CK(launch_fin_init(cg, ctx->part_cg, nb, ctx->stream));
+      {
+        ProfScope ps(ctx, PK_CGDIR);
+        CK(launch_cg_init(sg, ctx->prec, ctx->r, ctx->p, ctx->part_cg, nb, ctx->stream));
+      }
+      {
+        ProfScope ps(ctx, PK_FIN);
+        CK(launch_fin_init(cg, ctx->part_cg, nb, ctx->stream));
+      }
       continue;
     }
     for (int k = 0; k < every; ++k) {
@@ -781,7 +798,10 @@ dbfft_status solve_newton(dbfft_ctx ctx, const double* target, const uint8_t* ma
     total_cg += iters;
     if (st != DBFFT_OK) break;
     // u += du ; Fbar_f += dF_f
-    CK(launch_axpy(spec(ctx), ctx->u, ctx->x, 1.0, ctx->stream));
+    {
+      ProfScope ps(ctx, PK_OTHER);
+      CK(launch_axpy(spec(ctx), ctx->u, ctx->x, 1.0, ctx->stream));
+    }
     double de[9];
     for (int a = 0; a < 9; ++a) {
       de[a] = mask[a] ? ctx->h_cg->xe[a] : 0.0;
@@ -1166,6 +1186,7 @@ dbfft_status dbfft_precond(dbfft_ctx ctx, const void* r_hat, void* z_hat) {
     ctx->err = "precond before set_phases";
     return DBFFT_E_STATE;
   }
+  ProfScope ps(ctx, PK_OTHER);
   CK(launch_precond(spec(ctx), ctx->prec, (const cplx*)r_hat, (cplx*)z_hat, ctx->stream));
   return DBFFT_OK;
 }
@@ -1321,6 +1342,12 @@ dbfft_status dbfft_profile_read(dbfft_ctx ctx, int32_t id, double* total_ms, int
   prof_flush(ctx);
   if (total_ms) *total_ms = ctx->prof_ms[id];
   if (launches) *launches = ctx->prof_n[id];
+  return DBFFT_OK;
+}
+
+dbfft_status dbfft_launch_count(dbfft_ctx ctx, int64_t* count) {
+  if (!ctx || !count) return DBFFT_E_INVALID_ARG;
+  *count = ctx->nlaunch;
   return DBFFT_OK;
 }
 

@@ -43,7 +43,7 @@ STATUS = {0: "OK", 1: "E_INVALID_GRID", 2: "E_INVALID_ARG", 3: "E_STATE", 4: "E_
 EXPORTS = ["dbfft_create", "dbfft_destroy", "dbfft_last_error", "dbfft_spectral_layout", "dbfft_set_phases",
            "dbfft_apply_K", "dbfft_apply_K_aug", "dbfft_precond", "dbfft_eval_state", "dbfft_default_opts",
            "dbfft_solve_increment", "dbfft_get_field", "dbfft_profile_enable", "dbfft_profile_read",
-           "dbfft_profile_name", "dbfft_profile_count"]
+           "dbfft_profile_name", "dbfft_profile_count", "dbfft_launch_count"]
 
 _lib = None
 
@@ -83,6 +83,7 @@ def load_library(path=LIB_PATH):
     lib.dbfft_profile_name.argtypes = [I32]
     lib.dbfft_profile_name.restype = ctypes.c_char_p
     lib.dbfft_profile_count.restype = I32
+    lib.dbfft_launch_count.argtypes = [P, ctypes.POINTER(ctypes.c_int64)]
     for fn in EXPORTS:
         getattr(lib, fn).restype = getattr(lib, fn).restype if fn in (
             "dbfft_last_error", "dbfft_default_opts", "dbfft_profile_name", "dbfft_profile_count") else ctypes.c_int
@@ -231,6 +232,11 @@ class DBFFT:
     # ------------------------------------------------------------------ profiling
     def profile(self, enable=True):
         self._check(self.lib.dbfft_profile_enable(self.h, int(enable)))
+
+    def launch_count(self):
+        n = ctypes.c_int64()
+        self._check(self.lib.dbfft_launch_count(self.h, ctypes.byref(n)))
+        return n.value
 
     def profile_read(self):
         res = {}
