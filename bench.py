@@ -47,12 +47,15 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic():
-    """dram read+write bytes per launch of pass_X from the committed ncu --set full summary."""
+def ncu_traffic(variant):
+    """dram read+write bytes per launch of pass_X (this tangent variant) from the committed
+    ncu --set full summary (profiles/ncu_pass_x_summary.json), else None."""
     p = os.path.join(ROOT, "profiles", "ncu_pass_x_summary.json")
     if os.path.exists(p):
         with open(p) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            d = json.load(f)
+        v = d.get(variant)
+        return v.get("dram_bytes_per_launch") if v else None
     return None
 
 
@@ -112,21 +115,27 @@ class Clocks:
 # ------------------------------------------------------------------------------------------ GPU arm
 
 
-def bytes_pass_x(n, kin=9):
-    """Algorithmic bytes of one pass_X launch: c complex half-spectrum fields in
-    and out (16 B each) plus the per-voxel tangent read (45 fp64 = 360 B/voxel at finite strain)."""
+# per-voxel material bytes read by pass_X at finite strain:
+#   full    : 45 fp64 entries of the major-symmetric 9x9 tangent             = 360 B
+#   compact : F^-1 (9 fp64) + c1 (1 fp64) + phase id (u16), tangent rebuilt  =  82 B
+TANGENT_BYTES = {"full": 360, "compact": 82}
+
+
+def bytes_pass_x(n, variant, kin=9):
+    """Algorithmic bytes of one pass_X launch: c complex half-spectrum fields in and out
+    (16 B each) plus the per-voxel tangent data of the variant in use."""
     n1, n2, n3 = n
     H = (n1 // 2 + 1) * n2 * n3
     N = n1 * n2 * n3
-    return 2 * kin * 16 * H + (360 if kin == 9 else 168) * N
+    return 2 * kin * 16 * H + TANGENT_BYTES[variant] * N
 
 
-def bytes_apply_K(n, kin=9):
-    """Per-axis model schedule B_op = 16 * (66 | 52) * H + tangent bytes."""
+def bytes_apply_K(n, variant, kin=9):
+    """Per-axis 5-pass schedule 16 * 66 * H + the variant's tangent bytes."""
     n1, n2, n3 = n
     H = (n1 // 2 + 1) * n2 * n3
     N = n1 * n2 * n3
-    return 16 * (66 if kin == 9 else 52) * H + (360 if kin == 9 else 168) * N
+    return 16 * (66 if kin == 9 else 52) * H + TANGENT_BYTES[variant] * N
 
 
 def gpu_arm(args):
@@ -219,21 +228,26 @@ def gpu_arm(args):
 
     px_ms, px_n = prof.get("pass_X", (0.0, 0))
     peak, peak_src = measured_peaks()
-    bx = bytes_pass_x(n)
+    variant = "full" if os.environ.get("DBFFT_TANGENT") == "full" else "compact"
+    bx = bytes_pass_x(n, variant)
     avg_x = px_ms / max(px_n, 1) / 1e3
     achieved = bx / avg_x / 1e9 if px_n else None
     # whole operator (all five passes) for context
     op_ms = sum(prof.get(k, (0.0, 0))[0] for k in ("pass_I1", "pass_I2", "pass_X", "pass_F2", "pass_F3"))
     n_op = max(px_n, 1)
-    op_gbs = bytes_apply_K(n) / (op_ms / n_op / 1e3) / 1e9 if px_n else None
+    op_gbs = bytes_apply_K(n, variant) / (op_ms / n_op / 1e3) / 1e9 if px_n else None
+    t_model = bytes_apply_K(n, "full") / 8e12  # SURVEY 8(d) model: 14.97 GB at 8 TB/s = 1.871 ms
     total_prof = sum(v[0] for v in prof.values())
-    roofline = {"bound": "hbm", "kernel": "pass_X (x C2R + 9x9 tangent contraction + R2C)",
+    roofline = {"bound": "hbm", "kernel": f"pass_X (x C2R + neo-Hookean tangent contraction [{variant}] + R2C)",
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": ncu_traffic(),
+                "frac": (achieved / peak) if achieved else None, "traffic": ncu_traffic(variant),
+                "tangent": variant,
                 "algorithmic_bytes_per_launch": bx, "avg_launch_ms": avg_x * 1e3, "launches": px_n,
                 "peak_source": peak_src, "share_of_step": (px_ms / total_prof) if total_prof else None,
-                "apply_K": {"algorithmic_bytes": bytes_apply_K(n), "avg_ms": op_ms / n_op,
-                            "achieved_GBps": op_gbs, "frac": (op_gbs / peak) if op_gbs else None}}
+                "apply_K": {"algorithmic_bytes": bytes_apply_K(n, variant), "avg_ms": op_ms / n_op,
+                            "achieved_GBps": op_gbs, "frac": (op_gbs / peak) if op_gbs else None,
+                            "survey_model_ms_8TBps": t_model,
+                            "frac_of_survey_model": (t_model / (op_ms / n_op / 1e3)) if px_n else None}}
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",

@@ -82,7 +82,11 @@ dbfft_status dbfft_spectral_layout(dbfft_ctx ctx, int64_t shape[4], int64_t stri
  *                        C'_ijkl = R_ia R_jb R_kc R_ld C_abcd, R row-major        small strain
  *   DBFFT_MAT_NEOHOOKE : p = {mu, kappa}                  compressible neo-Hookean (R14)   finite
  *   DBFFT_MAT_J2       : p = {E, nu, sigma_y, n, edot0}   J2 Perzyna overstress (R16)     small
- * Linear kinds require no state; NEOHOOKE and J2 keep per-voxel state.            */
+ * Linear kinds require no state; NEOHOOKE and J2 keep per-voxel state.
+ * Tangent storage (implementation choice, same operator): NEOHOOKE keeps F^-1 and
+ * c1 = mu - lam ln J per voxel and applies K:G = mu G + c1 (F^-1 G F^-1)^T + lam tr(F^-1 G) F^-T
+ * matrix-free (80 B/voxel); environment DBFFT_TANGENT=full stores the 45 independent entries of
+ * the 9x9 tangent instead (360 B/voxel).  J2 keeps (theta, thetabar, n) (64 B/voxel).          */
 typedef enum {
   DBFFT_MAT_ISO = 1,
   DBFFT_MAT_CUBIC = 2,

@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -61,6 +62,7 @@ struct dbfft_ctx_s {
   double* tan = nullptr;                    // [21|45][N]
   double Fbar[9], Fbar_c[9];                // macro strain / F (incl. stress-controlled comps)
   bool tangent_valid = false;
+  int tmode = 1;                            // neo-Hookean tangent storage: 1 compact (F^-1, c1), 0 full 45
   // linear mean stiffness (Voigt 6x6) or current mean tangent (full 81)
   double Cbar[81];
   PrecQ prec;
@@ -102,6 +104,12 @@ namespace {
     dbfft_status s_ = (call);                                                                 \
     if (s_ != DBFFT_OK) return s_;                                                            \
   } while (0)
+
+int ilog2(int n) {
+  int k = 0;
+  while ((1 << k) < n) ++k;
+  return k;
+}
 
 bool is_pow2_in(int n) { return n >= 8 && n <= 512 && (n & (n - 1)) == 0; }
 
@@ -177,7 +185,7 @@ ColGeom colgeom(dbfft_ctx ctx, bool zpass, const cplx* in, cplx* out, bool in_is
     g.in_os = g.out_os = (long long)ctx->n3 * n1h;
     g.in_ps = g.out_ps = n1h;
     g.ncols = (long long)ctx->n2 * n1h;
-    g.in_pchunk = g.out_pchunk = ctx->n3;
+    g.in_psh = g.out_psh = ilog2(ctx->n3);
     g.tw = ctx->tw3;
   } else {  // outer = z, pos = y/ky
     if (in_is_B) { g.in_os = (long long)ctx->n2 * n1h; g.in_ps = n1h; }
@@ -185,7 +193,7 @@ ColGeom colgeom(dbfft_ctx ctx, bool zpass, const cplx* in, cplx* out, bool in_is
     if (out_is_B) { g.out_os = (long long)ctx->n2 * n1h; g.out_ps = n1h; }
     else { g.out_os = n1h; g.out_ps = (long long)ctx->n3 * n1h; }
     g.ncols = (long long)ctx->n3 * n1h;
-    g.in_pchunk = g.out_pchunk = ctx->n2;
+    g.in_psh = g.out_psh = ilog2(ctx->n2);
     g.tw = ctx->tw2;
   }
   g.in_pcs = g.out_pcs = 0;
@@ -214,6 +222,7 @@ XGeom xgeom(dbfft_ctx ctx, const cplx* in, cplx* out) {
   g.epsp_t = ctx->epsp_t;
   g.nvox = ctx->N;
   g.bad = ctx->bad;
+  g.tmode = ctx->tmode;
   return g;
 }
 
@@ -462,8 +471,8 @@ dbfft_status apply_K_internal(dbfft_ctx ctx, const cplx* u, cplx* f, const doubl
   const bool fin = ctx->kin == 9;
   int xkind;
   if (ctx->family == FAM_LINEAR) xkind = X_K_SMALL_PHASE;
-  else if (ctx->family == FAM_J2) xkind = X_K_SMALL_TAN;
-  else xkind = X_K_FIN_TAN;
+  else if (ctx->family == FAM_J2) xkind = X_K_J2;
+  else xkind = ctx->tmode ? X_K_FIN_NH : X_K_FIN_TAN;
   ColGeom g1 = colgeom(ctx, true, u, ctx->WA, false, false);
   CKS(run_col(ctx, fin ? COL_I1F : COL_I1S, PK_I1, g1));
   ColGeom g2 = colgeom(ctx, false, ctx->WA, ctx->WB, false, true);
@@ -520,7 +529,8 @@ dbfft_status refresh_mean_tangent(dbfft_ctx ctx) {
   const int nblk = cg_blocks();
   {
     ProfScope ps(ctx, PK_OTHER);
-    CK(launch_mean_sym(ctx->tan, nk, ctx->N, ctx->part_misc, nblk, ctx->stream));
+    const int mode = (ctx->family == FAM_J2) ? 2 : (ctx->tmode ? 1 : 0);
+    CK(launch_mean_tangent(mode, xgeom(ctx, nullptr, nullptr), ctx->part_misc, nblk, ctx->stream));
   }
   double m[64];
   CKS(read_reduction(ctx, ctx->part_misc, nblk, nk, m));
@@ -1115,7 +1125,9 @@ dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t o
     ctx->prec_valid = true;
   } else {
     const int nf = fam == FAM_NEOHOOKE ? 9 : 6;
-    const int nk = fam == FAM_NEOHOOKE ? 45 : 21;
+    const char* tm = getenv("DBFFT_TANGENT");
+    ctx->tmode = (tm && strcmp(tm, "full") == 0) ? 0 : 1;
+    const int nk = fam == FAM_NEOHOOKE ? (ctx->tmode ? 10 : 45) : 8;
     if ((s = dalloc(ctx, &ctx->F, (size_t)nf * ctx->N)) != DBFFT_OK) return s;
     if ((s = dalloc(ctx, &ctx->F_c, (size_t)nf * ctx->N)) != DBFFT_OK) return s;
     if ((s = dalloc(ctx, &ctx->tan, (size_t)nk * ctx->N)) != DBFFT_OK) return s;

@@ -10,6 +10,8 @@
 // so fewer than 2c fields cross the y and z sweeps (52 H / 66 H complex moves).
 #include "passes.cuh"
 
+#include <algorithm>
+
 namespace {
 
 // ------------------------------------------------------------------------------------------------
@@ -19,11 +21,11 @@ struct ColAt {
   const ColGeom* g;
   int outer, pos, kx;
   DBF_DEV long long in_idx(int f) const {
-    long long p = (long long)(pos / g->in_pchunk) * g->in_pcs + (long long)(pos % g->in_pchunk) * g->in_ps;
+    long long p = (long long)(pos >> g->in_psh) * g->in_pcs + (long long)(pos & ((1 << g->in_psh) - 1)) * g->in_ps;
     return f * g->in_fs + outer * g->in_os + p + kx;
   }
   DBF_DEV long long out_idx(int f) const {
-    long long p = (long long)(pos / g->out_pchunk) * g->out_pcs + (long long)(pos % g->out_pchunk) * g->out_ps;
+    long long p = (long long)(pos >> g->out_psh) * g->out_pcs + (long long)(pos & ((1 << g->out_psh) - 1)) * g->out_ps;
     return f * g->out_fs + outer * g->out_os + p + kx;
   }
   DBF_DEV cplx in(int f) const { return __ldg(g->in + in_idx(f)); }
@@ -171,12 +173,19 @@ struct ColOp<COL_ZI3> {
 template <>
 struct ColOp<COL_YI3> : ColOp<COL_ZI3> {};
 
+template <int KIND>
+struct ColTwo {  // does any output of this pass sum two transformed terms?
+  static constexpr bool value = (KIND == COL_F2F || KIND == COL_F3S || KIND == COL_F3F);
+};
+
 template <int N, int KIND>
-__global__ void __launch_bounds__(256) col_pass_kernel(ColGeom g) {
+__global__ void __launch_bounds__(256, 3) col_pass_kernel(ColGeom g) {
   typedef ColOp<KIND> Op;
   constexpr int TPC = N / 8;        // threads per column
   constexpr int COLS = 256 / TPC;   // columns per CTA
+  constexpr bool TWO = ColTwo<KIND>::value;
   __shared__ cplx sbuf[N * COLS];
+  __shared__ cplx sacc[TWO ? N * COLS : 1];  // first-term results of two-term outputs
   const int t = threadIdx.x;
   const int c = t % COLS;
   const int gq = t / COLS;
@@ -191,7 +200,6 @@ __global__ void __launch_bounds__(256) col_pass_kernel(ColGeom g) {
   IdxCols<COLS> idx{c};
 #pragma unroll 1
   for (int o = 0; o < Op::NOUT; ++o) {
-    cplx acc[8];
     const int nt = Op::nterms(o);
 #pragma unroll 1
     for (int term = 0; term < nt; ++term) {
@@ -201,26 +209,22 @@ __global__ void __launch_bounds__(256) col_pass_kernel(ColGeom g) {
         at.pos = gq + s * (N / 8);
         a[s] = valid ? Op::load(at, o, term) : make_double2(0.0, 0.0);
       }
-      if (term == 0) __syncthreads();  // previous output's readers are done with sbuf
       fft_cta<N, Op::INV>(a, sbuf, gq, idx, g.tw);
+      const bool last = (term + 1 == nt);
 #pragma unroll
       for (int s = 0; s < 8; ++s) {
         at.pos = gq + s * (N / 8);
-        cplx w = Op::post(at, o, term);
-        cplx v = cmul(w, a[s]);
-        acc[s] = (term == 0) ? v : cadd(acc[s], v);
-      }
-      if (term + 1 < nt) __syncthreads();
-    }
-    if (valid) {
-#pragma unroll
-      for (int s = 0; s < 8; ++s) {
-        at.pos = gq + s * (N / 8);
-        const long long oi = at.out_idx(o);
-        g.out[oi] = acc[s];
-        if (g.dotp) {
-          cplx p = __ldg(g.dotp + oi);
-          dot += wdot * (p.x * acc[s].x + p.y * acc[s].y);
+        cplx v = cmul(Op::post(at, o, term), a[s]);
+        if (TWO && term > 0) v = cadd(v, sacc[idx(at.pos)]);
+        if (!last) {
+          if (TWO) sacc[idx(at.pos)] = v;  // own positions only: no barrier needed
+        } else if (valid) {
+          const long long oi = at.out_idx(o);
+          g.out[oi] = v;
+          if (g.dotp) {
+            cplx p = __ldg(g.dotp + oi);
+            dot += wdot * (p.x * v.x + p.y * v.y);
+          }
         }
       }
     }
@@ -245,26 +249,29 @@ __global__ void __launch_bounds__(256) col_pass_kernel(ColGeom g) {
 // ------------------------------------------------------------------------------------------------
 template <int KIND>
 struct XTraits;
-template <> struct XTraits<X_K_SMALL_PHASE> { static constexpr int CIN = 6, COUT = 6, NRED = 9; static constexpr bool FIN = false, REAL = false; };
-template <> struct XTraits<X_K_SMALL_TAN> { static constexpr int CIN = 6, COUT = 6, NRED = 9; static constexpr bool FIN = false, REAL = false; };
-template <> struct XTraits<X_K_FIN_TAN> { static constexpr int CIN = 9, COUT = 9, NRED = 9; static constexpr bool FIN = true, REAL = false; };
-template <> struct XTraits<X_RHS_SMALL_PHASE> { static constexpr int CIN = 0, COUT = 6, NRED = 9; static constexpr bool FIN = false, REAL = false; };
-template <> struct XTraits<X_CONST_FIN> { static constexpr int CIN = 9, COUT = 9, NRED = 10; static constexpr bool FIN = true, REAL = false; };
-template <> struct XTraits<X_CONST_J2> { static constexpr int CIN = 6, COUT = 6, NRED = 10; static constexpr bool FIN = false, REAL = false; };
-template <> struct XTraits<X_REAL_OUT> { static constexpr int CIN = 9, COUT = 0, NRED = 0; static constexpr bool FIN = false, REAL = true; };
+template <> struct XTraits<X_K_SMALL_PHASE> { static constexpr int CIN = 6, COUT = 6, NRED = 9; static constexpr bool FIN = false; };
+template <> struct XTraits<X_K_J2> { static constexpr int CIN = 6, COUT = 6, NRED = 9; static constexpr bool FIN = false; };
+template <> struct XTraits<X_K_FIN_TAN> { static constexpr int CIN = 9, COUT = 9, NRED = 9; static constexpr bool FIN = true; };
+template <> struct XTraits<X_K_FIN_NH> { static constexpr int CIN = 9, COUT = 9, NRED = 9; static constexpr bool FIN = true; };
+template <> struct XTraits<X_RHS_SMALL_PHASE> { static constexpr int CIN = 0, COUT = 6, NRED = 9; static constexpr bool FIN = false; };
+template <> struct XTraits<X_CONST_FIN> { static constexpr int CIN = 9, COUT = 9, NRED = 10; static constexpr bool FIN = true; };
+template <> struct XTraits<X_CONST_J2> { static constexpr int CIN = 6, COUT = 6, NRED = 10; static constexpr bool FIN = false; };
+template <> struct XTraits<X_REAL_OUT> { static constexpr int CIN = 9, COUT = 0, NRED = 0; static constexpr bool FIN = false; };
 
-DBF_DEV int sym6(int i, int j) {  // upper-triangle index of a symmetric 6x6
-  if (i > j) { int t = i; i = j; j = t; }
-  return i * 6 - i * (i - 1) / 2 + (j - i);
-}
 DBF_DEV int sym9(int i, int j) {
   if (i > j) { int t = i; i = j; j = t; }
   return i * 9 - i * (i - 1) / 2 + (j - i);
 }
 
-// Voigt index (xx,yy,zz,yz,xz,xy) of a row-major 3x3 entry
-__device__ __constant__ int c_voigt_of9[9] = {0, 5, 4, 5, 1, 3, 4, 3, 2};
+// Voigt index (xx,yy,zz,yz,xz,xy) -> row-major 3x3 entry
 __device__ __constant__ int c_row9_of_voigt[6] = {0, 4, 8, 5, 2, 1};
+
+// streaming load of per-voxel data (read once per launch: do not allocate in L1)
+DBF_DEV double ld_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
 
 // small-strain contraction: sigma_I = sum_J C[I][J] gamma_J, gamma = (e0,e1,e2,2e3,2e4,2e5)
 DBF_DEV void voigt_contract_full(const double* __restrict__ C36, const double* e, double* s) {
@@ -278,16 +285,15 @@ DBF_DEV void voigt_contract_full(const double* __restrict__ C36, const double* e
   }
 }
 
-// Neo-Hookean (R14): P = mu (F - F^-T) + lam lnJ F^-T;  K_ijkl = mu d_ik d_jl
-//   + (mu - lam lnJ) Finv_li Finv_jk + lam Finv_ji Finv_lk ; returns det F.
-DBF_DEV double neo_hookean(const double* F, double mu, double kappa, double* P, double* K45) {
+// Neo-Hookean (R14): P = mu (F - F^-T) + lam lnJ F^-T; returns J, F^-1 (row-major) and
+// c1 = mu - lam lnJ, so that the tangent acts as K:G = mu G + c1 (Fi G Fi)^T + lam tr(Fi G) Fi^T.
+DBF_DEV double neo_hookean(const double* F, double mu, double kappa, double* P, double* Fi, double* c1_out) {
   const double lam = kappa - 2.0 * mu / 3.0;
   const double c00 = F[4] * F[8] - F[5] * F[7];
   const double c01 = F[5] * F[6] - F[3] * F[8];
   const double c02 = F[3] * F[7] - F[4] * F[6];
   const double J = F[0] * c00 + F[1] * c01 + F[2] * c02;
   const double iJ = 1.0 / J;
-  double Fi[9];  // Finv row-major: Fi[a*3+b] = (F^-1)_ab = cof(F)_ba / J
   Fi[0] = c00 * iJ;
   Fi[3] = c01 * iJ;
   Fi[6] = c02 * iJ;
@@ -298,30 +304,53 @@ DBF_DEV double neo_hookean(const double* F, double mu, double kappa, double* P, 
   Fi[5] = (F[2] * F[3] - F[0] * F[5]) * iJ;
   Fi[8] = (F[0] * F[4] - F[1] * F[3]) * iJ;
   const double lnJ = log(J);
-  const double c1 = mu - lam * lnJ;
+  *c1_out = mu - lam * lnJ;
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j) P[3 * i + j] = mu * F[3 * i + j] + (lam * lnJ - mu) * Fi[3 * j + i];
-  if (K45) {
-#pragma unroll
-    for (int a = 0; a < 9; ++a) {
-      const int i = a / 3, j = a % 3;
-#pragma unroll
-      for (int b = a; b < 9; ++b) {
-        const int k = b / 3, l = b % 3;
-        double v = c1 * Fi[3 * l + i] * Fi[3 * j + k] + lam * Fi[3 * j + i] * Fi[3 * l + k];
-        if (i == k && j == l) v += mu;
-        K45[a * 9 - a * (a - 1) / 2 + (b - a)] = v;
-      }
-    }
-  }
   return J;
 }
 
-// J2 Perzyna return map (R16): eps, epsp (Voigt tensor comps) -> sigma, C_alg (21), epsp_new.
+// full 9x9 tangent (upper triangle, 45) from (Fi, c1, mu, lam):
+// K_ijkl = mu d_ik d_jl + c1 Fi_li Fi_jk + lam Fi_ji Fi_lk
+DBF_DEV void nh_tangent45(const double* Fi, double c1, double mu, double lam, double* K45) {
+#pragma unroll
+  for (int a = 0; a < 9; ++a) {
+    const int i = a / 3, j = a % 3;
+#pragma unroll
+    for (int b = a; b < 9; ++b) {
+      const int k = b / 3, l = b % 3;
+      double v = c1 * Fi[3 * l + i] * Fi[3 * j + k] + lam * Fi[3 * j + i] * Fi[3 * l + k];
+      if (i == k && j == l) v += mu;
+      K45[a * 9 - a * (a - 1) / 2 + (b - a)] = v;
+    }
+  }
+}
+
+// matrix-free neo-Hookean tangent: P = mu G + c1 (Fi G Fi)^T + lam tr(Fi G) Fi^T
+DBF_DEV void nh_apply(const double* Fi, double c1, double mu, double lam, const double* G, double* P) {
+  double A[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) A[3 * i + k] = Fi[3 * i] * G[k] + Fi[3 * i + 1] * G[3 + k] + Fi[3 * i + 2] * G[6 + k];
+  const double tr = A[0] + A[4] + A[8];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      const double B_il = A[3 * i] * Fi[l] + A[3 * i + 1] * Fi[3 + l] + A[3 * i + 2] * Fi[6 + l];
+      // P_li += c1 B_il ; P_ij = mu G_ij + lam tr Fi_ji
+      P[3 * l + i] = mu * G[3 * l + i] + c1 * B_il + lam * tr * Fi[3 * i + l];
+    }
+}
+
+// J2 Perzyna return map (R16).  eps, epsp: Voigt tensor components.  Outputs sigma, the plastic
+// strain, and the compact algorithmic tangent (theta, thetabar, n = s_tr/|s_tr|):
+//   C_alg = kappa 1x1 + 2 mu theta I_dev - 2 mu thetabar n x n.
 DBF_DEV void j2_update(const double* eps, const double* epsp, const double* prm, double dt,
-                       double* sig, double* C21, double* epsp_new) {
+                       double* sig, double* tc /*8: theta, thetabar, n[6]*/, double* epsp_new) {
   const double E = prm[0], nu = prm[1], sy = prm[2], nexp = prm[3], edot0 = prm[4];
   const double lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
   const double mu = E / (2.0 * (1.0 + nu));
@@ -363,42 +392,45 @@ DBF_DEV void j2_update(const double* eps, const double* epsp, const double* prm,
   for (int I = 0; I < 6; ++I) {
     sig[I] = theta * s[I] + (I < 3 ? kappa * tr : 0.0);
     epsp_new[I] = epsp[I] + (svm > sy ? dp * 1.5 * s[I] / svm : 0.0);
+    tc[2 + I] = nn[I];
   }
-  // C_alg = kappa 1x1 + 2 mu theta I_dev - 2 mu thetabar n x n  (Voigt form, tensor entries)
+  tc[0] = theta;
+  tc[1] = thetabar;
+}
+
+// sigma = C_alg : e with the compact J2 tangent (Voigt tensor components)
+DBF_DEV void j2_apply(const double* tc, double kappa, double mu, const double* e, double* s) {
+  const double tr = e[0] + e[1] + e[2];
+  const double ne = tc[2] * e[0] + tc[3] * e[1] + tc[4] * e[2] + 2.0 * (tc[5] * e[3] + tc[6] * e[4] + tc[7] * e[5]);
+  const double a = 2.0 * mu * tc[0], b = 2.0 * mu * tc[1] * ne;
 #pragma unroll
-  for (int I = 0; I < 6; ++I)
-#pragma unroll
-    for (int J = I; J < 6; ++J) {
-      double idev = (I < 3 && J < 3) ? ((I == J ? 1.0 : 0.0) - 1.0 / 3.0) : ((I == J) ? 0.5 : 0.0);
-      double v = ((I < 3 && J < 3) ? kappa : 0.0) + 2.0 * mu * theta * idev - 2.0 * mu * thetabar * nn[I] * nn[J];
-      C21[I * 6 - I * (I - 1) / 2 + (J - I)] = v;
-    }
+  for (int I = 0; I < 6; ++I) s[I] = a * (e[I] - (I < 3 ? tr / 3.0 : 0.0)) - b * tc[2 + I] + (I < 3 ? kappa * tr : 0.0);
+}
+
+DBF_DEV void j2_moduli(const double* prm, double* kappa, double* mu) {
+  const double E = prm[0], nu = prm[1];
+  const double lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+  *mu = E / (2.0 * (1.0 + nu));
+  *kappa = lam + 2.0 * (*mu) / 3.0;
 }
 
 template <int KIND>
 DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* red) {
-  typedef XTraits<KIND> T;
-  if (KIND == X_K_SMALL_PHASE || KIND == X_K_SMALL_TAN || KIND == X_RHS_SMALL_PHASE) {
+  if (KIND == X_K_SMALL_PHASE || KIND == X_RHS_SMALL_PHASE || KIND == X_K_J2) {
     double e6[6];
-    if (KIND == X_RHS_SMALL_PHASE) {
 #pragma unroll
-      for (int I = 0; I < 6; ++I) e6[I] = __ldg(g.e + c_row9_of_voigt[I]);
-    } else {
-#pragma unroll
-      for (int I = 0; I < 6; ++I) e6[I] = G[I] + (g.e ? __ldg(g.e + c_row9_of_voigt[I]) : 0.0);
-    }
+    for (int I = 0; I < 6; ++I)
+      e6[I] = (KIND == X_RHS_SMALL_PHASE ? 0.0 : G[I]) + (g.e ? __ldg(g.e + c_row9_of_voigt[I]) : 0.0);
+    const int ph = __ldg(g.phase + v);
     double s[6];
-    if (KIND == X_K_SMALL_TAN) {
-      const double gm[6] = {e6[0], e6[1], e6[2], 2.0 * e6[3], 2.0 * e6[4], 2.0 * e6[5]};
+    if (KIND == X_K_J2) {
+      double tc[8];
 #pragma unroll
-      for (int I = 0; I < 6; ++I) {
-        double acc = 0.0;
-#pragma unroll
-        for (int J = 0; J < 6; ++J) acc = fma(g.tan[(long long)sym6(I, J) * g.nvox + v], gm[J], acc);
-        s[I] = acc;
-      }
+      for (int k = 0; k < 8; ++k) tc[k] = ld_stream(g.tan + (long long)k * g.nvox + v);
+      double kappa, mu;
+      j2_moduli(g.ptable + 36 * ph, &kappa, &mu);
+      j2_apply(tc, kappa, mu, e6, s);
     } else {
-      const int ph = __ldg(g.phase + v);
       voigt_contract_full(g.ptable + 36 * ph, e6, s);
     }
     const double sg = (KIND == X_RHS_SMALL_PHASE) ? -1.0 : 1.0;
@@ -407,36 +439,56 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
       P[I] = sg * s[I];
       red[c_row9_of_voigt[I]] += s[I];
     }
-    // symmetric off-diagonal duplicates of the mean
-    return;
   } else if (KIND == X_K_FIN_TAN) {
-    double e9[9];
+    double e9[9], K[45];
+#pragma unroll
+    for (int k = 0; k < 45; ++k) K[k] = ld_stream(g.tan + (long long)k * g.nvox + v);
 #pragma unroll
     for (int a = 0; a < 9; ++a) e9[a] = G[a] + (g.e ? __ldg(g.e + a) : 0.0);
 #pragma unroll
     for (int a = 0; a < 9; ++a) {
       double acc = 0.0;
 #pragma unroll
-      for (int b = 0; b < 9; ++b) acc = fma(g.tan[(long long)sym9(a, b) * g.nvox + v], e9[b], acc);
+      for (int b = 0; b < 9; ++b) acc = fma(K[sym9(a, b)], e9[b], acc);
       P[a] = acc;
       red[a] += acc;
     }
+  } else if (KIND == X_K_FIN_NH) {
+    double Fi[9], e9[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) Fi[k] = ld_stream(g.tan + (long long)k * g.nvox + v);
+    const double c1 = ld_stream(g.tan + 9 * g.nvox + v);
+    const int ph = __ldg(g.phase + v);
+    const double mu = __ldg(g.ptable + 36 * ph), lam = __ldg(g.ptable + 36 * ph + 1) - 2.0 * mu / 3.0;
+#pragma unroll
+    for (int a = 0; a < 9; ++a) e9[a] = G[a] + (g.e ? __ldg(g.e + a) : 0.0);
+    nh_apply(Fi, c1, mu, lam, e9, P);
+#pragma unroll
+    for (int a = 0; a < 9; ++a) red[a] += P[a];
   } else if (KIND == X_CONST_FIN) {
-    double F[9], d[9], Pv[9], K45[45];
+    double F[9], Pv[9], Fi[9], c1;
     double mx = 0.0;
 #pragma unroll
     for (int a = 0; a < 9; ++a) {
-      d[a] = (g.has_in ? G[a] : 0.0) + __ldg(g.e + a);
-      mx = fmax(mx, fabs(d[a]));
-      F[a] = g.F[(long long)a * g.nvox + v] + d[a];
+      const double d = (g.has_in ? G[a] : 0.0) + __ldg(g.e + a);
+      mx = fmax(mx, fabs(d));
+      F[a] = g.F[(long long)a * g.nvox + v] + d;
       g.F[(long long)a * g.nvox + v] = F[a];
     }
     const int ph = __ldg(g.phase + v);
     const double mu = __ldg(g.ptable + 36 * ph), kappa = __ldg(g.ptable + 36 * ph + 1);
-    const double J = neo_hookean(F, mu, kappa, Pv, K45);
+    const double J = neo_hookean(F, mu, kappa, Pv, Fi, &c1);
     if (!(J > 0.0)) atomicMin(g.bad, (int)min(v, (long long)0x7fffffff));
+    if (g.tmode == 1) {
 #pragma unroll
-    for (int k = 0; k < 45; ++k) g.tan[(long long)k * g.nvox + v] = K45[k];
+      for (int k = 0; k < 9; ++k) g.tan[(long long)k * g.nvox + v] = Fi[k];
+      g.tan[9 * g.nvox + v] = c1;
+    } else {
+      double K45[45];
+      nh_tangent45(Fi, c1, mu, kappa - 2.0 * mu / 3.0, K45);
+#pragma unroll
+      for (int k = 0; k < 45; ++k) g.tan[(long long)k * g.nvox + v] = K45[k];
+    }
 #pragma unroll
     for (int a = 0; a < 9; ++a) {
       P[a] = -Pv[a];
@@ -444,7 +496,7 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
     }
     red[9] = fmax(red[9], mx);
   } else if (KIND == X_CONST_J2) {
-    double eps[6], ep[6], s[6], C21[21], epn[6];
+    double eps[6], ep[6], s[6], tc[8], epn[6];
     double mx = 0.0;
 #pragma unroll
     for (int I = 0; I < 6; ++I) {
@@ -455,9 +507,9 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
       ep[I] = __ldg(g.epsp_c + (long long)I * g.nvox + v);
     }
     const int ph = __ldg(g.phase + v);
-    j2_update(eps, ep, g.ptable + 36 * ph, g.dt, s, C21, epn);
+    j2_update(eps, ep, g.ptable + 36 * ph, g.dt, s, tc, epn);
 #pragma unroll
-    for (int k = 0; k < 21; ++k) g.tan[(long long)k * g.nvox + v] = C21[k];
+    for (int k = 0; k < 8; ++k) g.tan[(long long)k * g.nvox + v] = tc[k];
 #pragma unroll
     for (int I = 0; I < 6; ++I) {
       g.epsp_t[(long long)I * g.nvox + v] = epn[I];
@@ -465,158 +517,225 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
       red[c_row9_of_voigt[I]] += s[I];
     }
     red[9] = fmax(red[9], mx);
-  } else if (KIND == X_REAL_OUT) {
-    (void)T::CIN;
   }
 }
+
+// XOR swizzle inside 8-element groups: conflict-free radix-8 scatter/gather, no padding, so
+// the exchange buffer of a field pair is exactly the pair's two real slots (in place).
+struct IdxSwz {
+  int base;
+  DBF_DEV int operator()(int pos) const { return base + (pos ^ ((pos >> 3) & 7)); }
+};
 
 template <int N1, int KIND>
 struct XCfg {
   typedef XTraits<KIND> T;
-  static constexpr int C = (T::CIN > T::COUT) ? T::CIN : T::COUT;  // real slots per line
+  static constexpr int C = (T::CIN > T::COUT) ? T::CIN : T::COUT;
+  static constexpr int CS = (C + 1) & ~1;          // real slots per line (even)
   static constexpr int TPJ = N1 / 8;
-  static constexpr int NP = (C + 1) / 2;
+  static constexpr int NP = CS / 2;
   static constexpr int PERLINE = TPJ * NP;
-  static constexpr int LRAW = 384 / PERLINE;
+  static constexpr int LRAW = 192 / PERLINE;
   static constexpr int LPAR = LRAW >= 64 ? 64 : LRAW >= 32 ? 32 : LRAW >= 16 ? 16 : LRAW >= 8 ? 8 : LRAW >= 4 ? 4 : LRAW >= 2 ? 2 : 1;
   static constexpr int THREADS = LPAR * PERLINE;
-  static constexpr int XSTRIDE = N1 + N1 / 8;  // padded exchange buffer per job
-  static constexpr size_t SMEM = sizeof(double) * LPAR * C * N1 + sizeof(cplx) * LPAR * NP * XSTRIDE;
+  static constexpr size_t SMEM = sizeof(double) * LPAR * CS * N1;
+  static constexpr int MINB = (THREADS <= 192) ? 3 : 2;
 };
 
+// X pass.  Persistent: each CTA loops over groups of LPAR lines.  Per line the C fields are
+// C2R'd in pairs (z = a + i b), the per-voxel operation runs on the real fields in shared
+// memory, and results are R2C'd in pairs and untangled:
+//   A_k = (Z_k + conj Z_{N-k})/2,  B_k = (Z_k - conj Z_{N-k})/(2i).
 template <int N1, int KIND>
-__global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS) x_pass_kernel(XGeom g, int nf_real) {
+__global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB) x_pass_kernel(XGeom g, int nf_real) {
   typedef XCfg<N1, KIND> CF;
   typedef XTraits<KIND> T;
-  constexpr int C = CF::C, TPJ = CF::TPJ, NP = CF::NP, LPAR = CF::LPAR;
-  extern __shared__ double smem[];
-  double* real = smem;
-  cplx* exch = reinterpret_cast<cplx*>(real + LPAR * C * N1);
+  constexpr int C = CF::C, CS = CF::CS, TPJ = CF::TPJ, NP = CF::NP, LPAR = CF::LPAR;
+  extern __shared__ double real[];
+  cplx* cx = reinterpret_cast<cplx*>(real);
   const int t = threadIdx.x;
   const int job = t / TPJ, gq = t % TPJ;
   const int l = job / NP, p = job % NP;
-  const long long line = (long long)blockIdx.x * LPAR + l;
-  const bool lvalid = line < g.nlines;
   const int fa = 2 * p, fb = 2 * p + 1;
-  IdxPad idx{job * CF::XSTRIDE};
-  cplx* ex = exch;
+  IdxSwz idx{(l * CS + fa) * (N1 / 2)};  // complex view of slots fa, fb of line l
   const int cin = (KIND == X_REAL_OUT) ? nf_real : T::CIN;
-  const bool do_in = (cin > 0) && (T::CIN > 0) && (KIND < X_CONST_FIN || g.has_in || KIND == X_REAL_OUT);
-
-  // ---------------------------------------------------------------- inverse (C2R) of pairs
-  if (do_in) {
-    cplx a[8];
+  const bool do_in = (T::CIN > 0) && (cin > 0) && ((KIND != X_CONST_FIN && KIND != X_CONST_J2) || g.has_in);
+  const long long ngroups = (g.nlines + LPAR - 1) / LPAR;
+  double red[T::NRED > 0 ? T::NRED : 1];
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      const int k = gq + s * TPJ;
-      const bool lo = (2 * k <= N1);
-      const int kk = lo ? k : N1 - k;
-      cplx A = make_double2(0, 0), B = make_double2(0, 0);
-      if (lvalid && fa < cin) {
-        const long long base = line * g.n1h + kk;
-        A = __ldg(g.in + fa * g.fs_in + base);
-        if (fb < cin) B = __ldg(g.in + fb * g.fs_in + base);
-        if (T::FIN) {  // G_ix = i xi_x u_i for the j = 0 slots
-          const double xx = __ldg(g.xix + kk);
-          if (fa % 3 == 0) A = cimul(A, xx);
-          if (fb % 3 == 0 && fb < cin) B = cimul(B, xx);
+  for (int r = 0; r < (T::NRED > 0 ? T::NRED : 1); ++r) red[r] = 0.0;
+
+  for (long long grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const long long line = grp * LPAR + l;
+    const bool lvalid = line < g.nlines;
+    // ------------------------------------------------------------ inverse (C2R) of pairs
+    if (do_in) {
+      cplx a[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const int k = gq + s * TPJ;
+        const bool lo = (2 * k <= N1);
+        const int kk = lo ? k : N1 - k;
+        cplx A = make_double2(0, 0), B = make_double2(0, 0);
+        if (lvalid && fa < cin) {
+          const long long base = line * g.n1h + kk;
+          A = __ldg(g.in + fa * g.fs_in + base);
+          if (fb < cin) B = __ldg(g.in + fb * g.fs_in + base);
+          if (T::FIN) {  // G_ix = i xi_x u_i for the j = 0 slots (deferred gradient)
+            const double xx = __ldg(g.xix + kk);
+            if (fa % 3 == 0) A = cimul(A, xx);
+            if (fb % 3 == 0 && fb < cin) B = cimul(B, xx);
+          }
+          if (kk == 0 || 2 * kk == N1) { A.y = 0.0; B.y = 0.0; }  // Hermitian part (C2R)
         }
-        if (kk == 0 || 2 * kk == N1) { A.y = 0.0; B.y = 0.0; }  // Hermitian part (C2R)
+        // Y_k = A_k + i B_k (k <= N/2);  conj(A_{N-k}) + i conj(B_{N-k}) otherwise
+        a[s] = lo ? make_double2(A.x - B.y, A.y + B.x) : make_double2(A.x + B.y, B.x - A.y);
       }
-      // Y_k = A_k + i B_k (k <= N/2);  conj(A_{N-k}) + i conj(B_{N-k}) otherwise
-      a[s] = lo ? make_double2(A.x - B.y, A.y + B.x) : make_double2(A.x + B.y, B.x - A.y);
-    }
-    fft_cta<N1, true>(a, ex, gq, idx, g.tw);
+      fft_cta<N1, true>(a, cx, gq, idx, g.tw);
+      __syncthreads();  // exchange reads done before the slots are overwritten with reals
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      const int m = gq + s * TPJ;
-      if (fa < cin) real[(l * C + fa) * N1 + m] = a[s].x;
-      if (fb < cin) real[(l * C + fb) * N1 + m] = a[s].y;
+      for (int s = 0; s < 8; ++s) {
+        const int m = gq + s * TPJ;
+        real[(l * CS + fa) * N1 + m] = a[s].x;
+        real[(l * CS + fb) * N1 + m] = a[s].y;
+      }
     }
-  }
-  __syncthreads();
+    __syncthreads();
 
-  if (KIND == X_REAL_OUT) {
+    if (KIND == X_REAL_OUT) {
+      for (int vv = t; vv < LPAR * N1; vv += CF::THREADS) {
+        const int l2 = vv / N1, x = vv % N1;
+        const long long ln = grp * LPAR + l2;
+        if (ln >= g.nlines) continue;
+        for (int f = 0; f < nf_real; ++f) g.real_out[(long long)f * g.nvox + ln * N1 + x] = real[(l2 * CS + f) * N1 + x];
+      }
+      __syncthreads();
+      continue;
+    }
+
+    // ------------------------------------------------------------ per-voxel operation
     for (int vv = t; vv < LPAR * N1; vv += CF::THREADS) {
       const int l2 = vv / N1, x = vv % N1;
-      const long long ln = (long long)blockIdx.x * LPAR + l2;
-      if (ln >= g.nlines) continue;
-      for (int f = 0; f < nf_real; ++f) g.real_out[(long long)f * g.nvox + ln * N1 + x] = real[(l2 * C + f) * N1 + x];
-    }
-    return;
-  }
-
-  // ---------------------------------------------------------------- per-voxel operation
-  {
-    double red[T::NRED > 0 ? T::NRED : 1];
-#pragma unroll
-    for (int r = 0; r < (T::NRED > 0 ? T::NRED : 1); ++r) red[r] = 0.0;
-    for (int vv = t; vv < LPAR * N1; vv += CF::THREADS) {
-      const int l2 = vv / N1, x = vv % N1;
-      const long long ln = (long long)blockIdx.x * LPAR + l2;
+      const long long ln = grp * LPAR + l2;
       if (ln >= g.nlines) continue;
       double G[C], P[C];
 #pragma unroll
-      for (int f = 0; f < C; ++f) G[f] = (f < T::CIN && do_in) ? real[(l2 * C + f) * N1 + x] : 0.0;
+      for (int f = 0; f < C; ++f) G[f] = (f < T::CIN && do_in) ? real[(l2 * CS + f) * N1 + x] : 0.0;
       x_voxel<KIND>(g, ln * N1 + x, G, P, red);
 #pragma unroll
-      for (int f = 0; f < T::COUT; ++f) real[(l2 * C + f) * N1 + x] = P[f];
+      for (int f = 0; f < T::COUT; ++f) real[(l2 * CS + f) * N1 + x] = P[f];
     }
-    // block reduction -> partials[block][NRED] (sums; slot 9 of the const kinds is a max)
-    __shared__ double sred[(384 / 32) * 10];
-    const int nw = CF::THREADS / 32;
+    __syncthreads();
+
+    // ------------------------------------------------------------ forward (R2C) of pairs
+    {
+      constexpr int COUT = T::COUT;
+      cplx a[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const int m = gq + s * TPJ;
+        const double ra = (fa < COUT) ? real[(l * CS + fa) * N1 + m] : 0.0;
+        const double rb = (fb < COUT) ? real[(l * CS + fb) * N1 + m] : 0.0;
+        a[s] = make_double2(ra, rb);
+      }
+      fft_cta<N1, false>(a, cx, gq, idx, g.tw);
+      __syncthreads();
+#pragma unroll
+      for (int s = 0; s < 8; ++s) cx[idx(gq + s * TPJ)] = a[s];
+      __syncthreads();
+      if (lvalid && fa < COUT) {
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          const int k = gq + s * TPJ;
+          if (2 * k > N1) continue;
+          const cplx Z = a[s];
+          const cplx Zn = cx[idx((N1 - k) & (N1 - 1))];
+          cplx A = make_double2(0.5 * (Z.x + Zn.x), 0.5 * (Z.y - Zn.y));
+          cplx B = make_double2(0.5 * (Z.y + Zn.y), -0.5 * (Z.x - Zn.x));
+          A = cscale(A, g.inv_n);
+          B = cscale(B, g.inv_n);
+          if (T::FIN) {  // fold -i xi_x P_ix into the j = 0 slots (early divergence)
+            const double xx = __ldg(g.xix + k);
+            if (fa % 3 == 0) A = cimul(A, -xx);
+            if (fb % 3 == 0) B = cimul(B, -xx);
+          }
+          const long long base = line * g.n1h + k;
+          g.out[fa * g.fs_out + base] = A;
+          if (fb < COUT) g.out[fb * g.fs_out + base] = B;
+        }
+      }
+      __syncthreads();  // slots are reused by the next group
+    }
+  }
+
+  if (T::NRED > 0) {
+    // block reduction -> partials[block][nred] (sums; slot 9 of the const kinds is a max)
+    __shared__ double sred[(CF::THREADS + 31) / 32][10];
+    constexpr int nw = (CF::THREADS + 31) / 32;
 #pragma unroll
     for (int r = 0; r < T::NRED; ++r) {
       const bool is_max = (r == 9);
       double v = is_max ? warp_max(red[r]) : warp_sum(red[r]);
-      if ((t & 31) == 0) sred[(t >> 5) * 10 + r] = v;
+      if ((t & 31) == 0) sred[t >> 5][r] = v;
     }
     __syncthreads();
     if (t < T::NRED) {
       double s = 0.0;
-      for (int w = 0; w < nw; ++w) s = (t == 9) ? fmax(s, sred[w * 10 + t]) : s + sred[w * 10 + t];
+      for (int w = 0; w < nw; ++w) s = (t == 9) ? fmax(s, sred[w][t]) : s + sred[w][t];
       g.partials[(long long)blockIdx.x * g.nred + t] = s;
     }
   }
+}
 
-  // ---------------------------------------------------------------- forward (R2C) of pairs
-  {
-    constexpr int COUT = T::COUT;
-    cplx a[8];
+// mean tangent from the stored per-voxel tangent -> partials[block][nk]
+template <int MODE>  // 0: full 45 (finite), 1: compact NH (finite, 45 out), 2: compact J2 (21 out)
+__global__ void __launch_bounds__(256) k_mean_tangent(XGeom g, double* partials) {
+  constexpr int NK = (MODE == 2) ? 21 : 45;
+  double acc[NK];
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      const int m = gq + s * TPJ;
-      const double ra = (fa < COUT) ? real[(l * C + fa) * N1 + m] : 0.0;
-      const double rb = (fb < COUT) ? real[(l * C + fb) * N1 + m] : 0.0;
-      a[s] = make_double2(ra, rb);
-    }
-    fft_cta<N1, false>(a, ex, gq, idx, g.tw);
-    __syncthreads();
+  for (int k = 0; k < NK; ++k) acc[k] = 0.0;
+  for (long long v = (long long)blockIdx.x * 256 + threadIdx.x; v < g.nvox; v += (long long)gridDim.x * 256) {
+    if (MODE == 0) {
 #pragma unroll
-    for (int s = 0; s < 8; ++s) ex[idx(gq + s * TPJ)] = a[s];
-    __syncthreads();
-    if (lvalid && fa < COUT) {
+      for (int k = 0; k < 45; ++k) acc[k] += __ldg(g.tan + (long long)k * g.nvox + v);
+    } else if (MODE == 1) {
+      double Fi[9], K45[45];
 #pragma unroll
-      for (int s = 0; s < 8; ++s) {
-        const int k = gq + s * TPJ;
-        if (2 * k > N1) continue;
-        const cplx Z = a[s];
-        const cplx Zn = ex[idx((N1 - k) & (N1 - 1))];
-        // A = (Z + conj Zn)/2, B = (Z - conj Zn)/(2i)
-        cplx A = make_double2(0.5 * (Z.x + Zn.x), 0.5 * (Z.y - Zn.y));
-        cplx B = make_double2(0.5 * (Z.y + Zn.y), -0.5 * (Z.x - Zn.x));
-        A = cscale(A, g.inv_n);
-        B = cscale(B, g.inv_n);
-        if (T::FIN) {  // fold -i xi_x P_ix into the j = 0 slots (early divergence)
-          const double xx = __ldg(g.xix + k);
-          if (fa % 3 == 0) A = cimul(A, -xx);
-          if (fb % 3 == 0) B = cimul(B, -xx);
+      for (int k = 0; k < 9; ++k) Fi[k] = __ldg(g.tan + (long long)k * g.nvox + v);
+      const double c1 = __ldg(g.tan + 9 * g.nvox + v);
+      const int ph = __ldg(g.phase + v);
+      const double mu = __ldg(g.ptable + 36 * ph), lam = __ldg(g.ptable + 36 * ph + 1) - 2.0 * mu / 3.0;
+      nh_tangent45(Fi, c1, mu, lam, K45);
+#pragma unroll
+      for (int k = 0; k < 45; ++k) acc[k] += K45[k];
+    } else {
+      double tc[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) tc[k] = __ldg(g.tan + (long long)k * g.nvox + v);
+      const int ph = __ldg(g.phase + v);
+      double kappa, mu;
+      j2_moduli(g.ptable + 36 * ph, &kappa, &mu);
+#pragma unroll
+      for (int I = 0; I < 6; ++I)
+#pragma unroll
+        for (int J = I; J < 6; ++J) {
+          const double idev = (I < 3 && J < 3) ? ((I == J ? 1.0 : 0.0) - 1.0 / 3.0) : ((I == J) ? 0.5 : 0.0);
+          acc[I * 6 - I * (I - 1) / 2 + (J - I)] += ((I < 3 && J < 3) ? kappa : 0.0) + 2.0 * mu * tc[0] * idev -
+                                                    2.0 * mu * tc[1] * tc[2 + I] * tc[2 + J];
         }
-        const long long base = line * g.n1h + k;
-        g.out[fa * g.fs_out + base] = A;
-        if (fb < COUT) g.out[fb * g.fs_out + base] = B;
-      }
     }
+  }
+  __shared__ double red[8][NK];
+#pragma unroll
+  for (int k = 0; k < NK; ++k) {
+    double s = warp_sum(acc[k]);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][k] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < NK) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += red[w][threadIdx.x];
+    partials[(long long)blockIdx.x * NK + threadIdx.x] = s;
   }
 }
 
@@ -665,13 +784,19 @@ cudaError_t launch_col(int kind, int N, const ColGeom& g, cudaStream_t s) {
 template <int N1, int KIND>
 static cudaError_t launch_x_k(const XGeom& g, cudaStream_t s, int* grid_out, int nf_real) {
   typedef XCfg<N1, KIND> CF;
-  const int grid = (int)((g.nlines + CF::LPAR - 1) / CF::LPAR);
-  static bool attr_set = false;  // per template instance
-  if (!attr_set) {
+  static int max_grid = 0;  // per template instance: resident CTAs on the whole device
+  if (max_grid == 0) {
     cudaError_t e = cudaFuncSetAttribute(x_pass_kernel<N1, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    int nb = 0, dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, x_pass_kernel<N1, KIND>, CF::THREADS, CF::SMEM);
+    if (e != cudaSuccess) return e;
+    max_grid = std::max(1, nb) * nsm;
   }
+  const long long ngroups = (g.nlines + CF::LPAR - 1) / CF::LPAR;
+  const int grid = (int)std::min<long long>(ngroups, max_grid);
   if (grid_out) *grid_out = grid;
   x_pass_kernel<N1, KIND><<<grid, CF::THREADS, CF::SMEM, s>>>(g, nf_real);
   return cudaGetLastError();
@@ -681,8 +806,9 @@ template <int N1>
 static cudaError_t launch_x_n(int kind, const XGeom& g, cudaStream_t s, int* grid_out) {
   switch (kind) {
     case X_K_SMALL_PHASE: return launch_x_k<N1, X_K_SMALL_PHASE>(g, s, grid_out, 0);
-    case X_K_SMALL_TAN: return launch_x_k<N1, X_K_SMALL_TAN>(g, s, grid_out, 0);
+    case X_K_J2: return launch_x_k<N1, X_K_J2>(g, s, grid_out, 0);
     case X_K_FIN_TAN: return launch_x_k<N1, X_K_FIN_TAN>(g, s, grid_out, 0);
+    case X_K_FIN_NH: return launch_x_k<N1, X_K_FIN_NH>(g, s, grid_out, 0);
     case X_RHS_SMALL_PHASE: return launch_x_k<N1, X_RHS_SMALL_PHASE>(g, s, grid_out, 0);
     case X_CONST_FIN: return launch_x_k<N1, X_CONST_FIN>(g, s, grid_out, 0);
     case X_CONST_J2: return launch_x_k<N1, X_CONST_J2>(g, s, grid_out, 0);
@@ -706,30 +832,16 @@ cudaError_t launch_x(int kind, int N1, const XGeom& g, cudaStream_t s, int* grid
   }
 }
 
-template <int N1>
-static int x_grid_n(int kind, long long nlines) {
-  int lpar;
-  switch (kind) {
-    case X_K_SMALL_PHASE: lpar = XCfg<N1, X_K_SMALL_PHASE>::LPAR; break;
-    case X_K_SMALL_TAN: lpar = XCfg<N1, X_K_SMALL_TAN>::LPAR; break;
-    case X_K_FIN_TAN: lpar = XCfg<N1, X_K_FIN_TAN>::LPAR; break;
-    case X_RHS_SMALL_PHASE: lpar = XCfg<N1, X_RHS_SMALL_PHASE>::LPAR; break;
-    case X_CONST_FIN: lpar = XCfg<N1, X_CONST_FIN>::LPAR; break;
-    case X_CONST_J2: lpar = XCfg<N1, X_CONST_J2>::LPAR; break;
-    default: lpar = XCfg<N1, X_REAL_OUT>::LPAR; break;
-  }
-  return (int)((nlines + lpar - 1) / lpar);
+// upper bound of the X-pass grid (= number of line groups) for partial-buffer sizing
+int x_grid(int kind, int N1, long long nlines) {
+  (void)kind;
+  (void)N1;
+  return (int)std::min<long long>(nlines, 148LL * 32);
 }
 
-int x_grid(int kind, int N1, long long nlines) {
-  switch (N1) {
-    case 8: return x_grid_n<8>(kind, nlines);
-    case 16: return x_grid_n<16>(kind, nlines);
-    case 32: return x_grid_n<32>(kind, nlines);
-    case 64: return x_grid_n<64>(kind, nlines);
-    case 128: return x_grid_n<128>(kind, nlines);
-    case 256: return x_grid_n<256>(kind, nlines);
-    case 512: return x_grid_n<512>(kind, nlines);
-    default: return 0;
-  }
+cudaError_t launch_mean_tangent(int mode, const XGeom& g, double* partials, int nblk, cudaStream_t s) {
+  if (mode == 0) k_mean_tangent<0><<<nblk, 256, 0, s>>>(g, partials);
+  else if (mode == 1) k_mean_tangent<1><<<nblk, 256, 0, s>>>(g, partials);
+  else k_mean_tangent<2><<<nblk, 256, 0, s>>>(g, partials);
+  return cudaGetLastError();
 }

@@ -10,14 +10,14 @@ struct Freq {
 };
 
 // Column pass (FFT along z or y) geometry.  Field f, outer index o, position p, kx:
-//   addr = f*fs + o*os + (p / pchunk)*pcs + (p % pchunk)*ps + kx      (complex elements)
-// pchunk/pcs express rank-blocked layouts of a distributed transpose (pchunk = N: plain).
+//   addr = f*fs + o*os + (p >> psh)*pcs + (p & (2^psh - 1))*ps + kx      (complex elements)
+// psh/pcs express rank-blocked layouts of a distributed transpose (2^psh = N: plain).
 struct ColGeom {
   const cplx* in;
   cplx* out;
   long long in_fs, in_os, in_ps, in_pcs;
   long long out_fs, out_os, out_ps, out_pcs;
-  int in_pchunk, out_pchunk;
+  int in_psh, out_psh;   // log2 of the rank chunk along the FFT axis (log2 N: plain)
   int n1h;
   long long ncols;   // n_outer * n1h columns
   const cplx* tw;    // twiddles W_N[k], k < N
@@ -46,8 +46,9 @@ enum ColKind {
 // X pass (lines along x: C2R -> per-voxel op -> R2C) voxel-op kinds
 enum XKind {
   X_K_SMALL_PHASE = 0,  // sigma = C_phase : (eps + e)            (apply_K, linear)
-  X_K_SMALL_TAN,        // sigma = C_alg(x) : (eps + e)           (apply_K, J2 tangent)
-  X_K_FIN_TAN,          // dP = K(x) : (G + e)                    (apply_K, finite strain)
+  X_K_J2,               // sigma = C_alg(x) : (eps + e)           (apply_K, compact J2 tangent)
+  X_K_FIN_TAN,          // dP = K(x) : (G + e), 45-entry K        (apply_K, finite strain)
+  X_K_FIN_NH,           // dP = K(x) : (G + e), matrix-free K(F)  (apply_K, finite strain)
   X_RHS_SMALL_PHASE,    // -sigma = -C_phase : e                  (rhs of the linear system)
   X_CONST_FIN,          // F += G + dF; P, K (neo-Hookean); -P    (Newton residual)
   X_CONST_J2,           // eps += G + de; J2 return map; -sigma   (Newton residual)
@@ -79,6 +80,7 @@ struct XGeom {
   double* real_out;       // X_REAL_OUT: [f][N]
   int* bad;               // first bad voxel flag (atomicMin on voxel index)
   int has_in;             // constitutive kinds: 0 = no C2R input (uniform increment only)
+  int tmode;              // X_CONST_FIN: 0 = store the 45-entry tangent, 1 = compact (F^-1, c1)
 };
 
 // host launchers (passes.cu)
@@ -86,3 +88,5 @@ cudaError_t launch_col(int kind, int N, const ColGeom& g, cudaStream_t s);
 cudaError_t launch_x(int kind, int N1, const XGeom& g, cudaStream_t s, int* grid_out);
 int x_grid(int kind, int N1, long long nlines);
 int col_grid(int N, long long ncols);
+// mean tangent partials (mode 0: full 45, 1: compact neo-Hookean -> 45, 2: compact J2 -> 21)
+cudaError_t launch_mean_tangent(int mode, const XGeom& g, double* partials, int nblk, cudaStream_t s);

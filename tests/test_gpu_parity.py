@@ -73,8 +73,10 @@ def test_apply_K_cubic_polycrystal(dbf, n):
     assert rel(gpu_full(dbf, f, n[0]), ref) <= 1e-12
 
 
+@pytest.mark.parametrize("tangent", ["compact", "full"])
 @pytest.mark.parametrize("n", [(8, 8, 8), (16, 32, 8), (32, 32, 32)])
-def test_apply_K_finite_neohooke(dbf, n):
+def test_apply_K_finite_neohooke(dbf, n, tangent, monkeypatch):
+    monkeypatch.setenv("DBFFT_TANGENT", tangent)
     ph = two_phase(n, 2)
     mats = [dict(kind="neohooke", mu=1.0, kappa=2.5), dict(kind="neohooke", mu=10.0, kappa=25.0)]
     F = np.eye(3).reshape(3, 3, 1, 1, 1) + 0.1 * ms.random_field((3, 3, n[2], n[1], n[0]), 9)
