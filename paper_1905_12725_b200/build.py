@@ -34,7 +34,7 @@ def build(force=False, verbose=False):
         with open(os.path.join(objdir, src + ".log"), "w") as f:
             f.write(r.stdout + r.stderr)
         if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr[-4000:]}")
+            raise RuntimeError(f"nvcc failed for {src} (rc={r.returncode}):\n{r.stderr[-4000:]}")
         return obj
 
     with ThreadPoolExecutor(len(SOURCES)) as ex:

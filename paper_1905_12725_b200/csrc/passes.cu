@@ -184,8 +184,9 @@ __global__ void __launch_bounds__(256, 3) col_pass_kernel(ColGeom g) {
   constexpr int TPC = N / 8;        // threads per column
   constexpr int COLS = 256 / TPC;   // columns per CTA
   constexpr bool TWO = ColTwo<KIND>::value;
-  __shared__ cplx sbuf[N * COLS];
-  __shared__ cplx sacc[TWO ? N * COLS : 1];  // first-term results of two-term outputs
+  extern __shared__ cplx col_smem[];
+  cplx* sbuf = col_smem;                 // FFT exchange, N * COLS
+  cplx* sacc = col_smem + N * COLS;      // first-term results of two-term outputs (TWO only)
   const int t = threadIdx.x;
   const int c = t % COLS;
   const int gq = t / COLS;
@@ -749,23 +750,35 @@ int col_grid(int N, long long ncols) {
   return (int)((ncols + cols - 1) / cols);
 }
 
+template <int N, int KIND>
+static cudaError_t launch_col_k(const ColGeom& g, cudaStream_t s) {
+  constexpr int COLS = 256 / (N / 8);
+  constexpr size_t smem = sizeof(cplx) * N * COLS * (ColTwo<KIND>::value ? 2 : 1);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(col_pass_kernel<N, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  col_pass_kernel<N, KIND><<<col_grid(N, g.ncols), 256, smem, s>>>(g);
+  return cudaGetLastError();
+}
+
 template <int N>
 static cudaError_t launch_col_n(int kind, const ColGeom& g, cudaStream_t s) {
-  const int grid = col_grid(N, g.ncols);
   switch (kind) {
-    case COL_I1S: col_pass_kernel<N, COL_I1S><<<grid, 256, 0, s>>>(g); break;
-    case COL_I1F: col_pass_kernel<N, COL_I1F><<<grid, 256, 0, s>>>(g); break;
-    case COL_I2S: col_pass_kernel<N, COL_I2S><<<grid, 256, 0, s>>>(g); break;
-    case COL_I2F: col_pass_kernel<N, COL_I2F><<<grid, 256, 0, s>>>(g); break;
-    case COL_F2S: col_pass_kernel<N, COL_F2S><<<grid, 256, 0, s>>>(g); break;
-    case COL_F2F: col_pass_kernel<N, COL_F2F><<<grid, 256, 0, s>>>(g); break;
-    case COL_F3S: col_pass_kernel<N, COL_F3S><<<grid, 256, 0, s>>>(g); break;
-    case COL_F3F: col_pass_kernel<N, COL_F3F><<<grid, 256, 0, s>>>(g); break;
-    case COL_ZI3: col_pass_kernel<N, COL_ZI3><<<grid, 256, 0, s>>>(g); break;
-    case COL_YI3: col_pass_kernel<N, COL_YI3><<<grid, 256, 0, s>>>(g); break;
+    case COL_I1S: return launch_col_k<N, COL_I1S>(g, s);
+    case COL_I1F: return launch_col_k<N, COL_I1F>(g, s);
+    case COL_I2S: return launch_col_k<N, COL_I2S>(g, s);
+    case COL_I2F: return launch_col_k<N, COL_I2F>(g, s);
+    case COL_F2S: return launch_col_k<N, COL_F2S>(g, s);
+    case COL_F2F: return launch_col_k<N, COL_F2F>(g, s);
+    case COL_F3S: return launch_col_k<N, COL_F3S>(g, s);
+    case COL_F3F: return launch_col_k<N, COL_F3F>(g, s);
+    case COL_ZI3: return launch_col_k<N, COL_ZI3>(g, s);
+    case COL_YI3: return launch_col_k<N, COL_YI3>(g, s);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 cudaError_t launch_col(int kind, int N, const ColGeom& g, cudaStream_t s) {
