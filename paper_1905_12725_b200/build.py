@@ -21,15 +21,18 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale():
+def build(force=False, verbose=False, lib=None, defines=()):
+    """Compile csrc/*.cu for sm_100a into `lib` (default: the in-tree libdbfft.so)."""
+    global LIB
+    target = lib or LIB
+    if lib is None and not force and not _stale():
         return LIB
-    objdir = os.path.join(HERE, "..", "build", "obj")
+    objdir = os.path.join(HERE, "..", "build", "obj" + ("_" + "_".join(defines) if defines else ""))
     os.makedirs(objdir, exist_ok=True)
 
     def comp(src):
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-Xptxas", "-v", "-c", os.path.join(SRC, src), "-o", obj]
+        cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-Xptxas", "-v", "-c", os.path.join(SRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         with open(os.path.join(objdir, src + ".log"), "w") as f:
             f.write(r.stdout + r.stderr)
@@ -39,13 +42,13 @@ def build(force=False, verbose=False):
 
     with ThreadPoolExecutor(len(SOURCES)) as ex:
         objs = list(ex.map(comp, SOURCES))
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *objs]
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", target, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stderr[-4000:])
     if verbose:
-        print("built", LIB)
-    return LIB
+        print("built", target)
+    return target
 
 
 if __name__ == "__main__":

@@ -173,3 +173,143 @@ DBF_DEV double warp_max(double v) {
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
+
+// ---------------------------------------------------------------------------------------------
+// Sub-warp FFT (column passes): a length-N transform is owned by T = N/P threads of ONE warp
+// (P points each, a[s] <-> position g + s*T), so every exchange needs only __syncwarp().
+// Stages: radix-P (P = 16: DFT-16 as 4x4 in registers) while possible, then one radix-R stage.
+// ---------------------------------------------------------------------------------------------
+template <bool INV>
+DBF_DEV cplx w16(int e) {  // W16^e, e in [0, 16)
+  const double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173, h = 0.70710678118654752440;
+  double c, s;
+  switch (e & 15) {
+    case 0: c = 1; s = 0; break;
+    case 1: c = c1; s = s1; break;
+    case 2: c = h; s = h; break;
+    case 3: c = s1; s = c1; break;
+    case 4: c = 0; s = 1; break;
+    case 5: c = -s1; s = c1; break;
+    case 6: c = -h; s = h; break;
+    case 7: c = -c1; s = s1; break;
+    case 8: c = -1; s = 0; break;
+    case 9: c = -c1; s = -s1; break;
+    case 10: c = -h; s = -h; break;
+    case 11: c = -s1; s = -c1; break;
+    case 12: c = 0; s = -1; break;
+    case 13: c = s1; s = -c1; break;
+    case 14: c = h; s = -h; break;
+    default: c = c1; s = -s1; break;
+  }
+  return make_double2(c, INV ? s : -s);  // exp(-+ 2 pi i e / 16)
+}
+
+// x[n*st + off] for n = 0..15 -> X[k] in place (natural order), via 4 x 4
+template <bool INV, int ST>
+DBF_DEV void dft16s(cplx* x, int off) {
+  cplx y[16];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    cplx v0 = x[off + ST * q], v1 = x[off + ST * (q + 4)], v2 = x[off + ST * (q + 8)], v3 = x[off + ST * (q + 12)];
+    dft4<INV>(v0, v1, v2, v3);  // over n1: outputs k1 = 0..3
+    y[4 * q + 0] = v0;
+    y[4 * q + 1] = cmul(v1, w16<INV>(q));
+    y[4 * q + 2] = cmul(v2, w16<INV>(2 * q));
+    y[4 * q + 3] = cmul(v3, w16<INV>(3 * q));
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) {
+    cplx v0 = y[k1], v1 = y[4 + k1], v2 = y[8 + k1], v3 = y[12 + k1];
+    dft4<INV>(v0, v1, v2, v3);  // over q: outputs k2
+    x[off + ST * (k1)] = v0;
+    x[off + ST * (k1 + 4)] = v1;
+    x[off + ST * (k1 + 8)] = v2;
+    x[off + ST * (k1 + 12)] = v3;
+  }
+}
+
+template <int N, int P>
+struct SubPlan {
+  static constexpr int log2n = (N == 8) ? 3 : (N == 16) ? 4 : (N == 32) ? 5 : (N == 64) ? 6 : (N == 128) ? 7 : (N == 256) ? 8 : (N == 512) ? 9 : (N == 1024) ? 10 : -1;
+  static constexpr int log2p = (P == 16) ? 4 : 3;
+  static constexpr int nfull = log2n / log2p;
+  static constexpr int last = 1 << (log2n - log2p * nfull);
+  static constexpr int nstages = nfull + (last > 1 ? 1 : 0);
+};
+
+template <int N, int P, int R, bool INV>
+DBF_DEV void sub_stage(cplx (&a)[P], int g, int Ns, const cplx* __restrict__ tw) {
+  constexpr int T = N / P;
+  constexpr int M = P / R;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int b = g + m * T;
+    const int k = b % Ns;
+    if (Ns > 1) {
+      const int step = (N / (Ns * R)) * k;
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        cplx w = __ldg(tw + r * step);
+        if (INV) w.y = -w.y;
+        a[m + M * r] = cmul(a[m + M * r], w);
+      }
+    }
+    if (R == 16) dft16s<INV, 1>(a, 0);
+    else if (R == 8) {
+      cplx t8[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) t8[r] = a[m + M * r];
+      dft8<INV>(t8);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) a[m + M * r] = t8[r];
+    } else if (R == 4) dft4<INV>(a[m], a[m + M], a[m + 2 * M], a[m + 3 * M]);
+    else dft2<INV>(a[m], a[m + M]);
+  }
+}
+
+// All T threads of the group must call it; SYNC() orders the group's shared-memory exchange.
+template <int N, int P, bool INV, class IDX, class SYNC>
+DBF_DEV void fft_sub(cplx (&a)[P], cplx* sbuf, int g, const IDX& idx, const cplx* __restrict__ tw, const SYNC& sync) {
+  typedef SubPlan<N, P> PL;
+  constexpr int T = N / P;
+  int Ns = 1;
+#pragma unroll
+  for (int st = 0; st < PL::nstages; ++st) {
+    const bool is_last = (st == PL::nstages - 1);
+    const int R = (st < PL::nfull) ? P : PL::last;
+    if (st > 0) {
+#pragma unroll
+      for (int s = 0; s < P; ++s) a[s] = sbuf[idx(g + s * T)];
+    }
+    if (R == 16) sub_stage<N, P, (P >= 16 ? 16 : 2), INV>(a, g, Ns, tw);
+    else if (R == 8) sub_stage<N, P, (P >= 8 ? 8 : 2), INV>(a, g, Ns, tw);
+    else if (R == 4) sub_stage<N, P, 4, INV>(a, g, Ns, tw);
+    else sub_stage<N, P, 2, INV>(a, g, Ns, tw);
+    if (!is_last) {
+      sync();  // the group finished reading the buffer
+      const int M = P / R;
+#pragma unroll
+      for (int m = 0; m < P; ++m) {
+        if (m >= M) break;
+        const int b = g + m * T;
+        const int base = (b / Ns) * Ns * R + (b % Ns);
+        for (int r = 0; r < R; ++r) sbuf[idx(base + r * Ns)] = a[m + M * r];
+      }
+      sync();
+    }
+    Ns *= R;
+  }
+}
+
+// per-group buffer of N complex, XOR swizzle of the low 3 bits by bits 4..6: conflict-free
+// radix-16 scatter (positions 16 g + r) and gather (g + 16 s)
+struct IdxGrp {
+  int base;
+  DBF_DEV int operator()(int pos) const { return base + (pos ^ ((pos >> 4) & 7)); }
+};
+struct SyncWarp {
+  DBF_DEV void operator()() const { __syncwarp(); }
+};
+struct SyncCta {
+  DBF_DEV void operator()() const { __syncthreads(); }
+};

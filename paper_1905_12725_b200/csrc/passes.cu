@@ -12,6 +12,18 @@
 
 #include <algorithm>
 
+#ifndef DBF_X_MINB
+#define DBF_X_MINB 3
+#endif
+#ifndef DBF_X_P
+#define DBF_X_P 8      // pass_X FFT points per thread: 8 (radix-8, CTA exchange) or 16 (radix-16, warp-local)
+#endif
+#ifndef DBF_X_LRAW
+#define DBF_X_LRAW 192  // target threads per pass_X CTA (lines per CTA = DBF_X_LRAW / threads per line)
+#endif
+#ifndef DBF_COL_MINB
+#define DBF_COL_MINB 4
+#endif
 namespace {
 
 // ------------------------------------------------------------------------------------------------
@@ -31,38 +43,53 @@ struct ColAt {
   DBF_DEV cplx in(int f) const { return __ldg(g->in + in_idx(f)); }
 };
 
+// Each pass is a list of NT "terms".  Term j FFTs one pre-weighted combination of one or two
+// input fields (raw values loaded first, so the next term's loads can be issued before the
+// current FFT: software pipelining in registers) and adds post-weight x FFT into output o.
+struct TermInfo {
+  int o;       // output field
+  int first;   // first term of output o
+  int last;    // last term of output o (store)
+  int f0, f1;  // input fields (f1 < 0: single field)
+};
+
 template <int KIND>
 struct ColOp;
 
-// z inverse, small strain.  outer = ky, pos = kz.
+// z inverse, small strain.  outer = ky, pos = kz.  out {u_x, u_y, eps_zz, eps_xz, eps_yz}
 template <>
 struct ColOp<COL_I1S> {
   static constexpr bool INV = true;
-  static constexpr int NOUT = 5;
-  DBF_DEV static int nterms(int) { return 1; }
-  DBF_DEV static cplx load(const ColAt& a, int o, int) {
-    const double xx = __ldg(a.g->fq.xx + a.kx), xy = __ldg(a.g->fq.xy + a.outer), xz = __ldg(a.g->fq.xz + a.pos);
-    switch (o) {
-      case 0: return a.in(0);
-      case 1: return a.in(1);
-      case 2: return cimul(a.in(2), xz);                                               // eps_zz
-      case 3: { cplx u0 = a.in(0), u2 = a.in(2); return cimul(make_double2(xz * u0.x + xx * u2.x, xz * u0.y + xx * u2.y), 0.5); }  // eps_xz
-      default: { cplx u1 = a.in(1), u2 = a.in(2); return cimul(make_double2(xz * u1.x + xy * u2.x, xz * u1.y + xy * u2.y), 0.5); }  // eps_yz
+  static constexpr int NT = 5, MAXIN = 2;
+  DBF_DEV static TermInfo term(int j) {
+    switch (j) {
+      case 0: return {0, 1, 1, 0, -1};
+      case 1: return {1, 1, 1, 1, -1};
+      case 2: return {2, 1, 1, 2, -1};
+      case 3: return {3, 1, 1, 0, 2};
+      default: return {4, 1, 1, 1, 2};
     }
   }
-  DBF_DEV static cplx post(const ColAt&, int, int) { return make_double2(1.0, 0.0); }
+  DBF_DEV static cplx pre(const ColAt& a, int j, cplx r0, cplx r1) {
+    const double xz = __ldg(a.g->fq.xz + a.pos);
+    switch (j) {
+      case 0: case 1: return r0;
+      case 2: return cimul(r0, xz);  // eps_zz
+      case 3: { const double xx = __ldg(a.g->fq.xx + a.kx); return cimul(make_double2(xz * r0.x + xx * r1.x, xz * r0.y + xx * r1.y), 0.5); }
+      default: { const double xy = __ldg(a.g->fq.xy + a.outer); return cimul(make_double2(xz * r0.x + xy * r1.x, xz * r0.y + xy * r1.y), 0.5); }
+    }
+  }
+  DBF_DEV static cplx post(const ColAt&, int) { return make_double2(1.0, 0.0); }
 };
 
+// z inverse, finite strain: u_i, G_iz = i xi_z u_i
 template <>
 struct ColOp<COL_I1F> {
   static constexpr bool INV = true;
-  static constexpr int NOUT = 6;
-  DBF_DEV static int nterms(int) { return 1; }
-  DBF_DEV static cplx load(const ColAt& a, int o, int) {
-    if (o < 3) return a.in(o);
-    return cimul(a.in(o - 3), __ldg(a.g->fq.xz + a.pos));  // G_iz = i xi_z u_i
-  }
-  DBF_DEV static cplx post(const ColAt&, int, int) { return make_double2(1.0, 0.0); }
+  static constexpr int NT = 6, MAXIN = 1;
+  DBF_DEV static TermInfo term(int j) { return {j, 1, 1, j < 3 ? j : j - 3, -1}; }
+  DBF_DEV static cplx pre(const ColAt& a, int j, cplx r0, cplx) { return j < 3 ? r0 : cimul(r0, __ldg(a.g->fq.xz + a.pos)); }
+  DBF_DEV static cplx post(const ColAt&, int) { return make_double2(1.0, 0.0); }
 };
 
 // y inverse, small strain.  outer = z, pos = ky.  in: {u_x, u_y, eps_zz, eps_xz, eps_yz}
@@ -70,20 +97,27 @@ struct ColOp<COL_I1F> {
 template <>
 struct ColOp<COL_I2S> {
   static constexpr bool INV = true;
-  static constexpr int NOUT = 6;
-  DBF_DEV static int nterms(int) { return 1; }
-  DBF_DEV static cplx load(const ColAt& a, int o, int) {
-    const double xx = __ldg(a.g->fq.xx + a.kx), xy = __ldg(a.g->fq.xy + a.pos);
-    switch (o) {
-      case 0: return cimul(a.in(0), xx);
-      case 1: return cimul(a.in(1), xy);
-      case 2: return a.in(2);
-      case 3: return a.in(4);
-      case 4: return a.in(3);
-      default: { cplx u0 = a.in(0), u1 = a.in(1); return cimul(make_double2(xy * u0.x + xx * u1.x, xy * u0.y + xx * u1.y), 0.5); }
+  static constexpr int NT = 6, MAXIN = 2;
+  DBF_DEV static TermInfo term(int j) {
+    switch (j) {
+      case 0: return {0, 1, 1, 0, -1};
+      case 1: return {1, 1, 1, 1, -1};
+      case 2: return {2, 1, 1, 2, -1};
+      case 3: return {3, 1, 1, 4, -1};
+      case 4: return {4, 1, 1, 3, -1};
+      default: return {5, 1, 1, 0, 1};
     }
   }
-  DBF_DEV static cplx post(const ColAt&, int, int) { return make_double2(1.0, 0.0); }
+  DBF_DEV static cplx pre(const ColAt& a, int j, cplx r0, cplx r1) {
+    switch (j) {
+      case 0: return cimul(r0, __ldg(a.g->fq.xx + a.kx));
+      case 1: return cimul(r0, __ldg(a.g->fq.xy + a.pos));
+      case 5: { const double xx = __ldg(a.g->fq.xx + a.kx), xy = __ldg(a.g->fq.xy + a.pos);
+                return cimul(make_double2(xy * r0.x + xx * r1.x, xy * r0.y + xx * r1.y), 0.5); }
+      default: return r0;
+    }
+  }
+  DBF_DEV static cplx post(const ColAt&, int) { return make_double2(1.0, 0.0); }
 };
 
 // y inverse, finite strain.  in: {u_0,u_1,u_2, G_0z,G_1z,G_2z}; out o = 3i+j:
@@ -91,38 +125,36 @@ struct ColOp<COL_I2S> {
 template <>
 struct ColOp<COL_I2F> {
   static constexpr bool INV = true;
-  static constexpr int NOUT = 9;
-  DBF_DEV static int nterms(int) { return 1; }
-  DBF_DEV static cplx load(const ColAt& a, int o, int) {
-    const int i = o / 3, j = o % 3;
-    if (j == 0) return a.in(i);
-    if (j == 1) return cimul(a.in(i), __ldg(a.g->fq.xy + a.pos));
-    return a.in(3 + i);
+  static constexpr int NT = 9, MAXIN = 1;
+  DBF_DEV static TermInfo term(int j) {
+    const int i = j / 3, jj = j % 3;
+    return {j, 1, 1, jj == 2 ? 3 + i : i, -1};
   }
-  DBF_DEV static cplx post(const ColAt&, int, int) { return make_double2(1.0, 0.0); }
+  DBF_DEV static cplx pre(const ColAt& a, int j, cplx r0, cplx) { return (j % 3 == 1) ? cimul(r0, __ldg(a.g->fq.xy + a.pos)) : r0; }
+  DBF_DEV static cplx post(const ColAt&, int) { return make_double2(1.0, 0.0); }
 };
 
 template <>
 struct ColOp<COL_F2S> {
   static constexpr bool INV = false;
-  static constexpr int NOUT = 6;
-  DBF_DEV static int nterms(int) { return 1; }
-  DBF_DEV static cplx load(const ColAt& a, int o, int) { return a.in(o); }
-  DBF_DEV static cplx post(const ColAt&, int, int) { return make_double2(1.0, 0.0); }
+  static constexpr int NT = 6, MAXIN = 1;
+  DBF_DEV static TermInfo term(int j) { return {j, 1, 1, j, -1}; }
+  DBF_DEV static cplx pre(const ColAt&, int, cplx r0, cplx) { return r0; }
+  DBF_DEV static cplx post(const ColAt&, int) { return make_double2(1.0, 0.0); }
 };
 
 // y forward, finite strain.  in o=3i+j: {g_i (xi_x folded), P_iy, P_iz};  out: g_i (+ -i xi_y P_iy), P_iz
 template <>
 struct ColOp<COL_F2F> {
   static constexpr bool INV = false;
-  static constexpr int NOUT = 6;
-  DBF_DEV static int nterms(int o) { return o < 3 ? 2 : 1; }
-  DBF_DEV static cplx load(const ColAt& a, int o, int t) {
-    if (o < 3) return a.in(3 * o + t);
-    return a.in(3 * (o - 3) + 2);
+  static constexpr int NT = 9, MAXIN = 1;
+  DBF_DEV static TermInfo term(int j) {
+    if (j < 6) return {j / 2, (j & 1) == 0, (j & 1) == 1, 3 * (j / 2) + (j & 1), -1};
+    return {j - 3, 1, 1, 3 * (j - 6) + 2, -1};
   }
-  DBF_DEV static cplx post(const ColAt& a, int o, int t) {
-    if (o < 3 && t == 1) return make_double2(0.0, -__ldg(a.g->fq.xy + a.pos));
+  DBF_DEV static cplx pre(const ColAt&, int, cplx r0, cplx) { return r0; }
+  DBF_DEV static cplx post(const ColAt& a, int j) {
+    if (j < 6 && (j & 1)) return make_double2(0.0, -__ldg(a.g->fq.xy + a.pos));
     return make_double2(1.0, 0.0);
   }
 };
@@ -132,20 +164,22 @@ struct ColOp<COL_F2F> {
 template <>
 struct ColOp<COL_F3S> {
   static constexpr bool INV = false;
-  static constexpr int NOUT = 3;
-  DBF_DEV static int nterms(int) { return 2; }
-  DBF_DEV static cplx load(const ColAt& a, int o, int t) {
-    const double xx = __ldg(a.g->fq.xx + a.kx), xy = __ldg(a.g->fq.xy + a.outer);
-    // (first, second) in-plane components and the z component of row o
-    const int fa = (o == 0) ? 0 : (o == 1) ? 5 : 4;   // s_ox
-    const int fb = (o == 0) ? 5 : (o == 1) ? 1 : 3;   // s_oy
-    const int fz = (o == 0) ? 4 : (o == 1) ? 3 : 2;   // s_oz
-    if (t == 1) return a.in(fz);
-    cplx sa = a.in(fa), sb = a.in(fb);
-    return cimul(make_double2(xx * sa.x + xy * sb.x, xx * sa.y + xy * sb.y), -1.0);
+  static constexpr int NT = 6, MAXIN = 2;
+  DBF_DEV static TermInfo term(int j) {
+    const int o = j / 2;
+    const int fa = (o == 0) ? 0 : (o == 1) ? 5 : 4;  // s_ox
+    const int fb = (o == 0) ? 5 : (o == 1) ? 1 : 3;  // s_oy
+    const int fz = (o == 0) ? 4 : (o == 1) ? 3 : 2;  // s_oz
+    if ((j & 1) == 0) return {o, 1, 0, fa, fb};
+    return {o, 0, 1, fz, -1};
   }
-  DBF_DEV static cplx post(const ColAt& a, int, int t) {
-    if (t == 1) return make_double2(0.0, -__ldg(a.g->fq.xz + a.pos));
+  DBF_DEV static cplx pre(const ColAt& a, int j, cplx r0, cplx r1) {
+    if (j & 1) return r0;
+    const double xx = __ldg(a.g->fq.xx + a.kx), xy = __ldg(a.g->fq.xy + a.outer);
+    return cimul(make_double2(xx * r0.x + xy * r1.x, xx * r0.y + xy * r1.y), -1.0);
+  }
+  DBF_DEV static cplx post(const ColAt& a, int j) {
+    if (j & 1) return make_double2(0.0, -__ldg(a.g->fq.xz + a.pos));
     return make_double2(1.0, 0.0);
   }
 };
@@ -153,11 +187,15 @@ struct ColOp<COL_F3S> {
 template <>
 struct ColOp<COL_F3F> {
   static constexpr bool INV = false;
-  static constexpr int NOUT = 3;
-  DBF_DEV static int nterms(int) { return 2; }
-  DBF_DEV static cplx load(const ColAt& a, int o, int t) { return a.in(t == 0 ? o : 3 + o); }
-  DBF_DEV static cplx post(const ColAt& a, int, int t) {
-    if (t == 1) return make_double2(0.0, -__ldg(a.g->fq.xz + a.pos));
+  static constexpr int NT = 6, MAXIN = 1;
+  DBF_DEV static TermInfo term(int j) {
+    const int o = j / 2;
+    if ((j & 1) == 0) return {o, 1, 0, o, -1};
+    return {o, 0, 1, 3 + o, -1};
+  }
+  DBF_DEV static cplx pre(const ColAt&, int, cplx r0, cplx) { return r0; }
+  DBF_DEV static cplx post(const ColAt& a, int j) {
+    if (j & 1) return make_double2(0.0, -__ldg(a.g->fq.xz + a.pos));
     return make_double2(1.0, 0.0);
   }
 };
@@ -165,10 +203,10 @@ struct ColOp<COL_F3F> {
 template <>
 struct ColOp<COL_ZI3> {
   static constexpr bool INV = true;
-  static constexpr int NOUT = 3;
-  DBF_DEV static int nterms(int) { return 1; }
-  DBF_DEV static cplx load(const ColAt& a, int o, int) { return a.in(o); }
-  DBF_DEV static cplx post(const ColAt&, int, int) { return make_double2(1.0, 0.0); }
+  static constexpr int NT = 3, MAXIN = 1;
+  DBF_DEV static TermInfo term(int j) { return {j, 1, 1, j, -1}; }
+  DBF_DEV static cplx pre(const ColAt&, int, cplx r0, cplx) { return r0; }
+  DBF_DEV static cplx post(const ColAt&, int) { return make_double2(1.0, 0.0); }
 };
 template <>
 struct ColOp<COL_YI3> : ColOp<COL_ZI3> {};
@@ -178,12 +216,30 @@ struct ColTwo {  // does any output of this pass sum two transformed terms?
   static constexpr bool value = (KIND == COL_F2F || KIND == COL_F3S || KIND == COL_F3F);
 };
 
+// Column-pass CTA geometry: 256 threads; a column's length-N FFT is done by N/8 threads
+// (8 points each); columns are kx-contiguous so each warp load is 128-byte row segments.
+template <int N>
+struct ColCfg {
+  static constexpr int THREADS = 256;
+  static constexpr int TPC = N / 8;
+  static constexpr int COLS = 256 / TPC;
+};
+
+// single-term passes pipeline the next term's loads in registers (2 CTAs/SM); two-term
+// passes keep the first term in shared memory and run without prefetch (3 CTAs/SM)
+template <int KIND>
+struct ColPref {
+  static constexpr bool value = !ColTwo<KIND>::value && ColOp<KIND>::MAXIN == 1;
+  static constexpr int MINB = ColTwo<KIND>::value ? 3 : 2;
+};
+
 template <int N, int KIND>
-__global__ void __launch_bounds__(256, 3) col_pass_kernel(ColGeom g) {
+__global__ void __launch_bounds__(256, ColPref<KIND>::MINB) col_pass_kernel(ColGeom g) {
   typedef ColOp<KIND> Op;
-  constexpr int TPC = N / 8;        // threads per column
-  constexpr int COLS = 256 / TPC;   // columns per CTA
+  constexpr int TPC = N / 8;
+  constexpr int COLS = 256 / TPC;
   constexpr bool TWO = ColTwo<KIND>::value;
+  constexpr bool PREF = ColPref<KIND>::value;
   extern __shared__ cplx col_smem[];
   cplx* sbuf = col_smem;                 // FFT exchange, N * COLS
   cplx* sacc = col_smem + N * COLS;      // first-term results of two-term outputs (TWO only)
@@ -199,33 +255,52 @@ __global__ void __launch_bounds__(256, 3) col_pass_kernel(ColGeom g) {
   const double wdot = (at.kx == 0 || 2 * at.kx == g.n1) ? 1.0 : 2.0;
   double dot = 0.0;
   IdxCols<COLS> idx{c};
-#pragma unroll 1
-  for (int o = 0; o < Op::NOUT; ++o) {
-    const int nt = Op::nterms(o);
-#pragma unroll 1
-    for (int term = 0; term < nt; ++term) {
-      cplx a[8];
+  cplx r0[PREF ? 8 : 1];
+  if (PREF) {
+    const TermInfo ti = Op::term(0);
 #pragma unroll
-      for (int s = 0; s < 8; ++s) {
-        at.pos = gq + s * (N / 8);
-        a[s] = valid ? Op::load(at, o, term) : make_double2(0.0, 0.0);
+    for (int s = 0; s < 8; ++s) {
+      at.pos = gq + s * (N / 8);
+      r0[PREF ? s : 0] = valid ? at.in(ti.f0) : make_double2(0.0, 0.0);
+    }
+  }
+#pragma unroll 1
+  for (int j = 0; j < Op::NT; ++j) {
+    const TermInfo ti = Op::term(j);
+    cplx a[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      at.pos = gq + s * (N / 8);
+      if (PREF) {
+        a[s] = Op::pre(at, j, r0[PREF ? s : 0], r0[PREF ? s : 0]);
+      } else {
+        const cplx v0 = valid ? at.in(ti.f0) : make_double2(0.0, 0.0);
+        const cplx v1 = (valid && ti.f1 >= 0) ? at.in(ti.f1) : make_double2(0.0, 0.0);
+        a[s] = Op::pre(at, j, v0, v1);
       }
-      fft_cta<N, Op::INV>(a, sbuf, gq, idx, g.tw);
-      const bool last = (term + 1 == nt);
+    }
+    if (PREF && j + 1 < Op::NT) {  // issue the next term's loads; they fly during this FFT
+      const TermInfo tn = Op::term(j + 1);
 #pragma unroll
       for (int s = 0; s < 8; ++s) {
         at.pos = gq + s * (N / 8);
-        cplx v = cmul(Op::post(at, o, term), a[s]);
-        if (TWO && term > 0) v = cadd(v, sacc[idx(at.pos)]);
-        if (!last) {
-          if (TWO) sacc[idx(at.pos)] = v;  // own positions only: no barrier needed
-        } else if (valid) {
-          const long long oi = at.out_idx(o);
-          g.out[oi] = v;
-          if (g.dotp) {
-            cplx p = __ldg(g.dotp + oi);
-            dot += wdot * (p.x * v.x + p.y * v.y);
-          }
+        r0[PREF ? s : 0] = valid ? at.in(tn.f0) : make_double2(0.0, 0.0);
+      }
+    }
+    fft_cta<N, Op::INV>(a, sbuf, gq, idx, g.tw);
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      at.pos = gq + s * (N / 8);
+      cplx v = cmul(Op::post(at, j), a[s]);
+      if (TWO && !ti.first) v = cadd(v, sacc[idx(at.pos)]);
+      if (!ti.last) {
+        if (TWO) sacc[idx(at.pos)] = v;  // own positions only: no barrier needed
+      } else if (valid) {
+        const long long oi = at.out_idx(ti.o);
+        g.out[oi] = v;
+        if (g.dotp) {
+          cplx p = __ldg(g.dotp + oi);
+          dot += wdot * (p.x * v.x + p.y * v.y);
         }
       }
     }
@@ -415,19 +490,20 @@ DBF_DEV void j2_moduli(const double* prm, double* kappa, double* mu) {
   *kappa = lam + 2.0 * (*mu) / 3.0;
 }
 
+// Per-voxel material data of the apply kinds come either from global memory (tp = tan + v,
+// ts = nvox) or from the CTA's shared-memory stage filled by bulk async copies (ts = N1).
 template <int KIND>
-DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* red) {
+DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* red, const double* tp, long long ts, int ph) {
   if (KIND == X_K_SMALL_PHASE || KIND == X_RHS_SMALL_PHASE || KIND == X_K_J2) {
     double e6[6];
 #pragma unroll
     for (int I = 0; I < 6; ++I)
       e6[I] = (KIND == X_RHS_SMALL_PHASE ? 0.0 : G[I]) + (g.e ? __ldg(g.e + c_row9_of_voigt[I]) : 0.0);
-    const int ph = __ldg(g.phase + v);
     double s[6];
     if (KIND == X_K_J2) {
       double tc[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) tc[k] = ld_stream(g.tan + (long long)k * g.nvox + v);
+      for (int k = 0; k < 8; ++k) tc[k] = tp[k * ts];
       double kappa, mu;
       j2_moduli(g.ptable + 36 * ph, &kappa, &mu);
       j2_apply(tc, kappa, mu, e6, s);
@@ -443,7 +519,7 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
   } else if (KIND == X_K_FIN_TAN) {
     double e9[9], K[45];
 #pragma unroll
-    for (int k = 0; k < 45; ++k) K[k] = ld_stream(g.tan + (long long)k * g.nvox + v);
+    for (int k = 0; k < 45; ++k) K[k] = ld_stream(tp + k * ts);
 #pragma unroll
     for (int a = 0; a < 9; ++a) e9[a] = G[a] + (g.e ? __ldg(g.e + a) : 0.0);
 #pragma unroll
@@ -457,9 +533,8 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
   } else if (KIND == X_K_FIN_NH) {
     double Fi[9], e9[9];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) Fi[k] = ld_stream(g.tan + (long long)k * g.nvox + v);
-    const double c1 = ld_stream(g.tan + 9 * g.nvox + v);
-    const int ph = __ldg(g.phase + v);
+    for (int k = 0; k < 9; ++k) Fi[k] = tp[k * ts];
+    const double c1 = tp[9 * ts];
     const double mu = __ldg(g.ptable + 36 * ph), lam = __ldg(g.ptable + 36 * ph + 1) - 2.0 * mu / 3.0;
 #pragma unroll
     for (int a = 0; a < 9; ++a) e9[a] = G[a] + (g.e ? __ldg(g.e + a) : 0.0);
@@ -528,60 +603,175 @@ struct IdxSwz {
   DBF_DEV int operator()(int pos) const { return base + (pos ^ ((pos >> 3) & 7)); }
 };
 
+// pass_X FFT of one field pair: radix-8 with CTA-wide exchange barriers (P = 8) or radix-16
+// with warp-local exchanges (P = 16, the pair's threads share a warp)
+template <int P>
+DBF_DEV int x_idx(int base, int pos) {
+  return P == 16 ? IdxGrp{base}(pos) : IdxSwz{base}(pos);
+}
+template <int P>
+DBF_DEV void x_jobsync() {
+  if (P == 16) __syncwarp();
+  else __syncthreads();
+}
+template <int N1, int P, bool INV>
+DBF_DEV void x_fft(cplx (&a)[P], cplx* cx, int gq, int base, const cplx* __restrict__ tw) {
+  if constexpr (P == 16) {
+    fft_sub<N1, 16, INV>(a, cx, gq, IdxGrp{base}, tw, SyncWarp{});
+  } else {
+    fft_cta<N1, INV>(a, cx, gq, IdxSwz{base}, tw);
+  }
+}
+
+// Which apply kinds stream their inputs through the shared-memory stage (bulk async copies)
+template <int KIND>
+struct XStage {
+  static constexpr bool IN = (KIND == X_K_SMALL_PHASE || KIND == X_K_J2 || KIND == X_K_FIN_TAN || KIND == X_K_FIN_NH);
+  static constexpr int NTAN = (KIND == X_K_J2) ? 8 : (KIND == X_K_FIN_NH) ? 10 : 0;  // staged per-voxel doubles
+  static constexpr bool PH = (KIND == X_K_SMALL_PHASE || KIND == X_K_J2 || KIND == X_K_FIN_NH);
+};
+
 template <int N1, int KIND>
 struct XCfg {
   typedef XTraits<KIND> T;
+  typedef XStage<KIND> S;
   static constexpr int C = (T::CIN > T::COUT) ? T::CIN : T::COUT;
   static constexpr int CS = (C + 1) & ~1;          // real slots per line (even)
-  static constexpr int TPJ = N1 / 8;
+  static constexpr int PX = (N1 >= 16) ? DBF_X_P : 8;   // FFT points per thread
+  static constexpr int TPJ = N1 / PX;              // threads per pair FFT (divides 32: warp-local)
   static constexpr int NP = CS / 2;
   static constexpr int PERLINE = TPJ * NP;
-  static constexpr int LRAW = 192 / PERLINE;
+  static constexpr int LRAW = DBF_X_LRAW / PERLINE;
   static constexpr int LPAR = LRAW >= 64 ? 64 : LRAW >= 32 ? 32 : LRAW >= 16 ? 16 : LRAW >= 8 ? 8 : LRAW >= 4 ? 4 : LRAW >= 2 ? 2 : 1;
   static constexpr int THREADS = LPAR * PERLINE;
-  static constexpr size_t SMEM = sizeof(double) * LPAR * CS * N1;
-  static constexpr int MINB = (THREADS <= 192) ? 3 : 2;
+  static constexpr int N1H = N1 / 2 + 1;
+  static constexpr size_t SLOTS = sizeof(double) * LPAR * CS * N1;
+  static constexpr size_t ST_IN = S::IN ? sizeof(cplx) * LPAR * T::CIN * N1H : 0;
+  static constexpr size_t ST_TAN = sizeof(double) * LPAR * S::NTAN * N1;
+  static constexpr size_t ST_PH = S::PH ? ((sizeof(uint16_t) * LPAR * N1 + 15) & ~size_t(15)) : 0;
+  static constexpr size_t SMEM = SLOTS + ST_IN + ST_TAN + ST_PH + 16;  // + 2 mbarriers
+  static constexpr int MINB = (THREADS <= 192) ? DBF_X_MINB : 2;
 };
+
+// ---- bulk async copy (TMA engine) + mbarrier helpers ------------------------------------------
+DBF_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+DBF_DEV void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+DBF_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+DBF_DEV bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+               : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+DBF_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try(bar, parity)) {
+  }
+}
+DBF_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+DBF_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// issue the stage copies of line group `grp` (one elected thread)
+template <int N1, int KIND>
+DBF_DEV void x_issue_in(const XGeom& g, long long grp, cplx* st_in, uint64_t* bar) {
+  typedef XCfg<N1, KIND> CF;
+  constexpr int CIN = XTraits<KIND>::CIN;
+  long long l0 = grp * CF::LPAR;
+  const int nl = (int)min((long long)CF::LPAR, g.nlines - l0);
+  const uint32_t row = sizeof(cplx) * CF::N1H;
+  mbar_expect_tx(bar, row * CIN * nl);
+  for (int l = 0; l < nl; ++l)
+    for (int f = 0; f < CIN; ++f) bulk_g2s(st_in + (l * CIN + f) * CF::N1H, g.in + f * g.fs_in + (l0 + l) * g.n1h, row, bar);
+}
+template <int N1, int KIND>
+DBF_DEV void x_issue_tan(const XGeom& g, long long grp, double* st_tan, uint16_t* st_ph, uint64_t* bar) {
+  typedef XCfg<N1, KIND> CF;
+  typedef XStage<KIND> S;
+  const long long l0 = grp * CF::LPAR;
+  const int nl = (int)min((long long)CF::LPAR, g.nlines - l0);
+  const long long v0 = l0 * N1;
+  const uint32_t trow = sizeof(double) * N1 * nl;  // LPAR lines are contiguous voxels
+  const uint32_t prow = sizeof(uint16_t) * N1 * nl;
+  const uint32_t pbytes = S::PH ? ((prow + 15) & ~15u) : 0;
+  mbar_expect_tx(bar, trow * S::NTAN + pbytes);
+  for (int k = 0; k < S::NTAN; ++k) bulk_g2s(st_tan + k * (CF::LPAR * N1), g.tan + (long long)k * g.nvox + v0, trow, bar);
+  if (S::PH) bulk_g2s(st_ph, g.phase + v0, pbytes, bar);
+}
 
 // X pass.  Persistent: each CTA loops over groups of LPAR lines.  Per line the C fields are
 // C2R'd in pairs (z = a + i b), the per-voxel operation runs on the real fields in shared
 // memory, and results are R2C'd in pairs and untangled:
 //   A_k = (Z_k + conj Z_{N-k})/2,  B_k = (Z_k - conj Z_{N-k})/(2i).
+// Apply kinds stream group i+1's spectra and per-voxel data into a shared-memory stage with
+// bulk async copies (cp.async.bulk -> TMA engine, mbarrier completion) while group i computes.
 template <int N1, int KIND>
 __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB) x_pass_kernel(XGeom g, int nf_real) {
   typedef XCfg<N1, KIND> CF;
   typedef XTraits<KIND> T;
-  constexpr int C = CF::C, CS = CF::CS, TPJ = CF::TPJ, NP = CF::NP, LPAR = CF::LPAR;
-  extern __shared__ double real[];
+  typedef XStage<KIND> S;
+  constexpr int C = CF::C, CS = CF::CS, TPJ = CF::TPJ, NP = CF::NP, LPAR = CF::LPAR, PX = CF::PX;
+  extern __shared__ __align__(16) double real[];
   cplx* cx = reinterpret_cast<cplx*>(real);
+  unsigned char* sb = reinterpret_cast<unsigned char*>(real);
+  cplx* st_in = reinterpret_cast<cplx*>(sb + CF::SLOTS);
+  double* st_tan = reinterpret_cast<double*>(sb + CF::SLOTS + CF::ST_IN);
+  uint16_t* st_ph = reinterpret_cast<uint16_t*>(sb + CF::SLOTS + CF::ST_IN + CF::ST_TAN);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sb + CF::SLOTS + CF::ST_IN + CF::ST_TAN + CF::ST_PH);
   const int t = threadIdx.x;
   const int job = t / TPJ, gq = t % TPJ;
   const int l = job / NP, p = job % NP;
   const int fa = 2 * p, fb = 2 * p + 1;
-  IdxSwz idx{(l * CS + fa) * (N1 / 2)};  // complex view of slots fa, fb of line l
+  const int jbase = (l * CS + fa) * (N1 / 2);  // complex view of slots fa, fb of line l (job buffer)
   const int cin = (KIND == X_REAL_OUT) ? nf_real : T::CIN;
   const bool do_in = (T::CIN > 0) && (cin > 0) && ((KIND != X_CONST_FIN && KIND != X_CONST_J2) || g.has_in);
   const long long ngroups = (g.nlines + LPAR - 1) / LPAR;
   double red[T::NRED > 0 ? T::NRED : 1];
 #pragma unroll
   for (int r = 0; r < (T::NRED > 0 ? T::NRED : 1); ++r) red[r] = 0.0;
+  constexpr bool STAGE_TAN = (S::NTAN > 0 || S::PH);
+  if (S::IN) {
+    if (t == 0) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (t == 0 && (long long)blockIdx.x < ngroups) {
+      x_issue_in<N1, KIND>(g, blockIdx.x, st_in, &bars[0]);
+      if (STAGE_TAN) x_issue_tan<N1, KIND>(g, blockIdx.x, st_tan, st_ph, &bars[1]);
+    }
+  }
+  uint32_t it = 0;
 
-  for (long long grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+  for (long long grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
     const long long line = grp * LPAR + l;
     const bool lvalid = line < g.nlines;
+    const long long nxt = grp + gridDim.x;
     // ------------------------------------------------------------ inverse (C2R) of pairs
     if (do_in) {
-      cplx a[8];
+      if (S::IN) mbar_wait(&bars[0], it & 1);
+      cplx a[PX];
 #pragma unroll
-      for (int s = 0; s < 8; ++s) {
+      for (int s = 0; s < PX; ++s) {
         const int k = gq + s * TPJ;
         const bool lo = (2 * k <= N1);
         const int kk = lo ? k : N1 - k;
         cplx A = make_double2(0, 0), B = make_double2(0, 0);
         if (lvalid && fa < cin) {
-          const long long base = line * g.n1h + kk;
-          A = __ldg(g.in + fa * g.fs_in + base);
-          if (fb < cin) B = __ldg(g.in + fb * g.fs_in + base);
+          if (S::IN) {
+            A = st_in[(l * T::CIN + fa) * CF::N1H + kk];
+            if (fb < cin) B = st_in[(l * T::CIN + fb) * CF::N1H + kk];
+          } else {
+            const long long base = line * g.n1h + kk;
+            A = __ldg(g.in + fa * g.fs_in + base);
+            if (fb < cin) B = __ldg(g.in + fb * g.fs_in + base);
+          }
           if (T::FIN) {  // G_ix = i xi_x u_i for the j = 0 slots (deferred gradient)
             const double xx = __ldg(g.xix + kk);
             if (fa % 3 == 0) A = cimul(A, xx);
@@ -592,10 +782,17 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
         // Y_k = A_k + i B_k (k <= N/2);  conj(A_{N-k}) + i conj(B_{N-k}) otherwise
         a[s] = lo ? make_double2(A.x - B.y, A.y + B.x) : make_double2(A.x + B.y, B.x - A.y);
       }
-      fft_cta<N1, true>(a, cx, gq, idx, g.tw);
-      __syncthreads();  // exchange reads done before the slots are overwritten with reals
+      if (S::IN) {
+        __syncthreads();  // everyone has read the input stage
+        if (t == 0 && nxt < ngroups) {
+          fence_proxy_async();
+          x_issue_in<N1, KIND>(g, nxt, st_in, &bars[0]);
+        }
+      }
+      x_fft<N1, PX, true>(a, cx, gq, jbase, g.tw);
+      x_jobsync<PX>();  // the job's exchange reads are done before its slots become reals
 #pragma unroll
-      for (int s = 0; s < 8; ++s) {
+      for (int s = 0; s < PX; ++s) {
         const int m = gq + s * TPJ;
         real[(l * CS + fa) * N1 + m] = a[s].x;
         real[(l * CS + fb) * N1 + m] = a[s].y;
@@ -615,6 +812,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
     }
 
     // ------------------------------------------------------------ per-voxel operation
+    if (S::IN && STAGE_TAN) mbar_wait(&bars[1], it & 1);
     for (int vv = t; vv < LPAR * N1; vv += CF::THREADS) {
       const int l2 = vv / N1, x = vv % N1;
       const long long ln = grp * LPAR + l2;
@@ -622,35 +820,52 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
       double G[C], P[C];
 #pragma unroll
       for (int f = 0; f < C; ++f) G[f] = (f < T::CIN && do_in) ? real[(l2 * CS + f) * N1 + x] : 0.0;
-      x_voxel<KIND>(g, ln * N1 + x, G, P, red);
+      const long long v = ln * N1 + x;
+      const double* tp;
+      long long ts;
+      int ph;
+      if (S::IN && STAGE_TAN) {
+        tp = st_tan + vv;
+        ts = LPAR * N1;
+        ph = S::PH ? (int)st_ph[vv] : 0;
+      } else {
+        tp = g.tan ? g.tan + v : nullptr;
+        ts = g.nvox;
+        ph = (KIND == X_K_FIN_TAN || KIND == X_REAL_OUT) ? 0 : (int)__ldg(g.phase + v);
+      }
+      x_voxel<KIND>(g, v, G, P, red, tp, ts, ph);
 #pragma unroll
       for (int f = 0; f < T::COUT; ++f) real[(l2 * CS + f) * N1 + x] = P[f];
     }
     __syncthreads();
+    if (S::IN && STAGE_TAN && t == 0 && nxt < ngroups) {
+      fence_proxy_async();
+      x_issue_tan<N1, KIND>(g, nxt, st_tan, st_ph, &bars[1]);
+    }
 
     // ------------------------------------------------------------ forward (R2C) of pairs
     {
       constexpr int COUT = T::COUT;
-      cplx a[8];
+      cplx a[PX];
 #pragma unroll
-      for (int s = 0; s < 8; ++s) {
+      for (int s = 0; s < PX; ++s) {
         const int m = gq + s * TPJ;
         const double ra = (fa < COUT) ? real[(l * CS + fa) * N1 + m] : 0.0;
         const double rb = (fb < COUT) ? real[(l * CS + fb) * N1 + m] : 0.0;
         a[s] = make_double2(ra, rb);
       }
-      fft_cta<N1, false>(a, cx, gq, idx, g.tw);
-      __syncthreads();
+      x_fft<N1, PX, false>(a, cx, gq, jbase, g.tw);
+      x_jobsync<PX>();
 #pragma unroll
-      for (int s = 0; s < 8; ++s) cx[idx(gq + s * TPJ)] = a[s];
-      __syncthreads();
+      for (int s = 0; s < PX; ++s) cx[x_idx<PX>(jbase, gq + s * TPJ)] = a[s];
+      x_jobsync<PX>();
       if (lvalid && fa < COUT) {
 #pragma unroll
-        for (int s = 0; s < 8; ++s) {
+        for (int s = 0; s < PX; ++s) {
           const int k = gq + s * TPJ;
           if (2 * k > N1) continue;
           const cplx Z = a[s];
-          const cplx Zn = cx[idx((N1 - k) & (N1 - 1))];
+          const cplx Zn = cx[x_idx<PX>(jbase, (N1 - k) & (N1 - 1))];
           cplx A = make_double2(0.5 * (Z.x + Zn.x), 0.5 * (Z.y - Zn.y));
           cplx B = make_double2(0.5 * (Z.y + Zn.y), -0.5 * (Z.x - Zn.x));
           A = cscale(A, g.inv_n);
@@ -745,14 +960,26 @@ __global__ void __launch_bounds__(256) k_mean_tangent(XGeom g, double* partials)
 // ------------------------------------------------------------------------------------------------
 // host launchers
 // ------------------------------------------------------------------------------------------------
+template <int N>
+static int col_cols() { return ColCfg<N>::COLS; }
+
 int col_grid(int N, long long ncols) {
-  const int cols = 256 / (N / 8);
+  int cols;
+  switch (N) {
+    case 8: cols = col_cols<8>(); break;
+    case 16: cols = col_cols<16>(); break;
+    case 32: cols = col_cols<32>(); break;
+    case 64: cols = col_cols<64>(); break;
+    case 128: cols = col_cols<128>(); break;
+    case 256: cols = col_cols<256>(); break;
+    default: cols = col_cols<512>(); break;
+  }
   return (int)((ncols + cols - 1) / cols);
 }
 
 template <int N, int KIND>
 static cudaError_t launch_col_k(const ColGeom& g, cudaStream_t s) {
-  constexpr int COLS = 256 / (N / 8);
+  constexpr int COLS = ColCfg<N>::COLS;
   constexpr size_t smem = sizeof(cplx) * N * COLS * (ColTwo<KIND>::value ? 2 : 1);
   static bool attr = false;
   if (!attr) {
@@ -760,7 +987,7 @@ static cudaError_t launch_col_k(const ColGeom& g, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  col_pass_kernel<N, KIND><<<col_grid(N, g.ncols), 256, smem, s>>>(g);
+  col_pass_kernel<N, KIND><<<col_grid(N, g.ncols), ColCfg<N>::THREADS, smem, s>>>(g);
   return cudaGetLastError();
 }
 

@@ -54,11 +54,13 @@ class DBFFTError(RuntimeError):
         self.status = status
 
 
-def load_library(path=LIB_PATH):
-    """Load libdbfft.so (raises if it was not built: there is no fallback path)."""
+def load_library(path=None):
+    """Load libdbfft.so (raises if it was not built: there is no fallback path).
+    DBFFT_LIB overrides the path (used to A/B kernel variants built by build.py)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("DBFFT_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise ImportError(f"{path} missing: run `python -m paper_1905_12725_b200.build` (CUDA extension required)")
     lib = ctypes.CDLL(path)

@@ -6,17 +6,24 @@ from collections import defaultdict
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
+kfilter = sys.argv[3] if len(sys.argv) > 3 else None
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
                      capture_output=True, text=True).stdout
 lines = out.splitlines()
 agg = defaultdict(lambda: [0, 0, ""])
 cur_file = None
+cur_fn = None
 hdr = None
 for row in csv.reader(lines):
     if not row:
         continue
     if row[0] == "File Path":
         cur_file = row[1].split("/")[-1]
+        continue
+    if row[0] == "Function Name":
+        cur_fn = row[1]
+        continue
+    if kfilter and kfilter not in (cur_fn or ""):
         continue
     if row[0] == "Line No":
         hdr = row
