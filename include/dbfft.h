@@ -30,7 +30,15 @@
  *  - Streams: all device work of a ctx is issued on env->cuda_stream (a cudaStream_t, e.g.
  *    torch.cuda.current_stream().cuda_stream) or on a ctx-owned stream if NULL.  Calls marked
  *    (async) return before the device work completes; the others synchronise that stream.
- *  - Distribution: env->world == 1 in this version (slab decomposition reserved).
+ *  - Distribution: with env->world = P > 1 (a power of two dividing n2 and n3)
+ *    real space is split in z-slabs (rank r owns z in [r n3/P, (r+1) n3/P)) and spectral space
+ *    in ky-slabs (ky in [r n2/P, (r+1) n2/P)).  Every call is collective over the P ranks.
+ *    NCCL mode (env->loopback = 0): one process per GPU; rank 0 calls dbfft_nccl_unique_id and
+ *    broadcasts the 128-byte id (e.g. via torch.distributed); each rank passes and receives
+ *    only its own slab (spectral vectors [3][n2/P][kz][kx]; real fields [c][n3/P][y][x]).
+ *    Loopback mode (env->loopback = 1): all P virtual ranks live in this process on one device
+ *    and exchange through device copies (tests the distributed data path on one GPU); API
+ *    arrays are then the global ones.
  */
 #ifndef DBFFT_H
 #define DBFFT_H
@@ -45,11 +53,12 @@ typedef struct dbfft_ctx_s* dbfft_ctx;
 
 typedef enum {
   DBFFT_OK = 0,
-  DBFFT_E_INVALID_GRID = 1,  /* n_a not a power of two in [8,512], or L_a <= 0            */
+  DBFFT_E_INVALID_GRID = 1,  /* n_a not a power of two in [8,512], L_a <= 0, or world not a power
+                                of two dividing n2 and n3                                 */
   DBFFT_E_INVALID_ARG = 2,   /* null pointer, unknown kind, phase id >= n_phases, bad parameters */
   DBFFT_E_STATE = 3,         /* call-order violation, e.g. apply_K before set_phases             */
   DBFFT_E_CUDA = 4,          /* CUDA error (message in dbfft_last_error)                          */
-  DBFFT_E_NCCL = 5,          /* reserved (multi-GPU)                                              */
+  DBFFT_E_NCCL = 5,          /* NCCL could not be loaded / initialised or a collective failed     */
   DBFFT_E_OOM = 6,           /* device allocation failed                                          */
   DBFFT_E_NOT_CONVERGED = 7, /* PCG max_cg or Newton max_newton exhausted; report filled; state
                                 rolled back to the last commit                                   */
@@ -60,11 +69,16 @@ typedef enum {
 typedef enum { DBFFT_SMALL_STRAIN = 6, DBFFT_FINITE_STRAIN = 9 } dbfft_kinematics;
 
 typedef struct {
-  int32_t rank, world;   /* world must be 1 in this version                        */
-  const void* nccl_id;   /* reserved, NULL                                         */
-  void* cuda_stream;     /* cudaStream_t or NULL (ctx creates its own stream)      */
-  int32_t device;        /* CUDA device ordinal (-1: current device)               */
+  int32_t rank, world;   /* this rank and the number of ranks P (1: single GPU)        */
+  const void* nccl_id;   /* 128-byte ncclUniqueId (NCCL mode, world > 1), else NULL    */
+  void* cuda_stream;     /* cudaStream_t or NULL (ctx creates its own stream)          */
+  int32_t device;        /* CUDA device ordinal (-1: current device)                   */
+  int32_t loopback;      /* 1: all `world` ranks virtual in this process (testing)     */
 } dbfft_env;
+
+/* NCCL bootstrap (rank 0): writes a 128-byte ncclUniqueId.  NCCL is loaded at run time
+ * (dlopen libnccl.so.2, or $DBFFT_NCCL_LIB); DBFFT_E_NCCL if it cannot be loaded. */
+dbfft_status dbfft_nccl_unique_id(void* out128);
 
 /* Create a context for grid n (voxels) and cell lengths L.  (sync) */
 dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinematics,

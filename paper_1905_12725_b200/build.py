@@ -42,7 +42,7 @@ def build(force=False, verbose=False, lib=None, defines=()):
 
     with ThreadPoolExecutor(len(SOURCES)) as ex:
         objs = list(ex.map(comp, SOURCES))
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", target, *objs]
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", target, *objs, "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stderr[-4000:])

@@ -218,117 +218,116 @@ DBF_DEV double norm9(const double* m) {
   return sqrt(s);
 }
 
-__global__ void __launch_bounds__(BLK) k_fin_init(CgDev* cg, const double* partials, int nblk) {
-  __shared__ double s[2];
-  cta_reduce(partials, nblk, 2, s);
-  if (threadIdx.x == 0) {
-    for (int a = 0; a < 9; ++a) {
-      double z = 0.0;
-      for (int b = 0; b < 9; ++b) z += cg->Minv_e[9 * a + b] * cg->re[b];
-      cg->ze[a] = z;
-    }
-    double rze = 0.0, ree = 0.0;
-    for (int a = 0; a < 9; ++a) {
-      cg->pe[a] = cg->ze[a];
-      rze += cg->re[a] * cg->ze[a];
-      ree += cg->re[a] * cg->re[a];
-    }
-    cg->rz = s[0] + rze;
-    cg->rr = s[1];
-    const double den = fmax(norm9(cg->msig), 1e-300);
-    cg->eps_eq = sqrt(s[1]) / den;
-    cg->eps_load = cg->macro ? sqrt(ree) / den : 0.0;
-    cg->converged = (cg->eps_eq <= cg->tol_eq && cg->eps_load <= cg->tol_load) ? 1 : 0;
-    if (!(cg->rz == cg->rz)) cg->breakdown = 1;
+// The finalizers read small vectors already reduced over CTAs (k_reduce) and, with several
+// ranks, over ranks (NCCL all-reduce or the loopback kernel below).
+
+// loc = [<r,z>_u, <r,r>_u]
+__global__ void k_fin_init(CgDev* cg, const double* loc) {
+  if (threadIdx.x != 0) return;
+  for (int a = 0; a < 9; ++a) {
+    double z = 0.0;
+    for (int b = 0; b < 9; ++b) z += cg->Minv_e[9 * a + b] * cg->re[b];
+    cg->ze[a] = z;
   }
+  double rze = 0.0, ree = 0.0;
+  for (int a = 0; a < 9; ++a) {
+    cg->pe[a] = cg->ze[a];
+    rze += cg->re[a] * cg->ze[a];
+    ree += cg->re[a] * cg->re[a];
+  }
+  cg->rz = loc[0] + rze;
+  cg->rr = loc[1];
+  const double den = fmax(norm9(cg->msig), 1e-300);
+  cg->eps_eq = sqrt(loc[1]) / den;
+  cg->eps_load = cg->macro ? sqrt(ree) / den : 0.0;
+  cg->converged = (cg->eps_eq <= cg->tol_eq && cg->eps_load <= cg->tol_load) ? 1 : 0;
+  if (!(cg->rz == cg->rz)) cg->breakdown = 1;
 }
 
-__global__ void __launch_bounds__(BLK) k_fin_alpha(CgDev* cg, const double* pq_part, int npq, const double* dc_part, int ndc, int nred) {
+// loc = [<p,q>_u, sum sigma(p) (9)]
+__global__ void k_fin_alpha(CgDev* cg, const double* loc) {
+  if (threadIdx.x != 0) return;
   if (cg->converged | cg->breakdown) return;
-  __shared__ double s[1];
-  __shared__ double dc[10];
-  cta_reduce(pq_part, npq, 1, s);
-  cta_reduce(dc_part, ndc, nred, dc);
-  if (threadIdx.x == 0) {
-    for (int a = 0; a < 9; ++a) cg->dc[a] = dc[a] * cg->inv_n;
-    if (cg->sym) sym9(cg->dc);
-    double pq = s[0];
-    for (int a = 0; a < 9; ++a) {
-      cg->qe[a] = cg->mask[a] * cg->dc[a];
-      pq += cg->pe[a] * cg->qe[a];
-    }
-    cg->pq = pq;
-    if (!(pq > 0.0) || !(pq == pq)) {
-      cg->breakdown = 1;
-      return;
-    }
-    const double alpha = cg->rz / pq;
-    cg->alpha = alpha;
-    for (int a = 0; a < 9; ++a) {
-      cg->xe[a] += alpha * cg->pe[a];
-      cg->re[a] -= alpha * cg->qe[a];
-      cg->msig[a] += alpha * cg->dc[a];
-    }
-    for (int a = 0; a < 9; ++a) {
-      double z = 0.0;
-      for (int b = 0; b < 9; ++b) z += cg->Minv_e[9 * a + b] * cg->re[b];
-      cg->ze[a] = z;
-    }
+  for (int a = 0; a < 9; ++a) cg->dc[a] = loc[1 + a] * cg->inv_n;
+  if (cg->sym) sym9(cg->dc);
+  double pq = loc[0];
+  for (int a = 0; a < 9; ++a) {
+    cg->qe[a] = cg->mask[a] * cg->dc[a];
+    pq += cg->pe[a] * cg->qe[a];
+  }
+  cg->pq = pq;
+  if (!(pq > 0.0) || !(pq == pq)) {
+    cg->breakdown = 1;
+    return;
+  }
+  const double alpha = cg->rz / pq;
+  cg->alpha = alpha;
+  for (int a = 0; a < 9; ++a) {
+    cg->xe[a] += alpha * cg->pe[a];
+    cg->re[a] -= alpha * cg->qe[a];
+    cg->msig[a] += alpha * cg->dc[a];
+  }
+  for (int a = 0; a < 9; ++a) {
+    double z = 0.0;
+    for (int b = 0; b < 9; ++b) z += cg->Minv_e[9 * a + b] * cg->re[b];
+    cg->ze[a] = z;
   }
 }
 
-__global__ void __launch_bounds__(BLK) k_fin_beta(CgDev* cg, const double* partials, int nblk) {
+// loc = [<r,z>_u, <r,r>_u]
+__global__ void k_fin_beta(CgDev* cg, const double* loc) {
+  if (threadIdx.x != 0) return;
   if (cg->converged | cg->breakdown) return;
-  __shared__ double s[2];
-  cta_reduce(partials, nblk, 2, s);
-  if (threadIdx.x == 0) {
-    double rze = 0.0, ree = 0.0;
-    for (int a = 0; a < 9; ++a) {
-      rze += cg->re[a] * cg->ze[a];
-      ree += cg->re[a] * cg->re[a];
-    }
-    const double rz_new = s[0] + rze;
-    cg->rr = s[1];
-    cg->iters += 1;
-    const double den = fmax(norm9(cg->msig), 1e-300);
-    cg->eps_eq = sqrt(s[1]) / den;
-    cg->eps_load = cg->macro ? sqrt(ree) / den : 0.0;
-    if (!(rz_new == rz_new)) {
-      cg->breakdown = 1;
-      return;
-    }
-    if (cg->eps_eq <= cg->tol_eq && cg->eps_load <= cg->tol_load) {
-      cg->converged = 1;
-      return;
-    }
-    const double beta = rz_new / cg->rz;
-    cg->beta = beta;
-    cg->rz = rz_new;
-    for (int a = 0; a < 9; ++a) cg->pe[a] = cg->ze[a] + beta * cg->pe[a];
-    if (cg->iters >= cg->max_iter) cg->converged = 2;  // exhausted
+  double rze = 0.0, ree = 0.0;
+  for (int a = 0; a < 9; ++a) {
+    rze += cg->re[a] * cg->ze[a];
+    ree += cg->re[a] * cg->re[a];
   }
+  const double rz_new = loc[0] + rze;
+  cg->rr = loc[1];
+  cg->iters += 1;
+  const double den = fmax(norm9(cg->msig), 1e-300);
+  cg->eps_eq = sqrt(loc[1]) / den;
+  cg->eps_load = cg->macro ? sqrt(ree) / den : 0.0;
+  if (!(rz_new == rz_new)) {
+    cg->breakdown = 1;
+    return;
+  }
+  if (cg->eps_eq <= cg->tol_eq && cg->eps_load <= cg->tol_load) {
+    cg->converged = 1;
+    return;
+  }
+  const double beta = rz_new / cg->rz;
+  cg->beta = beta;
+  cg->rz = rz_new;
+  for (int a = 0; a < 9; ++a) cg->pe[a] = cg->ze[a] + beta * cg->pe[a];
+  if (cg->iters >= cg->max_iter) cg->converged = 2;  // exhausted
 }
 
-// true residual: r = b - Ax already formed; msig = msig0 + <sigma(x)>; re = be - P<sigma(x)>
-__global__ void __launch_bounds__(BLK) k_fin_true(CgDev* cg, const double* rr_part, int nblk, const double* dc_part, int ndc, int nred) {
-  __shared__ double s[1];
-  __shared__ double dc[10];
-  cta_reduce(rr_part, nblk, 1, s);
-  cta_reduce(dc_part, ndc, nred, dc);
-  if (threadIdx.x == 0) {
-    for (int a = 0; a < 9; ++a) cg->dc[a] = dc[a] * cg->inv_n;
-    if (cg->sym) sym9(cg->dc);
-    double ree = 0.0;
-    for (int a = 0; a < 9; ++a) {
-      cg->msig[a] = cg->msig0[a] + cg->dc[a];
-      cg->re[a] = cg->be[a] - cg->mask[a] * cg->dc[a];
-      ree += cg->re[a] * cg->re[a];
-    }
-    const double den = fmax(norm9(cg->msig), 1e-300);
-    cg->rr = s[0];
-    cg->eps_eq = sqrt(s[0]) / den;
-    cg->eps_load = cg->macro ? sqrt(ree) / den : 0.0;
-    cg->converged = (cg->eps_eq <= cg->tol_eq && cg->eps_load <= cg->tol_load) ? 1 : 0;
+// true residual: r = b - Ax already formed.  loc = [<r,r>_u, sum sigma(x) (9)]
+__global__ void k_fin_true(CgDev* cg, const double* loc) {
+  if (threadIdx.x != 0) return;
+  for (int a = 0; a < 9; ++a) cg->dc[a] = loc[1 + a] * cg->inv_n;
+  if (cg->sym) sym9(cg->dc);
+  double ree = 0.0;
+  for (int a = 0; a < 9; ++a) {
+    cg->msig[a] = cg->msig0[a] + cg->dc[a];
+    cg->re[a] = cg->be[a] - cg->mask[a] * cg->dc[a];
+    ree += cg->re[a] * cg->re[a];
+  }
+  const double den = fmax(norm9(cg->msig), 1e-300);
+  cg->rr = loc[0];
+  cg->eps_eq = sqrt(loc[0]) / den;
+  cg->eps_load = cg->macro ? sqrt(ree) / den : 0.0;
+  cg->converged = (cg->eps_eq <= cg->tol_eq && cg->eps_load <= cg->tol_load) ? 1 : 0;
+}
+
+// loopback all-reduce over P virtual ranks of one process: v[r][k] <- op_r v[r][k] for all r
+__global__ void k_allreduce_lb(double* const* v, int P, int k, int is_max) {
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    double s = v[0][j];
+    for (int r = 1; r < P; ++r) s = is_max ? fmax(s, v[r][j]) : s + v[r][j];
+    for (int r = 0; r < P; ++r) v[r][j] = s;
   }
 }
 
@@ -338,30 +337,11 @@ __global__ void __launch_bounds__(BLK) k_reduce(const double* partials, int nblk
   if (threadIdx.x < nred) out[threadIdx.x] = s[threadIdx.x];
 }
 
-__global__ void __launch_bounds__(BLK) k_mean_sym(const double* __restrict__ tan, int nk, long long nvox, double* partials) {
-  // partials[block][nk]; nk <= 45
-  double acc[45];
-  for (int k = 0; k < 45; ++k) acc[k] = 0.0;
-  for (long long v = (long long)blockIdx.x * BLK + threadIdx.x; v < nvox; v += (long long)gridDim.x * BLK)
-    for (int k = 0; k < nk; ++k) acc[k] += __ldg(tan + (long long)k * nvox + v);
-  __shared__ double red[BLK / 32][45];
-  for (int k = 0; k < nk; ++k) {
-    double s = warp_sum(acc[k]);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][k] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x < nk) {
-    double s = 0.0;
-    for (int w = 0; w < BLK / 32; ++w) s += red[w][threadIdx.x];
-    partials[(long long)blockIdx.x * nk + threadIdx.x] = s;
-  }
-}
-
-__global__ void k_phase_hist(const uint16_t* __restrict__ ph, long long nvox, unsigned long long* counts, int nphase, int* bad) {
+__global__ void k_phase_hist(const uint16_t* __restrict__ ph, long long nvox, double* counts, int nphase, int* bad) {
   for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < nvox; v += (long long)gridDim.x * blockDim.x) {
     const int p = ph[v];
     if (p >= nphase) atomicExch(bad, 1);
-    else atomicAdd(counts + p, 1ull);
+    else atomicAdd(counts + p, 1.0);  // integer-valued doubles: exact below 2^53
   }
 }
 
@@ -390,24 +370,28 @@ cudaError_t launch_cg_direction(const SpecGeom& g, const PrecQ& q, const CgDev* 
   k_cg_direction<<<NBLK, BLK, 0, s>>>(g, q, cg, p, r);
   return cudaGetLastError();
 }
-cudaError_t launch_fin_init(CgDev* cg, const double* partials, int nblk, cudaStream_t s) {
-  k_fin_init<<<1, BLK, 0, s>>>(cg, partials, nblk);
+cudaError_t launch_fin_init(CgDev* cg, const double* loc, cudaStream_t s) {
+  k_fin_init<<<1, 32, 0, s>>>(cg, loc);
   return cudaGetLastError();
 }
-cudaError_t launch_fin_alpha(CgDev* cg, const double* pq_part, int npq, const double* dc_part, int ndc, int nred, cudaStream_t s) {
-  k_fin_alpha<<<1, BLK, 0, s>>>(cg, pq_part, npq, dc_part, ndc, nred);
+cudaError_t launch_fin_alpha(CgDev* cg, const double* loc, cudaStream_t s) {
+  k_fin_alpha<<<1, 32, 0, s>>>(cg, loc);
   return cudaGetLastError();
 }
-cudaError_t launch_fin_beta(CgDev* cg, const double* partials, int nblk, cudaStream_t s) {
-  k_fin_beta<<<1, BLK, 0, s>>>(cg, partials, nblk);
+cudaError_t launch_fin_beta(CgDev* cg, const double* loc, cudaStream_t s) {
+  k_fin_beta<<<1, 32, 0, s>>>(cg, loc);
   return cudaGetLastError();
 }
 cudaError_t launch_true_residual(const SpecGeom& g, const cplx* b, const cplx* Ax, cplx* r, double* partials, int nblk, cudaStream_t s) {
   k_true_residual<<<nblk, BLK, 0, s>>>(g, b, Ax, r, partials);
   return cudaGetLastError();
 }
-cudaError_t launch_fin_true(CgDev* cg, const double* rr_part, int nblk, const double* dc_part, int ndc, int nred, cudaStream_t s) {
-  k_fin_true<<<1, BLK, 0, s>>>(cg, rr_part, nblk, dc_part, ndc, nred);
+cudaError_t launch_fin_true(CgDev* cg, const double* loc, cudaStream_t s) {
+  k_fin_true<<<1, 32, 0, s>>>(cg, loc);
+  return cudaGetLastError();
+}
+cudaError_t launch_allreduce_lb(double* const* v, int P, int k, int is_max, cudaStream_t s) {
+  k_allreduce_lb<<<1, 64, 0, s>>>(v, P, k, is_max);
   return cudaGetLastError();
 }
 cudaError_t launch_axpy(const SpecGeom& g, cplx* y, const cplx* x, double a, cudaStream_t s) {
@@ -418,11 +402,7 @@ cudaError_t launch_reduce(const double* partials, int nblk, int nred, double* ou
   k_reduce<<<1, BLK, 0, s>>>(partials, nblk, nred, out);
   return cudaGetLastError();
 }
-cudaError_t launch_mean_sym(const double* tan, int nk, long long nvox, double* partials, int nblk, cudaStream_t s) {
-  k_mean_sym<<<nblk, BLK, 0, s>>>(tan, nk, nvox, partials);
-  return cudaGetLastError();
-}
-cudaError_t launch_phase_hist(const uint16_t* ph, long long nvox, unsigned long long* counts, int nphase, int* bad, cudaStream_t s) {
+cudaError_t launch_phase_hist(const uint16_t* ph, long long nvox, double* counts, int nphase, int* bad, cudaStream_t s) {
   k_phase_hist<<<NBLK, BLK, 0, s>>>(ph, nvox, counts, nphase, bad);
   return cudaGetLastError();
 }

@@ -35,14 +35,14 @@ cudaError_t launch_cg_init(const SpecGeom& g, const PrecQ& q, const cplx* r, cpl
 cudaError_t launch_cg_update(const SpecGeom& g, const PrecQ& q, CgDev* cg, cplx* x, const cplx* p, cplx* r, const cplx* qv,
                              double* partials, int nblk, cudaStream_t s);
 cudaError_t launch_cg_direction(const SpecGeom& g, const PrecQ& q, const CgDev* cg, cplx* p, const cplx* r, cudaStream_t s);
-cudaError_t launch_fin_init(CgDev* cg, const double* partials, int nblk, cudaStream_t s);
-cudaError_t launch_fin_alpha(CgDev* cg, const double* pq_part, int npq, const double* dc_part, int ndc, int nred, cudaStream_t s);
-cudaError_t launch_fin_beta(CgDev* cg, const double* partials, int nblk, cudaStream_t s);
+cudaError_t launch_fin_init(CgDev* cg, const double* loc, cudaStream_t s);
+cudaError_t launch_fin_alpha(CgDev* cg, const double* loc, cudaStream_t s);
+cudaError_t launch_fin_beta(CgDev* cg, const double* loc, cudaStream_t s);
 cudaError_t launch_true_residual(const SpecGeom& g, const cplx* b, const cplx* Ax, cplx* r, double* partials, int nblk, cudaStream_t s);
-cudaError_t launch_fin_true(CgDev* cg, const double* rr_part, int nblk, const double* dc_part, int ndc, int nred, cudaStream_t s);
+cudaError_t launch_fin_true(CgDev* cg, const double* loc, cudaStream_t s);
+cudaError_t launch_allreduce_lb(double* const* v, int P, int k, int is_max, cudaStream_t s);
 cudaError_t launch_axpy(const SpecGeom& g, cplx* y, const cplx* x, double a, cudaStream_t s);
 cudaError_t launch_reduce(const double* partials, int nblk, int nred, double* out, cudaStream_t s);
-cudaError_t launch_mean_sym(const double* tan, int nk, long long nvox, double* partials, int nblk, cudaStream_t s);
-cudaError_t launch_phase_hist(const uint16_t* ph, long long nvox, unsigned long long* counts, int nphase, int* bad, cudaStream_t s);
+cudaError_t launch_phase_hist(const uint16_t* ph, long long nvox, double* counts, int nphase, int* bad, cudaStream_t s);
 cudaError_t launch_fill(double* p, long long n, double v, cudaStream_t s);
 int cg_blocks();

@@ -1,10 +1,20 @@
-// dbfft.cu — C-ABI implementation and host driver (plan, buffers, PCG and Newton drivers).
+// dbfft.cu — C-ABI implementation and host driver (plan, slabs, exchanges, PCG and Newton).
 //
 // Host code only orchestrates: every arithmetic step of the hot path (gradient, FFTs,
 // contraction, divergence, preconditioner, CG algebra, constitutive updates, reductions) runs
 // in the kernels of passes.cu / cg.cu / this file.  The host does the O(1) macro algebra
 // (9x9 macro-block inverse, preconditioner coefficients from Cbar) once per increment.
+//
+// Distribution: real space in z-slabs, spectral space in ky-slabs.  The z pass
+// I1 writes its output already blocked by destination rank ([dest][f][ky_loc][z_loc][kx]), one
+// exchange moves the blocks, the y pass I2 reads them in place (rank-chunked addressing); F2
+// writes [dest][f][ky_loc][z_loc][kx] and the second exchange feeds F3.  Inner products are
+// per-rank partial sums followed by an all-reduce of <= 10 doubles.  Exchanges and all-reduces
+// use NCCL (dlopen'd at run time) across processes, or the in-process loopback (P virtual ranks
+// on one device, device-to-device copies) that tests the same kernels and layouts on one GPU.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -23,69 +33,126 @@ namespace {
 
 enum Family { FAM_NONE = 0, FAM_LINEAR = 1, FAM_NEOHOOKE = 2, FAM_J2 = 3 };
 
-enum ProfId { PK_I1 = 0, PK_I2, PK_X, PK_F2, PK_F3, PK_XCONST, PK_CGUPD, PK_CGDIR, PK_FIN, PK_OTHER, PK_COUNT };
+enum ProfId { PK_I1 = 0, PK_I2, PK_X, PK_F2, PK_F3, PK_XCONST, PK_CGUPD, PK_CGDIR, PK_FIN, PK_OTHER, PK_XCHG, PK_COUNT };
 const char* kProfNames[PK_COUNT] = {"pass_I1", "pass_I2", "pass_X", "pass_F2", "pass_F3", "pass_X_const",
-                                    "cg_update", "cg_direction", "cg_finalize", "other"};
-
-struct DevBuf {
-  void* p = nullptr;
-  size_t bytes = 0;
-};
+                                    "cg_update", "cg_direction", "cg_finalize", "other", "exchange"};
 
 std::string g_create_error;
 
+// ---------------------------------------------------------------- NCCL, loaded on demand
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+Nccl g_nccl;
+
+bool nccl_load(std::string* err) {
+  if (g_nccl.h) return true;
+  const char* names[] = {getenv("DBFFT_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
+  for (const char* nm : names) {
+    if (!nm) continue;
+    g_nccl.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+    if (g_nccl.h) break;
+  }
+  if (!g_nccl.h) {
+    *err = "cannot dlopen libnccl.so.2 (set DBFFT_NCCL_LIB)";
+    return false;
+  }
+#define LD(field, sym) g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(g_nccl.h, sym))
+  LD(GetUniqueId, "ncclGetUniqueId");
+  LD(CommInitRank, "ncclCommInitRank");
+  LD(CommDestroy, "ncclCommDestroy");
+  LD(AllReduce, "ncclAllReduce");
+  LD(Send, "ncclSend");
+  LD(Recv, "ncclRecv");
+  LD(GroupStart, "ncclGroupStart");
+  LD(GroupEnd, "ncclGroupEnd");
+  LD(GetErrorString, "ncclGetErrorString");
+#undef LD
+  if (!g_nccl.GetUniqueId || !g_nccl.CommInitRank || !g_nccl.AllReduce || !g_nccl.Send || !g_nccl.Recv || !g_nccl.GroupStart ||
+      !g_nccl.GroupEnd) {
+    *err = "libnccl is missing required symbols";
+    return false;
+  }
+  return true;
+}
+
+int ilog2(int n) {
+  int k = 0;
+  while ((1 << k) < n) ++k;
+  return k;
+}
+
+bool is_pow2_in(int n) { return n >= 8 && n <= 512 && (n & (n - 1)) == 0; }
+
 }  // namespace
+
+// one rank's share of the problem
+struct Slab {
+  int rank = 0;
+  int nyl = 0, nzl = 0, ky0 = 0, z0 = 0;
+  long long Hs = 0;       // complex points per field (= n1h * nyl * n3 = n1h * n2 * nzl)
+  long long Nloc = 0;     // voxels in the z-slab
+  long long nlines = 0;   // x lines in the z-slab
+  const double* xiy = nullptr;  // xi_y of the local ky slab (offset into the global table)
+  cplx *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *b = nullptr, *u = nullptr, *u_c = nullptr;
+  cplx *WA = nullptr, *WR = nullptr, *WB = nullptr;  // send, receive (== WA when P == 1), y-pass buffers
+  uint16_t* phase = nullptr;
+  double* ptable = nullptr;
+  double *F = nullptr, *F_c = nullptr, *epsp_c = nullptr, *epsp_t = nullptr, *tan = nullptr;
+  CgDev* cg = nullptr;
+  double *part_x = nullptr, *part_f3 = nullptr, *part_cg = nullptr, *part_misc = nullptr;
+  double* loc = nullptr;   // [64] small reduced vectors (also the all-reduce buffers)
+  double* e_dev = nullptr; // [9]
+  int* bad = nullptr;
+  double* counts = nullptr;
+  double* tmp_real = nullptr;
+};
 
 struct dbfft_ctx_s {
   int n1, n2, n3, n1h;
   double L[3];
   int kin;  // 6 or 9
-  long long N, Hs;
+  long long N;  // global voxels
+  int P = 1, rank = 0, loopback = 0;
   int device;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   std::string err;
-  // tables
+  ncclComm_t comm = nullptr;
+  std::vector<Slab> slabs;
+  double** loc_ptrs = nullptr;  // device array of the slabs' loc pointers (loopback all-reduce)
+  // tables (global)
   double *xix = nullptr, *xiy = nullptr, *xiz = nullptr;
   cplx *tw1 = nullptr, *tw2 = nullptr, *tw3 = nullptr;
-  // vectors [3][Hs]
-  cplx *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *b = nullptr, *u = nullptr, *u_c = nullptr;
-  cplx *WA = nullptr, *WB = nullptr;
-  // materials and state
+  // materials
   int family = FAM_NONE;
   int nph = 0;
-  uint16_t* phase = nullptr;
-  double* ptable = nullptr;
+  int tmode = 1;  // neo-Hookean tangent storage: 1 compact (F^-1, c1), 0 full 45
   std::vector<double> h_ptable;
-  double *F = nullptr, *F_c = nullptr;      // finite: F [9][N]; J2: eps [6][N]
-  double *epsp_c = nullptr, *epsp_t = nullptr;
-  double* tan = nullptr;                    // [21|45][N]
-  double Fbar[9], Fbar_c[9];                // macro strain / F (incl. stress-controlled comps)
-  bool tangent_valid = false;
-  int tmode = 1;                            // neo-Hookean tangent storage: 1 compact (F^-1, c1), 0 full 45
-  // linear mean stiffness (Voigt 6x6) or current mean tangent (full 81)
+  double Fbar[9], Fbar_c[9];  // macro strain / F (incl. stress-controlled comps)
   double Cbar[81];
   PrecQ prec;
   bool prec_valid = false;
-  // CG
-  CgDev* cg = nullptr;
-  CgDev* h_cg = nullptr;      // pinned mirror
-  double *part_x = nullptr, *part_f3 = nullptr, *part_cg = nullptr, *part_misc = nullptr;
-  double* red_out = nullptr;  // [64]
-  double* h_red = nullptr;    // pinned [64]
-  double* e_dev = nullptr;    // [9] macro block for passes
-  int* bad = nullptr;
+  CgDev* h_cg = nullptr;     // pinned mirror (slab 0)
+  double* h_red = nullptr;   // pinned [64]
   int* h_bad = nullptr;
-  unsigned long long* counts = nullptr;
-  double* tmp_real = nullptr;  // [9][N] scratch for get_field / eval_state
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
-  std::vector<std::pair<int, std::pair<int, int>>> ev_pending;  // id, (start idx, stop idx)
+  std::vector<std::pair<int, std::pair<int, int>>> ev_pending;
   size_t ev_next = 0;
   double prof_ms[PK_COUNT];
   long long prof_n[PK_COUNT];
-  long long nlaunch = 0;  // kernels launched by this ctx (always counted)
+  long long nlaunch = 0;
 };
 
 namespace {
@@ -105,13 +172,14 @@ namespace {
     if (s_ != DBFFT_OK) return s_;                                                            \
   } while (0)
 
-int ilog2(int n) {
-  int k = 0;
-  while ((1 << k) < n) ++k;
-  return k;
-}
-
-bool is_pow2_in(int n) { return n >= 8 && n <= 512 && (n & (n - 1)) == 0; }
+#define CKN(call)                                                                             \
+  do {                                                                                        \
+    ncclResult_t r_ = (call);                                                                 \
+    if (r_ != ncclSuccess) {                                                                  \
+      ctx->err = std::string(#call) + ": " + (g_nccl.GetErrorString ? g_nccl.GetErrorString(r_) : "nccl error"); \
+      return DBFFT_E_NCCL;                                                                    \
+    }                                                                                         \
+  } while (0)
 
 // ---------------------------------------------------------------- profiling helpers
 struct ProfScope {
@@ -154,81 +222,106 @@ void prof_flush(dbfft_ctx ctx) {
 }
 
 // ---------------------------------------------------------------- geometry builders
-Freq freq(dbfft_ctx ctx) { return Freq{ctx->xix, ctx->xiy, ctx->xiz}; }
-
-SpecGeom spec(dbfft_ctx ctx) {
+SpecGeom spec(dbfft_ctx ctx, const Slab& s) {
   SpecGeom g;
   g.n1h = ctx->n1h;
-  g.n2 = ctx->n2;
+  g.n2 = s.nyl;
   g.n3 = ctx->n3;
-  g.Hs = ctx->Hs;
-  g.fq = freq(ctx);
+  g.Hs = s.Hs;
+  g.fq = Freq{ctx->xix, s.xiy, ctx->xiz};
   g.n1 = ctx->n1;
   return g;
 }
 
-// layouts (complex elements):
-//   S  spectral [f][ky][kz][kx] : fs = Hs, ky stride n3*n1h, kz stride n1h
-//   A  after z   [f][ky][z][kx]  : same strides as S
-//   B  after y   [f][z][y][kx]   : fs = Hs, z stride n2*n1h, y stride n1h
-ColGeom colgeom(dbfft_ctx ctx, bool zpass, const cplx* in, cplx* out, bool in_is_B, bool out_is_B) {
+ColGeom colbase(dbfft_ctx ctx, const cplx* in, cplx* out) {
   ColGeom g;
   memset(&g, 0, sizeof(g));
-  const long long n1h = ctx->n1h;
   g.in = in;
   g.out = out;
-  g.in_fs = g.out_fs = ctx->Hs;
   g.n1h = ctx->n1h;
   g.n1 = ctx->n1;
-  g.fq = freq(ctx);
-  if (zpass) {  // outer = ky, pos = kz/z, both in S/A layout
-    g.in_os = g.out_os = (long long)ctx->n3 * n1h;
-    g.in_ps = g.out_ps = n1h;
-    g.ncols = (long long)ctx->n2 * n1h;
-    g.in_psh = g.out_psh = ilog2(ctx->n3);
-    g.tw = ctx->tw3;
-  } else {  // outer = z, pos = y/ky
-    if (in_is_B) { g.in_os = (long long)ctx->n2 * n1h; g.in_ps = n1h; }
-    else { g.in_os = n1h; g.in_ps = (long long)ctx->n3 * n1h; }
-    if (out_is_B) { g.out_os = (long long)ctx->n2 * n1h; g.out_ps = n1h; }
-    else { g.out_os = n1h; g.out_ps = (long long)ctx->n3 * n1h; }
-    g.ncols = (long long)ctx->n3 * n1h;
-    g.in_psh = g.out_psh = ilog2(ctx->n2);
-    g.tw = ctx->tw2;
-  }
-  g.in_pcs = g.out_pcs = 0;
   return g;
 }
 
-XGeom xgeom(dbfft_ctx ctx, const cplx* in, cplx* out) {
+// layouts (complex elements, per slab; P = 1 reduces every one of them to the plain layouts):
+//   S  spectral  [f][kyl][kz][kx]                     fs = Hs
+//   X1 I1 -> I2  [rank][f][kyl][zl][kx]  (sender: rank = destination, receiver: rank = source)
+//   B  y-pass    [f][zl][y][kx]                       fs = Hs
+//   X2 F2 -> F3  [rank][f][kyl][zl][kx]
+// chunk sizes: nf * nyl * nzl * n1h.
+ColGeom geom_I1(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf) {
+  ColGeom g = colbase(ctx, in, out);
+  const long long n1h = ctx->n1h;
+  g.in_fs = s.Hs; g.in_os = (long long)ctx->n3 * n1h; g.in_ps = n1h; g.in_psh = ilog2(ctx->n3); g.in_pcs = 0;
+  g.out_fs = (long long)s.nyl * s.nzl * n1h; g.out_os = (long long)s.nzl * n1h; g.out_ps = n1h;
+  g.out_psh = ilog2(s.nzl); g.out_pcs = (long long)nf * s.nyl * s.nzl * n1h;
+  g.ncols = (long long)s.nyl * n1h;
+  g.tw = ctx->tw3;
+  g.fq = Freq{ctx->xix, s.xiy, ctx->xiz};
+  return g;
+}
+ColGeom geom_I2(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_in) {
+  ColGeom g = colbase(ctx, in, out);
+  const long long n1h = ctx->n1h;
+  g.in_fs = (long long)s.nyl * s.nzl * n1h; g.in_os = n1h; g.in_ps = (long long)s.nzl * n1h;
+  g.in_psh = ilog2(s.nyl); g.in_pcs = (long long)nf_in * s.nyl * s.nzl * n1h;
+  g.out_fs = s.Hs; g.out_os = (long long)ctx->n2 * n1h; g.out_ps = n1h; g.out_psh = ilog2(ctx->n2); g.out_pcs = 0;
+  g.ncols = (long long)s.nzl * n1h;
+  g.tw = ctx->tw2;
+  g.fq = Freq{ctx->xix, ctx->xiy, ctx->xiz};
+  return g;
+}
+ColGeom geom_F2(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_out) {
+  ColGeom g = colbase(ctx, in, out);
+  const long long n1h = ctx->n1h;
+  g.in_fs = s.Hs; g.in_os = (long long)ctx->n2 * n1h; g.in_ps = n1h; g.in_psh = ilog2(ctx->n2); g.in_pcs = 0;
+  g.out_fs = (long long)s.nyl * s.nzl * n1h; g.out_os = n1h; g.out_ps = (long long)s.nzl * n1h;
+  g.out_psh = ilog2(s.nyl); g.out_pcs = (long long)nf_out * s.nyl * s.nzl * n1h;
+  g.ncols = (long long)s.nzl * n1h;
+  g.tw = ctx->tw2;
+  g.fq = Freq{ctx->xix, ctx->xiy, ctx->xiz};
+  return g;
+}
+ColGeom geom_F3(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_in) {
+  ColGeom g = colbase(ctx, in, out);
+  const long long n1h = ctx->n1h;
+  g.in_fs = (long long)s.nyl * s.nzl * n1h; g.in_os = (long long)s.nzl * n1h; g.in_ps = n1h;
+  g.in_psh = ilog2(s.nzl); g.in_pcs = (long long)nf_in * s.nyl * s.nzl * n1h;
+  g.out_fs = s.Hs; g.out_os = (long long)ctx->n3 * n1h; g.out_ps = n1h; g.out_psh = ilog2(ctx->n3); g.out_pcs = 0;
+  g.ncols = (long long)s.nyl * n1h;
+  g.tw = ctx->tw3;
+  g.fq = Freq{ctx->xix, s.xiy, ctx->xiz};
+  return g;
+}
+
+XGeom xgeom(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out) {
   XGeom g;
   memset(&g, 0, sizeof(g));
   g.in = in;
   g.out = out;
-  g.fs_in = g.fs_out = ctx->Hs;
+  g.fs_in = g.fs_out = s.Hs;
   g.n1h = ctx->n1h;
   g.n1 = ctx->n1;
-  g.nlines = (long long)ctx->n2 * ctx->n3;
+  g.nlines = s.nlines;
   g.tw = ctx->tw1;
   g.xix = ctx->xix;
   g.inv_n = 1.0 / (double)ctx->N;
-  g.partials = ctx->part_x;
+  g.partials = s.part_x;
   g.nred = 10;
-  g.phase = ctx->phase;
-  g.ptable = ctx->ptable;
-  g.tan = ctx->tan;
-  g.F = ctx->F;
-  g.epsp_c = ctx->epsp_c;
-  g.epsp_t = ctx->epsp_t;
-  g.nvox = ctx->N;
-  g.bad = ctx->bad;
+  g.phase = s.phase;
+  g.ptable = s.ptable;
+  g.tan = s.tan;
+  g.F = s.F;
+  g.epsp_c = s.epsp_c;
+  g.epsp_t = s.epsp_t;
+  g.nvox = s.Nloc;
+  g.bad = s.bad;
   g.tmode = ctx->tmode;
   return g;
 }
 
-dbfft_status run_col(dbfft_ctx ctx, int kind, int prof_id, const ColGeom& g) {
+dbfft_status run_col(dbfft_ctx ctx, int kind, int prof_id, const ColGeom& g, int N) {
   ProfScope ps(ctx, prof_id);
-  const int N = (kind == COL_I1S || kind == COL_I1F || kind == COL_F3S || kind == COL_F3F || kind == COL_ZI3) ? ctx->n3 : ctx->n2;
   CK(launch_col(kind, N, g, ctx->stream));
   return DBFFT_OK;
 }
@@ -236,6 +329,64 @@ dbfft_status run_col(dbfft_ctx ctx, int kind, int prof_id, const ColGeom& g) {
 dbfft_status run_x(dbfft_ctx ctx, int kind, int prof_id, const XGeom& g, int* grid) {
   ProfScope ps(ctx, prof_id);
   CK(launch_x(kind, ctx->n1, g, ctx->stream, grid));
+  return DBFFT_OK;
+}
+
+// ---------------------------------------------------------------- collectives
+// all-to-all of equal chunks: slab r sends WA[d*chunk] to rank d, which stores it at WR[r*chunk]
+dbfft_status exchange(dbfft_ctx ctx, long long chunk) {
+  if (ctx->P == 1) return DBFFT_OK;
+  ProfScope ps(ctx, PK_XCHG);
+  const size_t bytes = sizeof(cplx) * chunk;
+  if (ctx->loopback) {
+    for (int r = 0; r < ctx->P; ++r)
+      for (int d = 0; d < ctx->P; ++d)
+        CK(cudaMemcpyAsync(ctx->slabs[d].WR + (long long)r * chunk, ctx->slabs[r].WA + (long long)d * chunk, bytes,
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+    return DBFFT_OK;
+  }
+  Slab& s = ctx->slabs[0];
+  CK(cudaMemcpyAsync(s.WR + (long long)ctx->rank * chunk, s.WA + (long long)ctx->rank * chunk, bytes, cudaMemcpyDeviceToDevice,
+                     ctx->stream));
+  CKN(g_nccl.GroupStart());
+  for (int d = 0; d < ctx->P; ++d) {
+    if (d == ctx->rank) continue;
+    CKN(g_nccl.Send(s.WA + (long long)d * chunk, 2 * chunk, ncclFloat64, d, ctx->comm, ctx->stream));
+    CKN(g_nccl.Recv(s.WR + (long long)d * chunk, 2 * chunk, ncclFloat64, d, ctx->comm, ctx->stream));
+  }
+  CKN(g_nccl.GroupEnd());
+  return DBFFT_OK;
+}
+
+// all-reduce of slab.loc[off .. off+k) over ranks (sum or max)
+dbfft_status allreduce(dbfft_ctx ctx, int off, int k, bool is_max) {
+  if (ctx->P == 1) return DBFFT_OK;
+  ProfScope ps(ctx, PK_FIN);
+  if (ctx->loopback) {
+    std::vector<double*> h(ctx->P);
+    for (int r = 0; r < ctx->P; ++r) h[r] = ctx->slabs[r].loc + off;
+    CK(cudaMemcpyAsync(ctx->loc_ptrs, h.data(), sizeof(double*) * ctx->P, cudaMemcpyHostToDevice, ctx->stream));
+    CK(launch_allreduce_lb(ctx->loc_ptrs, ctx->P, k, is_max ? 1 : 0, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));  // h (host) must outlive the copy
+    return DBFFT_OK;
+  }
+  double* v = ctx->slabs[0].loc + off;
+  CKN(g_nccl.AllReduce(v, v, k, ncclFloat64, is_max ? ncclMax : ncclSum, ctx->comm, ctx->stream));
+  return DBFFT_OK;
+}
+
+// reduce CTA partials into slab.loc[off ..] (k values)
+dbfft_status reduce_to(dbfft_ctx ctx, Slab& s, const double* partials, int nblk, int nred, int off) {
+  ProfScope ps(ctx, PK_FIN);
+  CK(launch_reduce(partials, nblk, nred, s.loc + off, ctx->stream));
+  return DBFFT_OK;
+}
+
+// copy slab 0's loc[off .. off+k) to the host (all slabs hold the same values after allreduce)
+dbfft_status read_loc(dbfft_ctx ctx, int off, int k, double* host) {
+  CK(cudaMemcpyAsync(ctx->h_red, ctx->slabs[0].loc + off, sizeof(double) * k, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  memcpy(host, ctx->h_red, sizeof(double) * k);
   return DBFFT_OK;
 }
 
@@ -249,7 +400,6 @@ int voigt_of(int i, int j) {
   return 5;
 }
 
-// full C_ijkl (81) from a Voigt 6x6 of tensor entries
 void voigt_to_full(const double* CV, double* C81) {
   for (int i = 0; i < 3; ++i)
     for (int j = 0; j < 3; ++j)
@@ -268,17 +418,17 @@ void iso_voigt(double E, double nu, double* CV) {
 void cubic_voigt(double C11, double C12, double C44, const double* R, double* CV) {
   double C0[81], C[81];
   for (int a = 0; a < 81; ++a) C0[a] = 0.0;
+  auto idx = [](int i, int j, int k, int l) { return ((i * 3 + j) * 3 + k) * 3 + l; };
   for (int a = 0; a < 3; ++a)
     for (int b = 0; b < 3; ++b) {
-      C0[((a * 3 + a) * 3 + b) * 3 + b] = (a == b) ? C11 : C12;
+      C0[idx(a, a, b, b)] = (a == b) ? C11 : C12;
       if (a != b) {
-        C0[((a * 3 + b) * 3 + a) * 3 + b] = C44;
-        C0[((a * 3 + b) * 3 + b) * 3 + a] = C44;
+        C0[idx(a, b, a, b)] = C44;
+        C0[idx(a, b, b, a)] = C44;
       }
     }
   // rotate index by index: C_ijkl = R_ia R_jb R_kc R_ld C0_abcd (four successive contractions)
   double T1[81], T2[81], T3[81];
-  auto idx = [](int i, int j, int k, int l) { return ((i * 3 + j) * 3 + k) * 3 + l; };
   for (int i = 0; i < 3; ++i) for (int b = 0; b < 3; ++b) for (int c = 0; c < 3; ++c) for (int d = 0; d < 3; ++d) {
     double s = 0; for (int a = 0; a < 3; ++a) s += R[3 * i + a] * C0[idx(a, b, c, d)]; T1[idx(i, b, c, d)] = s; }
   for (int i = 0; i < 3; ++i) for (int j = 0; j < 3; ++j) for (int c = 0; c < 3; ++c) for (int d = 0; d < 3; ++d) {
@@ -368,16 +518,15 @@ bool macro_inverse(const double* C81, const uint8_t* mask, bool sym, double* Min
 
 // ---------------------------------------------------------------- small pointwise kernels
 __global__ void k_expand6(const double* __restrict__ v6, long long n, const double* macro9, double* __restrict__ out9) {
-  const int row9_of_voigt[6] = {0, 4, 8, 5, 2, 1};
-  (void)row9_of_voigt;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const int vo[9] = {0, 5, 4, 5, 1, 3, 4, 3, 2};
     for (int a = 0; a < 9; ++a) out9[(long long)a * n + i] = v6[(long long)vo[a] * n + i] + (macro9 ? macro9[a] : 0.0);
   }
 }
 
-__global__ void k_stress_linear(const double* __restrict__ e9, const uint16_t* __restrict__ ph, const double* __restrict__ pt,
-                                long long n, double* __restrict__ s9) {
+// in place allowed (e9 == s9): every voxel reads its 9 strains before writing its stresses
+__global__ void k_stress_linear(const double* e9, const uint16_t* __restrict__ ph, const double* __restrict__ pt, long long n,
+                                double* s9) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const double* C = pt + 36 * ph[i];
     const int ri[6] = {0, 4, 8, 5, 2, 1};
@@ -463,57 +612,59 @@ std::vector<double> axis_xi(int n, double L, int count) {
 
 // ---------------------------------------------------------------- operator application
 struct ApplyOut {
-  int grid_x = 0, grid_f3 = 0;
+  std::vector<int> grid_x, grid_f3;
 };
 
-// f = K(u) [+ e]; partials: part_x (DC of sigma), part_f3 (<u, f>)
-dbfft_status apply_K_internal(dbfft_ctx ctx, const cplx* u, cplx* f, const double* e, bool dot, ApplyOut* ao) {
+int nf_I1(dbfft_ctx ctx) { return ctx->kin == 9 ? 6 : 5; }
+
+// f = K(u) [+ e] on every slab; partials: part_x (DC of sigma), part_f3 (<u, f>) per slab.
+// u / f select per-slab vectors, e_member the macro block inside each slab's CgDev.
+typedef double Macro9[9];
+
+dbfft_status apply_K_slabs(dbfft_ctx ctx, cplx* Slab::*u, cplx* Slab::*f, bool use_e, Macro9 CgDev::*e_member, bool dot,
+                           ApplyOut* ao) {
   const bool fin = ctx->kin == 9;
   int xkind;
   if (ctx->family == FAM_LINEAR) xkind = X_K_SMALL_PHASE;
   else if (ctx->family == FAM_J2) xkind = X_K_J2;
   else xkind = ctx->tmode ? X_K_FIN_NH : X_K_FIN_TAN;
-  ColGeom g1 = colgeom(ctx, true, u, ctx->WA, false, false);
-  CKS(run_col(ctx, fin ? COL_I1F : COL_I1S, PK_I1, g1));
-  ColGeom g2 = colgeom(ctx, false, ctx->WA, ctx->WB, false, true);
-  CKS(run_col(ctx, fin ? COL_I2F : COL_I2S, PK_I2, g2));
-  XGeom gx = xgeom(ctx, ctx->WB, ctx->WB);
-  gx.e = e;
-  int gridx = 0;
-  CKS(run_x(ctx, xkind, PK_X, gx, &gridx));
-  ColGeom g4 = colgeom(ctx, false, ctx->WB, ctx->WA, true, false);
-  CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, g4));
-  ColGeom g5 = colgeom(ctx, true, ctx->WA, f, false, false);
-  if (dot) {
-    g5.dotp = u;
-    g5.partials = ctx->part_f3;
-  }
-  CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_F3, g5));
+  const int nf1 = nf_I1(ctx);
+  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_I1F : COL_I1S, PK_I1, geom_I1(ctx, s, s.*u, s.WA, nf1), ctx->n3));
+  CKS(exchange(ctx, (long long)nf1 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
+  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_I2F : COL_I2S, PK_I2, geom_I2(ctx, s, s.WR, s.WB, nf1), ctx->n2));
   if (ao) {
-    ao->grid_x = gridx;
-    ao->grid_f3 = col_grid(ctx->n3, g5.ncols);
+    ao->grid_x.assign(ctx->slabs.size(), 0);
+    ao->grid_f3.assign(ctx->slabs.size(), 0);
+  }
+  for (size_t k = 0; k < ctx->slabs.size(); ++k) {
+    Slab& s = ctx->slabs[k];
+    XGeom gx = xgeom(ctx, s, s.WB, s.WB);
+    gx.e = use_e ? (const double*)(s.cg->*e_member) : nullptr;
+    int gridx = 0;
+    CKS(run_x(ctx, xkind, PK_X, gx, &gridx));
+    if (ao) ao->grid_x[k] = gridx;
+  }
+  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, geom_F2(ctx, s, s.WB, s.WA, 6), ctx->n2));
+  CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
+  for (size_t k = 0; k < ctx->slabs.size(); ++k) {
+    Slab& s = ctx->slabs[k];
+    ColGeom g5 = geom_F3(ctx, s, s.WR, s.*f, 6);
+    if (dot) {
+      g5.dotp = s.*u;
+      g5.partials = s.part_f3;
+    }
+    CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_F3, g5, ctx->n3));
+    if (ao) ao->grid_f3[k] = col_grid(ctx->n3, g5.ncols);
   }
   return DBFFT_OK;
 }
 
-// forward tail of the rhs: WB holds -sigma spectra (from an X pass) -> F2 -> F3 -> out
-dbfft_status forward_tail(dbfft_ctx ctx, cplx* out) {
+// forward tail of the rhs: WB holds -sigma spectra (from an X pass) -> F2 -> F3 -> b
+dbfft_status forward_tail(dbfft_ctx ctx) {
   const bool fin = ctx->kin == 9;
-  ColGeom g4 = colgeom(ctx, false, ctx->WB, ctx->WA, true, false);
-  CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, g4));
-  ColGeom g5 = colgeom(ctx, true, ctx->WA, out, false, false);
-  CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_F3, g5));
-  return DBFFT_OK;
-}
-
-dbfft_status read_reduction(dbfft_ctx ctx, const double* partials, int nblk, int nred, double* host_out) {
-  {
-    ProfScope ps(ctx, PK_FIN);
-    CK(launch_reduce(partials, nblk, nred, ctx->red_out, ctx->stream));
-  }
-  CK(cudaMemcpyAsync(ctx->h_red, ctx->red_out, sizeof(double) * nred, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  memcpy(host_out, ctx->h_red, sizeof(double) * nred);
+  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, geom_F2(ctx, s, s.WB, s.WA, 6), ctx->n2));
+  CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
+  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_F3, geom_F3(ctx, s, s.WR, s.b, 6), ctx->n3));
   return DBFFT_OK;
 }
 
@@ -527,13 +678,17 @@ void sym_fill(double* m) {
 dbfft_status refresh_mean_tangent(dbfft_ctx ctx) {
   const int nk = ctx->kin == 9 ? 45 : 21;
   const int nblk = cg_blocks();
-  {
-    ProfScope ps(ctx, PK_OTHER);
-    const int mode = (ctx->family == FAM_J2) ? 2 : (ctx->tmode ? 1 : 0);
-    CK(launch_mean_tangent(mode, xgeom(ctx, nullptr, nullptr), ctx->part_misc, nblk, ctx->stream));
+  const int mode = (ctx->family == FAM_J2) ? 2 : (ctx->tmode ? 1 : 0);
+  for (Slab& s : ctx->slabs) {
+    {
+      ProfScope ps(ctx, PK_OTHER);
+      CK(launch_mean_tangent(mode, xgeom(ctx, s, nullptr, nullptr), s.part_misc, nblk, ctx->stream));
+    }
+    CKS(reduce_to(ctx, s, s.part_misc, nblk, nk, 0));
   }
+  CKS(allreduce(ctx, 0, nk, false));
   double m[64];
-  CKS(read_reduction(ctx, ctx->part_misc, nblk, nk, m));
+  CKS(read_loc(ctx, 0, nk, m));
   for (int k = 0; k < nk; ++k) m[k] /= (double)ctx->N;
   if (ctx->kin == 9) {
     for (int a = 0; a < 9; ++a)
@@ -555,30 +710,48 @@ dbfft_status refresh_mean_tangent(dbfft_ctx ctx) {
   return DBFFT_OK;
 }
 
+// X-pass reductions of every slab into loc[1..9] (sums) and loc[10] (max), all-reduced
+dbfft_status reduce_x(dbfft_ctx ctx, const std::vector<int>& grids, double* host10, bool with_max) {
+  for (size_t k = 0; k < ctx->slabs.size(); ++k) {
+    Slab& s = ctx->slabs[k];
+    CKS(reduce_to(ctx, s, s.part_x, grids[k], 10, 1));
+  }
+  CKS(allreduce(ctx, 1, 9, false));
+  if (with_max) CKS(allreduce(ctx, 10, 1, true));
+  CKS(read_loc(ctx, 1, 10, host10));
+  return DBFFT_OK;
+}
+
 // ---------------------------------------------------------------- PCG
-// Solves A {x | xe} = {b | be} with x0 = 0.  Requires cg->msig0, cg->be, cg->mask, Minv_e set.
-dbfft_status pcg(dbfft_ctx ctx, const dbfft_opts& o, const uint8_t* mask, int* iters_out) {
-  SpecGeom sg = spec(ctx);
+// Solves A {x | xe} = {b | be} with x0 = 0.  Requires CgDev (msig0, be, mask, Minv_e) set.
+// loc layout: [0] <p,q> / <r,z> / <r,r>, [1] <r,r> (CG pairs), [1..9] DC sums, [10] max.
+dbfft_status pcg(dbfft_ctx ctx, const dbfft_opts& o, int* iters_out) {
   const int nb = cg_blocks();
-  CgDev* cg = ctx->cg;
   const bool macro = ctx->h_cg->macro != 0;
-  const double* e_p = macro ? cg->pe : nullptr;
-  (void)mask;
-  CK(cudaMemsetAsync(ctx->x, 0, sizeof(cplx) * 3 * ctx->Hs, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->r, ctx->b, sizeof(cplx) * 3 * ctx->Hs, cudaMemcpyDeviceToDevice, ctx->stream));
-  {
-    ProfScope ps(ctx, PK_CGDIR);
-    CK(launch_cg_init(sg, ctx->prec, ctx->r, ctx->p, ctx->part_cg, nb, ctx->stream));
+  for (Slab& s : ctx->slabs) {
+    CK(cudaMemsetAsync(s.x, 0, sizeof(cplx) * 3 * s.Hs, ctx->stream));
+    CK(cudaMemcpyAsync(s.r, s.b, sizeof(cplx) * 3 * s.Hs, cudaMemcpyDeviceToDevice, ctx->stream));
   }
-  {
-    ProfScope ps(ctx, PK_FIN);
-    CK(launch_fin_init(cg, ctx->part_cg, nb, ctx->stream));
-  }
+  auto init_dir = [&]() -> dbfft_status {
+    for (Slab& s : ctx->slabs) {
+      {
+        ProfScope ps(ctx, PK_CGDIR);
+        CK(launch_cg_init(spec(ctx, s), ctx->prec, s.r, s.p, s.part_cg, nb, ctx->stream));
+      }
+      CKS(reduce_to(ctx, s, s.part_cg, nb, 2, 0));
+    }
+    CKS(allreduce(ctx, 0, 2, false));
+    for (Slab& s : ctx->slabs) {
+      ProfScope ps(ctx, PK_FIN);
+      CK(launch_fin_init(s.cg, s.loc, ctx->stream));
+    }
+    return DBFFT_OK;
+  };
+  CKS(init_dir());
   const int every = std::max(1, o.check_every);
   int restarts = 0;
   for (;;) {
-    // poll
-    CK(cudaMemcpyAsync(ctx->h_cg, cg, sizeof(CgDev), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_cg, ctx->slabs[0].cg, sizeof(CgDev), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     prof_flush(ctx);
     if (ctx->h_cg->breakdown) {
@@ -594,57 +767,67 @@ dbfft_status pcg(dbfft_ctx ctx, const dbfft_opts& o, const uint8_t* mask, int* i
     if (ctx->h_cg->converged == 1) {
       // true-residual confirmation (R7): r = b - A x
       ApplyOut ao;
-      CKS(apply_K_internal(ctx, ctx->x, ctx->q, macro ? cg->xe : nullptr, false, &ao));
-      {
-        ProfScope ps(ctx, PK_CGUPD);
-        CK(launch_true_residual(sg, ctx->b, ctx->q, ctx->r, ctx->part_cg, nb, ctx->stream));
+      CKS(apply_K_slabs(ctx, &Slab::x, &Slab::q, macro, &CgDev::xe, false, &ao));
+      for (size_t k = 0; k < ctx->slabs.size(); ++k) {
+        Slab& s = ctx->slabs[k];
+        {
+          ProfScope ps(ctx, PK_CGUPD);
+          CK(launch_true_residual(spec(ctx, s), s.b, s.q, s.r, s.part_cg, nb, ctx->stream));
+        }
+        CKS(reduce_to(ctx, s, s.part_cg, nb, 1, 0));
+        CKS(reduce_to(ctx, s, s.part_x, ao.grid_x[k], 10, 1));
       }
-      {
+      CKS(allreduce(ctx, 0, 10, false));
+      for (Slab& s : ctx->slabs) {
         ProfScope ps(ctx, PK_FIN);
-        CK(launch_fin_true(cg, ctx->part_cg, nb, ctx->part_x, ao.grid_x, 10, ctx->stream));
+        CK(launch_fin_true(s.cg, s.loc, ctx->stream));
       }
-      CK(cudaMemcpyAsync(ctx->h_cg, cg, sizeof(CgDev), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaMemcpyAsync(ctx->h_cg, ctx->slabs[0].cg, sizeof(CgDev), cudaMemcpyDeviceToHost, ctx->stream));
       CK(cudaStreamSynchronize(ctx->stream));
       if (ctx->h_cg->converged == 1 || restarts > 20) {
         *iters_out = ctx->h_cg->iters;
         return DBFFT_OK;
       }
-      // restart from the true residual: z = M r, p = z
-      ++restarts;
-      {
-        ProfScope ps(ctx, PK_CGDIR);
-        CK(launch_cg_init(sg, ctx->prec, ctx->r, ctx->p, ctx->part_cg, nb, ctx->stream));
-      }
-      {
-        ProfScope ps(ctx, PK_FIN);
-        CK(launch_fin_init(cg, ctx->part_cg, nb, ctx->stream));
-      }
+      ++restarts;  // restart from the true residual: z = M r, p = z
+      CKS(init_dir());
       continue;
     }
     for (int k = 0; k < every; ++k) {
       ApplyOut ao;
-      CKS(apply_K_internal(ctx, ctx->p, ctx->q, e_p, true, &ao));
-      {
-        ProfScope ps(ctx, PK_FIN);
-        CK(launch_fin_alpha(cg, ctx->part_f3, ao.grid_f3, ctx->part_x, ao.grid_x, 10, ctx->stream));
+      CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, macro, &CgDev::pe, true, &ao));
+      for (size_t j = 0; j < ctx->slabs.size(); ++j) {
+        Slab& s = ctx->slabs[j];
+        CKS(reduce_to(ctx, s, s.part_f3, ao.grid_f3[j], 1, 0));
+        CKS(reduce_to(ctx, s, s.part_x, ao.grid_x[j], 10, 1));
       }
-      {
-        ProfScope ps(ctx, PK_CGUPD);
-        CK(launch_cg_update(sg, ctx->prec, cg, ctx->x, ctx->p, ctx->r, ctx->q, ctx->part_cg, nb, ctx->stream));
+      CKS(allreduce(ctx, 0, 10, false));
+      for (Slab& s : ctx->slabs) {
+        {
+          ProfScope ps(ctx, PK_FIN);
+          CK(launch_fin_alpha(s.cg, s.loc, ctx->stream));
+        }
+        {
+          ProfScope ps(ctx, PK_CGUPD);
+          CK(launch_cg_update(spec(ctx, s), ctx->prec, s.cg, s.x, s.p, s.r, s.q, s.part_cg, nb, ctx->stream));
+        }
+        CKS(reduce_to(ctx, s, s.part_cg, nb, 2, 0));
       }
-      {
-        ProfScope ps(ctx, PK_FIN);
-        CK(launch_fin_beta(cg, ctx->part_cg, nb, ctx->stream));
-      }
-      {
-        ProfScope ps(ctx, PK_CGDIR);
-        CK(launch_cg_direction(sg, ctx->prec, cg, ctx->p, ctx->r, ctx->stream));
+      CKS(allreduce(ctx, 0, 2, false));
+      for (Slab& s : ctx->slabs) {
+        {
+          ProfScope ps(ctx, PK_FIN);
+          CK(launch_fin_beta(s.cg, s.loc, ctx->stream));
+        }
+        {
+          ProfScope ps(ctx, PK_CGDIR);
+          CK(launch_cg_direction(spec(ctx, s), ctx->prec, s.cg, s.p, s.r, ctx->stream));
+        }
       }
     }
   }
 }
 
-// set CgDev header fields on the host mirror and upload
+// set CgDev header fields on the host mirror and upload to every slab
 dbfft_status cg_setup(dbfft_ctx ctx, const dbfft_opts& o, const uint8_t* mask, const double* msig0, const double* be) {
   CgDev* h = ctx->h_cg;
   memset(h, 0, sizeof(CgDev));
@@ -665,7 +848,8 @@ dbfft_status cg_setup(dbfft_ctx ctx, const dbfft_opts& o, const uint8_t* mask, c
     ctx->err = "singular macro block (P Cbar P)";
     return DBFFT_E_INVALID_ARG;
   }
-  CK(cudaMemcpyAsync(ctx->cg, h, sizeof(CgDev), cudaMemcpyHostToDevice, ctx->stream));
+  for (Slab& s : ctx->slabs) CK(cudaMemcpyAsync(s.cg, h, sizeof(CgDev), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
   return DBFFT_OK;
 }
 
@@ -685,8 +869,14 @@ dbfft_status check_target(dbfft_ctx ctx, const double* target, const uint8_t* ma
   return DBFFT_OK;
 }
 
-dbfft_status finish_report(dbfft_ctx ctx, dbfft_report* rep, std::chrono::steady_clock::time_point t0) {
-  if (rep) rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+dbfft_status upload_e(dbfft_ctx ctx, const double* host9) {
+  for (Slab& s : ctx->slabs) CK(cudaMemcpyAsync(s.e_dev, host9, sizeof(double) * 9, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));  // host9 may be a stack array
+  return DBFFT_OK;
+}
+
+dbfft_status copy_vec_all(dbfft_ctx ctx, cplx* Slab::*dst, cplx* Slab::*src) {
+  for (Slab& s : ctx->slabs) CK(cudaMemcpyAsync(s.*dst, s.*src, sizeof(cplx) * 3 * s.Hs, cudaMemcpyDeviceToDevice, ctx->stream));
   return DBFFT_OK;
 }
 
@@ -697,22 +887,25 @@ dbfft_status solve_linear(dbfft_ctx ctx, const double* target, const uint8_t* ma
     epsU[a] = mask[a] ? 0.0 : target[a];
     sigf[a] = mask[a] ? target[a] : 0.0;
   }
-  CK(cudaMemcpyAsync(ctx->e_dev, epsU, sizeof(double) * 9, cudaMemcpyHostToDevice, ctx->stream));
+  CKS(upload_e(ctx, epsU));
   // rhs b = d:F(C:eps_U) (P:118 right-hand side, R3) and <C:eps_U>
-  XGeom gx = xgeom(ctx, nullptr, ctx->WB);
-  gx.e = ctx->e_dev;
-  int gridx = 0;
-  CKS(run_x(ctx, X_RHS_SMALL_PHASE, PK_XCONST, gx, &gridx));
-  CKS(forward_tail(ctx, ctx->b));
+  std::vector<int> grids(ctx->slabs.size());
+  for (size_t k = 0; k < ctx->slabs.size(); ++k) {
+    Slab& s = ctx->slabs[k];
+    XGeom gx = xgeom(ctx, s, nullptr, s.WB);
+    gx.e = s.e_dev;
+    CKS(run_x(ctx, X_RHS_SMALL_PHASE, PK_XCONST, gx, &grids[k]));
+  }
+  CKS(forward_tail(ctx));
   double red[10];
-  CKS(read_reduction(ctx, ctx->part_x, gridx, 10, red));
+  CKS(reduce_x(ctx, grids, red, false));
   double msig0[9], be[9];
   for (int a = 0; a < 9; ++a) msig0[a] = red[a] / (double)ctx->N;
   sym_fill(msig0);
   for (int a = 0; a < 9; ++a) be[a] = mask[a] ? sigf[a] - msig0[a] : 0.0;
   CKS(cg_setup(ctx, o, mask, msig0, be));
   int iters = 0;
-  dbfft_status st = pcg(ctx, o, mask, &iters);
+  dbfft_status st = pcg(ctx, o, &iters);
   if (rep) {
     rep->cg_iters = iters;
     rep->newton_iters = 0;
@@ -726,8 +919,8 @@ dbfft_status solve_linear(dbfft_ctx ctx, const double* target, const uint8_t* ma
     }
   }
   if (st != DBFFT_OK) return st;
-  CK(cudaMemcpyAsync(ctx->u, ctx->x, sizeof(cplx) * 3 * ctx->Hs, cudaMemcpyDeviceToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->u_c, ctx->x, sizeof(cplx) * 3 * ctx->Hs, cudaMemcpyDeviceToDevice, ctx->stream));
+  CKS(copy_vec_all(ctx, &Slab::u, &Slab::x));
+  CKS(copy_vec_all(ctx, &Slab::u_c, &Slab::x));
   for (int a = 0; a < 9; ++a) ctx->Fbar[a] = ctx->Fbar_c[a] = epsU[a] + ctx->h_cg->xe[a];
   CK(cudaStreamSynchronize(ctx->stream));
   return DBFFT_OK;
@@ -737,39 +930,50 @@ dbfft_status solve_linear(dbfft_ctx ctx, const double* target, const uint8_t* ma
 // constitutive pass: state += grad(du) + dF ; P, K ; b = F(div P) ; returns <P>, max|d|
 dbfft_status constitutive(dbfft_ctx ctx, bool has_in, const double* dF_host, double dt, double* meanP, double* maxd) {
   const bool fin = ctx->kin == 9;
-  CK(cudaMemcpyAsync(ctx->e_dev, dF_host, sizeof(double) * 9, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemsetAsync(ctx->bad, 0x7f, sizeof(int), ctx->stream));
+  CKS(upload_e(ctx, dF_host));
+  for (Slab& s : ctx->slabs) CK(cudaMemsetAsync(s.bad, 0x7f, sizeof(int), ctx->stream));
   if (has_in) {
-    ColGeom g1 = colgeom(ctx, true, ctx->x, ctx->WA, false, false);
-    CKS(run_col(ctx, fin ? COL_I1F : COL_I1S, PK_I1, g1));
-    ColGeom g2 = colgeom(ctx, false, ctx->WA, ctx->WB, false, true);
-    CKS(run_col(ctx, fin ? COL_I2F : COL_I2S, PK_I2, g2));
+    const int nf1 = nf_I1(ctx);
+    for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_I1F : COL_I1S, PK_I1, geom_I1(ctx, s, s.x, s.WA, nf1), ctx->n3));
+    CKS(exchange(ctx, (long long)nf1 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
+    for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_I2F : COL_I2S, PK_I2, geom_I2(ctx, s, s.WR, s.WB, nf1), ctx->n2));
   }
-  XGeom gx = xgeom(ctx, ctx->WB, ctx->WB);
-  gx.e = ctx->e_dev;
-  gx.has_in = has_in ? 1 : 0;
-  gx.dt = dt;
-  int gridx = 0;
-  CKS(run_x(ctx, fin ? X_CONST_FIN : X_CONST_J2, PK_XCONST, gx, &gridx));
-  CKS(forward_tail(ctx, ctx->b));
+  std::vector<int> grids(ctx->slabs.size());
+  for (size_t k = 0; k < ctx->slabs.size(); ++k) {
+    Slab& s = ctx->slabs[k];
+    XGeom gx = xgeom(ctx, s, s.WB, s.WB);
+    gx.e = s.e_dev;
+    gx.has_in = has_in ? 1 : 0;
+    gx.dt = dt;
+    CKS(run_x(ctx, fin ? X_CONST_FIN : X_CONST_J2, PK_XCONST, gx, &grids[k]));
+  }
+  CKS(forward_tail(ctx));
   double red[10];
-  CKS(read_reduction(ctx, ctx->part_x, gridx, 10, red));
+  CKS(reduce_x(ctx, grids, red, true));
   for (int a = 0; a < 9; ++a) meanP[a] = red[a] / (double)ctx->N;
   if (!fin) sym_fill(meanP);
   *maxd = red[9];
-  CK(cudaMemcpy(ctx->h_bad, ctx->bad, sizeof(int), cudaMemcpyDeviceToHost));
-  if (*ctx->h_bad != 0x7f7f7f7f) {
-    ctx->err = "det F <= 0 at voxel " + std::to_string(*ctx->h_bad);
+  int bad = 0x7f7f7f7f;
+  for (Slab& s : ctx->slabs) {
+    CK(cudaMemcpy(ctx->h_bad, s.bad, sizeof(int), cudaMemcpyDeviceToHost));
+    if (*ctx->h_bad != 0x7f7f7f7f && bad == 0x7f7f7f7f) bad = *ctx->h_bad + (int)(s.z0 * (long long)ctx->n1 * ctx->n2);
+  }
+  if (bad != 0x7f7f7f7f) {
+    *ctx->h_bad = bad;
+    ctx->err = "det F <= 0 at voxel " + std::to_string(bad);
     return DBFFT_E_MATERIAL;
   }
-  ctx->tangent_valid = true;
   return DBFFT_OK;
 }
 
+int state_fields(dbfft_ctx ctx) { return ctx->kin == 9 ? 9 : 6; }
+
 dbfft_status rollback(dbfft_ctx ctx) {
-  const int nf = ctx->kin == 9 ? 9 : 6;
-  CK(cudaMemcpyAsync(ctx->u, ctx->u_c, sizeof(cplx) * 3 * ctx->Hs, cudaMemcpyDeviceToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->F, ctx->F_c, sizeof(double) * nf * ctx->N, cudaMemcpyDeviceToDevice, ctx->stream));
+  const int nf = state_fields(ctx);
+  for (Slab& s : ctx->slabs) {
+    CK(cudaMemcpyAsync(s.u, s.u_c, sizeof(cplx) * 3 * s.Hs, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(s.F, s.F_c, sizeof(double) * nf * s.Nloc, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
   memcpy(ctx->Fbar, ctx->Fbar_c, sizeof(ctx->Fbar));
   CK(cudaStreamSynchronize(ctx->stream));
   return DBFFT_OK;
@@ -778,13 +982,14 @@ dbfft_status rollback(dbfft_ctx ctx) {
 dbfft_status solve_newton(dbfft_ctx ctx, const double* target, const uint8_t* mask, double dt, const dbfft_opts& o,
                           dbfft_report* rep) {
   const bool fin = ctx->kin == 9;
-  const int nf = fin ? 9 : 6;
-  // start from the committed state
-  CK(cudaMemcpyAsync(ctx->u, ctx->u_c, sizeof(cplx) * 3 * ctx->Hs, cudaMemcpyDeviceToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->F, ctx->F_c, sizeof(double) * nf * ctx->N, cudaMemcpyDeviceToDevice, ctx->stream));
+  const int nf = state_fields(ctx);
+  for (Slab& s : ctx->slabs) {  // start from the committed state
+    CK(cudaMemcpyAsync(s.u, s.u_c, sizeof(cplx) * 3 * s.Hs, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(s.F, s.F_c, sizeof(double) * nf * s.Nloc, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
   double Fbar_new[9], dF[9], Pf[9];
   for (int a = 0; a < 9; ++a) {
-    Fbar_new[a] = mask[a] ? ctx->Fbar_c[a] : target[a];   // F^0 = Fbar^{k+1} + grad u^k
+    Fbar_new[a] = mask[a] ? ctx->Fbar_c[a] : target[a];  // F^0 = Fbar^{k+1} + grad u^k
     dF[a] = Fbar_new[a] - ctx->Fbar_c[a];
     Pf[a] = mask[a] ? target[a] : 0.0;
   }
@@ -804,16 +1009,15 @@ dbfft_status solve_newton(dbfft_ctx ctx, const double* target, const uint8_t* ma
     st = cg_setup(ctx, o, mask, meanP, be);
     if (st != DBFFT_OK) break;
     int iters = 0;
-    st = pcg(ctx, o, mask, &iters);
+    st = pcg(ctx, o, &iters);
     total_cg += iters;
     if (st != DBFFT_OK) break;
-    // u += du ; Fbar_f += dF_f
-    {
+    for (Slab& s : ctx->slabs) {  // u += du
       ProfScope ps(ctx, PK_OTHER);
-      CK(launch_axpy(spec(ctx), ctx->u, ctx->x, 1.0, ctx->stream));
+      CK(launch_axpy(spec(ctx, s), s.u, s.x, 1.0, ctx->stream));
     }
     double de[9];
-    for (int a = 0; a < 9; ++a) {
+    for (int a = 0; a < 9; ++a) {  // Fbar_f += dF_f
       de[a] = mask[a] ? ctx->h_cg->xe[a] : 0.0;
       ctx->Fbar[a] += de[a];
     }
@@ -848,42 +1052,130 @@ dbfft_status solve_newton(dbfft_ctx ctx, const double* target, const uint8_t* ma
     rollback(ctx);
     return st;
   }
-  // commit (state accepted)
-  CK(cudaMemcpyAsync(ctx->u_c, ctx->u, sizeof(cplx) * 3 * ctx->Hs, cudaMemcpyDeviceToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->F_c, ctx->F, sizeof(double) * nf * ctx->N, cudaMemcpyDeviceToDevice, ctx->stream));
-  if (!fin) CK(cudaMemcpyAsync(ctx->epsp_c, ctx->epsp_t, sizeof(double) * 6 * ctx->N, cudaMemcpyDeviceToDevice, ctx->stream));
+  for (Slab& s : ctx->slabs) {  // commit (state accepted)
+    CK(cudaMemcpyAsync(s.u_c, s.u, sizeof(cplx) * 3 * s.Hs, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(s.F_c, s.F, sizeof(double) * nf * s.Nloc, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (!fin) CK(cudaMemcpyAsync(s.epsp_c, s.epsp_t, sizeof(double) * 6 * s.Nloc, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
   memcpy(ctx->Fbar_c, ctx->Fbar, sizeof(ctx->Fbar));
   CK(cudaStreamSynchronize(ctx->stream));
   return DBFFT_OK;
 }
 
+void free_slab(Slab& s) {
+  void* ptrs[] = {s.x, s.r, s.p, s.q, s.b, s.u, s.u_c, s.WA, s.WB, s.phase, s.ptable, s.F, s.F_c, s.epsp_c, s.epsp_t, s.tan,
+                  s.cg, s.part_x, s.part_f3, s.part_cg, s.part_misc, s.loc, s.e_dev, s.bad, s.counts, s.tmp_real};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (s.WR && s.WR != s.WA) cudaFree(s.WR);
+}
+
 void free_all(dbfft_ctx ctx) {
-  void* ptrs[] = {ctx->xix, ctx->xiy, ctx->xiz, ctx->tw1, ctx->tw2, ctx->tw3, ctx->x, ctx->r, ctx->p, ctx->q, ctx->b, ctx->u,
-                  ctx->u_c, ctx->WA, ctx->WB, ctx->phase, ctx->ptable, ctx->F, ctx->F_c, ctx->epsp_c, ctx->epsp_t, ctx->tan,
-                  ctx->cg, ctx->part_x, ctx->part_f3, ctx->part_cg, ctx->part_misc, ctx->red_out, ctx->e_dev, ctx->bad,
-                  ctx->counts, ctx->tmp_real};
+  for (Slab& s : ctx->slabs) free_slab(s);
+  void* ptrs[] = {ctx->xix, ctx->xiy, ctx->xiz, ctx->tw1, ctx->tw2, ctx->tw3, ctx->loc_ptrs};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->h_cg) cudaFreeHost(ctx->h_cg);
   if (ctx->h_red) cudaFreeHost(ctx->h_red);
   if (ctx->h_bad) cudaFreeHost(ctx->h_bad);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
 }
 
-dbfft_status free_state(dbfft_ctx ctx) {
-  void** ptrs[] = {(void**)&ctx->F, (void**)&ctx->F_c, (void**)&ctx->epsp_c, (void**)&ctx->epsp_t, (void**)&ctx->tan};
-  for (void** p : ptrs)
+void free_state(Slab& s) {
+  double** ptrs[] = {&s.F, &s.F_c, &s.epsp_c, &s.epsp_t, &s.tan};
+  for (double** p : ptrs)
     if (*p) {
       cudaFree(*p);
       *p = nullptr;
     }
+}
+
+dbfft_status ensure_tmp(dbfft_ctx ctx, Slab& s) {
+  if (!s.tmp_real) CKS(dalloc(ctx, &s.tmp_real, 9 * s.Nloc));
   return DBFFT_OK;
 }
 
-// real-field [9][N] temporary for outputs
-dbfft_status ensure_tmp(dbfft_ctx ctx) {
-  if (!ctx->tmp_real) CKS(dalloc(ctx, &ctx->tmp_real, 9 * ctx->N));
+// Real fields: the loopback API exposes global [c][z][y][x] arrays; with NCCL each rank passes
+// its own z-slab [c][zl][y][x].
+dbfft_status scatter_real(dbfft_ctx ctx, const double* src, int on_device, int ncomp, const int* comp_map, double* Slab::*dst) {
+  const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  const long long plane = (long long)ctx->n1 * ctx->n2;
+  const long long Nsrc = ctx->loopback ? ctx->N : ctx->slabs[0].Nloc;
+  for (Slab& s : ctx->slabs) {
+    const long long off = ctx->loopback ? (long long)s.z0 * plane : 0;
+    for (int c = 0; c < ncomp; ++c) {
+      const int sc = comp_map ? comp_map[c] : c;
+      CK(cudaMemcpyAsync(s.*dst + (long long)c * s.Nloc, src + (long long)sc * Nsrc + off, sizeof(double) * s.Nloc, kind, ctx->stream));
+    }
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return DBFFT_OK;
+}
+
+dbfft_status gather_real(dbfft_ctx ctx, double* Slab::*srcm, int ncomp, double* out, int out_on_device) {
+  const cudaMemcpyKind kind = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  const long long plane = (long long)ctx->n1 * ctx->n2;
+  const long long Ndst = ctx->loopback ? ctx->N : ctx->slabs[0].Nloc;
+  for (Slab& s : ctx->slabs) {
+    const long long off = ctx->loopback ? (long long)s.z0 * plane : 0;
+    for (int c = 0; c < ncomp; ++c)
+      CK(cudaMemcpyAsync(out + (long long)c * Ndst + off, s.*srcm + (long long)c * s.Nloc, sizeof(double) * s.Nloc, kind, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return DBFFT_OK;
+}
+
+// spectral vectors [3][ky][kz][kx]: loopback API vectors are global, slabs own ky ranges
+dbfft_status spec_in(dbfft_ctx ctx, const cplx* src, cplx* Slab::*dst) {
+  const long long Hs_glob = (long long)ctx->n1h * ctx->n2 * ctx->n3;
+  for (Slab& s : ctx->slabs) {
+    if (!ctx->loopback) {
+      CK(cudaMemcpyAsync(s.*dst, src, sizeof(cplx) * 3 * s.Hs, cudaMemcpyDeviceToDevice, ctx->stream));
+      continue;
+    }
+    for (int c = 0; c < 3; ++c)
+      CK(cudaMemcpyAsync(s.*dst + c * s.Hs, src + c * Hs_glob + (long long)s.ky0 * ctx->n3 * ctx->n1h, sizeof(cplx) * s.Hs,
+                         cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  return DBFFT_OK;
+}
+dbfft_status spec_out(dbfft_ctx ctx, cplx* Slab::*srcm, cplx* dst, cudaMemcpyKind kind) {
+  const long long Hs_glob = (long long)ctx->n1h * ctx->n2 * ctx->n3;
+  for (Slab& s : ctx->slabs) {
+    if (!ctx->loopback) {
+      CK(cudaMemcpyAsync(dst, s.*srcm, sizeof(cplx) * 3 * s.Hs, kind, ctx->stream));
+      continue;
+    }
+    for (int c = 0; c < 3; ++c)
+      CK(cudaMemcpyAsync(dst + c * Hs_glob + (long long)s.ky0 * ctx->n3 * ctx->n1h, s.*srcm + c * s.Hs, sizeof(cplx) * s.Hs, kind,
+                         ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return DBFFT_OK;
+}
+
+dbfft_status alloc_slab(dbfft_ctx ctx, Slab& s) {
+  const size_t v3 = 3 * s.Hs;
+  cplx** vecs[] = {&s.x, &s.r, &s.p, &s.q, &s.b, &s.u, &s.u_c};
+  for (cplx** v : vecs) CKS(dalloc(ctx, v, v3));
+  CK(cudaMemset(s.u, 0, sizeof(cplx) * v3));
+  CK(cudaMemset(s.u_c, 0, sizeof(cplx) * v3));
+  CKS(dalloc(ctx, &s.WA, (size_t)6 * s.Hs));
+  if (ctx->P > 1) CKS(dalloc(ctx, &s.WR, (size_t)6 * s.Hs));
+  else s.WR = s.WA;
+  CKS(dalloc(ctx, &s.WB, (size_t)ctx->kin * s.Hs));
+  CKS(dalloc(ctx, &s.cg, 1));
+  int gx = 0;
+  for (int k = 0; k < X_REAL_OUT; ++k) gx = std::max(gx, x_grid(k, ctx->n1, s.nlines));
+  CKS(dalloc(ctx, &s.part_x, (size_t)gx * 10));
+  CKS(dalloc(ctx, &s.part_f3, (size_t)col_grid(ctx->n3, (long long)s.nyl * ctx->n1h)));
+  CKS(dalloc(ctx, &s.part_cg, (size_t)cg_blocks() * 2));
+  CKS(dalloc(ctx, &s.part_misc, (size_t)cg_blocks() * 45));
+  CKS(dalloc(ctx, &s.loc, 64));
+  CKS(dalloc(ctx, &s.e_dev, 9));
+  CKS(dalloc(ctx, &s.bad, 1));
   return DBFFT_OK;
 }
 
@@ -908,6 +1200,22 @@ dbfft_opts dbfft_default_opts(void) {
 
 const char* dbfft_last_error(dbfft_ctx ctx) { return ctx ? ctx->err.c_str() : g_create_error.c_str(); }
 
+dbfft_status dbfft_nccl_unique_id(void* out128) {
+  if (!out128) return DBFFT_E_INVALID_ARG;
+  std::string err;
+  if (!nccl_load(&err)) {
+    g_create_error = err;
+    return DBFFT_E_NCCL;
+  }
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) {
+    g_create_error = "ncclGetUniqueId failed";
+    return DBFFT_E_NCCL;
+  }
+  memcpy(out128, &id, sizeof(id));
+  return DBFFT_OK;
+}
+
 dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinematics, const dbfft_env* env, dbfft_ctx* out) {
   if (!n || !L || !out) {
     g_create_error = "null argument";
@@ -923,8 +1231,15 @@ dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinemat
     g_create_error = "kinematics must be 6 (small strain) or 9 (finite strain)";
     return DBFFT_E_INVALID_ARG;
   }
-  if (env && env->world != 1) {
-    g_create_error = "world > 1 not supported in this build (slab decomposition reserved)";
+  const int P = env ? std::max(1, env->world) : 1;
+  const int rank = env ? env->rank : 0;
+  const int loopback = env ? env->loopback : 0;
+  if ((P & (P - 1)) != 0 || n[1] % P != 0 || n[2] % P != 0 || rank < 0 || rank >= P) {
+    g_create_error = "world must be a power of two dividing n2 and n3 (S:48), 0 <= rank < world";
+    return DBFFT_E_INVALID_GRID;
+  }
+  if (P > 1 && !loopback && !env->nccl_id) {
+    g_create_error = "world > 1 needs env->nccl_id (dbfft_nccl_unique_id on rank 0, broadcast) or env->loopback";
     return DBFFT_E_INVALID_ARG;
   }
   dbfft_ctx ctx = new dbfft_ctx_s();
@@ -935,7 +1250,9 @@ dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinemat
   for (int a = 0; a < 3; ++a) ctx->L[a] = L[a];
   ctx->kin = kinematics;
   ctx->N = (long long)n[0] * n[1] * n[2];
-  ctx->Hs = (long long)ctx->n1h * n[1] * n[2];
+  ctx->P = P;
+  ctx->loopback = (P > 1 && loopback) ? 1 : 0;
+  ctx->rank = ctx->loopback ? 0 : rank;
   memset(ctx->prof_ms, 0, sizeof(ctx->prof_ms));
   memset(ctx->prof_n, 0, sizeof(ctx->prof_n));
   for (int a = 0; a < 9; ++a) ctx->Fbar[a] = ctx->Fbar_c[a] = 0.0;
@@ -964,7 +1281,6 @@ dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinemat
     ctx->own_stream = true;
   }
   dbfft_status s;
-  // frequency tables and twiddles
   std::vector<double> hx = axis_xi(ctx->n1, L[0], ctx->n1h), hy = axis_xi(ctx->n2, L[1], ctx->n2), hz = axis_xi(ctx->n3, L[2], ctx->n3);
   if ((s = dalloc(ctx, &ctx->xix, hx.size())) != DBFFT_OK) return fail(s);
   if ((s = dalloc(ctx, &ctx->xiy, hy.size())) != DBFFT_OK) return fail(s);
@@ -975,28 +1291,36 @@ dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinemat
   if ((s = make_twiddles(ctx, ctx->n1, &ctx->tw1)) != DBFFT_OK) return fail(s);
   if ((s = make_twiddles(ctx, ctx->n2, &ctx->tw2)) != DBFFT_OK) return fail(s);
   if ((s = make_twiddles(ctx, ctx->n3, &ctx->tw3)) != DBFFT_OK) return fail(s);
-  const size_t v3 = 3 * ctx->Hs;
-  cplx** vecs[] = {&ctx->x, &ctx->r, &ctx->p, &ctx->q, &ctx->b, &ctx->u, &ctx->u_c};
-  for (cplx** v : vecs)
-    if ((s = dalloc(ctx, v, v3)) != DBFFT_OK) return fail(s);
-  const int c = kinematics;
-  if ((s = dalloc(ctx, &ctx->WA, (size_t)6 * ctx->Hs)) != DBFFT_OK) return fail(s);
-  if ((s = dalloc(ctx, &ctx->WB, (size_t)c * ctx->Hs)) != DBFFT_OK) return fail(s);
-  cudaMemset(ctx->u, 0, sizeof(cplx) * v3);
-  cudaMemset(ctx->u_c, 0, sizeof(cplx) * v3);
-  if ((s = dalloc(ctx, &ctx->cg, 1)) != DBFFT_OK) return fail(s);
-  // partial buffers
-  const long long nlines = (long long)ctx->n2 * ctx->n3;
-  int gx = 0;
-  for (int k = 0; k < X_REAL_OUT; ++k) gx = std::max(gx, x_grid(k, ctx->n1, nlines));
-  if ((s = dalloc(ctx, &ctx->part_x, (size_t)gx * 10)) != DBFFT_OK) return fail(s);
-  const int gf3 = col_grid(ctx->n3, (long long)ctx->n2 * ctx->n1h);
-  if ((s = dalloc(ctx, &ctx->part_f3, (size_t)gf3)) != DBFFT_OK) return fail(s);
-  if ((s = dalloc(ctx, &ctx->part_cg, (size_t)cg_blocks() * 2)) != DBFFT_OK) return fail(s);
-  if ((s = dalloc(ctx, &ctx->part_misc, (size_t)cg_blocks() * 45)) != DBFFT_OK) return fail(s);
-  if ((s = dalloc(ctx, &ctx->red_out, 64)) != DBFFT_OK) return fail(s);
-  if ((s = dalloc(ctx, &ctx->e_dev, 9)) != DBFFT_OK) return fail(s);
-  if ((s = dalloc(ctx, &ctx->bad, 1)) != DBFFT_OK) return fail(s);
+  // slabs: loopback holds all P virtual ranks, NCCL mode holds this rank's slab
+  const int nslab = ctx->loopback ? P : 1;
+  ctx->slabs.resize(nslab);
+  for (int k = 0; k < nslab; ++k) {
+    Slab& sl = ctx->slabs[k];
+    sl.rank = ctx->loopback ? k : rank;
+    sl.nyl = n[1] / P;
+    sl.nzl = n[2] / P;
+    sl.ky0 = sl.rank * sl.nyl;
+    sl.z0 = sl.rank * sl.nzl;
+    sl.Hs = (long long)ctx->n1h * sl.nyl * n[2];
+    sl.Nloc = (long long)n[0] * n[1] * sl.nzl;
+    sl.nlines = (long long)n[1] * sl.nzl;
+    sl.xiy = ctx->xiy + sl.ky0;
+    if ((s = alloc_slab(ctx, sl)) != DBFFT_OK) return fail(s);
+  }
+  if (ctx->loopback && (s = dalloc(ctx, &ctx->loc_ptrs, P)) != DBFFT_OK) return fail(s);
+  if (P > 1 && !ctx->loopback) {
+    std::string err;
+    if (!nccl_load(&err)) {
+      ctx->err = err;
+      return fail(DBFFT_E_NCCL);
+    }
+    ncclUniqueId id;
+    memcpy(&id, env->nccl_id, sizeof(id));
+    if (g_nccl.CommInitRank(&ctx->comm, P, id, rank) != ncclSuccess) {
+      ctx->err = "ncclCommInitRank failed";
+      return fail(DBFFT_E_NCCL);
+    }
+  }
   if (cudaMallocHost(&ctx->h_cg, sizeof(CgDev)) != cudaSuccess || cudaMallocHost(&ctx->h_red, 64 * sizeof(double)) != cudaSuccess ||
       cudaMallocHost(&ctx->h_bad, sizeof(int)) != cudaSuccess) {
     ctx->err = "cudaMallocHost failed";
@@ -1022,14 +1346,15 @@ dbfft_status dbfft_destroy(dbfft_ctx ctx) {
 
 dbfft_status dbfft_spectral_layout(dbfft_ctx ctx, int64_t shape[4], int64_t strides[4]) {
   if (!ctx || !shape || !strides) return DBFFT_E_INVALID_ARG;
+  const int nyl = ctx->loopback ? ctx->n2 : ctx->slabs[0].nyl;  // loopback API vectors are global
   shape[0] = 3;
-  shape[1] = ctx->n2;
+  shape[1] = nyl;
   shape[2] = ctx->n3;
   shape[3] = ctx->n1h;
   strides[3] = 1;
   strides[2] = ctx->n1h;
   strides[1] = (int64_t)ctx->n3 * ctx->n1h;
-  strides[0] = ctx->Hs;
+  strides[0] = (int64_t)nyl * ctx->n3 * ctx->n1h;
   return DBFFT_OK;
 }
 
@@ -1056,7 +1381,7 @@ dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t o
         f = FAM_LINEAR;
         break;
       case DBFFT_MAT_NEOHOOKE:
-        if (!(m.p[0] > 0) || !(m.p[1] > 2.0 * m.p[0] / 3.0 - 1e300)) { ctx->err = "NEOHOOKE: need mu > 0"; return DBFFT_E_INVALID_ARG; }
+        if (!(m.p[0] > 0)) { ctx->err = "NEOHOOKE: need mu > 0"; return DBFFT_E_INVALID_ARG; }
         d[0] = m.p[0];
         d[1] = m.p[1];
         f = FAM_NEOHOOKE;
@@ -1084,41 +1409,54 @@ dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t o
     return DBFFT_E_INVALID_ARG;
   }
   dbfft_status s;
-  if (!ctx->phase && (s = dalloc(ctx, &ctx->phase, ctx->N)) != DBFFT_OK) return s;
-  CK(cudaMemcpyAsync(ctx->phase, phase_id, sizeof(uint16_t) * ctx->N, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                     ctx->stream));
-  if (ctx->ptable) cudaFree(ctx->ptable);
-  ctx->ptable = nullptr;
-  if ((s = dalloc(ctx, &ctx->ptable, pt.size())) != DBFFT_OK) return s;
-  CK(cudaMemcpyAsync(ctx->ptable, pt.data(), sizeof(double) * pt.size(), cudaMemcpyHostToDevice, ctx->stream));
+  const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  const long long plane = (long long)ctx->n1 * ctx->n2;
+  for (Slab& sl : ctx->slabs) {
+    if (!sl.phase && (s = dalloc(ctx, &sl.phase, sl.Nloc)) != DBFFT_OK) return s;
+    const long long off = ctx->loopback ? (long long)sl.z0 * plane : 0;
+    CK(cudaMemcpyAsync(sl.phase, phase_id + off, sizeof(uint16_t) * sl.Nloc, kind, ctx->stream));
+    if (sl.ptable) cudaFree(sl.ptable);
+    sl.ptable = nullptr;
+    if ((s = dalloc(ctx, &sl.ptable, pt.size())) != DBFFT_OK) return s;
+    CK(cudaMemcpyAsync(sl.ptable, pt.data(), sizeof(double) * pt.size(), cudaMemcpyHostToDevice, ctx->stream));
+    if (sl.counts) cudaFree(sl.counts);
+    sl.counts = nullptr;
+    if ((s = dalloc(ctx, &sl.counts, n_phases)) != DBFFT_OK) return s;
+    CK(cudaMemsetAsync(sl.counts, 0, sizeof(double) * n_phases, ctx->stream));
+    CK(cudaMemsetAsync(sl.bad, 0, sizeof(int), ctx->stream));
+    CK(launch_phase_hist(sl.phase, sl.Nloc, sl.counts, n_phases, sl.bad, ctx->stream));
+  }
+  for (Slab& sl : ctx->slabs) {
+    CK(cudaMemcpyAsync(ctx->h_bad, sl.bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (*ctx->h_bad) {
+      ctx->err = "phase id >= n_phases";
+      return DBFFT_E_INVALID_ARG;
+    }
+  }
+  // phase counts (for the linear mean stiffness) summed over ranks
+  if (ctx->P > 1 && !ctx->loopback)
+    CKN(g_nccl.AllReduce(ctx->slabs[0].counts, ctx->slabs[0].counts, n_phases, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
+  std::vector<double> cnt(n_phases, 0.0);
+  for (Slab& sl : ctx->slabs) {
+    std::vector<double> c(n_phases);
+    CK(cudaMemcpyAsync(c.data(), sl.counts, sizeof(double) * n_phases, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int k = 0; k < n_phases; ++k) cnt[k] += c[k];
+  }
   ctx->h_ptable = pt;
   ctx->nph = n_phases;
-  // validate ids and count phases (for the linear mean stiffness)
-  if (ctx->counts) cudaFree(ctx->counts);
-  ctx->counts = nullptr;
-  if ((s = dalloc(ctx, &ctx->counts, n_phases)) != DBFFT_OK) return s;
-  CK(cudaMemsetAsync(ctx->counts, 0, sizeof(unsigned long long) * n_phases, ctx->stream));
-  CK(cudaMemsetAsync(ctx->bad, 0, sizeof(int), ctx->stream));
-  CK(launch_phase_hist(ctx->phase, ctx->N, ctx->counts, n_phases, ctx->bad, ctx->stream));
-  std::vector<unsigned long long> cnt(n_phases);
-  CK(cudaMemcpyAsync(cnt.data(), ctx->counts, sizeof(unsigned long long) * n_phases, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->h_bad, ctx->bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  if (*ctx->h_bad) {
-    ctx->err = "phase id >= n_phases";
-    return DBFFT_E_INVALID_ARG;
-  }
   ctx->family = fam;
-  // state
-  free_state(ctx);
-  CK(cudaMemsetAsync(ctx->u, 0, sizeof(cplx) * 3 * ctx->Hs, ctx->stream));
-  CK(cudaMemsetAsync(ctx->u_c, 0, sizeof(cplx) * 3 * ctx->Hs, ctx->stream));
+  for (Slab& sl : ctx->slabs) {
+    free_state(sl);
+    CK(cudaMemsetAsync(sl.u, 0, sizeof(cplx) * 3 * sl.Hs, ctx->stream));
+    CK(cudaMemsetAsync(sl.u_c, 0, sizeof(cplx) * 3 * sl.Hs, ctx->stream));
+  }
   for (int a = 0; a < 9; ++a) ctx->Fbar[a] = ctx->Fbar_c[a] = (fam == FAM_NEOHOOKE && a % 4 == 0) ? 1.0 : 0.0;
-  ctx->tangent_valid = false;
   if (fam == FAM_LINEAR) {
     double CV[36] = {0};
     for (int k = 0; k < n_phases; ++k)
-      for (int a = 0; a < 36; ++a) CV[a] += (double)cnt[k] * pt[36 * k + a];
+      for (int a = 0; a < 36; ++a) CV[a] += cnt[k] * pt[36 * k + a];
     for (int a = 0; a < 36; ++a) CV[a] /= (double)ctx->N;
     voigt_to_full(CV, ctx->Cbar);
     ctx->prec = make_prec(ctx->Cbar);
@@ -1128,19 +1466,22 @@ dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t o
     const char* tm = getenv("DBFFT_TANGENT");
     ctx->tmode = (tm && strcmp(tm, "full") == 0) ? 0 : 1;
     const int nk = fam == FAM_NEOHOOKE ? (ctx->tmode ? 10 : 45) : 8;
-    if ((s = dalloc(ctx, &ctx->F, (size_t)nf * ctx->N)) != DBFFT_OK) return s;
-    if ((s = dalloc(ctx, &ctx->F_c, (size_t)nf * ctx->N)) != DBFFT_OK) return s;
-    if ((s = dalloc(ctx, &ctx->tan, (size_t)nk * ctx->N)) != DBFFT_OK) return s;
-    if (fam == FAM_NEOHOOKE) {
-      k_identity9<<<1024, 256, 0, ctx->stream>>>(ctx->F_c, ctx->N);
-    } else {
-      CK(cudaMemsetAsync(ctx->F_c, 0, sizeof(double) * nf * ctx->N, ctx->stream));
-      if ((s = dalloc(ctx, &ctx->epsp_c, (size_t)6 * ctx->N)) != DBFFT_OK) return s;
-      if ((s = dalloc(ctx, &ctx->epsp_t, (size_t)6 * ctx->N)) != DBFFT_OK) return s;
-      CK(cudaMemsetAsync(ctx->epsp_c, 0, sizeof(double) * 6 * ctx->N, ctx->stream));
-      CK(cudaMemsetAsync(ctx->epsp_t, 0, sizeof(double) * 6 * ctx->N, ctx->stream));
+    for (Slab& sl : ctx->slabs) {
+      if ((s = dalloc(ctx, &sl.F, (size_t)nf * sl.Nloc)) != DBFFT_OK) return s;
+      if ((s = dalloc(ctx, &sl.F_c, (size_t)nf * sl.Nloc)) != DBFFT_OK) return s;
+      if ((s = dalloc(ctx, &sl.tan, (size_t)nk * sl.Nloc)) != DBFFT_OK) return s;
+      if (fam == FAM_NEOHOOKE) {
+        k_identity9<<<1024, 256, 0, ctx->stream>>>(sl.F_c, sl.Nloc);
+        CK(cudaGetLastError());
+      } else {
+        CK(cudaMemsetAsync(sl.F_c, 0, sizeof(double) * nf * sl.Nloc, ctx->stream));
+        if ((s = dalloc(ctx, &sl.epsp_c, (size_t)6 * sl.Nloc)) != DBFFT_OK) return s;
+        if ((s = dalloc(ctx, &sl.epsp_t, (size_t)6 * sl.Nloc)) != DBFFT_OK) return s;
+        CK(cudaMemsetAsync(sl.epsp_c, 0, sizeof(double) * 6 * sl.Nloc, ctx->stream));
+        CK(cudaMemsetAsync(sl.epsp_t, 0, sizeof(double) * 6 * sl.Nloc, ctx->stream));
+      }
+      CK(cudaMemcpyAsync(sl.F, sl.F_c, sizeof(double) * nf * sl.Nloc, cudaMemcpyDeviceToDevice, ctx->stream));
     }
-    CK(cudaMemcpyAsync(ctx->F, ctx->F_c, sizeof(double) * nf * ctx->N, cudaMemcpyDeviceToDevice, ctx->stream));
     // tangent at the undeformed state (so apply_K / precond are usable before a solve)
     double zero[9] = {0}, mp[9], mx;
     s = constitutive(ctx, false, zero, 1.0, mp, &mx);
@@ -1162,7 +1503,20 @@ dbfft_status dbfft_apply_K(dbfft_ctx ctx, const void* u_hat, void* f_hat) {
     ctx->err = "apply_K before set_phases";
     return DBFFT_E_STATE;
   }
-  return apply_K_internal(ctx, (const cplx*)u_hat, (cplx*)f_hat, nullptr, false, nullptr);
+  if (!ctx->loopback) {  // zero-copy on the caller's vectors
+    Slab& s = ctx->slabs[0];
+    cplx* su = s.p;
+    cplx* sf = s.q;
+    s.p = (cplx*)u_hat;
+    s.q = (cplx*)f_hat;
+    dbfft_status st = apply_K_slabs(ctx, &Slab::p, &Slab::q, false, &CgDev::pe, false, nullptr);
+    s.p = su;
+    s.q = sf;
+    return st;
+  }
+  CKS(spec_in(ctx, (const cplx*)u_hat, &Slab::p));
+  CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, false, &CgDev::pe, false, nullptr));
+  return spec_out(ctx, &Slab::q, (cplx*)f_hat, cudaMemcpyDeviceToDevice);
 }
 
 dbfft_status dbfft_apply_K_aug(dbfft_ctx ctx, const uint8_t mask[9], const void* u_hat, const double e_in[9], void* f_hat, double r_out[9]) {
@@ -1177,15 +1531,18 @@ dbfft_status dbfft_apply_K_aug(dbfft_ctx ctx, const uint8_t mask[9], const void*
   }
   double e[9];
   for (int a = 0; a < 9; ++a) e[a] = mask[a] ? e_in[a] : 0.0;
-  CK(cudaMemcpyAsync(ctx->e_dev, e, sizeof(e), cudaMemcpyHostToDevice, ctx->stream));
+  // the macro block travels in CgDev::pe of every slab
+  for (Slab& s : ctx->slabs) CK(cudaMemcpyAsync(&s.cg->pe, e, sizeof(e), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  CKS(spec_in(ctx, (const cplx*)u_hat, &Slab::p));
   ApplyOut ao;
-  CKS(apply_K_internal(ctx, (const cplx*)u_hat, (cplx*)f_hat, ctx->e_dev, false, &ao));
+  CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, true, &CgDev::pe, false, &ao));
   double red[10];
-  CKS(read_reduction(ctx, ctx->part_x, ao.grid_x, 10, red));
+  CKS(reduce_x(ctx, ao.grid_x, red, false));
   for (int a = 0; a < 9; ++a) red[a] /= (double)ctx->N;
   if (ctx->kin == 6) sym_fill(red);
   for (int a = 0; a < 9; ++a) r_out[a] = mask[a] ? red[a] : 0.0;
-  return DBFFT_OK;
+  return spec_out(ctx, &Slab::q, (cplx*)f_hat, cudaMemcpyDeviceToDevice);
 }
 
 dbfft_status dbfft_precond(dbfft_ctx ctx, const void* r_hat, void* z_hat) {
@@ -1198,9 +1555,12 @@ dbfft_status dbfft_precond(dbfft_ctx ctx, const void* r_hat, void* z_hat) {
     ctx->err = "precond before set_phases";
     return DBFFT_E_STATE;
   }
-  ProfScope ps(ctx, PK_OTHER);
-  CK(launch_precond(spec(ctx), ctx->prec, (const cplx*)r_hat, (cplx*)z_hat, ctx->stream));
-  return DBFFT_OK;
+  CKS(spec_in(ctx, (const cplx*)r_hat, &Slab::r));
+  for (Slab& s : ctx->slabs) {
+    ProfScope ps(ctx, PK_OTHER);
+    CK(launch_precond(spec(ctx, s), ctx->prec, s.r, s.q, ctx->stream));
+  }
+  return spec_out(ctx, &Slab::q, (cplx*)z_hat, cudaMemcpyDeviceToDevice);
 }
 
 dbfft_status dbfft_eval_state(dbfft_ctx ctx, const double* field, int32_t on_device, double dt) {
@@ -1214,13 +1574,11 @@ dbfft_status dbfft_eval_state(dbfft_ctx ctx, const double* field, int32_t on_dev
     ctx->err = "eval_state: null field";
     return DBFFT_E_INVALID_ARG;
   }
-  const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   if (ctx->family == FAM_NEOHOOKE) {
-    CK(cudaMemcpyAsync(ctx->F, field, sizeof(double) * 9 * ctx->N, kind, ctx->stream));
+    CKS(scatter_real(ctx, field, on_device, 9, nullptr, &Slab::F));
   } else {
     const int rowv[6] = {0, 4, 8, 5, 2, 1};
-    for (int I = 0; I < 6; ++I)
-      CK(cudaMemcpyAsync(ctx->F + (size_t)I * ctx->N, field + (size_t)rowv[I] * ctx->N, sizeof(double) * ctx->N, kind, ctx->stream));
+    CKS(scatter_real(ctx, field, on_device, 6, rowv, &Slab::F));
   }
   double zero[9] = {0}, mp[9], mx;
   CKS(constitutive(ctx, false, zero, dt, mp, &mx));
@@ -1244,8 +1602,10 @@ dbfft_status dbfft_solve_increment(dbfft_ctx ctx, const double target[9], const 
   }
   dbfft_status st = (ctx->family == FAM_LINEAR) ? solve_linear(ctx, target, mask, o, report) : solve_newton(ctx, target, mask, dt, o, report);
   prof_flush(ctx);
-  if (report) report->status = st;
-  finish_report(ctx, report, t0);
+  if (report) {
+    report->status = st;
+    report->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
   return st;
 }
 
@@ -1260,82 +1620,65 @@ dbfft_status dbfft_get_field(dbfft_ctx ctx, int32_t which, void* out, int32_t ou
     return DBFFT_E_STATE;
   }
   const cudaMemcpyKind k = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-  const long long N = ctx->N;
-  CKS(ensure_tmp(ctx));
+  for (Slab& s : ctx->slabs) CKS(ensure_tmp(ctx, s));
   switch (which) {
     case DBFFT_FIELD_U_HAT:
-      CK(cudaMemcpyAsync(out, ctx->u_c, sizeof(cplx) * 3 * ctx->Hs, k, ctx->stream));
-      break;
+      return spec_out(ctx, &Slab::u_c, (cplx*)out, k);
     case DBFFT_FIELD_U: {
-      ColGeom g1 = colgeom(ctx, true, ctx->u_c, ctx->WA, false, false);
-      CKS(run_col(ctx, COL_ZI3, PK_OTHER, g1));
-      ColGeom g2 = colgeom(ctx, false, ctx->WA, ctx->WB, false, true);
-      CKS(run_col(ctx, COL_YI3, PK_OTHER, g2));
-      XGeom gx = xgeom(ctx, ctx->WB, nullptr);
-      gx.real_out = ctx->tmp_real;
-      CKS(run_x(ctx, X_REAL_OUT + 3, PK_OTHER, gx, nullptr));
-      CK(cudaMemcpyAsync(out, ctx->tmp_real, sizeof(double) * 3 * N, k, ctx->stream));
-      break;
+      for (Slab& s : ctx->slabs) CKS(run_col(ctx, COL_ZI3, PK_OTHER, geom_I1(ctx, s, s.u_c, s.WA, 3), ctx->n3));
+      CKS(exchange(ctx, (long long)3 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
+      for (Slab& s : ctx->slabs) {
+        CKS(run_col(ctx, COL_YI3, PK_OTHER, geom_I2(ctx, s, s.WR, s.WB, 3), ctx->n2));
+        XGeom gx = xgeom(ctx, s, s.WB, nullptr);
+        gx.real_out = s.tmp_real;
+        CKS(run_x(ctx, X_REAL_OUT + 3, PK_OTHER, gx, nullptr));
+      }
+      return gather_real(ctx, &Slab::tmp_real, 3, (double*)out, out_on_device);
     }
     case DBFFT_FIELD_STRAIN:
     case DBFFT_FIELD_STRESS: {
-      double* strain9 = ctx->tmp_real;
-      double* dst = (which == DBFFT_FIELD_STRAIN) ? strain9 : nullptr;
-      double* tmp6 = nullptr;
       if (ctx->family == FAM_NEOHOOKE) {
-        if (which == DBFFT_FIELD_STRAIN) {
-          CK(cudaMemcpyAsync(out, ctx->F_c, sizeof(double) * 9 * N, k, ctx->stream));
-        } else {
-          k_stress_nh<<<1024, 256, 0, ctx->stream>>>(ctx->F_c, ctx->phase, ctx->ptable, N, ctx->tmp_real);
+        if (which == DBFFT_FIELD_STRAIN) return gather_real(ctx, &Slab::F_c, 9, (double*)out, out_on_device);
+        for (Slab& s : ctx->slabs) {
+          ProfScope ps(ctx, PK_OTHER);
+          k_stress_nh<<<1024, 256, 0, ctx->stream>>>(s.F_c, s.phase, s.ptable, s.Nloc, s.tmp_real);
           CK(cudaGetLastError());
-          CK(cudaMemcpyAsync(out, ctx->tmp_real, sizeof(double) * 9 * N, k, ctx->stream));
         }
-        break;
+        return gather_real(ctx, &Slab::tmp_real, 9, (double*)out, out_on_device);
       }
       if (ctx->family == FAM_J2) {
-        if (which == DBFFT_FIELD_STRAIN) {
-          k_expand6<<<1024, 256, 0, ctx->stream>>>(ctx->F_c, N, nullptr, ctx->tmp_real);
-        } else {
-          k_stress_j2<<<1024, 256, 0, ctx->stream>>>(ctx->F_c, ctx->epsp_c, ctx->phase, ctx->ptable, N, ctx->tmp_real);
+        for (Slab& s : ctx->slabs) {
+          ProfScope ps(ctx, PK_OTHER);
+          if (which == DBFFT_FIELD_STRAIN) k_expand6<<<1024, 256, 0, ctx->stream>>>(s.F_c, s.Nloc, nullptr, s.tmp_real);
+          else k_stress_j2<<<1024, 256, 0, ctx->stream>>>(s.F_c, s.epsp_c, s.phase, s.ptable, s.Nloc, s.tmp_real);
+          CK(cudaGetLastError());
         }
-        CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(out, ctx->tmp_real, sizeof(double) * 9 * N, k, ctx->stream));
-        break;
+        return gather_real(ctx, &Slab::tmp_real, 9, (double*)out, out_on_device);
       }
       // linear: eps = Ebar + sym grad u (Voigt 6 via the inverse passes), sigma = C:eps
-      CKS(dalloc(ctx, &tmp6, 6 * N));
-      ColGeom g1 = colgeom(ctx, true, ctx->u_c, ctx->WA, false, false);
-      CKS(run_col(ctx, COL_I1S, PK_OTHER, g1));
-      ColGeom g2 = colgeom(ctx, false, ctx->WA, ctx->WB, false, true);
-      CKS(run_col(ctx, COL_I2S, PK_OTHER, g2));
-      XGeom gx = xgeom(ctx, ctx->WB, nullptr);
-      gx.real_out = tmp6;
-      CKS(run_x(ctx, X_REAL_OUT + 6, PK_OTHER, gx, nullptr));
-      CK(cudaMemcpyAsync(ctx->e_dev, ctx->Fbar_c, sizeof(double) * 9, cudaMemcpyHostToDevice, ctx->stream));
-      k_expand6<<<1024, 256, 0, ctx->stream>>>(tmp6, N, ctx->e_dev, strain9);
-      CK(cudaGetLastError());
-      (void)dst;
-      CK(cudaStreamSynchronize(ctx->stream));
-      cudaFree(tmp6);
-      if (which == DBFFT_FIELD_STRAIN) {
-        CK(cudaMemcpyAsync(out, strain9, sizeof(double) * 9 * N, k, ctx->stream));
-      } else {
-        double* sig = nullptr;
-        CKS(dalloc(ctx, &sig, 9 * N));
-        k_stress_linear<<<1024, 256, 0, ctx->stream>>>(strain9, ctx->phase, ctx->ptable, N, sig);
+      CKS(upload_e(ctx, ctx->Fbar_c));
+      for (Slab& s : ctx->slabs) CKS(run_col(ctx, COL_I1S, PK_OTHER, geom_I1(ctx, s, s.u_c, s.WA, 5), ctx->n3));
+      CKS(exchange(ctx, (long long)5 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
+      for (Slab& s : ctx->slabs) {
+        CKS(run_col(ctx, COL_I2S, PK_OTHER, geom_I2(ctx, s, s.WR, s.WB, 5), ctx->n2));
+        double* tmp6 = reinterpret_cast<double*>(s.WA);  // 6 real fields fit in WA (6 complex fields)
+        XGeom gx = xgeom(ctx, s, s.WB, nullptr);
+        gx.real_out = tmp6;
+        CKS(run_x(ctx, X_REAL_OUT + 6, PK_OTHER, gx, nullptr));
+        ProfScope ps(ctx, PK_OTHER);
+        k_expand6<<<1024, 256, 0, ctx->stream>>>(tmp6, s.Nloc, s.e_dev, s.tmp_real);
         CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(out, sig, sizeof(double) * 9 * N, k, ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
-        cudaFree(sig);
+        if (which == DBFFT_FIELD_STRESS) {
+          k_stress_linear<<<1024, 256, 0, ctx->stream>>>(s.tmp_real, s.phase, s.ptable, s.Nloc, s.tmp_real);
+          CK(cudaGetLastError());
+        }
       }
-      break;
+      return gather_real(ctx, &Slab::tmp_real, 9, (double*)out, out_on_device);
     }
     default:
       ctx->err = "get_field: unknown field";
       return DBFFT_E_INVALID_ARG;
   }
-  CK(cudaStreamSynchronize(ctx->stream));
-  return DBFFT_OK;
 }
 
 dbfft_status dbfft_profile_enable(dbfft_ctx ctx, int32_t enable) {

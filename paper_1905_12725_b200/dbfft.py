@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(HERE, "libdbfft.so")
 
 class Env(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
-                ("cuda_stream", ctypes.c_void_p), ("device", ctypes.c_int32)]
+                ("cuda_stream", ctypes.c_void_p), ("device", ctypes.c_int32), ("loopback", ctypes.c_int32)]
 
 
 class Material(ctypes.Structure):
@@ -43,7 +43,7 @@ STATUS = {0: "OK", 1: "E_INVALID_GRID", 2: "E_INVALID_ARG", 3: "E_STATE", 4: "E_
 EXPORTS = ["dbfft_create", "dbfft_destroy", "dbfft_last_error", "dbfft_spectral_layout", "dbfft_set_phases",
            "dbfft_apply_K", "dbfft_apply_K_aug", "dbfft_precond", "dbfft_eval_state", "dbfft_default_opts",
            "dbfft_solve_increment", "dbfft_get_field", "dbfft_profile_enable", "dbfft_profile_read",
-           "dbfft_profile_name", "dbfft_profile_count", "dbfft_launch_count"]
+           "dbfft_profile_name", "dbfft_profile_count", "dbfft_launch_count", "dbfft_nccl_unique_id"]
 
 _lib = None
 
@@ -86,6 +86,7 @@ def load_library(path=None):
     lib.dbfft_profile_name.restype = ctypes.c_char_p
     lib.dbfft_profile_count.restype = I32
     lib.dbfft_launch_count.argtypes = [P, ctypes.POINTER(ctypes.c_int64)]
+    lib.dbfft_nccl_unique_id.argtypes = [P]
     for fn in EXPORTS:
         getattr(lib, fn).restype = getattr(lib, fn).restype if fn in (
             "dbfft_last_error", "dbfft_default_opts", "dbfft_profile_name", "dbfft_profile_count") else ctypes.c_int
@@ -116,10 +117,30 @@ def _dptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
+def nccl_unique_id_broadcast(rank, process_group=None):
+    """Rank 0 creates the NCCL unique id through the library; every rank receives it via
+    torch.distributed.broadcast_object_list (host-side bootstrap only)."""
+    import torch.distributed as dist
+    lib = load_library()
+    obj = [None]
+    if rank == 0:
+        buf = ctypes.create_string_buffer(128)
+        st = lib.dbfft_nccl_unique_id(buf)
+        if st != 0:
+            raise DBFFTError(st, lib.dbfft_last_error(None).decode())
+        obj = [bytes(buf.raw)]
+    dist.broadcast_object_list(obj, src=0, group=process_group)
+    return ctypes.create_string_buffer(obj[0], 128)
+
+
 class DBFFT:
     """One DBFFT context on one CUDA device (include/dbfft.h)."""
 
-    def __init__(self, n, L=(1.0, 1.0, 1.0), kinematics="small", device=0, stream=None):
+    def __init__(self, n, L=(1.0, 1.0, 1.0), kinematics="small", device=0, stream=None,
+                 world=1, rank=0, loopback=False, process_group=None):
+        """world > 1: slab decomposition (include/dbfft.h "Distribution").  loopback=True keeps
+        all `world` virtual ranks in this process; otherwise NCCL, with the unique id broadcast
+        over `process_group` (torch.distributed, any backend)."""
         import torch
         self.torch = torch
         self.lib = load_library()
@@ -128,7 +149,12 @@ class DBFFT:
         self.device = torch.device("cuda", device)
         torch.cuda.set_device(self.device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
-        env = Env(0, 1, None, ctypes.c_void_p(self.stream.cuda_stream), device)
+        self.world, self.rank, self.loopback = int(world), int(rank), bool(loopback)
+        self._nccl_id = None
+        if self.world > 1 and not self.loopback:
+            self._nccl_id = nccl_unique_id_broadcast(self.rank, process_group)
+        env = Env(self.rank, self.world, ctypes.cast(self._nccl_id, ctypes.c_void_p) if self._nccl_id else None,
+                  ctypes.c_void_p(self.stream.cuda_stream), device, int(self.loopback))
         h = ctypes.c_void_p()
         st = self.lib.dbfft_create((ctypes.c_int32 * 3)(*self.n), (ctypes.c_double * 3)(*L), self.kin,
                                    ctypes.byref(env), ctypes.byref(h))
