@@ -81,6 +81,37 @@ struct FftPlan {
   static constexpr int nstages = n8 + (last > 1 ? 1 : 0);
 };
 
+// a[m + M r] *= W^(r step) for r = 1..R-1.  Only W^step, W^2step, W^4step (and W^8step for
+// R = 16) come from the table; the others are products of two or three table entries
+// (<= 4 ulp), which keeps the L1 twiddle traffic at 3-4 loads per butterfly.
+template <int N, int R, bool INV, int P>
+DBF_DEV void twiddle_r(cplx (&a)[P], int m, int M, int step, const cplx* __restrict__ tw) {
+  cplx w[R];
+  auto ld = [&](int e) {
+    cplx v = __ldg(tw + e);
+    if (INV) v.y = -v.y;
+    return v;
+  };
+  w[1] = ld(step);
+  if (R >= 4) {
+    w[2] = ld(2 * step);
+    w[3] = cmul(w[1], w[2]);
+  }
+  if (R >= 8) {
+    w[4] = ld(4 * step);
+    w[5] = cmul(w[1], w[4]);
+    w[6] = cmul(w[2], w[4]);
+    w[7] = cmul(w[3], w[4]);
+  }
+  if (R >= 16) {
+    w[8] = ld(8 * step);
+#pragma unroll
+    for (int r = 9; r < 16; ++r) w[r] = cmul(w[r - 8], w[8]);
+  }
+#pragma unroll
+  for (int r = 1; r < R; ++r) a[m + M * r] = cmul(a[m + M * r], w[r]);
+}
+
 // One Stockham stage of radix R on the register array a[8] (positions g + s*N/8), reading
 // was already done; writes outputs to smem via idx(pos).  Ns = product of previous radices.
 template <int N, int R, bool INV>
@@ -90,15 +121,7 @@ DBF_DEV void stage_compute(cplx (&a)[8], int g, int Ns, const cplx* __restrict__
   for (int m = 0; m < M; ++m) {
     const int b = g + m * (N / 8);
     const int k = b % Ns;
-    if (Ns > 1) {
-      const int step = (N / (Ns * R)) * k;
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
-        cplx w = __ldg(tw + r * step);
-        if (INV) w.y = -w.y;
-        a[m + M * r] = cmul(a[m + M * r], w);
-      }
-    }
+    if (Ns > 1) twiddle_r<N, R, INV>(a, m, M, (N / (Ns * R)) * k, tw);
     if (R == 8) {
       dft8<INV>(a);
     } else if (R == 4) {
@@ -112,8 +135,12 @@ DBF_DEV void stage_compute(cplx (&a)[8], int g, int Ns, const cplx* __restrict__
 // Full in-CTA FFT.  On entry a[s] = x[g + s*N/8]; on exit a[s] = X[g + s*N/8].
 // IDX(pos) maps a line position to a shared-memory slot (column interleave or padding).
 // All threads of the CTA must call this (it contains __syncthreads()).
-template <int N, bool INV, class IDX>
-DBF_DEV void fft_cta(cplx (&a)[8], cplx* sbuf, int g, const IDX& idx, const cplx* __restrict__ tw) {
+struct SyncCtaDefault {
+  DBF_DEV void operator()() const { __syncthreads(); }
+};
+
+template <int N, bool INV, class IDX, class SYNC = SyncCtaDefault>
+DBF_DEV void fft_cta(cplx (&a)[8], cplx* sbuf, int g, const IDX& idx, const cplx* __restrict__ tw, const SYNC& sync = SYNC{}) {
   typedef FftPlan<N> P;
   int Ns = 1;
 #pragma unroll
@@ -131,7 +158,7 @@ DBF_DEV void fft_cta(cplx (&a)[8], cplx* sbuf, int g, const IDX& idx, const cplx
     else if (R == 4) stage_compute<N, 4, INV>(a, g, Ns, tw);
     else stage_compute<N, 2, INV>(a, g, Ns, tw);
     if (!is_last) {
-      __syncthreads();  // everyone finished reading the buffer
+      sync();  // the group finished reading the buffer
       const int M = 8 / R;
 #pragma unroll
       for (int m = 0; m < 8 / 2; ++m) {
@@ -140,9 +167,7 @@ DBF_DEV void fft_cta(cplx (&a)[8], cplx* sbuf, int g, const IDX& idx, const cplx
         const int base = (b / Ns) * Ns * R + (b % Ns);
         for (int r = 0; r < R; ++r) sbuf[idx(base + r * Ns)] = a[m + M * r];
       }
-      if (M == 8) {  // unreachable (R >= 2 gives M <= 4); kept for clarity
-      }
-      __syncthreads();
+      sync();
     }
     Ns *= R;
   }
@@ -245,15 +270,7 @@ DBF_DEV void sub_stage(cplx (&a)[P], int g, int Ns, const cplx* __restrict__ tw)
   for (int m = 0; m < M; ++m) {
     const int b = g + m * T;
     const int k = b % Ns;
-    if (Ns > 1) {
-      const int step = (N / (Ns * R)) * k;
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
-        cplx w = __ldg(tw + r * step);
-        if (INV) w.y = -w.y;
-        a[m + M * r] = cmul(a[m + M * r], w);
-      }
-    }
+    if (Ns > 1) twiddle_r<N, R, INV>(a, m, M, (N / (Ns * R)) * k, tw);
     if (R == 16) dft16s<INV, 1>(a, 0);
     else if (R == 8) {
       cplx t8[8];

@@ -609,17 +609,38 @@ template <int P>
 DBF_DEV int x_idx(int base, int pos) {
   return P == 16 ? IdxGrp{base}(pos) : IdxSwz{base}(pos);
 }
-template <int P>
+// a pair job's threads share one warp when N1 / P <= 32: exchanges need only __syncwarp
+template <int N1, int P>
 DBF_DEV void x_jobsync() {
-  if (P == 16) __syncwarp();
+  if (N1 / P <= 32) __syncwarp();
   else __syncthreads();
 }
+template <int N1, int P>
+struct XSync {
+  DBF_DEV void operator()() const { x_jobsync<N1, P>(); }
+};
 template <int N1, int P, bool INV>
 DBF_DEV void x_fft(cplx (&a)[P], cplx* cx, int gq, int base, const cplx* __restrict__ tw) {
   if constexpr (P == 16) {
-    fft_sub<N1, 16, INV>(a, cx, gq, IdxGrp{base}, tw, SyncWarp{});
+    fft_sub<N1, 16, INV>(a, cx, gq, IdxGrp{base}, tw, XSync<N1, 16>{});
   } else {
-    fft_cta<N1, INV>(a, cx, gq, IdxSwz{base}, tw);
+    fft_cta<N1, INV>(a, cx, gq, IdxSwz{base}, tw, XSync<N1, 8>{});
+  }
+}
+
+// Z[N-k] of the R2C untangle for the thread's outputs k = gq + s TPJ: held by job thread
+// (TPJ - gq) % TPJ in slot 7 - s (gq > 0) or by this thread in slot (8 - s) % 8 (gq = 0),
+// fetched with shuffles inside the job's warp segment (TPJ <= 32, P = 8).
+template <int TPJ>
+DBF_DEV void x_partner(const cplx (&a)[8], cplx (&zn)[8], int gq) {
+  const int src = (TPJ - gq) & (TPJ - 1);
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const cplx v = a[7 - s];
+    cplx r;
+    r.x = __shfl_sync(0xffffffffu, v.x, src, TPJ);
+    r.y = __shfl_sync(0xffffffffu, v.y, src, TPJ);
+    zn[s] = (gq == 0) ? a[(8 - s) & 7] : r;
   }
 }
 
@@ -790,7 +811,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
         }
       }
       x_fft<N1, PX, true>(a, cx, gq, jbase, g.tw);
-      x_jobsync<PX>();  // the job's exchange reads are done before its slots become reals
+      x_jobsync<N1, PX>();  // the job's exchange reads are done before its slots become reals
 #pragma unroll
       for (int s = 0; s < PX; ++s) {
         const int m = gq + s * TPJ;
@@ -855,17 +876,25 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
         a[s] = make_double2(ra, rb);
       }
       x_fft<N1, PX, false>(a, cx, gq, jbase, g.tw);
-      x_jobsync<PX>();
+      constexpr bool SHFL = (PX == 8 && TPJ <= 32);
+      cplx zn[PX];
+      if constexpr (SHFL) {
+        x_partner<TPJ>(a, zn, gq);
+      } else {
+        x_jobsync<N1, PX>();
 #pragma unroll
-      for (int s = 0; s < PX; ++s) cx[x_idx<PX>(jbase, gq + s * TPJ)] = a[s];
-      x_jobsync<PX>();
+        for (int s = 0; s < PX; ++s) cx[x_idx<PX>(jbase, gq + s * TPJ)] = a[s];
+        x_jobsync<N1, PX>();
+#pragma unroll
+        for (int s = 0; s < PX; ++s) zn[s] = cx[x_idx<PX>(jbase, (N1 - (gq + s * TPJ)) & (N1 - 1))];
+      }
       if (lvalid && fa < COUT) {
 #pragma unroll
         for (int s = 0; s < PX; ++s) {
           const int k = gq + s * TPJ;
           if (2 * k > N1) continue;
           const cplx Z = a[s];
-          const cplx Zn = cx[x_idx<PX>(jbase, (N1 - k) & (N1 - 1))];
+          const cplx Zn = zn[s];
           cplx A = make_double2(0.5 * (Z.x + Zn.x), 0.5 * (Z.y - Zn.y));
           cplx B = make_double2(0.5 * (Z.y + Zn.y), -0.5 * (Z.x - Zn.x));
           A = cscale(A, g.inv_n);
