@@ -24,6 +24,18 @@ covers say "parity unpinned" in their docstring.
 import numpy as np
 
 # ----------------------------------------------------------------------------
+# Volume average <a> = (1/N) sum_x a(x) ("average of the stiffness", the
+# macroscopic stress/strain of P:126).  Summed pairwise over a contiguous copy of
+# each component: numpy reduces a strided multi-axis mean by plain accumulation,
+# whose error grows like N eps (1e-11 relative at 2^20 voxels).
+# ----------------------------------------------------------------------------
+def volume_average(a):
+    a = np.asarray(a)
+    flat = np.ascontiguousarray(a).reshape(a.shape[:-3] + (-1,))
+    return flat.mean(axis=-1)
+
+
+# ----------------------------------------------------------------------------
 # Grid and frequencies (Eq. (1); reading R1 for even grids)
 # ----------------------------------------------------------------------------
 
@@ -294,7 +306,7 @@ def apply_K(u_hat, C, XI, e=None, finite=False):
     sig = contract(C, eps)
     f = -div_hat(fft(sig), XI)
     f[:, null_set(XI)] = 0.0
-    return f, sig.mean(axis=(-3, -2, -1))
+    return f, volume_average(sig)
 
 
 def rhs_from_stress(sig, XI):
@@ -465,10 +477,10 @@ def solve_small_strain(phase, materials, load, tol=1e-10, max_iter=10000, L=(1.0
     mask, target = _masks(load)
     eps_U = np.where(mask, 0.0, target)
     sig_f = np.where(mask, target, 0.0)
-    Cbar = C.mean(axis=(-3, -2, -1))
+    Cbar = volume_average(C)
     basis = macro_basis(mask, symmetric=True)
     sig_U = contract(C, eps_U.reshape(3, 3, 1, 1, 1) * np.ones((1, 1, nz, ny, nx)))
-    mean_sig_U = sig_U.mean(axis=(-3, -2, -1))
+    mean_sig_U = volume_average(sig_U)
     b = Aug(rhs_from_stress(sig_U, XI), np.where(mask, sig_f - mean_sig_U, 0.0))
     macro = bool(mask.any())
 
@@ -482,8 +494,8 @@ def solve_small_strain(phase, materials, load, tol=1e-10, max_iter=10000, L=(1.0
     x, iters, hist = pcg(apply_A, precond, b, mean_sig_U, tol, max_iter, macro)
     eps = ifft(sym_grad_hat(x.u, XI)) + (eps_U + x.e).reshape(3, 3, 1, 1, 1)
     sig = contract(C, eps)
-    return dict(u_hat=x.u, e=x.e, eps=eps, sig=sig, mean_eps=eps.mean(axis=(-3, -2, -1)),
-                mean_sig=sig.mean(axis=(-3, -2, -1)), iters=iters, hist=hist, XI=XI)
+    return dict(u_hat=x.u, e=x.e, eps=eps, sig=sig, mean_eps=volume_average(eps),
+                mean_sig=volume_average(sig), iters=iters, hist=hist, XI=XI)
 
 
 def displacement(u_hat):
@@ -524,10 +536,10 @@ def solve_finite_increment(state, phase, materials, load, tol=1e-10, tol_newton=
     Kbar = None
     while True:
         P, K = neo_hookean(F, mu, kappa)
-        meanP = P.mean(axis=(-3, -2, -1))
+        meanP = volume_average(P)
         b = Aug(rhs_from_stress(P, XI), np.where(mask, P_f - meanP, 0.0))
         if Kbar is None:
-            Kbar = K.mean(axis=(-3, -2, -1))
+            Kbar = volume_average(K)
 
         def apply_A(v, K=K):
             f, ms = apply_K(v.u, K, XI, e=v.e if macro else None, finite=True)
@@ -549,7 +561,7 @@ def solve_finite_increment(state, phase, materials, load, tol=1e-10, tol_newton=
     last = np.max(np.abs(dG))
     state.Fbar = Fbar
     P, _ = neo_hookean(F, mu, kappa)
-    return dict(F=F, P=P, mean_F=F.mean(axis=(-3, -2, -1)), mean_P=P.mean(axis=(-3, -2, -1)),
+    return dict(F=F, P=P, mean_F=volume_average(F), mean_P=volume_average(P),
                 cg_iters=total_cg, newton_iters=newton, converged=bool(last < tol_newton))
 
 
@@ -582,10 +594,10 @@ def solve_j2_increment(state, phase, materials, load, dt, tol=1e-10, tol_newton=
     while True:
         sig, Calg, eps_p, _ = j2_perzyna(eps, state.eps_p, par["E"], par["nu"], par["sigma_y"],
                                          par["n"], par["edot0"], dt)
-        mean_sig = sig.mean(axis=(-3, -2, -1))
+        mean_sig = volume_average(sig)
         b = Aug(rhs_from_stress(sig, XI), np.zeros((3, 3)))
         if Cbar is None:
-            Cbar = Calg.mean(axis=(-3, -2, -1))
+            Cbar = volume_average(Calg)
 
         def apply_A(v, C=Calg):
             f, ms = apply_K(v.u, C, XI)
@@ -606,8 +618,8 @@ def solve_j2_increment(state, phase, materials, load, dt, tol=1e-10, tol_newton=
                                   par["n"], par["edot0"], dt)
     state.eps_p = eps_p
     state.ebar = target.copy()
-    return dict(eps=eps, sig=sig, mean_eps=eps.mean(axis=(-3, -2, -1)),
-                mean_sig=sig.mean(axis=(-3, -2, -1)), cg_iters=total_cg, newton_iters=newton)
+    return dict(eps=eps, sig=sig, mean_eps=volume_average(eps),
+                mean_sig=volume_average(sig), cg_iters=total_cg, newton_iters=newton)
 
 
 # ----------------------------------------------------------------------------

@@ -419,7 +419,7 @@ def test_P9_P10_bounds_hill_mandel(c1_solution):
     C = O.stiffness_field(cfg["phase"], cfg["materials"])
     eps_bar = cfg["loads"][0]["target"]
     W = np.sum(res["mean_sig"] * eps_bar)
-    Cv = _mandel(C.mean(axis=(-3, -2, -1)))
+    Cv = _mandel(O.volume_average(C))
     Sr = np.mean([np.linalg.inv(_mandel(C[..., k, j, i])) for k in range(8) for j in range(8) for i in range(8)], axis=0)
     e = np.array([eps_bar[0, 0], eps_bar[1, 1], eps_bar[2, 2], 0, 0, 0])
     assert e @ np.linalg.inv(Sr) @ e < W < e @ Cv @ e
@@ -527,3 +527,26 @@ def test_j2_dbfft_homogeneous_matches_material_point():
         res = O.solve_j2_increment(st, ph, mats, dict(target=t, mask=np.zeros((3, 3), bool)), 1.0)
         s, _, epsp, _ = _j2(t, epsp)
         assert np.allclose(res["mean_sig"], s, rtol=1e-12, atol=1e-9)
+
+
+def test_volume_average_exact_sum():
+    """<a> over the voxel axes on a strided tensor field of 2^18 voxels: equals the
+    exactly rounded mean (math.fsum) to 1e-15, and a two-phase field's mean stiffness equals the
+    closed form (N - n1) C0 / N + n1 C1 / N (the phase-count formula)."""
+    import math
+    n = (32, 64, 128)
+    u = ms.SplitMix64(5).uniform(n[0] * n[1] * n[2]).reshape(n[2], n[1], n[0])
+    ph = (u < 0.3).astype(np.uint16)
+    mats = [dict(kind="iso", E=1.0, nu=0.3), dict(kind="iso", E=10.0, nu=0.25)]
+    C = O.stiffness_field(ph, mats)
+    assert not C.flags["C_CONTIGUOUS"] or C.strides[-1] != 8 * 81  # a strided field is the case to pin
+    m = O.volume_average(C)
+    N = ph.size
+    exact = np.array([math.fsum(C[i, j, k, l].ravel()) / N for i in range(3) for j in range(3)
+                      for k in range(3) for l in range(3)]).reshape(3, 3, 3, 3)
+    assert np.abs(m - exact).max() <= 1e-15 * np.abs(exact).max()
+    C0 = O.stiffness_field(np.zeros((1, 1, 1), np.uint16), mats)[..., 0, 0, 0]
+    C1 = O.stiffness_field(np.ones((1, 1, 1), np.uint16), mats)[..., 0, 0, 0]
+    n1 = int(ph.sum())
+    closed = ((N - n1) * C0 + n1 * C1) / N
+    assert np.abs(m - closed).max() <= 1e-15 * np.abs(closed).max()
