@@ -320,9 +320,9 @@ XGeom xgeom(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out) {
   return g;
 }
 
-dbfft_status run_col(dbfft_ctx ctx, int kind, int prof_id, const ColGeom& g, int N) {
+dbfft_status run_col(dbfft_ctx ctx, int kind, int prof_id, const ColGeom& g, int N, int* grid = nullptr) {
   ProfScope ps(ctx, prof_id);
-  CK(launch_col(kind, N, g, ctx->stream));
+  CK(launch_col(kind, N, g, ctx->stream, grid));
   return DBFFT_OK;
 }
 
@@ -653,8 +653,9 @@ dbfft_status apply_K_slabs(dbfft_ctx ctx, cplx* Slab::*u, cplx* Slab::*f, bool u
       g5.dotp = s.*u;
       g5.partials = s.part_f3;
     }
-    CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_F3, g5, ctx->n3));
-    if (ao) ao->grid_f3[k] = col_grid(ctx->n3, g5.ncols);
+    int grid5 = 0;
+    CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_F3, g5, ctx->n3, &grid5));
+    if (ao) ao->grid_f3[k] = grid5;
   }
   return DBFFT_OK;
 }
@@ -1170,7 +1171,7 @@ dbfft_status alloc_slab(dbfft_ctx ctx, Slab& s) {
   int gx = 0;
   for (int k = 0; k < X_REAL_OUT; ++k) gx = std::max(gx, x_grid(k, ctx->n1, s.nlines));
   CKS(dalloc(ctx, &s.part_x, (size_t)gx * 10));
-  CKS(dalloc(ctx, &s.part_f3, (size_t)col_grid(ctx->n3, (long long)s.nyl * ctx->n1h)));
+  CKS(dalloc(ctx, &s.part_f3, (size_t)std::max(col_grid(ctx->n3, (long long)s.nyl * ctx->n1h), 1024)));
   CKS(dalloc(ctx, &s.part_cg, (size_t)cg_blocks() * 2));
   CKS(dalloc(ctx, &s.part_misc, (size_t)cg_blocks() * 45));
   CKS(dalloc(ctx, &s.loc, 64));

@@ -10,6 +10,9 @@
 // so fewer than 2c fields cross the y and z sweeps (52 H / 66 H complex moves).
 #include "passes.cuh"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 
 #ifndef DBF_X_MINB
@@ -984,6 +987,280 @@ __global__ void __launch_bounds__(256) k_mean_tangent(XGeom g, double* partials)
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// Column passes, TMA pipeline.  Persistent, one CTA per SM:
+// warp 8 (one elected lane) streams 32 KB tiles — KC = 2048/N kx-columns x N positions of ONE
+// field, 128-byte rows — into an R-slot shared-memory ring with cp.async.bulk.tensor
+// (mbarrier complete_tx); warps 0-7 FFT the columns (a column's N/8 threads share one warp, so
+// every exchange is warp-local), apply the pass's pre/post weights, and write each finished
+// output tile into a staging buffer that one thread sends back with a TMA store.  A pass is a
+// static "program": the order in which input fields are loaded and the order of its terms, chosen
+// so that ring slots are released in load order (FIFO) — see c_prog.
+// Main tiles cover kx in [0, n1/2) in KC-column blocks of one outer index; tail tiles carry the
+// Nyquist column kx = n1/2 of KC consecutive outer indices (no compute is spent on padding).
+// ------------------------------------------------------------------------------------------------
+struct TProg {
+  int nl;                 // loads per tile
+  signed char ld[12];     // load i: input field (0..15) or dot-vector field (16 + f)
+  int nt;                 // terms
+  signed char j[10];      // ColOp term index
+  signed char la[10], lb[10], ldot[10];  // load indices of the term's inputs / dot vector (-1: none)
+  signed char rel[10];    // loads released (cumulative, FIFO) once the term is done
+  signed char acc[10];    // register accumulator of a two-term output
+};
+
+// index: 2*kind + dot (one table: host copy for the liveness check, constant-bank copy for the kernel)
+#define DBF_COL_PROGS \
+    /* COL_I1S: loads u0, u2, u1; terms 0, 2, 3{0,2}, 1, 4{1,2} */ \
+    {3, {0, 2, 1}, 5, {0, 2, 3, 1, 4}, {0, 1, 0, 2, 2}, {-1, -1, 1, -1, 1}, {-1, -1, -1, -1, -1}, {0, 0, 1, 1, 3}, {0, 0, 0, 0, 0}}, \
+    {0}, \
+    /* COL_I1F: u_i then i xi_z u_i from the same load */ \
+    {3, {0, 1, 2}, 6, {0, 3, 1, 4, 2, 5}, {0, 0, 1, 1, 2, 2}, {-1, -1, -1, -1, -1, -1}, {-1, -1, -1, -1, -1, -1}, {0, 1, 1, 2, 2, 3}, {0, 0, 0, 0, 0, 0}}, \
+    {0}, \
+    /* COL_I2S: loads 0,1,2,4,3; terms 0, 1, 5{0,1}, 2, 3{4}, 4{3} */ \
+    {5, {0, 1, 2, 4, 3}, 6, {0, 1, 5, 2, 3, 4}, {0, 1, 0, 2, 3, 4}, {-1, -1, 1, -1, -1, -1}, {-1, -1, -1, -1, -1, -1}, {0, 0, 2, 3, 4, 5}, {0, 0, 0, 0, 0, 0}}, \
+    {0}, \
+    /* COL_I2F: loads u0, G0z, u1, G1z, u2, G2z */ \
+    {6, {0, 3, 1, 4, 2, 5}, 9, {0, 1, 2, 3, 4, 5, 6, 7, 8}, {0, 0, 1, 2, 2, 3, 4, 4, 5}, {-1, -1, -1, -1, -1, -1, -1, -1, -1}, \
+     {-1, -1, -1, -1, -1, -1, -1, -1, -1}, {0, 1, 2, 2, 3, 4, 4, 5, 6}, {0, 0, 0, 0, 0, 0, 0, 0, 0}}, \
+    {0}, \
+    /* COL_F2S */ \
+    {6, {0, 1, 2, 3, 4, 5}, 6, {0, 1, 2, 3, 4, 5}, {0, 1, 2, 3, 4, 5}, {-1, -1, -1, -1, -1, -1}, {-1, -1, -1, -1, -1, -1}, {1, 2, 3, 4, 5, 6}, {0, 0, 0, 0, 0, 0}}, \
+    {0}, \
+    /* COL_F2F: term j reads field ld[j] */ \
+    {9, {0, 1, 3, 4, 6, 7, 2, 5, 8}, 9, {0, 1, 2, 3, 4, 5, 6, 7, 8}, {0, 1, 2, 3, 4, 5, 6, 7, 8}, {-1, -1, -1, -1, -1, -1, -1, -1, -1}, \
+     {-1, -1, -1, -1, -1, -1, -1, -1, -1}, {1, 2, 3, 4, 5, 6, 7, 8, 9}, {0, 0, 0, 0, 0, 0, 0, 0, 0}}, \
+    {0}, \
+    /* COL_F3S: loads 0,5,1,4,3,2; terms j0{0,5} j2{5,1} j1{4} j3{3} j4{4,3} j5{2} */ \
+    {6, {0, 5, 1, 4, 3, 2}, 6, {0, 2, 1, 3, 4, 5}, {0, 1, 3, 4, 3, 5}, {1, 2, -1, -1, 4, -1}, {-1, -1, -1, -1, -1, -1}, {1, 3, 3, 3, 5, 6}, {0, 1, 0, 1, 0, 0}}, \
+    /* COL_F3S + <p, f>: p_o loaded right before the term that stores output o */ \
+    {9, {0, 5, 1, 4, 16, 3, 17, 2, 18}, 6, {0, 2, 1, 3, 4, 5}, {0, 1, 3, 5, 3, 7}, {1, 2, -1, -1, 5, -1}, {-1, -1, 4, 6, -1, 8}, {1, 3, 3, 3, 7, 9}, {0, 1, 0, 1, 0, 0}}, \
+    /* COL_F3F */ \
+    {6, {0, 3, 1, 4, 2, 5}, 6, {0, 1, 2, 3, 4, 5}, {0, 1, 2, 3, 4, 5}, {-1, -1, -1, -1, -1, -1}, {-1, -1, -1, -1, -1, -1}, {1, 2, 3, 4, 5, 6}, {0, 0, 0, 0, 0, 0}}, \
+    {9, {0, 3, 16, 1, 4, 17, 2, 5, 18}, 6, {0, 1, 2, 3, 4, 5}, {0, 1, 3, 4, 6, 7}, {-1, -1, -1, -1, -1, -1}, {-1, 2, -1, 5, -1, 8}, {1, 3, 4, 6, 7, 9}, {0, 0, 0, 0, 0, 0}}, \
+    /* COL_ZI3, COL_YI3 */ \
+    {3, {0, 1, 2}, 3, {0, 1, 2}, {0, 1, 2}, {-1, -1, -1}, {-1, -1, -1}, {1, 2, 3}, {0, 0, 0}}, \
+    {0}, \
+    {3, {0, 1, 2}, 3, {0, 1, 2}, {0, 1, 2}, {-1, -1, -1}, {-1, -1, -1}, {1, 2, 3}, {0, 0, 0}}, \
+    {0},
+
+__device__ __constant__ TProg c_prog[2 * COL_NKINDS] = {DBF_COL_PROGS};
+static const TProg kColProgHost[2 * COL_NKINDS] = {DBF_COL_PROGS};
+
+struct ColTiles {
+  int n_outer;   // outer indices
+  int nkb;       // main kx blocks per outer (n1/2 / KC)
+  int n_main;    // n_outer * nkb
+  int n_tiles;   // n_main + ceil(n_outer / KC)
+  int tail_cols; // outer indices per tail box: min(KC, n_outer)
+};
+
+template <int N>
+struct TmaCfg {
+  static constexpr int KC = 2048 / N;          // columns per tile (32 KB of complex128)
+  static constexpr int TPC = N / 8;            // threads per column (8 points each)
+  static constexpr int CONS = 256;             // consumer threads (8 warps)
+  static constexpr int THREADS = CONS + 32;    // + producer warp
+  static constexpr int TILE = 32768;           // bytes per ring slot / staging buffer
+};
+
+// cplx offset of (pos, column c) inside a main tile: KC/8 sub-tiles of [N][8], 128B swizzle
+template <int N>
+DBF_DEV int tma_moff(int pos, int c) { return (c >> 3) * (N * 8) + pos * 8 + ((c & 7) ^ (pos & 7)); }
+// tail tile: [KC][N] unswizzled
+template <int N>
+DBF_DEV int tma_toff(int pos, int c) { return c * N + pos; }
+
+DBF_DEV void tma_load5(void* dst, const CUtensorMap* m, int c0, int c1, int c2, int c3, int c4, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+      ::"r"(smem_u32(dst)), "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar)) : "memory");
+}
+DBF_DEV void tma_store5(const CUtensorMap* m, int c0, int c1, int c2, int c3, int c4, const void* src) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];"
+               ::"l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(src)) : "memory");
+}
+DBF_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int K>
+DBF_DEV void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(K) : "memory"); }
+DBF_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+DBF_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+DBF_DEV void cons_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+struct TmaMaps {
+  CUtensorMap in_m, in_t, out_m, out_t, dot_m, dot_t;
+};
+
+template <int N, int KIND, bool DOT, int R>
+__global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __grid_constant__ TmaMaps maps, ColGeom g, ColTiles tl) {
+  typedef ColOp<KIND> Op;
+  typedef TmaCfg<N> CF;
+  constexpr int KC = CF::KC, TPC = CF::TPC;
+  constexpr int S = 2;  // staging buffers (TMA stores in flight)
+  extern __shared__ __align__(1024) unsigned char tsm[];
+  // 1024-byte alignment of the ring (128B swizzle atoms)
+  // (offset arithmetic on the shared array keeps the shared address space: LDS/STS, not LD/ST)
+  unsigned char* base = tsm + ((1024u - (smem_u32(tsm) & 1023u)) & 1023u);
+  cplx* ring = reinterpret_cast<cplx*>(base);
+  cplx* stg = reinterpret_cast<cplx*>(base + R * CF::TILE);
+  cplx* xb = reinterpret_cast<cplx*>(base + (R + S) * CF::TILE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + (R + S + 1) * CF::TILE);
+  uint64_t* empty = full + R;
+  const TProg& pg = c_prog[2 * KIND + (DOT ? 1 : 0)];
+  const int t = threadIdx.x;
+  const int warp = t >> 5;
+  if (t == 0) {
+    for (int i = 0; i < R; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], CF::CONS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int nl = pg.nl;
+
+  if (warp == CF::CONS / 32) {
+    // ------------------------------------------------------------------ producer
+    if ((t & 31) == 0) {
+      uint32_t seq = 0;
+      for (int tile = blockIdx.x; tile < tl.n_tiles; tile += gridDim.x) {
+        const bool tail = tile >= tl.n_main;
+        const int outer = tail ? (tile - tl.n_main) * KC : tile / tl.nkb;
+        const int kb = tail ? 0 : tile % tl.nkb;
+        for (int i = 0; i < nl; ++i, ++seq) {
+          const int slot = seq % R;
+          const uint32_t round = seq / R;
+          if (round > 0) mbar_wait(&empty[slot], (round - 1) & 1);
+          const int ld = pg.ld[i];
+          const bool isdot = ld >= 16;
+          const int f = ld & 15;
+          mbar_expect_tx(&full[slot], tail ? 16u * N * tl.tail_cols : (uint32_t)CF::TILE);
+          cplx* dst = ring + slot * (CF::TILE / 16);
+          if (tail) {
+            tma_load5(dst, isdot ? &maps.dot_t : &maps.in_t, 2 * (g.n1h - 1), 0, 0, outer, f, &full[slot]);
+          } else {
+#pragma unroll
+            for (int sb = 0; sb < KC / 8; ++sb)
+              tma_load5(dst + sb * N * 8, isdot ? &maps.dot_m : &maps.in_m, 2 * (kb * KC + sb * 8), 0, 0, outer, f, &full[slot]);
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------------- consumers
+  const int c = t / TPC;   // column of the tile
+  const int gq = t % TPC;  // position group
+  const int lane = t & 31;
+  cplx* xcol = xb + c * N;  // this column's FFT exchange buffer
+  double dot = 0.0;
+  uint32_t nout = 0;        // output tiles written (staging rotation)
+  uint32_t it = 0;
+  for (int tile = blockIdx.x; tile < tl.n_tiles; tile += gridDim.x, ++it) {
+    const bool tail = tile >= tl.n_main;
+    ColAt at;
+    at.g = &g;
+    at.outer = tail ? (tile - tl.n_main) * KC + c : tile / tl.nkb;
+    at.kx = tail ? g.n1h - 1 : (tile % tl.nkb) * KC + c;
+    const bool valid = at.outer < tl.n_outer;
+    if (!valid) at.outer = 0;
+    const double wdot = (at.kx == 0 || 2 * at.kx == g.n1) ? 1.0 : 2.0;
+    const uint32_t sbase = it * nl;
+    int released = 0;
+    constexpr int NACC = (KIND == COL_F3S) ? 2 : 1;  // pending two-term outputs
+    cplx acc0[8], acc1[NACC > 1 ? 8 : 1];
+#pragma unroll 1
+    for (int k = 0; k < pg.nt; ++k) {
+      const int j = pg.j[k];
+      const TermInfo ti = Op::term(j);
+      const int la = pg.la[k], lb = pg.lb[k];
+      const uint32_t qa = sbase + la;
+      mbar_wait(&full[qa % R], (qa / R) & 1);
+      const cplx* sa = ring + (qa % R) * (CF::TILE / 16);
+      const cplx* sbp = sa;
+      if (lb >= 0) {
+        const uint32_t qb = sbase + lb;
+        mbar_wait(&full[qb % R], (qb / R) & 1);
+        sbp = ring + (qb % R) * (CF::TILE / 16);
+      }
+      cplx a[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        at.pos = gq + s * TPC;
+        const int o = tail ? tma_toff<N>(at.pos, c) : tma_moff<N>(at.pos, c);
+        const cplx v0 = sa[o];
+        const cplx v1 = (lb >= 0) ? sbp[o] : v0;
+        a[s] = Op::pre(at, j, v0, v1);
+      }
+      fft_cta<N, Op::INV>(a, xcol, gq, IdxSwz{0}, g.tw, SyncWarp{});
+      const int ai = pg.acc[k];
+      const int ld = pg.ldot[k];
+      const cplx* sd = nullptr;
+      if (DOT && ti.last && ld >= 0) {
+        const uint32_t qd = sbase + ld;
+        mbar_wait(&full[qd % R], (qd / R) & 1);
+        sd = ring + (qd % R) * (CF::TILE / 16);
+      }
+      cplx* so = stg + (nout % S) * (CF::TILE / 16);
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        at.pos = gq + s * TPC;
+        cplx v = cmul(Op::post(at, j), a[s]);
+        if (ColTwo<KIND>::value && !ti.first) v = cadd(v, (NACC > 1 && ai) ? acc1[NACC > 1 ? s : 0] : acc0[s]);
+        if (ColTwo<KIND>::value && !ti.last) {
+          if (NACC > 1 && ai) acc1[NACC > 1 ? s : 0] = v;
+          else acc0[s] = v;
+        } else {
+          const int o = tail ? tma_toff<N>(at.pos, c) : tma_moff<N>(at.pos, c);
+          so[o] = v;
+          if (DOT && sd && valid) {
+            const cplx p = sd[o];
+            dot += wdot * (p.x * v.x + p.y * v.y);
+          }
+        }
+      }
+      // release the ring slots this term finished (FIFO): all lanes of the warp are done
+      const int rel = pg.rel[k];
+      __syncwarp();
+      if (lane == 0)
+        for (int i = released; i < rel; ++i) mbar_arrive(&empty[(sbase + i) % R]);
+      released = rel;
+      if (ti.last) {
+        // every consumer wrote its part of the output tile; the store S-1 outputs ago is done
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (t == 0) bulk_wait_read<S - 2>();
+        cons_sync();
+        if (t == 0) {
+          if (tail) tma_store5(&maps.out_t, 2 * (g.n1h - 1), 0, 0, (tile - tl.n_main) * KC, ti.o, so);
+          else tma_store5(&maps.out_m, 2 * ((tile % tl.nkb) * KC), 0, 0, tile / tl.nkb, ti.o, so);
+          if (!tail && KC > 8) {
+#pragma unroll
+            for (int sb = 1; sb < KC / 8; ++sb)
+              tma_store5(&maps.out_m, 2 * ((tile % tl.nkb) * KC + sb * 8), 0, 0, tile / tl.nkb, ti.o, so + sb * N * 8);
+          }
+          bulk_commit();
+        }
+        ++nout;
+      }
+    }
+  }
+  if (t == 0) bulk_wait_all();
+  if (DOT) {
+    __shared__ double red[8];
+    dot = warp_sum(dot);
+    if (lane == 0) red[warp] = dot;
+    cons_sync();
+    if (t == 0) {
+      double s = 0.0;
+      for (int w = 0; w < 8; ++w) s += red[w];
+      g.partials[blockIdx.x] = s;
+    }
+  }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------------------------------------
@@ -1037,7 +1314,142 @@ static cudaError_t launch_col_n(int kind, const ColGeom& g, cudaStream_t s) {
   }
 }
 
-cudaError_t launch_col(int kind, int N, const ColGeom& g, cudaStream_t s) {
+// ---- TMA column passes: tensor maps + dispatch ------------------------------------------------
+#ifndef DBF_COL_TMA
+#define DBF_COL_TMA 1
+#endif
+#ifndef DBF_TMA_PROMO
+#define DBF_TMA_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
+#ifndef DBF_COL_R
+#define DBF_COL_R 3
+#endif
+static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+// fields of the pass's input / output buffers (tensor-map bounds)
+static const int kColNfIn[COL_NKINDS] = {3, 3, 5, 6, 6, 9, 6, 6, 3, 3};
+static const int kColNfOut[COL_NKINDS] = {5, 6, 6, 9, 6, 6, 3, 3, 3, 3};
+
+// 5D view [field][outer][pos_hi][pos_lo][kx re/im] of a column-pass operand (complex strides)
+static bool col_map(CUtensorMap* m, const void* ptr, int N, int n1h, int psh, long long ps, long long pcs, int n_outer,
+                    long long os, int nf, long long fs, bool tail, int KC) {
+  auto enc = tma_encoder();
+  if (!enc || !ptr) return false;
+  long long L = 1LL << psh;
+  if (L >= N) {  // plain layout: re-express as chunks of <= 256 positions
+    L = N > 256 ? 256 : N;
+    pcs = L * ps;
+  } else if (L > 256) {
+    return false;
+  }
+  if (N / L > 256) return false;
+  cuuint64_t dims[5] = {(cuuint64_t)(2 * n1h), (cuuint64_t)L, (cuuint64_t)(N / L), (cuuint64_t)n_outer, (cuuint64_t)nf};
+  cuuint64_t strides[4] = {(cuuint64_t)(ps * 16), (cuuint64_t)(pcs * 16), (cuuint64_t)(os * 16), (cuuint64_t)(fs * 16)};
+  cuuint32_t box[5] = {tail ? 2u : 16u, (cuuint32_t)L, (cuuint32_t)(N / L), tail ? (cuuint32_t)std::min(KC, n_outer) : 1u, 1u};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, tail ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                   DBF_TMA_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+static int g_nsm = 0;
+static int num_sms() {
+  if (!g_nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return g_nsm;
+}
+
+template <int N>
+static bool col_tma_tiles(const ColGeom& g, ColTiles* tl) {
+  constexpr int KC = TmaCfg<N>::KC;
+  if (!DBF_COL_TMA || (g.n1h - 1) % KC != 0 || g.n1h - 1 < KC) return false;
+  tl->n_outer = (int)(g.ncols / g.n1h);
+  tl->nkb = (g.n1h - 1) / KC;
+  tl->n_main = tl->n_outer * tl->nkb;
+  tl->n_tiles = tl->n_main + (tl->n_outer + KC - 1) / KC;
+  tl->tail_cols = std::min(KC, tl->n_outer);
+  return true;
+}
+
+// ring slots a program needs: term k may use loads up to max(la, lb, ldot) while only rel[k-1]
+// have been released (FIFO), so R must exceed that span or producer and consumers deadlock
+static int col_prog_span(const TProg& p) {
+  int span = 1, released = 0;
+  for (int k = 0; k < p.nt; ++k) {
+    int need = std::max<int>(p.la[k], std::max<int>(p.lb[k], p.ldot[k]));
+    span = std::max(span, need - released + 1);
+    released = p.rel[k];
+  }
+  return span;
+}
+
+template <int KIND, bool DOT>
+struct ColRing {  // ring depth: 3 slots unless the program's live span needs more (F3S + dot: 4)
+  static constexpr int R = (KIND == COL_F3S && DOT) ? 4 : DBF_COL_R;
+};
+
+template <int N, int KIND, bool DOT>
+static cudaError_t launch_col_tma_k(const TmaMaps& maps, const ColGeom& g, const ColTiles& tl, cudaStream_t s, int* grid_out) {
+  constexpr int R = ColRing<KIND, DOT>::R;
+  constexpr size_t smem = (size_t)(R + 2 + 1) * TmaCfg<N>::TILE + 2 * R * sizeof(uint64_t) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    if (col_prog_span(kColProgHost[2 * KIND + (DOT ? 1 : 0)]) > R) return cudaErrorInvalidConfiguration;
+    cudaError_t e = cudaFuncSetAttribute(col_tma_kernel<N, KIND, DOT, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int grid = std::min(tl.n_tiles, num_sms());
+  if (grid_out) *grid_out = grid;
+  col_tma_kernel<N, KIND, DOT, R><<<grid, TmaCfg<N>::THREADS, smem, s>>>(maps, g, tl);
+  return cudaGetLastError();
+}
+
+// returns cudaErrorNotSupported when this geometry must take the register-pipelined kernel
+template <int N>
+static cudaError_t launch_col_tma(int kind, const ColGeom& g, cudaStream_t s, int* grid_out) {
+  ColTiles tl;
+  if (!col_tma_tiles<N>(g, &tl)) return cudaErrorNotSupported;
+  constexpr int KC = TmaCfg<N>::KC;
+  TmaMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  const int nfi = kColNfIn[kind], nfo = kColNfOut[kind];
+  bool ok = col_map(&maps.in_m, g.in, N, g.n1h, g.in_psh, g.in_ps, g.in_pcs, tl.n_outer, g.in_os, nfi, g.in_fs, false, KC) &&
+            col_map(&maps.in_t, g.in, N, g.n1h, g.in_psh, g.in_ps, g.in_pcs, tl.n_outer, g.in_os, nfi, g.in_fs, true, KC) &&
+            col_map(&maps.out_m, g.out, N, g.n1h, g.out_psh, g.out_ps, g.out_pcs, tl.n_outer, g.out_os, nfo, g.out_fs, false, KC) &&
+            col_map(&maps.out_t, g.out, N, g.n1h, g.out_psh, g.out_ps, g.out_pcs, tl.n_outer, g.out_os, nfo, g.out_fs, true, KC);
+  const bool dot = g.dotp != nullptr;
+  if (ok && dot)
+    ok = col_map(&maps.dot_m, g.dotp, N, g.n1h, g.out_psh, g.out_ps, g.out_pcs, tl.n_outer, g.out_os, 3, g.out_fs, false, KC) &&
+         col_map(&maps.dot_t, g.dotp, N, g.n1h, g.out_psh, g.out_ps, g.out_pcs, tl.n_outer, g.out_os, 3, g.out_fs, true, KC);
+  if (!ok) return cudaErrorNotSupported;
+#define DBF_TK(K)                                                                            \
+  case K:                                                                                   \
+    return dot ? launch_col_tma_k<N, K, true>(maps, g, tl, s, grid_out)                     \
+               : launch_col_tma_k<N, K, false>(maps, g, tl, s, grid_out);
+  switch (kind) {
+    DBF_TK(COL_I1S) DBF_TK(COL_I1F) DBF_TK(COL_I2S) DBF_TK(COL_I2F) DBF_TK(COL_F2S) DBF_TK(COL_F2F) DBF_TK(COL_F3S)
+    DBF_TK(COL_F3F) DBF_TK(COL_ZI3) DBF_TK(COL_YI3)
+    default: return cudaErrorInvalidValue;
+  }
+#undef DBF_TK
+}
+
+static cudaError_t launch_col_reg(int kind, int N, const ColGeom& g, cudaStream_t s) {
   switch (N) {
     case 8: return launch_col_n<8>(kind, g, s);
     case 16: return launch_col_n<16>(kind, g, s);
@@ -1048,6 +1460,16 @@ cudaError_t launch_col(int kind, int N, const ColGeom& g, cudaStream_t s) {
     case 512: return launch_col_n<512>(kind, g, s);
     default: return cudaErrorInvalidValue;
   }
+}
+
+cudaError_t launch_col(int kind, int N, const ColGeom& g, cudaStream_t s, int* grid_out) {
+  cudaError_t e = cudaErrorNotSupported;
+  if (N == 256) e = launch_col_tma<256>(kind, g, s, grid_out);
+  else if (N == 128) e = launch_col_tma<128>(kind, g, s, grid_out);
+  else if (N == 64) e = launch_col_tma<64>(kind, g, s, grid_out);
+  if (e != cudaErrorNotSupported) return e;
+  if (grid_out) *grid_out = col_grid(N, g.ncols);
+  return launch_col_reg(kind, N, g, s);
 }
 
 template <int N1, int KIND>

@@ -84,7 +84,8 @@ struct XGeom {
 };
 
 // host launchers (passes.cu)
-cudaError_t launch_col(int kind, int N, const ColGeom& g, cudaStream_t s);
+// grid_out: CTAs launched (= per-CTA partials written when dotp is set)
+cudaError_t launch_col(int kind, int N, const ColGeom& g, cudaStream_t s, int* grid_out = nullptr);
 cudaError_t launch_x(int kind, int N1, const XGeom& g, cudaStream_t s, int* grid_out);
 int x_grid(int kind, int N1, long long nlines);
 int col_grid(int N, long long ncols);

@@ -92,6 +92,38 @@ def test_apply_K_finite_neohooke(dbf, n, tangent, monkeypatch):
     assert rel(gpu_full(dbf, f, n[0]), ref) <= 1e-12
 
 
+# grids whose z / y sweeps take the TMA column kernel (N in {64, 128, 256}, n1/2 a multiple of
+# 2048/N): several kx blocks + the Nyquist tail tiles, and an outer count (8) below the tile
+# width (16 at N = 128: narrower tail boxes)
+TMA_GRIDS = [(32, 128, 256), (64, 256, 128), (32, 8, 128), (128, 64, 64)]
+
+
+@pytest.mark.parametrize("n", TMA_GRIDS)
+def test_apply_K_tma_small(dbf, n):
+    ph = two_phase(n, 31)
+    ctx = dbf.DBFFT(n, kinematics="small")
+    ctx.set_phases(ph, ISO2)
+    u = ms.random_field((3, n[2], n[1], n[0]), 32)
+    f = ctx.apply_K(to_gpu_spec(dbf, u))
+    ref, _ = O.apply_K(O.fft(u), O.stiffness_field(ph, ISO2), O.frequency_grid(n))
+    assert rel(gpu_full(dbf, f, n[0]), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("n", TMA_GRIDS[:3])
+def test_apply_K_tma_finite(dbf, n):
+    ph = two_phase(n, 33)
+    mats = [dict(kind="neohooke", mu=1.0, kappa=2.5), dict(kind="neohooke", mu=10.0, kappa=25.0)]
+    F = np.eye(3).reshape(3, 3, 1, 1, 1) + 0.1 * ms.random_field((3, 3, n[2], n[1], n[0]), 34)
+    ctx = dbf.DBFFT(n, kinematics="finite")
+    ctx.set_phases(ph, mats)
+    ctx.eval_state(F.reshape(9, n[2], n[1], n[0]))
+    u = ms.random_field((3, n[2], n[1], n[0]), 35)
+    f = ctx.apply_K(to_gpu_spec(dbf, u))
+    _, K = O.neo_hookean(F, np.array([1.0, 10.0])[ph], np.array([2.5, 25.0])[ph])
+    ref, _ = O.apply_K(O.fft(u), K, O.frequency_grid(n), finite=True)
+    assert rel(gpu_full(dbf, f, n[0]), ref) <= 1e-12
+
+
 @pytest.mark.parametrize("n", [(8, 8, 8), (32, 16, 16)])
 def test_apply_K_j2_tangent(dbf, n):
     ph = two_phase(n, 3, 0.5)
@@ -120,7 +152,7 @@ def test_precond_and_aug(dbf):
     r = ms.random_field((3, n[2], n[1], n[0]), 13)
     z = ctx.precond(to_gpu_spec(dbf, r))
     XI = O.frequency_grid(n)
-    zref = O.precondition(O.fft(r), C.mean(axis=(-3, -2, -1)), XI)
+    zref = O.precondition(O.fft(r), O.volume_average(C), XI)
     assert rel(gpu_full(dbf, z, n[0]), zref) <= 1e-12
     mask = np.zeros((3, 3), bool); mask[0, 0] = mask[1, 1] = mask[0, 1] = mask[1, 0] = True
     e = np.array([[1e-3, 2e-4, 0], [2e-4, -5e-4, 0], [0, 0, 0.0]])
@@ -224,6 +256,21 @@ def test_solve_c4_twin_newton(dbf):
         assert rel(rep["macro_strain"], ref["mean_F"]) <= 1e-9
         assert rel(ctx.get_field(dbf.FIELD_STRAIN), ref["F"]) <= 1e-8
         assert rel(ctx.get_field(dbf.FIELD_STRESS), ref["P"]) <= 1e-8
+
+
+def test_solve_tma_grids(dbf):
+    """Full PCG solves (fused <p, Kp> in the F3 TMA kernel, both kinematics) on a grid whose
+    column sweeps take the TMA path."""
+    n = (32, 64, 128)
+    ph = two_phase(n, 36)
+    L = dict(target=np.diag([1e-3, 0.0, 0.0]), mask=np.zeros((3, 3), bool))
+    ref = O.solve_small_strain(ph, ISO2, L, tol=1e-10)
+    ctx = dbf.DBFFT(n, kinematics="small")
+    ctx.set_phases(ph, ISO2)
+    rep = ctx.solve_increment(L["target"], L["mask"])
+    assert rep["converged"]
+    assert rel(rep["macro_stress"], ref["mean_sig"]) <= 1e-9
+    assert rel(ctx.get_field(dbf.FIELD_STRESS), ref["sig"]) <= 1e-8
 
 
 def test_solve_c5_twin_j2(dbf):
