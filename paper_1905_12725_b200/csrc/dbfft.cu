@@ -258,6 +258,7 @@ ColGeom geom_I1(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf)
   g.ncols = (long long)s.nyl * n1h;
   g.tw = ctx->tw3;
   g.fq = Freq{ctx->xix, s.xiy, ctx->xiz};
+  g.n_xy = s.nyl;
   return g;
 }
 ColGeom geom_I2(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_in) {
@@ -269,6 +270,7 @@ ColGeom geom_I2(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_
   g.ncols = (long long)s.nzl * n1h;
   g.tw = ctx->tw2;
   g.fq = Freq{ctx->xix, ctx->xiy, ctx->xiz};
+  g.n_xy = ctx->n2;
   return g;
 }
 ColGeom geom_F2(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_out) {
@@ -280,6 +282,7 @@ ColGeom geom_F2(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_
   g.ncols = (long long)s.nzl * n1h;
   g.tw = ctx->tw2;
   g.fq = Freq{ctx->xix, ctx->xiy, ctx->xiz};
+  g.n_xy = ctx->n2;
   return g;
 }
 ColGeom geom_F3(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_in) {
@@ -291,6 +294,7 @@ ColGeom geom_F3(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_
   g.ncols = (long long)s.nyl * n1h;
   g.tw = ctx->tw3;
   g.fq = Freq{ctx->xix, s.xiy, ctx->xiz};
+  g.n_xy = s.nyl;
   return g;
 }
 
@@ -306,6 +310,7 @@ XGeom xgeom(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out) {
   g.tw = ctx->tw1;
   g.xix = ctx->xix;
   g.inv_n = 1.0 / (double)ctx->N;
+  g.oscale = 0.5 / (double)ctx->N;  // exact: N is a power of two
   g.partials = s.part_x;
   g.nred = 10;
   g.phase = s.phase;

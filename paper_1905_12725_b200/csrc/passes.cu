@@ -24,6 +24,9 @@
 #ifndef DBF_X_LRAW
 #define DBF_X_LRAW 192  // target threads per pass_X CTA (lines per CTA = DBF_X_LRAW / threads per line)
 #endif
+#ifndef DBF_X_STAGE_IN
+#define DBF_X_STAGE_IN 1
+#endif
 #ifndef DBF_COL_MINB
 #define DBF_COL_MINB 4
 #endif
@@ -35,6 +38,13 @@ namespace {
 struct ColAt {
   const ColGeom* g;
   int outer, pos, kx;
+  double xxk, xyo;  // xi_x(kx) and xi_y(outer) of the column (set with kx / outer; y passes: xyo unused)
+  DBF_DEV void set_col(int o, int k) {
+    outer = o;
+    kx = k;
+    xxk = __ldg(g->fq.xx + k);
+    xyo = __ldg(g->fq.xy + (o < g->n_xy ? o : 0));
+  }
   DBF_DEV long long in_idx(int f) const {
     long long p = (long long)(pos >> g->in_psh) * g->in_pcs + (long long)(pos & ((1 << g->in_psh) - 1)) * g->in_ps;
     return f * g->in_fs + outer * g->in_os + p + kx;
@@ -78,8 +88,8 @@ struct ColOp<COL_I1S> {
     switch (j) {
       case 0: case 1: return r0;
       case 2: return cimul(r0, xz);  // eps_zz
-      case 3: { const double xx = __ldg(a.g->fq.xx + a.kx); return cimul(make_double2(xz * r0.x + xx * r1.x, xz * r0.y + xx * r1.y), 0.5); }
-      default: { const double xy = __ldg(a.g->fq.xy + a.outer); return cimul(make_double2(xz * r0.x + xy * r1.x, xz * r0.y + xy * r1.y), 0.5); }
+      case 3: { const double xx = a.xxk; return cimul(make_double2(xz * r0.x + xx * r1.x, xz * r0.y + xx * r1.y), 0.5); }
+      default: { const double xy = a.xyo; return cimul(make_double2(xz * r0.x + xy * r1.x, xz * r0.y + xy * r1.y), 0.5); }
     }
   }
   DBF_DEV static cplx post(const ColAt&, int) { return make_double2(1.0, 0.0); }
@@ -113,9 +123,9 @@ struct ColOp<COL_I2S> {
   }
   DBF_DEV static cplx pre(const ColAt& a, int j, cplx r0, cplx r1) {
     switch (j) {
-      case 0: return cimul(r0, __ldg(a.g->fq.xx + a.kx));
+      case 0: return cimul(r0, a.xxk);
       case 1: return cimul(r0, __ldg(a.g->fq.xy + a.pos));
-      case 5: { const double xx = __ldg(a.g->fq.xx + a.kx), xy = __ldg(a.g->fq.xy + a.pos);
+      case 5: { const double xx = a.xxk, xy = __ldg(a.g->fq.xy + a.pos);
                 return cimul(make_double2(xy * r0.x + xx * r1.x, xy * r0.y + xx * r1.y), 0.5); }
       default: return r0;
     }
@@ -124,7 +134,8 @@ struct ColOp<COL_I2S> {
 };
 
 // y inverse, finite strain.  in: {u_0,u_1,u_2, G_0z,G_1z,G_2z}; out o = 3i+j:
-// j=0: u_i (x derivative applied in the x pass), j=1: i xi_y u_i, j=2: G_iz.
+// j=0: G_ix = i xi_x u_i (post-weight: xi_x is constant along a y column), j=1: G_iy = i xi_y u_i,
+// j=2: G_iz.
 template <>
 struct ColOp<COL_I2F> {
   static constexpr bool INV = true;
@@ -134,7 +145,9 @@ struct ColOp<COL_I2F> {
     return {j, 1, 1, jj == 2 ? 3 + i : i, -1};
   }
   DBF_DEV static cplx pre(const ColAt& a, int j, cplx r0, cplx) { return (j % 3 == 1) ? cimul(r0, __ldg(a.g->fq.xy + a.pos)) : r0; }
-  DBF_DEV static cplx post(const ColAt&, int) { return make_double2(1.0, 0.0); }
+  DBF_DEV static cplx post(const ColAt& a, int j) {
+    return (j % 3 == 0) ? make_double2(0.0, a.xxk) : make_double2(1.0, 0.0);
+  }
 };
 
 template <>
@@ -146,7 +159,7 @@ struct ColOp<COL_F2S> {
   DBF_DEV static cplx post(const ColAt&, int) { return make_double2(1.0, 0.0); }
 };
 
-// y forward, finite strain.  in o=3i+j: {g_i (xi_x folded), P_iy, P_iz};  out: g_i (+ -i xi_y P_iy), P_iz
+// y forward, finite strain.  in o=3i+j: {P_ix, P_iy, P_iz};  out: g_i = -i xi_x P_ix - i xi_y P_iy, P_iz
 template <>
 struct ColOp<COL_F2F> {
   static constexpr bool INV = false;
@@ -155,7 +168,9 @@ struct ColOp<COL_F2F> {
     if (j < 6) return {j / 2, (j & 1) == 0, (j & 1) == 1, 3 * (j / 2) + (j & 1), -1};
     return {j - 3, 1, 1, 3 * (j - 6) + 2, -1};
   }
-  DBF_DEV static cplx pre(const ColAt&, int, cplx r0, cplx) { return r0; }
+  DBF_DEV static cplx pre(const ColAt& a, int j, cplx r0, cplx) {
+    return (j < 6 && (j & 1) == 0) ? cimul(r0, -a.xxk) : r0;
+  }
   DBF_DEV static cplx post(const ColAt& a, int j) {
     if (j < 6 && (j & 1)) return make_double2(0.0, -__ldg(a.g->fq.xy + a.pos));
     return make_double2(1.0, 0.0);
@@ -178,7 +193,7 @@ struct ColOp<COL_F3S> {
   }
   DBF_DEV static cplx pre(const ColAt& a, int j, cplx r0, cplx r1) {
     if (j & 1) return r0;
-    const double xx = __ldg(a.g->fq.xx + a.kx), xy = __ldg(a.g->fq.xy + a.outer);
+    const double xx = a.xxk, xy = a.xyo;
     return cimul(make_double2(xx * r0.x + xy * r1.x, xx * r0.y + xy * r1.y), -1.0);
   }
   DBF_DEV static cplx post(const ColAt& a, int j) {
@@ -253,8 +268,7 @@ __global__ void __launch_bounds__(256, ColPref<KIND>::MINB) col_pass_kernel(ColG
   const bool valid = col < g.ncols;
   ColAt at;
   at.g = &g;
-  at.outer = valid ? (int)(col / g.n1h) : 0;
-  at.kx = valid ? (int)(col % g.n1h) : 0;
+  at.set_col(valid ? (int)(col / g.n1h) : 0, valid ? (int)(col % g.n1h) : 0);
   const double wdot = (at.kx == 0 || 2 * at.kx == g.n1) ? 1.0 : 2.0;
   double dot = 0.0;
   IdxCols<COLS> idx{c};
@@ -513,7 +527,7 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
     } else {
       voigt_contract_full(g.ptable + 36 * ph, e6, s);
     }
-    const double sg = (KIND == X_RHS_SMALL_PHASE) ? -1.0 : 1.0;
+    const double sg = (KIND == X_RHS_SMALL_PHASE) ? -g.oscale : g.oscale;
 #pragma unroll
     for (int I = 0; I < 6; ++I) {
       P[I] = sg * s[I];
@@ -530,7 +544,7 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
       double acc = 0.0;
 #pragma unroll
       for (int b = 0; b < 9; ++b) acc = fma(K[sym9(a, b)], e9[b], acc);
-      P[a] = acc;
+      P[a] = acc * g.oscale;
       red[a] += acc;
     }
   } else if (KIND == X_K_FIN_NH) {
@@ -541,9 +555,7 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
     const double mu = __ldg(g.ptable + 36 * ph), lam = __ldg(g.ptable + 36 * ph + 1) - 2.0 * mu / 3.0;
 #pragma unroll
     for (int a = 0; a < 9; ++a) e9[a] = G[a] + (g.e ? __ldg(g.e + a) : 0.0);
-    nh_apply(Fi, c1, mu, lam, e9, P);
-#pragma unroll
-    for (int a = 0; a < 9; ++a) red[a] += P[a];
+    nh_apply(Fi, c1 * g.oscale, mu * g.oscale, lam * g.oscale, e9, P);  // P x 1/(2N): exact (powers of 2)
   } else if (KIND == X_CONST_FIN) {
     double F[9], Pv[9], Fi[9], c1;
     double mx = 0.0;
@@ -570,7 +582,7 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
     }
 #pragma unroll
     for (int a = 0; a < 9; ++a) {
-      P[a] = -Pv[a];
+      P[a] = -g.oscale * Pv[a];
       red[a] += Pv[a];
     }
     red[9] = fmax(red[9], mx);
@@ -592,7 +604,7 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
 #pragma unroll
     for (int I = 0; I < 6; ++I) {
       g.epsp_t[(long long)I * g.nvox + v] = epn[I];
-      P[I] = -s[I];
+      P[I] = -g.oscale * s[I];
       red[c_row9_of_voigt[I]] += s[I];
     }
     red[9] = fmax(red[9], mx);
@@ -647,10 +659,29 @@ DBF_DEV void x_partner(const cplx (&a)[8], cplx (&zn)[8], int gq) {
   }
 }
 
+// pass_X line positions k = gq + s TPJ (TPJ PX = N1): k <= N1/2 ("lo", stored half spectrum)
+// is static except at s = PX/2, where only gq = 0 (k = N1/2) qualifies
+template <int N1, int PX, int TPJ>
+DBF_DEV bool x_lo(int s, int gq) {
+  if (TPJ * PX != N1) return 2 * (gq + s * TPJ) <= N1;
+  return s < PX / 2 || (s == PX / 2 && gq == 0);
+}
+// apply kinds reduce <out> from the R2C DC (sums over the line), no per-voxel accumulators
+template <int KIND>
+struct XDcRed {
+  static constexpr bool value = (KIND == X_K_SMALL_PHASE || KIND == X_K_J2 || KIND == X_K_FIN_TAN || KIND == X_K_FIN_NH);
+};
+// reduction slot (row-major 3x3) of output field f: Voigt components at small strain
+template <int KIND>
+DBF_DEV int x_red_slot(int f) {
+  if (XTraits<KIND>::FIN) return f;
+  return f == 0 ? 0 : f == 1 ? 4 : f == 2 ? 8 : f == 3 ? 5 : f == 4 ? 2 : 1;
+}
+
 // Which apply kinds stream their inputs through the shared-memory stage (bulk async copies)
 template <int KIND>
 struct XStage {
-  static constexpr bool IN = (KIND == X_K_SMALL_PHASE || KIND == X_K_J2 || KIND == X_K_FIN_TAN || KIND == X_K_FIN_NH);
+  static constexpr bool IN = DBF_X_STAGE_IN && (KIND == X_K_SMALL_PHASE || KIND == X_K_J2 || KIND == X_K_FIN_TAN || KIND == X_K_FIN_NH);
   static constexpr int NTAN = (KIND == X_K_J2) ? 8 : (KIND == X_K_FIN_NH) ? 10 : 0;  // staged per-voxel doubles
   static constexpr bool PH = (KIND == X_K_SMALL_PHASE || KIND == X_K_J2 || KIND == X_K_FIN_NH);
 };
@@ -755,6 +786,12 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
   const int cin = (KIND == X_REAL_OUT) ? nf_real : T::CIN;
   const bool do_in = (T::CIN > 0) && (cin > 0) && ((KIND != X_CONST_FIN && KIND != X_CONST_J2) || g.has_in);
   const long long ngroups = (g.nlines + LPAR - 1) / LPAR;
+  // apply kinds: <sigma> / <dP> from the k = 0 outputs of the R2C (one owner thread per field)
+  constexpr bool DCRED = XDcRed<KIND>::value;
+  __shared__ double s_dc[DCRED ? LPAR : 1][10];  // per line slot of the CTA: one owner thread per entry
+  if (DCRED)
+    for (int i = t; i < 10 * LPAR; i += CF::THREADS) s_dc[i / 10][i % 10] = 0.0;
+  if (DCRED) __syncthreads();
   double red[T::NRED > 0 ? T::NRED : 1];
 #pragma unroll
   for (int r = 0; r < (T::NRED > 0 ? T::NRED : 1); ++r) red[r] = 0.0;
@@ -784,7 +821,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
 #pragma unroll
       for (int s = 0; s < PX; ++s) {
         const int k = gq + s * TPJ;
-        const bool lo = (2 * k <= N1);
+        const bool lo = x_lo<N1, PX, TPJ>(s, gq);
         const int kk = lo ? k : N1 - k;
         cplx A = make_double2(0, 0), B = make_double2(0, 0);
         if (lvalid && fa < cin) {
@@ -795,11 +832,6 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
             const long long base = line * g.n1h + kk;
             A = __ldg(g.in + fa * g.fs_in + base);
             if (fb < cin) B = __ldg(g.in + fb * g.fs_in + base);
-          }
-          if (T::FIN) {  // G_ix = i xi_x u_i for the j = 0 slots (deferred gradient)
-            const double xx = __ldg(g.xix + kk);
-            if (fa % 3 == 0) A = cimul(A, xx);
-            if (fb % 3 == 0 && fb < cin) B = cimul(B, xx);
           }
           if (kk == 0 || 2 * kk == N1) { A.y = 0.0; B.y = 0.0; }  // Hermitian part (C2R)
         }
@@ -895,17 +927,17 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
 #pragma unroll
         for (int s = 0; s < PX; ++s) {
           const int k = gq + s * TPJ;
-          if (2 * k > N1) continue;
+          if (!x_lo<N1, PX, TPJ>(s, gq)) continue;
           const cplx Z = a[s];
           const cplx Zn = zn[s];
-          cplx A = make_double2(0.5 * (Z.x + Zn.x), 0.5 * (Z.y - Zn.y));
-          cplx B = make_double2(0.5 * (Z.y + Zn.y), -0.5 * (Z.x - Zn.x));
-          A = cscale(A, g.inv_n);
-          B = cscale(B, g.inv_n);
-          if (T::FIN) {  // fold -i xi_x P_ix into the j = 0 slots (early divergence)
-            const double xx = __ldg(g.xix + k);
-            if (fa % 3 == 0) A = cimul(A, -xx);
-            if (fb % 3 == 0) B = cimul(B, -xx);
+          // 2x the spectra of the pair: with the voxel outputs scaled by 1/(2N) this is the
+          // mean-normalised spectrum (R5)
+          const cplx A = make_double2(Z.x + Zn.x, Z.y - Zn.y);
+          const cplx B = make_double2(Z.y + Zn.y, Zn.x - Z.x);
+          if (DCRED && s == 0 && gq == 0) {  // k = 0: the line sums of the pair (<sigma> / <dP>)
+            const double dcs = 0.5 / g.oscale;  // undo the exact 1/(2N) of the voxel outputs
+            s_dc[DCRED ? l : 0][x_red_slot<KIND>(fa)] += dcs * A.x;
+            if (fb < COUT) s_dc[DCRED ? l : 0][x_red_slot<KIND>(fb)] += dcs * B.x;
           }
           const long long base = line * g.n1h + k;
           g.out[fa * g.fs_out + base] = A;
@@ -916,7 +948,14 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
     }
   }
 
-  if (T::NRED > 0) {
+  if (DCRED) {
+    __syncthreads();
+    if (t < T::NRED) {
+      double s = 0.0;
+      for (int q = 0; q < (DCRED ? LPAR : 1); ++q) s += s_dc[q][t];
+      g.partials[(long long)blockIdx.x * g.nred + t] = s;
+    }
+  } else if (T::NRED > 0) {
     // block reduction -> partials[block][nred] (sums; slot 9 of the const kinds is a max)
     __shared__ double sred[(CF::THREADS + 31) / 32][10];
     constexpr int nw = (CF::THREADS + 31) / 32;
@@ -1163,10 +1202,9 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
     const bool tail = tile >= tl.n_main;
     ColAt at;
     at.g = &g;
-    at.outer = tail ? (tile - tl.n_main) * KC + c : tile / tl.nkb;
-    at.kx = tail ? g.n1h - 1 : (tile % tl.nkb) * KC + c;
-    const bool valid = at.outer < tl.n_outer;
-    if (!valid) at.outer = 0;
+    const int outer = tail ? (tile - tl.n_main) * KC + c : tile / tl.nkb;
+    const bool valid = outer < tl.n_outer;
+    at.set_col(valid ? outer : 0, tail ? g.n1h - 1 : (tile % tl.nkb) * KC + c);
     const double wdot = (at.kx == 0 || 2 * at.kx == g.n1) ? 1.0 : 2.0;
     const uint32_t sbase = it * nl;
     int released = 0;

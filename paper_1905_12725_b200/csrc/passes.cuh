@@ -26,6 +26,7 @@ struct ColGeom {
   const cplx* dotp;
   double* partials;  // one double per CTA
   int n1;            // full x length (weights: kx = 0 and n1/2 count once)
+  int n_xy;          // length of fq.xy (guards the per-column xi_y(outer) lookup of y passes)
 };
 
 // Column pass kinds
@@ -65,6 +66,7 @@ struct XGeom {
   const cplx* tw;       // twiddles W_{n1}
   const double* xix;    // xi_x [n1h]
   double inv_n;         // 1 / (n1 n2 n3)
+  double oscale;        // 1 / (2N): voxel outputs are pre-scaled so the unnormalised pair R2C (x2) is F/N
   double* partials;     // per CTA reduction outputs [grid][nred]
   int nred;
   // materials / state (SoA, voxel index = line*n1 + x)
