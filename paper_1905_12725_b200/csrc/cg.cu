@@ -337,12 +337,25 @@ __global__ void __launch_bounds__(BLK) k_reduce(const double* partials, int nblk
   if (threadIdx.x < nred) out[threadIdx.x] = s[threadIdx.x];
 }
 
+// phase counts: per-CTA shared-memory histogram (integer atomics), one global add per phase and
+// CTA (a global atomic per voxel serialises on the few phase addresses: 19 ms at 256^3)
+constexpr int HIST_SMEM = 4096;
 __global__ void k_phase_hist(const uint16_t* __restrict__ ph, long long nvox, double* counts, int nphase, int* bad) {
+  __shared__ unsigned int h[HIST_SMEM];
+  const bool local = nphase <= HIST_SMEM;
+  if (local)
+    for (int i = threadIdx.x; i < nphase; i += blockDim.x) h[i] = 0u;
+  __syncthreads();
   for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < nvox; v += (long long)gridDim.x * blockDim.x) {
     const int p = ph[v];
     if (p >= nphase) atomicExch(bad, 1);
+    else if (local) atomicAdd(h + p, 1u);
     else atomicAdd(counts + p, 1.0);  // integer-valued doubles: exact below 2^53
   }
+  __syncthreads();
+  if (local)
+    for (int i = threadIdx.x; i < nphase; i += blockDim.x)
+      if (h[i]) atomicAdd(counts + i, (double)h[i]);
 }
 
 __global__ void k_fill(double* p, long long n, double v) {
