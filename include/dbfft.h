@@ -141,8 +141,18 @@ typedef struct {
   int32_t max_cg;      /* default 10000                                                 */
   int32_t max_newton;  /* default 25                                                            */
   int32_t check_every; /* host convergence poll period in CG iterations (default 4)             */
-  int32_t precond_refresh; /* 0: mean tangent at the first Newton iterate of every increment
-                              (R12); 1: every Newton iteration                            */
+  int32_t precond_refresh; /* mean-tangent refresh policy of M:
+                              0: at the first Newton iterate of every increment (R12, default);
+                              1: every Newton iteration; 2: never — the tangent of the undeformed
+                              state computed by set_phases ("initial tangent"); 3: at the
+                              first iterate of every precond_period-th increment ("once in a
+                              while").  Linear phases: M is fixed, the policy is unused.   */
+  int32_t precond_period;  /* policy 3 period in increments (>= 1, default 1)                     */
+  int32_t precond_medium;  /* reference medium of M for linear phases: 0 arithmetic mean <C>
+                              (Eq. pred3, default); 1 harmonic <C^-1>^-1; 2 Hill (mean of
+                              0 and 1) — the ad-hoc preconditioners of P:394.  Nonlinear families
+                              accept 0 only (DBFFT_E_INVALID_ARG otherwise).  Changes iteration
+                              counts only: the solution is that of the same system.               */
 } dbfft_opts;
 dbfft_opts dbfft_default_opts(void);
 

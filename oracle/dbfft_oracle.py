@@ -463,7 +463,54 @@ def _masks(load):
     return mask, target
 
 
-def solve_small_strain(phase, materials, load, tol=1e-10, max_iter=10000, L=(1.0, 1.0, 1.0), C=None):
+_MANDEL_IDX = [(0, 0), (1, 1), (2, 2), (1, 2), (0, 2), (0, 1)]
+_MANDEL_W = np.array([1.0, 1.0, 1.0, np.sqrt(2.0), np.sqrt(2.0), np.sqrt(2.0)])
+
+
+def to_mandel(C):
+    """6x6 Mandel matrix(es) of minor-symmetric C[i,j,k,l,...] (leading four indices)."""
+    M = np.empty((6, 6) + C.shape[4:])
+    for a, (i, j) in enumerate(_MANDEL_IDX):
+        for b, (k, l) in enumerate(_MANDEL_IDX):
+            M[a, b] = C[i, j, k, l] * _MANDEL_W[a] * _MANDEL_W[b]
+    return M
+
+
+def from_mandel(M):
+    """Full C[i,j,k,l] (minor and major symmetric) of a 6x6 Mandel matrix."""
+    C = np.empty((3, 3, 3, 3))
+    for a, (i, j) in enumerate(_MANDEL_IDX):
+        for b, (k, l) in enumerate(_MANDEL_IDX):
+            v = M[a, b] / (_MANDEL_W[a] * _MANDEL_W[b])
+            for (p, q) in {(i, j), (j, i)}:
+                for (r, s) in {(k, l), (l, k)}:
+                    C[p, q, r, s] = v
+    return C
+
+
+def reference_medium(C, medium="arithmetic"):
+    """Reference stiffness of the preconditioner M(xi) = [xi.C0.xi]^-1 (Eq. pred3).
+
+    "arithmetic": C0 = <C(x)> (the paper's choice).  "harmonic": <C(x)^-1>^-1 (Reuss),
+    "hill": their mean - the "new ad-hoc preconditioners" left as future work at P:394
+    (SURVEY 8(f4) reading: any symmetric positive-definite C0 keeps PCG valid and changes only
+    the iteration count).  Small-strain (minor-symmetric) fields only for the harmonic mean."""
+    CA = volume_average(C)
+    if medium == "arithmetic":
+        return CA
+    M = to_mandel(C)                                    # 6 x 6 x nz x ny x nx
+    Mv = np.moveaxis(M.reshape(6, 6, -1), -1, 0)        # voxels x 6 x 6
+    S = np.linalg.inv(Mv).mean(axis=0)                  # <C^-1> (Mandel)
+    CR = from_mandel(np.linalg.inv(S))
+    if medium == "harmonic":
+        return CR
+    if medium == "hill":
+        return 0.5 * (CA + CR)
+    raise ValueError(medium)
+
+
+def solve_small_strain(phase, materials, load, tol=1e-10, max_iter=10000, L=(1.0, 1.0, 1.0), C=None,
+                       medium="arithmetic"):
     """Linear small-strain DBFFT under strain/stress/mixed control.
 
     Unknown {u_hat | eps_f}.  eps_U = target on strain-controlled
@@ -477,7 +524,7 @@ def solve_small_strain(phase, materials, load, tol=1e-10, max_iter=10000, L=(1.0
     mask, target = _masks(load)
     eps_U = np.where(mask, 0.0, target)
     sig_f = np.where(mask, target, 0.0)
-    Cbar = volume_average(C)
+    Cbar = reference_medium(C, medium)  # P:255 (arithmetic, default) / P:394 variants
     basis = macro_basis(mask, symmetric=True)
     sig_U = contract(C, eps_U.reshape(3, 3, 1, 1, 1) * np.ones((1, 1, nz, ny, nx)))
     mean_sig_U = volume_average(sig_U)

@@ -142,6 +142,11 @@ struct dbfft_ctx_s {
   double Cbar[81];
   PrecQ prec;
   bool prec_valid = false;
+  // preconditioner variants: reference medium of linear phases, initial tangent
+  std::vector<double> h_counts;  // voxels per phase (global)
+  int prec_medium = 0;           // medium the linear prec was built with (0 arithmetic, 1 harmonic, 2 Hill)
+  double Cbar_init[81];          // mean tangent at the undeformed state (set_phases), policy 2
+  long long n_incr = 0;          // committed increments since set_phases (policy 3)
   CgDev* h_cg = nullptr;     // pinned mirror (slab 0)
   double* h_red = nullptr;   // pinned [64]
   int* h_bad = nullptr;
@@ -458,6 +463,23 @@ PrecQ make_prec(const double* C81) {
       q.Q[6 * m + p] = (j == l) ? C(i, j, k, l) : C(i, j, k, l) + C(i, l, k, j);
     }
   return q;
+}
+
+// Mandel 6x6 of a symmetric fourth-order tensor (w = 1 normal, sqrt 2 shear) and back
+const double kMw[6] = {1.0, 1.0, 1.0, 1.4142135623730950488, 1.4142135623730950488, 1.4142135623730950488};
+void full_to_mandel(const double* C81, double* M) {
+  for (int I = 0; I < 6; ++I)
+    for (int J = 0; J < 6; ++J)
+      M[6 * I + J] = kMw[I] * kMw[J] * C81[((kVoigtI[I] * 3 + kVoigtJ[I]) * 3 + kVoigtI[J]) * 3 + kVoigtJ[J]];
+}
+void mandel_to_full(const double* M, double* C81) {
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      for (int k = 0; k < 3; ++k)
+        for (int l = 0; l < 3; ++l) {
+          const int I = voigt_of(i, j), J = voigt_of(k, l);
+          C81[((i * 3 + j) * 3 + k) * 3 + l] = M[6 * I + J] / (kMw[I] * kMw[J]);
+        }
 }
 
 bool invert(std::vector<double>& A, int n) {  // Gauss-Jordan with partial pivoting, in place
@@ -887,7 +909,61 @@ dbfft_status copy_vec_all(dbfft_ctx ctx, cplx* Slab::*dst, cplx* Slab::*src) {
 }
 
 // ---------------------------------------------------------------- linear solve
+// Reference medium of the linear preconditioner from the phase counts.  0: the paper's
+// arithmetic mean C = <C(x)>; 1: harmonic mean <C(x)^-1>^-1 (Reuss); 2: Hill, the mean of
+// the two.  1 and 2 are the "new ad-hoc preconditioners" of P:394; every variant
+// only changes M, never the solution.
+dbfft_status linear_reference(dbfft_ctx ctx, int medium) {
+  const int nph = ctx->nph;
+  const double* pt = ctx->h_ptable.data();
+  double CA[81] = {0}, CR[81] = {0};
+  double CV[36] = {0};
+  for (int k = 0; k < nph; ++k)
+    for (int a = 0; a < 36; ++a) CV[a] += ctx->h_counts[k] * pt[36 * k + a];
+  for (int a = 0; a < 36; ++a) CV[a] /= (double)ctx->N;
+  voigt_to_full(CV, CA);
+  if (medium != 0) {
+    std::vector<double> S(36, 0.0);
+    for (int k = 0; k < nph; ++k) {
+      if (ctx->h_counts[k] == 0.0) continue;
+      double C81[81], M[36];
+      voigt_to_full(pt + 36 * k, C81);
+      full_to_mandel(C81, M);
+      std::vector<double> Mi(M, M + 36);
+      if (!invert(Mi, 6)) {
+        ctx->err = "harmonic reference medium: singular phase stiffness";
+        return DBFFT_E_MATERIAL;
+      }
+      for (int a = 0; a < 36; ++a) S[a] += ctx->h_counts[k] * Mi[a];
+    }
+    for (int a = 0; a < 36; ++a) S[a] /= (double)ctx->N;
+    if (!invert(S, 6)) {
+      ctx->err = "harmonic reference medium: singular mean compliance";
+      return DBFFT_E_MATERIAL;
+    }
+    mandel_to_full(S.data(), CR);
+  }
+  for (int a = 0; a < 81; ++a) ctx->Cbar[a] = medium == 0 ? CA[a] : medium == 1 ? CR[a] : 0.5 * (CA[a] + CR[a]);
+  ctx->prec = make_prec(ctx->Cbar);
+  ctx->prec_valid = true;
+  ctx->prec_medium = medium;
+  return DBFFT_OK;
+}
+
+dbfft_status check_opts(dbfft_ctx ctx, const dbfft_opts& o) {
+  if (o.precond_refresh < 0 || o.precond_refresh > 3 || o.precond_period < 1 || o.precond_medium < 0 || o.precond_medium > 2) {
+    ctx->err = "opts: precond_refresh in 0..3, precond_period >= 1, precond_medium in 0..2";
+    return DBFFT_E_INVALID_ARG;
+  }
+  if (o.precond_medium != 0 && ctx->family != FAM_LINEAR) {
+    ctx->err = "opts: precond_medium 1/2 (harmonic / Hill reference medium) needs linear phases";
+    return DBFFT_E_INVALID_ARG;
+  }
+  return DBFFT_OK;
+}
+
 dbfft_status solve_linear(dbfft_ctx ctx, const double* target, const uint8_t* mask, const dbfft_opts& o, dbfft_report* rep) {
+  if (o.precond_medium != ctx->prec_medium) CKS(linear_reference(ctx, o.precond_medium));
   double epsU[9], sigf[9];
   for (int a = 0; a < 9; ++a) {
     epsU[a] = mask[a] ? 0.0 : target[a];
@@ -1006,7 +1082,14 @@ dbfft_status solve_newton(dbfft_ctx ctx, const double* target, const uint8_t* ma
   double last = 0.0;
   bool conv = false;
   while (st == DBFFT_OK) {
-    if (newton == 0 || o.precond_refresh) {
+    // preconditioner refresh policy ("computed at the beginning of the increment ... can be
+    // recomputed once in a while"; "computed with the initial tangent stiffness")
+    if (o.precond_refresh == 2) {
+      if (newton == 0) {
+        memcpy(ctx->Cbar, ctx->Cbar_init, sizeof(ctx->Cbar));
+        ctx->prec = make_prec(ctx->Cbar);
+      }
+    } else if (o.precond_refresh == 1 || (newton == 0 && (o.precond_refresh == 0 || ctx->n_incr % o.precond_period == 0))) {
       st = refresh_mean_tangent(ctx);
       if (st != DBFFT_OK) break;
     }
@@ -1064,6 +1147,7 @@ dbfft_status solve_newton(dbfft_ctx ctx, const double* target, const uint8_t* ma
     if (!fin) CK(cudaMemcpyAsync(s.epsp_c, s.epsp_t, sizeof(double) * 6 * s.Nloc, cudaMemcpyDeviceToDevice, ctx->stream));
   }
   memcpy(ctx->Fbar_c, ctx->Fbar, sizeof(ctx->Fbar));
+  ++ctx->n_incr;
   CK(cudaStreamSynchronize(ctx->stream));
   return DBFFT_OK;
 }
@@ -1201,6 +1285,8 @@ dbfft_opts dbfft_default_opts(void) {
   o.max_newton = 25;
   o.check_every = 4;
   o.precond_refresh = 0;
+  o.precond_period = 1;
+  o.precond_medium = 0;
   return o;
 }
 
@@ -1459,14 +1545,10 @@ dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t o
     CK(cudaMemsetAsync(sl.u_c, 0, sizeof(cplx) * 3 * sl.Hs, ctx->stream));
   }
   for (int a = 0; a < 9; ++a) ctx->Fbar[a] = ctx->Fbar_c[a] = (fam == FAM_NEOHOOKE && a % 4 == 0) ? 1.0 : 0.0;
+  ctx->h_counts = cnt;
+  ctx->n_incr = 0;
   if (fam == FAM_LINEAR) {
-    double CV[36] = {0};
-    for (int k = 0; k < n_phases; ++k)
-      for (int a = 0; a < 36; ++a) CV[a] += cnt[k] * pt[36 * k + a];
-    for (int a = 0; a < 36; ++a) CV[a] /= (double)ctx->N;
-    voigt_to_full(CV, ctx->Cbar);
-    ctx->prec = make_prec(ctx->Cbar);
-    ctx->prec_valid = true;
+    CKS(linear_reference(ctx, 0));
   } else {
     const int nf = fam == FAM_NEOHOOKE ? 9 : 6;
     const char* tm = getenv("DBFFT_TANGENT");
@@ -1494,6 +1576,7 @@ dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t o
     if (s != DBFFT_OK) return s;
     s = refresh_mean_tangent(ctx);
     if (s != DBFFT_OK) return s;
+    memcpy(ctx->Cbar_init, ctx->Cbar, sizeof(ctx->Cbar));  // refresh policy 2
   }
   CK(cudaStreamSynchronize(ctx->stream));
   return DBFFT_OK;
@@ -1601,6 +1684,7 @@ dbfft_status dbfft_solve_increment(dbfft_ctx ctx, const double target[9], const 
   }
   CKS(check_target(ctx, target, mask));
   dbfft_opts o = opts ? *opts : dbfft_default_opts();
+  CKS(check_opts(ctx, o));
   auto t0 = std::chrono::steady_clock::now();
   if (report) {
     memset(report, 0, sizeof(*report));

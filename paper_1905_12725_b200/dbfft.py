@@ -24,7 +24,8 @@ class Material(ctypes.Structure):
 class Opts(ctypes.Structure):
     _fields_ = [("tol_eq", ctypes.c_double), ("tol_load", ctypes.c_double), ("tol_newton", ctypes.c_double),
                 ("max_cg", ctypes.c_int32), ("max_newton", ctypes.c_int32), ("check_every", ctypes.c_int32),
-                ("precond_refresh", ctypes.c_int32)]
+                ("precond_refresh", ctypes.c_int32), ("precond_period", ctypes.c_int32),
+                ("precond_medium", ctypes.c_int32)]
 
 
 class Report(ctypes.Structure):

@@ -284,3 +284,66 @@ def test_solve_c5_twin_j2(dbf):
         assert rep["converged"]
         assert rel(rep["macro_stress"], ref["mean_sig"]) <= 1e-9
         assert rel(ctx.get_field(dbf.FIELD_STRESS), ref["sig"]) <= 1e-8
+
+
+# ------------------------------------------------------------- preconditioner variants (8(f4))
+
+NU2 = [dict(kind="iso", E=1.0, nu=0.2), dict(kind="iso", E=100.0, nu=0.45)]
+
+
+@pytest.mark.parametrize("medium", [0, 1, 2])
+def test_solve_reference_media(dbf, medium):
+    """Reference medium of M (P:255 arithmetic; P:394 harmonic / Hill): the GPU takes the same
+    PCG path as the oracle with the same medium (iteration count) and the same solution."""
+    cfg = configs.c2(n=32, radius_vox=3)
+    L = cfg["loads"][0]
+    name = ("arithmetic", "harmonic", "hill")[medium]
+    ref = O.solve_small_strain(cfg["phase"], NU2, L, tol=1e-10, medium=name)
+    ctx = dbf.DBFFT(cfg["n"], kinematics="small")
+    ctx.set_phases(cfg["phase"], NU2)
+    rep = ctx.solve_increment(L["target"], L["mask"], precond_medium=medium)
+    assert rep["converged"]
+    # same M, same algorithm: counts agree up to round-off near the stop test (~135 iterations)
+    assert abs(rep["cg_iters"] - ref["iters"]) <= max(2, 0.03 * ref["iters"]), (rep["cg_iters"], ref["iters"])
+    assert rel(rep["macro_stress"], ref["mean_sig"]) <= 1e-9
+    assert rel(ctx.get_field(dbf.FIELD_STRESS), ref["sig"]) <= 1e-8
+
+
+@pytest.mark.parametrize("policy", [(1, 1), (2, 1), (3, 2)])
+def test_solve_refresh_policies_finite(dbf, policy):
+    """Mean-tangent refresh of M every Newton iteration / never (initial tangent) / every
+    2nd increment: same Newton path and converged state as the oracle's per-increment
+    refresh (the preconditioner never changes the solution)."""
+    cfg = configs.c4(n=32, radius_vox=3, increments=10)
+    st = O.FiniteStrainState(cfg["n"])
+    ctx = dbf.DBFFT(cfg["n"], kinematics="finite")
+    ctx.set_phases(cfg["phase"], cfg["materials"])
+    for L in cfg["loads"][:3]:
+        ref = O.solve_finite_increment(st, cfg["phase"], cfg["materials"], L, tol=1e-10)
+        rep = ctx.solve_increment(L["target"], L["mask"], precond_refresh=policy[0], precond_period=policy[1])
+        assert rep["converged"] and rep["newton_iters"] == ref["newton_iters"]
+        assert rel(rep["macro_stress"], ref["mean_P"]) <= 1e-9
+        assert rel(ctx.get_field(dbf.FIELD_STRAIN), ref["F"]) <= 1e-8
+
+
+def test_solve_refresh_initial_j2(dbf):
+    cfg = configs.c5(n=16, grains=6, increments=4)
+    st = O.J2State(cfg["n"])
+    ctx = dbf.DBFFT(cfg["n"], kinematics="small")
+    ctx.set_phases(cfg["phase"], cfg["materials"])
+    for L in cfg["loads"]:
+        ref = O.solve_j2_increment(st, cfg["phase"], cfg["materials"], L, 1.0, tol=1e-10)
+        rep = ctx.solve_increment(L["target"], L["mask"], dt=1.0, precond_refresh=2)
+        assert rep["converged"]
+        assert rel(rep["macro_stress"], ref["mean_sig"]) <= 1e-9
+        assert rel(ctx.get_field(dbf.FIELD_STRESS), ref["sig"]) <= 1e-8
+
+
+def test_precond_opts_rejected(dbf):
+    cfg = configs.c4(n=8, radius_vox=1)
+    ctx = dbf.DBFFT(cfg["n"], kinematics="finite")
+    ctx.set_phases(cfg["phase"], cfg["materials"])
+    L = cfg["loads"][0]
+    for bad in (dict(precond_medium=1), dict(precond_refresh=4), dict(precond_refresh=3, precond_period=0)):
+        with pytest.raises(dbf.DBFFTError):
+            ctx.solve_increment(L["target"], L["mask"], **bad)

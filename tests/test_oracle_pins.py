@@ -550,3 +550,51 @@ def test_volume_average_exact_sum():
     n1 = int(ph.sum())
     closed = ((N - n1) * C0 + n1 * C1) / N
     assert np.abs(m - closed).max() <= 1e-15 * np.abs(closed).max()
+
+
+def test_reference_media_closed_forms_and_order():
+    """P:255 / P:394 reference media.  Homogeneous field: all media equal C.
+    Two isotropic phases: the harmonic mean is isotropic with K = 1/<1/K>, mu = 1/<1/mu>
+    (closed form), and Reuss <= Hill <= Voigt in the Loewner order (Mandel eigenvalues)."""
+    n = (8, 8, 8)
+    mats = [dict(kind="iso", E=1.0, nu=0.3), dict(kind="iso", E=10.0, nu=0.25)]
+    C0 = O.stiffness_field(np.zeros(n, np.uint16), mats)
+    for m in ("arithmetic", "harmonic", "hill"):
+        assert np.allclose(O.reference_medium(C0, m), C0[..., 0, 0, 0], rtol=1e-14, atol=1e-15)
+    u = ms.SplitMix64(9).uniform(512).reshape(n)
+    ph = (u < 0.35).astype(np.uint16)
+    C = O.stiffness_field(ph, mats)
+    f1 = ph.mean()
+
+    def KG(E, nu):
+        return E / (3 * (1 - 2 * nu)), E / (2 * (1 + nu))
+    (K0, G0), (K1, G1) = KG(1.0, 0.3), KG(10.0, 0.25)
+    KR = 1.0 / ((1 - f1) / K0 + f1 / K1)
+    GR = 1.0 / ((1 - f1) / G0 + f1 / G1)
+    CR = O.isotropic_from_lame(KR - 2.0 * GR / 3.0, GR)
+    assert np.allclose(O.reference_medium(C, "harmonic"), CR, rtol=1e-13, atol=1e-14)
+    MV = _mandel(O.reference_medium(C, "arithmetic"))
+    MH = _mandel(O.reference_medium(C, "hill"))
+    MR = _mandel(O.reference_medium(C, "harmonic"))
+    assert np.linalg.eigvalsh(MV - MH).min() >= -1e-12
+    assert np.linalg.eigvalsh(MH - MR).min() >= -1e-12
+
+
+def test_reference_medium_changes_iterations_not_solution():
+    """The preconditioner's reference medium (P:394 variants) never changes the solution of the
+    system.  c2 structure at 24^3 (mixed control, E contrast 100, equal nu): isotropic phases of
+    equal nu make every medium a multiple of <C>, and PCG is invariant under M -> cM, so the
+    iteration counts are identical too; with unequal nu (0.2 / 0.45) they differ."""
+    cfg = configs.c2(n=24, radius_vox=2)
+    L = cfg["loads"][0]
+    for mats, same_iters in ((cfg["materials"], True),
+                             ([dict(kind="iso", E=1.0, nu=0.2), dict(kind="iso", E=100.0, nu=0.45)], False)):
+        res = {m: O.solve_small_strain(cfg["phase"], mats, L, tol=1e-11, medium=m)
+               for m in ("arithmetic", "harmonic", "hill")}
+        ref = res["arithmetic"]
+        for m in ("harmonic", "hill"):
+            r = res[m]
+            assert np.linalg.norm(r["mean_sig"] - ref["mean_sig"]) <= 1e-9 * np.linalg.norm(ref["mean_sig"])
+            assert np.linalg.norm(r["sig"] - ref["sig"]) <= 1e-8 * np.linalg.norm(ref["sig"])
+        n_iters = {res[m]["iters"] for m in res}
+        assert (len(n_iters) == 1) == same_iters, n_iters
