@@ -96,7 +96,11 @@ dbfft_status dbfft_spectral_layout(dbfft_ctx ctx, int64_t shape[4], int64_t stri
  *                        C'_ijkl = R_ia R_jb R_kc R_ld C_abcd, R row-major        small strain
  *   DBFFT_MAT_NEOHOOKE : p = {mu, kappa}                  compressible neo-Hookean (R14)   finite
  *   DBFFT_MAT_J2       : p = {E, nu, sigma_y, n, edot0}   J2 Perzyna overstress (R16)     small
- * Linear kinds require no state; NEOHOOKE and J2 keep per-voxel state.
+ *   DBFFT_MAT_SVK      : p = {E, nu}                      Saint Venant-Kirchhoff:
+ *                        S = lam tr(E) I + 2 mu E, E = (F^T F - I)/2, P = F S        finite
+ * NEOHOOKE and SVK phases may be mixed (one finite-strain hyperelastic family); with any SVK
+ * phase the 45-entry tangent is stored.
+ * Linear kinds require no state; NEOHOOKE, SVK and J2 keep per-voxel state.
  * Tangent storage (implementation choice, same operator): NEOHOOKE keeps F^-1 and
  * c1 = mu - lam ln J per voxel and applies K:G = mu G + c1 (F^-1 G F^-1)^T + lam tr(F^-1 G) F^-T
  * matrix-free (80 B/voxel); environment DBFFT_TANGENT=full stores the 45 independent entries of
@@ -105,7 +109,8 @@ typedef enum {
   DBFFT_MAT_ISO = 1,
   DBFFT_MAT_CUBIC = 2,
   DBFFT_MAT_NEOHOOKE = 3,
-  DBFFT_MAT_J2 = 4
+  DBFFT_MAT_J2 = 4,
+  DBFFT_MAT_SVK = 5
 } dbfft_mat_kind;
 typedef struct { int32_t kind; double p[36]; } dbfft_material;
 

@@ -193,6 +193,8 @@ def material_stiffness(m):
     if m["kind"] == "neohooke":
         mu, kappa = m["mu"], m["kappa"]
         return isotropic_from_lame(kappa - 2.0 * mu / 3.0, mu)
+    if m["kind"] == "svk":
+        return isotropic_stiffness(m["E"], m["nu"])
     raise ValueError(m["kind"])
 
 
@@ -230,6 +232,52 @@ def neo_hookean(F, mu, kappa):
                 for l in range(3):
                     K[i, j, k, l] = (mu * I3[i, k] * I3[j, l] + c1 * Finv[l, i] * Finv[j, k]
                                      + lam * Finv[j, i] * Finv[l, k])
+    return P, K
+
+
+def svk(F, E, nu):
+    """Saint Venant-Kirchhoff (SS3.3 matrix and voids): W = lam/2 (tr E)^2 + mu E:E,
+    E = (F^T F - I)/2.  Returns (P, K): S = lam tr(E) I + 2 mu E, P = F S, and
+    K_ijkl = dP_ij/dF_kl = d_ik S_lj + lam F_ij F_kl + mu (F_il F_kj + (F F^T)_ik d_jl).
+    F: [3,3,...]; E, nu broadcastable."""
+    lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu))
+    mu = E / (2.0 * (1.0 + nu))
+    C = np.einsum("ki...,kj...->ij...", F, F)
+    Eg = 0.5 * (C - I3.reshape((3, 3) + (1,) * (F.ndim - 2)))
+    trE = Eg[0, 0] + Eg[1, 1] + Eg[2, 2]
+    S = 2.0 * mu * Eg + lam * trE * I3.reshape((3, 3) + (1,) * (F.ndim - 2))
+    P = np.einsum("ip...,pj...->ij...", F, S)
+    B = np.einsum("ip...,kp...->ik...", F, F)
+    K = np.zeros((3, 3, 3, 3) + F.shape[2:])
+    for i in range(3):
+        for j in range(3):
+            for k in range(3):
+                for l in range(3):
+                    K[i, j, k, l] = (I3[i, k] * S[l, j] + lam * F[i, j] * F[k, l]
+                                     + mu * (F[i, l] * F[k, j] + B[i, k] * I3[j, l]))
+    return P, K
+
+
+def hyperelastic(F, phase, materials):
+    """(P, K) voxelwise for a finite-strain phase map (neo-Hookean R14 / SVK P:326 phases)."""
+    kinds = np.array([m["kind"] for m in materials])
+    P = np.zeros_like(F)
+    K = np.zeros((3, 3) + F.shape)
+    for kind in set(kinds.tolist()):
+        sel = np.isin(phase, np.nonzero(kinds == kind)[0])
+        Fs = F[:, :, sel]
+        if kind == "neohooke":
+            mu = np.array([m.get("mu", 0.0) for m in materials])[phase][sel]
+            kap = np.array([m.get("kappa", 0.0) for m in materials])[phase][sel]
+            Ps, Ks = neo_hookean(Fs, mu, kap)
+        elif kind == "svk":
+            E = np.array([m.get("E", 0.0) for m in materials])[phase][sel]
+            nu = np.array([m.get("nu", 0.0) for m in materials])[phase][sel]
+            Ps, Ks = svk(Fs, E, nu)
+        else:
+            raise ValueError(kind)
+        P[:, :, sel] = Ps
+        K[:, :, :, :, sel] = Ks
     return P, K
 
 
@@ -567,12 +615,10 @@ def solve_finite_increment(state, phase, materials, load, tol=1e-10, tol_newton=
     (P:204), b = F(div P) and P(Pbar - <P>) (P:215, P:233-234 read as R11);
     K_bar and M at i = 0 (R12); solve the linear system by
     PCG; u~ += du~, Fbar_f += dF_f; stop when max|grad du~ + dF_f| < tol_newton
-    (R10).  Materials: neo-Hookean per phase.  Modifies `state`."""
+    (R10).  Materials: neo-Hookean (R14) / SVK per phase.  Modifies `state`."""
     nz, ny, nx = phase.shape
     XI = frequency_grid((nx, ny, nz), L)
     mask, target = _masks(load)
-    mu = np.array([m["mu"] for m in materials])[phase]
-    kappa = np.array([m["kappa"] for m in materials])[phase]
     Fbar = np.where(mask, state.Fbar, target)
     P_f = np.where(mask, target, 0.0)
     basis = macro_basis(mask, symmetric=False)
@@ -582,7 +628,7 @@ def solve_finite_increment(state, phase, materials, load, tol=1e-10, tol_newton=
     newton = 0
     Kbar = None
     while True:
-        P, K = neo_hookean(F, mu, kappa)
+        P, K = hyperelastic(F, phase, materials)
         meanP = volume_average(P)
         b = Aug(rhs_from_stress(P, XI), np.where(mask, P_f - meanP, 0.0))
         if Kbar is None:
@@ -607,7 +653,7 @@ def solve_finite_increment(state, phase, materials, load, tol=1e-10, tol_newton=
             break
     last = np.max(np.abs(dG))
     state.Fbar = Fbar
-    P, _ = neo_hookean(F, mu, kappa)
+    P, _ = hyperelastic(F, phase, materials)
     return dict(F=F, P=P, mean_F=volume_average(F), mean_P=volume_average(P),
                 cg_iters=total_cg, newton_iters=newton, converged=bool(last < tol_newton))
 

@@ -330,3 +330,46 @@ struct SyncWarp {
 struct SyncCta {
   DBF_DEV void operator()() const { __syncthreads(); }
 };
+
+// ---------------------------------------------------------------------------------------------
+// Saint Venant-Kirchhoff hyperelasticity (the paper's SS3.3 matrix and voids):
+//   E = (F^T F - I)/2,  S = lam tr(E) I + 2 mu E,  P = F S,
+//   K_ijkl = dP_ij/dF_kl = d_ik S_lj + lam F_ij F_kl + mu (F_il F_kj + (F F^T)_ik d_jl)
+// (major symmetric).  F, P row-major 3x3; K45 = upper triangle of the 9x9 (a = 3i+j <= b = 3k+l).
+// ---------------------------------------------------------------------------------------------
+DBF_DEV void svk_stress(const double* F, double mu, double lam, double* P, double* S) {
+  double C[9];
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) C[3 * p + q] = F[p] * F[q] + F[3 + p] * F[3 + q] + F[6 + p] * F[6 + q];
+  const double trE = 0.5 * (C[0] + C[4] + C[8] - 3.0);
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) S[3 * p + q] = mu * (C[3 * p + q] - (p == q ? 1.0 : 0.0)) + (p == q ? lam * trE : 0.0);
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) P[3 * i + j] = F[3 * i] * S[j] + F[3 * i + 1] * S[3 + j] + F[3 * i + 2] * S[6 + j];
+}
+
+DBF_DEV void svk_tangent45(const double* F, const double* S, double mu, double lam, double* K45) {
+  double B[9];  // F F^T
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) B[3 * i + k] = F[3 * i] * F[3 * k] + F[3 * i + 1] * F[3 * k + 1] + F[3 * i + 2] * F[3 * k + 2];
+#pragma unroll
+  for (int a = 0; a < 9; ++a) {
+    const int i = a / 3, j = a % 3;
+#pragma unroll
+    for (int b = a; b < 9; ++b) {
+      const int k = b / 3, l = b % 3;
+      double v = lam * F[3 * i + j] * F[3 * k + l] + mu * F[3 * i + l] * F[3 * k + j];
+      if (i == k) v += S[3 * l + j];
+      if (j == l) v += mu * B[3 * i + k];
+      K45[a * 9 - a * (a - 1) / 2 + (b - a)] = v;
+    }
+  }
+}

@@ -591,6 +591,12 @@ __global__ void k_stress_nh(const double* __restrict__ F9, const uint16_t* __res
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     double F[9];
     for (int a = 0; a < 9; ++a) F[a] = F9[(long long)a * n + i];
+    if (pt[36 * ph[i] + 2] != 0.0) {  // Saint Venant-Kirchhoff
+      double P[9], S[9];
+      svk_stress(F, pt[36 * ph[i]], pt[36 * ph[i] + 1], P, S);
+      for (int a = 0; a < 9; ++a) P9[(long long)a * n + i] = P[a];
+      continue;
+    }
     const double mu = pt[36 * ph[i]], kappa = pt[36 * ph[i] + 1];
     const double lam = kappa - 2.0 * mu / 3.0;
     const double c00 = F[4] * F[8] - F[5] * F[7], c01 = F[5] * F[6] - F[3] * F[8], c02 = F[3] * F[7] - F[4] * F[6];
@@ -1457,6 +1463,7 @@ dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t o
     return DBFFT_E_INVALID_ARG;
   }
   int fam = FAM_NONE;
+  bool has_svk = false;
   std::vector<double> pt(36 * (size_t)n_phases, 0.0);
   for (int k = 0; k < n_phases; ++k) {
     const dbfft_material& m = table[k];
@@ -1476,7 +1483,16 @@ dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t o
         if (!(m.p[0] > 0)) { ctx->err = "NEOHOOKE: need mu > 0"; return DBFFT_E_INVALID_ARG; }
         d[0] = m.p[0];
         d[1] = m.p[1];
+        d[2] = 0.0;  // model flag: neo-Hookean
         f = FAM_NEOHOOKE;
+        break;
+      case DBFFT_MAT_SVK:
+        if (!(m.p[0] > 0) || !(m.p[1] > -1.0 && m.p[1] < 0.5)) { ctx->err = "SVK: need E > 0, -1 < nu < 0.5"; return DBFFT_E_INVALID_ARG; }
+        d[0] = m.p[0] / (2.0 * (1.0 + m.p[1]));                         // mu
+        d[1] = m.p[0] * m.p[1] / ((1.0 + m.p[1]) * (1.0 - 2.0 * m.p[1]));  // lam
+        d[2] = 1.0;  // model flag: Saint Venant-Kirchhoff
+        f = FAM_NEOHOOKE;  // finite-strain hyperelastic family
+        has_svk = true;
         break;
       case DBFFT_MAT_J2:
         if (!(m.p[0] > 0) || !(m.p[1] > -1.0 && m.p[1] < 0.5) || !(m.p[2] > 0) || !(m.p[3] > 0) || !(m.p[4] > 0)) {
@@ -1497,7 +1513,7 @@ dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t o
     fam = f;
   }
   if ((fam == FAM_NEOHOOKE) != (ctx->kin == 9)) {
-    ctx->err = "NEOHOOKE requires a finite-strain context; ISO/CUBIC/J2 a small-strain one";
+    ctx->err = "NEOHOOKE/SVK require a finite-strain context; ISO/CUBIC/J2 a small-strain one";
     return DBFFT_E_INVALID_ARG;
   }
   dbfft_status s;
@@ -1552,7 +1568,8 @@ dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t o
   } else {
     const int nf = fam == FAM_NEOHOOKE ? 9 : 6;
     const char* tm = getenv("DBFFT_TANGENT");
-    ctx->tmode = (tm && strcmp(tm, "full") == 0) ? 0 : 1;
+    // the matrix-free compact tangent is neo-Hookean's; SVK phases store the 45-entry tangent
+    ctx->tmode = ((tm && strcmp(tm, "full") == 0) || has_svk) ? 0 : 1;
     const int nk = fam == FAM_NEOHOOKE ? (ctx->tmode ? 10 : 45) : 8;
     for (Slab& sl : ctx->slabs) {
       if ((s = dalloc(ctx, &sl.F, (size_t)nf * sl.Nloc)) != DBFFT_OK) return s;

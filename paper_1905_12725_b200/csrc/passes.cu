@@ -567,6 +567,21 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
       g.F[(long long)a * g.nvox + v] = F[a];
     }
     const int ph = __ldg(g.phase + v);
+    if (__ldg(g.ptable + 36 * ph + 2) != 0.0) {  // Saint Venant-Kirchhoff phase (full tangent storage)
+      const double mu = __ldg(g.ptable + 36 * ph), lam = __ldg(g.ptable + 36 * ph + 1);
+      double S[9], K45[45];
+      svk_stress(F, mu, lam, Pv, S);
+      svk_tangent45(F, S, mu, lam, K45);
+#pragma unroll
+      for (int k = 0; k < 45; ++k) g.tan[(long long)k * g.nvox + v] = K45[k];
+#pragma unroll
+      for (int a = 0; a < 9; ++a) {
+        P[a] = -g.oscale * Pv[a];
+        red[a] += Pv[a];
+      }
+      red[9] = fmax(red[9], mx);
+      return;
+    }
     const double mu = __ldg(g.ptable + 36 * ph), kappa = __ldg(g.ptable + 36 * ph + 1);
     const double J = neo_hookean(F, mu, kappa, Pv, Fi, &c1);
     if (!(J > 0.0)) atomicMin(g.bad, (int)min(v, (long long)0x7fffffff));

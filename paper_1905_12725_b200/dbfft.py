@@ -35,7 +35,7 @@ class Report(ctypes.Structure):
                 ("macro_stress", ctypes.c_double * 9), ("bad_voxel", ctypes.c_int64), ("seconds", ctypes.c_double)]
 
 
-MAT_ISO, MAT_CUBIC, MAT_NEOHOOKE, MAT_J2 = 1, 2, 3, 4
+MAT_ISO, MAT_CUBIC, MAT_NEOHOOKE, MAT_J2, MAT_SVK = 1, 2, 3, 4, 5
 FIELD_U, FIELD_STRAIN, FIELD_STRESS, FIELD_U_HAT = 0, 1, 2, 3
 STATUS = {0: "OK", 1: "E_INVALID_GRID", 2: "E_INVALID_ARG", 3: "E_STATE", 4: "E_CUDA", 5: "E_NCCL", 6: "E_OOM",
           7: "E_NOT_CONVERGED", 8: "E_BREAKDOWN", 9: "E_MATERIAL"}
@@ -107,6 +107,8 @@ def material_record(m):
         rec.kind, vals = MAT_NEOHOOKE, [m["mu"], m["kappa"]]
     elif k == "j2":
         rec.kind, vals = MAT_J2, [m["E"], m["nu"], m["sigma_y"], m["n"], m["edot0"]]
+    elif k == "svk":
+        rec.kind, vals = MAT_SVK, [m["E"], m["nu"]]
     else:
         raise ValueError(k)
     for i, v in enumerate(vals):

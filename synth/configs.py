@@ -10,6 +10,7 @@ Material records: dict(kind=..., params...) with kinds
   'cubic'    : C11, C12, C44, R (3x3)      (crystal frame stiffness + rotation)
   'neohooke' : mu, kappa                   (R14)
   'j2'       : E, nu, sigma_y, n, edot0    (R16)
+  'svk'      : E, nu                       (Saint Venant-Kirchhoff)
 Load: target (3x3), mask (3x3 bool, True = stress-controlled).
 """
 import numpy as np
@@ -88,4 +89,19 @@ def c5s(n=128, grains=31, seed=5, increments=20):
     return d
 
 
-CONFIGS = dict(c1=c1, c2=c2, c3=c3, c4=c4, c5=c5, c5s=c5s)
+def p33(n=64, pores=5, vf=0.2, seed=33, increments=5, stretch=2.0):
+    """The paper's own finite-strain benchmark (SS3.3), synthetic stand-in:
+    SVK matrix E = 70 MPa, nu = 0.3 with `pores` non-overlapping spherical voids of total volume
+    fraction `vf` modelled as 100x more compliant SVK inclusions; uniaxial elongation
+    lambda = L/L0 -> `stretch` along z with the other directions held (full deformation control),
+    in `increments` equal steps.  The paper's cell is 63^3 (odd grids: SURVEY 8(f1)); n = 64 here."""
+    radius = (vf * n ** 3 / pores * 3.0 / (4.0 * np.pi)) ** (1.0 / 3.0)
+    phase, _ = ms.rsa_spheres((n, n, n), pores, radius, seed)
+    mats = [dict(kind="svk", E=70.0, nu=0.3), dict(kind="svk", E=0.7, nu=0.3)]
+    loads = []
+    for k in range(1, increments + 1):
+        loads.append(_load(np.diag([1.0, 1.0, 1.0 + (stretch - 1.0) * k / increments]), np.zeros((3, 3), bool)))
+    return dict(name="p33", n=(n, n, n), kin=FINITE, phase=phase, materials=mats, loads=loads, dt=1.0)
+
+
+CONFIGS = dict(c1=c1, c2=c2, c3=c3, c4=c4, c5=c5, c5s=c5s, p33=p33)

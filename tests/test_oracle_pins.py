@@ -598,3 +598,59 @@ def test_reference_medium_changes_iterations_not_solution():
             assert np.linalg.norm(r["sig"] - ref["sig"]) <= 1e-8 * np.linalg.norm(ref["sig"])
         n_iters = {res[m]["iters"] for m in res}
         assert (len(n_iters) == 1) == same_iters, n_iters
+
+
+# ----------------------------------------------------------------- Saint Venant-Kirchhoff
+
+def _svk_energy(F, E, nu):
+    lam = E * nu / ((1 + nu) * (1 - 2 * nu))
+    mu = E / (2 * (1 + nu))
+    Eg = 0.5 * (F.T @ F - np.eye(3))
+    return 0.5 * lam * np.trace(Eg) ** 2 + mu * np.sum(Eg * Eg)
+
+
+def test_svk_energy_tangent_limits():
+    """SVK: P = dW/dF of W = lam/2 (tr E)^2 + mu E:E by central differences of W, K = dP/dF
+    by differences of P, K(I) = the isotropic C(E, nu), and frame indifference P(QF) = Q P(F)."""
+    E, nu = 70.0, 0.3
+    rng = np.random.default_rng(3)
+    F = np.eye(3) + 0.4 * rng.standard_normal((3, 3))
+    P, K = O.svk(F.reshape(3, 3, 1), E, nu)
+    P, K = P[..., 0], K[..., 0]
+    h = 1e-6
+    Pfd = np.zeros((3, 3))
+    Kfd = np.zeros((3, 3, 3, 3))
+    for k in range(3):
+        for l in range(3):
+            d = np.zeros((3, 3)); d[k, l] = h
+            Pfd[k, l] = (_svk_energy(F + d, E, nu) - _svk_energy(F - d, E, nu)) / (2 * h)
+            Kfd[:, :, k, l] = (O.svk((F + d).reshape(3, 3, 1), E, nu)[0][..., 0]
+                               - O.svk((F - d).reshape(3, 3, 1), E, nu)[0][..., 0]) / (2 * h)
+    assert np.abs(P - Pfd).max() <= 1e-7 * np.abs(P).max()
+    assert np.abs(K - Kfd).max() <= 1e-7 * np.abs(K).max()
+    _, K0 = O.svk(np.eye(3).reshape(3, 3, 1), E, nu)
+    assert np.allclose(K0[..., 0], O.isotropic_stiffness(E, nu), rtol=1e-14, atol=1e-12)
+    th = 0.7
+    Q = np.array([[np.cos(th), -np.sin(th), 0], [np.sin(th), np.cos(th), 0], [0, 0, 1.0]])
+    PQ, _ = O.svk((Q @ F).reshape(3, 3, 1), E, nu)
+    assert np.allclose(PQ[..., 0], Q @ P, rtol=1e-13, atol=1e-12)
+
+
+def test_svk_homogeneous_uniaxial_closed_form():
+    """Homogeneous SVK cell under the SS3.3 load (stretch lambda, other directions held):
+    F = diag(1, 1, lambda) exactly, P_zz = lambda (lam + 2 mu)(lambda^2 - 1)/2 and
+    P_xx = P_yy = lam (lambda^2 - 1)/2, with no PCG work (homogeneous medium)."""
+    n = (8, 8, 8)
+    E, nu = 70.0, 0.3
+    lam = E * nu / ((1 + nu) * (1 - 2 * nu)); mu = E / (2 * (1 + nu))
+    ph = np.zeros((n[2], n[1], n[0]), np.uint16)
+    mats = [dict(kind="svk", E=E, nu=nu)]
+    st = O.FiniteStrainState(n)
+    for stretch in (1.2, 1.6, 2.0):
+        L = dict(target=np.diag([1.0, 1.0, stretch]), mask=np.zeros((3, 3), bool))
+        r = O.solve_finite_increment(st, ph, mats, L, tol=1e-10)
+        assert r["converged"] and r["cg_iters"] == 0
+        e = 0.5 * (stretch ** 2 - 1)
+        assert r["mean_P"][2, 2] == pytest.approx(stretch * (lam + 2 * mu) * e, rel=1e-13)
+        assert r["mean_P"][0, 0] == pytest.approx(lam * e, rel=1e-13)
+        assert np.abs(r["F"] - np.diag([1.0, 1.0, stretch]).reshape(3, 3, 1, 1, 1)).max() <= 1e-14

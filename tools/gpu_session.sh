@@ -1,2 +1,1 @@
-timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-timeout 900 python tools/precond_variants.py > gpurun_out/precond_variants.jsonl 2> gpurun_out/precond_variants.err; tail -2 gpurun_out/precond_variants.err
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "svk or p33 or finite or c4_twin" 2>&1 | tail -5
