@@ -187,6 +187,26 @@ typedef enum {
 /* Copy a field of the committed state into `out` (host if out_on_device == 0). (sync) */
 dbfft_status dbfft_get_field(dbfft_ctx ctx, int32_t which, void* out, int32_t out_on_device);
 
+/* Residual monitors of the committed state (SS3 of the paper; finite strain P:327-330):
+ *   out[0] equilibrium   ||div sigma||_L2 / ||<sigma>||        (Eq. chedckeq; finite: P,
+ *                        reference divergence)
+ *   out[1] compatibility max|curl curl eps| / ||<eps>||         (Eq. chedckcomp; finite:
+ *                        max|curl_0 F| / ||<F> - I||)
+ *   out[2] loading       ||<eps> - eps_bar|| / ||eps_bar|| over the strain-controlled components
+ *                        and ||<sigma> - sigma_bar|| / ||<sigma>|| over the stress-controlled ones
+ *                        (Eq. chedckimp), the larger of the two
+ * target/mask as in dbfft_solve_increment (row-major 3x3).  ||.||_L2 is the voxel-mean L2 norm
+ * (Parseval on the mean-normalised half spectrum, R5/R6), ||.|| Frobenius, max over all
+ * components and voxels.  Derivatives are the method's discrete ones (i xi, Eq. 1, R1).
+ * Uses the context's work buffers; call between solves.  Errors: E_STATE before set_phases. */
+dbfft_status dbfft_residuals(dbfft_ctx ctx, const double target[9], const uint8_t mask[9], double out[3]);
+
+/* Unnormalised incompatibility of a given real tensor field field[9][n3][n2][n1] (row-major
+ * 3x3 per voxel, host if on_device == 0; loopback: global array, NCCL: this rank's z-slab):
+ * max|curl curl eps| for a small-strain context (the field's symmetric part is used),
+ * max|curl F| (row-wise curl) for a finite-strain one.  Same derivatives as dbfft_residuals. */
+dbfft_status dbfft_incompatibility(dbfft_ctx ctx, const double* field, int32_t on_device, double* out);
+
 /* Per-kernel device-time accounting: while enabled, CUDA events are recorded on the ctx stream
  * around every kernel launch and accumulated per kernel id (names via dbfft_profile_name). */
 dbfft_status dbfft_profile_enable(dbfft_ctx ctx, int32_t enable);

@@ -593,6 +593,51 @@ def solve_small_strain(phase, materials, load, tol=1e-10, max_iter=10000, L=(1.0
                 mean_sig=volume_average(sig), iters=iters, hist=hist, XI=XI)
 
 
+# ----------------------------------------------------------------------------
+# Residual monitors (P:270-290 Eqs. chedckeq / chedckcomp / chedckimp; finite strain
+# P:327-330).  Derivatives are the method's discrete ones (i xi, Eq. 1 with R1).
+# ----------------------------------------------------------------------------
+def _levi_civita():
+    e = np.zeros((3, 3, 3))
+    e[0, 1, 2] = e[1, 2, 0] = e[2, 0, 1] = 1.0
+    e[0, 2, 1] = e[2, 1, 0] = e[1, 0, 2] = -1.0
+    return e
+
+
+def incompatibility(field, XI, finite):
+    """max over components and voxels of |curl curl eps| (small strain, the symmetric part of
+    `field`, Eq. chedckcomp) or of |curl_0 F| (finite strain, row-wise curl
+    (curl F)_ij = e_jkl d_k F_il).  field: [3,3,z,y,x] real.  Unnormalised."""
+    e = _levi_civita()
+    dhat = 1j * XI                                          # spectral d_k
+    if finite:
+        Fh = fft(field)
+        C = np.einsum("jkl,k...,il...->ij...", e, dhat, Fh)
+        return float(np.max(np.abs(ifft(C, check=False))))
+    eps = 0.5 * (field + np.swapaxes(field, 0, 1))
+    Eh = fft(eps)
+    eta = np.einsum("ikl,jmn,k...,m...,ln...->ij...", e, e, dhat, dhat, Eh)
+    return float(np.max(np.abs(ifft(eta, check=False))))
+
+
+def equilibrium_residual(sig, XI):
+    """||div sigma||_L2 / ||<sigma>|| (Eq. chedckeq; P / reference divergence at finite
+    strain).  ||.||_L2 = voxel-mean L2 norm = sqrt(sum |f_hat|^2) (Parseval, R5)."""
+    f = div_hat(fft(sig), XI)
+    return float(np.sqrt(np.sum(np.abs(f) ** 2)) / np.linalg.norm(volume_average(sig)))
+
+
+def loading_residual(mean_eps, mean_sig, target, mask):
+    """Eq. chedckimp: ||<eps> - eps_bar|| / ||eps_bar|| over the strain-controlled
+    components, ||<sigma> - sigma_bar|| / ||<sigma>|| over the stress-controlled ones (mixed
+    control: the larger)."""
+    de = np.where(mask, 0.0, mean_eps - target)
+    te = np.where(mask, 0.0, target)
+    ds = np.where(mask, mean_sig - target, 0.0)
+    r1 = np.linalg.norm(de) / np.linalg.norm(te) if np.linalg.norm(te) > 0 else np.linalg.norm(de)
+    return float(max(r1, np.linalg.norm(ds) / np.linalg.norm(mean_sig)))
+
+
 def displacement(u_hat):
     """Real-space fluctuation displacement u~(x) (obtained directly)."""
     return ifft(u_hat)

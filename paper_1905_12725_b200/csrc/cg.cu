@@ -13,25 +13,6 @@ namespace {
 constexpr int BLK = 256;
 constexpr int NBLK = 148 * 4;
 
-struct Pt {
-  double xx, xy, xz;
-  double w;
-  bool null;
-};
-
-DBF_DEV Pt point(const SpecGeom& g, long long i) {
-  const int kx = (int)(i % g.n1h);
-  const long long rest = i / g.n1h;
-  const int kz = (int)(rest % g.n3);
-  const int ky = (int)(rest / g.n3);
-  Pt p;
-  p.xx = __ldg(g.fq.xx + kx);
-  p.xy = __ldg(g.fq.xy + ky);
-  p.xz = __ldg(g.fq.xz + kz);
-  p.w = (kx == 0 || 2 * kx == g.n1) ? 1.0 : 2.0;
-  p.null = (p.xx == 0.0 && p.xy == 0.0 && p.xz == 0.0);
-  return p;
-}
 
 // z = A^-1 r with A = xi.Cbar.xi (symmetric 3x3), 0 on the null set Z (R4)
 DBF_DEV void apply_M(const PrecQ& Q, const Pt& p, const cplx* r, cplx* z) {

@@ -46,3 +46,24 @@ cudaError_t launch_reduce(const double* partials, int nblk, int nred, double* ou
 cudaError_t launch_phase_hist(const uint16_t* ph, long long nvox, double* counts, int nphase, int* bad, cudaStream_t s);
 cudaError_t launch_fill(double* p, long long n, double v, cudaStream_t s);
 int cg_blocks();
+
+// frequency of spectral point i of a SpecGeom layout [ky][kz][kx] (Eq. 1, R1), Hermitian weight
+struct Pt {
+  double xx, xy, xz;
+  double w;
+  bool null;
+};
+
+DBF_DEV Pt point(const SpecGeom& g, long long i) {
+  const int kx = (int)(i % g.n1h);
+  const long long rest = i / g.n1h;
+  const int kz = (int)(rest % g.n3);
+  const int ky = (int)(rest / g.n3);
+  Pt p;
+  p.xx = __ldg(g.fq.xx + kx);
+  p.xy = __ldg(g.fq.xy + ky);
+  p.xz = __ldg(g.fq.xz + kz);
+  p.w = (kx == 0 || 2 * kx == g.n1) ? 1.0 : 2.0;
+  p.null = (p.xx == 0.0 && p.xy == 0.0 && p.xz == 0.0);
+  return p;
+}

@@ -28,6 +28,7 @@
 #include "../../include/dbfft.h"
 #include "cg.cuh"
 #include "passes.cuh"
+#include "monitors.cuh"
 
 namespace {
 
@@ -316,6 +317,7 @@ XGeom xgeom(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out) {
   g.xix = ctx->xix;
   g.inv_n = 1.0 / (double)ctx->N;
   g.oscale = 0.5 / (double)ctx->N;  // exact: N is a power of two
+  for (int f = 0; f < 9; ++f) g.real_map[f] = f;
   g.partials = s.part_x;
   g.nred = 10;
   g.phase = s.phase;
@@ -1716,6 +1718,165 @@ dbfft_status dbfft_solve_increment(dbfft_ctx ctx, const double target[9], const 
   return st;
 }
 
+// committed strain (eps or F) / stress (sigma or P) -> every slab's tmp_real [9][Nloc], row-major 3x3
+dbfft_status field_to_tmp(dbfft_ctx ctx, int which) {
+  for (Slab& s : ctx->slabs) CKS(ensure_tmp(ctx, s));
+  if (ctx->family == FAM_NEOHOOKE) {
+    for (Slab& s : ctx->slabs) {
+      ProfScope ps(ctx, PK_OTHER);
+      if (which == DBFFT_FIELD_STRAIN) {
+        CK(cudaMemcpyAsync(s.tmp_real, s.F_c, sizeof(double) * 9 * s.Nloc, cudaMemcpyDeviceToDevice, ctx->stream));
+      } else {
+        k_stress_nh<<<1024, 256, 0, ctx->stream>>>(s.F_c, s.phase, s.ptable, s.Nloc, s.tmp_real);
+        CK(cudaGetLastError());
+      }
+    }
+    return DBFFT_OK;
+  }
+  if (ctx->family == FAM_J2) {
+    for (Slab& s : ctx->slabs) {
+      ProfScope ps(ctx, PK_OTHER);
+      if (which == DBFFT_FIELD_STRAIN) k_expand6<<<1024, 256, 0, ctx->stream>>>(s.F_c, s.Nloc, nullptr, s.tmp_real);
+      else k_stress_j2<<<1024, 256, 0, ctx->stream>>>(s.F_c, s.epsp_c, s.phase, s.ptable, s.Nloc, s.tmp_real);
+      CK(cudaGetLastError());
+    }
+    return DBFFT_OK;
+  }
+  // linear: eps = Ebar + sym grad u (Voigt 6 via the inverse passes), sigma = C:eps
+  CKS(upload_e(ctx, ctx->Fbar_c));
+  for (Slab& s : ctx->slabs) CKS(run_col(ctx, COL_I1S, PK_OTHER, geom_I1(ctx, s, s.u_c, s.WA, 5), ctx->n3));
+  CKS(exchange(ctx, (long long)5 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
+  for (Slab& s : ctx->slabs) {
+    CKS(run_col(ctx, COL_I2S, PK_OTHER, geom_I2(ctx, s, s.WR, s.WB, 5), ctx->n2));
+    double* tmp6 = reinterpret_cast<double*>(s.WA);  // 6 real fields fit in WA (6 complex fields)
+    XGeom gx = xgeom(ctx, s, s.WB, nullptr);
+    gx.real_out = tmp6;
+    CKS(run_x(ctx, X_REAL_OUT + 6, PK_OTHER, gx, nullptr));
+    ProfScope ps(ctx, PK_OTHER);
+    k_expand6<<<1024, 256, 0, ctx->stream>>>(tmp6, s.Nloc, s.e_dev, s.tmp_real);
+    CK(cudaGetLastError());
+    if (which == DBFFT_FIELD_STRESS) {
+      k_stress_linear<<<1024, 256, 0, ctx->stream>>>(s.tmp_real, s.phase, s.ptable, s.Nloc, s.tmp_real);
+      CK(cudaGetLastError());
+    }
+  }
+  return DBFFT_OK;
+}
+
+// ---------------------------------------------------------------- residual monitors
+const int kRowMajorVoigt[6] = {0, 4, 8, 5, 2, 1};
+
+// per-slab scalar (sum or max of monitor partials) combined over slabs and ranks
+dbfft_status monitor_combine(dbfft_ctx ctx, std::vector<double>& per_slab, bool is_max, double* out) {
+  for (size_t k = 0; k < ctx->slabs.size(); ++k)
+    CK(cudaMemcpyAsync(ctx->slabs[k].loc + 60, &per_slab[k], sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  CKS(allreduce(ctx, 60, 1, is_max));
+  return read_loc(ctx, 60, 1, out);
+}
+
+dbfft_status partials_host(dbfft_ctx ctx, Slab& s, bool is_max, double* v) {
+  const int nb = monitor_blocks();
+  std::vector<double> h(nb);
+  CK(cudaMemcpyAsync(h.data(), s.part_misc, sizeof(double) * nb, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  double r = 0.0;
+  for (int b = 0; b < nb; ++b) r = is_max ? std::max(r, h[b]) : r + h[b];
+  *v = r;
+  return DBFFT_OK;
+}
+
+// max over the field in tmp_real of |curl curl eps| (kinematics 6, symmetric) or |curl F| (rows,
+// kinematics 9): forward transforms (X R2C, y, z), the spectral curl, inverse transforms, max
+dbfft_status incompat_max(dbfft_ctx ctx, double* result) {
+  const bool fin = ctx->kin == 9;
+  std::vector<double> mx(ctx->slabs.size(), 0.0);
+  const int nrow = fin ? 3 : 1, nf = fin ? 3 : 6;
+  const long long chunk = (long long)nf * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h;
+  for (int row = 0; row < nrow; ++row) {
+    for (Slab& s : ctx->slabs) {
+      XGeom gx = xgeom(ctx, s, nullptr, s.WB);
+      gx.real_in = s.tmp_real;
+      for (int f = 0; f < nf; ++f) gx.real_map[f] = fin ? 3 * row + f : kRowMajorVoigt[f];
+      CKS(run_x(ctx, X_REAL_IN + nf, PK_OTHER, gx, nullptr));
+      CKS(run_col(ctx, fin ? COL_YF3 : COL_YF6, PK_OTHER, geom_F2(ctx, s, s.WB, s.WA, nf), ctx->n2));
+    }
+    CKS(exchange(ctx, chunk));
+    for (Slab& s : ctx->slabs) {
+      CKS(run_col(ctx, fin ? COL_ZF3 : COL_ZF6, PK_OTHER, geom_F3(ctx, s, s.WR, s.WB, nf), ctx->n3));
+      ProfScope ps(ctx, PK_OTHER);
+      CK(fin ? launch_curl3(spec(ctx, s), s.WB, ctx->stream) : launch_curlcurl6(spec(ctx, s), s.WB, ctx->stream));
+    }
+    for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_ZI3 : COL_ZI6, PK_OTHER, geom_I1(ctx, s, s.WB, s.WA, nf), ctx->n3));
+    CKS(exchange(ctx, chunk));
+    for (size_t k = 0; k < ctx->slabs.size(); ++k) {
+      Slab& s = ctx->slabs[k];
+      CKS(run_col(ctx, fin ? COL_YI3 : COL_YI6, PK_OTHER, geom_I2(ctx, s, s.WR, s.WB, nf), ctx->n2));
+      double* out = reinterpret_cast<double*>(s.WA);
+      XGeom gx = xgeom(ctx, s, s.WB, nullptr);
+      gx.real_out = out;
+      CKS(run_x(ctx, X_REAL_OUT + nf, PK_OTHER, gx, nullptr));
+      {
+        ProfScope ps(ctx, PK_OTHER);
+        CK(launch_maxabs(out, (long long)nf * s.Nloc, s.part_misc, ctx->stream));
+      }
+      double m;
+      CKS(partials_host(ctx, s, true, &m));
+      mx[k] = std::max(mx[k], m);
+    }
+  }
+  return monitor_combine(ctx, mx, true, result);
+}
+
+// ||div sigma||_L2 (Parseval over the half spectrum, R6) of the stress field in tmp_real, and its
+// volume average <sigma> (row-major 9)
+dbfft_status div_norm(dbfft_ctx ctx, double* norm, double* mean9) {
+  const bool fin = ctx->kin == 9;
+  const int nf = fin ? 9 : 6;
+  std::vector<double> n2(ctx->slabs.size());
+  for (int a = 0; a < 9; ++a) {
+    std::vector<double> sum(ctx->slabs.size());
+    for (size_t k = 0; k < ctx->slabs.size(); ++k) {
+      Slab& s = ctx->slabs[k];
+      {
+        ProfScope ps(ctx, PK_OTHER);
+        CK(launch_sum(s.tmp_real + (long long)a * s.Nloc, s.Nloc, s.part_misc, ctx->stream));
+      }
+      CKS(partials_host(ctx, s, false, &sum[k]));
+    }
+    CKS(monitor_combine(ctx, sum, false, &mean9[a]));
+    mean9[a] /= (double)ctx->N;
+  }
+  for (Slab& s : ctx->slabs) {
+    XGeom gx = xgeom(ctx, s, nullptr, s.WB);
+    gx.real_in = s.tmp_real;
+    for (int f = 0; f < nf; ++f) gx.real_map[f] = fin ? f : kRowMajorVoigt[f];
+    CKS(run_x(ctx, X_REAL_IN + nf, PK_OTHER, gx, nullptr));
+  }
+  // the operator's forward tail: f = -i xi . sigma_hat (positive form, R3) into q
+  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_OTHER, geom_F2(ctx, s, s.WB, s.WA, 6), ctx->n2));
+  CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
+  for (size_t k = 0; k < ctx->slabs.size(); ++k) {
+    Slab& s = ctx->slabs[k];
+    CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_OTHER, geom_F3(ctx, s, s.WR, s.q, 6), ctx->n3));
+    {
+      ProfScope ps(ctx, PK_OTHER);
+      CK(launch_specnorm2(spec(ctx, s), s.q, 3, s.part_misc, ctx->stream));
+    }
+    CKS(partials_host(ctx, s, false, &n2[k]));
+  }
+  double tot;
+  CKS(monitor_combine(ctx, n2, false, &tot));
+  *norm = std::sqrt(tot);
+  return DBFFT_OK;
+}
+
+double frob9(const double* a) {
+  double s = 0.0;
+  for (int k = 0; k < 9; ++k) s += a[k] * a[k];
+  return std::sqrt(s);
+}
+
 dbfft_status dbfft_get_field(dbfft_ctx ctx, int32_t which, void* out, int32_t out_on_device) {
   if (!ctx) return DBFFT_E_INVALID_ARG;
   if (!out) {
@@ -1743,45 +1904,9 @@ dbfft_status dbfft_get_field(dbfft_ctx ctx, int32_t which, void* out, int32_t ou
       return gather_real(ctx, &Slab::tmp_real, 3, (double*)out, out_on_device);
     }
     case DBFFT_FIELD_STRAIN:
-    case DBFFT_FIELD_STRESS: {
-      if (ctx->family == FAM_NEOHOOKE) {
-        if (which == DBFFT_FIELD_STRAIN) return gather_real(ctx, &Slab::F_c, 9, (double*)out, out_on_device);
-        for (Slab& s : ctx->slabs) {
-          ProfScope ps(ctx, PK_OTHER);
-          k_stress_nh<<<1024, 256, 0, ctx->stream>>>(s.F_c, s.phase, s.ptable, s.Nloc, s.tmp_real);
-          CK(cudaGetLastError());
-        }
-        return gather_real(ctx, &Slab::tmp_real, 9, (double*)out, out_on_device);
-      }
-      if (ctx->family == FAM_J2) {
-        for (Slab& s : ctx->slabs) {
-          ProfScope ps(ctx, PK_OTHER);
-          if (which == DBFFT_FIELD_STRAIN) k_expand6<<<1024, 256, 0, ctx->stream>>>(s.F_c, s.Nloc, nullptr, s.tmp_real);
-          else k_stress_j2<<<1024, 256, 0, ctx->stream>>>(s.F_c, s.epsp_c, s.phase, s.ptable, s.Nloc, s.tmp_real);
-          CK(cudaGetLastError());
-        }
-        return gather_real(ctx, &Slab::tmp_real, 9, (double*)out, out_on_device);
-      }
-      // linear: eps = Ebar + sym grad u (Voigt 6 via the inverse passes), sigma = C:eps
-      CKS(upload_e(ctx, ctx->Fbar_c));
-      for (Slab& s : ctx->slabs) CKS(run_col(ctx, COL_I1S, PK_OTHER, geom_I1(ctx, s, s.u_c, s.WA, 5), ctx->n3));
-      CKS(exchange(ctx, (long long)5 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
-      for (Slab& s : ctx->slabs) {
-        CKS(run_col(ctx, COL_I2S, PK_OTHER, geom_I2(ctx, s, s.WR, s.WB, 5), ctx->n2));
-        double* tmp6 = reinterpret_cast<double*>(s.WA);  // 6 real fields fit in WA (6 complex fields)
-        XGeom gx = xgeom(ctx, s, s.WB, nullptr);
-        gx.real_out = tmp6;
-        CKS(run_x(ctx, X_REAL_OUT + 6, PK_OTHER, gx, nullptr));
-        ProfScope ps(ctx, PK_OTHER);
-        k_expand6<<<1024, 256, 0, ctx->stream>>>(tmp6, s.Nloc, s.e_dev, s.tmp_real);
-        CK(cudaGetLastError());
-        if (which == DBFFT_FIELD_STRESS) {
-          k_stress_linear<<<1024, 256, 0, ctx->stream>>>(s.tmp_real, s.phase, s.ptable, s.Nloc, s.tmp_real);
-          CK(cudaGetLastError());
-        }
-      }
+    case DBFFT_FIELD_STRESS:
+      CKS(field_to_tmp(ctx, which));
       return gather_real(ctx, &Slab::tmp_real, 9, (double*)out, out_on_device);
-    }
     default:
       ctx->err = "get_field: unknown field";
       return DBFFT_E_INVALID_ARG;
@@ -1817,3 +1942,39 @@ const char* dbfft_profile_name(int32_t id) { return (id >= 0 && id < PK_COUNT) ?
 int32_t dbfft_profile_count(void) { return PK_COUNT; }
 
 }  // extern "C"
+
+dbfft_status dbfft_residuals(dbfft_ctx ctx, const double target[9], const uint8_t mask[9], double out[3]) {
+  if (!ctx || !target || !mask || !out) return DBFFT_E_INVALID_ARG;
+  if (ctx->family == FAM_NONE) {
+    ctx->err = "residuals before set_phases";
+    return DBFFT_E_STATE;
+  }
+  const bool fin = ctx->kin == 9;
+  double msig[9], meps[9], nrm, mx;
+  CKS(field_to_tmp(ctx, DBFFT_FIELD_STRESS));
+  CKS(div_norm(ctx, &nrm, msig));
+  CKS(field_to_tmp(ctx, DBFFT_FIELD_STRAIN));
+  for (int a = 0; a < 9; ++a) meps[a] = ctx->Fbar_c[a];
+  CKS(incompat_max(ctx, &mx));
+  double ref[9];
+  for (int a = 0; a < 9; ++a) ref[a] = meps[a] - ((fin && a % 4 == 0) ? 1.0 : 0.0);
+  out[0] = nrm / std::max(frob9(msig), 1e-300);   // Eq. chedckeq
+  out[1] = mx / std::max(frob9(ref), 1e-300);     // Eq. chedckcomp / P:330
+  double de[9], te[9], ds[9];
+  for (int a = 0; a < 9; ++a) {                   // Eq. chedckimp per control type
+    de[a] = mask[a] ? 0.0 : meps[a] - target[a];
+    te[a] = mask[a] ? 0.0 : target[a];
+    ds[a] = mask[a] ? msig[a] - target[a] : 0.0;
+  }
+  const double te_n = frob9(te);
+  out[2] = std::max(te_n > 0 ? frob9(de) / te_n : frob9(de), frob9(ds) / std::max(frob9(msig), 1e-300));
+  return DBFFT_OK;
+}
+
+dbfft_status dbfft_incompatibility(dbfft_ctx ctx, const double* field, int32_t on_device, double* out) {
+  if (!ctx || !field || !out) return DBFFT_E_INVALID_ARG;
+  for (Slab& s : ctx->slabs) CKS(ensure_tmp(ctx, s));
+  CKS(scatter_real(ctx, field, on_device, 9, nullptr, &Slab::tmp_real));
+  return incompat_max(ctx, out);
+}
+

@@ -229,6 +229,22 @@ struct ColOp<COL_ZI3> {
 template <>
 struct ColOp<COL_YI3> : ColOp<COL_ZI3> {};
 
+// plain transforms of NF fields (no weights): residual monitors
+template <int NF, bool INVERSE>
+struct ColPlain {
+  static constexpr bool INV = INVERSE;
+  static constexpr int NT = NF, MAXIN = 1;
+  DBF_DEV static TermInfo term(int j) { return {j, 1, 1, j, -1}; }
+  DBF_DEV static cplx pre(const ColAt&, int, cplx r0, cplx) { return r0; }
+  DBF_DEV static cplx post(const ColAt&, int) { return make_double2(1.0, 0.0); }
+};
+template <> struct ColOp<COL_ZI6> : ColPlain<6, true> {};
+template <> struct ColOp<COL_YI6> : ColPlain<6, true> {};
+template <> struct ColOp<COL_ZF3> : ColPlain<3, false> {};
+template <> struct ColOp<COL_YF3> : ColPlain<3, false> {};
+template <> struct ColOp<COL_ZF6> : ColPlain<6, false> {};
+template <> struct ColOp<COL_YF6> : ColPlain<6, false> {};
+
 template <int KIND>
 struct ColTwo {  // does any output of this pass sum two transformed terms?
   static constexpr bool value = (KIND == COL_F2F || KIND == COL_F3S || KIND == COL_F3F);
@@ -350,6 +366,7 @@ template <> struct XTraits<X_RHS_SMALL_PHASE> { static constexpr int CIN = 0, CO
 template <> struct XTraits<X_CONST_FIN> { static constexpr int CIN = 9, COUT = 9, NRED = 10; static constexpr bool FIN = true; };
 template <> struct XTraits<X_CONST_J2> { static constexpr int CIN = 6, COUT = 6, NRED = 10; static constexpr bool FIN = false; };
 template <> struct XTraits<X_REAL_OUT> { static constexpr int CIN = 9, COUT = 0, NRED = 0; static constexpr bool FIN = false; };
+template <> struct XTraits<X_REAL_IN> { static constexpr int CIN = 0, COUT = 9, NRED = 0; static constexpr bool FIN = false; };
 
 DBF_DEV int sym9(int i, int j) {
   if (i > j) { int t = i; i = j; j = t; }
@@ -799,6 +816,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
   const int fa = 2 * p, fb = 2 * p + 1;
   const int jbase = (l * CS + fa) * (N1 / 2);  // complex view of slots fa, fb of line l (job buffer)
   const int cin = (KIND == X_REAL_OUT) ? nf_real : T::CIN;
+  const int cout_rt = (KIND == X_REAL_IN) ? nf_real : T::COUT;  // spectral outputs written
   const bool do_in = (T::CIN > 0) && (cin > 0) && ((KIND != X_CONST_FIN && KIND != X_CONST_J2) || g.has_in);
   const long long ngroups = (g.nlines + LPAR - 1) / LPAR;
   // apply kinds: <sigma> / <dP> from the k = 0 outputs of the R2C (one owner thread per field)
@@ -881,10 +899,19 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
       __syncthreads();
       continue;
     }
+    if (KIND == X_REAL_IN) {  // real fields -> slots, pre-scaled by 1/(2N) like the voxel outputs
+      for (int vv = t; vv < LPAR * N1; vv += CF::THREADS) {
+        const int l2 = vv / N1, x = vv % N1;
+        const long long ln = grp * LPAR + l2;
+        for (int f = 0; f < CS; ++f)
+          real[(l2 * CS + f) * N1 + x] =
+              (ln < g.nlines && f < nf_real) ? g.oscale * __ldg(g.real_in + (long long)g.real_map[f] * g.nvox + ln * N1 + x) : 0.0;
+      }
+    }
 
     // ------------------------------------------------------------ per-voxel operation
     if (S::IN && STAGE_TAN) mbar_wait(&bars[1], it & 1);
-    for (int vv = t; vv < LPAR * N1; vv += CF::THREADS) {
+    for (int vv = t; KIND != X_REAL_IN && vv < LPAR * N1; vv += CF::THREADS) {
       const int l2 = vv / N1, x = vv % N1;
       const long long ln = grp * LPAR + l2;
       if (ln >= g.nlines) continue;
@@ -938,7 +965,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
 #pragma unroll
         for (int s = 0; s < PX; ++s) zn[s] = cx[x_idx<PX>(jbase, (N1 - (gq + s * TPJ)) & (N1 - 1))];
       }
-      if (lvalid && fa < COUT) {
+      if (lvalid && fa < cout_rt) {
 #pragma unroll
         for (int s = 0; s < PX; ++s) {
           const int k = gq + s * TPJ;
@@ -956,7 +983,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
           }
           const long long base = line * g.n1h + k;
           g.out[fa * g.fs_out + base] = A;
-          if (fb < COUT) g.out[fb * g.fs_out + base] = B;
+          if (fb < cout_rt) g.out[fb * g.fs_out + base] = B;
         }
       }
       __syncthreads();  // slots are reused by the next group
@@ -1063,6 +1090,10 @@ struct TProg {
   signed char acc[10];    // register accumulator of a two-term output
 };
 
+#define DBF_PLAIN3 {3, {0, 1, 2}, 3, {0, 1, 2}, {0, 1, 2}, {-1, -1, -1}, {-1, -1, -1}, {1, 2, 3}, {0, 0, 0}}
+#define DBF_PLAIN6                                                                                               \
+  {6, {0, 1, 2, 3, 4, 5}, 6, {0, 1, 2, 3, 4, 5}, {0, 1, 2, 3, 4, 5}, {-1, -1, -1, -1, -1, -1}, {-1, -1, -1, -1, -1, -1}, \
+   {1, 2, 3, 4, 5, 6}, {0, 0, 0, 0, 0, 0}}
 // index: 2*kind + dot (one table: host copy for the liveness check, constant-bank copy for the kernel)
 #define DBF_COL_PROGS \
     /* COL_I1S: loads u0, u2, u1; terms 0, 2, 3{0,2}, 1, 4{1,2} */ \
@@ -1093,10 +1124,9 @@ struct TProg {
     {6, {0, 3, 1, 4, 2, 5}, 6, {0, 1, 2, 3, 4, 5}, {0, 1, 2, 3, 4, 5}, {-1, -1, -1, -1, -1, -1}, {-1, -1, -1, -1, -1, -1}, {1, 2, 3, 4, 5, 6}, {0, 0, 0, 0, 0, 0}}, \
     {9, {0, 3, 16, 1, 4, 17, 2, 5, 18}, 6, {0, 1, 2, 3, 4, 5}, {0, 1, 3, 4, 6, 7}, {-1, -1, -1, -1, -1, -1}, {-1, 2, -1, 5, -1, 8}, {1, 3, 4, 6, 7, 9}, {0, 0, 0, 0, 0, 0}}, \
     /* COL_ZI3, COL_YI3 */ \
-    {3, {0, 1, 2}, 3, {0, 1, 2}, {0, 1, 2}, {-1, -1, -1}, {-1, -1, -1}, {1, 2, 3}, {0, 0, 0}}, \
-    {0}, \
-    {3, {0, 1, 2}, 3, {0, 1, 2}, {0, 1, 2}, {-1, -1, -1}, {-1, -1, -1}, {1, 2, 3}, {0, 0, 0}}, \
-    {0},
+    DBF_PLAIN3, {0}, DBF_PLAIN3, {0}, \
+    /* COL_ZI6, COL_YI6, COL_ZF3, COL_YF3, COL_ZF6, COL_YF6 */ \
+    DBF_PLAIN6, {0}, DBF_PLAIN6, {0}, DBF_PLAIN3, {0}, DBF_PLAIN3, {0}, DBF_PLAIN6, {0}, DBF_PLAIN6, {0},
 
 __device__ __constant__ TProg c_prog[2 * COL_NKINDS] = {DBF_COL_PROGS};
 static const TProg kColProgHost[2 * COL_NKINDS] = {DBF_COL_PROGS};
@@ -1363,6 +1393,12 @@ static cudaError_t launch_col_n(int kind, const ColGeom& g, cudaStream_t s) {
     case COL_F3F: return launch_col_k<N, COL_F3F>(g, s);
     case COL_ZI3: return launch_col_k<N, COL_ZI3>(g, s);
     case COL_YI3: return launch_col_k<N, COL_YI3>(g, s);
+    case COL_ZI6: return launch_col_k<N, COL_ZI6>(g, s);
+    case COL_YI6: return launch_col_k<N, COL_YI6>(g, s);
+    case COL_ZF3: return launch_col_k<N, COL_ZF3>(g, s);
+    case COL_YF3: return launch_col_k<N, COL_YF3>(g, s);
+    case COL_ZF6: return launch_col_k<N, COL_ZF6>(g, s);
+    case COL_YF6: return launch_col_k<N, COL_YF6>(g, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -1390,8 +1426,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
 }
 
 // fields of the pass's input / output buffers (tensor-map bounds)
-static const int kColNfIn[COL_NKINDS] = {3, 3, 5, 6, 6, 9, 6, 6, 3, 3};
-static const int kColNfOut[COL_NKINDS] = {5, 6, 6, 9, 6, 6, 3, 3, 3, 3};
+static const int kColNfIn[COL_NKINDS] = {3, 3, 5, 6, 6, 9, 6, 6, 3, 3, 6, 6, 3, 3, 6, 6};
+static const int kColNfOut[COL_NKINDS] = {5, 6, 6, 9, 6, 6, 3, 3, 3, 3, 6, 6, 3, 3, 6, 6};
 
 // 5D view [field][outer][pos_hi][pos_lo][kx re/im] of a column-pass operand (complex strides)
 static bool col_map(CUtensorMap* m, const void* ptr, int N, int n1h, int psh, long long ps, long long pcs, int n_outer,
@@ -1496,7 +1532,8 @@ static cudaError_t launch_col_tma(int kind, const ColGeom& g, cudaStream_t s, in
                : launch_col_tma_k<N, K, false>(maps, g, tl, s, grid_out);
   switch (kind) {
     DBF_TK(COL_I1S) DBF_TK(COL_I1F) DBF_TK(COL_I2S) DBF_TK(COL_I2F) DBF_TK(COL_F2S) DBF_TK(COL_F2F) DBF_TK(COL_F3S)
-    DBF_TK(COL_F3F) DBF_TK(COL_ZI3) DBF_TK(COL_YI3)
+    DBF_TK(COL_F3F) DBF_TK(COL_ZI3) DBF_TK(COL_YI3) DBF_TK(COL_ZI6) DBF_TK(COL_YI6) DBF_TK(COL_ZF3)
+    DBF_TK(COL_YF3) DBF_TK(COL_ZF6) DBF_TK(COL_YF6)
     default: return cudaErrorInvalidValue;
   }
 #undef DBF_TK
@@ -1558,6 +1595,7 @@ static cudaError_t launch_x_n(int kind, const XGeom& g, cudaStream_t s, int* gri
     case X_CONST_J2: return launch_x_k<N1, X_CONST_J2>(g, s, grid_out, 0);
     default: break;
   }
+  if (kind >= X_REAL_IN) return launch_x_k<N1, X_REAL_IN>(g, s, grid_out, kind - X_REAL_IN);
   if (kind >= X_REAL_OUT) return launch_x_k<N1, X_REAL_OUT>(g, s, grid_out, kind - X_REAL_OUT);
   return cudaErrorInvalidValue;
 }

@@ -41,6 +41,12 @@ enum ColKind {
   COL_F3F,      // finite strain, z forward + divergence: 6 -> f (3)
   COL_ZI3,      // plain z inverse of a vector (3)
   COL_YI3,      // plain y inverse of a vector (3)
+  COL_ZI6,      // plain z / y inverse and forward transforms of 3 or 6 fields (residual monitors)
+  COL_YI6,
+  COL_ZF3,
+  COL_YF3,
+  COL_ZF6,
+  COL_YF6,
   COL_NKINDS
 };
 
@@ -53,8 +59,9 @@ enum XKind {
   X_RHS_SMALL_PHASE,    // -sigma = -C_phase : e                  (rhs of the linear system)
   X_CONST_FIN,          // F += G + dF; P, K (neo-Hookean); -P    (Newton residual)
   X_CONST_J2,           // eps += G + de; J2 return map; -sigma   (Newton residual)
-  X_REAL_OUT,           // C2R only -> real fields
-  X_NKINDS
+  X_REAL_OUT,           // C2R only -> real fields (kind X_REAL_OUT + nf)
+  X_NKINDS,
+  X_REAL_IN = 32        // R2C only <- real fields [f][N] (kind X_REAL_IN + nf, nf <= 9)
 };
 
 struct XGeom {
@@ -80,6 +87,8 @@ struct XGeom {
   double dt;
   long long nvox;
   double* real_out;       // X_REAL_OUT: [f][N]
+  const double* real_in;  // X_REAL_IN: field f at real_in + real_map[f] * nvox
+  int real_map[9];
   int* bad;               // first bad voxel flag (atomicMin on voxel index)
   int has_in;             // constitutive kinds: 0 = no C2R input (uniform increment only)
   int tmode;              // X_CONST_FIN: 0 = store the 45-entry tangent, 1 = compact (F^-1, c1)

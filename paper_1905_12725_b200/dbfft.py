@@ -44,7 +44,8 @@ STATUS = {0: "OK", 1: "E_INVALID_GRID", 2: "E_INVALID_ARG", 3: "E_STATE", 4: "E_
 EXPORTS = ["dbfft_create", "dbfft_destroy", "dbfft_last_error", "dbfft_spectral_layout", "dbfft_set_phases",
            "dbfft_apply_K", "dbfft_apply_K_aug", "dbfft_precond", "dbfft_eval_state", "dbfft_default_opts",
            "dbfft_solve_increment", "dbfft_get_field", "dbfft_profile_enable", "dbfft_profile_read",
-           "dbfft_profile_name", "dbfft_profile_count", "dbfft_launch_count", "dbfft_nccl_unique_id"]
+           "dbfft_profile_name", "dbfft_profile_count", "dbfft_launch_count", "dbfft_nccl_unique_id",
+           "dbfft_residuals", "dbfft_incompatibility"]
 
 _lib = None
 
@@ -88,6 +89,8 @@ def load_library(path=None):
     lib.dbfft_profile_count.restype = I32
     lib.dbfft_launch_count.argtypes = [P, ctypes.POINTER(ctypes.c_int64)]
     lib.dbfft_nccl_unique_id.argtypes = [P]
+    lib.dbfft_residuals.argtypes = [P, ctypes.POINTER(D), ctypes.POINTER(ctypes.c_uint8), ctypes.POINTER(D)]
+    lib.dbfft_incompatibility.argtypes = [P, P, I32, ctypes.POINTER(D)]
     for fn in EXPORTS:
         getattr(lib, fn).restype = getattr(lib, fn).restype if fn in (
             "dbfft_last_error", "dbfft_default_opts", "dbfft_profile_name", "dbfft_profile_count") else ctypes.c_int
@@ -259,6 +262,22 @@ class DBFFT:
         if ncomp == 9:
             out = out.reshape(3, 3, n3, n2, n1)
         return out
+
+    # ------------------------------------------------------------------ residual monitors
+    def residuals(self, target, mask):
+        """(equilibrium, compatibility, loading) of the committed state."""
+        t = (ctypes.c_double * 9)(*np.asarray(target, float).ravel())
+        m = (ctypes.c_uint8 * 9)(*np.asarray(mask, np.uint8).ravel())
+        out = (ctypes.c_double * 3)()
+        self._check(self.lib.dbfft_residuals(self.h, t, m, out))
+        return dict(equilibrium=out[0], compatibility=out[1], loading=out[2])
+
+    def incompatibility(self, field):
+        """max|curl curl eps| (small) or max|curl F| (finite) of a real [3,3,z,y,x] field."""
+        f = np.ascontiguousarray(np.asarray(field, np.float64).reshape(9, -1))
+        out = ctypes.c_double()
+        self._check(self.lib.dbfft_incompatibility(self.h, f.ctypes.data_as(ctypes.c_void_p), 0, ctypes.byref(out)))
+        return out.value
 
     # ------------------------------------------------------------------ profiling
     def profile(self, enable=True):

@@ -383,3 +383,59 @@ def test_solve_p33_porous_twin(dbf):
         assert rel(rep["macro_stress"], ref["mean_P"]) <= 1e-9
         assert rel(ctx.get_field(dbf.FIELD_STRAIN), ref["F"]) <= 1e-8
         assert rel(ctx.get_field(dbf.FIELD_STRESS), ref["P"]) <= 1e-8
+
+
+# ------------------------------------------------------ residual monitors
+
+@pytest.mark.parametrize("kin", ["small", "finite"])
+@pytest.mark.parametrize("n", [(16, 8, 32), (32, 64, 128)])
+def test_incompatibility_vs_oracle(dbf, kin, n):
+    """max|curl curl eps| / max|curl F| of an incompatible random field: same value as the oracle."""
+    fin = kin == "finite"
+    f = ms.random_field((3, 3, n[2], n[1], n[0]), 61)
+    if not fin:
+        f = 0.5 * (f + np.swapaxes(f, 0, 1))
+    ctx = dbf.DBFFT(n, kinematics=kin)
+    mats = [dict(kind="neohooke", mu=1.0, kappa=2.5)] if fin else ISO2[:1]
+    ctx.set_phases(np.zeros((n[2], n[1], n[0]), np.uint16), mats)
+    got = ctx.incompatibility(f)
+    ref = O.incompatibility(f, O.frequency_grid(n), finite=fin)
+    assert got == pytest.approx(ref, rel=1e-12)
+
+
+def test_residuals_after_solves(dbf):
+    """The three residuals of a converged state (GPU) against the oracle's on its own solution:
+    equilibrium at the PCG tolerance level on both, compatibility at round-off, loading 0."""
+    # linear mixed control (c2 structure, 32^3)
+    cfg = configs.c2(n=32, radius_vox=3)
+    L = cfg["loads"][0]
+    ctx = dbf.DBFFT(cfg["n"], kinematics="small")
+    ctx.set_phases(cfg["phase"], cfg["materials"])
+    ctx.solve_increment(L["target"], L["mask"])
+    r = ctx.residuals(L["target"], L["mask"])
+    ref = O.solve_small_strain(cfg["phase"], cfg["materials"], L, tol=1e-10)
+    XI = O.frequency_grid(cfg["n"])
+    eq_ref = O.equilibrium_residual(ref["sig"], XI)
+    assert r["equilibrium"] <= 2e-10 and eq_ref <= 2e-10
+    xi2 = np.max(np.abs(XI)) ** 2  # round-off bound of a compatible field: ~ eps_machine |xi|^2
+    assert r["compatibility"] <= 1e-14 * xi2
+    assert O.incompatibility(ref["eps"], XI, finite=False) / np.linalg.norm(ref["mean_eps"]) <= 1e-14 * xi2
+    assert r["loading"] <= 1e-10
+    # finite strain: p33 twin, two increments
+    from synth import configs as C
+    cfg = C.p33(n=16)
+    ctx = dbf.DBFFT(cfg["n"], kinematics="finite")
+    ctx.set_phases(cfg["phase"], cfg["materials"])
+    st = O.FiniteStrainState(cfg["n"])
+    for L in cfg["loads"][:2]:
+        ctx.solve_increment(L["target"], L["mask"])
+        ref = O.solve_finite_increment(st, cfg["phase"], cfg["materials"], L, tol=1e-10)
+    r = ctx.residuals(L["target"], L["mask"])
+    XI = O.frequency_grid(cfg["n"])
+    assert r["loading"] <= 1e-14
+    assert r["compatibility"] <= 1e-10
+    assert O.incompatibility(ref["F"], XI, finite=True) / np.linalg.norm(ref["mean_F"] - np.eye(3)) <= 1e-10
+    # equilibrium of the converged Newton state: both sides below the Newton-level tolerance
+    eq_ref = O.equilibrium_residual(ref["P"], XI)
+    assert r["equilibrium"] <= 1e-6 and eq_ref <= 1e-6
+    assert r["equilibrium"] == pytest.approx(eq_ref, rel=0.5, abs=1e-11)

@@ -654,3 +654,47 @@ def test_svk_homogeneous_uniaxial_closed_form():
         assert r["mean_P"][2, 2] == pytest.approx(stretch * (lam + 2 * mu) * e, rel=1e-13)
         assert r["mean_P"][0, 0] == pytest.approx(lam * e, rel=1e-13)
         assert np.abs(r["F"] - np.diag([1.0, 1.0, stretch]).reshape(3, 3, 1, 1, 1)).max() <= 1e-14
+
+
+# ----------------------------------------------------------- residual monitors
+
+def test_incompatibility_closed_forms():
+    """eps_xx = a sin(2 pi y): curl curl eps has eta_zz = -d_yy eps_xx, max = (2 pi)^2 a; F_xy =
+    a sin(2 pi z): curl of row x has (curl F)_xx = -d_z F_xy, max = 2 pi a; symmetric gradients and
+    F = I + grad u are compatible (round-off only)."""
+    n = (8, 12, 16)
+    XI = O.frequency_grid(n)
+    z, y, x = np.meshgrid(np.arange(n[2]) / n[2], np.arange(n[1]) / n[1], np.arange(n[0]) / n[0], indexing="ij")
+    a = 1e-3
+    eps = np.zeros((3, 3) + z.shape)
+    eps[0, 0] = a * np.sin(2 * np.pi * y)
+    assert O.incompatibility(eps, XI, finite=False) == pytest.approx((2 * np.pi) ** 2 * a, rel=1e-12)
+    F = np.zeros((3, 3) + z.shape) + np.eye(3).reshape(3, 3, 1, 1, 1)
+    F[0, 1] += a * np.sin(2 * np.pi * z)
+    assert O.incompatibility(F, XI, finite=True) == pytest.approx(2 * np.pi * a, rel=1e-12)
+    u = O.fft(ms.random_field((3,) + z.shape, 51))
+    xi2 = np.max(np.abs(XI)) ** 2
+    E = O.ifft(O.sym_grad_hat(u, XI))
+    assert O.incompatibility(E, XI, finite=False) <= 1e-14 * xi2 * np.abs(E).max()  # vs ~(2 pi a) xi^2
+    G = O.ifft(O.grad_hat(u, XI))
+    assert O.incompatibility(np.eye(3).reshape(3, 3, 1, 1, 1) + G, XI, finite=True) <= 1e-14 * np.sqrt(xi2) * np.abs(G).max()
+
+
+def test_equilibrium_and_loading_residual_closed_forms():
+    """sigma_xy = sigma_yx = s0 + sin(2 pi x): (div sigma)_y = 2 pi cos(2 pi x), rms = 2 pi/sqrt 2,
+    <sigma> = s0 (e_xy + e_yx); a converged c1 solve has equilibrium <= its PCG tolerance (R7)
+    and loading 0 under strain control."""
+    n = (16, 8, 8)
+    XI = O.frequency_grid(n)
+    z, y, x = np.meshgrid(np.arange(n[2]) / n[2], np.arange(n[1]) / n[1], np.arange(n[0]) / n[0], indexing="ij")
+    s0 = 3.0
+    sig = np.zeros((3, 3) + z.shape)
+    sig[0, 1] = sig[1, 0] = s0 + np.sin(2 * np.pi * x)
+    assert O.equilibrium_residual(sig, XI) == pytest.approx((2 * np.pi / np.sqrt(2)) / (s0 * np.sqrt(2)), rel=1e-12)
+    cfg = configs.c1()
+    L = cfg["loads"][0]
+    r = O.solve_small_strain(cfg["phase"], cfg["materials"], L, tol=1e-10)
+    X1 = O.frequency_grid(cfg["n"])
+    assert O.equilibrium_residual(r["sig"], X1) <= 1e-10
+    assert O.loading_residual(r["mean_eps"], r["mean_sig"], L["target"], L["mask"]) <= 1e-15
+    assert O.incompatibility(r["eps"], X1, finite=False) <= 1e-12

@@ -45,6 +45,8 @@ for name in names:
     t = ev0.elapsed_time(ev1) / 1e3
     prof = ctx.profile_read()
     last = reps[-1]
+    ctx.profile(False)
+    res = ctx.residuals(loads[-1]["target"], loads[-1]["mask"])  # P:270-290 monitors, final state
     print(json.dumps({"config": name, "grid": list(n), "increments": len(loads), "cg_iters": iters,
                       "newton_iters": newton, "time_to_solution_s": t, "setup_s": t_setup, "gen_s": t_gen,
                       "voxel_iter_per_s": N * iters / t,
@@ -52,6 +54,7 @@ for name in names:
                       "macro_strain": np.round(last["macro_strain"], 10).tolist(),
                       "macro_stress": np.round(last["macro_stress"], 10).tolist(),
                       "eps_eq": last["eps_eq"],
+                      "residuals_final": res,
                       "kernel_ms": {k: round(v[0], 3) for k, v in prof.items()}}), flush=True)
     ctx.close()
     del ctx
