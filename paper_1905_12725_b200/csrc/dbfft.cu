@@ -761,6 +761,8 @@ dbfft_status reduce_x(dbfft_ctx ctx, const std::vector<int>& grids, double* host
 // ---------------------------------------------------------------- PCG
 // Solves A {x | xe} = {b | be} with x0 = 0.  Requires CgDev (msig0, be, mask, Minv_e) set.
 // loc layout: [0] <p,q> / <r,z> / <r,r>, [1] <r,r> (CG pairs), [1..9] DC sums, [10] max.
+dbfft_status pcg_body(dbfft_ctx ctx, int every, bool macro, int nb);
+
 dbfft_status pcg(dbfft_ctx ctx, const dbfft_opts& o, int* iters_out) {
   const int nb = cg_blocks();
   const bool macro = ctx->h_cg->macro != 0;
@@ -786,6 +788,19 @@ dbfft_status pcg(dbfft_ctx ctx, const dbfft_opts& o, int* iters_out) {
   CKS(init_dir());
   const int every = std::max(1, o.check_every);
   int restarts = 0;
+  // graphs: single GPU or NCCL ranks (the loopback all-reduce synchronises on the host), and not
+  // while the per-kernel profiler records events; DBFFT_GRAPHS=0 disables
+  const char* genv = getenv("DBFFT_GRAPHS");
+  const bool use_graph = !ctx->prof && !(ctx->P > 1 && ctx->loopback) && !(genv && genv[0] == '0');
+  cudaGraphExec_t graph_exec = nullptr;
+  long long graph_launches = 0;
+  int rounds = 0;
+  struct ExecGuard {
+    cudaGraphExec_t exec = nullptr;
+    ~ExecGuard() {
+      if (exec) cudaGraphExecDestroy(exec);
+    }
+  } guard;
   for (;;) {
     CK(cudaMemcpyAsync(ctx->h_cg, ctx->slabs[0].cg, sizeof(CgDev), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -828,6 +843,41 @@ dbfft_status pcg(dbfft_ctx ctx, const dbfft_opts& o, int* iters_out) {
       CKS(init_dir());
       continue;
     }
+    // `every` PCG iterations between host polls: replayed from a CUDA graph once captured (the
+    // steady-state loop is launch-bound on small grids); captured per pcg() call because M's
+    // coefficients are kernel parameters
+    if (graph_exec) {
+      CK(cudaGraphLaunch(graph_exec, ctx->stream));
+      ctx->nlaunch += graph_launches;
+      continue;
+    }
+    const bool capture = use_graph && rounds > 0;
+    const long long nl0 = ctx->nlaunch;
+    if (capture) CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    ++rounds;
+    dbfft_status bst = pcg_body(ctx, every, macro, nb);
+    if (capture) {
+      cudaGraph_t graph = nullptr;
+      cudaError_t ce = cudaStreamEndCapture(ctx->stream, &graph);
+      if (bst != DBFFT_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return bst;
+      }
+      CK(ce);
+      ce = cudaGraphInstantiate(&graph_exec, graph, 0);
+      cudaGraphDestroy(graph);
+      CK(ce);
+      graph_launches = ctx->nlaunch - nl0;
+      guard.exec = graph_exec;
+      CK(cudaGraphLaunch(graph_exec, ctx->stream));  // the captured round has not run yet
+      continue;
+    }
+    CKS(bst);
+  }
+}
+
+dbfft_status pcg_body(dbfft_ctx ctx, int every, bool macro, int nb) {
+  {
     for (int k = 0; k < every; ++k) {
       ApplyOut ao;
       CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, macro, &CgDev::pe, true, &ao));
@@ -861,6 +911,7 @@ dbfft_status pcg(dbfft_ctx ctx, const dbfft_opts& o, int* iters_out) {
       }
     }
   }
+  return DBFFT_OK;
 }
 
 // set CgDev header fields on the host mirror and upload to every slab

@@ -30,7 +30,8 @@ for name in names:
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
     loads = cfg["loads"][: incs or len(cfg["loads"])]
-    ctx.profile(True)
+    if "--noprof" not in sys.argv:  # the per-kernel profiler disables the CUDA-graph PCG rounds
+        ctx.profile(True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(ctx.stream)
     iters = newton = 0
