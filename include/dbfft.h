@@ -80,7 +80,10 @@ typedef struct {
  * (dlopen libnccl.so.2, or $DBFFT_NCCL_LIB); DBFFT_E_NCCL if it cannot be loaded. */
 dbfft_status dbfft_nccl_unique_id(void* out128);
 
-/* Create a context for grid n (voxels) and cell lengths L.  (sync) */
+/* Create a context for grid n (voxels) and cell lengths L.  Each n[a] is a power of
+ * two in [8, 512] (Nyquist frequencies neglected, R1) or one of the odd sizes 15, 21, 27, 63
+ * (Eq. 1 of P:41-43 verbatim, mixed-radix 3/5/7 FFTs; the paper's cells are 63^3).  world > 1
+ * needs powers of two dividing n2 and n3.  DBFFT_E_INVALID_GRID otherwise.  (sync) */
 dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinematics,
                           const dbfft_env* env, dbfft_ctx* out);
 dbfft_status dbfft_destroy(dbfft_ctx ctx);

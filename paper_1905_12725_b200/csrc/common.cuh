@@ -373,3 +373,116 @@ DBF_DEV void svk_tangent45(const double* F, const double* S, double mu, double l
     }
   }
 }
+
+// ---------------------------------------------------------------------------------------------
+// Mixed-radix FFT for the odd grids of the paper (N = 15, 21, 27, 63 = 3^2 7; Eq. 1 without a
+// Nyquist frequency).  Same Stockham scheme as fft_cta: T = N/P threads per
+// transform, thread g owns positions g + s T (s < P); stage radices R in {3, 5, 7} with R | P,
+// so a thread runs P/R butterflies per stage; exchanges through shared memory via IDX/SYNC.
+// ---------------------------------------------------------------------------------------------
+template <int N>
+struct OddPlan {  // points per thread and the radix sequence (product = N)
+  static constexpr int P = (N == 15) ? 15 : (N == 21) ? 21 : (N == 27) ? 9 : (N == 63) ? 21 : 0;
+  static constexpr int NST = (N == 15) ? 2 : (N == 21) ? 2 : (N == 27) ? 3 : (N == 63) ? 3 : 0;
+  DBF_DEV static constexpr int radix(int st) {
+    return (N == 15) ? (st == 0 ? 3 : 5) : (N == 21) ? (st == 0 ? 3 : 7) : (N == 27) ? 3 : (st < 2 ? 3 : 7);
+  }
+  static_assert(P > 0, "unsupported odd FFT length");
+};
+
+// cos / sin of 2 pi e / R (R = 3, 5, 7), correctly rounded literals (constant-folded when unrolled)
+template <int R>
+DBF_DEV void w_root(int e, double& cs, double& sn) {
+  cs = 1.0;
+  sn = 0.0;
+  if (R == 3) { const double c[3] = {1.000000000000000000000e+00, -5.000000000000000000000e-01, -5.000000000000000000000e-01}; const double s[3] = {0.000000000000000000000e+00, 8.660254037844385965883e-01, -8.660254037844385965883e-01}; cs = c[e]; sn = s[e]; }
+  if (R == 5) { const double c[5] = {1.000000000000000000000e+00, 3.090169943749474512629e-01, -8.090169943749474512629e-01, -8.090169943749474512629e-01, 3.090169943749474512629e-01}; const double s[5] = {0.000000000000000000000e+00, 9.510565162951535311819e-01, 5.877852522924731371035e-01, -5.877852522924731371035e-01, -9.510565162951535311819e-01}; cs = c[e]; sn = s[e]; }
+  if (R == 7) { const double c[7] = {1.000000000000000000000e+00, 6.234898018587334833640e-01, -2.225209339563143928764e-01, -9.009688679024191459987e-01, -9.009688679024191459987e-01, -2.225209339563143928764e-01, 6.234898018587334833640e-01}; const double s[7] = {0.000000000000000000000e+00, 7.818314824680298036341e-01, 9.749279121818236193420e-01, 4.338837391175581204017e-01, -4.338837391175581204017e-01, -9.749279121818236193420e-01, -7.818314824680298036341e-01}; cs = c[e]; sn = s[e]; }
+}
+
+// points per thread of a column / X-pair FFT: 8 for powers of two, OddPlan<N>::P for odd N
+template <int N, bool ODD = (N & 1) != 0>
+struct PtsPerThread { static constexpr int value = 8; };
+template <int N>
+struct PtsPerThread<N, true> { static constexpr int value = OddPlan<N>::P; };
+
+// y_k = sum_r x_r W_R^(rk), W_R = exp(-+2 pi i / R), in place on x[m + M r]
+template <int R, bool INV, int P>
+DBF_DEV void dft_small(cplx (&a)[P], int m, int M) {
+  cplx x[R], y[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) x[r] = a[m + M * r];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    cplx acc = x[0];
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      const int e = (r * k) % R;
+      if (e == 0) {
+        acc = cadd(acc, x[r]);
+      } else {
+        double c, s;
+        w_root<R>(e, c, s);
+        const cplx w = make_double2(c, INV ? s : -s);
+        acc = cadd(acc, cmul(x[r], w));
+      }
+    }
+    y[k] = acc;
+  }
+#pragma unroll
+  for (int k = 0; k < R; ++k) a[m + M * k] = y[k];
+}
+
+template <int N, int R, bool INV, int P>
+DBF_DEV void odd_stage(cplx (&a)[P], int g, int Ns, const cplx* __restrict__ tw) {
+  constexpr int T = N / P;
+  constexpr int M = P / R;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int b = g + m * T;
+    const int k = b % Ns;
+    if (Ns > 1) {
+      const int step = (N / (Ns * R)) * k;
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        cplx w = tw[(r * step) % N];
+        if (INV) w.y = -w.y;
+        a[m + M * r] = cmul(a[m + M * r], w);
+      }
+    }
+    dft_small<R, INV>(a, m, M);
+  }
+}
+
+template <int N, bool INV, class IDX, class SYNC>
+DBF_DEV void fft_odd(cplx (&a)[OddPlan<N>::P], cplx* sbuf, int g, const IDX& idx, const cplx* __restrict__ tw, const SYNC& sync) {
+  typedef OddPlan<N> PL;
+  constexpr int P = PL::P, T = N / P;
+  int Ns = 1;
+#pragma unroll
+  for (int st = 0; st < PL::NST; ++st) {
+    const int R = PL::radix(st);
+    if (st > 0) {
+#pragma unroll
+      for (int s = 0; s < P; ++s) a[s] = sbuf[idx(g + s * T)];
+    }
+    if (R == 3) odd_stage<N, 3, INV>(a, g, Ns, tw);
+    else if (R == 5) odd_stage<N, 5, INV>(a, g, Ns, tw);
+    else odd_stage<N, 7, INV>(a, g, Ns, tw);
+    if (st < PL::NST - 1) {
+      sync();
+      const int M = P / R;
+#pragma unroll
+      for (int m = 0; m < P; ++m) {
+        if (m >= M) break;
+        const int b = g + m * T;
+        const int base = (b / Ns) * Ns * R + (b % Ns);
+#pragma unroll
+        for (int r = 0; r < 7; ++r)
+          if (r < R) sbuf[idx(base + r * Ns)] = a[m + M * r];
+      }
+      sync();
+    }
+    Ns *= R;
+  }
+}

@@ -92,7 +92,9 @@ int ilog2(int n) {
   return k;
 }
 
-bool is_pow2_in(int n) { return n >= 8 && n <= 512 && (n & (n - 1)) == 0; }
+// grid sizes with FFT kernels: powers of two 8..512, and the odd sizes 15, 21, 27, 63 (the
+// paper's 63^3 cells, Eq. 1 without a Nyquist frequency)
+bool is_pow2_in(int n) { return (n >= 8 && n <= 512 && (n & (n - 1)) == 0) || n == 15 || n == 21 || n == 27 || n == 63; }
 
 }  // namespace
 
@@ -1375,7 +1377,7 @@ dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinemat
   *out = nullptr;
   for (int a = 0; a < 3; ++a)
     if (!is_pow2_in(n[a]) || !(L[a] > 0)) {
-      g_create_error = "grid dims must be powers of two in [8,512] and L > 0";
+      g_create_error = "grid dims must be powers of two in [8,512] or one of 15, 21, 27, 63, and L > 0";
       return DBFFT_E_INVALID_GRID;
     }
   if (kinematics != 6 && kinematics != 9) {

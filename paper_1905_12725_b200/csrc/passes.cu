@@ -252,12 +252,22 @@ struct ColTwo {  // does any output of this pass sum two transformed terms?
 
 // Column-pass CTA geometry: 256 threads; a column's length-N FFT is done by N/8 threads
 // (8 points each); columns are kx-contiguous so each warp load is 128-byte row segments.
+// Odd N (the paper's 63^3 grids): OddPlan<N>::P points per thread, mixed radix.
 template <int N>
 struct ColCfg {
-  static constexpr int THREADS = 256;
-  static constexpr int TPC = N / 8;
+  static constexpr bool ODD = (N & 1) != 0;
+  static constexpr int P = PtsPerThread<N>::value;  // points per thread
+  static constexpr int TPC = N / P;
   static constexpr int COLS = 256 / TPC;
+  static constexpr int THREADS = COLS * TPC;
 };
+
+// the in-CTA FFT of a column pass / X pair: radix-8 (powers of two) or mixed radix (odd N)
+template <int N, bool INV, class IDX, class SYNC>
+DBF_DEV void fft_col(cplx (&a)[ColCfg<N>::P], cplx* sbuf, int g, const IDX& idx, const cplx* __restrict__ tw, const SYNC& sync) {
+  if constexpr (ColCfg<N>::ODD) fft_odd<N, INV>(a, sbuf, g, idx, tw, sync);
+  else fft_cta<N, INV>(a, sbuf, g, idx, tw, sync);
+}
 
 // single-term passes pipeline the next term's loads in registers (2 CTAs/SM); two-term
 // passes keep the first term in shared memory and run without prefetch (3 CTAs/SM)
@@ -268,10 +278,10 @@ struct ColPref {
 };
 
 template <int N, int KIND>
-__global__ void __launch_bounds__(256, ColPref<KIND>::MINB) col_pass_kernel(ColGeom g) {
+__global__ void __launch_bounds__(256, ColCfg<N>::ODD ? 1 : ColPref<KIND>::MINB) col_pass_kernel(ColGeom g) {
   typedef ColOp<KIND> Op;
-  constexpr int TPC = N / 8;
-  constexpr int COLS = 256 / TPC;
+  typedef ColCfg<N> CF;
+  constexpr int P = CF::P, TPC = CF::TPC, COLS = CF::COLS;
   constexpr bool TWO = ColTwo<KIND>::value;
   constexpr bool PREF = ColPref<KIND>::value;
   extern __shared__ cplx col_smem[];
@@ -288,22 +298,22 @@ __global__ void __launch_bounds__(256, ColPref<KIND>::MINB) col_pass_kernel(ColG
   const double wdot = (at.kx == 0 || 2 * at.kx == g.n1) ? 1.0 : 2.0;
   double dot = 0.0;
   IdxCols<COLS> idx{c};
-  cplx r0[PREF ? 8 : 1];
+  cplx r0[PREF ? P : 1];
   if (PREF) {
     const TermInfo ti = Op::term(0);
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      at.pos = gq + s * (N / 8);
+    for (int s = 0; s < P; ++s) {
+      at.pos = gq + s * TPC;
       r0[PREF ? s : 0] = valid ? at.in(ti.f0) : make_double2(0.0, 0.0);
     }
   }
 #pragma unroll 1
   for (int j = 0; j < Op::NT; ++j) {
     const TermInfo ti = Op::term(j);
-    cplx a[8];
+    cplx a[P];
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      at.pos = gq + s * (N / 8);
+    for (int s = 0; s < P; ++s) {
+      at.pos = gq + s * TPC;
       if (PREF) {
         a[s] = Op::pre(at, j, r0[PREF ? s : 0], r0[PREF ? s : 0]);
       } else {
@@ -315,15 +325,15 @@ __global__ void __launch_bounds__(256, ColPref<KIND>::MINB) col_pass_kernel(ColG
     if (PREF && j + 1 < Op::NT) {  // issue the next term's loads; they fly during this FFT
       const TermInfo tn = Op::term(j + 1);
 #pragma unroll
-      for (int s = 0; s < 8; ++s) {
-        at.pos = gq + s * (N / 8);
+      for (int s = 0; s < P; ++s) {
+        at.pos = gq + s * TPC;
         r0[PREF ? s : 0] = valid ? at.in(tn.f0) : make_double2(0.0, 0.0);
       }
     }
-    fft_cta<N, Op::INV>(a, sbuf, gq, idx, g.tw);
+    fft_col<N, Op::INV>(a, sbuf, gq, idx, g.tw, SyncCtaDefault{});
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      at.pos = gq + s * (N / 8);
+    for (int s = 0; s < P; ++s) {
+      at.pos = gq + s * TPC;
       cplx v = cmul(Op::post(at, j), a[s]);
       if (TWO && !ti.first) v = cadd(v, sacc[idx(at.pos)]);
       if (!ti.last) {
@@ -652,14 +662,18 @@ struct IdxSwz {
 
 // pass_X FFT of one field pair: radix-8 with CTA-wide exchange barriers (P = 8) or radix-16
 // with warp-local exchanges (P = 16, the pair's threads share a warp)
-template <int P>
+struct IdxPlain {
+  int base;
+  DBF_DEV int operator()(int pos) const { return base + pos; }
+};
+template <int N1, int P>
 DBF_DEV int x_idx(int base, int pos) {
-  return P == 16 ? IdxGrp{base}(pos) : IdxSwz{base}(pos);
+  return (N1 & 1) ? IdxPlain{base}(pos) : P == 16 ? IdxGrp{base}(pos) : IdxSwz{base}(pos);
 }
-// a pair job's threads share one warp when N1 / P <= 32: exchanges need only __syncwarp
+// a pair job's threads share one warp when N1 / P divides 32: exchanges need only __syncwarp
 template <int N1, int P>
 DBF_DEV void x_jobsync() {
-  if (N1 / P <= 32) __syncwarp();
+  if (N1 / P <= 32 && 32 % (N1 / P) == 0) __syncwarp();
   else __syncthreads();
 }
 template <int N1, int P>
@@ -668,7 +682,9 @@ struct XSync {
 };
 template <int N1, int P, bool INV>
 DBF_DEV void x_fft(cplx (&a)[P], cplx* cx, int gq, int base, const cplx* __restrict__ tw) {
-  if constexpr (P == 16) {
+  if constexpr ((N1 & 1) != 0) {
+    fft_odd<N1, INV>(a, cx, gq, IdxPlain{base}, tw, XSync<N1, P>{});
+  } else if constexpr (P == 16) {
     fft_sub<N1, 16, INV>(a, cx, gq, IdxGrp{base}, tw, XSync<N1, 16>{});
   } else {
     fft_cta<N1, INV>(a, cx, gq, IdxSwz{base}, tw, XSync<N1, 8>{});
@@ -695,7 +711,7 @@ DBF_DEV void x_partner(const cplx (&a)[8], cplx (&zn)[8], int gq) {
 // is static except at s = PX/2, where only gq = 0 (k = N1/2) qualifies
 template <int N1, int PX, int TPJ>
 DBF_DEV bool x_lo(int s, int gq) {
-  if (TPJ * PX != N1) return 2 * (gq + s * TPJ) <= N1;
+  if (TPJ * PX != N1 || (N1 & 1)) return 2 * (gq + s * TPJ) <= N1;
   return s < PX / 2 || (s == PX / 2 && gq == 0);
 }
 // apply kinds reduce <out> from the R2C DC (sums over the line), no per-voxel accumulators
@@ -724,7 +740,7 @@ struct XCfg {
   typedef XStage<KIND> S;
   static constexpr int C = (T::CIN > T::COUT) ? T::CIN : T::COUT;
   static constexpr int CS = (C + 1) & ~1;          // real slots per line (even)
-  static constexpr int PX = (N1 >= 16) ? DBF_X_P : 8;   // FFT points per thread
+  static constexpr int PX = (N1 & 1) ? PtsPerThread<N1>::value : (N1 >= 16) ? DBF_X_P : 8;   // FFT points per thread
   static constexpr int TPJ = N1 / PX;              // threads per pair FFT (divides 32: warp-local)
   static constexpr int NP = CS / 2;
   static constexpr int PERLINE = TPJ * NP;
@@ -733,9 +749,11 @@ struct XCfg {
   static constexpr int THREADS = LPAR * PERLINE;
   static constexpr int N1H = N1 / 2 + 1;
   static constexpr size_t SLOTS = sizeof(double) * LPAR * CS * N1;
-  static constexpr size_t ST_IN = S::IN ? sizeof(cplx) * LPAR * T::CIN * N1H : 0;
-  static constexpr size_t ST_TAN = sizeof(double) * LPAR * S::NTAN * N1;
-  static constexpr size_t ST_PH = S::PH ? ((sizeof(uint16_t) * LPAR * N1 + 15) & ~size_t(15)) : 0;
+  // bulk-copy staging needs 16-byte rows: powers of two only (odd lines load directly)
+  static constexpr bool STG = S::IN && (N1 & 1) == 0;
+  static constexpr size_t ST_IN = STG ? sizeof(cplx) * LPAR * T::CIN * N1H : 0;
+  static constexpr size_t ST_TAN = STG ? sizeof(double) * LPAR * S::NTAN * N1 : 0;
+  static constexpr size_t ST_PH = (STG && S::PH) ? ((sizeof(uint16_t) * LPAR * N1 + 15) & ~size_t(15)) : 0;
   static constexpr size_t SMEM = SLOTS + ST_IN + ST_TAN + ST_PH + 16;  // + 2 mbarriers
   static constexpr int MINB = (THREADS <= 192) ? DBF_X_MINB : 2;
 };
@@ -803,6 +821,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
   typedef XTraits<KIND> T;
   typedef XStage<KIND> S;
   constexpr int C = CF::C, CS = CF::CS, TPJ = CF::TPJ, NP = CF::NP, LPAR = CF::LPAR, PX = CF::PX;
+  constexpr bool SIN = CF::STG;  // stage inputs / tangent with bulk copies
   extern __shared__ __align__(16) double real[];
   cplx* cx = reinterpret_cast<cplx*>(real);
   unsigned char* sb = reinterpret_cast<unsigned char*>(real);
@@ -814,7 +833,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
   const int job = t / TPJ, gq = t % TPJ;
   const int l = job / NP, p = job % NP;
   const int fa = 2 * p, fb = 2 * p + 1;
-  const int jbase = (l * CS + fa) * (N1 / 2);  // complex view of slots fa, fb of line l (job buffer)
+  const int jbase = ((l * CS + fa) * N1) / 2;  // complex view of slots fa, fb of line l (job buffer)
   const int cin = (KIND == X_REAL_OUT) ? nf_real : T::CIN;
   const int cout_rt = (KIND == X_REAL_IN) ? nf_real : T::COUT;  // spectral outputs written
   const bool do_in = (T::CIN > 0) && (cin > 0) && ((KIND != X_CONST_FIN && KIND != X_CONST_J2) || g.has_in);
@@ -829,7 +848,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
 #pragma unroll
   for (int r = 0; r < (T::NRED > 0 ? T::NRED : 1); ++r) red[r] = 0.0;
   constexpr bool STAGE_TAN = (S::NTAN > 0 || S::PH);
-  if (S::IN) {
+  if (SIN) {
     if (t == 0) {
       mbar_init(&bars[0], 1);
       mbar_init(&bars[1], 1);
@@ -849,7 +868,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
     const long long nxt = grp + gridDim.x;
     // ------------------------------------------------------------ inverse (C2R) of pairs
     if (do_in) {
-      if (S::IN) mbar_wait(&bars[0], it & 1);
+      if (SIN) mbar_wait(&bars[0], it & 1);
       cplx a[PX];
 #pragma unroll
       for (int s = 0; s < PX; ++s) {
@@ -858,7 +877,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
         const int kk = lo ? k : N1 - k;
         cplx A = make_double2(0, 0), B = make_double2(0, 0);
         if (lvalid && fa < cin) {
-          if (S::IN) {
+          if (SIN) {
             A = st_in[(l * T::CIN + fa) * CF::N1H + kk];
             if (fb < cin) B = st_in[(l * T::CIN + fb) * CF::N1H + kk];
           } else {
@@ -871,7 +890,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
         // Y_k = A_k + i B_k (k <= N/2);  conj(A_{N-k}) + i conj(B_{N-k}) otherwise
         a[s] = lo ? make_double2(A.x - B.y, A.y + B.x) : make_double2(A.x + B.y, B.x - A.y);
       }
-      if (S::IN) {
+      if (SIN) {
         __syncthreads();  // everyone has read the input stage
         if (t == 0 && nxt < ngroups) {
           fence_proxy_async();
@@ -910,7 +929,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
     }
 
     // ------------------------------------------------------------ per-voxel operation
-    if (S::IN && STAGE_TAN) mbar_wait(&bars[1], it & 1);
+    if (SIN && STAGE_TAN) mbar_wait(&bars[1], it & 1);
     for (int vv = t; KIND != X_REAL_IN && vv < LPAR * N1; vv += CF::THREADS) {
       const int l2 = vv / N1, x = vv % N1;
       const long long ln = grp * LPAR + l2;
@@ -922,7 +941,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
       const double* tp;
       long long ts;
       int ph;
-      if (S::IN && STAGE_TAN) {
+      if (SIN && STAGE_TAN) {
         tp = st_tan + vv;
         ts = LPAR * N1;
         ph = S::PH ? (int)st_ph[vv] : 0;
@@ -936,7 +955,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
       for (int f = 0; f < T::COUT; ++f) real[(l2 * CS + f) * N1 + x] = P[f];
     }
     __syncthreads();
-    if (S::IN && STAGE_TAN && t == 0 && nxt < ngroups) {
+    if (SIN && STAGE_TAN && t == 0 && nxt < ngroups) {
       fence_proxy_async();
       x_issue_tan<N1, KIND>(g, nxt, st_tan, st_ph, &bars[1]);
     }
@@ -960,10 +979,10 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
       } else {
         x_jobsync<N1, PX>();
 #pragma unroll
-        for (int s = 0; s < PX; ++s) cx[x_idx<PX>(jbase, gq + s * TPJ)] = a[s];
+        for (int s = 0; s < PX; ++s) cx[x_idx<N1, PX>(jbase, gq + s * TPJ)] = a[s];
         x_jobsync<N1, PX>();
 #pragma unroll
-        for (int s = 0; s < PX; ++s) zn[s] = cx[x_idx<PX>(jbase, (N1 - (gq + s * TPJ)) & (N1 - 1))];
+        for (int s = 0; s < PX; ++s) zn[s] = cx[x_idx<N1, PX>(jbase, (N1 - (gq + s * TPJ)) % N1)];
       }
       if (lvalid && fa < cout_rt) {
 #pragma unroll
@@ -1361,6 +1380,10 @@ int col_grid(int N, long long ncols) {
     case 64: cols = col_cols<64>(); break;
     case 128: cols = col_cols<128>(); break;
     case 256: cols = col_cols<256>(); break;
+    case 15: cols = col_cols<15>(); break;
+    case 21: cols = col_cols<21>(); break;
+    case 27: cols = col_cols<27>(); break;
+    case 63: cols = col_cols<63>(); break;
     default: cols = col_cols<512>(); break;
   }
   return (int)((ncols + cols - 1) / cols);
@@ -1548,6 +1571,10 @@ static cudaError_t launch_col_reg(int kind, int N, const ColGeom& g, cudaStream_
     case 128: return launch_col_n<128>(kind, g, s);
     case 256: return launch_col_n<256>(kind, g, s);
     case 512: return launch_col_n<512>(kind, g, s);
+    case 15: return launch_col_n<15>(kind, g, s);
+    case 21: return launch_col_n<21>(kind, g, s);
+    case 27: return launch_col_n<27>(kind, g, s);
+    case 63: return launch_col_n<63>(kind, g, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -1610,6 +1637,10 @@ cudaError_t launch_x(int kind, int N1, const XGeom& g, cudaStream_t s, int* grid
     case 128: return launch_x_n<128>(kind, g, s, grid_out);
     case 256: return launch_x_n<256>(kind, g, s, grid_out);
     case 512: return launch_x_n<512>(kind, g, s, grid_out);
+    case 15: return launch_x_n<15>(kind, g, s, grid_out);
+    case 21: return launch_x_n<21>(kind, g, s, grid_out);
+    case 27: return launch_x_n<27>(kind, g, s, grid_out);
+    case 63: return launch_x_n<63>(kind, g, s, grid_out);
     default: return cudaErrorInvalidValue;
   }
 }

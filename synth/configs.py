@@ -89,6 +89,18 @@ def c5s(n=128, grains=31, seed=5, increments=20):
     return d
 
 
+def s31(n=63, contrast=10.0, vf=0.2):
+    """The paper's SS3.1 cell: one centred spherical inclusion of volume fraction
+    `vf` in an n^3 cell (63^3 in the paper), matrix E = 70 MPa, nu = 0.3, inclusion E = k E_m;
+    uniaxial strain 0.1 % (full strain control, other components 0)."""
+    r = (3.0 * vf / (4.0 * np.pi)) ** (1.0 / 3.0)
+    phase = ms.centred_sphere((n, n, n), r)
+    mats = [dict(kind="iso", E=70.0, nu=0.3), dict(kind="iso", E=70.0 * contrast, nu=0.3)]
+    t = np.zeros((3, 3)); t[0, 0] = 1e-3
+    return dict(name="s31", n=(n, n, n), kin=SMALL, phase=phase, materials=mats,
+                loads=[_load(t, np.zeros((3, 3), bool))], dt=1.0)
+
+
 def p33(n=64, pores=5, vf=0.2, seed=33, increments=5, stretch=2.0):
     """The paper's own finite-strain benchmark (SS3.3), synthetic stand-in:
     SVK matrix E = 70 MPa, nu = 0.3 with `pores` non-overlapping spherical voids of total volume
@@ -104,4 +116,4 @@ def p33(n=64, pores=5, vf=0.2, seed=33, increments=5, stretch=2.0):
     return dict(name="p33", n=(n, n, n), kin=FINITE, phase=phase, materials=mats, loads=loads, dt=1.0)
 
 
-CONFIGS = dict(c1=c1, c2=c2, c3=c3, c4=c4, c5=c5, c5s=c5s, p33=p33)
+CONFIGS = dict(c1=c1, c2=c2, c3=c3, c4=c4, c5=c5, c5s=c5s, p33=p33, s31=s31)

@@ -439,3 +439,67 @@ def test_residuals_after_solves(dbf):
     eq_ref = O.equilibrium_residual(ref["P"], XI)
     assert r["equilibrium"] <= 1e-6 and eq_ref <= 1e-6
     assert r["equilibrium"] == pytest.approx(eq_ref, rel=0.5, abs=1e-11)
+
+
+# ------------------------------------------------------ odd grids, Eq. 1 verbatim
+
+ODD_GRIDS = [(15, 21, 27), (63, 15, 21), (21, 16, 63), (27, 27, 27)]
+
+
+@pytest.mark.parametrize("n", ODD_GRIDS)
+def test_apply_K_odd_small(dbf, n):
+    """Mixed-radix (3, 5, 7) column and X passes, no Nyquist frequency (Eq. 1)."""
+    ph = two_phase(n, 71)
+    ctx = dbf.DBFFT(n, kinematics="small")
+    ctx.set_phases(ph, ISO2)
+    u = ms.random_field((3, n[2], n[1], n[0]), 72)
+    f = ctx.apply_K(to_gpu_spec(dbf, u))
+    ref, _ = O.apply_K(O.fft(u), O.stiffness_field(ph, ISO2), O.frequency_grid(n))
+    assert rel(gpu_full(dbf, f, n[0]), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("n", ODD_GRIDS[:3])
+def test_apply_K_odd_finite(dbf, n):
+    ph = two_phase(n, 73)
+    mats = [dict(kind="svk", E=70.0, nu=0.3), dict(kind="neohooke", mu=1.0, kappa=2.5)]
+    F = np.eye(3).reshape(3, 3, 1, 1, 1) + 0.1 * ms.random_field((3, 3, n[2], n[1], n[0]), 74)
+    ctx = dbf.DBFFT(n, kinematics="finite")
+    ctx.set_phases(ph, mats)
+    ctx.eval_state(F.reshape(9, n[2], n[1], n[0]))
+    u = ms.random_field((3, n[2], n[1], n[0]), 75)
+    f = ctx.apply_K(to_gpu_spec(dbf, u))
+    _, K = O.hyperelastic(F, ph, mats)
+    ref, _ = O.apply_K(O.fft(u), K, O.frequency_grid(n), finite=True)
+    assert rel(gpu_full(dbf, f, n[0]), ref) <= 1e-12
+
+
+def test_solve_odd_63_sphere_contrast(dbf):
+    """The paper's SS3.1 cell: 63^3, centred sphere vf 0.2, E_m = 70, nu = 0.3, uniaxial
+    strain 0.1 %, contrast k = 10 (and a soft k = 1e-2 case): GPU = oracle."""
+    from synth import configs as C
+    for k in (10.0, 1e-2):
+        cfg = C.s31(n=63, contrast=k)
+        L = cfg["loads"][0]
+        ref = O.solve_small_strain(cfg["phase"], cfg["materials"], L, tol=1e-10)
+        ctx = dbf.DBFFT(cfg["n"], kinematics="small")
+        ctx.set_phases(cfg["phase"], cfg["materials"])
+        rep = ctx.solve_increment(L["target"], L["mask"])
+        assert rep["converged"]
+        assert abs(rep["cg_iters"] - ref["iters"]) <= max(2, 0.03 * ref["iters"])
+        assert rel(rep["macro_stress"], ref["mean_sig"]) <= 1e-9
+        assert rel(ctx.get_field(dbf.FIELD_STRESS), ref["sig"]) <= 1e-8
+
+
+def test_solve_odd_p33_twin(dbf):
+    """SS3.3 on an odd grid (21^3 twin of the 63^3 cell): two increments, GPU = oracle."""
+    from synth import configs as C
+    cfg = C.p33(n=21)
+    st = O.FiniteStrainState(cfg["n"])
+    ctx = dbf.DBFFT(cfg["n"], kinematics="finite")
+    ctx.set_phases(cfg["phase"], cfg["materials"])
+    for L in cfg["loads"][:2]:
+        ref = O.solve_finite_increment(st, cfg["phase"], cfg["materials"], L, tol=1e-10)
+        rep = ctx.solve_increment(L["target"], L["mask"])
+        assert rep["converged"] and rep["newton_iters"] == ref["newton_iters"]
+        assert rel(rep["macro_stress"], ref["mean_P"]) <= 1e-9
+        assert rel(ctx.get_field(dbf.FIELD_STRAIN), ref["F"]) <= 1e-8

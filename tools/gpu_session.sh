@@ -1,2 +1,2 @@
-timeout 900 python tools/run_configs.py c1 c2 c3 p33 --noprof > gpurun_out/configs_g.jsonl 2>&1
-DBFFT_GRAPHS=0 timeout 900 python tools/run_configs.py c1 c2 c3 p33 --noprof > gpurun_out/configs_ng.jsonl 2>&1
+timeout 1800 python -m pytest tests -m gpu -q 2>&1 | tail -3
+timeout 900 python tools/contrast_sweep.py 63 > gpurun_out/contrast63.jsonl 2> gpurun_out/contrast63.err; tail -2 gpurun_out/contrast63.err
