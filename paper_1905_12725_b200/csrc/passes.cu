@@ -1165,11 +1165,22 @@ struct TmaCfg {
   static constexpr int CONS = 256;             // consumer threads (8 warps)
   static constexpr int THREADS = CONS + 32;    // + producer warp
   static constexpr int TILE = 32768;           // bytes per ring slot / staging buffer
+  static constexpr int SW = KC < 8 ? KC : 8;   // sub-tile width in columns (TMA box rows of 16 SW bytes)
 };
 
 // cplx offset of (pos, column c) inside a main tile: KC/8 sub-tiles of [N][8], 128B swizzle
 template <int N>
-DBF_DEV int tma_moff(int pos, int c) { return (c >> 3) * (N * 8) + pos * 8 + ((c & 7) ^ (pos & 7)); }
+DBF_DEV int tma_moff(int pos, int c) {
+  constexpr int SW = TmaCfg<N>::SW;  // columns per sub-tile row: 8 (128B swizzle) or 4 (64B)
+  if (SW == 8) return (c >> 3) * (N * 8) + pos * 8 + ((c & 7) ^ (pos & 7));
+  return (c / SW) * (N * SW) + pos * SW + ((c % SW) ^ ((pos >> 1) & 3));
+}
+// exchange sync of one column's N/8 threads: the warp, or a named barrier when a column spans
+// two warps (N = 512: 64 threads, ids 2..5)
+struct SyncCol {
+  int id, nthreads;
+  DBF_DEV void operator()() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory"); }
+};
 // tail tile: [KC][N] unswizzled
 template <int N>
 DBF_DEV int tma_toff(int pos, int c) { return c * N + pos; }
@@ -1245,8 +1256,9 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
             tma_load5(dst, isdot ? &maps.dot_t : &maps.in_t, 2 * (g.n1h - 1), 0, 0, outer, f, &full[slot]);
           } else {
 #pragma unroll
-            for (int sb = 0; sb < KC / 8; ++sb)
-              tma_load5(dst + sb * N * 8, isdot ? &maps.dot_m : &maps.in_m, 2 * (kb * KC + sb * 8), 0, 0, outer, f, &full[slot]);
+            for (int sb = 0; sb < KC / CF::SW; ++sb)
+              tma_load5(dst + sb * N * CF::SW, isdot ? &maps.dot_m : &maps.in_m, 2 * (kb * KC + sb * CF::SW), 0, 0, outer, f,
+                        &full[slot]);
           }
         }
       }
@@ -1297,7 +1309,8 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
         const cplx v1 = (lb >= 0) ? sbp[o] : v0;
         a[s] = Op::pre(at, j, v0, v1);
       }
-      fft_cta<N, Op::INV>(a, xcol, gq, IdxSwz{0}, g.tw, SyncWarp{});
+      if constexpr (TPC <= 32) fft_cta<N, Op::INV>(a, xcol, gq, IdxSwz{0}, g.tw, SyncWarp{});
+      else fft_cta<N, Op::INV>(a, xcol, gq, IdxSwz{0}, g.tw, SyncCol{2 + c, TPC});
       const int ai = pg.acc[k];
       const int ld = pg.ldot[k];
       const cplx* sd = nullptr;
@@ -1338,10 +1351,10 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
         if (t == 0) {
           if (tail) tma_store5(&maps.out_t, 2 * (g.n1h - 1), 0, 0, (tile - tl.n_main) * KC, ti.o, so);
           else tma_store5(&maps.out_m, 2 * ((tile % tl.nkb) * KC), 0, 0, tile / tl.nkb, ti.o, so);
-          if (!tail && KC > 8) {
+          if (!tail && KC > CF::SW) {
 #pragma unroll
-            for (int sb = 1; sb < KC / 8; ++sb)
-              tma_store5(&maps.out_m, 2 * ((tile % tl.nkb) * KC + sb * 8), 0, 0, tile / tl.nkb, ti.o, so + sb * N * 8);
+            for (int sb = 1; sb < KC / CF::SW; ++sb)
+              tma_store5(&maps.out_m, 2 * ((tile % tl.nkb) * KC + sb * CF::SW), 0, 0, tile / tl.nkb, ti.o, so + sb * N * CF::SW);
           }
           bulk_commit();
         }
@@ -1467,10 +1480,12 @@ static bool col_map(CUtensorMap* m, const void* ptr, int N, int n1h, int psh, lo
   if (N / L > 256) return false;
   cuuint64_t dims[5] = {(cuuint64_t)(2 * n1h), (cuuint64_t)L, (cuuint64_t)(N / L), (cuuint64_t)n_outer, (cuuint64_t)nf};
   cuuint64_t strides[4] = {(cuuint64_t)(ps * 16), (cuuint64_t)(pcs * 16), (cuuint64_t)(os * 16), (cuuint64_t)(fs * 16)};
-  cuuint32_t box[5] = {tail ? 2u : 16u, (cuuint32_t)L, (cuuint32_t)(N / L), tail ? (cuuint32_t)std::min(KC, n_outer) : 1u, 1u};
+  const int SW = KC < 8 ? KC : 8;
+  cuuint32_t box[5] = {tail ? 2u : (cuuint32_t)(2 * SW), (cuuint32_t)L, (cuuint32_t)(N / L), tail ? (cuuint32_t)std::min(KC, n_outer) : 1u, 1u};
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<void*>(ptr), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, tail ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   tail ? CU_TENSOR_MAP_SWIZZLE_NONE : (SW == 8 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B),
                    DBF_TMA_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -1581,7 +1596,11 @@ static cudaError_t launch_col_reg(int kind, int N, const ColGeom& g, cudaStream_
 
 cudaError_t launch_col(int kind, int N, const ColGeom& g, cudaStream_t s, int* grid_out) {
   cudaError_t e = cudaErrorNotSupported;
-  if (N == 256) e = launch_col_tma<256>(kind, g, s, grid_out);
+  // N = 512 y-forward passes write rows 2 MB apart (the ky stride of [f][ky][z][kx] at 512^2): the
+  // TMA store path ran them at 2.2 TB/s against 4 TB/s for direct stores (B200, kbench 512^3)
+  const bool far_store = N == 512 && (kind == COL_F2S || kind == COL_F2F || kind == COL_YF3 || kind == COL_YF6);
+  if (N == 512 && !far_store) e = launch_col_tma<512>(kind, g, s, grid_out);
+  else if (N == 256) e = launch_col_tma<256>(kind, g, s, grid_out);
   else if (N == 128) e = launch_col_tma<128>(kind, g, s, grid_out);
   else if (N == 64) e = launch_col_tma<64>(kind, g, s, grid_out);
   if (e != cudaErrorNotSupported) return e;

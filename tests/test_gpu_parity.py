@@ -94,8 +94,9 @@ def test_apply_K_finite_neohooke(dbf, n, tangent, monkeypatch):
 
 # grids whose z / y sweeps take the TMA column kernel (N in {64, 128, 256}, n1/2 a multiple of
 # 2048/N): several kx blocks + the Nyquist tail tiles, and an outer count (8) below the tile
-# width (16 at N = 128: narrower tail boxes)
-TMA_GRIDS = [(32, 128, 256), (64, 256, 128), (32, 8, 128), (128, 64, 64)]
+# width (16 at N = 128: narrower tail boxes); N = 512 runs 4-column tiles (64-byte rows, 64B
+# swizzle) with a column's 64 threads on two warps (named-barrier exchanges)
+TMA_GRIDS = [(32, 128, 256), (64, 256, 128), (32, 8, 128), (128, 64, 64), (16, 8, 512), (8, 512, 16)]
 
 
 @pytest.mark.parametrize("n", TMA_GRIDS)
@@ -109,7 +110,7 @@ def test_apply_K_tma_small(dbf, n):
     assert rel(gpu_full(dbf, f, n[0]), ref) <= 1e-12
 
 
-@pytest.mark.parametrize("n", TMA_GRIDS[:3])
+@pytest.mark.parametrize("n", TMA_GRIDS[:3] + TMA_GRIDS[4:])
 def test_apply_K_tma_finite(dbf, n):
     ph = two_phase(n, 33)
     mats = [dict(kind="neohooke", mu=1.0, kappa=2.5), dict(kind="neohooke", mu=10.0, kappa=25.0)]

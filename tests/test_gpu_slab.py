@@ -34,7 +34,7 @@ ISO2 = [dict(kind="iso", E=1.0, nu=0.3), dict(kind="iso", E=10.0, nu=0.25)]
 
 
 @pytest.mark.parametrize("P", [2, 4, 8])
-@pytest.mark.parametrize("n", [(16, 8, 32), (32, 32, 16), (32, 128, 256)])
+@pytest.mark.parametrize("n", [(16, 8, 32), (32, 32, 16), (32, 128, 256), (16, 32, 512)])
 def test_apply_K_small_loopback(dbf, n, P):
     if n[1] % P or n[2] % P:
         pytest.skip("P must divide n2 and n3")

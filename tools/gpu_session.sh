@@ -1,2 +1,2 @@
-timeout 1800 python -m pytest tests -m gpu -q 2>&1 | tail -3
-timeout 900 python tools/contrast_sweep.py 63 > gpurun_out/contrast63.jsonl 2> gpurun_out/contrast63.err; tail -2 gpurun_out/contrast63.err
+timeout 300 python tools/kbench.py 512 5 small
+timeout 1800 python tools/run_configs.py c5 --noprof > gpurun_out/c5.jsonl 2> gpurun_out/c5.err; tail -2 gpurun_out/c5.err; cat gpurun_out/c5.jsonl
