@@ -91,9 +91,10 @@ __global__ void __launch_bounds__(BLK) k_cg_init(SpecGeom g, PrecQ Q, const cplx
 }
 
 // x += alpha p ; r -= alpha q ; z = M r ; partials (<r, z>, <r, r>)
-__global__ void __launch_bounds__(BLK) k_cg_update(SpecGeom g, PrecQ Q, const CgDev* __restrict__ cg, cplx* __restrict__ x,
-                                                   const cplx* __restrict__ pv, cplx* __restrict__ r, const cplx* __restrict__ qv,
-                                                   double* partials) {
+// r -= alpha q, z = M r on the fly, partial <r,z>, <r,r> (x += alpha p is deferred to the
+// direction kernel, which reads p anyway: 3 vector transfers here instead of 6)
+__global__ void __launch_bounds__(BLK) k_cg_update(SpecGeom g, PrecQ Q, const CgDev* __restrict__ cg, cplx* __restrict__ r,
+                                                   const cplx* __restrict__ qv, double* partials) {
   if (cg->converged | cg->breakdown) return;
   const double alpha = cg->alpha;
   double acc[2] = {0.0, 0.0};
@@ -103,10 +104,8 @@ __global__ void __launch_bounds__(BLK) k_cg_update(SpecGeom g, PrecQ Q, const Cg
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const long long j = c * g.Hs + i;
-      cplx pj = __ldg(pv + j), xj = x[j], rj = r[j], qj = __ldg(qv + j);
-      xj.x = fma(alpha, pj.x, xj.x); xj.y = fma(alpha, pj.y, xj.y);
+      cplx rj = r[j], qj = __ldg(qv + j);
       rj.x = fma(-alpha, qj.x, rj.x); rj.y = fma(-alpha, qj.y, rj.y);
-      x[j] = xj;
       r[j] = rj;
       rv[c] = rj;
     }
@@ -121,23 +120,50 @@ __global__ void __launch_bounds__(BLK) k_cg_update(SpecGeom g, PrecQ Q, const Cg
   block_store<2>(acc, partials);
 }
 
-// p = M r + beta p
-__global__ void __launch_bounds__(BLK) k_cg_direction(SpecGeom g, PrecQ Q, const CgDev* __restrict__ cg, cplx* __restrict__ pv,
-                                                      const cplx* __restrict__ r) {
-  if (cg->converged | cg->breakdown) return;
-  const double beta = cg->beta;
+// x += alpha p (owed since k_fin_alpha), then p = M r + beta p unless PCG has converged.  All
+// loads of a point are issued before any arithmetic (5 vector transfers per iteration).
+template <bool DO_X, bool DO_P>
+DBF_DEV void cg_direction_body(const SpecGeom& g, const PrecQ& Q, double alpha, double beta, cplx* __restrict__ x,
+                               cplx* __restrict__ pv, const cplx* __restrict__ r) {
   for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < g.Hs; i += (long long)gridDim.x * BLK) {
-    Pt p = point(g, i);
-    cplx rv[3] = {__ldg(r + i), __ldg(r + g.Hs + i), __ldg(r + 2 * g.Hs + i)};
-    cplx zv[3];
-    apply_M(Q, p, rv, zv);
+    cplx rv[3], pj[3], xj[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const long long j = c * g.Hs + i;
-      cplx pj = pv[j];
-      pv[j] = make_double2(fma(beta, pj.x, zv[c].x), fma(beta, pj.y, zv[c].y));
+      pj[c] = pv[j];
+      if (DO_P) rv[c] = __ldg(r + j);
+      if (DO_X) xj[c] = x[j];
+    }
+    if (DO_X) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        xj[c].x = fma(alpha, pj[c].x, xj[c].x);
+        xj[c].y = fma(alpha, pj[c].y, xj[c].y);
+        x[c * g.Hs + i] = xj[c];
+      }
+    }
+    if (DO_P) {
+      const Pt p = point(g, i);
+      cplx zv[3];
+      apply_M(Q, p, rv, zv);
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        pv[c * g.Hs + i] = make_double2(fma(beta, pj[c].x, zv[c].x), fma(beta, pj[c].y, zv[c].y));
     }
   }
+}
+
+__global__ void __launch_bounds__(BLK) k_cg_direction(SpecGeom g, PrecQ Q, const CgDev* __restrict__ cg, cplx* __restrict__ x,
+                                                      cplx* __restrict__ pv, const cplx* __restrict__ r) {
+  if (cg->breakdown) return;
+  const bool do_x = cg->xphase != 0, do_p = cg->converged == 0;
+  if (do_x && do_p) cg_direction_body<true, true>(g, Q, cg->alpha, cg->beta, x, pv, r);
+  else if (do_p) cg_direction_body<false, true>(g, Q, cg->alpha, cg->beta, x, pv, r);
+  else if (do_x) cg_direction_body<true, false>(g, Q, cg->alpha, cg->beta, x, pv, r);
+}
+
+__global__ void k_fin_x(CgDev* cg) {
+  if (threadIdx.x == 0) cg->xphase = 0;
 }
 
 // r = b - Ax ; partial <r, r>
@@ -166,11 +192,11 @@ __global__ void __launch_bounds__(BLK) k_axpy(SpecGeom g, cplx* __restrict__ y, 
 }
 
 // ---- single-CTA finalizers ---------------------------------------------------------------------
-// sum partials[j*nred + k] over j for k < nred into out[k] (slot 9 of nred = 10 is a max)
-DBF_DEV void cta_reduce(const double* partials, int nblk, int nred, double* out) {
+// sum partials[j*nred + k] over j for k < nred into out[k] (slot max_slot, if >= 0, is a max)
+DBF_DEV void cta_reduce(const double* partials, int nblk, int nred, double* out, int max_slot) {
   __shared__ double red[BLK];
   for (int k = 0; k < nred; ++k) {
-    const bool is_max = (nred == 10 && k == 9);
+    const bool is_max = (k == max_slot);
     double s = 0.0;
     for (int j = threadIdx.x; j < nblk; j += BLK) {
       double v = partials[(long long)j * nred + k];
@@ -231,7 +257,9 @@ __global__ void k_fin_alpha(CgDev* cg, const double* loc) {
   if (cg->converged | cg->breakdown) return;
   for (int a = 0; a < 9; ++a) cg->dc[a] = loc[1 + a] * cg->inv_n;
   if (cg->sym) sym9(cg->dc);
-  double pq = loc[0];
+  // <p, A p> = <p_u, q_u> + p_e . q_e; <p_u, q_u> = (1/N) sum_x grad p_u : sigma(p) from the X pass
+  // (loc[10], Parseval), so F3 does not re-read p
+  double pq = loc[10] * cg->inv_n;
   for (int a = 0; a < 9; ++a) {
     cg->qe[a] = cg->mask[a] * cg->dc[a];
     pq += cg->pe[a] * cg->qe[a];
@@ -243,6 +271,7 @@ __global__ void k_fin_alpha(CgDev* cg, const double* loc) {
   }
   const double alpha = cg->rz / pq;
   cg->alpha = alpha;
+  cg->xphase = 1;
   for (int a = 0; a < 9; ++a) {
     cg->xe[a] += alpha * cg->pe[a];
     cg->re[a] -= alpha * cg->qe[a];
@@ -312,9 +341,9 @@ __global__ void k_allreduce_lb(double* const* v, int P, int k, int is_max) {
   }
 }
 
-__global__ void __launch_bounds__(BLK) k_reduce(const double* partials, int nblk, int nred, double* out) {
+__global__ void __launch_bounds__(BLK) k_reduce(const double* partials, int nblk, int nred, double* out, int max_slot) {
   __shared__ double s[64];
-  cta_reduce(partials, nblk, nred, s);
+  cta_reduce(partials, nblk, nred, s, max_slot);
   if (threadIdx.x < nred) out[threadIdx.x] = s[threadIdx.x];
 }
 
@@ -355,13 +384,17 @@ cudaError_t launch_cg_init(const SpecGeom& g, const PrecQ& q, const cplx* r, cpl
   k_cg_init<<<nblk, BLK, 0, s>>>(g, q, r, p, partials);
   return cudaGetLastError();
 }
-cudaError_t launch_cg_update(const SpecGeom& g, const PrecQ& q, CgDev* cg, cplx* x, const cplx* p, cplx* r, const cplx* qv,
+cudaError_t launch_cg_update(const SpecGeom& g, const PrecQ& q, CgDev* cg, cplx* r, const cplx* qv,
                              double* partials, int nblk, cudaStream_t s) {
-  k_cg_update<<<nblk, BLK, 0, s>>>(g, q, cg, x, p, r, qv, partials);
+  k_cg_update<<<nblk, BLK, 0, s>>>(g, q, cg, r, qv, partials);
   return cudaGetLastError();
 }
-cudaError_t launch_cg_direction(const SpecGeom& g, const PrecQ& q, const CgDev* cg, cplx* p, const cplx* r, cudaStream_t s) {
-  k_cg_direction<<<NBLK, BLK, 0, s>>>(g, q, cg, p, r);
+cudaError_t launch_cg_direction(const SpecGeom& g, const PrecQ& q, const CgDev* cg, cplx* x, cplx* p, const cplx* r, cudaStream_t s) {
+  k_cg_direction<<<NBLK, BLK, 0, s>>>(g, q, cg, x, p, r);
+  return cudaGetLastError();
+}
+cudaError_t launch_fin_x(CgDev* cg, cudaStream_t s) {
+  k_fin_x<<<1, 32, 0, s>>>(cg);
   return cudaGetLastError();
 }
 cudaError_t launch_fin_init(CgDev* cg, const double* loc, cudaStream_t s) {
@@ -392,8 +425,8 @@ cudaError_t launch_axpy(const SpecGeom& g, cplx* y, const cplx* x, double a, cud
   k_axpy<<<NBLK, BLK, 0, s>>>(g, y, x, a);
   return cudaGetLastError();
 }
-cudaError_t launch_reduce(const double* partials, int nblk, int nred, double* out, cudaStream_t s) {
-  k_reduce<<<1, BLK, 0, s>>>(partials, nblk, nred, out);
+cudaError_t launch_reduce(const double* partials, int nblk, int nred, double* out, cudaStream_t s, int max_slot) {
+  k_reduce<<<1, BLK, 0, s>>>(partials, nblk, nred, out, max_slot);
   return cudaGetLastError();
 }
 cudaError_t launch_phase_hist(const uint16_t* ph, long long nvox, double* counts, int nphase, int* bad, cudaStream_t s) {

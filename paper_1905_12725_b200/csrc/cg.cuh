@@ -16,7 +16,9 @@ struct CgDev {
   double dc[9];        // <sigma(p)> of the latest operator application
   double mask[9];      // 1 = stress controlled
   double Minv_e[81];   // (P Cbar P)^-1 on the stress-controlled subspace (R4), 9x9 row-major
-  int converged, breakdown, iters, sym, macro, max_iter, pad0, pad1;
+  int converged, breakdown, iters, sym, macro, max_iter;
+  int xphase;  // 1 between k_fin_alpha and k_fin_x: the direction kernel still owes x += alpha p
+  int pad0;
 };
 
 // spectral-point preconditioner coefficients: A_m(xi) = sum_p Q[m][p] q_p(xi),
@@ -32,9 +34,10 @@ struct SpecGeom {
 
 cudaError_t launch_precond(const SpecGeom& g, const PrecQ& q, const cplx* r, cplx* z, cudaStream_t s);
 cudaError_t launch_cg_init(const SpecGeom& g, const PrecQ& q, const cplx* r, cplx* p, double* partials, int nblk, cudaStream_t s);
-cudaError_t launch_cg_update(const SpecGeom& g, const PrecQ& q, CgDev* cg, cplx* x, const cplx* p, cplx* r, const cplx* qv,
+cudaError_t launch_cg_update(const SpecGeom& g, const PrecQ& q, CgDev* cg, cplx* r, const cplx* qv,
                              double* partials, int nblk, cudaStream_t s);
-cudaError_t launch_cg_direction(const SpecGeom& g, const PrecQ& q, const CgDev* cg, cplx* p, const cplx* r, cudaStream_t s);
+cudaError_t launch_cg_direction(const SpecGeom& g, const PrecQ& q, const CgDev* cg, cplx* x, cplx* p, const cplx* r, cudaStream_t s);
+cudaError_t launch_fin_x(CgDev* cg, cudaStream_t s);
 cudaError_t launch_fin_init(CgDev* cg, const double* loc, cudaStream_t s);
 cudaError_t launch_fin_alpha(CgDev* cg, const double* loc, cudaStream_t s);
 cudaError_t launch_fin_beta(CgDev* cg, const double* loc, cudaStream_t s);
@@ -42,7 +45,8 @@ cudaError_t launch_true_residual(const SpecGeom& g, const cplx* b, const cplx* A
 cudaError_t launch_fin_true(CgDev* cg, const double* loc, cudaStream_t s);
 cudaError_t launch_allreduce_lb(double* const* v, int P, int k, int is_max, cudaStream_t s);
 cudaError_t launch_axpy(const SpecGeom& g, cplx* y, const cplx* x, double a, cudaStream_t s);
-cudaError_t launch_reduce(const double* partials, int nblk, int nred, double* out, cudaStream_t s);
+// out[k] = sum_j partials[j nred + k] (max over j for k == max_slot)
+cudaError_t launch_reduce(const double* partials, int nblk, int nred, double* out, cudaStream_t s, int max_slot = -1);
 cudaError_t launch_phase_hist(const uint16_t* ph, long long nvox, double* counts, int nphase, int* bad, cudaStream_t s);
 cudaError_t launch_fill(double* p, long long n, double v, cudaStream_t s);
 int cg_blocks();

@@ -390,9 +390,9 @@ dbfft_status allreduce(dbfft_ctx ctx, int off, int k, bool is_max) {
 }
 
 // reduce CTA partials into slab.loc[off ..] (k values)
-dbfft_status reduce_to(dbfft_ctx ctx, Slab& s, const double* partials, int nblk, int nred, int off) {
+dbfft_status reduce_to(dbfft_ctx ctx, Slab& s, const double* partials, int nblk, int nred, int off, int max_slot = -1) {
   ProfScope ps(ctx, PK_FIN);
-  CK(launch_reduce(partials, nblk, nred, s.loc + off, ctx->stream));
+  CK(launch_reduce(partials, nblk, nred, s.loc + off, ctx->stream, max_slot));
   return DBFFT_OK;
 }
 
@@ -752,7 +752,7 @@ dbfft_status refresh_mean_tangent(dbfft_ctx ctx) {
 dbfft_status reduce_x(dbfft_ctx ctx, const std::vector<int>& grids, double* host10, bool with_max) {
   for (size_t k = 0; k < ctx->slabs.size(); ++k) {
     Slab& s = ctx->slabs[k];
-    CKS(reduce_to(ctx, s, s.part_x, grids[k], 10, 1));
+    CKS(reduce_to(ctx, s, s.part_x, grids[k], 10, 1, 9));  // constitutive kinds: slot 9 = max |d|
   }
   CKS(allreduce(ctx, 1, 9, false));
   if (with_max) CKS(allreduce(ctx, 10, 1, true));
@@ -882,13 +882,14 @@ dbfft_status pcg_body(dbfft_ctx ctx, int every, bool macro, int nb) {
   {
     for (int k = 0; k < every; ++k) {
       ApplyOut ao;
-      CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, macro, &CgDev::pe, true, &ao));
+      // <p, A p> comes from the X pass (slot 9: sum (grad p + p_e) : sigma, Parseval), so F3 does
+      // not re-read p
+      CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, macro, &CgDev::pe, false, &ao));
       for (size_t j = 0; j < ctx->slabs.size(); ++j) {
         Slab& s = ctx->slabs[j];
-        CKS(reduce_to(ctx, s, s.part_f3, ao.grid_f3[j], 1, 0));
         CKS(reduce_to(ctx, s, s.part_x, ao.grid_x[j], 10, 1));
       }
-      CKS(allreduce(ctx, 0, 10, false));
+      CKS(allreduce(ctx, 1, 10, false));
       for (Slab& s : ctx->slabs) {
         {
           ProfScope ps(ctx, PK_FIN);
@@ -896,7 +897,7 @@ dbfft_status pcg_body(dbfft_ctx ctx, int every, bool macro, int nb) {
         }
         {
           ProfScope ps(ctx, PK_CGUPD);
-          CK(launch_cg_update(spec(ctx, s), ctx->prec, s.cg, s.x, s.p, s.r, s.q, s.part_cg, nb, ctx->stream));
+          CK(launch_cg_update(spec(ctx, s), ctx->prec, s.cg, s.r, s.q, s.part_cg, nb, ctx->stream));
         }
         CKS(reduce_to(ctx, s, s.part_cg, nb, 2, 0));
       }
@@ -908,7 +909,11 @@ dbfft_status pcg_body(dbfft_ctx ctx, int every, bool macro, int nb) {
         }
         {
           ProfScope ps(ctx, PK_CGDIR);
-          CK(launch_cg_direction(spec(ctx, s), ctx->prec, s.cg, s.p, s.r, ctx->stream));
+          CK(launch_cg_direction(spec(ctx, s), ctx->prec, s.cg, s.x, s.p, s.r, ctx->stream));
+        }
+        {
+          ProfScope ps(ctx, PK_FIN);
+          CK(launch_fin_x(s.cg, ctx->stream));
         }
       }
     }

@@ -536,8 +536,12 @@ DBF_DEV void j2_moduli(const double* prm, double* kappa, double* mu) {
 
 // Per-voxel material data of the apply kinds come either from global memory (tp = tan + v,
 // ts = nvox) or from the CTA's shared-memory stage filled by bulk async copies (ts = N1).
+// xd: the apply kinds accumulate grad p : sigma of the voxel, so <p_u, K p_u> = sum / N (Parseval:
+// the operator's Hermitian form in real space, sigma including the macro part; FIN_NH accumulates
+// the 1/(2N)-scaled P)
 template <int KIND>
-DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* red, const double* tp, long long ts, int ph) {
+DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* red, const double* tp, long long ts, int ph,
+                     double& xd) {
   if (KIND == X_K_SMALL_PHASE || KIND == X_RHS_SMALL_PHASE || KIND == X_K_J2) {
     double e6[6];
 #pragma unroll
@@ -554,6 +558,8 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
     } else {
       voigt_contract_full(g.ptable + 36 * ph, e6, s);
     }
+    if (KIND != X_RHS_SMALL_PHASE)
+      xd += G[0] * s[0] + G[1] * s[1] + G[2] * s[2] + 2.0 * (G[3] * s[3] + G[4] * s[4] + G[5] * s[5]);
     const double sg = (KIND == X_RHS_SMALL_PHASE) ? -g.oscale : g.oscale;
 #pragma unroll
     for (int I = 0; I < 6; ++I) {
@@ -573,6 +579,7 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
       for (int b = 0; b < 9; ++b) acc = fma(K[sym9(a, b)], e9[b], acc);
       P[a] = acc * g.oscale;
       red[a] += acc;
+      xd += G[a] * acc;
     }
   } else if (KIND == X_K_FIN_NH) {
     double Fi[9], e9[9];
@@ -583,6 +590,8 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
 #pragma unroll
     for (int a = 0; a < 9; ++a) e9[a] = G[a] + (g.e ? __ldg(g.e + a) : 0.0);
     nh_apply(Fi, c1 * g.oscale, mu * g.oscale, lam * g.oscale, e9, P);  // P x 1/(2N): exact (powers of 2)
+#pragma unroll
+    for (int a = 0; a < 9; ++a) xd += G[a] * P[a];
   } else if (KIND == X_CONST_FIN) {
     double F[9], Pv[9], Fi[9], c1;
     double mx = 0.0;
@@ -844,6 +853,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
   if (DCRED)
     for (int i = t; i < 10 * LPAR; i += CF::THREADS) s_dc[i / 10][i % 10] = 0.0;
   if (DCRED) __syncthreads();
+  double xdot = 0.0;  // apply kinds: sum (G + e) : sigma over the CTA's voxels
   double red[T::NRED > 0 ? T::NRED : 1];
 #pragma unroll
   for (int r = 0; r < (T::NRED > 0 ? T::NRED : 1); ++r) red[r] = 0.0;
@@ -950,7 +960,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
         ts = g.nvox;
         ph = (KIND == X_K_FIN_TAN || KIND == X_REAL_OUT) ? 0 : (int)__ldg(g.phase + v);
       }
-      x_voxel<KIND>(g, v, G, P, red, tp, ts, ph);
+      x_voxel<KIND>(g, v, G, P, red, tp, ts, ph, xdot);
 #pragma unroll
       for (int f = 0; f < T::COUT; ++f) real[(l2 * CS + f) * N1 + x] = P[f];
     }
@@ -1009,28 +1019,40 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
     }
   }
 
-  if (DCRED) {
+  // block reductions in a fixed order (deterministic); warp shuffles only for full warps
+  // (odd line lengths give a partial last warp)
+  constexpr int nw = (CF::THREADS + 31) / 32;
+  constexpr bool FULLW = (CF::THREADS % 32) == 0;
+  __shared__ double sred[FULLW ? nw : CF::THREADS];
+  auto block_red = [&](double v, bool is_max) -> double {  // result valid in thread 0
     __syncthreads();
+    if (FULLW) {
+      v = is_max ? warp_max(v) : warp_sum(v);
+      if ((t & 31) == 0) sred[t >> 5] = v;
+    } else {
+      sred[t] = v;
+    }
+    __syncthreads();
+    double s = 0.0;
+    if (t == 0)
+      for (int w = 0; w < (FULLW ? nw : CF::THREADS); ++w) s = is_max ? fmax(s, sred[w]) : s + sred[w];
+    return s;
+  };
+  if (DCRED) {
+    const double xs = block_red(xdot, false);
     if (t < T::NRED) {
       double s = 0.0;
       for (int q = 0; q < (DCRED ? LPAR : 1); ++q) s += s_dc[q][t];
       g.partials[(long long)blockIdx.x * g.nred + t] = s;
     }
+    // slot 9: sum grad p : sigma (unscaled; FIN_NH summed the exactly 1/(2N)-scaled P)
+    if (t == 0) g.partials[(long long)blockIdx.x * g.nred + 9] = (KIND == X_K_FIN_NH) ? xs / g.oscale : xs;
   } else if (T::NRED > 0) {
-    // block reduction -> partials[block][nred] (sums; slot 9 of the const kinds is a max)
-    __shared__ double sred[(CF::THREADS + 31) / 32][10];
-    constexpr int nw = (CF::THREADS + 31) / 32;
+    // partials[block][nred] (sums; slot 9 of the const kinds is a max)
 #pragma unroll
     for (int r = 0; r < T::NRED; ++r) {
-      const bool is_max = (r == 9);
-      double v = is_max ? warp_max(red[r]) : warp_sum(red[r]);
-      if ((t & 31) == 0) sred[t >> 5][r] = v;
-    }
-    __syncthreads();
-    if (t < T::NRED) {
-      double s = 0.0;
-      for (int w = 0; w < nw; ++w) s = (t == 9) ? fmax(s, sred[w][t]) : s + sred[w][t];
-      g.partials[(long long)blockIdx.x * g.nred + t] = s;
+      const double s = block_red(red[r], r == 9);
+      if (t == 0) g.partials[(long long)blockIdx.x * g.nred + r] = s;
     }
   }
 }

@@ -1,2 +1,2 @@
-timeout 300 python tools/kbench.py 512 5 small
-timeout 1800 python tools/run_configs.py c5 --noprof > gpurun_out/c5.jsonl 2> gpurun_out/c5.err; tail -2 gpurun_out/c5.err; cat gpurun_out/c5.jsonl
+timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_s7.json 2> gpurun_out/bench_s7.err; tail -1 gpurun_out/bench_s7.err
+timeout 1800 python -m pytest tests -m gpu -x -q 2>&1 | grep -E "^E |passed|failed" | head -8
