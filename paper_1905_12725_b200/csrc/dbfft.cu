@@ -790,10 +790,11 @@ dbfft_status pcg(dbfft_ctx ctx, const dbfft_opts& o, int* iters_out) {
   CKS(init_dir());
   const int every = std::max(1, o.check_every);
   int restarts = 0;
-  // graphs: single GPU or NCCL ranks (the loopback all-reduce synchronises on the host), and not
-  // while the per-kernel profiler records events; DBFFT_GRAPHS=0 disables
+  // graphs: single GPU only (the loopback all-reduce synchronises on the host, and NCCL capture
+  // is not exercised on the one-GPU test boxes), and not while the per-kernel profiler records
+  // events; DBFFT_GRAPHS=0 disables
   const char* genv = getenv("DBFFT_GRAPHS");
-  const bool use_graph = !ctx->prof && !(ctx->P > 1 && ctx->loopback) && !(genv && genv[0] == '0');
+  const bool use_graph = !ctx->prof && ctx->P == 1 && !(genv && genv[0] == '0');
   cudaGraphExec_t graph_exec = nullptr;
   long long graph_launches = 0;
   int rounds = 0;
