@@ -110,7 +110,7 @@ def test_apply_K_tma_small(dbf, n):
     assert rel(gpu_full(dbf, f, n[0]), ref) <= 1e-12
 
 
-@pytest.mark.parametrize("n", TMA_GRIDS[:3] + TMA_GRIDS[4:])
+@pytest.mark.parametrize("n", TMA_GRIDS[:3] + TMA_GRIDS[4:] + [(256, 16, 8), (256, 8, 32)])
 def test_apply_K_tma_finite(dbf, n):
     ph = two_phase(n, 33)
     mats = [dict(kind="neohooke", mu=1.0, kappa=2.5), dict(kind="neohooke", mu=10.0, kappa=25.0)]
