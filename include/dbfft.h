@@ -210,6 +210,13 @@ dbfft_status dbfft_residuals(dbfft_ctx ctx, const double target[9], const uint8_
  * max|curl F| (row-wise curl) for a finite-strain one.  Same derivatives as dbfft_residuals. */
 dbfft_status dbfft_incompatibility(dbfft_ctx ctx, const double* field, int32_t on_device, double* out);
 
+/* Residual history of the last dbfft_solve_increment (the paper's Fig. div): pairs
+ * (eps_equilibrium, eps_loading) of Eq. chedckeq / chedckimp as the PCG tracks them (R7) — at the
+ * start and after every iteration of every PCG solve (one per Newton iteration), concatenated in
+ * order; a true-residual restart continues the same sequence.  *n = number of pairs recorded (at
+ * most 65536); min(cap, *n) pairs are copied to out[2 cap] (host).  (sync) */
+dbfft_status dbfft_get_trace(dbfft_ctx ctx, double* out, int32_t cap, int32_t* n);
+
 /* Per-kernel device-time accounting: while enabled, CUDA events are recorded on the ctx stream
  * around every kernel launch and accumulated per kernel id (names via dbfft_profile_name). */
 dbfft_status dbfft_profile_enable(dbfft_ctx ctx, int32_t enable);

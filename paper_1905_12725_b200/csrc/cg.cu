@@ -248,6 +248,10 @@ __global__ void k_fin_init(CgDev* cg, const double* loc) {
   cg->eps_eq = sqrt(loc[1]) / den;
   cg->eps_load = cg->macro ? sqrt(ree) / den : 0.0;
   cg->converged = (cg->eps_eq <= cg->tol_eq && cg->eps_load <= cg->tol_load) ? 1 : 0;
+  if (cg->trace && cg->iters == 0 && cg->trace_cap > 0) {  // restarts keep the history
+    cg->trace[0] = cg->eps_eq;
+    cg->trace[1] = cg->eps_load;
+  }
   if (!(cg->rz == cg->rz)) cg->breakdown = 1;
 }
 
@@ -299,6 +303,10 @@ __global__ void k_fin_beta(CgDev* cg, const double* loc) {
   const double den = fmax(norm9(cg->msig), 1e-300);
   cg->eps_eq = sqrt(loc[1]) / den;
   cg->eps_load = cg->macro ? sqrt(ree) / den : 0.0;
+  if (cg->trace && cg->iters < cg->trace_cap) {
+    cg->trace[2 * cg->iters] = cg->eps_eq;
+    cg->trace[2 * cg->iters + 1] = cg->eps_load;
+  }
   if (!(rz_new == rz_new)) {
     cg->breakdown = 1;
     return;

@@ -18,7 +18,8 @@ struct CgDev {
   double Minv_e[81];   // (P Cbar P)^-1 on the stress-controlled subspace (R4), 9x9 row-major
   int converged, breakdown, iters, sym, macro, max_iter;
   int xphase;  // 1 between k_fin_alpha and k_fin_x: the direction kernel still owes x += alpha p
-  int pad0;
+  int trace_cap;   // entries available at trace (0: no trace)
+  double* trace;   // per-iteration (eps_eq, eps_load) of this PCG call: [0] initial, [k] after k
 };
 
 // spectral-point preconditioner coefficients: A_m(xi) = sum_p Q[m][p] q_p(xi),

@@ -150,6 +150,9 @@ struct dbfft_ctx_s {
   int prec_medium = 0;           // medium the linear prec was built with (0 arithmetic, 1 harmonic, 2 Hill)
   double Cbar_init[81];          // mean tangent at the undeformed state (set_phases), policy 2
   long long n_incr = 0;          // committed increments since set_phases (policy 3)
+  // residual trace of the last solve_increment (P:304 Fig. div): (eps_eq, eps_load) per iteration
+  double* trace_dev = nullptr;
+  int trace_cap = 0, trace_n = 0;
   CgDev* h_cg = nullptr;     // pinned mirror (slab 0)
   double* h_red = nullptr;   // pinned [64]
   int* h_bad = nullptr;
@@ -943,8 +946,12 @@ dbfft_status cg_setup(dbfft_ctx ctx, const dbfft_opts& o, const uint8_t* mask, c
     ctx->err = "singular macro block (P Cbar P)";
     return DBFFT_E_INVALID_ARG;
   }
-  for (Slab& s : ctx->slabs) CK(cudaMemcpyAsync(s.cg, h, sizeof(CgDev), cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
+  for (size_t k = 0; k < ctx->slabs.size(); ++k) {
+    h->trace = (k == 0 && ctx->trace_dev) ? ctx->trace_dev + 2 * (size_t)ctx->trace_n : nullptr;
+    h->trace_cap = h->trace ? ctx->trace_cap - ctx->trace_n : 0;
+    CK(cudaMemcpyAsync(ctx->slabs[k].cg, h, sizeof(CgDev), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));  // h is reused for the next slab
+  }
   return DBFFT_OK;
 }
 
@@ -1055,6 +1062,7 @@ dbfft_status solve_linear(dbfft_ctx ctx, const double* target, const uint8_t* ma
   CKS(cg_setup(ctx, o, mask, msig0, be));
   int iters = 0;
   dbfft_status st = pcg(ctx, o, &iters);
+  ctx->trace_n = std::min(ctx->trace_cap, ctx->trace_n + iters + 1);
   if (rep) {
     rep->cg_iters = iters;
     rep->newton_iters = 0;
@@ -1166,6 +1174,7 @@ dbfft_status solve_newton(dbfft_ctx ctx, const double* target, const uint8_t* ma
     if (st != DBFFT_OK) break;
     int iters = 0;
     st = pcg(ctx, o, &iters);
+    ctx->trace_n = std::min(ctx->trace_cap, ctx->trace_n + iters + 1);
     total_cg += iters;
     if (st != DBFFT_OK) break;
     for (Slab& s : ctx->slabs) {  // u += du
@@ -1229,7 +1238,7 @@ void free_slab(Slab& s) {
 
 void free_all(dbfft_ctx ctx) {
   for (Slab& s : ctx->slabs) free_slab(s);
-  void* ptrs[] = {ctx->xix, ctx->xiy, ctx->xiz, ctx->tw1, ctx->tw2, ctx->tw3, ctx->loc_ptrs};
+  void* ptrs[] = {ctx->xix, ctx->xiy, ctx->xiz, ctx->tw1, ctx->tw2, ctx->tw3, ctx->loc_ptrs, ctx->trace_dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->h_cg) cudaFreeHost(ctx->h_cg);
@@ -1763,6 +1772,11 @@ dbfft_status dbfft_solve_increment(dbfft_ctx ctx, const double target[9], const 
   CKS(check_target(ctx, target, mask));
   dbfft_opts o = opts ? *opts : dbfft_default_opts();
   CKS(check_opts(ctx, o));
+  if (!ctx->trace_dev) {
+    ctx->trace_cap = 1 << 16;
+    CKS(dalloc(ctx, &ctx->trace_dev, 2 * (size_t)ctx->trace_cap));
+  }
+  ctx->trace_n = 0;
   auto t0 = std::chrono::steady_clock::now();
   if (report) {
     memset(report, 0, sizeof(*report));
@@ -2037,3 +2051,10 @@ dbfft_status dbfft_incompatibility(dbfft_ctx ctx, const double* field, int32_t o
   return incompat_max(ctx, out);
 }
 
+dbfft_status dbfft_get_trace(dbfft_ctx ctx, double* out, int32_t cap, int32_t* n) {
+  if (!ctx || !n || (cap > 0 && !out)) return DBFFT_E_INVALID_ARG;
+  *n = ctx->trace_n;
+  const int m = std::min(cap, ctx->trace_n);
+  if (m > 0) CK(cudaMemcpy(out, ctx->trace_dev, sizeof(double) * 2 * (size_t)m, cudaMemcpyDeviceToHost));
+  return DBFFT_OK;
+}

@@ -45,7 +45,7 @@ EXPORTS = ["dbfft_create", "dbfft_destroy", "dbfft_last_error", "dbfft_spectral_
            "dbfft_apply_K", "dbfft_apply_K_aug", "dbfft_precond", "dbfft_eval_state", "dbfft_default_opts",
            "dbfft_solve_increment", "dbfft_get_field", "dbfft_profile_enable", "dbfft_profile_read",
            "dbfft_profile_name", "dbfft_profile_count", "dbfft_launch_count", "dbfft_nccl_unique_id",
-           "dbfft_residuals", "dbfft_incompatibility"]
+           "dbfft_residuals", "dbfft_incompatibility", "dbfft_get_trace"]
 
 _lib = None
 
@@ -91,6 +91,7 @@ def load_library(path=None):
     lib.dbfft_nccl_unique_id.argtypes = [P]
     lib.dbfft_residuals.argtypes = [P, ctypes.POINTER(D), ctypes.POINTER(ctypes.c_uint8), ctypes.POINTER(D)]
     lib.dbfft_incompatibility.argtypes = [P, P, I32, ctypes.POINTER(D)]
+    lib.dbfft_get_trace.argtypes = [P, ctypes.POINTER(D), I32, ctypes.POINTER(I32)]
     for fn in EXPORTS:
         getattr(lib, fn).restype = getattr(lib, fn).restype if fn in (
             "dbfft_last_error", "dbfft_default_opts", "dbfft_profile_name", "dbfft_profile_count") else ctypes.c_int
@@ -245,7 +246,9 @@ class DBFFT:
             raise DBFFTError(st, self.lib.dbfft_last_error(self.h).decode())
         return out
 
-    def get_field(self, which, on_device=False):
+    def get_field(self, which, on_device=False, pinned=False):
+        """Committed field (C ABI dbfft_get_field).  Host results land in a fresh numpy array;
+        pinned=True allocates it in page-locked memory (faster D2H copy)."""
         n1, n2, n3 = self.n
         N = n1 * n2 * n3
         if which == FIELD_U_HAT:
@@ -257,7 +260,10 @@ class DBFFT:
             out = self.torch.empty((ncomp, n3, n2, n1), dtype=self.torch.float64, device=self.device)
             self._check(self.lib.dbfft_get_field(self.h, which, _dptr(out), 1))
             return out
-        out = np.empty((ncomp, n3, n2, n1))
+        if pinned:
+            out = self.torch.empty((ncomp, n3, n2, n1), dtype=self.torch.float64, pin_memory=True).numpy()
+        else:
+            out = np.empty((ncomp, n3, n2, n1))
         self._check(self.lib.dbfft_get_field(self.h, which, out.ctypes.data_as(ctypes.c_void_p), 0))
         if ncomp == 9:
             out = out.reshape(3, 3, n3, n2, n1)
@@ -271,6 +277,15 @@ class DBFFT:
         out = (ctypes.c_double * 3)()
         self._check(self.lib.dbfft_residuals(self.h, t, m, out))
         return dict(equilibrium=out[0], compatibility=out[1], loading=out[2])
+
+    def trace(self):
+        """(eps_eq, eps_load) per PCG iteration of the last solve_increment, shape (n, 2)."""
+        n = ctypes.c_int32()
+        self._check(self.lib.dbfft_get_trace(self.h, None, 0, ctypes.byref(n)))
+        out = np.zeros((max(n.value, 1), 2))
+        self._check(self.lib.dbfft_get_trace(self.h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), n.value,
+                                             ctypes.byref(n)))
+        return out[:n.value]
 
     def incompatibility(self, field):
         """max|curl curl eps| (small) or max|curl F| (finite) of a real [3,3,z,y,x] field."""

@@ -504,3 +504,31 @@ def test_solve_odd_p33_twin(dbf):
         assert rep["converged"] and rep["newton_iters"] == ref["newton_iters"]
         assert rel(rep["macro_stress"], ref["mean_P"]) <= 1e-9
         assert rel(ctx.get_field(dbf.FIELD_STRAIN), ref["F"]) <= 1e-8
+
+
+def test_residual_trace_vs_oracle(dbf):
+    """Per-iteration equilibrium residual (the paper's Fig. div): the GPU's PCG history
+    follows the oracle's iteration by iteration (same algorithm, round-off apart)."""
+    for name in ("c1", "c2"):
+        cfg = configs.c1() if name == "c1" else configs.c2(n=32, radius_vox=3)
+        L = cfg["loads"][0]
+        ref = O.solve_small_strain(cfg["phase"], cfg["materials"], L, tol=1e-10)
+        ctx = dbf.DBFFT(cfg["n"], kinematics="small")
+        ctx.set_phases(cfg["phase"], cfg["materials"])
+        rep = ctx.solve_increment(L["target"], L["mask"])
+        tr = ctx.trace()
+        hist = np.asarray(ref["hist"])
+        assert tr.shape[0] == rep["cg_iters"] + 1
+        m = min(len(hist), tr.shape[0], 40)
+        # early iterations agree tightly; PCG round-off grows with the iteration count
+        assert np.allclose(tr[:m, 0], hist[:m], rtol=1e-6, atol=1e-12 * hist[0])  # atol: round-off floor
+        assert tr[-1, 0] <= 1e-10
+    # Newton: one PCG history per Newton iteration, concatenated
+    cfg = configs.c4(n=16, radius_vox=2)
+    ctx = dbf.DBFFT(cfg["n"], kinematics="finite")
+    ctx.set_phases(cfg["phase"], cfg["materials"])
+    L = cfg["loads"][0]
+    rep = ctx.solve_increment(L["target"], L["mask"])
+    tr = ctx.trace()
+    assert tr.shape[0] == rep["cg_iters"] + rep["newton_iters"]
+    assert np.sum(tr[:, 0] <= 1e-10) >= rep["newton_iters"]

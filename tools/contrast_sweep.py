@@ -38,9 +38,11 @@ for control in ("strain", "stress"):
         ev1.record(ctx.stream)
         torch.cuda.synchronize()
         res = ctx.residuals(target, mask)
+        trace = ctx.trace()[:, 0]  # eps_eq per PCG iteration (the paper's Fig. div)
         print(json.dumps(dict(section="3.1" if control == "strain" else "3.2", control=control, contrast=k,
                               grid=list(cfg["n"]), status=rep["status"], cg_iters=rep["cg_iters"],
                               solve_ms=ev0.elapsed_time(ev1), residuals=res,
                               macro_strain_xx=float(rep["macro_strain"][0, 0]),
-                              macro_stress_xx=float(rep["macro_stress"][0, 0]))), flush=True)
+                              macro_stress_xx=float(rep["macro_stress"][0, 0]),
+                              eps_eq_trace_every_10=[float(v) for v in trace[::10]])), flush=True)
         ctx.close()
