@@ -486,3 +486,31 @@ DBF_DEV void fft_odd(cplx (&a)[OddPlan<N>::P], cplx* sbuf, int g, const IDX& idx
     Ns *= R;
   }
 }
+
+// ---------------------------------------------------------------------------------------------
+// Preconditioner at one frequency (Eqs. pred2/pred3): z = A^-1 r, A = xi . Cbar . xi,
+// A_m = sum_k Q36[6m + k] q_k(xi) with q = (xx xx, yy yy, zz zz, yy zz, xx zz, xx yy) products;
+// inverse by cofactors.  Callers handle the null set (xi = 0: z = 0).
+// ---------------------------------------------------------------------------------------------
+DBF_DEV void prec_apply(const double* Q36, double xx, double xy, double xz, const cplx* r, cplx* z) {
+  const double q[6] = {xx * xx, xy * xy, xz * xz, xy * xz, xx * xz, xx * xy};
+  double A[6];
+#pragma unroll
+  for (int m = 0; m < 6; ++m) {
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) a = fma(Q36[6 * m + k], q[k], a);
+    A[m] = a;
+  }
+  // A = [[A0, A5, A4], [A5, A1, A3], [A4, A3, A2]]
+  const double c00 = A[1] * A[2] - A[3] * A[3];
+  const double c01 = A[4] * A[3] - A[5] * A[2];
+  const double c02 = A[5] * A[3] - A[1] * A[4];
+  const double c11 = A[0] * A[2] - A[4] * A[4];
+  const double c12 = A[5] * A[4] - A[0] * A[3];
+  const double c22 = A[0] * A[1] - A[5] * A[5];
+  const double id = 1.0 / (A[0] * c00 + A[5] * c01 + A[4] * c02);
+  z[0] = make_double2((c00 * r[0].x + c01 * r[1].x + c02 * r[2].x) * id, (c00 * r[0].y + c01 * r[1].y + c02 * r[2].y) * id);
+  z[1] = make_double2((c01 * r[0].x + c11 * r[1].x + c12 * r[2].x) * id, (c01 * r[0].y + c11 * r[1].y + c12 * r[2].y) * id);
+  z[2] = make_double2((c02 * r[0].x + c12 * r[1].x + c22 * r[2].x) * id, (c02 * r[0].y + c12 * r[1].y + c22 * r[2].y) * id);
+}

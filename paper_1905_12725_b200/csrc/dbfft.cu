@@ -662,7 +662,7 @@ int nf_I1(dbfft_ctx ctx) { return ctx->kin == 9 ? 6 : 5; }
 typedef double Macro9[9];
 
 dbfft_status apply_K_slabs(dbfft_ctx ctx, cplx* Slab::*u, cplx* Slab::*f, bool use_e, Macro9 CgDev::*e_member, bool dot,
-                           ApplyOut* ao) {
+                           ApplyOut* ao, bool front_only = false) {
   const bool fin = ctx->kin == 9;
   int xkind;
   if (ctx->family == FAM_LINEAR) xkind = X_K_SMALL_PHASE;
@@ -684,6 +684,7 @@ dbfft_status apply_K_slabs(dbfft_ctx ctx, cplx* Slab::*u, cplx* Slab::*f, bool u
     CKS(run_x(ctx, xkind, PK_X, gx, &gridx));
     if (ao) ao->grid_x[k] = gridx;
   }
+  if (front_only) return DBFFT_OK;  // the caller runs the forward tail (PCG: F3 fused with r -= alpha q)
   for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, geom_F2(ctx, s, s.WB, s.WA, 6), ctx->n2));
   CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
   for (size_t k = 0; k < ctx->slabs.size(); ++k) {
@@ -882,7 +883,74 @@ dbfft_status pcg(dbfft_ctx ctx, const dbfft_opts& o, int* iters_out) {
   }
 }
 
+// F3 geometry of the fused PCG step: q = K p is never stored; r -= alpha q, <r, M r>, <r, r>
+ColGeom geom_F3_update(dbfft_ctx ctx, Slab& s) {
+  ColGeom g5 = geom_F3(ctx, s, s.WR, s.r, 6);
+  g5.dotp = s.r;
+  g5.partials = s.part_cg;
+  g5.upd = 1;
+  g5.cg_alpha = &s.cg->alpha;
+  g5.cg_stop0 = &s.cg->converged;
+  g5.cg_stop1 = &s.cg->breakdown;
+  memcpy(g5.precq, ctx->prec.Q, sizeof(g5.precq));
+  return g5;
+}
+
+bool pcg_fused(dbfft_ctx ctx) {
+  const char* e = getenv("DBFFT_FUSED_UPDATE");
+  if ((e && e[0] == '0') || ctx->kin != 9) return false;  // F3F only (F3S's program needs a 4-slot ring)
+  for (Slab& s : ctx->slabs)
+    if (!col_upd_supported(ctx->n3, geom_F3_update(ctx, s))) return false;
+  return true;
+}
+
+// one PCG iteration with the residual update fused into F3 (8 - 3 + 1 = 6 vector transfers of
+// CG algebra per iteration instead of 8): I1 I2 X | alpha | F2 F3(r -= alpha q, <r,z>, <r,r>) |
+// beta | direction (x += alpha p, p = z + beta p)
+dbfft_status pcg_iteration_fused(dbfft_ctx ctx, bool macro, int nb) {
+  const bool fin = ctx->kin == 9;
+  ApplyOut ao;
+  CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, macro, &CgDev::pe, false, &ao, true));
+  for (size_t j = 0; j < ctx->slabs.size(); ++j) {
+    Slab& s = ctx->slabs[j];
+    CKS(reduce_to(ctx, s, s.part_x, ao.grid_x[j], 10, 1));
+  }
+  CKS(allreduce(ctx, 1, 10, false));
+  for (Slab& s : ctx->slabs) {
+    ProfScope ps(ctx, PK_FIN);
+    CK(launch_fin_alpha(s.cg, s.loc, ctx->stream));
+  }
+  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, geom_F2(ctx, s, s.WB, s.WA, 6), ctx->n2));
+  CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
+  std::vector<int> g3(ctx->slabs.size(), 0);
+  for (size_t j = 0; j < ctx->slabs.size(); ++j) {
+    Slab& s = ctx->slabs[j];
+    CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_F3, geom_F3_update(ctx, s), ctx->n3, &g3[j]));
+    CKS(reduce_to(ctx, s, s.part_cg, g3[j], 2, 0));
+  }
+  CKS(allreduce(ctx, 0, 2, false));
+  for (Slab& s : ctx->slabs) {
+    {
+      ProfScope ps(ctx, PK_FIN);
+      CK(launch_fin_beta(s.cg, s.loc, ctx->stream));
+    }
+    {
+      ProfScope ps(ctx, PK_CGDIR);
+      CK(launch_cg_direction(spec(ctx, s), ctx->prec, s.cg, s.x, s.p, s.r, ctx->stream));
+    }
+    {
+      ProfScope ps(ctx, PK_FIN);
+      CK(launch_fin_x(s.cg, ctx->stream));
+    }
+  }
+  return DBFFT_OK;
+}
+
 dbfft_status pcg_body(dbfft_ctx ctx, int every, bool macro, int nb) {
+  if (pcg_fused(ctx)) {
+    for (int k = 0; k < every; ++k) CKS(pcg_iteration_fused(ctx, macro, nb));
+    return DBFFT_OK;
+  }
   {
     for (int k = 0; k < every; ++k) {
       ApplyOut ao;

@@ -1229,12 +1229,13 @@ struct TmaMaps {
   CUtensorMap in_m, in_t, out_m, out_t, dot_m, dot_t;
 };
 
-template <int N, int KIND, bool DOT, int R>
+template <int N, int KIND, bool DOT, int R, bool UPD = false>
 __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __grid_constant__ TmaMaps maps, ColGeom g, ColTiles tl) {
   typedef ColOp<KIND> Op;
   typedef TmaCfg<N> CF;
+  if (UPD && (*g.cg_stop0 | *g.cg_stop1)) return;  // PCG stopped: r stays as it is
   constexpr int KC = CF::KC, TPC = CF::TPC;
-  constexpr int S = 2;  // staging buffers (TMA stores in flight)
+  constexpr int S = UPD ? 3 : 2;  // staging buffers (UPD: r_0, r_1 of a tile stay readable until r_2)
   extern __shared__ __align__(1024) unsigned char tsm[];
   // 1024-byte alignment of the ring (128B swizzle atoms)
   // (offset arithmetic on the shared array keeps the shared address space: LDS/STS, not LD/ST)
@@ -1294,6 +1295,8 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
   const int lane = t & 31;
   cplx* xcol = xb + c * N;  // this column's FFT exchange buffer
   double dot = 0.0;
+  double acc_rz = 0.0, acc_rr = 0.0;  // UPD: partial <r, M r>, <r, r>
+  const double alpha = UPD ? *g.cg_alpha : 0.0;
   uint32_t nout = 0;        // output tiles written (staging rotation)
   uint32_t it = 0;
   for (int tile = blockIdx.x; tile < tl.n_tiles; tile += gridDim.x, ++it) {
@@ -1352,8 +1355,23 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
           else acc0[s] = v;
         } else {
           const int o = tail ? tma_toff<N>(at.pos, c) : tma_moff<N>(at.pos, c);
+          if (UPD) {  // r_o -= alpha q_o (the F3 output is q = K p); the tile's r is staged in sd
+            const cplx rr = sd[o];
+            v = make_double2(fma(-alpha, v.x, rr.x), fma(-alpha, v.y, rr.y));
+            if (ti.o == 2 && valid) {  // r_0, r_1 are in the previous two staging buffers
+              const cplx r3[3] = {stg[((nout + S - 2) % S) * (CF::TILE / 16) + o], stg[((nout + S - 1) % S) * (CF::TILE / 16) + o], v};
+              const double xz = __ldg(g.fq.xz + at.pos);
+              cplx z3[3] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
+              if (!(at.xxk == 0.0 && at.xyo == 0.0 && xz == 0.0)) prec_apply(g.precq, at.xxk, at.xyo, xz, r3, z3);
+#pragma unroll
+              for (int q = 0; q < 3; ++q) {
+                acc_rz += wdot * (r3[q].x * z3[q].x + r3[q].y * z3[q].y);
+                acc_rr += wdot * (r3[q].x * r3[q].x + r3[q].y * r3[q].y);
+              }
+            }
+          }
           so[o] = v;
-          if (DOT && sd && valid) {
+          if (DOT && !UPD && sd && valid) {
             const cplx p = sd[o];
             dot += wdot * (p.x * v.x + p.y * v.y);
           }
@@ -1368,7 +1386,7 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
       if (ti.last) {
         // every consumer wrote its part of the output tile; the store S-1 outputs ago is done
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        if (t == 0) bulk_wait_read<S - 2>();
+        if (t == 0) bulk_wait_read<S - 2>();  // staging[(nout + 1) % S] is free for the next output
         cons_sync();
         if (t == 0) {
           if (tail) tma_store5(&maps.out_t, 2 * (g.n1h - 1), 0, 0, (tile - tl.n_main) * KC, ti.o, so);
@@ -1385,7 +1403,21 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
     }
   }
   if (t == 0) bulk_wait_all();
-  if (DOT) {
+  if (UPD) {
+    __shared__ double red2[8][2];
+    acc_rz = warp_sum(acc_rz);
+    acc_rr = warp_sum(acc_rr);
+    if (lane == 0) {
+      red2[warp][0] = acc_rz;
+      red2[warp][1] = acc_rr;
+    }
+    cons_sync();
+    if (t < 2) {
+      double s = 0.0;
+      for (int w = 0; w < 8; ++w) s += red2[w][t];
+      g.partials[2 * blockIdx.x + t] = s;
+    }
+  } else if (DOT) {
     __shared__ double red[8];
     dot = warp_sum(dot);
     if (lane == 0) red[warp] = dot;
@@ -1551,20 +1583,20 @@ struct ColRing {  // ring depth: 3 slots unless the program's live span needs mo
   static constexpr int R = (KIND == COL_F3S && DOT) ? 4 : DBF_COL_R;
 };
 
-template <int N, int KIND, bool DOT>
+template <int N, int KIND, bool DOT, bool UPD = false>
 static cudaError_t launch_col_tma_k(const TmaMaps& maps, const ColGeom& g, const ColTiles& tl, cudaStream_t s, int* grid_out) {
   constexpr int R = ColRing<KIND, DOT>::R;
-  constexpr size_t smem = (size_t)(R + 2 + 1) * TmaCfg<N>::TILE + 2 * R * sizeof(uint64_t) + 1024;
+  constexpr size_t smem = (size_t)(R + (UPD ? 3 : 2) + 1) * TmaCfg<N>::TILE + 2 * R * sizeof(uint64_t) + 1024;
   static bool attr = false;
   if (!attr) {
     if (col_prog_span(kColProgHost[2 * KIND + (DOT ? 1 : 0)]) > R) return cudaErrorInvalidConfiguration;
-    cudaError_t e = cudaFuncSetAttribute(col_tma_kernel<N, KIND, DOT, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(col_tma_kernel<N, KIND, DOT, R, UPD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int grid = std::min(tl.n_tiles, num_sms());
   if (grid_out) *grid_out = grid;
-  col_tma_kernel<N, KIND, DOT, R><<<grid, TmaCfg<N>::THREADS, smem, s>>>(maps, g, tl);
+  col_tma_kernel<N, KIND, DOT, R, UPD><<<grid, TmaCfg<N>::THREADS, smem, s>>>(maps, g, tl);
   return cudaGetLastError();
 }
 
@@ -1590,6 +1622,11 @@ static cudaError_t launch_col_tma(int kind, const ColGeom& g, cudaStream_t s, in
   case K:                                                                                   \
     return dot ? launch_col_tma_k<N, K, true>(maps, g, tl, s, grid_out)                     \
                : launch_col_tma_k<N, K, false>(maps, g, tl, s, grid_out);
+  if (g.upd) {  // F3 fused with the PCG residual update
+    if (!dot) return cudaErrorInvalidValue;
+    if (kind == COL_F3F) return launch_col_tma_k<N, COL_F3F, true, true>(maps, g, tl, s, grid_out);
+    return cudaErrorInvalidValue;
+  }
   switch (kind) {
     DBF_TK(COL_I1S) DBF_TK(COL_I1F) DBF_TK(COL_I2S) DBF_TK(COL_I2F) DBF_TK(COL_F2S) DBF_TK(COL_F2F) DBF_TK(COL_F3S)
     DBF_TK(COL_F3F) DBF_TK(COL_ZI3) DBF_TK(COL_YI3) DBF_TK(COL_ZI6) DBF_TK(COL_YI6) DBF_TK(COL_ZF3)
@@ -1616,6 +1653,15 @@ static cudaError_t launch_col_reg(int kind, int N, const ColGeom& g, cudaStream_
   }
 }
 
+bool col_upd_supported(int N, const ColGeom& g) {
+  ColTiles tl;
+  if (N == 512) return col_tma_tiles<512>(g, &tl);
+  if (N == 256) return col_tma_tiles<256>(g, &tl);
+  if (N == 128) return col_tma_tiles<128>(g, &tl);
+  if (N == 64) return col_tma_tiles<64>(g, &tl);
+  return false;
+}
+
 cudaError_t launch_col(int kind, int N, const ColGeom& g, cudaStream_t s, int* grid_out) {
   cudaError_t e = cudaErrorNotSupported;
   // N = 512 y-forward passes write rows 2 MB apart (the ky stride of [f][ky][z][kx] at 512^2): the
@@ -1626,6 +1672,7 @@ cudaError_t launch_col(int kind, int N, const ColGeom& g, cudaStream_t s, int* g
   else if (N == 128) e = launch_col_tma<128>(kind, g, s, grid_out);
   else if (N == 64) e = launch_col_tma<64>(kind, g, s, grid_out);
   if (e != cudaErrorNotSupported) return e;
+  if (g.upd) return cudaErrorInvalidValue;  // the fused update exists on the TMA path only
   if (grid_out) *grid_out = col_grid(N, g.ncols);
   return launch_col_reg(kind, N, g, s);
 }

@@ -26,6 +26,13 @@ struct ColGeom {
   const cplx* dotp;
   double* partials;  // one double per CTA
   int n1;            // full x length (weights: kx = 0 and n1/2 count once)
+  // F3 fused with the PCG residual update (TMA path): out = dotp = r; r -= alpha q, partial
+  // <r, M r>, <r, r> per CTA into partials[2 blockIdx]; skipped once PCG stopped
+  int upd;
+  const double* cg_alpha;
+  const int* cg_stop0;   // CgDev.converged
+  const int* cg_stop1;   // CgDev.breakdown
+  double precq[36];      // preconditioner coefficients (prec_apply)
   int n_xy;          // length of fq.xy (guards the per-column xi_y(outer) lookup of y passes)
 };
 
@@ -97,6 +104,8 @@ struct XGeom {
 // host launchers (passes.cu)
 // grid_out: CTAs launched (= per-CTA partials written when dotp is set)
 cudaError_t launch_col(int kind, int N, const ColGeom& g, cudaStream_t s, int* grid_out = nullptr);
+// can F3 on this geometry run fused with the PCG residual update (TMA column path)?
+bool col_upd_supported(int N, const ColGeom& g);
 cudaError_t launch_x(int kind, int N1, const XGeom& g, cudaStream_t s, int* grid_out);
 int x_grid(int kind, int N1, long long nlines);
 int col_grid(int N, long long ncols);
