@@ -532,3 +532,30 @@ def test_residual_trace_vs_oracle(dbf):
     tr = ctx.trace()
     assert tr.shape[0] == rep["cg_iters"] + rep["newton_iters"]
     assert np.sum(tr[:, 0] <= 1e-10) >= rep["newton_iters"]
+
+
+def test_solve_fused_update_finite(dbf, monkeypatch):
+    """Finite-strain PCG with the residual update fused into the TMA F3 pass (z sweep of 256): same
+    Newton path and state as the oracle, and as the unfused GPU path."""
+    n = (16, 8, 256)
+    ph = two_phase(n, 81)
+    mats = [dict(kind="neohooke", mu=1.0, kappa=2.5), dict(kind="neohooke", mu=10.0, kappa=25.0)]
+    loads = []
+    for k in (1, 2):
+        t = np.eye(3); t[2, 2] = 1.0 + 0.01 * k
+        m = np.zeros((3, 3), bool); m[0, 0] = m[1, 1] = True
+        loads.append(dict(target=np.where(m, 0.0, t), mask=m))
+    st = O.FiniteStrainState(n)
+    runs = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("DBFFT_FUSED_UPDATE", fused)
+        ctx = dbf.DBFFT(n, kinematics="finite")
+        ctx.set_phases(ph, mats)
+        runs[fused] = [ctx.solve_increment(L["target"], L["mask"]) for L in loads]
+        runs[fused + "F"] = ctx.get_field(dbf.FIELD_STRAIN)
+    for L, r1, r0 in zip(loads, runs["1"], runs["0"]):
+        ref = O.solve_finite_increment(st, ph, mats, L, tol=1e-10)
+        assert r1["converged"] and r1["newton_iters"] == ref["newton_iters"] == r0["newton_iters"]
+        assert abs(r1["cg_iters"] - r0["cg_iters"]) <= 2
+        assert rel(r1["macro_stress"], ref["mean_P"]) <= 1e-9
+    assert rel(runs["1F"], ref["F"]) <= 1e-8
