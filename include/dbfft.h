@@ -71,7 +71,8 @@ typedef enum { DBFFT_SMALL_STRAIN = 6, DBFFT_FINITE_STRAIN = 9 } dbfft_kinematic
 typedef struct {
   int32_t rank, world;   /* this rank and the number of ranks P (1: single GPU)        */
   const void* nccl_id;   /* 128-byte ncclUniqueId (NCCL mode, world > 1), else NULL    */
-  void* cuda_stream;     /* cudaStream_t or NULL (ctx creates its own stream)          */
+  void* cuda_stream;     /* cudaStream_t, or NULL: ctx creates its own *blocking* stream,
+                            ordered with the caller's legacy default stream              */
   int32_t device;        /* CUDA device ordinal (-1: current device)                   */
   int32_t loopback;      /* 1: all `world` ranks virtual in this process (testing)     */
 } dbfft_env;

@@ -1510,7 +1510,9 @@ dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinemat
   if (env && env->cuda_stream) {
     ctx->stream = (cudaStream_t)env->cuda_stream;
   } else {
-    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    // a blocking stream: work a caller issues on the legacy default stream (NULL) is ordered
+    // with the context's kernels, and events recorded there bracket them
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamDefault) != cudaSuccess) {
       ctx->err = "cudaStreamCreate failed (no CUDA device?)";
       return fail(DBFFT_E_CUDA);
     }

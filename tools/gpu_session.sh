@@ -1,1 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "fused" 2>&1 | grep -E "^E |FAILED|passed|failed" | head -8
+PYTHONPATH=. timeout 300 python tools/dbg2.py
+timeout 600 python bench.py > gpurun_out/bench_s11.json 2> gpurun_out/bench_s11.err; tail -3 gpurun_out/bench_s11.err
