@@ -559,3 +559,79 @@ def test_solve_fused_update_finite(dbf, monkeypatch):
         assert abs(r1["cg_iters"] - r0["cg_iters"]) <= 2
         assert rel(r1["macro_stress"], ref["mean_P"]) <= 1e-9
     assert rel(runs["1F"], ref["F"]) <= 1e-8
+
+
+# ------------------------------------------------------------- full size and degenerate cases
+
+def _half_xi(n):
+    """Eq. 1 frequencies on the product's half-spectrum layout [ky][kz][kx <= n1/2] (oracle tables)."""
+    fx = O.axis_frequencies(n[0], 1.0)[: n[0] // 2 + 1]
+    fy = O.axis_frequencies(n[1], 1.0)
+    fz = O.axis_frequencies(n[2], 1.0)
+    X, Z, Y = np.broadcast_arrays(fx[None, None, :], fz[None, :, None], fy[:, None, None])
+    return np.stack([X, Y, Z])  # XI[a] = xi_a (a = x, y, z) on [ky][kz][kx]
+
+
+@pytest.mark.parametrize("kin", ["small", "finite"])
+def test_apply_K_full_size_homogeneous(dbf, kin):
+    """At c4's full 256^3 size, in the bench's launch configuration: a homogeneous medium makes the
+    operator diagonal in Fourier space, f(xi) = A(xi) u(xi) with A = xi . C . xi (closed form at
+    every one of the 8.5M points), so the whole FFT chain is checked element by element."""
+    n = (256, 256, 256)
+    if kin == "small":
+        mats = [dict(kind="iso", E=3.0, nu=0.28)]
+        C = O.isotropic_stiffness(3.0, 0.28)
+    else:  # neo-Hookean at F = I: K = isotropic (lam = kappa - 2 mu / 3, mu)
+        mats = [dict(kind="neohooke", mu=1.3, kappa=3.1)]
+        C = O.isotropic_from_lame(3.1 - 2.0 * 1.3 / 3.0, 1.3)
+    ctx = dbf.DBFFT(n, kinematics=kin)
+    ctx.set_phases(np.zeros((n[2], n[1], n[0]), np.uint16), mats)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn((3, n[2], n[1], n[0]), dtype=torch.float64, device="cuda", generator=g)
+    u = (torch.fft.rfftn(x, dim=(1, 2, 3)) / x[0].numel()).permute(0, 2, 1, 3).contiguous()  # [3][ky][kz][kx]
+    del x
+    f = ctx.apply_K(u).cpu().numpy()
+    un = u.cpu().numpy()
+    XI = _half_xi(n)                                    # [a][ky][kz][kx]
+    A = np.einsum("ijkl,j...,l...->ik...", C, XI, XI)   # [3,3][ky][kz][kx]
+    ref = np.einsum("ik...,k...->i...", A, un)
+    assert rel(f, ref) <= 1e-12
+
+
+def test_degenerate_homogeneous_and_zero_load(dbf):
+    """Homogeneous media converge with no PCG iteration to the uniform Hooke state (P7), for linear
+    strain control and finite-strain mixed control; a zero load returns the zero state."""
+    n = (32, 16, 64)
+    ph = np.zeros((n[2], n[1], n[0]), np.uint16)
+    ctx = dbf.DBFFT(n, kinematics="small")
+    ctx.set_phases(ph, [dict(kind="iso", E=2.0, nu=0.3)])
+    t = np.array([[1e-3, 2e-4, 0], [2e-4, -5e-4, 0], [0, 0, 3e-4]])
+    rep = ctx.solve_increment(t, np.zeros((3, 3), bool))
+    assert rep["converged"] and rep["cg_iters"] == 0
+    sig = np.einsum("ijkl,kl->ij", O.isotropic_stiffness(2.0, 0.3), t)
+    assert np.abs(ctx.get_field(dbf.FIELD_STRESS) - sig.reshape(3, 3, 1, 1, 1)).max() <= 1e-15 * np.abs(sig).max() * 10
+    rep = ctx.solve_increment(np.zeros((3, 3)), np.zeros((3, 3), bool))
+    assert rep["converged"] and rep["cg_iters"] == 0 and np.abs(ctx.get_field(dbf.FIELD_STRESS)).max() == 0.0
+    ctx = dbf.DBFFT(n, kinematics="finite")
+    ctx.set_phases(ph, [dict(kind="neohooke", mu=1.0, kappa=2.5)])
+    m = np.zeros((3, 3), bool); m[0, 0] = m[1, 1] = True
+    tf = np.eye(3); tf[2, 2] = 1.05; tf[0, 0] = tf[1, 1] = 0.0
+    rep = ctx.solve_increment(tf, m)
+    # mixed control: the macro block is solved exactly by (P Cbar P)^-1 - one PCG step per Newton step
+    assert rep["converged"] and rep["cg_iters"] <= rep["newton_iters"]
+    assert abs(rep["macro_stress"][0, 0]) <= 1e-10 and abs(rep["macro_stress"][1, 1]) <= 1e-10
+    F = ctx.get_field(dbf.FIELD_STRAIN)
+    assert np.abs(F - F[:, :, :1, :1, :1]).max() <= 1e-14  # uniform deformation
+
+
+def test_invalid_inputs_rejected(dbf):
+    """Bad grids, out-of-range phase ids and material/kinematics mismatches fail loudly."""
+    with pytest.raises(dbf.DBFFTError):
+        dbf.DBFFT((12, 16, 16), kinematics="small")
+    with pytest.raises(dbf.DBFFTError):
+        dbf.DBFFT((16, 16, 1024), kinematics="small")
+    ctx = dbf.DBFFT((8, 8, 8), kinematics="small")
+    with pytest.raises(dbf.DBFFTError):
+        ctx.set_phases(np.full((8, 8, 8), 3, np.uint16), ISO2)
+    with pytest.raises(dbf.DBFFTError):
+        ctx.set_phases(np.zeros((8, 8, 8), np.uint16), [dict(kind="neohooke", mu=1.0, kappa=2.0)])
