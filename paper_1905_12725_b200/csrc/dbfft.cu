@@ -898,7 +898,7 @@ ColGeom geom_F3_update(dbfft_ctx ctx, Slab& s) {
 
 bool pcg_fused(dbfft_ctx ctx) {
   const char* e = getenv("DBFFT_FUSED_UPDATE");
-  if ((e && e[0] == '0') || ctx->kin != 9) return false;  // F3F only (F3S's program needs a 4-slot ring)
+  if (e && e[0] == '0') return false;
   for (Slab& s : ctx->slabs)
     if (!col_upd_supported(ctx->n3, geom_F3_update(ctx, s))) return false;
   return true;

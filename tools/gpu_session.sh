@@ -1,2 +1,2 @@
-PYTHONPATH=. timeout 300 python tools/dbg2.py
-timeout 600 python bench.py > gpurun_out/bench_s11.json 2> gpurun_out/bench_s11.err; tail -3 gpurun_out/bench_s11.err
+timeout 1800 python -m pytest tests -m gpu -x -q 2>&1 | grep -E "^E |FAILED|passed|failed" | head -8
+timeout 1800 python tools/run_configs.py c5 --noprof > gpurun_out/c5b.jsonl 2> gpurun_out/c5b.err; tail -2 gpurun_out/c5b.err; cat gpurun_out/c5b.jsonl | cut -c1-400
