@@ -679,24 +679,29 @@ template <int N1, int P>
 DBF_DEV int x_idx(int base, int pos) {
   return (N1 & 1) ? IdxPlain{base}(pos) : P == 16 ? IdxGrp{base}(pos) : IdxSwz{base}(pos);
 }
-// a pair job's threads share one warp when N1 / P divides 32: exchanges need only __syncwarp
+// exchange sync of one pair job (N1 / P threads): the warp when the job fits in one; a named
+// barrier of the job's warps when it spans several (N1 = 512: 64 threads, ids 1 + job); the CTA
+// barrier otherwise (odd lengths: jobs of 3 threads straddle warps)
 template <int N1, int P>
-DBF_DEV void x_jobsync() {
-  if (N1 / P <= 32 && 32 % (N1 / P) == 0) __syncwarp();
+DBF_DEV void x_jobsync(int job) {
+  constexpr int TPJ = N1 / P;
+  if (TPJ <= 32 && 32 % TPJ == 0) __syncwarp();
+  else if (TPJ % 32 == 0) asm volatile("bar.sync %0, %1;" ::"r"(1 + job), "r"(TPJ) : "memory");
   else __syncthreads();
 }
 template <int N1, int P>
 struct XSync {
-  DBF_DEV void operator()() const { x_jobsync<N1, P>(); }
+  int job;
+  DBF_DEV void operator()() const { x_jobsync<N1, P>(job); }
 };
 template <int N1, int P, bool INV>
-DBF_DEV void x_fft(cplx (&a)[P], cplx* cx, int gq, int base, const cplx* __restrict__ tw) {
+DBF_DEV void x_fft(cplx (&a)[P], cplx* cx, int gq, int base, const cplx* __restrict__ tw, int job) {
   if constexpr ((N1 & 1) != 0) {
-    fft_odd<N1, INV>(a, cx, gq, IdxPlain{base}, tw, XSync<N1, P>{});
+    fft_odd<N1, INV>(a, cx, gq, IdxPlain{base}, tw, XSync<N1, P>{job});
   } else if constexpr (P == 16) {
-    fft_sub<N1, 16, INV>(a, cx, gq, IdxGrp{base}, tw, XSync<N1, 16>{});
+    fft_sub<N1, 16, INV>(a, cx, gq, IdxGrp{base}, tw, XSync<N1, 16>{job});
   } else {
-    fft_cta<N1, INV>(a, cx, gq, IdxSwz{base}, tw, XSync<N1, 8>{});
+    fft_cta<N1, INV>(a, cx, gq, IdxSwz{base}, tw, XSync<N1, 8>{job});
   }
 }
 
@@ -907,8 +912,8 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
           x_issue_in<N1, KIND>(g, nxt, st_in, &bars[0]);
         }
       }
-      x_fft<N1, PX, true>(a, cx, gq, jbase, g.tw);
-      x_jobsync<N1, PX>();  // the job's exchange reads are done before its slots become reals
+      x_fft<N1, PX, true>(a, cx, gq, jbase, g.tw, job);
+      x_jobsync<N1, PX>(job);  // the job's exchange reads are done before its slots become reals
 #pragma unroll
       for (int s = 0; s < PX; ++s) {
         const int m = gq + s * TPJ;
@@ -981,16 +986,16 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
         const double rb = (fb < COUT) ? real[(l * CS + fb) * N1 + m] : 0.0;
         a[s] = make_double2(ra, rb);
       }
-      x_fft<N1, PX, false>(a, cx, gq, jbase, g.tw);
+      x_fft<N1, PX, false>(a, cx, gq, jbase, g.tw, job);
       constexpr bool SHFL = (PX == 8 && TPJ <= 32);
       cplx zn[PX];
       if constexpr (SHFL) {
         x_partner<TPJ>(a, zn, gq);
       } else {
-        x_jobsync<N1, PX>();
+        x_jobsync<N1, PX>(job);
 #pragma unroll
         for (int s = 0; s < PX; ++s) cx[x_idx<N1, PX>(jbase, gq + s * TPJ)] = a[s];
-        x_jobsync<N1, PX>();
+        x_jobsync<N1, PX>(job);
 #pragma unroll
         for (int s = 0; s < PX; ++s) zn[s] = cx[x_idx<N1, PX>(jbase, (N1 - (gq + s * TPJ)) % N1)];
       }
