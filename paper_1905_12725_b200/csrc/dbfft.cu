@@ -898,7 +898,10 @@ ColGeom geom_F3_update(dbfft_ctx ctx, Slab& s) {
 
 bool pcg_fused(dbfft_ctx ctx) {
   const char* e = getenv("DBFFT_FUSED_UPDATE");
-  if (e && e[0] == '0') return false;
+  // finite strain only: small strain's F3S program leaves no ring slot for r, and the variant
+  // that loads r straight from global memory ran slower than F3 + k_cg_update (c5 512^3: 8.6 vs
+  // 6.2 ms per iteration)
+  if ((e && e[0] == '0') || ctx->kin != 9) return false;
   for (Slab& s : ctx->slabs)
     if (!col_upd_supported(ctx->n3, geom_F3_update(ctx, s))) return false;
   return true;

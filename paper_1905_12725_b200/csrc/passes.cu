@@ -1330,17 +1330,6 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
         mbar_wait(&full[qb % R], (qb / R) & 1);
         sbp = ring + (qb % R) * (CF::TILE / 16);
       }
-      // UPD without a ring slot for r (small strain: the F3S program leaves no room): the term that
-      // completes output o reads r_o straight from global memory, in flight during the FFT
-      constexpr bool RLDG = UPD && !DOT;
-      cplx rl[RLDG ? 8 : 1];
-      if (RLDG && ti.last) {
-#pragma unroll
-        for (int s = 0; s < 8; ++s) {
-          at.pos = gq + s * TPC;
-          rl[RLDG ? s : 0] = valid ? __ldg(g.dotp + at.out_idx(ti.o)) : make_double2(0.0, 0.0);
-        }
-      }
       cplx a[8];
 #pragma unroll
       for (int s = 0; s < 8; ++s) {
@@ -1372,7 +1361,7 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
         } else {
           const int o = tail ? tma_toff<N>(at.pos, c) : tma_moff<N>(at.pos, c);
           if (UPD) {  // r_o -= alpha q_o (the F3 output is q = K p); the tile's r is staged in sd
-            const cplx rr = RLDG ? rl[RLDG ? s : 0] : sd[o];
+            const cplx rr = sd[o];
             v = make_double2(fma(-alpha, v.x, rr.x), fma(-alpha, v.y, rr.y));
             if (ti.o == 2 && valid) {  // r_0, r_1 are in the previous two staging buffers
               const cplx r3[3] = {stg[((nout + S - 2) % S) * (CF::TILE / 16) + o], stg[((nout + S - 1) % S) * (CF::TILE / 16) + o], v};
@@ -1638,10 +1627,9 @@ static cudaError_t launch_col_tma(int kind, const ColGeom& g, cudaStream_t s, in
   case K:                                                                                   \
     return dot ? launch_col_tma_k<N, K, true>(maps, g, tl, s, grid_out)                     \
                : launch_col_tma_k<N, K, false>(maps, g, tl, s, grid_out);
-  if (g.upd) {  // F3 fused with the PCG residual update (r through the ring / straight loads)
+  if (g.upd) {  // F3 fused with the PCG residual update (r through the ring)
     if (!dot) return cudaErrorInvalidValue;
     if (kind == COL_F3F) return launch_col_tma_k<N, COL_F3F, true, true>(maps, g, tl, s, grid_out);
-    if (kind == COL_F3S) return launch_col_tma_k<N, COL_F3S, false, true>(maps, g, tl, s, grid_out);
     return cudaErrorInvalidValue;
   }
   switch (kind) {
