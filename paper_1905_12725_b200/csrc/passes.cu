@@ -489,9 +489,19 @@ DBF_DEV void j2_update(const double* eps, const double* epsp, const double* prm,
   if (svm > sy) {
     // g(x) = svm - 3 mu rdt x^n - sy (1 + x) = 0, x = (dp / rdt)^(1/n); safeguarded Newton
     const double rdt = edot0 * dt, m3 = 3.0 * mu * rdt;
+    // x^(n-1) by binary powering when the rate exponent is an integer (c5: n = 20), else pow
+    const int ni = (int)nexp;
+    const bool nint = (double)ni == nexp && ni >= 1 && ni <= 64;
+    auto xpow_n1 = [&](double b) {
+      if (!nint) return pow(b, nexp - 1.0);
+      double r = 1.0;
+      for (int e = ni - 1; e; e >>= 1, b *= b)
+        if (e & 1) r *= b;
+      return r;
+    };
     double lo = 0.0, hi = svm / sy - 1.0, x = 0.5 * hi;
     for (int it = 0; it < 200; ++it) {
-      const double xn1 = pow(x, nexp - 1.0);
+      const double xn1 = xpow_n1(x);
       const double gx = svm - m3 * xn1 * x - sy * (1.0 + x);
       if (gx > 0) lo = x; else hi = x;
       const double dg = -m3 * nexp * xn1 - sy;
@@ -500,9 +510,11 @@ DBF_DEV void j2_update(const double* eps, const double* epsp, const double* prm,
       if (fabs(xn - x) <= 1e-16 * x || hi - lo <= 1e-16 * hi) { x = xn; break; }
       x = xn;
     }
-    dp = rdt * pow(x, nexp);
+    const double xn1 = xpow_n1(x);
+    dp = rdt * x * xn1;  // rdt x^n
     theta = 1.0 - 3.0 * mu * dp / svm;
-    const double Hp = (dp > 0) ? sy / (nexp * rdt) * pow(dp / rdt, 1.0 / nexp - 1.0) : 0.0;
+    // H' = d(sy (1 + x))/d(dp) = sy/(n rdt) (dp/rdt)^(1/n - 1) = sy/(n rdt) x^(1 - n)
+    const double Hp = (dp > 0) ? sy / (nexp * rdt) / xn1 : 0.0;
     thetabar = 1.0 / (1.0 + Hp / (3.0 * mu)) - (1.0 - theta);
     const double is = 1.0 / sqrt(ss);
 #pragma unroll
