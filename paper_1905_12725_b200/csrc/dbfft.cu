@@ -112,7 +112,7 @@ struct Slab {
   double* ptable = nullptr;
   double *F = nullptr, *F_c = nullptr, *epsp_c = nullptr, *epsp_t = nullptr, *tan = nullptr;
   CgDev* cg = nullptr;
-  double *part_x = nullptr, *part_f3 = nullptr, *part_cg = nullptr, *part_misc = nullptr;
+  double *part_x = nullptr, *part_cg = nullptr, *part_misc = nullptr;
   double* loc = nullptr;   // [64] small reduced vectors (also the all-reduce buffers)
   double* e_dev = nullptr; // [9]
   int* bad = nullptr;
@@ -652,16 +652,16 @@ std::vector<double> axis_xi(int n, double L, int count) {
 
 // ---------------------------------------------------------------- operator application
 struct ApplyOut {
-  std::vector<int> grid_x, grid_f3;
+  std::vector<int> grid_x;  // X-pass CTAs per slab (partials to reduce)
 };
 
 int nf_I1(dbfft_ctx ctx) { return ctx->kin == 9 ? 6 : 5; }
 
-// f = K(u) [+ e] on every slab; partials: part_x (DC of sigma), part_f3 (<u, f>) per slab.
+// f = K(u) [+ e] on every slab; partials: part_x (DC of sigma, and <u, f> in slot 9) per slab.
 // u / f select per-slab vectors, e_member the macro block inside each slab's CgDev.
 typedef double Macro9[9];
 
-dbfft_status apply_K_slabs(dbfft_ctx ctx, cplx* Slab::*u, cplx* Slab::*f, bool use_e, Macro9 CgDev::*e_member, bool dot,
+dbfft_status apply_K_slabs(dbfft_ctx ctx, cplx* Slab::*u, cplx* Slab::*f, bool use_e, Macro9 CgDev::*e_member,
                            ApplyOut* ao, bool front_only = false) {
   const bool fin = ctx->kin == 9;
   int xkind;
@@ -672,10 +672,7 @@ dbfft_status apply_K_slabs(dbfft_ctx ctx, cplx* Slab::*u, cplx* Slab::*f, bool u
   for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_I1F : COL_I1S, PK_I1, geom_I1(ctx, s, s.*u, s.WA, nf1), ctx->n3));
   CKS(exchange(ctx, (long long)nf1 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
   for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_I2F : COL_I2S, PK_I2, geom_I2(ctx, s, s.WR, s.WB, nf1), ctx->n2));
-  if (ao) {
-    ao->grid_x.assign(ctx->slabs.size(), 0);
-    ao->grid_f3.assign(ctx->slabs.size(), 0);
-  }
+  if (ao) ao->grid_x.assign(ctx->slabs.size(), 0);
   for (size_t k = 0; k < ctx->slabs.size(); ++k) {
     Slab& s = ctx->slabs[k];
     XGeom gx = xgeom(ctx, s, s.WB, s.WB);
@@ -687,17 +684,7 @@ dbfft_status apply_K_slabs(dbfft_ctx ctx, cplx* Slab::*u, cplx* Slab::*f, bool u
   if (front_only) return DBFFT_OK;  // the caller runs the forward tail (PCG: F3 fused with r -= alpha q)
   for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, geom_F2(ctx, s, s.WB, s.WA, 6), ctx->n2));
   CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
-  for (size_t k = 0; k < ctx->slabs.size(); ++k) {
-    Slab& s = ctx->slabs[k];
-    ColGeom g5 = geom_F3(ctx, s, s.WR, s.*f, 6);
-    if (dot) {
-      g5.dotp = s.*u;
-      g5.partials = s.part_f3;
-    }
-    int grid5 = 0;
-    CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_F3, g5, ctx->n3, &grid5));
-    if (ao) ao->grid_f3[k] = grid5;
-  }
+  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_F3, geom_F3(ctx, s, s.WR, s.*f, 6), ctx->n3));
   return DBFFT_OK;
 }
 
@@ -825,7 +812,7 @@ dbfft_status pcg(dbfft_ctx ctx, const dbfft_opts& o, int* iters_out) {
     if (ctx->h_cg->converged == 1) {
       // true-residual confirmation (R7): r = b - A x
       ApplyOut ao;
-      CKS(apply_K_slabs(ctx, &Slab::x, &Slab::q, macro, &CgDev::xe, false, &ao));
+      CKS(apply_K_slabs(ctx, &Slab::x, &Slab::q, macro, &CgDev::xe, &ao));
       for (size_t k = 0; k < ctx->slabs.size(); ++k) {
         Slab& s = ctx->slabs[k];
         {
@@ -913,7 +900,7 @@ bool pcg_fused(dbfft_ctx ctx) {
 dbfft_status pcg_iteration_fused(dbfft_ctx ctx, bool macro, int nb) {
   const bool fin = ctx->kin == 9;
   ApplyOut ao;
-  CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, macro, &CgDev::pe, false, &ao, true));
+  CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, macro, &CgDev::pe, &ao, true));
   for (size_t j = 0; j < ctx->slabs.size(); ++j) {
     Slab& s = ctx->slabs[j];
     CKS(reduce_to(ctx, s, s.part_x, ao.grid_x[j], 10, 1));
@@ -959,7 +946,7 @@ dbfft_status pcg_body(dbfft_ctx ctx, int every, bool macro, int nb) {
       ApplyOut ao;
       // <p, A p> comes from the X pass (slot 9: sum (grad p + p_e) : sigma, Parseval), so F3 does
       // not re-read p
-      CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, macro, &CgDev::pe, false, &ao));
+      CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, macro, &CgDev::pe, &ao));
       for (size_t j = 0; j < ctx->slabs.size(); ++j) {
         Slab& s = ctx->slabs[j];
         CKS(reduce_to(ctx, s, s.part_x, ao.grid_x[j], 10, 1));
@@ -1301,7 +1288,7 @@ dbfft_status solve_newton(dbfft_ctx ctx, const double* target, const uint8_t* ma
 
 void free_slab(Slab& s) {
   void* ptrs[] = {s.x, s.r, s.p, s.q, s.b, s.u, s.u_c, s.WA, s.WB, s.phase, s.ptable, s.F, s.F_c, s.epsp_c, s.epsp_t, s.tan,
-                  s.cg, s.part_x, s.part_f3, s.part_cg, s.part_misc, s.loc, s.e_dev, s.bad, s.counts, s.tmp_real};
+                  s.cg, s.part_x, s.part_cg, s.part_misc, s.loc, s.e_dev, s.bad, s.counts, s.tmp_real};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (s.WR && s.WR != s.WA) cudaFree(s.WR);
@@ -1407,7 +1394,6 @@ dbfft_status alloc_slab(dbfft_ctx ctx, Slab& s) {
   int gx = 0;
   for (int k = 0; k < X_REAL_OUT; ++k) gx = std::max(gx, x_grid(k, ctx->n1, s.nlines));
   CKS(dalloc(ctx, &s.part_x, (size_t)gx * 10));
-  CKS(dalloc(ctx, &s.part_f3, (size_t)std::max(col_grid(ctx->n3, (long long)s.nyl * ctx->n1h), 1024)));
   CKS(dalloc(ctx, &s.part_cg, (size_t)cg_blocks() * 2));
   CKS(dalloc(ctx, &s.part_misc, (size_t)cg_blocks() * 45));
   CKS(dalloc(ctx, &s.loc, 64));
@@ -1758,13 +1744,13 @@ dbfft_status dbfft_apply_K(dbfft_ctx ctx, const void* u_hat, void* f_hat) {
     cplx* sf = s.q;
     s.p = (cplx*)u_hat;
     s.q = (cplx*)f_hat;
-    dbfft_status st = apply_K_slabs(ctx, &Slab::p, &Slab::q, false, &CgDev::pe, false, nullptr);
+    dbfft_status st = apply_K_slabs(ctx, &Slab::p, &Slab::q, false, &CgDev::pe, nullptr);
     s.p = su;
     s.q = sf;
     return st;
   }
   CKS(spec_in(ctx, (const cplx*)u_hat, &Slab::p));
-  CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, false, &CgDev::pe, false, nullptr));
+  CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, false, &CgDev::pe, nullptr));
   return spec_out(ctx, &Slab::q, (cplx*)f_hat, cudaMemcpyDeviceToDevice);
 }
 
@@ -1785,7 +1771,7 @@ dbfft_status dbfft_apply_K_aug(dbfft_ctx ctx, const uint8_t mask[9], const void*
   CK(cudaStreamSynchronize(ctx->stream));
   CKS(spec_in(ctx, (const cplx*)u_hat, &Slab::p));
   ApplyOut ao;
-  CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, true, &CgDev::pe, false, &ao));
+  CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, true, &CgDev::pe, &ao));
   double red[10];
   CKS(reduce_x(ctx, ao.grid_x, red, false));
   for (int a = 0; a < 9; ++a) red[a] /= (double)ctx->N;

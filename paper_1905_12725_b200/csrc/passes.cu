@@ -295,8 +295,6 @@ __global__ void __launch_bounds__(256, ColCfg<N>::ODD ? 1 : ColPref<KIND>::MINB)
   ColAt at;
   at.g = &g;
   at.set_col(valid ? (int)(col / g.n1h) : 0, valid ? (int)(col % g.n1h) : 0);
-  const double wdot = (at.kx == 0 || 2 * at.kx == g.n1) ? 1.0 : 2.0;
-  double dot = 0.0;
   IdxCols<COLS> idx{c};
   cplx r0[PREF ? P : 1];
   if (PREF) {
@@ -339,24 +337,8 @@ __global__ void __launch_bounds__(256, ColCfg<N>::ODD ? 1 : ColPref<KIND>::MINB)
       if (!ti.last) {
         if (TWO) sacc[idx(at.pos)] = v;  // own positions only: no barrier needed
       } else if (valid) {
-        const long long oi = at.out_idx(ti.o);
-        g.out[oi] = v;
-        if (g.dotp) {
-          cplx p = __ldg(g.dotp + oi);
-          dot += wdot * (p.x * v.x + p.y * v.y);
-        }
+        g.out[at.out_idx(ti.o)] = v;
       }
-    }
-  }
-  if (g.dotp) {
-    __shared__ double red[8];
-    dot = warp_sum(dot);
-    if ((t & 31) == 0) red[t >> 5] = dot;
-    __syncthreads();
-    if (t == 0) {
-      double s = 0.0;
-      for (int w = 0; w < 8; ++w) s += red[w];
-      g.partials[blockIdx.x] = s;
     }
   }
 }
@@ -1311,7 +1293,6 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
   const int gq = t % TPC;  // position group
   const int lane = t & 31;
   cplx* xcol = xb + c * N;  // this column's FFT exchange buffer
-  double dot = 0.0;
   double acc_rz = 0.0, acc_rr = 0.0;  // UPD: partial <r, M r>, <r, r>
   const double alpha = UPD ? *g.cg_alpha : 0.0;
   uint32_t nout = 0;        // output tiles written (staging rotation)
@@ -1388,10 +1369,6 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
             }
           }
           so[o] = v;
-          if (DOT && !UPD && sd && valid) {
-            const cplx p = sd[o];
-            dot += wdot * (p.x * v.x + p.y * v.y);
-          }
         }
       }
       // release the ring slots this term finished (FIFO): all lanes of the warp are done
@@ -1433,16 +1410,6 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
       double s = 0.0;
       for (int w = 0; w < 8; ++w) s += red2[w][t];
       g.partials[2 * blockIdx.x + t] = s;
-    }
-  } else if (DOT) {
-    __shared__ double red[8];
-    dot = warp_sum(dot);
-    if (lane == 0) red[warp] = dot;
-    cons_sync();
-    if (t == 0) {
-      double s = 0.0;
-      for (int w = 0; w < 8; ++w) s += red[w];
-      g.partials[blockIdx.x] = s;
     }
   }
 }
@@ -1635,15 +1602,13 @@ static cudaError_t launch_col_tma(int kind, const ColGeom& g, cudaStream_t s, in
     ok = col_map(&maps.dot_m, g.dotp, N, g.n1h, g.out_psh, g.out_ps, g.out_pcs, tl.n_outer, g.out_os, 3, g.out_fs, false, KC) &&
          col_map(&maps.dot_t, g.dotp, N, g.n1h, g.out_psh, g.out_ps, g.out_pcs, tl.n_outer, g.out_os, 3, g.out_fs, true, KC);
   if (!ok) return cudaErrorNotSupported;
-#define DBF_TK(K)                                                                            \
-  case K:                                                                                   \
-    return dot ? launch_col_tma_k<N, K, true>(maps, g, tl, s, grid_out)                     \
-               : launch_col_tma_k<N, K, false>(maps, g, tl, s, grid_out);
+#define DBF_TK(K) \
+  case K: return launch_col_tma_k<N, K, false>(maps, g, tl, s, grid_out);
   if (g.upd) {  // F3 fused with the PCG residual update (r through the ring)
-    if (!dot) return cudaErrorInvalidValue;
-    if (kind == COL_F3F) return launch_col_tma_k<N, COL_F3F, true, true>(maps, g, tl, s, grid_out);
-    return cudaErrorInvalidValue;
+    if (!dot || kind != COL_F3F) return cudaErrorInvalidValue;
+    return launch_col_tma_k<N, COL_F3F, true, true>(maps, g, tl, s, grid_out);
   }
+  if (dot) return cudaErrorInvalidValue;  // the ring-loaded operand exists only for the fused update
   switch (kind) {
     DBF_TK(COL_I1S) DBF_TK(COL_I1F) DBF_TK(COL_I2S) DBF_TK(COL_I2F) DBF_TK(COL_F2S) DBF_TK(COL_F2F) DBF_TK(COL_F3S)
     DBF_TK(COL_F3F) DBF_TK(COL_ZI3) DBF_TK(COL_YI3) DBF_TK(COL_ZI6) DBF_TK(COL_YI6) DBF_TK(COL_ZF3)
@@ -1689,7 +1654,7 @@ cudaError_t launch_col(int kind, int N, const ColGeom& g, cudaStream_t s, int* g
   else if (N == 128) e = launch_col_tma<128>(kind, g, s, grid_out);
   else if (N == 64) e = launch_col_tma<64>(kind, g, s, grid_out);
   if (e != cudaErrorNotSupported) return e;
-  if (g.upd) return cudaErrorInvalidValue;  // the fused update exists on the TMA path only
+  if (g.upd || g.dotp) return cudaErrorInvalidValue;  // the fused update exists on the TMA path only
   if (grid_out) *grid_out = col_grid(N, g.ncols);
   return launch_col_reg(kind, N, g, s);
 }

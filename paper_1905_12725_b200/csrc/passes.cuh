@@ -22,12 +22,12 @@ struct ColGeom {
   long long ncols;   // n_outer * n1h columns
   const cplx* tw;    // twiddles W_N[k], k < N
   Freq fq;
-  // fused <p, out> (F3): weighted Hermitian dot with a vector in the output layout
+  // F3 fused with the PCG residual update (TMA path only): out = dotp = r, streamed through the
+  // ring; r -= alpha q, partial <r, M r>, <r, r> per CTA into partials[2 blockIdx] (Hermitian
+  // weights: kx = 0 and n1/2 count once); skipped once PCG stopped
   const cplx* dotp;
-  double* partials;  // one double per CTA
-  int n1;            // full x length (weights: kx = 0 and n1/2 count once)
-  // F3 fused with the PCG residual update (TMA path): out = dotp = r; r -= alpha q, partial
-  // <r, M r>, <r, r> per CTA into partials[2 blockIdx]; skipped once PCG stopped
+  double* partials;
+  int n1;            // full x length
   int upd;
   const double* cg_alpha;
   const int* cg_stop0;   // CgDev.converged
@@ -102,7 +102,7 @@ struct XGeom {
 };
 
 // host launchers (passes.cu)
-// grid_out: CTAs launched (= per-CTA partials written when dotp is set)
+// grid_out: CTAs launched (= per-CTA partial pairs written when upd is set)
 cudaError_t launch_col(int kind, int N, const ColGeom& g, cudaStream_t s, int* grid_out = nullptr);
 // can F3 on this geometry run fused with the PCG residual update (TMA column path)?
 bool col_upd_supported(int N, const ColGeom& g);
