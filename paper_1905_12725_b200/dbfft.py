@@ -246,11 +246,21 @@ class DBFFT:
             raise DBFFTError(st, self.lib.dbfft_last_error(self.h).decode())
         return out
 
-    def get_field(self, which, on_device=False, pinned=False):
+    def get_field(self, which, on_device=False, pinned=False, out=None):
         """Committed field (C ABI dbfft_get_field).  Host results land in a fresh numpy array;
-        pinned=True allocates it in page-locked memory (faster D2H copy)."""
+        pinned=True allocates it in page-locked memory (faster D2H copy); `out` (a C-contiguous
+        float64 host array of the field's size, e.g. a reused pinned buffer) receives it instead."""
         n1, n2, n3 = self.n
+        if self.world > 1 and not self.loopback:
+            n3 //= self.world  # NCCL slab mode: this rank's z-slab
         N = n1 * n2 * n3
+        if out is not None:
+            ncomp = 3 if which == FIELD_U else 9
+            if which == FIELD_U_HAT or not isinstance(out, np.ndarray) or out.dtype != np.float64 \
+                    or out.size != ncomp * N or not out.flags["C_CONTIGUOUS"]:
+                raise ValueError("get_field(out=): a C-contiguous float64 host array of the field's size")
+            self._check(self.lib.dbfft_get_field(self.h, which, out.ctypes.data_as(ctypes.c_void_p), 0))
+            return out
         if which == FIELD_U_HAT:
             out = self.empty_spectral()
             self._check(self.lib.dbfft_get_field(self.h, which, _dptr(out), 1))

@@ -215,6 +215,16 @@ def test_solve_c1(dbf):
     assert rel(ctx.get_field(dbf.FIELD_STRESS), ref["sig"]) <= 1e-8
     assert rel(ctx.get_field(dbf.FIELD_STRAIN), ref["eps"]) <= 1e-8
     assert rel(ctx.get_field(dbf.FIELD_U), O.displacement(ref["u_hat"])) <= 1e-8
+    # caller-owned host buffers (bench.py's e2e reuses a pinned one)
+    import torch
+    buf = torch.empty((3,) + cfg["phase"].shape, dtype=torch.float64, pin_memory=True).numpy()
+    assert ctx.get_field(dbf.FIELD_U, out=buf) is buf
+    assert rel(buf, O.displacement(ref["u_hat"])) <= 1e-8
+    buf9 = np.empty((9,) + cfg["phase"].shape)
+    ctx.get_field(dbf.FIELD_STRESS, out=buf9)
+    assert rel(buf9.reshape(3, 3, *cfg["phase"].shape), ref["sig"]) <= 1e-8
+    with pytest.raises(ValueError):
+        ctx.get_field(dbf.FIELD_U, out=np.empty(5))
 
 
 @pytest.mark.parametrize("n", [32, 64])
