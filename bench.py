@@ -170,10 +170,13 @@ def gpu_arm(args):
     phase = cfg["phase"]
     if world > 1 and not args.replicas:
         try:
-            ctx = dbfft.DBFFT(n, kinematics="finite", device=local, stream=stream, world=world, rank=rank)
+            ctx = dbfft.DBFFT(n, kinematics="finite", device=local, stream=stream, world=world, rank=rank,
+                              transport=args.transport)
             nzl = n[2] // world
             phase = np.ascontiguousarray(cfg["phase"][rank * nzl:(rank + 1) * nzl])
-            mode = f"slab x{world} (z-slabs / ky-slabs, NCCL all-to-all + all-reduce)"
+            mode = (f"slab x{world} (z-slabs / ky-slabs, " +
+                    ("passes store into peer memory (VMM windows) + NCCL all-reduce)" if args.transport == "peer"
+                     else "NCCL all-to-all + all-reduce)"))
         except Exception as exc:  # noqa: BLE001
             mode = f"replicas x{world} (slab init failed: {str(exc)[:120]})"
             ctx = dbfft.DBFFT(n, kinematics="finite", device=local, stream=stream)
@@ -410,6 +413,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of slabs")
+    ap.add_argument("--transport", choices=("nccl", "peer"), default="nccl",
+                    help="N > 1 slabs: NCCL all-to-all exchanges, or passes storing into peer memory")
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args)

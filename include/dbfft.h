@@ -75,7 +75,34 @@ typedef struct {
                             ordered with the caller's legacy default stream              */
   int32_t device;        /* CUDA device ordinal (-1: current device)                   */
   int32_t loopback;      /* 1: all `world` ranks virtual in this process (testing)     */
+  int32_t transport;     /* world > 1: how the two all-to-alls per operator application
+                             move data.  DBFFT_TRANSPORT_NCCL: grouped
+                            ncclSend/ncclRecv of the rank-chunked pass outputs.
+                            DBFFT_TRANSPORT_PEER: the z-inverse and y-forward passes store
+                            their chunk for rank d straight into rank d's receive buffer
+                            through a CUDA VMM window (NVLink peer memory; one node), a
+                            device barrier replaces the exchange.  All-reduces stay NCCL. */
 } dbfft_env;
+enum { DBFFT_TRANSPORT_NCCL = 0, DBFFT_TRANSPORT_PEER = 1 };
+
+/* Host helper of the peer transport's bootstrap: all-gather of nfd (1..16) file descriptors among
+ * the `world` processes of one node over abstract Unix sockets (SCM_RIGHTS), rendezvous name
+ * "dbfft-<tag>-<rank>".  out[src * nfd + i] receives a descriptor of process src's fds[i] (owned
+ * by the caller; out[rank * nfd + i] = fds[i] itself).  DBFFT_E_INVALID_ARG on bad arguments,
+ * DBFFT_E_STATE on a socket error or timeout (message in dbfft_last_error(NULL)).  (sync) */
+dbfft_status dbfft_fd_allgather(const char* tag, int32_t rank, int32_t world, const int32_t* fds, int32_t nfd,
+                                int32_t* out, int32_t timeout_ms);
+
+/* Probe of the peer transport's cross-process windows (tests; no ctx, no NCCL): every process
+ * builds an exchange buffer of `world` chunks exactly as dbfft_create does for
+ * DBFFT_TRANSPORT_PEER (cuMemCreate, POSIX-fd export, dbfft_fd_allgather(tag), import, window
+ * mapping), then stores 1000*rank + d into the first 1024 words of its window chunk d, i.e. into
+ * rank d's buffer.  After a host barrier among the processes, _check counts the words of this
+ * rank's buffer that differ from what rank src wrote into chunk src (0 = every window landed).
+ * Several processes may share one GPU (no kernel waits on another process).  (sync) */
+dbfft_status dbfft_peer_probe_open(const char* tag, int32_t rank, int32_t world, int32_t device, void** out);
+dbfft_status dbfft_peer_probe_check(void* probe, int32_t* bad_words);
+dbfft_status dbfft_peer_probe_close(void* probe);
 
 /* NCCL bootstrap (rank 0): writes a 128-byte ncclUniqueId.  NCCL is loaded at run time
  * (dlopen libnccl.so.2, or $DBFFT_NCCL_LIB); DBFFT_E_NCCL if it cannot be loaded. */

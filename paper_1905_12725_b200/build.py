@@ -7,7 +7,7 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdbfft.so")
-SOURCES = ["passes.cu", "cg.cu", "monitors.cu", "dbfft.cu"]
+SOURCES = ["passes.cu", "cg.cu", "monitors.cu", "peer.cu", "dbfft.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "-diag-suppress", "128,177,550"]

@@ -29,6 +29,7 @@
 #include "cg.cuh"
 #include "passes.cuh"
 #include "monitors.cuh"
+#include "peer.cuh"
 
 namespace {
 
@@ -108,6 +109,10 @@ struct Slab {
   const double* xiy = nullptr;  // xi_y of the local ky slab (offset into the global table)
   cplx *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *b = nullptr, *u = nullptr, *u_c = nullptr;
   cplx *WA = nullptr, *WR = nullptr, *WB = nullptr;  // send, receive (== WA when P == 1), y-pass buffers
+  // exchange targets: the I1-type passes store into WS1, their readers take WR; the F2-type into
+  // WS2, read from WR2.  NCCL transport: WS1 = WS2 = WA, WR2 = WR.  Peer transport: WS1 / WS2 are
+  // windows onto every rank's WR / WR2 (peer.cuh), WA stays local scratch.
+  cplx *WS1 = nullptr, *WS2 = nullptr, *WR2 = nullptr;
   uint16_t* phase = nullptr;
   double* ptable = nullptr;
   double *F = nullptr, *F_c = nullptr, *epsp_c = nullptr, *epsp_t = nullptr, *tan = nullptr;
@@ -131,6 +136,12 @@ struct dbfft_ctx_s {
   bool own_stream = false;
   std::string err;
   ncclComm_t comm = nullptr;
+  // peer transport (env->transport = 1): exchange windows, flag window, barrier bookkeeping
+  int peer = 0;
+  PeerBuf pb1, pb2, pbf;
+  long long xpcs = 0;            // chunk stride of the exchange layouts (complex elements)
+  unsigned epoch = 0;            // barriers issued
+  long long read_at[2] = {-1, -1};  // epoch at the last local read of WR / WR2
   std::vector<Slab> slabs;
   double** loc_ptrs = nullptr;  // device array of the slabs' loc pointers (loopback all-reduce)
   // tables (global)
@@ -260,12 +271,18 @@ ColGeom colbase(dbfft_ctx ctx, const cplx* in, cplx* out) {
 //   B  y-pass    [f][zl][y][kx]                       fs = Hs
 //   X2 F2 -> F3  [rank][f][kyl][zl][kx]
 // chunk sizes: nf * nyl * nzl * n1h.
+// chunk stride of the rank-chunked exchange layouts [rank][f][ky_loc][z_loc][kx]: dense, or the
+// granularity-padded chunk of the peer windows
+long long xpcs(dbfft_ctx ctx, const Slab& s, int nf) {
+  return ctx->peer ? ctx->xpcs : (long long)nf * s.nyl * s.nzl * ctx->n1h;
+}
+
 ColGeom geom_I1(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf) {
   ColGeom g = colbase(ctx, in, out);
   const long long n1h = ctx->n1h;
   g.in_fs = s.Hs; g.in_os = (long long)ctx->n3 * n1h; g.in_ps = n1h; g.in_psh = ilog2(ctx->n3); g.in_pcs = 0;
   g.out_fs = (long long)s.nyl * s.nzl * n1h; g.out_os = (long long)s.nzl * n1h; g.out_ps = n1h;
-  g.out_psh = ilog2(s.nzl); g.out_pcs = (long long)nf * s.nyl * s.nzl * n1h;
+  g.out_psh = ilog2(s.nzl); g.out_pcs = xpcs(ctx, s, nf);
   g.ncols = (long long)s.nyl * n1h;
   g.tw = ctx->tw3;
   g.fq = Freq{ctx->xix, s.xiy, ctx->xiz};
@@ -276,7 +293,7 @@ ColGeom geom_I2(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_
   ColGeom g = colbase(ctx, in, out);
   const long long n1h = ctx->n1h;
   g.in_fs = (long long)s.nyl * s.nzl * n1h; g.in_os = n1h; g.in_ps = (long long)s.nzl * n1h;
-  g.in_psh = ilog2(s.nyl); g.in_pcs = (long long)nf_in * s.nyl * s.nzl * n1h;
+  g.in_psh = ilog2(s.nyl); g.in_pcs = xpcs(ctx, s, nf_in);
   g.out_fs = s.Hs; g.out_os = (long long)ctx->n2 * n1h; g.out_ps = n1h; g.out_psh = ilog2(ctx->n2); g.out_pcs = 0;
   g.ncols = (long long)s.nzl * n1h;
   g.tw = ctx->tw2;
@@ -289,7 +306,7 @@ ColGeom geom_F2(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_
   const long long n1h = ctx->n1h;
   g.in_fs = s.Hs; g.in_os = (long long)ctx->n2 * n1h; g.in_ps = n1h; g.in_psh = ilog2(ctx->n2); g.in_pcs = 0;
   g.out_fs = (long long)s.nyl * s.nzl * n1h; g.out_os = n1h; g.out_ps = (long long)s.nzl * n1h;
-  g.out_psh = ilog2(s.nyl); g.out_pcs = (long long)nf_out * s.nyl * s.nzl * n1h;
+  g.out_psh = ilog2(s.nyl); g.out_pcs = xpcs(ctx, s, nf_out);
   g.ncols = (long long)s.nzl * n1h;
   g.tw = ctx->tw2;
   g.fq = Freq{ctx->xix, ctx->xiy, ctx->xiz};
@@ -300,7 +317,7 @@ ColGeom geom_F3(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_
   ColGeom g = colbase(ctx, in, out);
   const long long n1h = ctx->n1h;
   g.in_fs = (long long)s.nyl * s.nzl * n1h; g.in_os = (long long)s.nzl * n1h; g.in_ps = n1h;
-  g.in_psh = ilog2(s.nzl); g.in_pcs = (long long)nf_in * s.nyl * s.nzl * n1h;
+  g.in_psh = ilog2(s.nzl); g.in_pcs = xpcs(ctx, s, nf_in);
   g.out_fs = s.Hs; g.out_os = (long long)ctx->n3 * n1h; g.out_ps = n1h; g.out_psh = ilog2(ctx->n3); g.out_pcs = 0;
   g.ncols = (long long)s.nyl * n1h;
   g.tw = ctx->tw3;
@@ -337,9 +354,35 @@ XGeom xgeom(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out) {
   return g;
 }
 
+dbfft_status peer_barrier(dbfft_ctx ctx) {
+  ProfScope ps(ctx, PK_XCHG);
+  Slab& s = ctx->slabs[0];
+  (void)s;
+  ++ctx->epoch;
+  CK(launch_peer_barrier((unsigned*)ctx->pbf.recv[0], (char*)ctx->pbf.win[0], ctx->pbf.chunk, ctx->P, ctx->rank, ctx->epoch,
+                         ctx->stream));
+  return DBFFT_OK;
+}
+
 dbfft_status run_col(dbfft_ctx ctx, int kind, int prof_id, const ColGeom& g, int N, int* grid = nullptr) {
-  ProfScope ps(ctx, prof_id);
-  CK(launch_col(kind, N, g, ctx->stream, grid));
+  // peer transport across processes: a pass may store into a window only once every rank has
+  // finished reading the receive buffers behind it, i.e. after a barrier that follows the last
+  // read (all ranks issue the same pass sequence, so the local bookkeeping stands for all)
+  const bool guard = ctx->peer && !ctx->loopback;
+  if (guard) {
+    const Slab& s = ctx->slabs[0];
+    const int w = (g.out == s.WS1) ? 0 : (g.out == s.WS2) ? 1 : -1;
+    if (w >= 0 && ctx->read_at[w] >= (long long)ctx->epoch) CKS(peer_barrier(ctx));
+  }
+  {
+    ProfScope ps(ctx, prof_id);
+    CK(launch_col(kind, N, g, ctx->stream, grid));
+  }
+  if (guard) {
+    const Slab& s = ctx->slabs[0];
+    if (g.in == s.WR) ctx->read_at[0] = ctx->epoch;
+    if (g.in == s.WR2) ctx->read_at[1] = ctx->epoch;
+  }
   return DBFFT_OK;
 }
 
@@ -353,6 +396,10 @@ dbfft_status run_x(dbfft_ctx ctx, int kind, int prof_id, const XGeom& g, int* gr
 // all-to-all of equal chunks: slab r sends WA[d*chunk] to rank d, which stores it at WR[r*chunk]
 dbfft_status exchange(dbfft_ctx ctx, long long chunk) {
   if (ctx->P == 1) return DBFFT_OK;
+  if (ctx->peer) {  // the pass already stored into the peers' receive buffers: wait until all have
+    if (ctx->loopback) return DBFFT_OK;  // one stream orders the virtual ranks
+    return peer_barrier(ctx);
+  }
   ProfScope ps(ctx, PK_XCHG);
   const size_t bytes = sizeof(cplx) * chunk;
   if (ctx->loopback) {
@@ -669,7 +716,7 @@ dbfft_status apply_K_slabs(dbfft_ctx ctx, cplx* Slab::*u, cplx* Slab::*f, bool u
   else if (ctx->family == FAM_J2) xkind = X_K_J2;
   else xkind = ctx->tmode ? X_K_FIN_NH : X_K_FIN_TAN;
   const int nf1 = nf_I1(ctx);
-  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_I1F : COL_I1S, PK_I1, geom_I1(ctx, s, s.*u, s.WA, nf1), ctx->n3));
+  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_I1F : COL_I1S, PK_I1, geom_I1(ctx, s, s.*u, s.WS1, nf1), ctx->n3));
   CKS(exchange(ctx, (long long)nf1 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
   for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_I2F : COL_I2S, PK_I2, geom_I2(ctx, s, s.WR, s.WB, nf1), ctx->n2));
   if (ao) ao->grid_x.assign(ctx->slabs.size(), 0);
@@ -682,18 +729,18 @@ dbfft_status apply_K_slabs(dbfft_ctx ctx, cplx* Slab::*u, cplx* Slab::*f, bool u
     if (ao) ao->grid_x[k] = gridx;
   }
   if (front_only) return DBFFT_OK;  // the caller runs the forward tail (PCG: F3 fused with r -= alpha q)
-  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, geom_F2(ctx, s, s.WB, s.WA, 6), ctx->n2));
+  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, geom_F2(ctx, s, s.WB, s.WS2, 6), ctx->n2));
   CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
-  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_F3, geom_F3(ctx, s, s.WR, s.*f, 6), ctx->n3));
+  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_F3, geom_F3(ctx, s, s.WR2, s.*f, 6), ctx->n3));
   return DBFFT_OK;
 }
 
 // forward tail of the rhs: WB holds -sigma spectra (from an X pass) -> F2 -> F3 -> b
 dbfft_status forward_tail(dbfft_ctx ctx) {
   const bool fin = ctx->kin == 9;
-  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, geom_F2(ctx, s, s.WB, s.WA, 6), ctx->n2));
+  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, geom_F2(ctx, s, s.WB, s.WS2, 6), ctx->n2));
   CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
-  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_F3, geom_F3(ctx, s, s.WR, s.b, 6), ctx->n3));
+  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_F3, geom_F3(ctx, s, s.WR2, s.b, 6), ctx->n3));
   return DBFFT_OK;
 }
 
@@ -872,7 +919,7 @@ dbfft_status pcg(dbfft_ctx ctx, const dbfft_opts& o, int* iters_out) {
 
 // F3 geometry of the fused PCG step: q = K p is never stored; r -= alpha q, <r, M r>, <r, r>
 ColGeom geom_F3_update(dbfft_ctx ctx, Slab& s) {
-  ColGeom g5 = geom_F3(ctx, s, s.WR, s.r, 6);
+  ColGeom g5 = geom_F3(ctx, s, s.WR2, s.r, 6);
   g5.dotp = s.r;
   g5.partials = s.part_cg;
   g5.upd = 1;
@@ -910,7 +957,7 @@ dbfft_status pcg_iteration_fused(dbfft_ctx ctx, bool macro, int nb) {
     ProfScope ps(ctx, PK_FIN);
     CK(launch_fin_alpha(s.cg, s.loc, ctx->stream));
   }
-  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, geom_F2(ctx, s, s.WB, s.WA, 6), ctx->n2));
+  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, geom_F2(ctx, s, s.WB, s.WS2, 6), ctx->n2));
   CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
   std::vector<int> g3(ctx->slabs.size(), 0);
   for (size_t j = 0; j < ctx->slabs.size(); ++j) {
@@ -1149,7 +1196,7 @@ dbfft_status constitutive(dbfft_ctx ctx, bool has_in, const double* dF_host, dou
   for (Slab& s : ctx->slabs) CK(cudaMemsetAsync(s.bad, 0x7f, sizeof(int), ctx->stream));
   if (has_in) {
     const int nf1 = nf_I1(ctx);
-    for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_I1F : COL_I1S, PK_I1, geom_I1(ctx, s, s.x, s.WA, nf1), ctx->n3));
+    for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_I1F : COL_I1S, PK_I1, geom_I1(ctx, s, s.x, s.WS1, nf1), ctx->n3));
     CKS(exchange(ctx, (long long)nf1 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
     for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_I2F : COL_I2S, PK_I2, geom_I2(ctx, s, s.WR, s.WB, nf1), ctx->n2));
   }
@@ -1286,16 +1333,19 @@ dbfft_status solve_newton(dbfft_ctx ctx, const double* target, const uint8_t* ma
   return DBFFT_OK;
 }
 
-void free_slab(Slab& s) {
+void free_slab(Slab& s, bool peer) {
   void* ptrs[] = {s.x, s.r, s.p, s.q, s.b, s.u, s.u_c, s.WA, s.WB, s.phase, s.ptable, s.F, s.F_c, s.epsp_c, s.epsp_t, s.tan,
                   s.cg, s.part_x, s.part_cg, s.part_misc, s.loc, s.e_dev, s.bad, s.counts, s.tmp_real};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  if (s.WR && s.WR != s.WA) cudaFree(s.WR);
+  if (!peer && s.WR && s.WR != s.WA) cudaFree(s.WR);
 }
 
 void free_all(dbfft_ctx ctx) {
-  for (Slab& s : ctx->slabs) free_slab(s);
+  for (Slab& s : ctx->slabs) free_slab(s, ctx->peer);
+  peer_free(&ctx->pb1);
+  peer_free(&ctx->pb2);
+  peer_free(&ctx->pbf);
   void* ptrs[] = {ctx->xix, ctx->xiy, ctx->xiz, ctx->tw1, ctx->tw2, ctx->tw3, ctx->loc_ptrs, ctx->trace_dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -1387,8 +1437,11 @@ dbfft_status alloc_slab(dbfft_ctx ctx, Slab& s) {
   CK(cudaMemset(s.u, 0, sizeof(cplx) * v3));
   CK(cudaMemset(s.u_c, 0, sizeof(cplx) * v3));
   CKS(dalloc(ctx, &s.WA, (size_t)6 * s.Hs));
-  if (ctx->P > 1) CKS(dalloc(ctx, &s.WR, (size_t)6 * s.Hs));
-  else s.WR = s.WA;
+  if (ctx->P == 1) s.WR = s.WA;
+  else if (!ctx->peer) CKS(dalloc(ctx, &s.WR, (size_t)6 * s.Hs));
+  // peer transport: WR / WR2 / WS1 / WS2 are mapped by build_peer once all slabs exist
+  s.WS1 = s.WS2 = s.WA;
+  s.WR2 = s.WR;
   CKS(dalloc(ctx, &s.WB, (size_t)ctx->kin * s.Hs));
   CKS(dalloc(ctx, &s.cg, 1));
   int gx = 0;
@@ -1441,6 +1494,45 @@ dbfft_status dbfft_nccl_unique_id(void* out128) {
   return DBFFT_OK;
 }
 
+// peer transport: the two exchange buffers as VMM windows over all ranks (peer.cuh), plus the
+// barrier flags (NCCL mode only: loopback ranks share one stream)
+static int g_peer_seq = 0;
+static dbfft_status build_peer(dbfft_ctx ctx, const void* nccl_id) {
+  std::string err;
+  const Slab& s0 = ctx->slabs[0];
+  const size_t chunk = peer_chunk(sizeof(cplx) * 6 * (size_t)s0.nyl * s0.nzl * ctx->n1h, ctx->device, &err);
+  const size_t fchunk = chunk ? peer_chunk(4096, ctx->device, &err) : 0;
+  bool ok = chunk && fchunk;
+  if (ok && ctx->loopback) {
+    ok = peer_build_loopback(&ctx->pb1, ctx->P, chunk, ctx->device, true, false, &err) &&
+         peer_build_loopback(&ctx->pb2, ctx->P, chunk, ctx->device, true, false, &err);
+  } else if (ok) {
+    // rendezvous tag: a hash of the job's NCCL unique id (equal on all ranks) + a per-process
+    // sequence number (all ranks create their contexts in the same order)
+    unsigned long long h = 1469598103934665603ull;
+    const unsigned char* b = static_cast<const unsigned char*>(nccl_id);
+    for (int i = 0; i < 128; ++i) h = (h ^ b[i]) * 1099511628211ull;
+    char tag[64];
+    snprintf(tag, sizeof(tag), "%016llx-%d", h, g_peer_seq++);
+    ok = peer_build_ipc(&ctx->pbf, ctx->P, ctx->rank, fchunk, ctx->device, false, true, std::string(tag) + "-f", &err) &&
+         peer_build_ipc(&ctx->pb1, ctx->P, ctx->rank, chunk, ctx->device, true, false, std::string(tag) + "-1", &err) &&
+         peer_build_ipc(&ctx->pb2, ctx->P, ctx->rank, chunk, ctx->device, true, false, std::string(tag) + "-2", &err);
+  }
+  if (!ok) {
+    ctx->err = err;
+    return DBFFT_E_CUDA;
+  }
+  ctx->xpcs = (long long)(chunk / sizeof(cplx));
+  for (size_t k = 0; k < ctx->slabs.size(); ++k) {
+    Slab& s = ctx->slabs[k];
+    s.WR = reinterpret_cast<cplx*>(ctx->pb1.recv[k]);
+    s.WS1 = reinterpret_cast<cplx*>(ctx->pb1.win[k]);
+    s.WR2 = reinterpret_cast<cplx*>(ctx->pb2.recv[k]);
+    s.WS2 = reinterpret_cast<cplx*>(ctx->pb2.win[k]);
+  }
+  return DBFFT_OK;
+}
+
 dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinematics, const dbfft_env* env, dbfft_ctx* out) {
   if (!n || !L || !out) {
     g_create_error = "null argument";
@@ -1478,6 +1570,7 @@ dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinemat
   ctx->P = P;
   ctx->loopback = (P > 1 && loopback) ? 1 : 0;
   ctx->rank = ctx->loopback ? 0 : rank;
+  ctx->peer = (P > 1 && env && env->transport == DBFFT_TRANSPORT_PEER) ? 1 : 0;
   memset(ctx->prof_ms, 0, sizeof(ctx->prof_ms));
   memset(ctx->prof_n, 0, sizeof(ctx->prof_n));
   for (int a = 0; a < 9; ++a) ctx->Fbar[a] = ctx->Fbar_c[a] = 0.0;
@@ -1548,6 +1641,7 @@ dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinemat
       return fail(DBFFT_E_NCCL);
     }
   }
+  if (ctx->peer && (s = build_peer(ctx, env->nccl_id)) != DBFFT_OK) return fail(s);
   if (cudaMallocHost(&ctx->h_cg, sizeof(CgDev)) != cudaSuccess || cudaMallocHost(&ctx->h_red, 64 * sizeof(double)) != cudaSuccess ||
       cudaMallocHost(&ctx->h_bad, sizeof(int)) != cudaSuccess) {
     ctx->err = "cudaMallocHost failed";
@@ -1560,6 +1654,89 @@ dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinemat
     return fail(DBFFT_E_CUDA);
   }
   *out = ctx;
+  return DBFFT_OK;
+}
+
+dbfft_status dbfft_fd_allgather(const char* tag, int32_t rank, int32_t world, const int32_t* fds, int32_t nfd,
+                                int32_t* out, int32_t timeout_ms) {
+  if (!tag || !fds || !out || world < 1 || rank < 0 || rank >= world || nfd < 1 || nfd > 16 || timeout_ms < 0) {
+    g_create_error = "fd_allgather: bad arguments";
+    return DBFFT_E_INVALID_ARG;
+  }
+  std::string err;
+  if (fd_allgather(tag, rank, world, fds, nfd, out, timeout_ms, &err) != 0) {
+    g_create_error = err;
+    return DBFFT_E_STATE;
+  }
+  return DBFFT_OK;
+}
+
+// ---------------------------------------------------------------- peer-window probe (tests)
+__global__ void k_peer_fill(unsigned* win, size_t chunk_words, int P, unsigned base, int nwords) {
+  for (int i = threadIdx.x; i < P * nwords; i += blockDim.x) {
+    const int d = i / nwords;
+    win[(size_t)d * chunk_words + i % nwords] = base + d;
+  }
+}
+
+struct dbfft_peer_probe_s {
+  PeerBuf b;
+  int rank = 0, P = 1;
+};
+
+dbfft_status dbfft_peer_probe_open(const char* tag, int32_t rank, int32_t world, int32_t device, void** out) {
+  if (!tag || !out || world < 1 || rank < 0 || rank >= world) {
+    g_create_error = "peer_probe_open: bad arguments";
+    return DBFFT_E_INVALID_ARG;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) {
+    g_create_error = "peer_probe_open: cudaSetDevice";
+    return DBFFT_E_CUDA;
+  }
+  auto* pr = new dbfft_peer_probe_s();
+  pr->rank = rank;
+  pr->P = world;
+  std::string err;
+  const size_t chunk = peer_chunk(4096, device, &err);
+  if (!chunk || !peer_build_ipc(&pr->b, world, rank, chunk, device, true, true, tag, &err)) {
+    g_create_error = err;
+    peer_free(&pr->b);
+    delete pr;
+    return DBFFT_E_CUDA;
+  }
+  // store 1000 rank + d into the first 1024 words of window chunk d (rank d's buffer, chunk rank)
+  k_peer_fill<<<1, 256>>>(reinterpret_cast<unsigned*>(pr->b.win[0]), chunk / 4, world, 1000u * rank, 1024);
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    g_create_error = "peer_probe_open: fill kernel failed";
+    peer_free(&pr->b);
+    delete pr;
+    return DBFFT_E_CUDA;
+  }
+  *out = pr;
+  return DBFFT_OK;
+}
+
+dbfft_status dbfft_peer_probe_check(void* h, int32_t* bad_words) {
+  auto* pr = static_cast<dbfft_peer_probe_s*>(h);
+  if (!pr || !bad_words) return DBFFT_E_INVALID_ARG;
+  std::vector<unsigned> host(1024);
+  int bad = 0;
+  for (int src = 0; src < pr->P; ++src) {
+    if (cudaMemcpy(host.data(), reinterpret_cast<char*>(pr->b.recv[0]) + (size_t)src * pr->b.chunk, 4096,
+                   cudaMemcpyDeviceToHost) != cudaSuccess)
+      return DBFFT_E_CUDA;
+    for (unsigned w : host) bad += (w != 1000u * src + pr->rank);
+  }
+  *bad_words = bad;
+  return DBFFT_OK;
+}
+
+dbfft_status dbfft_peer_probe_close(void* h) {
+  auto* pr = static_cast<dbfft_peer_probe_s*>(h);
+  if (!pr) return DBFFT_E_INVALID_ARG;
+  cudaDeviceSynchronize();
+  peer_free(&pr->b);
+  delete pr;
   return DBFFT_OK;
 }
 
@@ -1876,7 +2053,7 @@ dbfft_status field_to_tmp(dbfft_ctx ctx, int which) {
   }
   // linear: eps = Ebar + sym grad u (Voigt 6 via the inverse passes), sigma = C:eps
   CKS(upload_e(ctx, ctx->Fbar_c));
-  for (Slab& s : ctx->slabs) CKS(run_col(ctx, COL_I1S, PK_OTHER, geom_I1(ctx, s, s.u_c, s.WA, 5), ctx->n3));
+  for (Slab& s : ctx->slabs) CKS(run_col(ctx, COL_I1S, PK_OTHER, geom_I1(ctx, s, s.u_c, s.WS1, 5), ctx->n3));
   CKS(exchange(ctx, (long long)5 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
   for (Slab& s : ctx->slabs) {
     CKS(run_col(ctx, COL_I2S, PK_OTHER, geom_I2(ctx, s, s.WR, s.WB, 5), ctx->n2));
@@ -1931,15 +2108,15 @@ dbfft_status incompat_max(dbfft_ctx ctx, double* result) {
       gx.real_in = s.tmp_real;
       for (int f = 0; f < nf; ++f) gx.real_map[f] = fin ? 3 * row + f : kRowMajorVoigt[f];
       CKS(run_x(ctx, X_REAL_IN + nf, PK_OTHER, gx, nullptr));
-      CKS(run_col(ctx, fin ? COL_YF3 : COL_YF6, PK_OTHER, geom_F2(ctx, s, s.WB, s.WA, nf), ctx->n2));
+      CKS(run_col(ctx, fin ? COL_YF3 : COL_YF6, PK_OTHER, geom_F2(ctx, s, s.WB, s.WS2, nf), ctx->n2));
     }
     CKS(exchange(ctx, chunk));
     for (Slab& s : ctx->slabs) {
-      CKS(run_col(ctx, fin ? COL_ZF3 : COL_ZF6, PK_OTHER, geom_F3(ctx, s, s.WR, s.WB, nf), ctx->n3));
+      CKS(run_col(ctx, fin ? COL_ZF3 : COL_ZF6, PK_OTHER, geom_F3(ctx, s, s.WR2, s.WB, nf), ctx->n3));
       ProfScope ps(ctx, PK_OTHER);
       CK(fin ? launch_curl3(spec(ctx, s), s.WB, ctx->stream) : launch_curlcurl6(spec(ctx, s), s.WB, ctx->stream));
     }
-    for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_ZI3 : COL_ZI6, PK_OTHER, geom_I1(ctx, s, s.WB, s.WA, nf), ctx->n3));
+    for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_ZI3 : COL_ZI6, PK_OTHER, geom_I1(ctx, s, s.WB, s.WS1, nf), ctx->n3));
     CKS(exchange(ctx, chunk));
     for (size_t k = 0; k < ctx->slabs.size(); ++k) {
       Slab& s = ctx->slabs[k];
@@ -1986,11 +2163,11 @@ dbfft_status div_norm(dbfft_ctx ctx, double* norm, double* mean9) {
     CKS(run_x(ctx, X_REAL_IN + nf, PK_OTHER, gx, nullptr));
   }
   // the operator's forward tail: f = -i xi . sigma_hat (positive form, R3) into q
-  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_OTHER, geom_F2(ctx, s, s.WB, s.WA, 6), ctx->n2));
+  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_OTHER, geom_F2(ctx, s, s.WB, s.WS2, 6), ctx->n2));
   CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
   for (size_t k = 0; k < ctx->slabs.size(); ++k) {
     Slab& s = ctx->slabs[k];
-    CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_OTHER, geom_F3(ctx, s, s.WR, s.q, 6), ctx->n3));
+    CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_OTHER, geom_F3(ctx, s, s.WR2, s.q, 6), ctx->n3));
     {
       ProfScope ps(ctx, PK_OTHER);
       CK(launch_specnorm2(spec(ctx, s), s.q, 3, s.part_misc, ctx->stream));
@@ -2025,7 +2202,7 @@ dbfft_status dbfft_get_field(dbfft_ctx ctx, int32_t which, void* out, int32_t ou
     case DBFFT_FIELD_U_HAT:
       return spec_out(ctx, &Slab::u_c, (cplx*)out, k);
     case DBFFT_FIELD_U: {
-      for (Slab& s : ctx->slabs) CKS(run_col(ctx, COL_ZI3, PK_OTHER, geom_I1(ctx, s, s.u_c, s.WA, 3), ctx->n3));
+      for (Slab& s : ctx->slabs) CKS(run_col(ctx, COL_ZI3, PK_OTHER, geom_I1(ctx, s, s.u_c, s.WS1, 3), ctx->n3));
       CKS(exchange(ctx, (long long)3 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
       for (Slab& s : ctx->slabs) {
         CKS(run_col(ctx, COL_YI3, PK_OTHER, geom_I2(ctx, s, s.WR, s.WB, 3), ctx->n2));

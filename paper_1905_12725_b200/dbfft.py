@@ -14,7 +14,10 @@ LIB_PATH = os.path.join(HERE, "libdbfft.so")
 
 class Env(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
-                ("cuda_stream", ctypes.c_void_p), ("device", ctypes.c_int32), ("loopback", ctypes.c_int32)]
+                ("cuda_stream", ctypes.c_void_p), ("device", ctypes.c_int32), ("loopback", ctypes.c_int32),
+                ("transport", ctypes.c_int32)]
+
+TRANSPORTS = {"nccl": 0, "peer": 1}
 
 
 class Material(ctypes.Structure):
@@ -45,7 +48,8 @@ EXPORTS = ["dbfft_create", "dbfft_destroy", "dbfft_last_error", "dbfft_spectral_
            "dbfft_apply_K", "dbfft_apply_K_aug", "dbfft_precond", "dbfft_eval_state", "dbfft_default_opts",
            "dbfft_solve_increment", "dbfft_get_field", "dbfft_profile_enable", "dbfft_profile_read",
            "dbfft_profile_name", "dbfft_profile_count", "dbfft_launch_count", "dbfft_nccl_unique_id",
-           "dbfft_residuals", "dbfft_incompatibility", "dbfft_get_trace"]
+           "dbfft_residuals", "dbfft_incompatibility", "dbfft_get_trace", "dbfft_fd_allgather",
+           "dbfft_peer_probe_open", "dbfft_peer_probe_check", "dbfft_peer_probe_close"]
 
 _lib = None
 
@@ -70,6 +74,11 @@ def load_library(path=None):
     lib.dbfft_create.argtypes = [ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double), I32,
                                  ctypes.POINTER(Env), ctypes.POINTER(P)]
     lib.dbfft_destroy.argtypes = [P]
+    lib.dbfft_fd_allgather.argtypes = [ctypes.c_char_p, I32, I32, ctypes.POINTER(ctypes.c_int32), I32,
+                                       ctypes.POINTER(ctypes.c_int32), I32]
+    lib.dbfft_peer_probe_open.argtypes = [ctypes.c_char_p, I32, I32, I32, ctypes.POINTER(ctypes.c_void_p)]
+    lib.dbfft_peer_probe_check.argtypes = [P, ctypes.POINTER(ctypes.c_int32)]
+    lib.dbfft_peer_probe_close.argtypes = [P]
     lib.dbfft_last_error.argtypes = [P]
     lib.dbfft_last_error.restype = ctypes.c_char_p
     lib.dbfft_spectral_layout.argtypes = [P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
@@ -144,10 +153,11 @@ class DBFFT:
     """One DBFFT context on one CUDA device (include/dbfft.h)."""
 
     def __init__(self, n, L=(1.0, 1.0, 1.0), kinematics="small", device=0, stream=None,
-                 world=1, rank=0, loopback=False, process_group=None):
+                 world=1, rank=0, loopback=False, process_group=None, transport="nccl"):
         """world > 1: slab decomposition (include/dbfft.h "Distribution").  loopback=True keeps
         all `world` virtual ranks in this process; otherwise NCCL, with the unique id broadcast
-        over `process_group` (torch.distributed, any backend)."""
+        over `process_group` (torch.distributed, any backend).  transport: "nccl" (all-to-all
+        exchanges) or "peer" (passes store into the peers' receive buffers, dbfft_env.transport)."""
         import torch
         self.torch = torch
         self.lib = load_library()
@@ -161,7 +171,7 @@ class DBFFT:
         if self.world > 1 and not self.loopback:
             self._nccl_id = nccl_unique_id_broadcast(self.rank, process_group)
         env = Env(self.rank, self.world, ctypes.cast(self._nccl_id, ctypes.c_void_p) if self._nccl_id else None,
-                  ctypes.c_void_p(self.stream.cuda_stream), device, int(self.loopback))
+                  ctypes.c_void_p(self.stream.cuda_stream), device, int(self.loopback), TRANSPORTS[transport])
         h = ctypes.c_void_p()
         st = self.lib.dbfft_create((ctypes.c_int32 * 3)(*self.n), (ctypes.c_double * 3)(*L), self.kin,
                                    ctypes.byref(env), ctypes.byref(h))
