@@ -24,6 +24,9 @@
 #ifndef DBF_X_LRAW
 #define DBF_X_LRAW 192  // target threads per pass_X CTA (lines per CTA = DBF_X_LRAW / threads per line)
 #endif
+#ifndef DBF_X_STAGE_SPEC
+#define DBF_X_STAGE_SPEC 1  // pass_X: stage the input spectra too (else only the per-voxel data)
+#endif
 #ifndef DBF_X_STAGE_IN
 #define DBF_X_STAGE_IN 1
 #endif
@@ -759,7 +762,8 @@ struct XCfg {
   static constexpr size_t SLOTS = sizeof(double) * LPAR * CS * N1;
   // bulk-copy staging needs 16-byte rows: powers of two only (odd lines load directly)
   static constexpr bool STG = S::IN && (N1 & 1) == 0;
-  static constexpr size_t ST_IN = STG ? sizeof(cplx) * LPAR * T::CIN * N1H : 0;
+  static constexpr bool STG_SPEC = STG && DBF_X_STAGE_SPEC;
+  static constexpr size_t ST_IN = STG_SPEC ? sizeof(cplx) * LPAR * T::CIN * N1H : 0;
   static constexpr size_t ST_TAN = STG ? sizeof(double) * LPAR * S::NTAN * N1 : 0;
   static constexpr size_t ST_PH = (STG && S::PH) ? ((sizeof(uint16_t) * LPAR * N1 + 15) & ~size_t(15)) : 0;
   static constexpr size_t SMEM = SLOTS + ST_IN + ST_TAN + ST_PH + 16;  // + 2 mbarriers
@@ -829,7 +833,8 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
   typedef XTraits<KIND> T;
   typedef XStage<KIND> S;
   constexpr int C = CF::C, CS = CF::CS, TPJ = CF::TPJ, NP = CF::NP, LPAR = CF::LPAR, PX = CF::PX;
-  constexpr bool SIN = CF::STG;  // stage inputs / tangent with bulk copies
+  constexpr bool SIN = CF::STG;  // stage per-voxel data (and the spectra: SSP) with bulk copies
+  constexpr bool SSP = CF::STG_SPEC;
   extern __shared__ __align__(16) double real[];
   cplx* cx = reinterpret_cast<cplx*>(real);
   unsigned char* sb = reinterpret_cast<unsigned char*>(real);
@@ -865,7 +870,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
     }
     __syncthreads();
     if (t == 0 && (long long)blockIdx.x < ngroups) {
-      x_issue_in<N1, KIND>(g, blockIdx.x, st_in, &bars[0]);
+      if (SSP) x_issue_in<N1, KIND>(g, blockIdx.x, st_in, &bars[0]);
       if (STAGE_TAN) x_issue_tan<N1, KIND>(g, blockIdx.x, st_tan, st_ph, &bars[1]);
     }
   }
@@ -877,7 +882,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
     const long long nxt = grp + gridDim.x;
     // ------------------------------------------------------------ inverse (C2R) of pairs
     if (do_in) {
-      if (SIN) mbar_wait(&bars[0], it & 1);
+      if (SSP) mbar_wait(&bars[0], it & 1);
       cplx a[PX];
 #pragma unroll
       for (int s = 0; s < PX; ++s) {
@@ -886,7 +891,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
         const int kk = lo ? k : N1 - k;
         cplx A = make_double2(0, 0), B = make_double2(0, 0);
         if (lvalid && fa < cin) {
-          if (SIN) {
+          if (SSP) {
             A = st_in[(l * T::CIN + fa) * CF::N1H + kk];
             if (fb < cin) B = st_in[(l * T::CIN + fb) * CF::N1H + kk];
           } else {
@@ -899,7 +904,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
         // Y_k = A_k + i B_k (k <= N/2);  conj(A_{N-k}) + i conj(B_{N-k}) otherwise
         a[s] = lo ? make_double2(A.x - B.y, A.y + B.x) : make_double2(A.x + B.y, B.x - A.y);
       }
-      if (SIN) {
+      if (SSP) {
         __syncthreads();  // everyone has read the input stage
         if (t == 0 && nxt < ngroups) {
           fence_proxy_async();
