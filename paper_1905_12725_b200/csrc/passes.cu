@@ -1568,8 +1568,9 @@ static int col_prog_span(const TProg& p) {
 }
 
 template <int KIND, bool DOT>
-struct ColRing {  // ring depth: 3 slots unless the program's live span needs more (F3S + dot: 4)
-  static constexpr int R = (KIND == COL_F3S && DOT) ? 4 : DBF_COL_R;
+struct ColRing {  // ring depth: 3 slots; small-strain F3 (two-term outputs from 6 inputs) takes 4
+  // (B200: 512^3 3.35 -> 3.26 ms, 256^3 0.400 -> 0.392 ms; R = 4 everywhere was slower overall)
+  static constexpr int R = (KIND == COL_F3S) ? 4 : DBF_COL_R;
 };
 
 template <int N, int KIND, bool DOT, bool UPD = false>

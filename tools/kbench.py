@@ -1,6 +1,6 @@
 """Kernel-level timing of the operator passes (library CUDA-event profiler, no ncu).
 
-    python tools/kbench.py [n] [reps] [small|finite]
+    python tools/kbench.py [n] [reps] [small|finite|j2]
 
 Prints per-pass average ms and GB/s against the SURVEY 8(d) model bytes of each pass."""
 import json
@@ -18,9 +18,11 @@ reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 kin = sys.argv[3] if len(sys.argv) > 3 else "finite"
 if kin == "finite":
     cfg = configs.c4(n=n, radius_vox=max(1, round(10 * n / 256)))
+elif kin == "j2":  # c5's J2-Perzyna polycrystal (elastic tangent right after set_phases)
+    cfg = configs.c5(n=n)
 else:
     cfg = configs.c3(n=n)
-ctx = dbfft.DBFFT(cfg["n"], kinematics=kin)
+ctx = dbfft.DBFFT(cfg["n"], kinematics="finite" if kin == "finite" else "small")
 ctx.set_phases(cfg["phase"], cfg["materials"])
 g = torch.Generator(device="cuda").manual_seed(0)
 x = torch.randn((3, n, n, n), dtype=torch.float64, device="cuda", generator=g)
