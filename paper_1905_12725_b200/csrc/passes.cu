@@ -27,6 +27,10 @@
 #ifndef DBF_X_STAGE_SPEC
 #define DBF_X_STAGE_SPEC 1  // pass_X: stage the input spectra too (else only the per-voxel data)
 #endif
+#ifndef DBF_X_STAGE_TAN_J2
+#define DBF_X_STAGE_TAN_J2 0  // pass_X J2 kind: stage the 8 per-voxel tangent doubles (1), or load
+                              // them in the voxel loop and run 4 CTAs/SM (0; B200 512^3: 7.89 -> 7.08 ms)
+#endif
 #ifndef DBF_X_STAGE_IN
 #define DBF_X_STAGE_IN 1
 #endif
@@ -741,7 +745,7 @@ DBF_DEV int x_red_slot(int f) {
 template <int KIND>
 struct XStage {
   static constexpr bool IN = DBF_X_STAGE_IN && (KIND == X_K_SMALL_PHASE || KIND == X_K_J2 || KIND == X_K_FIN_TAN || KIND == X_K_FIN_NH);
-  static constexpr int NTAN = (KIND == X_K_J2) ? 8 : (KIND == X_K_FIN_NH) ? 10 : 0;  // staged per-voxel doubles
+  static constexpr int NTAN = (KIND == X_K_J2) ? (DBF_X_STAGE_TAN_J2 ? 8 : 0) : (KIND == X_K_FIN_NH) ? 10 : 0;  // staged per-voxel doubles
   static constexpr bool PH = (KIND == X_K_SMALL_PHASE || KIND == X_K_J2 || KIND == X_K_FIN_NH);
 };
 
@@ -767,7 +771,7 @@ struct XCfg {
   static constexpr size_t ST_TAN = STG ? sizeof(double) * LPAR * S::NTAN * N1 : 0;
   static constexpr size_t ST_PH = (STG && S::PH) ? ((sizeof(uint16_t) * LPAR * N1 + 15) & ~size_t(15)) : 0;
   static constexpr size_t SMEM = SLOTS + ST_IN + ST_TAN + ST_PH + 16;  // + 2 mbarriers
-  static constexpr int MINB = (THREADS <= 192) ? DBF_X_MINB : 2;
+  static constexpr int MINB = (KIND == X_K_J2 && !DBF_X_STAGE_TAN_J2) ? 4 : (THREADS <= 192) ? DBF_X_MINB : 2;
 };
 
 // ---- bulk async copy (TMA engine) + mbarrier helpers ------------------------------------------
@@ -956,8 +960,8 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
       long long ts;
       int ph;
       if (SIN && STAGE_TAN) {
-        tp = st_tan + vv;
-        ts = LPAR * N1;
+        tp = (S::NTAN > 0) ? st_tan + vv : (g.tan ? g.tan + v : nullptr);
+        ts = (S::NTAN > 0) ? (long long)LPAR * N1 : g.nvox;
         ph = S::PH ? (int)st_ph[vv] : 0;
       } else {
         tp = g.tan ? g.tan + v : nullptr;
