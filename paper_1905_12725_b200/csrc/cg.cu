@@ -11,7 +11,12 @@
 namespace {
 
 constexpr int BLK = 256;
-constexpr int NBLK = 148 * 4;
+// grid-stride kernels run whole waves (a partial second wave — a 4-per-SM grid at 3 resident
+// CTAs per SM — made k_cg_update 1.5x slower, B200 512^3): 3 CTAs of 256 per SM (<= 85
+// registers, no spills); k_cg_direction holds 2 (94 registers; 3 would spill) and runs two
+// full waves of them (measured a little faster than one)
+constexpr int NBLK = 148 * 3;
+constexpr int NBLK_DIR = 148 * 4;
 
 
 // z = A^-1 r with A = xi.Cbar.xi (symmetric 3x3), 0 on the null set Z (R4)
@@ -41,7 +46,7 @@ DBF_DEV void block_store(double (&v)[NV], double* partials) {
   }
 }
 
-__global__ void __launch_bounds__(BLK) k_precond(SpecGeom g, PrecQ Q, const cplx* __restrict__ r, cplx* __restrict__ z) {
+__global__ void __launch_bounds__(BLK, NBLK / 148) k_precond(SpecGeom g, PrecQ Q, const cplx* __restrict__ r, cplx* __restrict__ z) {
   for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < g.Hs; i += (long long)gridDim.x * BLK) {
     Pt p = point(g, i);
     cplx rv[3] = {__ldg(r + i), __ldg(r + g.Hs + i), __ldg(r + 2 * g.Hs + i)};
@@ -54,7 +59,7 @@ __global__ void __launch_bounds__(BLK) k_precond(SpecGeom g, PrecQ Q, const cplx
 }
 
 // p = M r ; partials (<r, p>, <r, r>)
-__global__ void __launch_bounds__(BLK) k_cg_init(SpecGeom g, PrecQ Q, const cplx* __restrict__ r, cplx* __restrict__ pv, double* partials) {
+__global__ void __launch_bounds__(BLK, NBLK / 148) k_cg_init(SpecGeom g, PrecQ Q, const cplx* __restrict__ r, cplx* __restrict__ pv, double* partials) {
   double acc[2] = {0.0, 0.0};
   for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < g.Hs; i += (long long)gridDim.x * BLK) {
     Pt p = point(g, i);
@@ -74,21 +79,24 @@ __global__ void __launch_bounds__(BLK) k_cg_init(SpecGeom g, PrecQ Q, const cplx
 // x += alpha p ; r -= alpha q ; z = M r ; partials (<r, z>, <r, r>)
 // r -= alpha q, z = M r on the fly, partial <r,z>, <r,r> (x += alpha p is deferred to the
 // direction kernel, which reads p anyway: 3 vector transfers here instead of 6)
-__global__ void __launch_bounds__(BLK) k_cg_update(SpecGeom g, PrecQ Q, const CgDev* __restrict__ cg, cplx* __restrict__ r,
+__global__ void __launch_bounds__(BLK, NBLK / 148) k_cg_update(SpecGeom g, PrecQ Q, const CgDev* __restrict__ cg, cplx* __restrict__ r,
                                                    const cplx* __restrict__ qv, double* partials) {
   if (cg->converged | cg->breakdown) return;
   const double alpha = cg->alpha;
   double acc[2] = {0.0, 0.0};
   for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < g.Hs; i += (long long)gridDim.x * BLK) {
-    Pt p = point(g, i);
-    cplx rv[3];
+    cplx rv[3], qj[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {  // every load of the point in flight before any arithmetic
+      rv[c] = r[c * g.Hs + i];
+      qj[c] = __ldg(qv + c * g.Hs + i);
+    }
+    const Pt p = point(g, i);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const long long j = c * g.Hs + i;
-      cplx rj = r[j], qj = __ldg(qv + j);
-      rj.x = fma(-alpha, qj.x, rj.x); rj.y = fma(-alpha, qj.y, rj.y);
-      r[j] = rj;
-      rv[c] = rj;
+      rv[c].x = fma(-alpha, qj[c].x, rv[c].x);
+      rv[c].y = fma(-alpha, qj[c].y, rv[c].y);
+      r[c * g.Hs + i] = rv[c];
     }
     cplx zv[3];
     apply_M(Q, p, rv, zv);
@@ -134,7 +142,7 @@ DBF_DEV void cg_direction_body(const SpecGeom& g, const PrecQ& Q, double alpha, 
   }
 }
 
-__global__ void __launch_bounds__(BLK) k_cg_direction(SpecGeom g, PrecQ Q, const CgDev* __restrict__ cg, cplx* __restrict__ x,
+__global__ void __launch_bounds__(BLK, 2) k_cg_direction(SpecGeom g, PrecQ Q, const CgDev* __restrict__ cg, cplx* __restrict__ x,
                                                       cplx* __restrict__ pv, const cplx* __restrict__ r) {
   if (cg->breakdown) return;
   const bool do_x = cg->xphase != 0, do_p = cg->converged == 0;
@@ -148,7 +156,7 @@ __global__ void k_fin_x(CgDev* cg) {
 }
 
 // r = b - Ax ; partial <r, r>
-__global__ void __launch_bounds__(BLK) k_true_residual(SpecGeom g, const cplx* __restrict__ b, const cplx* __restrict__ ax,
+__global__ void __launch_bounds__(BLK, NBLK / 148) k_true_residual(SpecGeom g, const cplx* __restrict__ b, const cplx* __restrict__ ax,
                                                        cplx* __restrict__ r, double* partials) {
   double acc[1] = {0.0};
   for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < g.Hs; i += (long long)gridDim.x * BLK) {
@@ -165,7 +173,7 @@ __global__ void __launch_bounds__(BLK) k_true_residual(SpecGeom g, const cplx* _
   block_store<1>(acc, partials);
 }
 
-__global__ void __launch_bounds__(BLK) k_axpy(SpecGeom g, cplx* __restrict__ y, const cplx* __restrict__ x, double a) {
+__global__ void __launch_bounds__(BLK, NBLK / 148) k_axpy(SpecGeom g, cplx* __restrict__ y, const cplx* __restrict__ x, double a) {
   for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < 3 * g.Hs; i += (long long)gridDim.x * BLK) {
     cplx xv = __ldg(x + i), yv = y[i];
     y[i] = make_double2(fma(a, xv.x, yv.x), fma(a, xv.y, yv.y));
@@ -379,7 +387,7 @@ cudaError_t launch_cg_update(const SpecGeom& g, const PrecQ& q, CgDev* cg, cplx*
   return cudaGetLastError();
 }
 cudaError_t launch_cg_direction(const SpecGeom& g, const PrecQ& q, const CgDev* cg, cplx* x, cplx* p, const cplx* r, cudaStream_t s) {
-  k_cg_direction<<<NBLK, BLK, 0, s>>>(g, q, cg, x, p, r);
+  k_cg_direction<<<NBLK_DIR, BLK, 0, s>>>(g, q, cg, x, p, r);
   return cudaGetLastError();
 }
 cudaError_t launch_fin_x(CgDev* cg, cudaStream_t s) {

@@ -14,10 +14,10 @@ import torch  # noqa: E402
 from paper_1905_12725_b200 import dbfft  # noqa: E402
 from synth import configs  # noqa: E402
 
-names = [a for a in sys.argv[1:] if not a.startswith("--")] or ["c1", "c2", "c3", "c4", "c5"]
 incs = None
 if "--incs" in sys.argv:
     incs = int(sys.argv[sys.argv.index("--incs") + 1])
+names = [a for a in sys.argv[1:] if not a.startswith("--") and a != str(incs)] or ["c1", "c2", "c3", "c4", "c5"]
 for name in names:
     t0 = time.perf_counter()
     cfg = configs.CONFIGS[name]()
