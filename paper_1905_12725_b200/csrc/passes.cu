@@ -1493,6 +1493,9 @@ static cudaError_t launch_col_n(int kind, const ColGeom& g, cudaStream_t s) {
 #ifndef DBF_TMA_PROMO
 #define DBF_TMA_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
 #endif
+#ifndef DBF_REG512_MASK
+#define DBF_REG512_MASK 0  // bit k: column kind k at N = 512 takes the register-pipelined kernel
+#endif
 #ifndef DBF_COL_R
 #define DBF_COL_R 3
 #endif
@@ -1658,7 +1661,8 @@ cudaError_t launch_col(int kind, int N, const ColGeom& g, cudaStream_t s, int* g
   cudaError_t e = cudaErrorNotSupported;
   // N = 512 y-forward passes write rows 2 MB apart (the ky stride of [f][ky][z][kx] at 512^2): the
   // TMA store path ran them at 2.2 TB/s against 4 TB/s for direct stores (B200, kbench 512^3)
-  const bool far_store = N == 512 && (kind == COL_F2S || kind == COL_F2F || kind == COL_YF3 || kind == COL_YF6);
+  const bool far_store = N == 512 && (kind == COL_F2S || kind == COL_F2F || kind == COL_YF3 || kind == COL_YF6 ||
+                                       ((DBF_REG512_MASK >> kind) & 1));
   if (N == 512 && !far_store) e = launch_col_tma<512>(kind, g, s, grid_out);
   else if (N == 256) e = launch_col_tma<256>(kind, g, s, grid_out);
   else if (N == 128) e = launch_col_tma<128>(kind, g, s, grid_out);
