@@ -240,6 +240,11 @@ def gpu_arm(args):
         torch.cuda.synchronize()
         phase_host = torch.from_numpy(np.ascontiguousarray(phase, dtype=np.uint16).view(np.int16)).pin_memory().numpy().view(np.uint16)
         u_host = torch.empty((3,) + tuple(phase.shape), dtype=torch.float64, pin_memory=True).numpy()
+        # untimed warm-up of the calls only this leg makes (the library's real-space scratch for
+        # get_field is allocated on first use; lazily loaded kernels load on first launch)
+        ctx.set_phases(phase_host, cfg["materials"])
+        ctx.get_field(dbfft.FIELD_U, out=u_host)
+        torch.cuda.synchronize()
         h2d = d2h = 0
         e_iters = 0
         k = 0
