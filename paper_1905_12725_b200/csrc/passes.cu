@@ -31,6 +31,13 @@
 #define DBF_X_STAGE_TAN_J2 0  // pass_X J2 kind: stage the 8 per-voxel tangent doubles (1), or load
                               // them in the voxel loop and run 4 CTAs/SM (0; B200 512^3: 7.89 -> 7.08 ms)
 #endif
+#ifndef DBF_X_STAGE_TAN_NH
+#define DBF_X_STAGE_TAN_NH 0  // pass_X compact neo-Hookean kind: stage the 10 per-voxel tangent doubles (1),
+                              // or load them in the voxel loop at 4 CTAs/SM (0; B200 256^3: 1.120 -> 1.098 ms)
+#endif
+#ifndef DBF_X_MINB_NOTAN
+#define DBF_X_MINB_NOTAN 4  // CTAs per SM of the pass_X kinds that load their tangent in the voxel loop
+#endif
 #ifndef DBF_X_STAGE_IN
 #define DBF_X_STAGE_IN 1
 #endif
@@ -745,7 +752,7 @@ DBF_DEV int x_red_slot(int f) {
 template <int KIND>
 struct XStage {
   static constexpr bool IN = DBF_X_STAGE_IN && (KIND == X_K_SMALL_PHASE || KIND == X_K_J2 || KIND == X_K_FIN_TAN || KIND == X_K_FIN_NH);
-  static constexpr int NTAN = (KIND == X_K_J2) ? (DBF_X_STAGE_TAN_J2 ? 8 : 0) : (KIND == X_K_FIN_NH) ? 10 : 0;  // staged per-voxel doubles
+  static constexpr int NTAN = (KIND == X_K_J2) ? (DBF_X_STAGE_TAN_J2 ? 8 : 0) : (KIND == X_K_FIN_NH) ? (DBF_X_STAGE_TAN_NH ? 10 : 0) : 0;  // staged per-voxel doubles
   static constexpr bool PH = (KIND == X_K_SMALL_PHASE || KIND == X_K_J2 || KIND == X_K_FIN_NH);
 };
 
@@ -771,7 +778,9 @@ struct XCfg {
   static constexpr size_t ST_TAN = STG ? sizeof(double) * LPAR * S::NTAN * N1 : 0;
   static constexpr size_t ST_PH = (STG && S::PH) ? ((sizeof(uint16_t) * LPAR * N1 + 15) & ~size_t(15)) : 0;
   static constexpr size_t SMEM = SLOTS + ST_IN + ST_TAN + ST_PH + 16;  // + 2 mbarriers
-  static constexpr int MINB = (KIND == X_K_J2 && !DBF_X_STAGE_TAN_J2) ? 4 : (THREADS <= 192) ? DBF_X_MINB : 2;
+  static constexpr int MINB = ((KIND == X_K_J2 && !DBF_X_STAGE_TAN_J2) || (KIND == X_K_FIN_NH && !DBF_X_STAGE_TAN_NH))
+                                   ? DBF_X_MINB_NOTAN
+                                   : (THREADS <= 192) ? DBF_X_MINB : 2;
 };
 
 // ---- bulk async copy (TMA engine) + mbarrier helpers ------------------------------------------
