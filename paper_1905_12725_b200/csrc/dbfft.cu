@@ -104,6 +104,7 @@ struct Slab {
   int rank = 0;
   int nyl = 0, nzl = 0, ky0 = 0, z0 = 0;
   long long Hs = 0;       // complex points per field (= n1h * nyl * n3 = n1h * n2 * nzl)
+  long long Hsp = 0;      // the same with the padded kx pitch of the intermediate layouts (kxp)
   long long Nloc = 0;     // voxels in the z-slab
   long long nlines = 0;   // x lines in the z-slab
   const double* xiy = nullptr;  // xi_y of the local ky slab (offset into the global table)
@@ -127,6 +128,7 @@ struct Slab {
 
 struct dbfft_ctx_s {
   int n1, n2, n3, n1h;
+  int kxp;  // kx pitch of the intermediate layouts (X1, B, X2): n1h, or rounded up to 8 (DBFFT_KX_PAD=1)
   double L[3];
   int kin;  // 6 or 9
   long long N;  // global voxels
@@ -266,22 +268,23 @@ ColGeom colbase(dbfft_ctx ctx, const cplx* in, cplx* out) {
 }
 
 // layouts (complex elements, per slab; P = 1 reduces every one of them to the plain layouts):
-//   S  spectral  [f][kyl][kz][kx]                     fs = Hs
+//   S  spectral  [f][kyl][kz][kx]                     fs = Hs   (kx dense: the API layout)
 //   X1 I1 -> I2  [rank][f][kyl][zl][kx]  (sender: rank = destination, receiver: rank = source)
-//   B  y-pass    [f][zl][y][kx]                       fs = Hs
+//   B  y-pass    [f][zl][y][kx]                       fs = Hsp
 //   X2 F2 -> F3  [rank][f][kyl][zl][kx]
-// chunk sizes: nf * nyl * nzl * n1h.
+// X1, B, X2 rows have the padded kx pitch kxp; chunk sizes nf * nyl * nzl * kxp.
 // chunk stride of the rank-chunked exchange layouts [rank][f][ky_loc][z_loc][kx]: dense, or the
 // granularity-padded chunk of the peer windows
 long long xpcs(dbfft_ctx ctx, const Slab& s, int nf) {
-  return ctx->peer ? ctx->xpcs : (long long)nf * s.nyl * s.nzl * ctx->n1h;
+  return ctx->peer ? ctx->xpcs : (long long)nf * s.nyl * s.nzl * ctx->kxp;
 }
 
 ColGeom geom_I1(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf) {
   ColGeom g = colbase(ctx, in, out);
   const long long n1h = ctx->n1h;
+  const long long kxp = ctx->kxp;
   g.in_fs = s.Hs; g.in_os = (long long)ctx->n3 * n1h; g.in_ps = n1h; g.in_psh = ilog2(ctx->n3); g.in_pcs = 0;
-  g.out_fs = (long long)s.nyl * s.nzl * n1h; g.out_os = (long long)s.nzl * n1h; g.out_ps = n1h;
+  g.out_fs = (long long)s.nyl * s.nzl * kxp; g.out_os = (long long)s.nzl * kxp; g.out_ps = kxp;
   g.out_psh = ilog2(s.nzl); g.out_pcs = xpcs(ctx, s, nf);
   g.ncols = (long long)s.nyl * n1h;
   g.tw = ctx->tw3;
@@ -292,9 +295,10 @@ ColGeom geom_I1(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf)
 ColGeom geom_I2(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_in) {
   ColGeom g = colbase(ctx, in, out);
   const long long n1h = ctx->n1h;
-  g.in_fs = (long long)s.nyl * s.nzl * n1h; g.in_os = n1h; g.in_ps = (long long)s.nzl * n1h;
+  const long long kxp = ctx->kxp;
+  g.in_fs = (long long)s.nyl * s.nzl * kxp; g.in_os = kxp; g.in_ps = (long long)s.nzl * kxp;
   g.in_psh = ilog2(s.nyl); g.in_pcs = xpcs(ctx, s, nf_in);
-  g.out_fs = s.Hs; g.out_os = (long long)ctx->n2 * n1h; g.out_ps = n1h; g.out_psh = ilog2(ctx->n2); g.out_pcs = 0;
+  g.out_fs = s.Hsp; g.out_os = (long long)ctx->n2 * kxp; g.out_ps = kxp; g.out_psh = ilog2(ctx->n2); g.out_pcs = 0;
   g.ncols = (long long)s.nzl * n1h;
   g.tw = ctx->tw2;
   g.fq = Freq{ctx->xix, ctx->xiy, ctx->xiz};
@@ -304,8 +308,9 @@ ColGeom geom_I2(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_
 ColGeom geom_F2(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_out) {
   ColGeom g = colbase(ctx, in, out);
   const long long n1h = ctx->n1h;
-  g.in_fs = s.Hs; g.in_os = (long long)ctx->n2 * n1h; g.in_ps = n1h; g.in_psh = ilog2(ctx->n2); g.in_pcs = 0;
-  g.out_fs = (long long)s.nyl * s.nzl * n1h; g.out_os = n1h; g.out_ps = (long long)s.nzl * n1h;
+  const long long kxp = ctx->kxp;
+  g.in_fs = s.Hsp; g.in_os = (long long)ctx->n2 * kxp; g.in_ps = kxp; g.in_psh = ilog2(ctx->n2); g.in_pcs = 0;
+  g.out_fs = (long long)s.nyl * s.nzl * kxp; g.out_os = kxp; g.out_ps = (long long)s.nzl * kxp;
   g.out_psh = ilog2(s.nyl); g.out_pcs = xpcs(ctx, s, nf_out);
   g.ncols = (long long)s.nzl * n1h;
   g.tw = ctx->tw2;
@@ -316,7 +321,8 @@ ColGeom geom_F2(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_
 ColGeom geom_F3(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_in) {
   ColGeom g = colbase(ctx, in, out);
   const long long n1h = ctx->n1h;
-  g.in_fs = (long long)s.nyl * s.nzl * n1h; g.in_os = (long long)s.nzl * n1h; g.in_ps = n1h;
+  const long long kxp = ctx->kxp;
+  g.in_fs = (long long)s.nyl * s.nzl * kxp; g.in_os = (long long)s.nzl * kxp; g.in_ps = kxp;
   g.in_psh = ilog2(s.nzl); g.in_pcs = xpcs(ctx, s, nf_in);
   g.out_fs = s.Hs; g.out_os = (long long)ctx->n3 * n1h; g.out_ps = n1h; g.out_psh = ilog2(ctx->n3); g.out_pcs = 0;
   g.ncols = (long long)s.nyl * n1h;
@@ -331,8 +337,9 @@ XGeom xgeom(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out) {
   memset(&g, 0, sizeof(g));
   g.in = in;
   g.out = out;
-  g.fs_in = g.fs_out = s.Hs;
+  g.fs_in = g.fs_out = s.Hsp;
   g.n1h = ctx->n1h;
+  g.kxp = ctx->kxp;
   g.n1 = ctx->n1;
   g.nlines = s.nlines;
   g.tw = ctx->tw1;
@@ -717,7 +724,7 @@ dbfft_status apply_K_slabs(dbfft_ctx ctx, cplx* Slab::*u, cplx* Slab::*f, bool u
   else xkind = ctx->tmode ? X_K_FIN_NH : X_K_FIN_TAN;
   const int nf1 = nf_I1(ctx);
   for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_I1F : COL_I1S, PK_I1, geom_I1(ctx, s, s.*u, s.WS1, nf1), ctx->n3));
-  CKS(exchange(ctx, (long long)nf1 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
+  CKS(exchange(ctx, (long long)nf1 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->kxp));
   for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_I2F : COL_I2S, PK_I2, geom_I2(ctx, s, s.WR, s.WB, nf1), ctx->n2));
   if (ao) ao->grid_x.assign(ctx->slabs.size(), 0);
   for (size_t k = 0; k < ctx->slabs.size(); ++k) {
@@ -730,7 +737,7 @@ dbfft_status apply_K_slabs(dbfft_ctx ctx, cplx* Slab::*u, cplx* Slab::*f, bool u
   }
   if (front_only) return DBFFT_OK;  // the caller runs the forward tail (PCG: F3 fused with r -= alpha q)
   for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, geom_F2(ctx, s, s.WB, s.WS2, 6), ctx->n2));
-  CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
+  CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->kxp));
   for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_F3, geom_F3(ctx, s, s.WR2, s.*f, 6), ctx->n3));
   return DBFFT_OK;
 }
@@ -739,7 +746,7 @@ dbfft_status apply_K_slabs(dbfft_ctx ctx, cplx* Slab::*u, cplx* Slab::*f, bool u
 dbfft_status forward_tail(dbfft_ctx ctx) {
   const bool fin = ctx->kin == 9;
   for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, geom_F2(ctx, s, s.WB, s.WS2, 6), ctx->n2));
-  CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
+  CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->kxp));
   for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_F3, geom_F3(ctx, s, s.WR2, s.b, 6), ctx->n3));
   return DBFFT_OK;
 }
@@ -958,7 +965,7 @@ dbfft_status pcg_iteration_fused(dbfft_ctx ctx, bool macro, int nb) {
     CK(launch_fin_alpha(s.cg, s.loc, ctx->stream));
   }
   for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, geom_F2(ctx, s, s.WB, s.WS2, 6), ctx->n2));
-  CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
+  CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->kxp));
   std::vector<int> g3(ctx->slabs.size(), 0);
   for (size_t j = 0; j < ctx->slabs.size(); ++j) {
     Slab& s = ctx->slabs[j];
@@ -1197,7 +1204,7 @@ dbfft_status constitutive(dbfft_ctx ctx, bool has_in, const double* dF_host, dou
   if (has_in) {
     const int nf1 = nf_I1(ctx);
     for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_I1F : COL_I1S, PK_I1, geom_I1(ctx, s, s.x, s.WS1, nf1), ctx->n3));
-    CKS(exchange(ctx, (long long)nf1 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
+    CKS(exchange(ctx, (long long)nf1 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->kxp));
     for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_I2F : COL_I2S, PK_I2, geom_I2(ctx, s, s.WR, s.WB, nf1), ctx->n2));
   }
   std::vector<int> grids(ctx->slabs.size());
@@ -1436,13 +1443,13 @@ dbfft_status alloc_slab(dbfft_ctx ctx, Slab& s) {
   for (cplx** v : vecs) CKS(dalloc(ctx, v, v3));
   CK(cudaMemset(s.u, 0, sizeof(cplx) * v3));
   CK(cudaMemset(s.u_c, 0, sizeof(cplx) * v3));
-  CKS(dalloc(ctx, &s.WA, (size_t)6 * s.Hs));
+  CKS(dalloc(ctx, &s.WA, (size_t)6 * s.Hsp));
   if (ctx->P == 1) s.WR = s.WA;
-  else if (!ctx->peer) CKS(dalloc(ctx, &s.WR, (size_t)6 * s.Hs));
+  else if (!ctx->peer) CKS(dalloc(ctx, &s.WR, (size_t)6 * s.Hsp));
   // peer transport: WR / WR2 / WS1 / WS2 are mapped by build_peer once all slabs exist
   s.WS1 = s.WS2 = s.WA;
   s.WR2 = s.WR;
-  CKS(dalloc(ctx, &s.WB, (size_t)ctx->kin * s.Hs));
+  CKS(dalloc(ctx, &s.WB, (size_t)ctx->kin * s.Hsp));
   CKS(dalloc(ctx, &s.cg, 1));
   int gx = 0;
   for (int k = 0; k < X_REAL_OUT; ++k) gx = std::max(gx, x_grid(k, ctx->n1, s.nlines));
@@ -1500,7 +1507,7 @@ static int g_peer_seq = 0;
 static dbfft_status build_peer(dbfft_ctx ctx, const void* nccl_id) {
   std::string err;
   const Slab& s0 = ctx->slabs[0];
-  const size_t chunk = peer_chunk(sizeof(cplx) * 6 * (size_t)s0.nyl * s0.nzl * ctx->n1h, ctx->device, &err);
+  const size_t chunk = peer_chunk(sizeof(cplx) * 6 * (size_t)s0.nyl * s0.nzl * ctx->kxp, ctx->device, &err);
   const size_t fchunk = chunk ? peer_chunk(4096, ctx->device, &err) : 0;
   bool ok = chunk && fchunk;
   if (ok && ctx->loopback) {
@@ -1564,6 +1571,14 @@ dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinemat
   ctx->n2 = n[1];
   ctx->n3 = n[2];
   ctx->n1h = n[0] / 2 + 1;
+  {
+    // DBFFT_KX_PAD=1: 128-byte aligned rows (n1h rounded up to 8) in the intermediate layouts.
+    // The strided-tile membench gained 6 % from it (4.65 -> 4.93 TB/s at 256^3) but the passes
+    // did not (256^3 finite apply_K 2.732 ms either way; 512^3 F2 2.88 -> 3.20 ms), so the
+    // default is the dense pitch; the full GPU suite passes with either.
+    const char* e = getenv("DBFFT_KX_PAD");
+    ctx->kxp = (e && e[0] == '1') ? (ctx->n1h + 7) / 8 * 8 : ctx->n1h;
+  }
   for (int a = 0; a < 3; ++a) ctx->L[a] = L[a];
   ctx->kin = kinematics;
   ctx->N = (long long)n[0] * n[1] * n[2];
@@ -1622,6 +1637,7 @@ dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinemat
     sl.ky0 = sl.rank * sl.nyl;
     sl.z0 = sl.rank * sl.nzl;
     sl.Hs = (long long)ctx->n1h * sl.nyl * n[2];
+    sl.Hsp = (long long)ctx->kxp * sl.nyl * n[2];
     sl.Nloc = (long long)n[0] * n[1] * sl.nzl;
     sl.nlines = (long long)n[1] * sl.nzl;
     sl.xiy = ctx->xiy + sl.ky0;
@@ -2054,7 +2070,7 @@ dbfft_status field_to_tmp(dbfft_ctx ctx, int which) {
   // linear: eps = Ebar + sym grad u (Voigt 6 via the inverse passes), sigma = C:eps
   CKS(upload_e(ctx, ctx->Fbar_c));
   for (Slab& s : ctx->slabs) CKS(run_col(ctx, COL_I1S, PK_OTHER, geom_I1(ctx, s, s.u_c, s.WS1, 5), ctx->n3));
-  CKS(exchange(ctx, (long long)5 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
+  CKS(exchange(ctx, (long long)5 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->kxp));
   for (Slab& s : ctx->slabs) {
     CKS(run_col(ctx, COL_I2S, PK_OTHER, geom_I2(ctx, s, s.WR, s.WB, 5), ctx->n2));
     double* tmp6 = reinterpret_cast<double*>(s.WA);  // 6 real fields fit in WA (6 complex fields)
@@ -2101,7 +2117,7 @@ dbfft_status incompat_max(dbfft_ctx ctx, double* result) {
   const bool fin = ctx->kin == 9;
   std::vector<double> mx(ctx->slabs.size(), 0.0);
   const int nrow = fin ? 3 : 1, nf = fin ? 3 : 6;
-  const long long chunk = (long long)nf * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h;
+  const long long chunk = (long long)nf * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->kxp;
   for (int row = 0; row < nrow; ++row) {
     for (Slab& s : ctx->slabs) {
       XGeom gx = xgeom(ctx, s, nullptr, s.WB);
@@ -2164,7 +2180,7 @@ dbfft_status div_norm(dbfft_ctx ctx, double* norm, double* mean9) {
   }
   // the operator's forward tail: f = -i xi . sigma_hat (positive form, R3) into q
   for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_OTHER, geom_F2(ctx, s, s.WB, s.WS2, 6), ctx->n2));
-  CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
+  CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->kxp));
   for (size_t k = 0; k < ctx->slabs.size(); ++k) {
     Slab& s = ctx->slabs[k];
     CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_OTHER, geom_F3(ctx, s, s.WR2, s.q, 6), ctx->n3));
@@ -2203,7 +2219,7 @@ dbfft_status dbfft_get_field(dbfft_ctx ctx, int32_t which, void* out, int32_t ou
       return spec_out(ctx, &Slab::u_c, (cplx*)out, k);
     case DBFFT_FIELD_U: {
       for (Slab& s : ctx->slabs) CKS(run_col(ctx, COL_ZI3, PK_OTHER, geom_I1(ctx, s, s.u_c, s.WS1, 3), ctx->n3));
-      CKS(exchange(ctx, (long long)3 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->n1h));
+      CKS(exchange(ctx, (long long)3 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->kxp));
       for (Slab& s : ctx->slabs) {
         CKS(run_col(ctx, COL_YI3, PK_OTHER, geom_I2(ctx, s, s.WR, s.WB, 3), ctx->n2));
         XGeom gx = xgeom(ctx, s, s.WB, nullptr);

@@ -817,7 +817,7 @@ DBF_DEV void x_issue_in(const XGeom& g, long long grp, cplx* st_in, uint64_t* ba
   const uint32_t row = sizeof(cplx) * CF::N1H;
   mbar_expect_tx(bar, row * CIN * nl);
   for (int l = 0; l < nl; ++l)
-    for (int f = 0; f < CIN; ++f) bulk_g2s(st_in + (l * CIN + f) * CF::N1H, g.in + f * g.fs_in + (l0 + l) * g.n1h, row, bar);
+    for (int f = 0; f < CIN; ++f) bulk_g2s(st_in + (l * CIN + f) * CF::N1H, g.in + f * g.fs_in + (l0 + l) * g.kxp, row, bar);
 }
 template <int N1, int KIND>
 DBF_DEV void x_issue_tan(const XGeom& g, long long grp, double* st_tan, uint16_t* st_ph, uint64_t* bar) {
@@ -908,7 +908,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
             A = st_in[(l * T::CIN + fa) * CF::N1H + kk];
             if (fb < cin) B = st_in[(l * T::CIN + fb) * CF::N1H + kk];
           } else {
-            const long long base = line * g.n1h + kk;
+            const long long base = line * g.kxp + kk;
             A = __ldg(g.in + fa * g.fs_in + base);
             if (fb < cin) B = __ldg(g.in + fb * g.fs_in + base);
           }
@@ -1027,7 +1027,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
             s_dc[DCRED ? l : 0][x_red_slot<KIND>(fa)] += dcs * A.x;
             if (fb < COUT) s_dc[DCRED ? l : 0][x_red_slot<KIND>(fb)] += dcs * B.x;
           }
-          const long long base = line * g.n1h + k;
+          const long long base = line * g.kxp + k;
           g.out[fa * g.fs_out + base] = A;
           if (fb < cout_rt) g.out[fb * g.fs_out + base] = B;
         }

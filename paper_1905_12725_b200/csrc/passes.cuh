@@ -76,6 +76,7 @@ struct XGeom {
   cplx* out;
   long long fs_in, fs_out;
   int n1h, n1;
+  int kxp;              // line pitch of in / out (complex elements, >= n1h)
   long long nlines;
   const cplx* tw;       // twiddles W_{n1}
   const double* xix;    // xi_x [n1h]
