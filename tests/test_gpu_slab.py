@@ -240,3 +240,22 @@ def test_peer_windows_across_processes(dbf, world):
     for p in procs:
         p.join(timeout=60)
     assert all(res[r] == 0 for r in range(world)), res
+
+
+@pytest.mark.parametrize("world,transport", [(1, "nccl"), (2, "nccl"), (4, "peer")])
+def test_kx_pitch_padding_bit_identical(dbf, world, transport, monkeypatch):
+    """DBFFT_KX_PAD=1 pads the kx pitch of the intermediate layouts (X1, B, X2) to 128-byte rows;
+    the arithmetic is unchanged, so a finite-strain increment must agree bit for bit."""
+    cfg = configs.c4(n=32, radius_vox=3)
+    L = cfg["loads"][0]
+    out = {}
+    for pad in ("0", "1"):
+        monkeypatch.setenv("DBFFT_KX_PAD", pad)
+        ctx = dbf.DBFFT(cfg["n"], kinematics="finite", world=world, loopback=world > 1,
+                        transport=transport)
+        ctx.set_phases(cfg["phase"], cfg["materials"])
+        rep = ctx.solve_increment(L["target"], L["mask"])
+        out[pad] = (rep["cg_iters"], rep["macro_stress"], ctx.get_field(dbf.FIELD_STRESS))
+        ctx.close()
+    assert out["0"][0] == out["1"][0]
+    assert np.array_equal(out["0"][1], out["1"][1]) and np.array_equal(out["0"][2], out["1"][2])
