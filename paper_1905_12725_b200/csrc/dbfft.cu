@@ -363,8 +363,6 @@ XGeom xgeom(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out) {
 
 dbfft_status peer_barrier(dbfft_ctx ctx) {
   ProfScope ps(ctx, PK_XCHG);
-  Slab& s = ctx->slabs[0];
-  (void)s;
   ++ctx->epoch;
   CK(launch_peer_barrier((unsigned*)ctx->pbf.recv[0], (char*)ctx->pbf.win[0], ctx->pbf.chunk, ctx->P, ctx->rank, ctx->epoch,
                          ctx->stream));
@@ -1506,6 +1504,10 @@ dbfft_status dbfft_nccl_unique_id(void* out128) {
 static int g_peer_seq = 0;
 static dbfft_status build_peer(dbfft_ctx ctx, const void* nccl_id) {
   std::string err;
+  if (ctx->P > 32) {  // the barrier kernel runs one warp, one lane per rank
+    ctx->err = "peer transport: at most 32 ranks";
+    return DBFFT_E_INVALID_ARG;
+  }
   const Slab& s0 = ctx->slabs[0];
   const size_t chunk = peer_chunk(sizeof(cplx) * 6 * (size_t)s0.nyl * s0.nzl * ctx->kxp, ctx->device, &err);
   const size_t fchunk = chunk ? peer_chunk(4096, ctx->device, &err) : 0;
