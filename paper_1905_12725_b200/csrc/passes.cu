@@ -35,6 +35,9 @@
 #define DBF_X_STAGE_TAN_NH 0  // pass_X compact neo-Hookean kind: stage the 10 per-voxel tangent doubles (1),
                               // or load them in the voxel loop at 4 CTAs/SM (0; B200 256^3: 1.120 -> 1.098 ms)
 #endif
+#ifndef DBF_X_MINB_CONST
+#define DBF_X_MINB_CONST 3  // CTAs per SM of the constitutive-update kinds (Newton residual)
+#endif
 #ifndef DBF_X_MINB_NOTAN
 #define DBF_X_MINB_NOTAN 4  // CTAs per SM of the pass_X kinds that load their tangent in the voxel loop
 #endif
@@ -780,7 +783,8 @@ struct XCfg {
   static constexpr size_t SMEM = SLOTS + ST_IN + ST_TAN + ST_PH + 16;  // + 2 mbarriers
   static constexpr int MINB = ((KIND == X_K_J2 && !DBF_X_STAGE_TAN_J2) || (KIND == X_K_FIN_NH && !DBF_X_STAGE_TAN_NH))
                                    ? DBF_X_MINB_NOTAN
-                                   : (THREADS <= 192) ? DBF_X_MINB : 2;
+                               : (KIND == X_CONST_FIN || KIND == X_CONST_J2) ? DBF_X_MINB_CONST
+                               : (THREADS <= 192) ? DBF_X_MINB : 2;
 };
 
 // ---- bulk async copy (TMA engine) + mbarrier helpers ------------------------------------------
