@@ -1589,8 +1589,10 @@ static int col_prog_span(const TProg& p) {
 
 template <int KIND, bool DOT>
 struct ColRing {  // ring depth: 3 slots; small-strain F3 (two-term outputs from 6 inputs) takes 4
-  // (B200: 512^3 3.35 -> 3.26 ms, 256^3 0.400 -> 0.392 ms; R = 4 everywhere was slower overall)
-  static constexpr int R = (KIND == COL_F3S) ? 4 : DBF_COL_R;
+  // (B200: 512^3 3.35 -> 3.26 ms, 256^3 0.400 -> 0.392 ms; R = 4 everywhere was slower overall);
+  // the finite-strain I1 and F2 run faster with 2 (256^3: I1 0.319 -> 0.300 ms, F2 0.530 -> 0.522;
+  // I2 was slower with 2)
+  static constexpr int R = (KIND == COL_F3S) ? 4 : (KIND == COL_I1F || KIND == COL_F2F) ? 2 : DBF_COL_R;
 };
 
 template <int N, int KIND, bool DOT, bool UPD = false>
