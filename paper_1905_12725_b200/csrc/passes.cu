@@ -1506,6 +1506,9 @@ static cudaError_t launch_col_n(int kind, const ColGeom& g, cudaStream_t s) {
 #ifndef DBF_TMA_PROMO
 #define DBF_TMA_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
 #endif
+#ifndef DBF_RING2_SMALL
+#define DBF_RING2_SMALL 0  // 2-deep ring for the small-strain I1 / F2 too (slower: 256^3 I1S 0.319 -> 0.381 ms)
+#endif
 #ifndef DBF_REG512_MASK
 #define DBF_REG512_MASK 0  // bit k: column kind k at N = 512 takes the register-pipelined kernel
 #endif
@@ -1592,7 +1595,9 @@ struct ColRing {  // ring depth: 3 slots; small-strain F3 (two-term outputs from
   // (B200: 512^3 3.35 -> 3.26 ms, 256^3 0.400 -> 0.392 ms; R = 4 everywhere was slower overall);
   // the finite-strain I1 and F2 run faster with 2 (256^3: I1 0.319 -> 0.300 ms, F2 0.530 -> 0.522;
   // I2 was slower with 2)
-  static constexpr int R = (KIND == COL_F3S) ? 4 : (KIND == COL_I1F || KIND == COL_F2F) ? 2 : DBF_COL_R;
+  static constexpr int R = (KIND == COL_F3S) ? 4
+                           : (KIND == COL_I1F || KIND == COL_F2F || (DBF_RING2_SMALL && (KIND == COL_I1S || KIND == COL_F2S))) ? 2
+                           : DBF_COL_R;
 };
 
 template <int N, int KIND, bool DOT, bool UPD = false>
