@@ -14,9 +14,10 @@ constexpr int BLK = 256;
 // grid-stride kernels run whole waves (a partial second wave — a 4-per-SM grid at 3 resident
 // CTAs per SM — made k_cg_update 1.5x slower, B200 512^3): 3 CTAs of 256 per SM (<= 85
 // registers, no spills); k_cg_direction holds 2 (94 registers; 3 would spill) and runs two
-// full waves of them (measured a little faster than one)
-constexpr int NBLK = 148 * 3;
-constexpr int NBLK_DIR = 148 * 4;
+// full waves of them (measured a little faster than one).  Grids follow the device's SM count.
+constexpr int MINB = 3;
+int nblk() { return MINB * num_sms(); }
+int nblk_dir() { return 4 * num_sms(); }
 
 
 // z = A^-1 r with A = xi.Cbar.xi (symmetric 3x3), 0 on the null set Z (R4)
@@ -46,7 +47,7 @@ DBF_DEV void block_store(double (&v)[NV], double* partials) {
   }
 }
 
-__global__ void __launch_bounds__(BLK, NBLK / 148) k_precond(SpecGeom g, PrecQ Q, const cplx* __restrict__ r, cplx* __restrict__ z) {
+__global__ void __launch_bounds__(BLK, MINB) k_precond(SpecGeom g, PrecQ Q, const cplx* __restrict__ r, cplx* __restrict__ z) {
   for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < g.Hs; i += (long long)gridDim.x * BLK) {
     Pt p = point(g, i);
     cplx rv[3] = {__ldg(r + i), __ldg(r + g.Hs + i), __ldg(r + 2 * g.Hs + i)};
@@ -59,7 +60,7 @@ __global__ void __launch_bounds__(BLK, NBLK / 148) k_precond(SpecGeom g, PrecQ Q
 }
 
 // p = M r ; partials (<r, p>, <r, r>)
-__global__ void __launch_bounds__(BLK, NBLK / 148) k_cg_init(SpecGeom g, PrecQ Q, const cplx* __restrict__ r, cplx* __restrict__ pv, double* partials) {
+__global__ void __launch_bounds__(BLK, MINB) k_cg_init(SpecGeom g, PrecQ Q, const cplx* __restrict__ r, cplx* __restrict__ pv, double* partials) {
   double acc[2] = {0.0, 0.0};
   for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < g.Hs; i += (long long)gridDim.x * BLK) {
     Pt p = point(g, i);
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(BLK, NBLK / 148) k_cg_init(SpecGeom g, PrecQ Q
 // x += alpha p ; r -= alpha q ; z = M r ; partials (<r, z>, <r, r>)
 // r -= alpha q, z = M r on the fly, partial <r,z>, <r,r> (x += alpha p is deferred to the
 // direction kernel, which reads p anyway: 3 vector transfers here instead of 6)
-__global__ void __launch_bounds__(BLK, NBLK / 148) k_cg_update(SpecGeom g, PrecQ Q, const CgDev* __restrict__ cg, cplx* __restrict__ r,
+__global__ void __launch_bounds__(BLK, MINB) k_cg_update(SpecGeom g, PrecQ Q, const CgDev* __restrict__ cg, cplx* __restrict__ r,
                                                    const cplx* __restrict__ qv, double* partials) {
   if (cg->converged | cg->breakdown) return;
   const double alpha = cg->alpha;
@@ -156,7 +157,7 @@ __global__ void k_fin_x(CgDev* cg) {
 }
 
 // r = b - Ax ; partial <r, r>
-__global__ void __launch_bounds__(BLK, NBLK / 148) k_true_residual(SpecGeom g, const cplx* __restrict__ b, const cplx* __restrict__ ax,
+__global__ void __launch_bounds__(BLK, MINB) k_true_residual(SpecGeom g, const cplx* __restrict__ b, const cplx* __restrict__ ax,
                                                        cplx* __restrict__ r, double* partials) {
   double acc[1] = {0.0};
   for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < g.Hs; i += (long long)gridDim.x * BLK) {
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(BLK, NBLK / 148) k_true_residual(SpecGeom g, c
   block_store<1>(acc, partials);
 }
 
-__global__ void __launch_bounds__(BLK, NBLK / 148) k_axpy(SpecGeom g, cplx* __restrict__ y, const cplx* __restrict__ x, double a) {
+__global__ void __launch_bounds__(BLK, MINB) k_axpy(SpecGeom g, cplx* __restrict__ y, const cplx* __restrict__ x, double a) {
   for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < 3 * g.Hs; i += (long long)gridDim.x * BLK) {
     cplx xv = __ldg(x + i), yv = y[i];
     y[i] = make_double2(fma(a, xv.x, yv.x), fma(a, xv.y, yv.y));
@@ -371,10 +372,10 @@ __global__ void k_fill(double* p, long long n, double v) {
 
 }  // namespace
 
-int cg_blocks() { return NBLK; }
+int cg_blocks() { return nblk(); }
 
 cudaError_t launch_precond(const SpecGeom& g, const PrecQ& q, const cplx* r, cplx* z, cudaStream_t s) {
-  k_precond<<<NBLK, BLK, 0, s>>>(g, q, r, z);
+  k_precond<<<nblk(), BLK, 0, s>>>(g, q, r, z);
   return cudaGetLastError();
 }
 cudaError_t launch_cg_init(const SpecGeom& g, const PrecQ& q, const cplx* r, cplx* p, double* partials, int nblk, cudaStream_t s) {
@@ -387,7 +388,7 @@ cudaError_t launch_cg_update(const SpecGeom& g, const PrecQ& q, CgDev* cg, cplx*
   return cudaGetLastError();
 }
 cudaError_t launch_cg_direction(const SpecGeom& g, const PrecQ& q, const CgDev* cg, cplx* x, cplx* p, const cplx* r, cudaStream_t s) {
-  k_cg_direction<<<NBLK_DIR, BLK, 0, s>>>(g, q, cg, x, p, r);
+  k_cg_direction<<<nblk_dir(), BLK, 0, s>>>(g, q, cg, x, p, r);
   return cudaGetLastError();
 }
 cudaError_t launch_fin_x(CgDev* cg, cudaStream_t s) {
@@ -419,7 +420,7 @@ cudaError_t launch_allreduce_lb(double* const* v, int P, int k, int is_max, cuda
   return cudaGetLastError();
 }
 cudaError_t launch_axpy(const SpecGeom& g, cplx* y, const cplx* x, double a, cudaStream_t s) {
-  k_axpy<<<NBLK, BLK, 0, s>>>(g, y, x, a);
+  k_axpy<<<nblk(), BLK, 0, s>>>(g, y, x, a);
   return cudaGetLastError();
 }
 cudaError_t launch_reduce(const double* partials, int nblk, int nred, double* out, cudaStream_t s, int max_slot) {
@@ -427,10 +428,10 @@ cudaError_t launch_reduce(const double* partials, int nblk, int nred, double* ou
   return cudaGetLastError();
 }
 cudaError_t launch_phase_hist(const uint16_t* ph, long long nvox, double* counts, int nphase, int* bad, cudaStream_t s) {
-  k_phase_hist<<<NBLK, BLK, 0, s>>>(ph, nvox, counts, nphase, bad);
+  k_phase_hist<<<nblk(), BLK, 0, s>>>(ph, nvox, counts, nphase, bad);
   return cudaGetLastError();
 }
 cudaError_t launch_fill(double* p, long long n, double v, cudaStream_t s) {
-  k_fill<<<NBLK, BLK, 0, s>>>(p, n, v);
+  k_fill<<<nblk(), BLK, 0, s>>>(p, n, v);
   return cudaGetLastError();
 }

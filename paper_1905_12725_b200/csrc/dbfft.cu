@@ -205,6 +205,18 @@ namespace {
     }                                                                                         \
   } while (0)
 
+// Every ABI call on a ctx runs with the ctx's device current (kernels, the per-device kernel
+// attribute / occupancy caches of passes.cu, stream work) and restores the caller's device.
+struct DevGuard {
+  int prev = -1, dev;
+  explicit DevGuard(int d) : dev(d) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+  }
+  ~DevGuard() {
+    if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+  }
+};
+
 // ---------------------------------------------------------------- profiling helpers
 struct ProfScope {
   dbfft_ctx ctx;
@@ -345,7 +357,7 @@ XGeom xgeom(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out) {
   g.tw = ctx->tw1;
   g.xix = ctx->xix;
   g.inv_n = 1.0 / (double)ctx->N;
-  g.oscale = 0.5 / (double)ctx->N;  // exact: N is a power of two
+  g.oscale = 0.5 / (double)ctx->N;  // exact scaling when N is a power of two; odd grids round once (1 ulp)
   for (int f = 0; f < 9; ++f) g.real_map[f] = f;
   g.partials = s.part_x;
   g.nred = 10;
@@ -881,9 +893,14 @@ dbfft_status pcg(dbfft_ctx ctx, const dbfft_opts& o, int* iters_out) {
       }
       CK(cudaMemcpyAsync(ctx->h_cg, ctx->slabs[0].cg, sizeof(CgDev), cudaMemcpyDeviceToHost, ctx->stream));
       CK(cudaStreamSynchronize(ctx->stream));
-      if (ctx->h_cg->converged == 1 || restarts > 20) {
-        *iters_out = ctx->h_cg->iters;
-        return DBFFT_OK;
+      *iters_out = ctx->h_cg->iters;
+      if (ctx->h_cg->converged == 1) return DBFFT_OK;
+      // the restarted iterations count against max_cg (cg->iters carries over); a true residual
+      // that stays above tolerance after the restart budget is a failure, not a success
+      if (restarts >= 20 || ctx->h_cg->iters >= o.max_cg) {
+        ctx->err = "PCG did not converge: true residual b - Ax above tolerance after " + std::to_string(restarts) +
+                   " restarts (eps_eq " + std::to_string(ctx->h_cg->eps_eq) + ")";
+        return DBFFT_E_NOT_CONVERGED;
       }
       ++restarts;  // restart from the true residual: z = M r, p = z
       CKS(init_dir());
@@ -1760,6 +1777,7 @@ dbfft_status dbfft_peer_probe_close(void* h) {
 
 dbfft_status dbfft_destroy(dbfft_ctx ctx) {
   if (!ctx) return DBFFT_E_INVALID_ARG;
+  DevGuard dev_guard(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   free_all(ctx);
   delete ctx;
@@ -1782,6 +1800,7 @@ dbfft_status dbfft_spectral_layout(dbfft_ctx ctx, int64_t shape[4], int64_t stri
 
 dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t on_device, int32_t n_phases, const dbfft_material* table) {
   if (!ctx) return DBFFT_E_INVALID_ARG;
+  DevGuard dev_guard(ctx->device);
   if (!phase_id || !table || n_phases <= 0 || n_phases > 65535) {
     ctx->err = "set_phases: bad arguments";
     return DBFFT_E_INVALID_ARG;
@@ -1925,6 +1944,7 @@ dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t o
 
 dbfft_status dbfft_apply_K(dbfft_ctx ctx, const void* u_hat, void* f_hat) {
   if (!ctx) return DBFFT_E_INVALID_ARG;
+  DevGuard dev_guard(ctx->device);
   if (!u_hat || !f_hat || u_hat == f_hat) {
     ctx->err = "apply_K: null or aliased vectors";
     return DBFFT_E_INVALID_ARG;
@@ -1951,6 +1971,7 @@ dbfft_status dbfft_apply_K(dbfft_ctx ctx, const void* u_hat, void* f_hat) {
 
 dbfft_status dbfft_apply_K_aug(dbfft_ctx ctx, const uint8_t mask[9], const void* u_hat, const double e_in[9], void* f_hat, double r_out[9]) {
   if (!ctx) return DBFFT_E_INVALID_ARG;
+  DevGuard dev_guard(ctx->device);
   if (!mask || !u_hat || !e_in || !f_hat || !r_out || u_hat == f_hat) {
     ctx->err = "apply_K_aug: bad arguments";
     return DBFFT_E_INVALID_ARG;
@@ -1977,6 +1998,7 @@ dbfft_status dbfft_apply_K_aug(dbfft_ctx ctx, const uint8_t mask[9], const void*
 
 dbfft_status dbfft_precond(dbfft_ctx ctx, const void* r_hat, void* z_hat) {
   if (!ctx) return DBFFT_E_INVALID_ARG;
+  DevGuard dev_guard(ctx->device);
   if (!r_hat || !z_hat) {
     ctx->err = "precond: null vectors";
     return DBFFT_E_INVALID_ARG;
@@ -1995,6 +2017,7 @@ dbfft_status dbfft_precond(dbfft_ctx ctx, const void* r_hat, void* z_hat) {
 
 dbfft_status dbfft_eval_state(dbfft_ctx ctx, const double* field, int32_t on_device, double dt) {
   if (!ctx) return DBFFT_E_INVALID_ARG;
+  DevGuard dev_guard(ctx->device);
   if (ctx->family == FAM_NONE) {
     ctx->err = "eval_state before set_phases";
     return DBFFT_E_STATE;
@@ -2019,6 +2042,7 @@ dbfft_status dbfft_eval_state(dbfft_ctx ctx, const double* field, int32_t on_dev
 dbfft_status dbfft_solve_increment(dbfft_ctx ctx, const double target[9], const uint8_t mask[9], double dt, const dbfft_opts* opts,
                                    dbfft_report* report) {
   if (!ctx) return DBFFT_E_INVALID_ARG;
+  DevGuard dev_guard(ctx->device);
   if (ctx->family == FAM_NONE) {
     ctx->err = "solve_increment before set_phases";
     return DBFFT_E_STATE;
@@ -2206,6 +2230,7 @@ double frob9(const double* a) {
 
 dbfft_status dbfft_get_field(dbfft_ctx ctx, int32_t which, void* out, int32_t out_on_device) {
   if (!ctx) return DBFFT_E_INVALID_ARG;
+  DevGuard dev_guard(ctx->device);
   if (!out) {
     ctx->err = "get_field: null output";
     return DBFFT_E_INVALID_ARG;
@@ -2242,6 +2267,7 @@ dbfft_status dbfft_get_field(dbfft_ctx ctx, int32_t which, void* out, int32_t ou
 
 dbfft_status dbfft_profile_enable(dbfft_ctx ctx, int32_t enable) {
   if (!ctx) return DBFFT_E_INVALID_ARG;
+  DevGuard dev_guard(ctx->device);
   prof_flush(ctx);
   ctx->prof = enable != 0;
   if (enable) {
@@ -2253,6 +2279,7 @@ dbfft_status dbfft_profile_enable(dbfft_ctx ctx, int32_t enable) {
 
 dbfft_status dbfft_profile_read(dbfft_ctx ctx, int32_t id, double* total_ms, int64_t* launches) {
   if (!ctx || id < 0 || id >= PK_COUNT) return DBFFT_E_INVALID_ARG;
+  DevGuard dev_guard(ctx->device);
   prof_flush(ctx);
   if (total_ms) *total_ms = ctx->prof_ms[id];
   if (launches) *launches = ctx->prof_n[id];
@@ -2272,6 +2299,7 @@ int32_t dbfft_profile_count(void) { return PK_COUNT; }
 
 dbfft_status dbfft_residuals(dbfft_ctx ctx, const double target[9], const uint8_t mask[9], double out[3]) {
   if (!ctx || !target || !mask || !out) return DBFFT_E_INVALID_ARG;
+  DevGuard dev_guard(ctx->device);
   if (ctx->family == FAM_NONE) {
     ctx->err = "residuals before set_phases";
     return DBFFT_E_STATE;
@@ -2300,6 +2328,7 @@ dbfft_status dbfft_residuals(dbfft_ctx ctx, const double target[9], const uint8_
 
 dbfft_status dbfft_incompatibility(dbfft_ctx ctx, const double* field, int32_t on_device, double* out) {
   if (!ctx || !field || !out) return DBFFT_E_INVALID_ARG;
+  DevGuard dev_guard(ctx->device);
   for (Slab& s : ctx->slabs) CKS(ensure_tmp(ctx, s));
   CKS(scatter_real(ctx, field, on_device, 9, nullptr, &Slab::tmp_real));
   return incompat_max(ctx, out);
@@ -2307,6 +2336,7 @@ dbfft_status dbfft_incompatibility(dbfft_ctx ctx, const double* field, int32_t o
 
 dbfft_status dbfft_get_trace(dbfft_ctx ctx, double* out, int32_t cap, int32_t* n) {
   if (!ctx || !n || (cap > 0 && !out)) return DBFFT_E_INVALID_ARG;
+  DevGuard dev_guard(ctx->device);
   *n = ctx->trace_n;
   const int m = std::min(cap, ctx->trace_n);
   if (m > 0) CK(cudaMemcpy(out, ctx->trace_dev, sizeof(double) * 2 * (size_t)m, cudaMemcpyDeviceToHost));

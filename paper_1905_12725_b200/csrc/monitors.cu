@@ -5,7 +5,7 @@
 namespace {
 
 constexpr int MB = 256;
-constexpr int MNB = 148 * 4;
+static int mnb() { return 4 * num_sms(); }  // monitor grid: 4 CTAs per SM
 
 DBF_DEV int eps3(int i, int j, int k) {  // Levi-Civita symbol
   return (i == j || j == k || i == k) ? 0 : (((j - i + 3) % 3) == 1 ? 1 : -1);
@@ -141,25 +141,25 @@ __global__ void __launch_bounds__(MB) k_specnorm2(SpecGeom g, const cplx* __rest
 
 }  // namespace
 
-int monitor_blocks() { return MNB; }
+int monitor_blocks() { return mnb(); }
 
 cudaError_t launch_curl3(const SpecGeom& g, cplx* v, cudaStream_t s) {
-  k_curl3<<<MNB, MB, 0, s>>>(g, v);
+  k_curl3<<<mnb(), MB, 0, s>>>(g, v);
   return cudaGetLastError();
 }
 cudaError_t launch_curlcurl6(const SpecGeom& g, cplx* v, cudaStream_t s) {
-  k_curlcurl6<<<MNB, MB, 0, s>>>(g, v);
+  k_curlcurl6<<<mnb(), MB, 0, s>>>(g, v);
   return cudaGetLastError();
 }
 cudaError_t launch_maxabs(const double* x, long long n, double* partials, cudaStream_t s) {
-  k_maxabs<<<MNB, MB, 0, s>>>(x, n, partials);
+  k_maxabs<<<mnb(), MB, 0, s>>>(x, n, partials);
   return cudaGetLastError();
 }
 cudaError_t launch_sum(const double* x, long long n, double* partials, cudaStream_t s) {
-  k_sum<<<MNB, MB, 0, s>>>(x, n, partials);
+  k_sum<<<mnb(), MB, 0, s>>>(x, n, partials);
   return cudaGetLastError();
 }
 cudaError_t launch_specnorm2(const SpecGeom& g, const cplx* v, int nf, double* partials, cudaStream_t s) {
-  k_specnorm2<<<MNB, MB, 0, s>>>(g, v, nf, partials);
+  k_specnorm2<<<mnb(), MB, 0, s>>>(g, v, nf, partials);
   return cudaGetLastError();
 }

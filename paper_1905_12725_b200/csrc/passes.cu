@@ -14,6 +14,37 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <mutex>
+
+// Per-device one-time initialisation (kernel attributes, occupancy-derived grids): a process may
+// hold contexts on several devices, each call runs with its ctx's device current (dbfft.cu).
+namespace {
+constexpr int kMaxDevices = 64;
+struct DevOnce {
+  std::once_flag flag[kMaxDevices];
+  cudaError_t err[kMaxDevices] = {};
+  int val[kMaxDevices] = {};
+};
+int current_device() {
+  int d = 0;
+  return cudaGetDevice(&d) == cudaSuccess ? d : -1;
+}
+template <class F>
+cudaError_t dev_once(DevOnce& o, F init, int* val = nullptr) {
+  const int d = current_device();
+  if (d < 0 || d >= kMaxDevices) return cudaErrorInvalidDevice;
+  std::call_once(o.flag[d], [&] { o.err[d] = init(o.val[d]); });
+  if (val) *val = o.val[d];
+  return o.err[d];
+}
+}  // namespace
+
+int num_sms() {
+  static DevOnce once;
+  int n = 0;
+  dev_once(once, [](int& v) { return cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, current_device()); }, &n);
+  return n > 0 ? n : 148;
+}
 
 #ifndef DBF_X_MINB
 #define DBF_X_MINB 3
@@ -600,7 +631,7 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
     const double mu = __ldg(g.ptable + 36 * ph), lam = __ldg(g.ptable + 36 * ph + 1) - 2.0 * mu / 3.0;
 #pragma unroll
     for (int a = 0; a < 9; ++a) e9[a] = G[a] + (g.e ? __ldg(g.e + a) : 0.0);
-    nh_apply(Fi, c1 * g.oscale, mu * g.oscale, lam * g.oscale, e9, P);  // P x 1/(2N): exact (powers of 2)
+    nh_apply(Fi, c1 * g.oscale, mu * g.oscale, lam * g.oscale, e9, P);  // P x 1/(2N): exact for powers of 2
 #pragma unroll
     for (int a = 0; a < 9; ++a) xd += G[a] * P[a];
   } else if (KIND == X_CONST_FIN) {
@@ -1466,12 +1497,11 @@ template <int N, int KIND>
 static cudaError_t launch_col_k(const ColGeom& g, cudaStream_t s) {
   constexpr int COLS = ColCfg<N>::COLS;
   constexpr size_t smem = sizeof(cplx) * N * COLS * (ColTwo<KIND>::value ? 2 : 1);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(col_pass_kernel<N, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static DevOnce once;
+  cudaError_t e = dev_once(once, [](int&) {
+    return cudaFuncSetAttribute(col_pass_kernel<N, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  if (e != cudaSuccess) return e;
   col_pass_kernel<N, KIND><<<col_grid(N, g.ncols), ColCfg<N>::THREADS, smem, s>>>(g);
   return cudaGetLastError();
 }
@@ -1556,15 +1586,6 @@ static bool col_map(CUtensorMap* m, const void* ptr, int N, int n1h, int psh, lo
   return r == CUDA_SUCCESS;
 }
 
-static int g_nsm = 0;
-static int num_sms() {
-  if (!g_nsm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_nsm, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return g_nsm;
-}
 
 template <int N>
 static bool col_tma_tiles(const ColGeom& g, ColTiles* tl) {
@@ -1604,13 +1625,12 @@ template <int N, int KIND, bool DOT, bool UPD = false>
 static cudaError_t launch_col_tma_k(const TmaMaps& maps, const ColGeom& g, const ColTiles& tl, cudaStream_t s, int* grid_out) {
   constexpr int R = ColRing<KIND, DOT>::R;
   constexpr size_t smem = (size_t)(R + (UPD ? 3 : 2) + 1) * TmaCfg<N>::TILE + 2 * R * sizeof(uint64_t) + 1024;
-  static bool attr = false;
-  if (!attr) {
+  static DevOnce once;
+  cudaError_t e = dev_once(once, [](int&) {
     if (col_prog_span(kColProgHost[2 * KIND + (DOT ? 1 : 0)]) > R) return cudaErrorInvalidConfiguration;
-    cudaError_t e = cudaFuncSetAttribute(col_tma_kernel<N, KIND, DOT, R, UPD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+    return cudaFuncSetAttribute(col_tma_kernel<N, KIND, DOT, R, UPD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  if (e != cudaSuccess) return e;
   const int grid = std::min(tl.n_tiles, num_sms());
   if (grid_out) *grid_out = grid;
   col_tma_kernel<N, KIND, DOT, R, UPD><<<grid, TmaCfg<N>::THREADS, smem, s>>>(maps, g, tl);
@@ -1696,19 +1716,23 @@ cudaError_t launch_col(int kind, int N, const ColGeom& g, cudaStream_t s, int* g
 template <int N1, int KIND>
 static cudaError_t launch_x_k(const XGeom& g, cudaStream_t s, int* grid_out, int nf_real) {
   typedef XCfg<N1, KIND> CF;
-  static int max_grid = 0;  // per template instance: resident CTAs on the whole device
-  if (max_grid == 0) {
-    cudaError_t e = cudaFuncSetAttribute(x_pass_kernel<N1, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
-    if (e != cudaSuccess) return e;
-    int nb = 0, dev = 0, nsm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, x_pass_kernel<N1, KIND>, CF::THREADS, CF::SMEM);
-    if (e != cudaSuccess) return e;
-    max_grid = std::max(1, nb) * nsm;
-  }
+  static DevOnce once;  // per template instance and device: resident CTAs on the whole device
+  int max_grid = 0;
+  cudaError_t e = dev_once(
+      once,
+      [](int& mg) {
+        cudaError_t e2 = cudaFuncSetAttribute(x_pass_kernel<N1, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
+        if (e2 != cudaSuccess) return e2;
+        int nb = 0;
+        e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, x_pass_kernel<N1, KIND>, CF::THREADS, CF::SMEM);
+        mg = std::max(1, nb) * num_sms();
+        return e2;
+      },
+      &max_grid);
+  if (e != cudaSuccess) return e;
   const long long ngroups = (g.nlines + CF::LPAR - 1) / CF::LPAR;
-  const int grid = (int)std::min<long long>(ngroups, max_grid);
+  // never more CTAs than partial slots were allocated for (x_grid)
+  const int grid = (int)std::min<long long>(std::min<long long>(ngroups, max_grid), x_grid(KIND, N1, g.nlines));
   if (grid_out) *grid_out = grid;
   x_pass_kernel<N1, KIND><<<grid, CF::THREADS, CF::SMEM, s>>>(g, nf_real);
   return cudaGetLastError();
@@ -1753,7 +1777,7 @@ cudaError_t launch_x(int kind, int N1, const XGeom& g, cudaStream_t s, int* grid
 int x_grid(int kind, int N1, long long nlines) {
   (void)kind;
   (void)N1;
-  return (int)std::min<long long>(nlines, 148LL * 32);
+  return (int)std::min<long long>(nlines, 32LL * num_sms());  // <= 32 resident CTAs per SM
 }
 
 cudaError_t launch_mean_tangent(int mode, const XGeom& g, double* partials, int nblk, cudaStream_t s) {

@@ -109,6 +109,8 @@ cudaError_t launch_col(int kind, int N, const ColGeom& g, cudaStream_t s, int* g
 bool col_upd_supported(int N, const ColGeom& g);
 cudaError_t launch_x(int kind, int N1, const XGeom& g, cudaStream_t s, int* grid_out);
 int x_grid(int kind, int N1, long long nlines);
+// streaming multiprocessors of the current device (cached per device)
+int num_sms();
 int col_grid(int N, long long ncols);
 // mean tangent partials (mode 0: full 45, 1: compact neo-Hookean -> 45, 2: compact J2 -> 21)
 cudaError_t launch_mean_tangent(int mode, const XGeom& g, double* partials, int nblk, cudaStream_t s);

@@ -34,6 +34,26 @@ long long now_ms() {
 
 }  // namespace
 
+// Credentials of the process at the other end of a connected AF_UNIX socket must be this user's:
+// abstract-namespace names carry no file permissions, so any local process could bind a rank's
+// name first or connect and pose as a rank.
+static bool peer_is_same_user(int sock) {
+  ucred cr;
+  socklen_t len = sizeof(cr);
+  if (getsockopt(sock, SOL_SOCKET, SO_PEERCRED, &cr, &len) != 0 || len != sizeof(cr)) return false;
+  return cr.uid == getuid();
+}
+
+// close every descriptor carried by the SCM_RIGHTS messages of m
+static void close_cmsg_fds(msghdr* m) {
+  for (cmsghdr* cm = CMSG_FIRSTHDR(m); cm; cm = CMSG_NXTHDR(m, cm)) {
+    if (cm->cmsg_level != SOL_SOCKET || cm->cmsg_type != SCM_RIGHTS) continue;
+    const size_t n = (cm->cmsg_len - CMSG_LEN(0)) / sizeof(int);
+    int* f = reinterpret_cast<int*>(CMSG_DATA(cm));
+    for (size_t i = 0; i < n; ++i) close(f[i]);
+  }
+}
+
 int fd_allgather(const std::string& tag, int rank, int P, const int* fds, int nfd, int* out, int timeout_ms,
                  std::string* err) {
   for (int i = 0; i < nfd; ++i) out[rank * nfd + i] = fds[i];
@@ -43,9 +63,13 @@ int fd_allgather(const std::string& tag, int rank, int P, const int* fds, int nf
     return -1;
   }
   const long long deadline = now_ms() + timeout_ms;
+  std::vector<char> have(P, 0);  // peers whose descriptors arrived (each exactly once)
   auto fail = [&](const std::string& what, int ls) {
     *err = "fd_allgather: " + what + " (" + strerror(errno) + ")";
     if (ls >= 0) close(ls);
+    for (int d = 0; d < P; ++d)  // received descriptors are owned here until success
+      if (d != rank && have[d])
+        for (int i = 0; i < nfd; ++i) close(out[d * nfd + i]);
     return -1;
   };
   int ls = socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
@@ -53,7 +77,7 @@ int fd_allgather(const std::string& tag, int rank, int P, const int* fds, int nf
   sockaddr_un addr;
   socklen_t alen = abstract_addr(&addr, sock_name(tag, rank));
   if (bind(ls, (sockaddr*)&addr, alen) != 0) return fail("bind " + sock_name(tag, rank), ls);
-  if (listen(ls, P) != 0) return fail("listen", ls);
+  if (listen(ls, 2 * P) != 0) return fail("listen", ls);
   // send ours to every peer (connect succeeds as soon as the peer listens; the message waits in
   // its backlog until it accepts, so every rank can send before it receives)
   for (int d = 0; d < P; ++d) {
@@ -68,6 +92,11 @@ int fd_allgather(const std::string& tag, int rank, int P, const int* fds, int nf
       close(c);
       if (now_ms() > deadline) return fail("connect to rank " + std::to_string(d) + " timed out", ls);
       std::this_thread::sleep_for(std::chrono::milliseconds(2));
+    }
+    if (!peer_is_same_user(c)) {  // never hand our memory to a listener of another user
+      close(c);
+      errno = EPERM;
+      return fail("listener of rank " + std::to_string(d) + " belongs to another user", ls);
     }
     int32_t me = rank;
     iovec iov{&me, sizeof(me)};
@@ -84,20 +113,26 @@ int fd_allgather(const std::string& tag, int rank, int P, const int* fds, int nf
     cm->cmsg_type = SCM_RIGHTS;
     cm->cmsg_len = CMSG_LEN(nfd * sizeof(int));
     memcpy(CMSG_DATA(cm), fds, nfd * sizeof(int));
-    const ssize_t w = sendmsg(c, &m, 0);
+    const ssize_t w = sendmsg(c, &m, MSG_NOSIGNAL);
     close(c);
     if (w != (ssize_t)sizeof(me)) return fail("sendmsg to rank " + std::to_string(d), ls);
   }
-  // receive every peer's
-  for (int k = 0; k < P - 1; ++k) {
+  // receive every peer's: connections from other users, malformed messages and repeated ranks are
+  // dropped (their descriptors closed) and waiting continues until every rank arrived or timeout
+  int got = 0;
+  while (got < P - 1) {
     pollfd pf{ls, POLLIN, 0};
     const long long left = deadline - now_ms();
     if (left <= 0 || poll(&pf, 1, (int)left) != 1) {
       errno = ETIMEDOUT;
-      return fail("accept timed out", ls);
+      return fail("accept timed out (" + std::to_string(got) + " of " + std::to_string(P - 1) + " peers)", ls);
     }
     int a = accept4(ls, nullptr, nullptr, SOCK_CLOEXEC);
     if (a < 0) return fail("accept", ls);
+    if (!peer_is_same_user(a)) {
+      close(a);
+      continue;
+    }
     int32_t src = -1;
     iovec iov{&src, sizeof(src)};
     alignas(cmsghdr) char ctl[CMSG_SPACE(16 * sizeof(int))];
@@ -109,13 +144,17 @@ int fd_allgather(const std::string& tag, int rank, int P, const int* fds, int nf
     m.msg_controllen = sizeof(ctl);
     const ssize_t r = recvmsg(a, &m, MSG_CMSG_CLOEXEC);
     close(a);
-    cmsghdr* cm = CMSG_FIRSTHDR(&m);
-    if (r != (ssize_t)sizeof(src) || src < 0 || src >= P || src == rank || !cm || cm->cmsg_type != SCM_RIGHTS ||
-        cm->cmsg_len != CMSG_LEN(nfd * sizeof(int))) {
-      errno = EPROTO;
-      return fail("bad message", ls);
+    cmsghdr* cm = r >= 0 ? CMSG_FIRSTHDR(&m) : nullptr;
+    const bool ok = r == (ssize_t)sizeof(src) && !(m.msg_flags & MSG_CTRUNC) && src >= 0 && src < P && src != rank &&
+                    !have[src] && cm && cm->cmsg_level == SOL_SOCKET && cm->cmsg_type == SCM_RIGHTS &&
+                    cm->cmsg_len == CMSG_LEN(nfd * sizeof(int)) && !CMSG_NXTHDR(&m, cm);
+    if (!ok) {
+      if (r >= 0) close_cmsg_fds(&m);
+      continue;
     }
     memcpy(out + src * nfd, CMSG_DATA(cm), nfd * sizeof(int));
+    have[src] = 1;
+    ++got;
   }
   close(ls);
   return 0;

@@ -199,44 +199,105 @@ class DBFFT:
             pass
 
     # ------------------------------------------------------------------ setup
+    def _nloc(self):
+        n1, n2, n3 = self.n
+        if self.world > 1 and not self.loopback:
+            n3 //= self.world  # NCCL slab mode: this rank's z-slab
+        return n1 * n2 * n3
+
     def set_phases(self, phase, materials):
+        """phase: integer ids [z][y][x] (numpy array or torch tensor; any integer dtype with values in
+        [0, 65535]), host or on this context's device.  The C ABI takes uint16 (include/dbfft.h)."""
         recs = (Material * len(materials))(*[material_record(m) for m in materials])
-        if isinstance(phase, np.ndarray):
-            ph = np.ascontiguousarray(phase, dtype=np.uint16)
-            self._check(self.lib.dbfft_set_phases(self.h, ph.ctypes.data_as(ctypes.c_void_p), 0, len(materials), recs))
-        else:
-            ph = phase.contiguous()
+        torch = self.torch
+        if isinstance(phase, torch.Tensor) and phase.device.type != "cuda":
+            phase = phase.numpy()
+        if isinstance(phase, torch.Tensor):
+            if phase.device != self.device:
+                raise ValueError(f"set_phases: phase tensor on {phase.device}, context on {self.device}")
+            if phase.numel() != self._nloc():
+                raise ValueError(f"set_phases: {phase.numel()} ids for {self._nloc()} voxels")
+            if phase.dtype in (torch.int16, getattr(torch, "uint16", torch.int16)):
+                ph = phase.contiguous()
+            else:
+                if phase.is_floating_point() or phase.is_complex() or phase.dtype == torch.bool:
+                    raise TypeError(f"set_phases: integer phase ids required, got {phase.dtype}")
+                t32 = phase.to(torch.int32)
+                if int(t32.min()) < 0 or int(t32.max()) > 65535:
+                    raise ValueError("set_phases: phase ids outside [0, 65535]")
+                ph = torch.where(t32 >= 32768, t32 - 65536, t32).to(torch.int16).contiguous()  # uint16 bits
             self._check(self.lib.dbfft_set_phases(self.h, _dptr(ph), 1, len(materials), recs))
+            return
+        arr = np.asarray(phase)
+        if arr.dtype != np.uint16:
+            if not np.issubdtype(arr.dtype, np.integer):
+                raise TypeError(f"set_phases: integer phase ids required, got {arr.dtype}")
+            if arr.size and (arr.min() < 0 or arr.max() > 65535):
+                raise ValueError("set_phases: phase ids outside [0, 65535]")
+        if arr.size != self._nloc():
+            raise ValueError(f"set_phases: {arr.size} ids for {self._nloc()} voxels")
+        ph = np.ascontiguousarray(arr, dtype=np.uint16)
+        self._check(self.lib.dbfft_set_phases(self.h, ph.ctypes.data_as(ctypes.c_void_p), 0, len(materials), recs))
 
     def empty_spectral(self):
         return self.torch.empty(self.spec_shape, dtype=self.torch.complex128, device=self.device)
 
+    def _spec_in(self, t, name):
+        """A spectral vector argument: complex128, this device, spec_shape; returned contiguous (the
+        caller keeps the returned tensor alive until the C call returns)."""
+        torch = self.torch
+        if not isinstance(t, torch.Tensor) or t.dtype != torch.complex128 or t.device != self.device \
+                or tuple(t.shape) != self.spec_shape:
+            raise ValueError(f"{name}: complex128 tensor of shape {self.spec_shape} on {self.device} required, got "
+                             f"{getattr(t, 'dtype', type(t))} {tuple(getattr(t, 'shape', ()))} on {getattr(t, 'device', '?')}")
+        return t.contiguous()
+
+    def _spec_out(self, out, name):
+        if out is None:
+            return self.empty_spectral()
+        o = self._spec_in(out, name)
+        if o.data_ptr() != out.data_ptr():
+            raise ValueError(f"{name}: output tensor must be contiguous")
+        return out
+
     # ------------------------------------------------------------------ operator
     def apply_K(self, u_hat, out=None):
-        out = self.empty_spectral() if out is None else out
-        self._check(self.lib.dbfft_apply_K(self.h, _dptr(u_hat.contiguous()), _dptr(out)))
+        u = self._spec_in(u_hat, "apply_K(u_hat)")
+        out = self._spec_out(out, "apply_K(out)")
+        self._check(self.lib.dbfft_apply_K(self.h, _dptr(u), _dptr(out)))
         return out
 
     def apply_K_aug(self, mask, u_hat, e, out=None):
-        out = self.empty_spectral() if out is None else out
+        u = self._spec_in(u_hat, "apply_K_aug(u_hat)")
+        out = self._spec_out(out, "apply_K_aug(out)")
         m = (ctypes.c_uint8 * 9)(*np.asarray(mask, np.uint8).ravel())
         ein = (ctypes.c_double * 9)(*np.asarray(e, float).ravel())
         rout = (ctypes.c_double * 9)()
-        self._check(self.lib.dbfft_apply_K_aug(self.h, m, _dptr(u_hat.contiguous()), ein, _dptr(out), rout))
+        self._check(self.lib.dbfft_apply_K_aug(self.h, m, _dptr(u), ein, _dptr(out), rout))
         return out, np.array(rout[:]).reshape(3, 3)
 
     def precond(self, r_hat, out=None):
-        out = self.empty_spectral() if out is None else out
-        self._check(self.lib.dbfft_precond(self.h, _dptr(r_hat.contiguous()), _dptr(out)))
+        r = self._spec_in(r_hat, "precond(r_hat)")
+        out = self._spec_out(out, "precond(out)")
+        self._check(self.lib.dbfft_precond(self.h, _dptr(r), _dptr(out)))
         return out
 
     def eval_state(self, field, dt=1.0):
-        if isinstance(field, np.ndarray):
-            f = np.ascontiguousarray(field, dtype=np.float64)
-            self._check(self.lib.dbfft_eval_state(self.h, f.ctypes.data_as(ctypes.c_void_p), 0, float(dt)))
-        else:
+        """field: real [3,3,z,y,x] eps (small strain) or F (finite), numpy or a float64 tensor on
+        this device."""
+        torch = self.torch
+        if isinstance(field, torch.Tensor) and field.device.type != "cuda":
+            field = field.numpy()
+        if isinstance(field, torch.Tensor):
+            if field.dtype != torch.float64 or field.device != self.device or field.numel() != 9 * self._nloc():
+                raise ValueError(f"eval_state: float64 tensor of {9 * self._nloc()} values on {self.device} required")
             f = field.contiguous()
             self._check(self.lib.dbfft_eval_state(self.h, _dptr(f), 1, float(dt)))
+            return
+        f = np.ascontiguousarray(field, dtype=np.float64)
+        if f.size != 9 * self._nloc():
+            raise ValueError(f"eval_state: {f.size} values for a 9 x {self._nloc()} field")
+        self._check(self.lib.dbfft_eval_state(self.h, f.ctypes.data_as(ctypes.c_void_p), 0, float(dt)))
 
     # ------------------------------------------------------------------ solve
     def solve_increment(self, target, mask, dt=1.0, raise_on_error=True, **opts):
@@ -331,24 +392,3 @@ class DBFFT:
             self._check(self.lib.dbfft_profile_read(self.h, k, ctypes.byref(ms), ctypes.byref(n)))
             res[self.lib.dbfft_profile_name(k).decode()] = (ms.value, n.value)
         return res
-
-
-def half_spectrum(u_real):
-    """Test/bench helper: mean-normalised half spectrum of a real [3][z][y][x] field laid out as
-    [3][ky][kz][kx] (numpy rfftn; input preparation, not part of the product path)."""
-    n3, n2, n1 = u_real.shape[1:]
-    h = np.fft.rfftn(u_real, axes=(1, 2, 3)) / (n1 * n2 * n3)   # [3][kz][ky][kx]
-    return np.ascontiguousarray(np.transpose(h, (0, 2, 1, 3)))
-
-
-def full_from_half(h, n1):
-    """Inverse of the layout of `half_spectrum`: [3][ky][kz][kx] -> full [3][kz][ky][kx] spectrum."""
-    hz = np.transpose(h, (0, 2, 1, 3))  # [3][kz][ky][kx<=n1/2]
-    n3, n2 = hz.shape[1], hz.shape[2]
-    full = np.zeros((hz.shape[0], n3, n2, n1), dtype=np.complex128)
-    full[..., : n1 // 2 + 1] = hz
-    kz = (-np.arange(n3)) % n3
-    ky = (-np.arange(n2)) % n2
-    for kx in range(n1 // 2 + 1, n1):
-        full[..., kx] = np.conj(hz[:, kz][:, :, ky][..., n1 - kx])
-    return full

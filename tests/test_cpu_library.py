@@ -56,7 +56,7 @@ def test_invalid_grid_rejected_without_device(lib):
 
 
 def test_half_spectrum_layout_roundtrip():
-    from paper_1905_12725_b200.dbfft import full_from_half, half_spectrum
+    from spectra import full_from_half, half_spectrum
     u = ms.random_field((3, 6, 4, 8), 3)  # [3][z][y][x]: n = (8, 4, 6)
     h = half_spectrum(u)
     assert h.shape == (3, 4, 6, 5)  # [3][ky][kz][kx<=n1/2]

@@ -6,6 +6,7 @@ import numpy as np
 import pytest
 
 from oracle import dbfft_oracle as O
+from spectra import full_from_half, half_spectrum
 from synth import configs, microstructure as ms
 
 pytestmark = pytest.mark.gpu
@@ -27,11 +28,11 @@ def rel(a, b):
 
 
 def to_gpu_spec(dbf, u_real):
-    return torch.from_numpy(dbf.half_spectrum(u_real)).cuda()
+    return torch.from_numpy(half_spectrum(u_real)).cuda()
 
 
 def gpu_full(dbf, t, n1):
-    return dbf.full_from_half(t.cpu().numpy(), n1)
+    return full_from_half(t.cpu().numpy(), n1)
 
 
 def two_phase(n, seed, frac=0.3):

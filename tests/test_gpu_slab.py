@@ -6,6 +6,7 @@ import numpy as np
 import pytest
 
 from oracle import dbfft_oracle as O
+from spectra import full_from_half, half_spectrum
 from synth import configs, microstructure as ms
 
 pytestmark = pytest.mark.gpu
@@ -42,13 +43,13 @@ def test_apply_K_small_loopback(dbf, n, P):
     ctx = dbf.DBFFT(n, kinematics="small", world=P, loopback=True)
     ctx.set_phases(ph, ISO2)
     u = ms.random_field((3, n[2], n[1], n[0]), 22)
-    f = ctx.apply_K(torch.from_numpy(dbf.half_spectrum(u)).cuda())
+    f = ctx.apply_K(torch.from_numpy(half_spectrum(u)).cuda())
     ref, _ = O.apply_K(O.fft(u), O.stiffness_field(ph, ISO2), O.frequency_grid(n))
-    assert rel(dbf.full_from_half(f.cpu().numpy(), n[0]), ref) <= 1e-12
+    assert rel(full_from_half(f.cpu().numpy(), n[0]), ref) <= 1e-12
     # preconditioner with the rank-local ky offsets of xi_y
-    z = ctx.precond(torch.from_numpy(dbf.half_spectrum(u)).cuda())
+    z = ctx.precond(torch.from_numpy(half_spectrum(u)).cuda())
     zref = O.precondition(O.fft(u), O.volume_average(O.stiffness_field(ph, ISO2)), O.frequency_grid(n))
-    assert rel(dbf.full_from_half(z.cpu().numpy(), n[0]), zref) <= 1e-12
+    assert rel(full_from_half(z.cpu().numpy(), n[0]), zref) <= 1e-12
 
 
 @pytest.mark.parametrize("P", [2, 4])
@@ -61,10 +62,10 @@ def test_apply_K_finite_loopback(dbf, P):
     ctx.set_phases(ph, mats)
     ctx.eval_state(F.reshape(9, n[2], n[1], n[0]))
     u = ms.random_field((3, n[2], n[1], n[0]), 25)
-    f = ctx.apply_K(torch.from_numpy(dbf.half_spectrum(u)).cuda())
+    f = ctx.apply_K(torch.from_numpy(half_spectrum(u)).cuda())
     _, K = O.neo_hookean(F, np.array([1.0, 10.0])[ph], np.array([2.5, 25.0])[ph])
     ref, _ = O.apply_K(O.fft(u), K, O.frequency_grid(n), finite=True)
-    assert rel(dbf.full_from_half(f.cpu().numpy(), n[0]), ref) <= 1e-12
+    assert rel(full_from_half(f.cpu().numpy(), n[0]), ref) <= 1e-12
 
 
 @pytest.mark.parametrize("P", [2, 8])
@@ -135,7 +136,7 @@ def test_apply_K_small_peer(dbf, n, P):
         pytest.skip("P must divide n2 and n3")
     ph = two_phase(n, 31)
     u_real = ms.random_field((3, n[2], n[1], n[0]), 32)
-    u = torch.from_numpy(dbf.half_spectrum(u_real)).cuda()
+    u = torch.from_numpy(half_spectrum(u_real)).cuda()
     out = {}
     for tr in ("nccl", "peer"):
         ctx = dbf.DBFFT(n, kinematics="small", world=P, loopback=True, transport=tr)
@@ -144,7 +145,7 @@ def test_apply_K_small_peer(dbf, n, P):
         ctx.close()
     assert np.array_equal(out["peer"], out["nccl"])
     ref, _ = O.apply_K(O.fft(u_real), O.stiffness_field(ph, ISO2), O.frequency_grid(n))
-    assert rel(dbf.full_from_half(out["peer"], n[0]), ref) <= 1e-12
+    assert rel(full_from_half(out["peer"], n[0]), ref) <= 1e-12
 
 
 @pytest.mark.parametrize("P", [2, 4])
@@ -157,10 +158,10 @@ def test_apply_K_finite_peer(dbf, P):
     ctx = dbf.DBFFT(n, kinematics="finite", world=P, loopback=True, transport="peer")
     ctx.set_phases(ph, mats)
     ctx.eval_state(F.reshape(9, n[2], n[1], n[0]))
-    f = ctx.apply_K(torch.from_numpy(dbf.half_spectrum(u)).cuda())
+    f = ctx.apply_K(torch.from_numpy(half_spectrum(u)).cuda())
     _, K = O.neo_hookean(F, np.array([1.0, 10.0])[ph], np.array([2.5, 25.0])[ph])
     ref, _ = O.apply_K(O.fft(u), K, O.frequency_grid(n), finite=True)
-    assert rel(dbf.full_from_half(f.cpu().numpy(), n[0]), ref) <= 1e-12
+    assert rel(full_from_half(f.cpu().numpy(), n[0]), ref) <= 1e-12
 
 
 def test_solve_c4_twin_peer_matches_nccl(dbf):
