@@ -719,7 +719,10 @@ def solve_j2_increment(state, phase, materials, load, dt, tol=1e-10, tol_newton=
 
     Same Newton structure as P:201-221 with sym grad and the
     algorithmic tangent; state committed at the end.  Strain control only
-    (R17).  parity unpinned beyond P15 (constitutive) and P12/P10."""
+    (R17).  Returns `converged` (max|d eps| < tol_newton before max_newton).
+    Pinned by the elasto-viscoplastic laminate (per-layer uniform strains, out-of-plane
+    tractions continuous: a 3-unknown root per increment) and by equilibrium + Hill-Mandel
+    on a heterogeneous polycrystal twin (tests/test_oracle_pins.py)."""
     nz, ny, nx = phase.shape
     XI = frequency_grid((nx, ny, nz), L)
     mask, target = _masks(load)
@@ -750,14 +753,16 @@ def solve_j2_increment(state, phase, materials, load, dt, tol=1e-10, tol_newton=
         de = ifft(sym_grad_hat(dx.u, XI), check=False)  # real part (R6)
         state.u_hat = state.u_hat + dx.u
         eps = eps + de
-        if np.max(np.abs(de)) < tol_newton or newton >= max_newton:
+        last = np.max(np.abs(de))
+        if last < tol_newton or newton >= max_newton:
             break
-    sig, _, eps_p, _ = j2_perzyna(eps, state.eps_p, par["E"], par["nu"], par["sigma_y"],
-                                  par["n"], par["edot0"], dt)
+    sig, _, eps_p, dp = j2_perzyna(eps, state.eps_p, par["E"], par["nu"], par["sigma_y"],
+                                   par["n"], par["edot0"], dt)
     state.eps_p = eps_p
     state.ebar = target.copy()
-    return dict(eps=eps, sig=sig, mean_eps=volume_average(eps),
-                mean_sig=volume_average(sig), cg_iters=total_cg, newton_iters=newton)
+    return dict(eps=eps, sig=sig, mean_eps=volume_average(eps), eps_p=eps_p, dp=dp,
+                mean_sig=volume_average(sig), cg_iters=total_cg, newton_iters=newton,
+                converged=bool(last < tol_newton))
 
 
 # ----------------------------------------------------------------------------

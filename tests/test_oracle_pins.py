@@ -698,3 +698,164 @@ def test_equilibrium_and_loading_residual_closed_forms():
     assert O.equilibrium_residual(r["sig"], X1) <= 1e-10
     assert O.loading_residual(r["mean_eps"], r["mean_sig"], L["target"], L["mask"]) <= 1e-15
     assert O.incompatibility(r["eps"], X1, finite=False) <= 1e-12
+
+
+# ----------------------------------------------------------------- mixed hyperelastic families
+
+def _nh_energy(F, mu, kappa):
+    """R14: W = mu/2 (tr F^T F - 3) - mu ln J + lam/2 (ln J)^2, lam = kappa - 2 mu/3."""
+    lam = kappa - 2.0 * mu / 3.0
+    J = np.linalg.det(F)
+    return 0.5 * mu * (np.trace(F.T @ F) - 3.0) - mu * np.log(J) + 0.5 * lam * np.log(J) ** 2
+
+
+def test_hyperelastic_mixed_phase_dispatch():
+    """A phase map mixing neo-Hookean (R14) and SVK phases: at every voxel P = dW/dF of
+    THAT voxel's phase energy (central differences of W, written out here), and K = dP/dF by
+    differences of the mixed P — a phase routed to the wrong law or parameters fails."""
+    mats = [dict(kind="neohooke", mu=1.0, kappa=2.5), dict(kind="svk", E=70.0, nu=0.3),
+            dict(kind="neohooke", mu=7.0, kappa=20.0), dict(kind="svk", E=5.0, nu=0.2)]
+    rng = np.random.default_rng(11)
+    nv = 12
+    phase = np.array([0, 1, 2, 3, 3, 2, 1, 0, 1, 3, 0, 2], np.uint16).reshape(1, 1, nv)
+    F = np.eye(3).reshape(3, 3, 1, 1, 1) + 0.3 * rng.standard_normal((3, 3, 1, 1, nv))
+    P, K = O.hyperelastic(F, phase, mats)
+    h = 1e-6
+
+    def W(Fv, m):
+        return _nh_energy(Fv, m["mu"], m["kappa"]) if m["kind"] == "neohooke" else _svk_energy(Fv, m["E"], m["nu"])
+
+    for v in range(nv):
+        m = mats[phase[0, 0, v]]
+        Fv = F[:, :, 0, 0, v]
+        Pfd = np.zeros((3, 3))
+        Kfd = np.zeros((3, 3, 3, 3))
+        for k in range(3):
+            for l in range(3):
+                d = np.zeros((3, 3)); d[k, l] = h
+                Pfd[k, l] = (W(Fv + d, m) - W(Fv - d, m)) / (2 * h)
+                Fp, Fm = F.copy(), F.copy()
+                Fp[k, l, 0, 0, v] += h
+                Fm[k, l, 0, 0, v] -= h
+                Kfd[:, :, k, l] = (O.hyperelastic(Fp, phase, mats)[0][:, :, 0, 0, v]
+                                   - O.hyperelastic(Fm, phase, mats)[0][:, :, 0, 0, v]) / (2 * h)
+        Pv, Kv = P[:, :, 0, 0, v], K[:, :, :, :, 0, 0, v]
+        assert np.abs(Pv - Pfd).max() <= 1e-7 * max(np.abs(Pv).max(), 1.0), (v, m)
+        assert np.abs(Kv - Kfd).max() <= 1e-6 * np.abs(Kv).max(), (v, m)
+
+
+# ----------------------------------------------------------------- loading residual (P:282)
+
+def test_loading_residual_stress_branch_closed_forms():
+    """Eq. chedckimp under mixed control, worked by hand: the stress-controlled part is
+    ||<sigma> - sigma_bar|| / ||<sigma>|| over the masked components, the strain part
+    ||<eps> - eps_bar|| / ||eps_bar|| over the others, the residual the larger of the two."""
+    mask = np.zeros((3, 3), bool)
+    mask[0, 0] = True                          # sigma_xx prescribed
+    target = np.diag([2.0, 1e-3, 0.0])         # sigma_xx = 2; eps_yy = 1e-3, other strains 0
+    mean_sig = np.diag([2.5, 0.0, 0.0])        # |2.5 - 2| / 2.5 = 0.2
+    mean_eps = np.diag([7.0, 1e-3 + 1e-6, 0.0])  # eps_xx is free; |1e-6| / 1e-3 = 1e-3
+    assert O.loading_residual(mean_eps, mean_sig, target, mask) == pytest.approx(0.2, rel=1e-14)
+    # strain part dominating: <eps_yy> off by 5e-4 -> 0.5; stress exact
+    mean_sig = np.diag([2.0, 0.0, 0.0])
+    mean_eps = np.diag([7.0, 1.5e-3, 0.0])
+    assert O.loading_residual(mean_eps, mean_sig, target, mask) == pytest.approx(0.5, rel=1e-12)
+    # a zero prescribed stress: relative to ||<sigma>|| (3, 4 -> 5), not to the target
+    mask = np.zeros((3, 3), bool)
+    mask[1, 1] = mask[2, 2] = True
+    target = np.diag([1e-3, 0.0, 0.0])
+    mean_sig = np.diag([0.0, 3.0, 4.0])
+    mean_eps = np.diag([1e-3, 9.0, 9.0])
+    assert O.loading_residual(mean_eps, mean_sig, target, mask) == pytest.approx(1.0, rel=1e-14)
+
+
+# ----------------------------------------------------------------- heterogeneous J2 Newton (P:201-221, R16)
+
+def _j2_mats(sy):
+    return [dict(kind="j2", E=J2P["E"], nu=J2P["nu"], sigma_y=s, n=J2P["nexp"], edot0=J2P["edot0"]) for s in sy]
+
+
+def _j2_point(eps, epsp, m, dt):
+    s, C, ep, dp = O.j2_perzyna(eps.reshape(3, 3, 1), epsp.reshape(3, 3, 1), m["E"], m["nu"], m["sigma_y"],
+                                m["n"], m["edot0"], dt)
+    return s[..., 0], ep[..., 0], dp[0]
+
+
+def test_j2_laminate_elasto_viscoplastic():
+    """Elasto-viscoplastic laminate (layers normal to x, 50/50, yield stresses 300 / 450), three
+    plastic increments under strain control.  The exact discrete solution has uniform strain in
+    each layer: the in-plane components (yy, zz, yz) equal the macro strain, the out-of-plane
+    ones (xx, xy, xz) average to it, and the tractions sigma_xx, sigma_xy, sigma_xz are continuous
+    across the interfaces (equilibrium).  That is a 3-unknown root per increment on the
+    material-point update (P15) — solved here with scipy, independent of the DBFFT machinery —
+    against solve_j2_increment's Newton-PCG on the full grid (even layer widths: no Nyquist
+    content, R1)."""
+    from scipy.optimize import root
+    n = (8, 4, 4)
+    ph = ms.laminate(n, axis=0, thickness=4)            # phase 1 in the first 4 x-planes
+    mats = _j2_mats([300.0, 450.0])
+    st = O.J2State(n)
+    dt = 1.0
+    oop = [(0, 0), (0, 1), (0, 2)]
+    base = 2e-3 * np.diag([-0.5, -0.5, 1.0])
+    base[0, 1] = base[1, 0] = 0.6e-3
+    base[1, 2] = base[2, 1] = 0.3e-3
+    ep = [np.zeros((3, 3)), np.zeros((3, 3))]
+    for k in range(1, 4):
+        target = k * base
+
+        def layers(a):
+            e = [target.copy(), target.copy()]
+            for (i, j), v in zip(oop, a):
+                e[0][i, j] = e[0][j, i] = v
+                e[1][i, j] = e[1][j, i] = 2.0 * target[i, j] - v   # 50/50 average
+            return e
+
+        def resid(a):
+            e = layers(a)
+            s0 = _j2_point(e[0], ep[0], mats[0], dt)[0]
+            s1 = _j2_point(e[1], ep[1], mats[1], dt)[0]
+            return [(s0[i, j] - s1[i, j]) / J2P["E"] for (i, j) in oop]
+
+        sol = root(resid, [target[i, j] for (i, j) in oop], method="hybr", tol=1e-14)
+        assert np.max(np.abs(resid(sol.x))) < 1e-15   # tractions equal to ~1e-12 relative
+        e = layers(sol.x)
+        pts = [_j2_point(e[p], ep[p], mats[p], dt) for p in range(2)]
+        res = O.solve_j2_increment(st, ph, mats, dict(target=target, mask=np.zeros((3, 3), bool)), dt,
+                                   tol=1e-12, tol_newton=1e-12)
+        assert res["converged"]
+        for p in range(2):
+            sel = ph == p
+            scale = np.abs(e[p]).max()
+            assert np.abs(res["eps"][:, :, sel] - e[p][:, :, None]).max() <= 1e-10 * scale, (k, p)
+            assert np.abs(res["sig"][:, :, sel] - pts[p][0][:, :, None]).max() <= 1e-9 * np.abs(pts[p][0]).max()
+            assert np.abs(res["eps_p"][:, :, sel] - pts[p][1][:, :, None]).max() <= 1e-10 * scale
+        ep = [pts[0][1], pts[1][1]]
+        mean_ref = 0.5 * (pts[0][0] + pts[1][0])
+        assert np.abs(res["mean_sig"] - mean_ref).max() <= 1e-10 * np.abs(mean_ref).max()
+    assert pts[0][2] > 0 and pts[1][2] > 0   # both layers flow in the last increment
+
+
+def test_j2_polycrystal_twin_equilibrium_hill_mandel():
+    """Heterogeneous J2 polycrystal (c5 recipe, 8^3 / 6 grains, lognormal yield stresses), three
+    increments into plastic flow: every increment converges (flag), the final stress field is in
+    equilibrium (Eq. chedckeq, <= 1e-9: PCG tol 1e-10 then one more constitutive update)
+    and satisfies Hill-Mandel <sigma:eps> = <sigma>:<eps> (an equilibrated stress against a
+    compatible fluctuation strain: their product averages to zero), and the plastic strain is
+    traceless (J2 flow) and non-zero."""
+    cfg = configs.c5(n=8, grains=6, increments=3)
+    st = O.J2State(cfg["n"])
+    newton = []
+    for L in cfg["loads"]:
+        res = O.solve_j2_increment(st, cfg["phase"], cfg["materials"], L, cfg["dt"], tol=1e-10)
+        assert res["converged"]
+        newton.append(res["newton_iters"])
+    assert newton[0] == 1 and newton[-1] >= 3   # elastic first increment; plastic Newton later
+    XI = O.frequency_grid(cfg["n"])
+    assert O.equilibrium_residual(res["sig"], XI) <= 1e-9
+    hm = O.volume_average(np.einsum("ij...,ij...->...", res["sig"], res["eps"]))
+    macro = np.sum(res["mean_sig"] * res["mean_eps"])
+    assert abs(hm - macro) <= 1e-9 * abs(macro)
+    tr = res["eps_p"][0, 0] + res["eps_p"][1, 1] + res["eps_p"][2, 2]
+    assert np.abs(tr).max() <= 1e-18 + 1e-12 * np.abs(res["eps_p"]).max()
+    assert (res["dp"] > 0).sum() > 0
