@@ -9,8 +9,8 @@ Everything follows Lucarini & Segurado, "DBFFT" (PAPER.md = /root/reference/
 PAPER.md; citations are "P:<line> <equation/section>").  Where the paper is
 silent or garbled, the reading of SURVEY.md section 8(c) (R1..R22) is used and
 named.  Deliberate choices:
-  * full complex spectra (numpy.fft.fftn as the library FFT step), no half
-    spectrum, no fusion;
+  * full complex spectra (scipy.fft.fftn on all host cores as the library FFT
+    step), no half spectrum, no fusion;
   * tensors are full 3x3 / 3x3x3x3 arrays contracted with explicit einsum
     index strings (no Voigt/Mandel packing);
   * spectra are mean-normalised, u_hat = F(u)/N (R5), so the Euclidean
@@ -21,7 +21,14 @@ named.  Deliberate choices:
 Pinned by tests/test_oracle_pins.py (-m "not gpu").  Functions that no pin
 covers say "parity unpinned" in their docstring.
 """
+import os
+
 import numpy as np
+import scipy.fft
+
+# the library FFT step runs on every host core (scipy's pocketfft, the same transform numpy's
+# fft computes; bit-identical results here); the rest of the oracle is plain numpy
+FFT_WORKERS = os.cpu_count() or 1
 
 # ----------------------------------------------------------------------------
 # Volume average <a> = (1/N) sum_x a(x) (P:255 "average of the stiffness", the
@@ -87,13 +94,13 @@ def null_set(XI):
 def fft(f):
     """F(f)/N over the last three axes (library FFT as one step)."""
     N = f.shape[-1] * f.shape[-2] * f.shape[-3]
-    return np.fft.fftn(f, axes=(-3, -2, -1)) / N
+    return scipy.fft.fftn(f, axes=(-3, -2, -1), workers=FFT_WORKERS) / N
 
 
 def ifft(fh, check=True):
     """Inverse of `fft`; returns the real part, asserting |Im| is round-off only."""
     N = fh.shape[-1] * fh.shape[-2] * fh.shape[-3]
-    f = np.fft.ifftn(fh, axes=(-3, -2, -1)) * N
+    f = scipy.fft.ifftn(fh, axes=(-3, -2, -1), workers=FFT_WORKERS) * N
     if check:
         scale = max(np.max(np.abs(f.real)), 1e-300)
         assert np.max(np.abs(f.imag)) <= 1e-10 * scale, "spectrum is not Hermitian"
