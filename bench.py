@@ -8,13 +8,17 @@ residual, mean tangent and preconditioner, and Newton-PCG to tol_eq = 1e-10 / Ne
 i.e. every row of SURVEY 8(a).  Steps walk the increments in order (state carried over);
 after increment 10 the state is reset (inside the step that wraps).
 
-value = voxels x PCG iterations / max-over-ranks device time.
+value = voxels x PCG iterations / max-over-ranks device time, measured on the production path
+(CUDA graphs with the device-side PCG loop, no per-kernel instrumentation).  Per-kernel times
+(kernel_ms, the roofline of pass_X) come from a separate profiled pass of the next steps of the
+walk (events around every launch, one PCG iteration per host poll so no launch is an early exit).
 N > 1: the same c4 problem slab-decomposed over the N GPUs (z-slabs / ky-slabs, NCCL
-all-to-all + all-reduce; "scaling": "strong").  If NCCL cannot be initialised the run falls
-back to independent replicas ("scaling": "weak") and says so in config.parallelism.
+all-to-all + all-reduce, or the peer transport; "scaling": "strong"); a rank that cannot build
+its slab context fails the run (no silent fallback).  --replicas runs N independent copies.
 
---impl reference: the CPU oracle (oracle/dbfft_oracle.py) timed on this host, one oracle PCG
-iteration per step on c4's 128^3 twin (bounded sample).
+--impl reference: the CPU oracle (oracle/dbfft_oracle.py) timed on this host: one oracle PCG
+iteration (apply_K + preconditioner + CG algebra) of c4's first Newton step at 256^3 per step,
+FFTs on all host cores.
 """
 import argparse
 import json
@@ -169,17 +173,14 @@ def gpu_arm(args):
     mode = "single GPU"
     phase = cfg["phase"]
     if world > 1 and not args.replicas:
-        try:
-            ctx = dbfft.DBFFT(n, kinematics="finite", device=local, stream=stream, world=world, rank=rank,
-                              transport=args.transport)
-            nzl = n[2] // world
-            phase = np.ascontiguousarray(cfg["phase"][rank * nzl:(rank + 1) * nzl])
-            mode = (f"slab x{world} (z-slabs / ky-slabs, " +
-                    ("passes store into peer memory (VMM windows) + NCCL all-reduce)" if args.transport == "peer"
-                     else "NCCL all-to-all + all-reduce)"))
-        except Exception as exc:  # noqa: BLE001
-            mode = f"replicas x{world} (slab init failed: {str(exc)[:120]})"
-            ctx = dbfft.DBFFT(n, kinematics="finite", device=local, stream=stream)
+        # no fallback: a slab context that cannot be built (NCCL, peer windows) fails the run
+        ctx = dbfft.DBFFT(n, kinematics="finite", device=local, stream=stream, world=world, rank=rank,
+                          transport=args.transport)
+        nzl = n[2] // world
+        phase = np.ascontiguousarray(cfg["phase"][rank * nzl:(rank + 1) * nzl])
+        mode = (f"slab x{world} (z-slabs / ky-slabs, " +
+                ("passes store into peer memory (VMM windows) + NCCL all-reduce)" if args.transport == "peer"
+                 else "NCCL all-to-all + all-reduce)"))
     else:
         ctx = dbfft.DBFFT(n, kinematics="finite", device=local, stream=stream)
         if world > 1:
@@ -203,7 +204,6 @@ def gpu_arm(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ctx.profile(True)
     launches0 = ctx.launch_count()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -220,6 +220,15 @@ def gpu_arm(args):
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
     launches = ctx.launch_count() - launches0
+    pcg_loop = ctx.info()
+    # per-kernel device times: a separate pass over the next steps of the walk with CUDA events
+    # around every launch (graphs off, one PCG iteration per poll: no early-exit launches)
+    prof_steps = max(1, min(args.steps, args.profile_steps))
+    ctx.profile(True)
+    prof_iters = 0
+    for _ in range(prof_steps):
+        prof_iters += step()["cg_iters"]
+    torch.cuda.synchronize()
     prof = ctx.profile_read()
     ctx.profile(False)
     t_local = ms / 1e3
@@ -321,13 +330,19 @@ def gpu_arm(args):
                                   "F_zz->1.10 in 10 increments, P_xx=P_yy=0; one step = one increment",
                       "grid": list(n), "parallelism": mode,
                       "l2": "inputs larger than L2 (working set ~15 GB per GPU)", "tol_eq": 1e-10,
-                      "tol_newton": 1e-6, "cg_iters_timed": iters, "newton_iters_timed": newton},
+                      "tol_newton": 1e-6, "cg_iters_timed": iters, "newton_iters_timed": newton,
+                      "pcg_loop": pcg_loop,
+                      "timing": "value: CUDA events around the K steps on the production path (graphs, "
+                                "no instrumentation); kernel_ms / roofline: a separate profiled pass of "
+                                f"{prof_steps} further steps ({prof_iters} PCG iterations)"},
            "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches),
            "kernel_ms": {k: v[0] for k, v in prof.items()}}
     clk_sum = clk.summary()
     out["clocks"] = clk_sum
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(iters=2)
+        del ctx
+        torch.cuda.empty_cache()
+        out["cpu_baseline"] = cpu_baseline(args.cpu_n, reps=3)
     if rank == 0:
         print(json.dumps(out))
     if world > 1:
@@ -337,7 +352,40 @@ def gpu_arm(args):
 # ------------------------------------------------------------------------------------------ oracle
 
 
-def oracle_setup(n=128):
+def host_info():
+    """Host cores, CPU model and memory (recorded with the oracle baseline)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    info["cpu_model"] = line.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as f:
+            for line in f:
+                k, v = line.split(":", 1)
+                if k in ("MemTotal", "MemAvailable"):
+                    info[k.lower() + "_gb"] = round(int(v.split()[0]) / 2 ** 20, 1)
+    except OSError:
+        pass
+    return info
+
+
+ORACLE_BYTES_PER_VOXEL = 1400  # full 3x3x3x3 tangent (648 B) + spectra / temporaries of one iteration
+
+
+def oracle_grid(n_req):
+    """Largest grid <= n_req whose oracle iteration fits the host memory (c4 at 256^3 needs ~24 GB)."""
+    avail = host_info().get("memavailable_gb")
+    n = n_req
+    while avail is not None and n > 32 and n ** 3 * ORACLE_BYTES_PER_VOXEL > 0.8 * avail * 2 ** 30:
+        n //= 2
+    return n
+
+
+def oracle_setup(n=256):
+    """c4's first Newton step at grid n (the c4 phase map at n = 256): the tangent field at the
+    first increment's homogeneous F, its mean, and the rhs b = F(div P) — oracle functions only."""
     from oracle import dbfft_oracle as O
     from synth import configs
     cfg = configs.c4(n=n, radius_vox=max(1, round(10 * n / 256)))
@@ -347,8 +395,9 @@ def oracle_setup(n=128):
     L = cfg["loads"][0]
     F = np.where(L["mask"], np.eye(3), L["target"]).reshape(3, 3, 1, 1, 1) * np.ones((1, 1) + ph.shape)
     P, K = O.neo_hookean(F, mu, kap)
+    del F, mu, kap
     XI = O.frequency_grid(cfg["n"])
-    Kbar = K.mean(axis=(-3, -2, -1))
+    Kbar = O.volume_average(K)
     b = O.rhs_from_stress(P, XI)
     return dict(O=O, K=K, XI=XI, Kbar=Kbar, b=b, mask=L["mask"], N=ph.size, n=cfg["n"])
 
@@ -365,45 +414,66 @@ def oracle_iteration(S, p, r, rz):
     return p, r, rz_new
 
 
-def cpu_baseline(iters=2):
-    S = oracle_setup(128)
+def oracle_start(S):
     O = S["O"]
     r = S["b"]
     z = O.precondition(r, S["Kbar"], S["XI"])
-    p, rz = z, O.inner(r, z)
-    t0 = time.perf_counter()
-    for _ in range(iters):
+    return z, r, O.inner(r, z)
+
+
+def oracle_sample_text(n, what):
+    from oracle import dbfft_oracle as O
+    return (f"{what} of c4's first Newton step at {n}^3 (c4's phase map, full 3x3x3x3 tangent, full complex "
+            f"spectra): apply_K + preconditioner + CG algebra; scipy.fft on {O.FFT_WORKERS} threads, the rest "
+            "numpy on one thread")
+
+
+def cpu_baseline(n_req=256, reps=3):
+    """The oracle as it stands on this host: median over `reps` PCG iterations at c4's grid."""
+    n = oracle_grid(n_req)
+    from oracle import dbfft_oracle as O
+    S = oracle_setup(n)
+    p, r, rz = oracle_start(S)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
         p, r, rz = oracle_iteration(S, p, r, rz)
-    t = time.perf_counter() - t0
-    return {"value": S["N"] * iters / t, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{iters} oracle PCG iterations (apply_K + preconditioner + CG algebra) of c4's first "
-                      f"Newton step on its 128^3 twin (same structure, r=5); numpy single-threaded FFT/einsum",
-            "seconds": t}
+        times.append(time.perf_counter() - t0)
+    t = float(np.median(times))
+    what = f"median of {reps} oracle PCG iterations"
+    if n != n_req:
+        what += f" (host memory too small for {n_req}^3: measured at {n}^3)"
+    return {"value": S["N"] / t, "unit": UNIT, "cores": O.FFT_WORKERS, "kind": "oracle",
+            "sample": oracle_sample_text(n, what), "seconds_per_iteration": t, "iterations": times,
+            "grid": [n] * 3, "host": host_info()}
 
 
 def reference_arm(args):
+    """The oracle (this tier's reference) on the bench's metric and workload: one oracle PCG
+    iteration of c4 at 256^3 per step (one warm-up iteration: the oracle has no state to warm)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    S = oracle_setup(128)
-    O = S["O"]
-    r = S["b"]
-    z = O.precondition(r, S["Kbar"], S["XI"])
-    p, rz = z, O.inner(r, z)
-    for _ in range(args.warmup):
+    n = oracle_grid(args.cpu_n)
+    from oracle import dbfft_oracle as O
+    S = oracle_setup(n)
+    p, r, rz = oracle_start(S)
+    for _ in range(min(args.warmup, 1)):
         p, r, rz = oracle_iteration(S, p, r, rz)
     t0 = time.perf_counter()
     for _ in range(args.steps):
         p, r, rz = oracle_iteration(S, p, r, rz)
     t = time.perf_counter() - t0
     v = S["N"] * args.steps / t
-    sample = ("one oracle PCG iteration per step (apply_K + preconditioner + CG algebra) on c4's 128^3 twin, "
-              "first Newton step; numpy single-threaded")
+    sample = oracle_sample_text(n, "one oracle PCG iteration per step")
     print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
                       "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
                       "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                      "data": "synthetic", "config": {"workload": "c4 128^3 twin (bounded oracle sample)"},
-                      "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+                      "data": "synthetic",
+                      "config": {"workload": f"c4: {n}^3 finite-strain neo-Hookean (oracle, first Newton step)",
+                                 "grid": [n] * 3, "host": host_info()},
+                      "cpu_baseline": {"value": v, "unit": UNIT, "cores": O.FFT_WORKERS, "kind": "oracle",
+                                       "sample": sample},
                       "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
 
 
@@ -417,6 +487,8 @@ def main():
     ap.add_argument("--check-every", type=int, default=8)
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-n", type=int, default=256, help="grid of the oracle baseline (c4 at 256^3)")
+    ap.add_argument("--profile-steps", type=int, default=2, help="steps of the separate per-kernel profiled pass")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of slabs")
     ap.add_argument("--transport", choices=("nccl", "peer"), default="nccl",
                     help="N > 1 slabs: NCCL all-to-all exchanges, or passes storing into peer memory")

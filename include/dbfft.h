@@ -254,6 +254,13 @@ const char* dbfft_profile_name(int32_t kernel_id);
 dbfft_status dbfft_launch_count(dbfft_ctx ctx, int64_t* count);
 int32_t dbfft_profile_count(void);
 
+/* One-line JSON description of ctx (host): device and SM count, world / rank / loopback, the
+ * transport of the two all-to-alls ("none" | "nccl" | "peer"), whether an NCCL communicator is
+ * live, and how the last PCG loop ran ("device-side WHILE graph", host-polled graph rounds or
+ * eager, with the reason of a fallback).  DBFFT_E_INVALID_ARG if it does not fit in cap bytes
+ * (truncated, NUL-terminated).  (sync) */
+dbfft_status dbfft_info(dbfft_ctx ctx, char* buf, int32_t cap);
+
 #ifdef __cplusplus
 }
 #endif

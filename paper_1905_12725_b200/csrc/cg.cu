@@ -31,6 +31,13 @@ DBF_DEV void apply_M(const PrecQ& Q, const Pt& p, const cplx* r, cplx* z) {
 
 DBF_DEV double cdot(cplx a, cplx b) { return a.x * b.x + a.y * b.y; }  // Re(conj(a) b)
 
+// M's 36 coefficients live in device memory (updated when Cbar changes, so a captured CUDA graph
+// of the PCG loop stays valid across solves); every CTA stages them in shared memory once
+DBF_DEV void load_prec(PrecQ& sq, const PrecQ* __restrict__ q) {
+  for (int i = threadIdx.x; i < 36; i += blockDim.x) sq.Q[i] = q->Q[i];
+  __syncthreads();
+}
+
 template <int NV>
 DBF_DEV void block_store(double (&v)[NV], double* partials) {
   __shared__ double red[BLK / 32][NV];
@@ -47,7 +54,9 @@ DBF_DEV void block_store(double (&v)[NV], double* partials) {
   }
 }
 
-__global__ void __launch_bounds__(BLK, MINB) k_precond(SpecGeom g, PrecQ Q, const cplx* __restrict__ r, cplx* __restrict__ z) {
+__global__ void __launch_bounds__(BLK, MINB) k_precond(SpecGeom g, const PrecQ* __restrict__ q, const cplx* __restrict__ r, cplx* __restrict__ z) {
+  __shared__ PrecQ Q;
+  load_prec(Q, q);
   for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < g.Hs; i += (long long)gridDim.x * BLK) {
     Pt p = point(g, i);
     cplx rv[3] = {__ldg(r + i), __ldg(r + g.Hs + i), __ldg(r + 2 * g.Hs + i)};
@@ -60,7 +69,9 @@ __global__ void __launch_bounds__(BLK, MINB) k_precond(SpecGeom g, PrecQ Q, cons
 }
 
 // p = M r ; partials (<r, p>, <r, r>)
-__global__ void __launch_bounds__(BLK, MINB) k_cg_init(SpecGeom g, PrecQ Q, const cplx* __restrict__ r, cplx* __restrict__ pv, double* partials) {
+__global__ void __launch_bounds__(BLK, MINB) k_cg_init(SpecGeom g, const PrecQ* __restrict__ q, const cplx* __restrict__ r, cplx* __restrict__ pv, double* partials) {
+  __shared__ PrecQ Q;
+  load_prec(Q, q);
   double acc[2] = {0.0, 0.0};
   for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < g.Hs; i += (long long)gridDim.x * BLK) {
     Pt p = point(g, i);
@@ -80,9 +91,11 @@ __global__ void __launch_bounds__(BLK, MINB) k_cg_init(SpecGeom g, PrecQ Q, cons
 // x += alpha p ; r -= alpha q ; z = M r ; partials (<r, z>, <r, r>)
 // r -= alpha q, z = M r on the fly, partial <r,z>, <r,r> (x += alpha p is deferred to the
 // direction kernel, which reads p anyway: 3 vector transfers here instead of 6)
-__global__ void __launch_bounds__(BLK, MINB) k_cg_update(SpecGeom g, PrecQ Q, const CgDev* __restrict__ cg, cplx* __restrict__ r,
+__global__ void __launch_bounds__(BLK, MINB) k_cg_update(SpecGeom g, const PrecQ* __restrict__ pq, const CgDev* __restrict__ cg, cplx* __restrict__ r,
                                                    const cplx* __restrict__ qv, double* partials) {
   if (cg->converged | cg->breakdown) return;
+  __shared__ PrecQ Q;
+  load_prec(Q, pq);
   const double alpha = cg->alpha;
   double acc[2] = {0.0, 0.0};
   for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < g.Hs; i += (long long)gridDim.x * BLK) {
@@ -143,17 +156,28 @@ DBF_DEV void cg_direction_body(const SpecGeom& g, const PrecQ& Q, double alpha, 
   }
 }
 
-__global__ void __launch_bounds__(BLK, 2) k_cg_direction(SpecGeom g, PrecQ Q, const CgDev* __restrict__ cg, cplx* __restrict__ x,
+__global__ void __launch_bounds__(BLK, 2) k_cg_direction(SpecGeom g, const PrecQ* __restrict__ q, const CgDev* __restrict__ cg, cplx* __restrict__ x,
                                                       cplx* __restrict__ pv, const cplx* __restrict__ r) {
   if (cg->breakdown) return;
+  __shared__ PrecQ Q;
+  load_prec(Q, q);
   const bool do_x = cg->xphase != 0, do_p = cg->converged == 0;
   if (do_x && do_p) cg_direction_body<true, true>(g, Q, cg->alpha, cg->beta, x, pv, r);
   else if (do_p) cg_direction_body<false, true>(g, Q, cg->alpha, cg->beta, x, pv, r);
   else if (do_x) cg_direction_body<true, false>(g, Q, cg->alpha, cg->beta, x, pv, r);
 }
 
-__global__ void k_fin_x(CgDev* cg) {
-  if (threadIdx.x == 0) cg->xphase = 0;
+// end of a PCG iteration; inside the device-side loop (a CUDA graph WHILE node) it also decides
+// whether the body runs again
+__global__ void k_fin_x(CgDev* cg, cudaGraphConditionalHandle cond, int set_cond) {
+  if (threadIdx.x != 0) return;
+  cg->xphase = 0;
+  if (set_cond) cudaGraphSetConditional(cond, (cg->converged | cg->breakdown) ? 0u : 1u);
+}
+
+// entry of the device-side loop: run the body only if PCG has not stopped yet
+__global__ void k_loop_cond(const CgDev* cg, cudaGraphConditionalHandle cond) {
+  if (threadIdx.x == 0) cudaGraphSetConditional(cond, (cg->converged | cg->breakdown) ? 0u : 1u);
 }
 
 // r = b - Ax ; partial <r, r>
@@ -330,12 +354,13 @@ __global__ void k_fin_true(CgDev* cg, const double* loc) {
   cg->converged = (cg->eps_eq <= cg->tol_eq && cg->eps_load <= cg->tol_load) ? 1 : 0;
 }
 
-// loopback all-reduce over P virtual ranks of one process: v[r][k] <- op_r v[r][k] for all r
-__global__ void k_allreduce_lb(double* const* v, int P, int k, int is_max) {
+// loopback all-reduce over P virtual ranks of one process: v[r][off + j] <- op_r v[r][off + j]
+// (v: the slabs' loc buffers, a device array uploaded once at creation)
+__global__ void k_allreduce_lb(double* const* v, int off, int P, int k, int is_max) {
   for (int j = threadIdx.x; j < k; j += blockDim.x) {
-    double s = v[0][j];
-    for (int r = 1; r < P; ++r) s = is_max ? fmax(s, v[r][j]) : s + v[r][j];
-    for (int r = 0; r < P; ++r) v[r][j] = s;
+    double s = v[0][off + j];
+    for (int r = 1; r < P; ++r) s = is_max ? fmax(s, v[r][off + j]) : s + v[r][off + j];
+    for (int r = 0; r < P; ++r) v[r][off + j] = s;
   }
 }
 
@@ -374,25 +399,29 @@ __global__ void k_fill(double* p, long long n, double v) {
 
 int cg_blocks() { return nblk(); }
 
-cudaError_t launch_precond(const SpecGeom& g, const PrecQ& q, const cplx* r, cplx* z, cudaStream_t s) {
+cudaError_t launch_precond(const SpecGeom& g, const PrecQ* q, const cplx* r, cplx* z, cudaStream_t s) {
   k_precond<<<nblk(), BLK, 0, s>>>(g, q, r, z);
   return cudaGetLastError();
 }
-cudaError_t launch_cg_init(const SpecGeom& g, const PrecQ& q, const cplx* r, cplx* p, double* partials, int nblk, cudaStream_t s) {
+cudaError_t launch_cg_init(const SpecGeom& g, const PrecQ* q, const cplx* r, cplx* p, double* partials, int nblk, cudaStream_t s) {
   k_cg_init<<<nblk, BLK, 0, s>>>(g, q, r, p, partials);
   return cudaGetLastError();
 }
-cudaError_t launch_cg_update(const SpecGeom& g, const PrecQ& q, CgDev* cg, cplx* r, const cplx* qv,
+cudaError_t launch_cg_update(const SpecGeom& g, const PrecQ* q, CgDev* cg, cplx* r, const cplx* qv,
                              double* partials, int nblk, cudaStream_t s) {
   k_cg_update<<<nblk, BLK, 0, s>>>(g, q, cg, r, qv, partials);
   return cudaGetLastError();
 }
-cudaError_t launch_cg_direction(const SpecGeom& g, const PrecQ& q, const CgDev* cg, cplx* x, cplx* p, const cplx* r, cudaStream_t s) {
+cudaError_t launch_cg_direction(const SpecGeom& g, const PrecQ* q, const CgDev* cg, cplx* x, cplx* p, const cplx* r, cudaStream_t s) {
   k_cg_direction<<<nblk_dir(), BLK, 0, s>>>(g, q, cg, x, p, r);
   return cudaGetLastError();
 }
-cudaError_t launch_fin_x(CgDev* cg, cudaStream_t s) {
-  k_fin_x<<<1, 32, 0, s>>>(cg);
+cudaError_t launch_fin_x(CgDev* cg, cudaStream_t s, cudaGraphConditionalHandle cond, int set_cond) {
+  k_fin_x<<<1, 32, 0, s>>>(cg, cond, set_cond);
+  return cudaGetLastError();
+}
+cudaError_t launch_loop_cond(const CgDev* cg, cudaGraphConditionalHandle cond, cudaStream_t s) {
+  k_loop_cond<<<1, 32, 0, s>>>(cg, cond);
   return cudaGetLastError();
 }
 cudaError_t launch_fin_init(CgDev* cg, const double* loc, cudaStream_t s) {
@@ -415,8 +444,8 @@ cudaError_t launch_fin_true(CgDev* cg, const double* loc, cudaStream_t s) {
   k_fin_true<<<1, 32, 0, s>>>(cg, loc);
   return cudaGetLastError();
 }
-cudaError_t launch_allreduce_lb(double* const* v, int P, int k, int is_max, cudaStream_t s) {
-  k_allreduce_lb<<<1, 64, 0, s>>>(v, P, k, is_max);
+cudaError_t launch_allreduce_lb(double* const* v, int off, int P, int k, int is_max, cudaStream_t s) {
+  k_allreduce_lb<<<1, 64, 0, s>>>(v, off, P, k, is_max);
   return cudaGetLastError();
 }
 cudaError_t launch_axpy(const SpecGeom& g, cplx* y, const cplx* x, double a, cudaStream_t s) {

@@ -33,18 +33,21 @@ struct SpecGeom {
   int n1;
 };
 
-cudaError_t launch_precond(const SpecGeom& g, const PrecQ& q, const cplx* r, cplx* z, cudaStream_t s);
-cudaError_t launch_cg_init(const SpecGeom& g, const PrecQ& q, const cplx* r, cplx* p, double* partials, int nblk, cudaStream_t s);
-cudaError_t launch_cg_update(const SpecGeom& g, const PrecQ& q, CgDev* cg, cplx* r, const cplx* qv,
+cudaError_t launch_precond(const SpecGeom& g, const PrecQ* q, const cplx* r, cplx* z, cudaStream_t s);
+cudaError_t launch_cg_init(const SpecGeom& g, const PrecQ* q, const cplx* r, cplx* p, double* partials, int nblk, cudaStream_t s);
+cudaError_t launch_cg_update(const SpecGeom& g, const PrecQ* q, CgDev* cg, cplx* r, const cplx* qv,
                              double* partials, int nblk, cudaStream_t s);
-cudaError_t launch_cg_direction(const SpecGeom& g, const PrecQ& q, const CgDev* cg, cplx* x, cplx* p, const cplx* r, cudaStream_t s);
-cudaError_t launch_fin_x(CgDev* cg, cudaStream_t s);
+cudaError_t launch_cg_direction(const SpecGeom& g, const PrecQ* q, const CgDev* cg, cplx* x, cplx* p, const cplx* r, cudaStream_t s);
+// cond/set_cond: inside the device-side PCG loop (CUDA graph WHILE node) k_fin_x also sets the
+// loop condition to "not converged and no breakdown"
+cudaError_t launch_fin_x(CgDev* cg, cudaStream_t s, cudaGraphConditionalHandle cond = 0, int set_cond = 0);
+cudaError_t launch_loop_cond(const CgDev* cg, cudaGraphConditionalHandle cond, cudaStream_t s);
 cudaError_t launch_fin_init(CgDev* cg, const double* loc, cudaStream_t s);
 cudaError_t launch_fin_alpha(CgDev* cg, const double* loc, cudaStream_t s);
 cudaError_t launch_fin_beta(CgDev* cg, const double* loc, cudaStream_t s);
 cudaError_t launch_true_residual(const SpecGeom& g, const cplx* b, const cplx* Ax, cplx* r, double* partials, int nblk, cudaStream_t s);
 cudaError_t launch_fin_true(CgDev* cg, const double* loc, cudaStream_t s);
-cudaError_t launch_allreduce_lb(double* const* v, int P, int k, int is_max, cudaStream_t s);
+cudaError_t launch_allreduce_lb(double* const* v, int off, int P, int k, int is_max, cudaStream_t s);
 cudaError_t launch_axpy(const SpecGeom& g, cplx* y, const cplx* x, double a, cudaStream_t s);
 // out[k] = sum_j partials[j nred + k] (max over j for k == max_slot)
 cudaError_t launch_reduce(const double* partials, int nblk, int nred, double* out, cudaStream_t s, int max_slot = -1);

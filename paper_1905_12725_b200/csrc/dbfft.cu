@@ -142,8 +142,7 @@ struct dbfft_ctx_s {
   int peer = 0;
   PeerBuf pb1, pb2, pbf;
   long long xpcs = 0;            // chunk stride of the exchange layouts (complex elements)
-  unsigned epoch = 0;            // barriers issued
-  long long read_at[2] = {-1, -1};  // epoch at the last local read of WR / WR2
+  bool pending[2] = {false, false};  // a local read of WR / WR2 since the last device barrier
   std::vector<Slab> slabs;
   double** loc_ptrs = nullptr;  // device array of the slabs' loc pointers (loopback all-reduce)
   // tables (global)
@@ -156,8 +155,20 @@ struct dbfft_ctx_s {
   std::vector<double> h_ptable;
   double Fbar[9], Fbar_c[9];  // macro strain / F (incl. stress-controlled comps)
   double Cbar[81];
-  PrecQ prec;
+  PrecQ prec;                    // host copy of M's coefficients ...
+  PrecQ* prec_dev = nullptr;     // ... and the device copy the kernels read
   bool prec_valid = false;
+  // device-side PCG loop (CUDA graph with a WHILE node), one per parameter key, rebuilt when
+  // set_phases reallocates the buffers baked into it (gen)
+  struct LoopGraph {
+    cudaGraphExec_t exec = nullptr;
+    long long gen = -1;
+    long long body_launches = 0;
+  };
+  LoopGraph loop[4], rounds[4];  // WHILE-node loop / host-polled round of check_every iterations
+  long long gen = 0;
+  int loop_fail = 0;             // 1: WHILE graph unavailable here, 2: round graphs too (eager)
+  std::string loop_note;         // how the last PCG loop ran (dbfft_info)
   // preconditioner variants: reference medium of linear phases, initial tangent
   std::vector<double> h_counts;  // voxels per phase (global)
   int prec_medium = 0;           // medium the linear prec was built with (0 arithmetic, 1 harmonic, 2 Hill)
@@ -375,9 +386,9 @@ XGeom xgeom(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out) {
 
 dbfft_status peer_barrier(dbfft_ctx ctx) {
   ProfScope ps(ctx, PK_XCHG);
-  ++ctx->epoch;
-  CK(launch_peer_barrier((unsigned*)ctx->pbf.recv[0], (char*)ctx->pbf.win[0], ctx->pbf.chunk, ctx->P, ctx->rank, ctx->epoch,
-                         ctx->stream));
+  // the epoch is a device-side counter (a replayed CUDA graph issues the same launches)
+  CK(launch_peer_barrier((unsigned*)ctx->pbf.recv[0], (char*)ctx->pbf.win[0], ctx->pbf.chunk, ctx->P, ctx->rank, ctx->stream));
+  ctx->pending[0] = ctx->pending[1] = false;
   return DBFFT_OK;
 }
 
@@ -389,7 +400,7 @@ dbfft_status run_col(dbfft_ctx ctx, int kind, int prof_id, const ColGeom& g, int
   if (guard) {
     const Slab& s = ctx->slabs[0];
     const int w = (g.out == s.WS1) ? 0 : (g.out == s.WS2) ? 1 : -1;
-    if (w >= 0 && ctx->read_at[w] >= (long long)ctx->epoch) CKS(peer_barrier(ctx));
+    if (w >= 0 && ctx->pending[w]) CKS(peer_barrier(ctx));
   }
   {
     ProfScope ps(ctx, prof_id);
@@ -397,8 +408,8 @@ dbfft_status run_col(dbfft_ctx ctx, int kind, int prof_id, const ColGeom& g, int
   }
   if (guard) {
     const Slab& s = ctx->slabs[0];
-    if (g.in == s.WR) ctx->read_at[0] = ctx->epoch;
-    if (g.in == s.WR2) ctx->read_at[1] = ctx->epoch;
+    if (g.in == s.WR) ctx->pending[0] = true;
+    if (g.in == s.WR2) ctx->pending[1] = true;
   }
   return DBFFT_OK;
 }
@@ -443,12 +454,8 @@ dbfft_status exchange(dbfft_ctx ctx, long long chunk) {
 dbfft_status allreduce(dbfft_ctx ctx, int off, int k, bool is_max) {
   if (ctx->P == 1) return DBFFT_OK;
   ProfScope ps(ctx, PK_FIN);
-  if (ctx->loopback) {
-    std::vector<double*> h(ctx->P);
-    for (int r = 0; r < ctx->P; ++r) h[r] = ctx->slabs[r].loc + off;
-    CK(cudaMemcpyAsync(ctx->loc_ptrs, h.data(), sizeof(double*) * ctx->P, cudaMemcpyHostToDevice, ctx->stream));
-    CK(launch_allreduce_lb(ctx->loc_ptrs, ctx->P, k, is_max ? 1 : 0, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));  // h (host) must outlive the copy
+  if (ctx->loopback) {  // loc_ptrs: the slabs' loc buffers (uploaded at creation)
+    CK(launch_allreduce_lb(ctx->loc_ptrs, off, ctx->P, k, is_max ? 1 : 0, ctx->stream));
     return DBFFT_OK;
   }
   double* v = ctx->slabs[0].loc + off;
@@ -534,6 +541,16 @@ PrecQ make_prec(const double* C81) {
       q.Q[6 * m + p] = (j == l) ? C(i, j, k, l) : C(i, j, k, l) + C(i, l, k, j);
     }
   return q;
+}
+
+// M's coefficients from Cbar (host), then the device copy the kernels read (stream ordered: kernels
+// queued before keep the previous M)
+dbfft_status set_prec(dbfft_ctx ctx, const double* C81) {
+  ctx->prec = make_prec(C81);
+  CK(cudaMemcpyAsync(ctx->prec_dev, &ctx->prec, sizeof(PrecQ), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));  // the host copy may change again before a pageable copy ran
+  ctx->prec_valid = true;
+  return DBFFT_OK;
 }
 
 // Mandel 6x6 of a symmetric fourth-order tensor (w = 1 normal, sqrt 2 shear) and back
@@ -725,30 +742,62 @@ int nf_I1(dbfft_ctx ctx) { return ctx->kin == 9 ? 6 : 5; }
 // u / f select per-slab vectors, e_member the macro block inside each slab's CgDev.
 typedef double Macro9[9];
 
+// PCG-loop early exit: the passes of an iteration return at once once PCG has stopped
+template <class G>
+void guard_geom(G& g, const Slab& s);
+template <>
+void guard_geom(ColGeom& g, const Slab& s) {
+  g.cg_stop0 = &s.cg->converged;
+  g.cg_stop1 = &s.cg->breakdown;
+}
+template <>
+void guard_geom(XGeom& g, const Slab& s) {
+  g.stop0 = &s.cg->converged;
+  g.stop1 = &s.cg->breakdown;
+}
+
+// guard: inside the PCG loop (early exit of every pass once PCG stopped)
 dbfft_status apply_K_slabs(dbfft_ctx ctx, cplx* Slab::*u, cplx* Slab::*f, bool use_e, Macro9 CgDev::*e_member,
-                           ApplyOut* ao, bool front_only = false) {
+                           ApplyOut* ao, bool front_only = false, bool guard = false) {
   const bool fin = ctx->kin == 9;
   int xkind;
   if (ctx->family == FAM_LINEAR) xkind = X_K_SMALL_PHASE;
   else if (ctx->family == FAM_J2) xkind = X_K_J2;
   else xkind = ctx->tmode ? X_K_FIN_NH : X_K_FIN_TAN;
   const int nf1 = nf_I1(ctx);
-  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_I1F : COL_I1S, PK_I1, geom_I1(ctx, s, s.*u, s.WS1, nf1), ctx->n3));
+  for (Slab& s : ctx->slabs) {
+    ColGeom g = geom_I1(ctx, s, s.*u, s.WS1, nf1);
+    if (guard) guard_geom(g, s);
+    CKS(run_col(ctx, fin ? COL_I1F : COL_I1S, PK_I1, g, ctx->n3));
+  }
   CKS(exchange(ctx, (long long)nf1 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->kxp));
-  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_I2F : COL_I2S, PK_I2, geom_I2(ctx, s, s.WR, s.WB, nf1), ctx->n2));
+  for (Slab& s : ctx->slabs) {
+    ColGeom g = geom_I2(ctx, s, s.WR, s.WB, nf1);
+    if (guard) guard_geom(g, s);
+    CKS(run_col(ctx, fin ? COL_I2F : COL_I2S, PK_I2, g, ctx->n2));
+  }
   if (ao) ao->grid_x.assign(ctx->slabs.size(), 0);
   for (size_t k = 0; k < ctx->slabs.size(); ++k) {
     Slab& s = ctx->slabs[k];
     XGeom gx = xgeom(ctx, s, s.WB, s.WB);
     gx.e = use_e ? (const double*)(s.cg->*e_member) : nullptr;
+    if (guard) guard_geom(gx, s);
     int gridx = 0;
     CKS(run_x(ctx, xkind, PK_X, gx, &gridx));
     if (ao) ao->grid_x[k] = gridx;
   }
   if (front_only) return DBFFT_OK;  // the caller runs the forward tail (PCG: F3 fused with r -= alpha q)
-  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, geom_F2(ctx, s, s.WB, s.WS2, 6), ctx->n2));
+  for (Slab& s : ctx->slabs) {
+    ColGeom g = geom_F2(ctx, s, s.WB, s.WS2, 6);
+    if (guard) guard_geom(g, s);
+    CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, g, ctx->n2));
+  }
   CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->kxp));
-  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_F3, geom_F3(ctx, s, s.WR2, s.*f, 6), ctx->n3));
+  for (Slab& s : ctx->slabs) {
+    ColGeom g = geom_F3(ctx, s, s.WR2, s.*f, 6);
+    if (guard) guard_geom(g, s);
+    CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_F3, g, ctx->n3));
+  }
   return DBFFT_OK;
 }
 
@@ -798,9 +847,7 @@ dbfft_status refresh_mean_tangent(dbfft_ctx ctx) {
       }
     voigt_to_full(CV, ctx->Cbar);
   }
-  ctx->prec = make_prec(ctx->Cbar);
-  ctx->prec_valid = true;
-  return DBFFT_OK;
+  return set_prec(ctx, ctx->Cbar);
 }
 
 // X-pass reductions of every slab into loc[1..9] (sums) and loc[10] (max), all-reduced
@@ -818,7 +865,150 @@ dbfft_status reduce_x(dbfft_ctx ctx, const std::vector<int>& grids, double* host
 // ---------------------------------------------------------------- PCG
 // Solves A {x | xe} = {b | be} with x0 = 0.  Requires CgDev (msig0, be, mask, Minv_e) set.
 // loc layout: [0] <p,q> / <r,z> / <r,r>, [1] <r,r> (CG pairs), [1..9] DC sums, [10] max.
-dbfft_status pcg_body(dbfft_ctx ctx, int every, bool macro, int nb);
+//
+// The iterations run on the device: one CUDA graph per parameter key holds a WHILE node whose
+// body is one PCG iteration; the body's last kernel sets the loop condition from CgDev
+// (converged / breakdown / max_cg), so the host launches the loop once per solve and waits once —
+// no host polls, no operator application after convergence, no per-solve re-capture (M's
+// coefficients and every scalar live in device memory).  Fallbacks, in order, when a WHILE
+// graph cannot be built here (e.g. collectives that cannot sit inside a conditional body) or
+// while the per-kernel profiler records events: host-polled rounds of check_every iterations
+// replayed from a plain graph, then eager launches; in both every pass of an iteration exits at
+// once after convergence.
+dbfft_status pcg_body(dbfft_ctx ctx, int every, bool macro, int nb, cudaGraphConditionalHandle cond);
+bool pcg_fused(dbfft_ctx ctx);
+
+struct GraphDel {
+  cudaGraph_t g = nullptr;
+  ~GraphDel() {
+    if (g) cudaGraphDestroy(g);
+  }
+};
+
+// end a capture whose issue failed; clears the sticky capture error
+void abort_capture(dbfft_ctx ctx) {
+  cudaGraph_t junk = nullptr;
+  cudaStreamEndCapture(ctx->stream, &junk);
+  if (junk) cudaGraphDestroy(junk);
+  cudaGetLastError();
+}
+
+int loop_key(dbfft_ctx ctx, bool macro) { return (macro ? 1 : 0) | (pcg_fused(ctx) ? 2 : 0); }
+
+// the device-side loop: [k_loop_cond] -> WHILE(cond) { one PCG iteration; k_fin_x sets cond }
+dbfft_status build_loop_graph(dbfft_ctx ctx, bool macro, int nb, dbfft_ctx_s::LoopGraph* lg) {
+  GraphDel g;
+  CK(cudaGraphCreate(&g.g, 0));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, g.g, 0, 0));
+  CK(cudaStreamBeginCaptureToGraph(ctx->stream, g.g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  cudaError_t e = launch_loop_cond(ctx->slabs[0].cg, h, ctx->stream);
+  cudaGraph_t cap = nullptr;
+  cudaError_t e2 = cudaStreamEndCapture(ctx->stream, &cap);
+  CK(e);
+  CK(e2);
+  size_t nn = 0;
+  CK(cudaGraphGetNodes(g.g, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn);
+  CK(cudaGraphGetNodes(g.g, nodes.data(), &nn));
+  alignas(cudaGraphNodeParams) unsigned char cpbuf[sizeof(cudaGraphNodeParams)] = {};  // (no default ctor)
+  cudaGraphNodeParams& cp = *reinterpret_cast<cudaGraphNodeParams*>(cpbuf);
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cn;
+  CK(cudaGraphAddNode(&cn, g.g, nodes.data(), nn, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CK(cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  const long long nl0 = ctx->nlaunch;
+  const dbfft_status bst = pcg_body(ctx, 1, macro, nb, h);
+  if (bst != DBFFT_OK) {
+    abort_capture(ctx);
+    return bst;
+  }
+  e2 = cudaStreamEndCapture(ctx->stream, &cap);
+  CK(e2);
+  lg->body_launches = ctx->nlaunch - nl0;
+  ctx->nlaunch = nl0;  // captured, not launched
+  if (lg->exec) cudaGraphExecDestroy(lg->exec);
+  lg->exec = nullptr;
+  CK(cudaGraphInstantiate(&lg->exec, g.g, 0));
+  lg->gen = ctx->gen;
+  return DBFFT_OK;
+}
+
+// host-polled round: `every` PCG iterations captured into a plain graph (reused across solves)
+dbfft_status build_round_graph(dbfft_ctx ctx, int every, bool macro, int nb, dbfft_ctx_s::LoopGraph* lg) {
+  CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  const long long nl0 = ctx->nlaunch;
+  const dbfft_status bst = pcg_body(ctx, every, macro, nb, 0);
+  if (bst != DBFFT_OK) {
+    abort_capture(ctx);
+    return bst;
+  }
+  GraphDel g;
+  CK(cudaStreamEndCapture(ctx->stream, &g.g));
+  lg->body_launches = ctx->nlaunch - nl0;
+  ctx->nlaunch = nl0;
+  if (lg->exec) cudaGraphExecDestroy(lg->exec);
+  lg->exec = nullptr;
+  CK(cudaGraphInstantiate(&lg->exec, g.g, 0));
+  lg->gen = ctx->gen;
+  return DBFFT_OK;
+}
+
+// run PCG iterations until CgDev says stop (converged, breakdown or max_cg); h_cg is current on return
+dbfft_status pcg_iterate(dbfft_ctx ctx, const dbfft_opts& o, bool macro, int nb) {
+  const char* genv = getenv("DBFFT_GRAPHS");
+  const bool graphs = !ctx->prof && !(genv && genv[0] == '0');
+  const int key = loop_key(ctx, macro);
+  const int it0 = ctx->h_cg->iters;
+  if (graphs && ctx->loop_fail == 0) {
+    dbfft_ctx_s::LoopGraph& lg = ctx->loop[key];
+    dbfft_status st = DBFFT_OK;
+    if (!lg.exec || lg.gen != ctx->gen) st = build_loop_graph(ctx, macro, nb, &lg);
+    if (st == DBFFT_OK) {
+      CK(cudaGraphLaunch(lg.exec, ctx->stream));
+      CK(cudaMemcpyAsync(ctx->h_cg, ctx->slabs[0].cg, sizeof(CgDev), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      ctx->nlaunch += 1 + lg.body_launches * std::max(1, ctx->h_cg->iters - it0);
+      ctx->loop_note = "device-side WHILE graph";
+      return DBFFT_OK;
+    }
+    // not available here: remember, fall back to host-polled rounds
+    ctx->loop_fail = 1;
+    ctx->loop_note = "WHILE graph unavailable (" + ctx->err + "); host-polled graph rounds";
+    cudaGetLastError();
+  }
+  // profiler on: poll every iteration, so no launch is an early exit and the per-kernel event
+  // times are those of real work
+  const int every = ctx->prof ? 1 : std::max(1, o.check_every);
+  for (;;) {
+    CK(cudaMemcpyAsync(ctx->h_cg, ctx->slabs[0].cg, sizeof(CgDev), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    prof_flush(ctx);
+    const CgDev* h = ctx->h_cg;
+    if (h->converged || h->breakdown || h->iters >= o.max_cg) return DBFFT_OK;
+    if (graphs && ctx->loop_fail < 2) {
+      dbfft_ctx_s::LoopGraph& lg = ctx->rounds[key];
+      dbfft_status st = DBFFT_OK;
+      if (!lg.exec || lg.gen != ctx->gen || lg.body_launches == 0) st = build_round_graph(ctx, every, macro, nb, &lg);
+      if (st == DBFFT_OK) {
+        CK(cudaGraphLaunch(lg.exec, ctx->stream));
+        ctx->nlaunch += lg.body_launches;
+        if (ctx->loop_fail == 0) ctx->loop_note = "host-polled graph rounds";
+        continue;
+      }
+      ctx->loop_fail = 2;
+      ctx->loop_note += "; round graphs unavailable, eager";
+      cudaGetLastError();
+    } else if (!graphs) {
+      ctx->loop_note = "eager (profiler on or DBFFT_GRAPHS=0)";
+    }
+    CKS(pcg_body(ctx, every, macro, nb, 0));
+  }
+}
 
 dbfft_status pcg(dbfft_ctx ctx, const dbfft_opts& o, int* iters_out) {
   const int nb = cg_blocks();
@@ -831,7 +1021,7 @@ dbfft_status pcg(dbfft_ctx ctx, const dbfft_opts& o, int* iters_out) {
     for (Slab& s : ctx->slabs) {
       {
         ProfScope ps(ctx, PK_CGDIR);
-        CK(launch_cg_init(spec(ctx, s), ctx->prec, s.r, s.p, s.part_cg, nb, ctx->stream));
+        CK(launch_cg_init(spec(ctx, s), ctx->prec_dev, s.r, s.p, s.part_cg, nb, ctx->stream));
       }
       CKS(reduce_to(ctx, s, s.part_cg, nb, 2, 0));
     }
@@ -840,102 +1030,54 @@ dbfft_status pcg(dbfft_ctx ctx, const dbfft_opts& o, int* iters_out) {
       ProfScope ps(ctx, PK_FIN);
       CK(launch_fin_init(s.cg, s.loc, ctx->stream));
     }
+    CK(cudaMemcpyAsync(ctx->h_cg, ctx->slabs[0].cg, sizeof(CgDev), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     return DBFFT_OK;
   };
   CKS(init_dir());
-  const int every = std::max(1, o.check_every);
   int restarts = 0;
-  // graphs: single GPU only (the loopback all-reduce synchronises on the host, and NCCL capture
-  // is not exercised on the one-GPU test boxes), and not while the per-kernel profiler records
-  // events; DBFFT_GRAPHS=0 disables
-  const char* genv = getenv("DBFFT_GRAPHS");
-  const bool use_graph = !ctx->prof && ctx->P == 1 && !(genv && genv[0] == '0');
-  cudaGraphExec_t graph_exec = nullptr;
-  long long graph_launches = 0;
-  int rounds = 0;
-  struct ExecGuard {
-    cudaGraphExec_t exec = nullptr;
-    ~ExecGuard() {
-      if (exec) cudaGraphExecDestroy(exec);
-    }
-  } guard;
   for (;;) {
-    CK(cudaMemcpyAsync(ctx->h_cg, ctx->slabs[0].cg, sizeof(CgDev), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    CKS(pcg_iterate(ctx, o, macro, nb));  // h_cg current
     prof_flush(ctx);
+    *iters_out = ctx->h_cg->iters;
     if (ctx->h_cg->breakdown) {
       ctx->err = "PCG breakdown: <p,Kp> <= 0 or NaN";
-      *iters_out = ctx->h_cg->iters;
       return DBFFT_E_BREAKDOWN;
     }
-    if (ctx->h_cg->converged == 2 || ctx->h_cg->iters >= o.max_cg) {
-      *iters_out = ctx->h_cg->iters;
+    if (ctx->h_cg->converged != 1) {
       ctx->err = "PCG did not converge within max_cg";
       return DBFFT_E_NOT_CONVERGED;
     }
-    if (ctx->h_cg->converged == 1) {
-      // true-residual confirmation (R7): r = b - A x
-      ApplyOut ao;
-      CKS(apply_K_slabs(ctx, &Slab::x, &Slab::q, macro, &CgDev::xe, &ao));
-      for (size_t k = 0; k < ctx->slabs.size(); ++k) {
-        Slab& s = ctx->slabs[k];
-        {
-          ProfScope ps(ctx, PK_CGUPD);
-          CK(launch_true_residual(spec(ctx, s), s.b, s.q, s.r, s.part_cg, nb, ctx->stream));
-        }
-        CKS(reduce_to(ctx, s, s.part_cg, nb, 1, 0));
-        CKS(reduce_to(ctx, s, s.part_x, ao.grid_x[k], 10, 1));
+    // true-residual confirmation (R7): r = b - A x
+    ApplyOut ao;
+    CKS(apply_K_slabs(ctx, &Slab::x, &Slab::q, macro, &CgDev::xe, &ao));
+    for (size_t k = 0; k < ctx->slabs.size(); ++k) {
+      Slab& s = ctx->slabs[k];
+      {
+        ProfScope ps(ctx, PK_CGUPD);
+        CK(launch_true_residual(spec(ctx, s), s.b, s.q, s.r, s.part_cg, nb, ctx->stream));
       }
-      CKS(allreduce(ctx, 0, 10, false));
-      for (Slab& s : ctx->slabs) {
-        ProfScope ps(ctx, PK_FIN);
-        CK(launch_fin_true(s.cg, s.loc, ctx->stream));
-      }
-      CK(cudaMemcpyAsync(ctx->h_cg, ctx->slabs[0].cg, sizeof(CgDev), cudaMemcpyDeviceToHost, ctx->stream));
-      CK(cudaStreamSynchronize(ctx->stream));
-      *iters_out = ctx->h_cg->iters;
-      if (ctx->h_cg->converged == 1) return DBFFT_OK;
-      // the restarted iterations count against max_cg (cg->iters carries over); a true residual
-      // that stays above tolerance after the restart budget is a failure, not a success
-      if (restarts >= 20 || ctx->h_cg->iters >= o.max_cg) {
-        ctx->err = "PCG did not converge: true residual b - Ax above tolerance after " + std::to_string(restarts) +
-                   " restarts (eps_eq " + std::to_string(ctx->h_cg->eps_eq) + ")";
-        return DBFFT_E_NOT_CONVERGED;
-      }
-      ++restarts;  // restart from the true residual: z = M r, p = z
-      CKS(init_dir());
-      continue;
+      CKS(reduce_to(ctx, s, s.part_cg, nb, 1, 0));
+      CKS(reduce_to(ctx, s, s.part_x, ao.grid_x[k], 10, 1));
     }
-    // `every` PCG iterations between host polls: replayed from a CUDA graph once captured (the
-    // steady-state loop is launch-bound on small grids); captured per pcg() call because M's
-    // coefficients are kernel parameters
-    if (graph_exec) {
-      CK(cudaGraphLaunch(graph_exec, ctx->stream));
-      ctx->nlaunch += graph_launches;
-      continue;
+    CKS(allreduce(ctx, 0, 10, false));
+    for (Slab& s : ctx->slabs) {
+      ProfScope ps(ctx, PK_FIN);
+      CK(launch_fin_true(s.cg, s.loc, ctx->stream));
     }
-    const bool capture = use_graph && rounds > 0;
-    const long long nl0 = ctx->nlaunch;
-    if (capture) CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-    ++rounds;
-    dbfft_status bst = pcg_body(ctx, every, macro, nb);
-    if (capture) {
-      cudaGraph_t graph = nullptr;
-      cudaError_t ce = cudaStreamEndCapture(ctx->stream, &graph);
-      if (bst != DBFFT_OK) {
-        if (graph) cudaGraphDestroy(graph);
-        return bst;
-      }
-      CK(ce);
-      ce = cudaGraphInstantiate(&graph_exec, graph, 0);
-      cudaGraphDestroy(graph);
-      CK(ce);
-      graph_launches = ctx->nlaunch - nl0;
-      guard.exec = graph_exec;
-      CK(cudaGraphLaunch(graph_exec, ctx->stream));  // the captured round has not run yet
-      continue;
+    CK(cudaMemcpyAsync(ctx->h_cg, ctx->slabs[0].cg, sizeof(CgDev), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    *iters_out = ctx->h_cg->iters;
+    if (ctx->h_cg->converged == 1) return DBFFT_OK;
+    // the restarted iterations count against max_cg (cg->iters carries over); a true residual
+    // that stays above tolerance after the restart budget is a failure, not a success
+    if (restarts >= 20 || ctx->h_cg->iters >= o.max_cg) {
+      ctx->err = "PCG did not converge: true residual b - Ax above tolerance after " + std::to_string(restarts) +
+                 " restarts (eps_eq " + std::to_string(ctx->h_cg->eps_eq) + ")";
+      return DBFFT_E_NOT_CONVERGED;
     }
-    CKS(bst);
+    ++restarts;  // restart from the true residual: z = M r, p = z
+    CKS(init_dir());
   }
 }
 
@@ -948,7 +1090,7 @@ ColGeom geom_F3_update(dbfft_ctx ctx, Slab& s) {
   g5.cg_alpha = &s.cg->alpha;
   g5.cg_stop0 = &s.cg->converged;
   g5.cg_stop1 = &s.cg->breakdown;
-  memcpy(g5.precq, ctx->prec.Q, sizeof(g5.precq));
+  g5.precq = ctx->prec_dev->Q;
   return g5;
 }
 
@@ -963,13 +1105,23 @@ bool pcg_fused(dbfft_ctx ctx) {
   return true;
 }
 
+// end of an iteration: x += alpha p owed by the direction kernel is settled; slab 0's k_fin_x
+// decides whether the device-side loop runs again (all slabs hold the same reduced scalars)
+dbfft_status fin_x_all(dbfft_ctx ctx, cudaGraphConditionalHandle cond) {
+  for (size_t k = 0; k < ctx->slabs.size(); ++k) {
+    ProfScope ps(ctx, PK_FIN);
+    CK(launch_fin_x(ctx->slabs[k].cg, ctx->stream, cond, (cond && k == 0) ? 1 : 0));
+  }
+  return DBFFT_OK;
+}
+
 // one PCG iteration with the residual update fused into F3 (8 - 3 + 1 = 6 vector transfers of
 // CG algebra per iteration instead of 8): I1 I2 X | alpha | F2 F3(r -= alpha q, <r,z>, <r,r>) |
 // beta | direction (x += alpha p, p = z + beta p)
-dbfft_status pcg_iteration_fused(dbfft_ctx ctx, bool macro, int nb) {
+dbfft_status pcg_iteration_fused(dbfft_ctx ctx, bool macro, int nb, cudaGraphConditionalHandle cond) {
   const bool fin = ctx->kin == 9;
   ApplyOut ao;
-  CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, macro, &CgDev::pe, &ao, true));
+  CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, macro, &CgDev::pe, &ao, true, true));
   for (size_t j = 0; j < ctx->slabs.size(); ++j) {
     Slab& s = ctx->slabs[j];
     CKS(reduce_to(ctx, s, s.part_x, ao.grid_x[j], 10, 1));
@@ -979,7 +1131,11 @@ dbfft_status pcg_iteration_fused(dbfft_ctx ctx, bool macro, int nb) {
     ProfScope ps(ctx, PK_FIN);
     CK(launch_fin_alpha(s.cg, s.loc, ctx->stream));
   }
-  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, geom_F2(ctx, s, s.WB, s.WS2, 6), ctx->n2));
+  for (Slab& s : ctx->slabs) {
+    ColGeom g = geom_F2(ctx, s, s.WB, s.WS2, 6);
+    guard_geom(g, s);
+    CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, g, ctx->n2));
+  }
   CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->kxp));
   std::vector<int> g3(ctx->slabs.size(), 0);
   for (size_t j = 0; j < ctx->slabs.size(); ++j) {
@@ -995,59 +1151,50 @@ dbfft_status pcg_iteration_fused(dbfft_ctx ctx, bool macro, int nb) {
     }
     {
       ProfScope ps(ctx, PK_CGDIR);
-      CK(launch_cg_direction(spec(ctx, s), ctx->prec, s.cg, s.x, s.p, s.r, ctx->stream));
-    }
-    {
-      ProfScope ps(ctx, PK_FIN);
-      CK(launch_fin_x(s.cg, ctx->stream));
+      CK(launch_cg_direction(spec(ctx, s), ctx->prec_dev, s.cg, s.x, s.p, s.r, ctx->stream));
     }
   }
-  return DBFFT_OK;
+  return fin_x_all(ctx, cond);
 }
 
-dbfft_status pcg_body(dbfft_ctx ctx, int every, bool macro, int nb) {
+dbfft_status pcg_body(dbfft_ctx ctx, int every, bool macro, int nb, cudaGraphConditionalHandle cond) {
   if (pcg_fused(ctx)) {
-    for (int k = 0; k < every; ++k) CKS(pcg_iteration_fused(ctx, macro, nb));
+    for (int k = 0; k < every; ++k) CKS(pcg_iteration_fused(ctx, macro, nb, cond));
     return DBFFT_OK;
   }
-  {
-    for (int k = 0; k < every; ++k) {
-      ApplyOut ao;
-      // <p, A p> comes from the X pass (slot 9: sum (grad p + p_e) : sigma, Parseval), so F3 does
-      // not re-read p
-      CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, macro, &CgDev::pe, &ao));
-      for (size_t j = 0; j < ctx->slabs.size(); ++j) {
-        Slab& s = ctx->slabs[j];
-        CKS(reduce_to(ctx, s, s.part_x, ao.grid_x[j], 10, 1));
+  for (int k = 0; k < every; ++k) {
+    ApplyOut ao;
+    // <p, A p> comes from the X pass (slot 9: sum (grad p + p_e) : sigma, Parseval), so F3 does
+    // not re-read p
+    CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, macro, &CgDev::pe, &ao, false, true));
+    for (size_t j = 0; j < ctx->slabs.size(); ++j) {
+      Slab& s = ctx->slabs[j];
+      CKS(reduce_to(ctx, s, s.part_x, ao.grid_x[j], 10, 1));
+    }
+    CKS(allreduce(ctx, 1, 10, false));
+    for (Slab& s : ctx->slabs) {
+      {
+        ProfScope ps(ctx, PK_FIN);
+        CK(launch_fin_alpha(s.cg, s.loc, ctx->stream));
       }
-      CKS(allreduce(ctx, 1, 10, false));
-      for (Slab& s : ctx->slabs) {
-        {
-          ProfScope ps(ctx, PK_FIN);
-          CK(launch_fin_alpha(s.cg, s.loc, ctx->stream));
-        }
-        {
-          ProfScope ps(ctx, PK_CGUPD);
-          CK(launch_cg_update(spec(ctx, s), ctx->prec, s.cg, s.r, s.q, s.part_cg, nb, ctx->stream));
-        }
-        CKS(reduce_to(ctx, s, s.part_cg, nb, 2, 0));
+      {
+        ProfScope ps(ctx, PK_CGUPD);
+        CK(launch_cg_update(spec(ctx, s), ctx->prec_dev, s.cg, s.r, s.q, s.part_cg, nb, ctx->stream));
       }
-      CKS(allreduce(ctx, 0, 2, false));
-      for (Slab& s : ctx->slabs) {
-        {
-          ProfScope ps(ctx, PK_FIN);
-          CK(launch_fin_beta(s.cg, s.loc, ctx->stream));
-        }
-        {
-          ProfScope ps(ctx, PK_CGDIR);
-          CK(launch_cg_direction(spec(ctx, s), ctx->prec, s.cg, s.x, s.p, s.r, ctx->stream));
-        }
-        {
-          ProfScope ps(ctx, PK_FIN);
-          CK(launch_fin_x(s.cg, ctx->stream));
-        }
+      CKS(reduce_to(ctx, s, s.part_cg, nb, 2, 0));
+    }
+    CKS(allreduce(ctx, 0, 2, false));
+    for (Slab& s : ctx->slabs) {
+      {
+        ProfScope ps(ctx, PK_FIN);
+        CK(launch_fin_beta(s.cg, s.loc, ctx->stream));
+      }
+      {
+        ProfScope ps(ctx, PK_CGDIR);
+        CK(launch_cg_direction(spec(ctx, s), ctx->prec_dev, s.cg, s.x, s.p, s.r, ctx->stream));
       }
     }
+    CKS(fin_x_all(ctx, cond));
   }
   return DBFFT_OK;
 }
@@ -1145,10 +1292,8 @@ dbfft_status linear_reference(dbfft_ctx ctx, int medium) {
     mandel_to_full(S.data(), CR);
   }
   for (int a = 0; a < 81; ++a) ctx->Cbar[a] = medium == 0 ? CA[a] : medium == 1 ? CR[a] : 0.5 * (CA[a] + CR[a]);
-  ctx->prec = make_prec(ctx->Cbar);
-  ctx->prec_valid = true;
   ctx->prec_medium = medium;
-  return DBFFT_OK;
+  return set_prec(ctx, ctx->Cbar);
 }
 
 dbfft_status check_opts(dbfft_ctx ctx, const dbfft_opts& o) {
@@ -1289,7 +1434,8 @@ dbfft_status solve_newton(dbfft_ctx ctx, const double* target, const uint8_t* ma
     if (o.precond_refresh == 2) {
       if (newton == 0) {
         memcpy(ctx->Cbar, ctx->Cbar_init, sizeof(ctx->Cbar));
-        ctx->prec = make_prec(ctx->Cbar);
+        st = set_prec(ctx, ctx->Cbar);
+        if (st != DBFFT_OK) break;
       }
     } else if (o.precond_refresh == 1 || (newton == 0 && (o.precond_refresh == 0 || ctx->n_incr % o.precond_period == 0))) {
       st = refresh_mean_tangent(ctx);
@@ -1368,7 +1514,10 @@ void free_all(dbfft_ctx ctx) {
   peer_free(&ctx->pb1);
   peer_free(&ctx->pb2);
   peer_free(&ctx->pbf);
-  void* ptrs[] = {ctx->xix, ctx->xiy, ctx->xiz, ctx->tw1, ctx->tw2, ctx->tw3, ctx->loc_ptrs, ctx->trace_dev};
+  for (auto* lg : {ctx->loop, ctx->rounds})
+    for (int k = 0; k < 4; ++k)
+      if (lg[k].exec) cudaGraphExecDestroy(lg[k].exec);
+  void* ptrs[] = {ctx->xix, ctx->xiy, ctx->xiz, ctx->tw1, ctx->tw2, ctx->tw3, ctx->loc_ptrs, ctx->trace_dev, ctx->prec_dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ctx->h_cg) cudaFreeHost(ctx->h_cg);
@@ -1662,7 +1811,16 @@ dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinemat
     sl.xiy = ctx->xiy + sl.ky0;
     if ((s = alloc_slab(ctx, sl)) != DBFFT_OK) return fail(s);
   }
-  if (ctx->loopback && (s = dalloc(ctx, &ctx->loc_ptrs, P)) != DBFFT_OK) return fail(s);
+  if ((s = dalloc(ctx, &ctx->prec_dev, 1)) != DBFFT_OK) return fail(s);
+  if (ctx->loopback) {  // the slabs' loc buffers for the loopback all-reduce kernel
+    if ((s = dalloc(ctx, &ctx->loc_ptrs, P)) != DBFFT_OK) return fail(s);
+    std::vector<double*> h(P);
+    for (int r = 0; r < P; ++r) h[r] = ctx->slabs[r].loc;
+    if (cudaMemcpy(ctx->loc_ptrs, h.data(), sizeof(double*) * P, cudaMemcpyHostToDevice) != cudaSuccess) {
+      ctx->err = "create: loc pointer upload failed";
+      return fail(DBFFT_E_CUDA);
+    }
+  }
   if (P > 1 && !ctx->loopback) {
     std::string err;
     if (!nccl_load(&err)) {
@@ -1898,6 +2056,7 @@ dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t o
   ctx->h_ptable = pt;
   ctx->nph = n_phases;
   ctx->family = fam;
+  ++ctx->gen;  // buffers baked into captured PCG loops change below
   for (Slab& sl : ctx->slabs) {
     free_state(sl);
     CK(cudaMemsetAsync(sl.u, 0, sizeof(cplx) * 3 * sl.Hs, ctx->stream));
@@ -2010,7 +2169,7 @@ dbfft_status dbfft_precond(dbfft_ctx ctx, const void* r_hat, void* z_hat) {
   CKS(spec_in(ctx, (const cplx*)r_hat, &Slab::r));
   for (Slab& s : ctx->slabs) {
     ProfScope ps(ctx, PK_OTHER);
-    CK(launch_precond(spec(ctx, s), ctx->prec, s.r, s.q, ctx->stream));
+    CK(launch_precond(spec(ctx, s), ctx->prec_dev, s.r, s.q, ctx->stream));
   }
   return spec_out(ctx, &Slab::q, (cplx*)z_hat, cudaMemcpyDeviceToDevice);
 }
@@ -2293,6 +2452,20 @@ dbfft_status dbfft_launch_count(dbfft_ctx ctx, int64_t* count) {
 }
 
 const char* dbfft_profile_name(int32_t id) { return (id >= 0 && id < PK_COUNT) ? kProfNames[id] : ""; }
+
+dbfft_status dbfft_info(dbfft_ctx ctx, char* buf, int32_t cap) {
+  if (!ctx || !buf || cap <= 0) return DBFFT_E_INVALID_ARG;
+  DevGuard dev_guard(ctx->device);
+  const char* tr = ctx->P == 1 ? "none" : ctx->peer ? "peer" : "nccl";
+  std::string j = "{\"device\": " + std::to_string(ctx->device) + ", \"sms\": " + std::to_string(num_sms()) +
+                  ", \"world\": " + std::to_string(ctx->P) + ", \"rank\": " + std::to_string(ctx->rank) +
+                  ", \"loopback\": " + std::to_string(ctx->loopback) + ", \"transport\": \"" + tr +
+                  "\", \"nccl_comm\": " + (ctx->comm ? "true" : "false") + ", \"pcg_loop\": \"" + ctx->loop_note + "\"}";
+  for (char& c : j)
+    if (c == '\n') c = ' ';
+  snprintf(buf, (size_t)cap, "%s", j.c_str());
+  return (int)j.size() < cap ? DBFFT_OK : DBFFT_E_INVALID_ARG;
+}
 int32_t dbfft_profile_count(void) { return PK_COUNT; }
 
 }  // extern "C"

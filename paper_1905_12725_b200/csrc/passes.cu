@@ -327,6 +327,7 @@ struct ColPref {
 
 template <int N, int KIND>
 __global__ void __launch_bounds__(256, ColCfg<N>::ODD ? 1 : ColPref<KIND>::MINB) col_pass_kernel(ColGeom g) {
+  if (g.cg_stop0 && (*g.cg_stop0 | *g.cg_stop1)) return;  // PCG stopped: nothing to compute
   typedef ColOp<KIND> Op;
   typedef ColCfg<N> CF;
   constexpr int P = CF::P, TPC = CF::TPC, COLS = CF::COLS;
@@ -877,6 +878,7 @@ DBF_DEV void x_issue_tan(const XGeom& g, long long grp, double* st_tan, uint16_t
 // bulk async copies (cp.async.bulk -> TMA engine, mbarrier completion) while group i computes.
 template <int N1, int KIND>
 __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB) x_pass_kernel(XGeom g, int nf_real) {
+  if (g.stop0 && (*g.stop0 | *g.stop1)) return;  // PCG stopped: nothing to compute
   typedef XCfg<N1, KIND> CF;
   typedef XTraits<KIND> T;
   typedef XStage<KIND> S;
@@ -1285,7 +1287,7 @@ template <int N, int KIND, bool DOT, int R, bool UPD = false>
 __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __grid_constant__ TmaMaps maps, ColGeom g, ColTiles tl) {
   typedef ColOp<KIND> Op;
   typedef TmaCfg<N> CF;
-  if (UPD && (*g.cg_stop0 | *g.cg_stop1)) return;  // PCG stopped: r stays as it is
+  if (g.cg_stop0 && (*g.cg_stop0 | *g.cg_stop1)) return;  // PCG stopped (UPD: r stays as it is)
   constexpr int KC = CF::KC, TPC = CF::TPC;
   constexpr int S = UPD ? 3 : 2;  // staging buffers (UPD: r_0, r_1 of a tile stay readable until r_2)
   extern __shared__ __align__(1024) unsigned char tsm[];
@@ -1348,6 +1350,11 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
   cplx* xcol = xb + c * N;  // this column's FFT exchange buffer
   double acc_rz = 0.0, acc_rr = 0.0;  // UPD: partial <r, M r>, <r, r>
   const double alpha = UPD ? *g.cg_alpha : 0.0;
+  __shared__ double sprec[UPD ? 36 : 1];  // M's coefficients (device memory -> shared, once)
+  if (UPD) {
+    for (int i = t; i < 36; i += CF::CONS) sprec[i] = g.precq[i];
+    cons_sync();
+  }
   uint32_t nout = 0;        // output tiles written (staging rotation)
   uint32_t it = 0;
   for (int tile = blockIdx.x; tile < tl.n_tiles; tile += gridDim.x, ++it) {
@@ -1413,7 +1420,7 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
               const cplx r3[3] = {stg[((nout + S - 2) % S) * (CF::TILE / 16) + o], stg[((nout + S - 1) % S) * (CF::TILE / 16) + o], v};
               const double xz = __ldg(g.fq.xz + at.pos);
               cplx z3[3] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
-              if (!(at.xxk == 0.0 && at.xyo == 0.0 && xz == 0.0)) prec_apply(g.precq, at.xxk, at.xyo, xz, r3, z3);
+              if (!(at.xxk == 0.0 && at.xyo == 0.0 && xz == 0.0)) prec_apply(sprec, at.xxk, at.xyo, xz, r3, z3);
 #pragma unroll
               for (int q = 0; q < 3; ++q) {
                 acc_rz += wdot * (r3[q].x * z3[q].x + r3[q].y * z3[q].y);

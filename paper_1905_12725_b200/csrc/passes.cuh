@@ -30,9 +30,11 @@ struct ColGeom {
   int n1;            // full x length
   int upd;
   const double* cg_alpha;
+  // early exit (any column kind): inside the PCG loop the passes of an iteration return at once
+  // when PCG has stopped (CgDev.converged / .breakdown; null: always run)
   const int* cg_stop0;   // CgDev.converged
   const int* cg_stop1;   // CgDev.breakdown
-  double precq[36];      // preconditioner coefficients (prec_apply)
+  const double* precq;   // preconditioner coefficients (prec_apply; 36 doubles, device)
   int n_xy;          // length of fq.xy (guards the per-column xi_y(outer) lookup of y passes)
 };
 
@@ -100,6 +102,8 @@ struct XGeom {
   int* bad;               // first bad voxel flag (atomicMin on voxel index)
   int has_in;             // constitutive kinds: 0 = no C2R input (uniform increment only)
   int tmode;              // X_CONST_FIN: 0 = store the 45-entry tangent, 1 = compact (F^-1, c1)
+  const int* stop0;       // PCG loop early exit (CgDev.converged / .breakdown), null: always run
+  const int* stop1;
 };
 
 // host launchers (passes.cu)

@@ -344,8 +344,18 @@ void peer_free(PeerBuf* b) {
 }
 
 // ------------------------------------------------------------------ device barrier
-__global__ void k_peer_barrier(unsigned* flags, char* fwin, size_t chunk, int P, int rank, unsigned epoch) {
+// epoch: a per-rank device counter at flags[kEpochWord] (peers only write the words 32 r, r < 32),
+// advanced by every barrier in stream order, so a replayed CUDA graph issues fresh epochs; all
+// ranks run the same barrier sequence, so their counters agree
+constexpr int kEpochWord = 32 * 32;
+__global__ void k_peer_barrier(unsigned* flags, char* fwin, size_t chunk, int P, int rank) {
   const int j = threadIdx.x;
+  unsigned epoch = 0;
+  if (j == 0) {
+    epoch = flags[kEpochWord] + 1;
+    flags[kEpochWord] = epoch;
+  }
+  epoch = __shfl_sync(0xffffffffu, epoch, 0);
   if (j >= P) return;
   // the preceding kernels' stores (including those into peer memory) before the arrival
   asm volatile("fence.sc.sys;" ::: "memory");
@@ -360,8 +370,7 @@ __global__ void k_peer_barrier(unsigned* flags, char* fwin, size_t chunk, int P,
   }
 }
 
-cudaError_t launch_peer_barrier(unsigned* flags, char* fwin, size_t chunk, int P, int rank, unsigned epoch,
-                                cudaStream_t s) {
-  k_peer_barrier<<<1, 32, 0, s>>>(flags, fwin, chunk, P, rank, epoch);
+cudaError_t launch_peer_barrier(unsigned* flags, char* fwin, size_t chunk, int P, int rank, cudaStream_t s) {
+  k_peer_barrier<<<1, 32, 0, s>>>(flags, fwin, chunk, P, rank);
   return cudaGetLastError();
 }

@@ -49,8 +49,8 @@ bool peer_build_ipc(PeerBuf* b, int P, int rank, size_t chunk, int device, bool 
                     const std::string& tag, std::string* err);
 void peer_free(PeerBuf* b);
 
-// device barrier among the P ranks of a peer set: every rank stores `epoch` into its slot of every
-// rank's flag buffer (release, system scope) and waits until all P slots of its own buffer reached
-// it (acquire).  flags: this rank's own flag buffer; fwin: the flag window (chunk stride `chunk`).
-cudaError_t launch_peer_barrier(unsigned* flags, char* fwin, size_t chunk, int P, int rank, unsigned epoch,
-                                cudaStream_t s);
+// device barrier among the P ranks of a peer set: every rank advances its device-side epoch
+// counter, stores the epoch into its slot of every rank's flag buffer (release, system scope) and
+// waits until all P slots of its own buffer reached it (acquire).  flags: this rank's own flag
+// buffer (zeroed; word 1024 holds the counter); fwin: the flag window (chunk stride `chunk`).
+cudaError_t launch_peer_barrier(unsigned* flags, char* fwin, size_t chunk, int P, int rank, cudaStream_t s);

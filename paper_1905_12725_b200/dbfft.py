@@ -49,7 +49,7 @@ EXPORTS = ["dbfft_create", "dbfft_destroy", "dbfft_last_error", "dbfft_spectral_
            "dbfft_solve_increment", "dbfft_get_field", "dbfft_profile_enable", "dbfft_profile_read",
            "dbfft_profile_name", "dbfft_profile_count", "dbfft_launch_count", "dbfft_nccl_unique_id",
            "dbfft_residuals", "dbfft_incompatibility", "dbfft_get_trace", "dbfft_fd_allgather",
-           "dbfft_peer_probe_open", "dbfft_peer_probe_check", "dbfft_peer_probe_close"]
+           "dbfft_peer_probe_open", "dbfft_peer_probe_check", "dbfft_peer_probe_close", "dbfft_info"]
 
 _lib = None
 
@@ -101,6 +101,7 @@ def load_library(path=None):
     lib.dbfft_residuals.argtypes = [P, ctypes.POINTER(D), ctypes.POINTER(ctypes.c_uint8), ctypes.POINTER(D)]
     lib.dbfft_incompatibility.argtypes = [P, P, I32, ctypes.POINTER(D)]
     lib.dbfft_get_trace.argtypes = [P, ctypes.POINTER(D), I32, ctypes.POINTER(I32)]
+    lib.dbfft_info.argtypes = [P, ctypes.c_char_p, I32]
     for fn in EXPORTS:
         getattr(lib, fn).restype = getattr(lib, fn).restype if fn in (
             "dbfft_last_error", "dbfft_default_opts", "dbfft_profile_name", "dbfft_profile_count") else ctypes.c_int
@@ -376,6 +377,13 @@ class DBFFT:
         return out.value
 
     # ------------------------------------------------------------------ profiling
+    def info(self):
+        """dbfft_info: device, ranks, transport, NCCL communicator, how the last PCG loop ran."""
+        import json
+        buf = ctypes.create_string_buffer(1024)
+        self._check(self.lib.dbfft_info(self.h, buf, len(buf)))
+        return json.loads(buf.value.decode())
+
     def profile(self, enable=True):
         self._check(self.lib.dbfft_profile_enable(self.h, int(enable)))
 
