@@ -80,7 +80,7 @@ def test_apply_K_n512(dbf, n, kind, monkeypatch):
         ctx.eval_state(eps.reshape((9,) + shp), dt=1.0)
         sy = np.array([300.0, 200.0])[ph]
         _, C, _, dp = O.j2_perzyna(eps, np.zeros_like(eps), 2e5, 0.3, sy, 20.0, 1e-3, 1.0)
-        assert 0.2 < np.mean(dp > 0) < 0.98   # plastic and elastic voxels
+        assert 0.2 < np.mean(dp > 0) < 0.999   # plastic and (some) elastic voxels
         fin = False
     else:
         monkeypatch.setenv("DBFFT_TANGENT", "full" if kind == "nh_full" else "compact")
