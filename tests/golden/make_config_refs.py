@@ -6,7 +6,7 @@ tens of minutes on CPU, longer than a GPU test should wait, so its results are s
 macroscopic quantities in full, fields at a seeded set of voxels / frequencies (SAMPLES of them,
 plus the full-field norms for relative errors).  Usage:
 
-    python tests/golden/make_config_refs.py c3 c5s c4op     # -> tests/golden/<name>_ref.npz
+    python tests/golden/make_config_refs.py c3 c5s c4op c4inc    # -> tests/golden/<name>_ref.npz
 """
 import os
 import sys
@@ -108,6 +108,21 @@ def c4op():
     pts = freq_sample(n)
     vals = f[:, pts[:, 0], pts[:, 1], pts[:, 2]]
     return dict(points=pts, f=vals, f_norm=np.linalg.norm(f), mean_sig=msig, seconds=time.time() - t0)
+
+
+def c4inc():
+    """c4's first load increment at 256^3 (Newton-PCG, mixed control P_xx = P_yy = 0, F_zz = 1.01):
+    macro F / P, Newton and PCG counts, sampled F and P fields."""
+    cfg = configs.c4()
+    st = O.FiniteStrainState(cfg["n"])
+    t0 = time.time()
+    r = O.solve_finite_increment(st, cfg["phase"], cfg["materials"], cfg["loads"][0], tol=1e-10)
+    assert r["converged"]
+    vs = voxel_sample(cfg["n"])
+    F = r["F"].reshape(9, -1)
+    P = r["P"].reshape(9, -1)
+    return dict(mean_F=r["mean_F"], mean_P=r["mean_P"], newton=r["newton_iters"], cg=r["cg_iters"], voxels=vs,
+                F=F[:, vs], P=P[:, vs], F_norm=np.linalg.norm(F), P_norm=np.linalg.norm(P), seconds=time.time() - t0)
 
 
 if __name__ == "__main__":
