@@ -132,6 +132,20 @@ DBF_DEV void stage_compute(cplx (&a)[8], int g, int Ns, const cplx* __restrict__
   }
 }
 
+// Stage-ordered twiddle table (powers of two): for every stage st >= 1 of FftPlan<N> (radix R,
+// Ns = product of the earlier radices) and every k < Ns, the R-1 twiddles W_N^(r (N/(Ns R)) k),
+// r = 1..R-1, each a correctly rounded table value (no products); N-1 entries in all.  The
+// twiddles of a butterfly are then R-1 independent loads from one contiguous row.
+template <int N, int R, bool INV, int P>
+DBF_DEV void twiddle_tab(cplx (&a)[P], int m, int M, const cplx* __restrict__ ts) {
+#pragma unroll
+  for (int r = 1; r < R; ++r) {
+    cplx w = ts[r - 1];
+    if (INV) w.y = -w.y;
+    a[m + M * r] = cmul(a[m + M * r], w);
+  }
+}
+
 // Full in-CTA FFT.  On entry a[s] = x[g + s*N/8]; on exit a[s] = X[g + s*N/8].
 // IDX(pos) maps a line position to a shared-memory slot (column interleave or padding).
 // All threads of the CTA must call this (it contains __syncthreads()).
@@ -139,14 +153,32 @@ struct SyncCtaDefault {
   DBF_DEV void operator()() const { __syncthreads(); }
 };
 
-template <int N, bool INV, class IDX, class SYNC = SyncCtaDefault>
+// TAB: `tw` is the stage-ordered table (stage_twiddles on the host) instead of W_N[k].
+template <int N, int R, bool INV>
+DBF_DEV void stage_compute_tab(cplx (&a)[8], int g, int Ns, const cplx* __restrict__ stab) {
+  constexpr int M = 8 / R;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int b = g + m * (N / 8);
+    const int k = b % Ns;
+    if (Ns > 1) twiddle_tab<N, R, INV>(a, m, M, stab + k * (R - 1));
+    if (R == 8) {
+      dft8<INV>(a);
+    } else if (R == 4) {
+      dft4<INV>(a[m], a[m + M], a[m + 2 * M], a[m + 3 * M]);
+    } else {
+      dft2<INV>(a[m], a[m + M]);
+    }
+  }
+}
+
+template <int N, bool INV, class IDX, class SYNC = SyncCtaDefault, bool TAB = false>
 DBF_DEV void fft_cta(cplx (&a)[8], cplx* sbuf, int g, const IDX& idx, const cplx* __restrict__ tw, const SYNC& sync = SYNC{}) {
   typedef FftPlan<N> P;
   int Ns = 1;
+  int tbase = 0;  // TAB: offset of this stage's rows in the stage-ordered table
 #pragma unroll
   for (int st = 0; st < P::nstages; ++st) {
-    constexpr int dummy = 0;
-    (void)dummy;
     const bool is_last = (st == P::nstages - 1);
     const int R = (st < P::n8) ? 8 : P::last;
     if (st > 0) {
@@ -154,7 +186,12 @@ DBF_DEV void fft_cta(cplx (&a)[8], cplx* sbuf, int g, const IDX& idx, const cplx
 #pragma unroll
       for (int s = 0; s < 8; ++s) a[s] = sbuf[idx(g + s * (N / 8))];
     }
-    if (R == 8) stage_compute<N, 8, INV>(a, g, Ns, tw);
+    if (TAB) {
+      if (R == 8) stage_compute_tab<N, 8, INV>(a, g, Ns, tw + tbase);
+      else if (R == 4) stage_compute_tab<N, 4, INV>(a, g, Ns, tw + tbase);
+      else stage_compute_tab<N, 2, INV>(a, g, Ns, tw + tbase);
+      if (Ns > 1) tbase += Ns * (R - 1);
+    } else if (R == 8) stage_compute<N, 8, INV>(a, g, Ns, tw);
     else if (R == 4) stage_compute<N, 4, INV>(a, g, Ns, tw);
     else stage_compute<N, 2, INV>(a, g, Ns, tw);
     if (!is_last) {

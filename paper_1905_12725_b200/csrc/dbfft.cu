@@ -311,6 +311,7 @@ ColGeom geom_I1(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf)
   g.out_psh = ilog2(s.nzl); g.out_pcs = xpcs(ctx, s, nf);
   g.ncols = (long long)s.nyl * n1h;
   g.tw = ctx->tw3;
+  g.fpos = ctx->xiz;
   g.fq = Freq{ctx->xix, s.xiy, ctx->xiz};
   g.n_xy = s.nyl;
   return g;
@@ -324,6 +325,7 @@ ColGeom geom_I2(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_
   g.out_fs = s.Hsp; g.out_os = (long long)ctx->n2 * kxp; g.out_ps = kxp; g.out_psh = ilog2(ctx->n2); g.out_pcs = 0;
   g.ncols = (long long)s.nzl * n1h;
   g.tw = ctx->tw2;
+  g.fpos = ctx->xiy;
   g.fq = Freq{ctx->xix, ctx->xiy, ctx->xiz};
   g.n_xy = ctx->n2;
   return g;
@@ -337,6 +339,7 @@ ColGeom geom_F2(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_
   g.out_psh = ilog2(s.nyl); g.out_pcs = xpcs(ctx, s, nf_out);
   g.ncols = (long long)s.nzl * n1h;
   g.tw = ctx->tw2;
+  g.fpos = ctx->xiy;
   g.fq = Freq{ctx->xix, ctx->xiy, ctx->xiz};
   g.n_xy = ctx->n2;
   return g;
@@ -350,6 +353,7 @@ ColGeom geom_F3(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_
   g.out_fs = s.Hs; g.out_os = (long long)ctx->n3 * n1h; g.out_ps = n1h; g.out_psh = ilog2(ctx->n3); g.out_pcs = 0;
   g.ncols = (long long)s.nyl * n1h;
   g.tw = ctx->tw3;
+  g.fpos = ctx->xiz;
   g.fq = Freq{ctx->xix, s.xiy, ctx->xiz};
   g.n_xy = s.nyl;
   return g;
@@ -709,14 +713,32 @@ dbfft_status dalloc(dbfft_ctx ctx, T** p, size_t count) {
   return DBFFT_OK;
 }
 
+// W_n[k] = exp(-2 pi i k / n), k < n, from long double (0.5 ulp), followed for powers of two by the
+// stage-ordered table of the radix-8 plan (common.cuh fft_cta TAB): for every stage with Ns > 1,
+// rows k < Ns of the R-1 twiddles W_n^(r (n/(Ns R)) k) — each entry a table value, no products.
 dbfft_status make_twiddles(dbfft_ctx ctx, int n, cplx** out) {
-  std::vector<double2> h(n);
-  for (int k = 0; k < n; ++k) {
-    long double a = -2.0L * 3.14159265358979323846264338327950288L * (long double)k / (long double)n;
-    h[k] = make_double2((double)cosl(a), (double)sinl(a));
+  std::vector<double2> h(2 * (size_t)n);
+  auto W = [n](long long e) {
+    long double a = -2.0L * 3.14159265358979323846264338327950288L * (long double)(e % n) / (long double)n;
+    return make_double2((double)cosl(a), (double)sinl(a));
+  };
+  for (int k = 0; k < n; ++k) h[k] = W(k);
+  if ((n & (n - 1)) == 0) {
+    const int log2n = ilog2(n);
+    const int n8 = log2n / 3, last = 1 << (log2n - 3 * n8);
+    const int nst = n8 + (last > 1 ? 1 : 0);
+    size_t o = n;
+    int Ns = 1;
+    for (int st = 0; st < nst; ++st) {
+      const int R = st < n8 ? 8 : last;
+      if (Ns > 1)
+        for (int k = 0; k < Ns; ++k)
+          for (int r = 1; r < R; ++r) h[o++] = W((long long)r * (n / (Ns * R)) * k);
+      Ns *= R;
+    }
   }
-  CKS(dalloc(ctx, out, n));
-  CK(cudaMemcpy(*out, h.data(), sizeof(double2) * n, cudaMemcpyHostToDevice));
+  CKS(dalloc(ctx, out, h.size()));
+  CK(cudaMemcpy(*out, h.data(), sizeof(double2) * h.size(), cudaMemcpyHostToDevice));
   return DBFFT_OK;
 }
 

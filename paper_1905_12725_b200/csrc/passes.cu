@@ -75,8 +75,14 @@ int num_sms() {
 #ifndef DBF_X_STAGE_IN
 #define DBF_X_STAGE_IN 1
 #endif
+#ifndef DBF_X_PACK
+#define DBF_X_PACK 0  // 1: finite-strain apply kinds pair the 9 fields of two lines into 9 FFT jobs (B200 256^3: 0.990 -> 1.058 ms, slower)
+#endif
 #ifndef DBF_COL_MINB
 #define DBF_COL_MINB 4
+#endif
+#ifndef DBF_COL_TAB512
+#define DBF_COL_TAB512 0  // stage-table twiddles in the N = 512 TMA column passes too
 #endif
 namespace {
 
@@ -87,6 +93,7 @@ struct ColAt {
   const ColGeom* g;
   int outer, pos, kx;
   double xxk, xyo;  // xi_x(kx) and xi_y(outer) of the column (set with kx / outer; y passes: xyo unused)
+  double xp;        // xi along the pass's FFT axis at `pos` (z passes: xi_z, y passes: xi_y)
   DBF_DEV void set_col(int o, int k) {
     outer = o;
     kx = k;
@@ -132,7 +139,7 @@ struct ColOp<COL_I1S> {
     }
   }
   DBF_DEV static cplx pre(const ColAt& a, int j, cplx r0, cplx r1) {
-    const double xz = __ldg(a.g->fq.xz + a.pos);
+    const double xz = a.xp;
     switch (j) {
       case 0: case 1: return r0;
       case 2: return cimul(r0, xz);  // eps_zz
@@ -149,7 +156,7 @@ struct ColOp<COL_I1F> {
   static constexpr bool INV = true;
   static constexpr int NT = 6, MAXIN = 1;
   DBF_DEV static TermInfo term(int j) { return {j, 1, 1, j < 3 ? j : j - 3, -1}; }
-  DBF_DEV static cplx pre(const ColAt& a, int j, cplx r0, cplx) { return j < 3 ? r0 : cimul(r0, __ldg(a.g->fq.xz + a.pos)); }
+  DBF_DEV static cplx pre(const ColAt& a, int j, cplx r0, cplx) { return j < 3 ? r0 : cimul(r0, a.xp); }
   DBF_DEV static cplx post(const ColAt&, int) { return make_double2(1.0, 0.0); }
 };
 
@@ -172,8 +179,8 @@ struct ColOp<COL_I2S> {
   DBF_DEV static cplx pre(const ColAt& a, int j, cplx r0, cplx r1) {
     switch (j) {
       case 0: return cimul(r0, a.xxk);
-      case 1: return cimul(r0, __ldg(a.g->fq.xy + a.pos));
-      case 5: { const double xx = a.xxk, xy = __ldg(a.g->fq.xy + a.pos);
+      case 1: return cimul(r0, a.xp);
+      case 5: { const double xx = a.xxk, xy = a.xp;
                 return cimul(make_double2(xy * r0.x + xx * r1.x, xy * r0.y + xx * r1.y), 0.5); }
       default: return r0;
     }
@@ -192,7 +199,7 @@ struct ColOp<COL_I2F> {
     const int i = j / 3, jj = j % 3;
     return {j, 1, 1, jj == 2 ? 3 + i : i, -1};
   }
-  DBF_DEV static cplx pre(const ColAt& a, int j, cplx r0, cplx) { return (j % 3 == 1) ? cimul(r0, __ldg(a.g->fq.xy + a.pos)) : r0; }
+  DBF_DEV static cplx pre(const ColAt& a, int j, cplx r0, cplx) { return (j % 3 == 1) ? cimul(r0, a.xp) : r0; }
   DBF_DEV static cplx post(const ColAt& a, int j) {
     return (j % 3 == 0) ? make_double2(0.0, a.xxk) : make_double2(1.0, 0.0);
   }
@@ -220,7 +227,7 @@ struct ColOp<COL_F2F> {
     return (j < 6 && (j & 1) == 0) ? cimul(r0, -a.xxk) : r0;
   }
   DBF_DEV static cplx post(const ColAt& a, int j) {
-    if (j < 6 && (j & 1)) return make_double2(0.0, -__ldg(a.g->fq.xy + a.pos));
+    if (j < 6 && (j & 1)) return make_double2(0.0, -a.xp);
     return make_double2(1.0, 0.0);
   }
 };
@@ -245,7 +252,7 @@ struct ColOp<COL_F3S> {
     return cimul(make_double2(xx * r0.x + xy * r1.x, xx * r0.y + xy * r1.y), -1.0);
   }
   DBF_DEV static cplx post(const ColAt& a, int j) {
-    if (j & 1) return make_double2(0.0, -__ldg(a.g->fq.xz + a.pos));
+    if (j & 1) return make_double2(0.0, -a.xp);
     return make_double2(1.0, 0.0);
   }
 };
@@ -261,7 +268,7 @@ struct ColOp<COL_F3F> {
   }
   DBF_DEV static cplx pre(const ColAt&, int, cplx r0, cplx) { return r0; }
   DBF_DEV static cplx post(const ColAt& a, int j) {
-    if (j & 1) return make_double2(0.0, -__ldg(a.g->fq.xz + a.pos));
+    if (j & 1) return make_double2(0.0, -a.xp);
     return make_double2(1.0, 0.0);
   }
 };
@@ -351,6 +358,7 @@ __global__ void __launch_bounds__(256, ColCfg<N>::ODD ? 1 : ColPref<KIND>::MINB)
 #pragma unroll
     for (int s = 0; s < P; ++s) {
       at.pos = gq + s * TPC;
+      at.xp = __ldg(g.fpos + at.pos);
       r0[PREF ? s : 0] = valid ? at.in(ti.f0) : make_double2(0.0, 0.0);
     }
   }
@@ -361,6 +369,7 @@ __global__ void __launch_bounds__(256, ColCfg<N>::ODD ? 1 : ColPref<KIND>::MINB)
 #pragma unroll
     for (int s = 0; s < P; ++s) {
       at.pos = gq + s * TPC;
+      at.xp = __ldg(g.fpos + at.pos);
       if (PREF) {
         a[s] = Op::pre(at, j, r0[PREF ? s : 0], r0[PREF ? s : 0]);
       } else {
@@ -374,6 +383,7 @@ __global__ void __launch_bounds__(256, ColCfg<N>::ODD ? 1 : ColPref<KIND>::MINB)
 #pragma unroll
       for (int s = 0; s < P; ++s) {
         at.pos = gq + s * TPC;
+        at.xp = __ldg(g.fpos + at.pos);
         r0[PREF ? s : 0] = valid ? at.in(tn.f0) : make_double2(0.0, 0.0);
       }
     }
@@ -381,6 +391,7 @@ __global__ void __launch_bounds__(256, ColCfg<N>::ODD ? 1 : ColPref<KIND>::MINB)
 #pragma unroll
     for (int s = 0; s < P; ++s) {
       at.pos = gq + s * TPC;
+      at.xp = __ldg(g.fpos + at.pos);
       cplx v = cmul(Op::post(at, j), a[s]);
       if (TWO && !ti.first) v = cadd(v, sacc[idx(at.pos)]);
       if (!ti.last) {
@@ -737,14 +748,14 @@ struct XSync {
   int job;
   DBF_DEV void operator()() const { x_jobsync<N1, P>(job); }
 };
-template <int N1, int P, bool INV>
+template <int N1, int P, bool INV, bool TAB>
 DBF_DEV void x_fft(cplx (&a)[P], cplx* cx, int gq, int base, const cplx* __restrict__ tw, int job) {
   if constexpr ((N1 & 1) != 0) {
     fft_odd<N1, INV>(a, cx, gq, IdxPlain{base}, tw, XSync<N1, P>{job});
   } else if constexpr (P == 16) {
     fft_sub<N1, 16, INV>(a, cx, gq, IdxGrp{base}, tw, XSync<N1, 16>{job});
   } else {
-    fft_cta<N1, INV>(a, cx, gq, IdxSwz{base}, tw, XSync<N1, 8>{job});
+    fft_cta<N1, INV, IdxSwz, XSync<N1, 8>, TAB>(a, cx, gq, IdxSwz{base}, tw, XSync<N1, 8>{job});  // TAB: stage table
   }
 }
 
@@ -796,14 +807,22 @@ struct XCfg {
   typedef XTraits<KIND> T;
   typedef XStage<KIND> S;
   static constexpr int C = (T::CIN > T::COUT) ? T::CIN : T::COUT;
-  static constexpr int CS = (C + 1) & ~1;          // real slots per line (even)
+  // PACK (an odd field count, 9): the fields of LPAR (even) lines are numbered line-major and
+  // paired consecutively — the 18 fields of two lines make 9 pair FFTs, one pair spanning the two
+  // lines, instead of 2 x 5 pairs with an empty slot each (10 % less FFT work, and the voxel loop
+  // of 512 voxels over 288 threads idles less than 256 voxels over 160)
+  static constexpr bool PACK = DBF_X_PACK && (C & 1) && (N1 & 1) == 0 && (KIND == X_K_FIN_NH || KIND == X_K_FIN_TAN);
+  static constexpr int CS = PACK ? C : (C + 1) & ~1;  // real slots per line
   static constexpr int PX = (N1 & 1) ? PtsPerThread<N1>::value : (N1 >= 16) ? DBF_X_P : 8;   // FFT points per thread
   static constexpr int TPJ = N1 / PX;              // threads per pair FFT (divides 32: warp-local)
   static constexpr int NP = CS / 2;
   static constexpr int PERLINE = TPJ * NP;
-  static constexpr int LRAW = DBF_X_LRAW / PERLINE;
+  // PACK: 64/TPJ lines (at least 2) so that the CTA is whole warps (the untangle shuffles)
+  static constexpr int LRAW = PACK ? (TPJ >= 32 ? 2 : 64 / TPJ) : DBF_X_LRAW / PERLINE;
   static constexpr int LPAR = LRAW >= 64 ? 64 : LRAW >= 32 ? 32 : LRAW >= 16 ? 16 : LRAW >= 8 ? 8 : LRAW >= 4 ? 4 : LRAW >= 2 ? 2 : 1;
-  static constexpr int THREADS = LPAR * PERLINE;
+  static constexpr int NJOB = PACK ? LPAR * C / 2 : LPAR * NP;  // pair FFT jobs per line group
+  static constexpr int THREADS = NJOB * TPJ;
+  static_assert(!PACK || THREADS % 32 == 0, "packed pass_X CTAs are whole warps");
   static constexpr int N1H = N1 / 2 + 1;
   static constexpr size_t SLOTS = sizeof(double) * LPAR * CS * N1;
   // bulk-copy staging needs 16-byte rows: powers of two only (odd lines load directly)
@@ -812,8 +831,13 @@ struct XCfg {
   static constexpr size_t ST_IN = STG_SPEC ? sizeof(cplx) * LPAR * T::CIN * N1H : 0;
   static constexpr size_t ST_TAN = STG ? sizeof(double) * LPAR * S::NTAN * N1 : 0;
   static constexpr size_t ST_PH = (STG && S::PH) ? ((sizeof(uint16_t) * LPAR * N1 + 15) & ~size_t(15)) : 0;
-  static constexpr size_t SMEM = SLOTS + ST_IN + ST_TAN + ST_PH + 16;  // + 2 mbarriers
-  static constexpr int MINB = ((KIND == X_K_J2 && !DBF_X_STAGE_TAN_J2) || (KIND == X_K_FIN_NH && !DBF_X_STAGE_TAN_NH))
+  // stage-ordered twiddles (N1 - 1) in shared memory for the 9-field kinds (B200 256^3 finite
+  // pass_X 1.099 -> 0.990 ms); the 6-field small-strain kinds measured a little slower with it
+  static constexpr bool TAB = (N1 & 1) == 0 && C == 9;
+  static constexpr size_t ST_TW = TAB ? sizeof(cplx) * N1 : 0;
+  static constexpr size_t SMEM = SLOTS + ST_IN + ST_TAN + ST_PH + 16 + ST_TW;  // + 2 mbarriers
+  static constexpr int MINB = PACK ? (THREADS <= 160 ? DBF_X_MINB_NOTAN : THREADS <= 320 ? 2 : 1)
+                               : ((KIND == X_K_J2 && !DBF_X_STAGE_TAN_J2) || (KIND == X_K_FIN_NH && !DBF_X_STAGE_TAN_NH))
                                    ? DBF_X_MINB_NOTAN
                                : (KIND == X_CONST_FIN || KIND == X_CONST_J2) ? DBF_X_MINB_CONST
                                : (THREADS <= 192) ? DBF_X_MINB : 2;
@@ -892,11 +916,20 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
   double* st_tan = reinterpret_cast<double*>(sb + CF::SLOTS + CF::ST_IN);
   uint16_t* st_ph = reinterpret_cast<uint16_t*>(sb + CF::SLOTS + CF::ST_IN + CF::ST_TAN);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sb + CF::SLOTS + CF::ST_IN + CF::ST_TAN + CF::ST_PH);
+  cplx* stab = reinterpret_cast<cplx*>(bars + 2);
+  // odd lengths keep the plain W_N table (mixed-radix fft_odd); CF::TAB kinds the stage table
+  const cplx* twx = CF::TAB ? stab : g.tw;
+  if constexpr (CF::TAB) {
+    for (int i = threadIdx.x; i < N1 - 1; i += CF::THREADS) stab[i] = __ldg(g.tw + N1 + i);
+    __syncthreads();
+  }
   const int t = threadIdx.x;
   const int job = t / TPJ, gq = t % TPJ;
-  const int l = job / NP, p = job % NP;
-  const int fa = 2 * p, fb = 2 * p + 1;
-  const int jbase = ((l * CS + fa) * N1) / 2;  // complex view of slots fa, fb of line l (job buffer)
+  // the job's two fields: slots ca, cb of the line group (line-major, CS per line); without PACK
+  // both lie in one line, with PACK a pair may span two lines
+  const int ca = 2 * job, cb = 2 * job + 1;
+  const int la = ca / CS, fa = ca % CS, lb = cb / CS, fb = cb % CS;
+  const int jbase = (ca * N1) / 2;  // complex view of the job's two slots (its FFT exchange buffer)
   const int cin = (KIND == X_REAL_OUT) ? nf_real : T::CIN;
   const int cout_rt = (KIND == X_REAL_IN) ? nf_real : T::COUT;  // spectral outputs written
   const bool do_in = (T::CIN > 0) && (cin > 0) && ((KIND != X_CONST_FIN && KIND != X_CONST_J2) || g.has_in);
@@ -927,8 +960,8 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
   uint32_t it = 0;
 
   for (long long grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
-    const long long line = grp * LPAR + l;
-    const bool lvalid = line < g.nlines;
+    const long long linea = grp * LPAR + la, lineb = grp * LPAR + lb;
+    const bool va = linea < g.nlines, vb = lineb < g.nlines;
     const long long nxt = grp + gridDim.x;
     // ------------------------------------------------------------ inverse (C2R) of pairs
     if (do_in) {
@@ -940,17 +973,9 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
         const bool lo = x_lo<N1, PX, TPJ>(s, gq);
         const int kk = lo ? k : N1 - k;
         cplx A = make_double2(0, 0), B = make_double2(0, 0);
-        if (lvalid && fa < cin) {
-          if (SSP) {
-            A = st_in[(l * T::CIN + fa) * CF::N1H + kk];
-            if (fb < cin) B = st_in[(l * T::CIN + fb) * CF::N1H + kk];
-          } else {
-            const long long base = line * g.kxp + kk;
-            A = __ldg(g.in + fa * g.fs_in + base);
-            if (fb < cin) B = __ldg(g.in + fb * g.fs_in + base);
-          }
-          if (kk == 0 || 2 * kk == N1) { A.y = 0.0; B.y = 0.0; }  // Hermitian part (C2R)
-        }
+        if (va && fa < cin) A = SSP ? st_in[(la * T::CIN + fa) * CF::N1H + kk] : __ldg(g.in + fa * g.fs_in + linea * g.kxp + kk);
+        if (vb && fb < cin) B = SSP ? st_in[(lb * T::CIN + fb) * CF::N1H + kk] : __ldg(g.in + fb * g.fs_in + lineb * g.kxp + kk);
+        if (kk == 0 || 2 * kk == N1) { A.y = 0.0; B.y = 0.0; }  // Hermitian part (C2R)
         // Y_k = A_k + i B_k (k <= N/2);  conj(A_{N-k}) + i conj(B_{N-k}) otherwise
         a[s] = lo ? make_double2(A.x - B.y, A.y + B.x) : make_double2(A.x + B.y, B.x - A.y);
       }
@@ -961,13 +986,13 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
           x_issue_in<N1, KIND>(g, nxt, st_in, &bars[0]);
         }
       }
-      x_fft<N1, PX, true>(a, cx, gq, jbase, g.tw, job);
+      x_fft<N1, PX, true, CF::TAB>(a, cx, gq, jbase, twx, job);
       x_jobsync<N1, PX>(job);  // the job's exchange reads are done before its slots become reals
 #pragma unroll
       for (int s = 0; s < PX; ++s) {
         const int m = gq + s * TPJ;
-        real[(l * CS + fa) * N1 + m] = a[s].x;
-        real[(l * CS + fb) * N1 + m] = a[s].y;
+        real[ca * N1 + m] = a[s].x;
+        real[cb * N1 + m] = a[s].y;
       }
     }
     __syncthreads();
@@ -1031,11 +1056,11 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
 #pragma unroll
       for (int s = 0; s < PX; ++s) {
         const int m = gq + s * TPJ;
-        const double ra = (fa < COUT) ? real[(l * CS + fa) * N1 + m] : 0.0;
-        const double rb = (fb < COUT) ? real[(l * CS + fb) * N1 + m] : 0.0;
+        const double ra = (fa < COUT) ? real[ca * N1 + m] : 0.0;
+        const double rb = (fb < COUT) ? real[cb * N1 + m] : 0.0;
         a[s] = make_double2(ra, rb);
       }
-      x_fft<N1, PX, false>(a, cx, gq, jbase, g.tw, job);
+      x_fft<N1, PX, false, CF::TAB>(a, cx, gq, jbase, twx, job);
       constexpr bool SHFL = (PX == 8 && TPJ <= 32);
       cplx zn[PX];
       if constexpr (SHFL) {
@@ -1048,7 +1073,8 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
 #pragma unroll
         for (int s = 0; s < PX; ++s) zn[s] = cx[x_idx<N1, PX>(jbase, (N1 - (gq + s * TPJ)) % N1)];
       }
-      if (lvalid && fa < cout_rt) {
+      const bool sta = va && fa < cout_rt, stb = vb && fb < cout_rt;
+      if (sta || stb) {
 #pragma unroll
         for (int s = 0; s < PX; ++s) {
           const int k = gq + s * TPJ;
@@ -1061,12 +1087,11 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
           const cplx B = make_double2(Z.y + Zn.y, Zn.x - Z.x);
           if (DCRED && s == 0 && gq == 0) {  // k = 0: the line sums of the pair (<sigma> / <dP>)
             const double dcs = 0.5 / g.oscale;  // undo the exact 1/(2N) of the voxel outputs
-            s_dc[DCRED ? l : 0][x_red_slot<KIND>(fa)] += dcs * A.x;
-            if (fb < COUT) s_dc[DCRED ? l : 0][x_red_slot<KIND>(fb)] += dcs * B.x;
+            if (sta) s_dc[DCRED ? la : 0][x_red_slot<KIND>(fa)] += dcs * A.x;
+            if (stb && fb < COUT) s_dc[DCRED ? lb : 0][x_red_slot<KIND>(fb)] += dcs * B.x;
           }
-          const long long base = line * g.kxp + k;
-          g.out[fa * g.fs_out + base] = A;
-          if (fb < cout_rt) g.out[fb * g.fs_out + base] = B;
+          if (sta) g.out[fa * g.fs_out + linea * g.kxp + k] = A;
+          if (stb) g.out[fb * g.fs_out + lineb * g.kxp + k] = B;
         }
       }
       __syncthreads();  // slots are reused by the next group
@@ -1242,6 +1267,19 @@ struct TmaCfg {
   static constexpr int THREADS = CONS + 32;    // + producer warp
   static constexpr int TILE = 32768;           // bytes per ring slot / staging buffer
   static constexpr int SW = KC < 8 ? KC : 8;   // sub-tile width in columns (TMA box rows of 16 SW bytes)
+  // twiddles from the stage-ordered table in shared memory (B200 256^3 finite apply_K 2.71 -> 2.43
+  // ms); at N = 512 the product-of-table-entries twiddles stayed faster for I1 / I2 (2.55 / 6.15 ms
+  // vs 2.78 / 7.15 ms with the table)
+  static constexpr bool TAB = N <= 256 || DBF_COL_TAB512;
+};
+// per pass: the small-strain F2 (a plain 6 -> 6 transform, the fastest pass at 5.1 TB/s) ran
+// slower with the table (256^3: 0.318 -> 0.343 ms) and keeps the products
+template <int N, int KIND>
+struct ColTab {
+  static constexpr bool value = TmaCfg<N>::TAB && KIND != COL_F2S;
+  // xi at the thread's positions hoisted into registers (not where the 168-register cap of the
+  // 288-thread CTA would spill: the two-accumulator small-strain F3 at N = 512)
+  static constexpr bool HOIST = !(KIND == COL_F3S && N == 512);
 };
 
 // cplx offset of (pos, column c) inside a main tile: KC/8 sub-tiles of [N][8], 128B swizzle
@@ -1287,6 +1325,7 @@ template <int N, int KIND, bool DOT, int R, bool UPD = false>
 __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __grid_constant__ TmaMaps maps, ColGeom g, ColTiles tl) {
   typedef ColOp<KIND> Op;
   typedef TmaCfg<N> CF;
+  constexpr bool TAB = ColTab<N, KIND>::value;
   if (g.cg_stop0 && (*g.cg_stop0 | *g.cg_stop1)) return;  // PCG stopped (UPD: r stays as it is)
   constexpr int KC = CF::KC, TPC = CF::TPC;
   constexpr int S = UPD ? 3 : 2;  // staging buffers (UPD: r_0, r_1 of a tile stay readable until r_2)
@@ -1299,6 +1338,7 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
   cplx* xb = reinterpret_cast<cplx*>(base + (R + S) * CF::TILE);
   uint64_t* full = reinterpret_cast<uint64_t*>(base + (R + S + 1) * CF::TILE);
   uint64_t* empty = full + R;
+  cplx* stab = reinterpret_cast<cplx*>(empty + R);  // stage-ordered twiddles (N - 1), copied once
   const TProg& pg = c_prog[2 * KIND + (DOT ? 1 : 0)];
   const int t = threadIdx.x;
   const int warp = t >> 5;
@@ -1309,6 +1349,8 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (TAB)
+    for (int i = t; i < N - 1; i += CF::THREADS) stab[i] = __ldg(g.tw + N + i);
   __syncthreads();
   const int nl = pg.nl;
 
@@ -1348,6 +1390,10 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
   const int gq = t % TPC;  // position group
   const int lane = t & 31;
   cplx* xcol = xb + c * N;  // this column's FFT exchange buffer
+  double xpos[ColTab<N, KIND>::HOIST ? 8 : 1];  // xi along the FFT axis at this thread's positions (every tile)
+  if (ColTab<N, KIND>::HOIST)
+#pragma unroll
+    for (int s = 0; s < 8; ++s) xpos[ColTab<N, KIND>::HOIST ? s : 0] = __ldg(g.fpos + gq + s * TPC);
   double acc_rz = 0.0, acc_rr = 0.0;  // UPD: partial <r, M r>, <r, r>
   const double alpha = UPD ? *g.cg_alpha : 0.0;
   __shared__ double sprec[UPD ? 36 : 1];  // M's coefficients (device memory -> shared, once)
@@ -1387,13 +1433,14 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
 #pragma unroll
       for (int s = 0; s < 8; ++s) {
         at.pos = gq + s * TPC;
+        at.xp = ColTab<N, KIND>::HOIST ? xpos[ColTab<N, KIND>::HOIST ? s : 0] : __ldg(g.fpos + at.pos);
         const int o = tail ? tma_toff<N>(at.pos, c) : tma_moff<N>(at.pos, c);
         const cplx v0 = sa[o];
         const cplx v1 = (lb >= 0) ? sbp[o] : v0;
         a[s] = Op::pre(at, j, v0, v1);
       }
-      if constexpr (TPC <= 32) fft_cta<N, Op::INV>(a, xcol, gq, IdxSwz{0}, g.tw, SyncWarp{});
-      else fft_cta<N, Op::INV>(a, xcol, gq, IdxSwz{0}, g.tw, SyncCol{2 + c, TPC});
+      if constexpr (TPC <= 32) fft_cta<N, Op::INV, IdxSwz, SyncWarp, TAB>(a, xcol, gq, IdxSwz{0}, TAB ? stab : g.tw, SyncWarp{});
+      else fft_cta<N, Op::INV, IdxSwz, SyncCol, TAB>(a, xcol, gq, IdxSwz{0}, TAB ? stab : g.tw, SyncCol{2 + c, TPC});
       const int ai = pg.acc[k];
       const int ld = pg.ldot[k];
       const cplx* sd = nullptr;
@@ -1406,6 +1453,7 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
 #pragma unroll
       for (int s = 0; s < 8; ++s) {
         at.pos = gq + s * TPC;
+        at.xp = ColTab<N, KIND>::HOIST ? xpos[ColTab<N, KIND>::HOIST ? s : 0] : __ldg(g.fpos + at.pos);
         cplx v = cmul(Op::post(at, j), a[s]);
         if (ColTwo<KIND>::value && !ti.first) v = cadd(v, (NACC > 1 && ai) ? acc1[NACC > 1 ? s : 0] : acc0[s]);
         if (ColTwo<KIND>::value && !ti.last) {
@@ -1552,6 +1600,7 @@ static cudaError_t launch_col_n(int kind, const ColGeom& g, cudaStream_t s) {
 #ifndef DBF_COL_R
 #define DBF_COL_R 3
 #endif
+
 static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -1627,11 +1676,19 @@ struct ColRing {  // ring depth: 3 slots; small-strain F3 (two-term outputs from
                            : (KIND == COL_I1F || KIND == COL_F2F || (DBF_RING2_SMALL && (KIND == COL_I1S || KIND == COL_F2S))) ? 2
                            : DBF_COL_R;
 };
+// ring depth of a launch: the fused F3 + residual update (3 staging buffers) takes 2 slots — its
+// program's live span is 2 — and the small-strain F3 3 (span 2) when the stage twiddle table is
+// in shared memory, so that everything fits 227 KB
+template <int N, int KIND, bool DOT, bool UPD>
+struct ColRingL {
+  static constexpr int R = UPD ? 2 : (KIND == COL_F3S && ColTab<N, KIND>::value) ? 3 : ColRing<KIND, DOT>::R;
+};
 
 template <int N, int KIND, bool DOT, bool UPD = false>
 static cudaError_t launch_col_tma_k(const TmaMaps& maps, const ColGeom& g, const ColTiles& tl, cudaStream_t s, int* grid_out) {
-  constexpr int R = ColRing<KIND, DOT>::R;
-  constexpr size_t smem = (size_t)(R + (UPD ? 3 : 2) + 1) * TmaCfg<N>::TILE + 2 * R * sizeof(uint64_t) + 1024;
+  constexpr int R = ColRingL<N, KIND, DOT, UPD>::R;
+  constexpr size_t smem = (size_t)(R + (UPD ? 3 : 2) + 1) * TmaCfg<N>::TILE + 2 * R * sizeof(uint64_t) +
+                          (ColTab<N, KIND>::value ? sizeof(cplx) * N : 0) + 1024;
   static DevOnce once;
   cudaError_t e = dev_once(once, [](int&) {
     if (col_prog_span(kColProgHost[2 * KIND + (DOT ? 1 : 0)]) > R) return cudaErrorInvalidConfiguration;

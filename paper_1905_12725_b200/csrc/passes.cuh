@@ -20,7 +20,8 @@ struct ColGeom {
   int in_psh, out_psh;   // log2 of the rank chunk along the FFT axis (log2 N: plain)
   int n1h;
   long long ncols;   // n_outer * n1h columns
-  const cplx* tw;    // twiddles W_N[k], k < N
+  const cplx* tw;    // twiddles W_N[k], k < N, then the stage-ordered table (N - 1, powers of two)
+  const double* fpos;  // xi along the FFT axis, indexed by position (z passes: xi_z, y passes: xi_y)
   Freq fq;
   // F3 fused with the PCG residual update (TMA path only): out = dotp = r, streamed through the
   // ring; r -= alpha q, partial <r, M r>, <r, r> per CTA into partials[2 blockIdx] (Hermitian
