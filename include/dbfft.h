@@ -25,7 +25,8 @@
  *  - REAL FIELD layout (host or device, double): [component][z][y][x] (x fastest).
  *    Second-order tensors have 9 components, row-major (c = 3 i + j).
  *  - Macro 3x3 quantities (targets, masks, e blocks, reports): 9 entries, row-major.
- *  - Ownership: the ctx owns all of its device memory (cudaMalloc).  Pointers passed in are
+ *  - Ownership: the ctx owns all of its device memory (cudaMalloc, or the env allocator hooks
+ *    below, e.g. torch's caching allocator).  Pointers passed in are
  *    borrowed for the duration of the call only; inputs are copied when retained.
  *  - Streams: all device work of a ctx is issued on env->cuda_stream (a cudaStream_t, e.g.
  *    torch.cuda.current_stream().cuda_stream) or on a ctx-owned stream if NULL.  Calls marked
@@ -82,6 +83,14 @@ typedef struct {
                             their chunk for rank d straight into rank d's receive buffer
                             through a CUDA VMM window (NVLink peer memory; one node), a
                             device barrier replaces the exchange.  All-reduces stay NCCL. */
+  /* Device memory of the ctx (every buffer except the peer transport's CUDA VMM windows):
+   * dev_alloc(bytes, alloc_user) returns device memory on `device` (NULL: DBFFT_E_OOM) and
+   * dev_free(ptr, alloc_user) releases it — e.g. torch's caching allocator.  Both NULL: cudaMalloc
+   * / cudaFree.  Called from the thread calling the ABI; frees happen after the ctx stream has
+   * drained (destroy, set_phases). */
+  void* (*dev_alloc)(size_t bytes, void* alloc_user);
+  void (*dev_free)(void* ptr, void* alloc_user);
+  void* alloc_user;
 } dbfft_env;
 enum { DBFFT_TRANSPORT_NCCL = 0, DBFFT_TRANSPORT_PEER = 1 };
 
@@ -213,9 +222,14 @@ typedef enum {
   DBFFT_FIELD_U = 0,        /* fluctuation displacement u~(x): 3 x N doubles          */
   DBFFT_FIELD_STRAIN = 1,   /* eps (small) or F (finite): 9 x N doubles                        */
   DBFFT_FIELD_STRESS = 2,   /* sigma (small) or P (finite): 9 x N doubles                      */
-  DBFFT_FIELD_U_HAT = 3     /* u~_hat, spectral vector layout (3 x H complex)                  */
+  DBFFT_FIELD_U_HAT = 3,    /* u~_hat, spectral vector layout (3 x H complex)                  */
+  DBFFT_FIELD_TANGENT = 4   /* the tangent apply_K uses, 81 x N doubles [(9a + b)][z][y][x] with
+                               a = 3i + j, b = 3k + l: C_ijkl (small strain: the phase stiffness or
+                               the J2 algorithmic tangent, P:204 / R16) or dP_ij/dF_kl (finite,
+                               R14 / P:326), of the last Newton iterate / eval_state              */
 } dbfft_field;
-/* Copy a field of the committed state into `out` (host if out_on_device == 0). (sync) */
+/* Copy a field of the committed state (TANGENT: of the current state) into `out` (host if
+ * out_on_device == 0; loopback: the global array, NCCL: this rank's z-slab). (sync) */
 dbfft_status dbfft_get_field(dbfft_ctx ctx, int32_t which, void* out, int32_t out_on_device);
 
 /* Residual monitors of the committed state (SS3 of the paper; finite strain P:327-330):

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -136,6 +137,10 @@ struct dbfft_ctx_s {
   int device;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  // device allocations: the caller's allocator (e.g. torch's caching allocator) or cudaMalloc
+  void* (*dev_alloc)(size_t, void*) = nullptr;
+  void (*dev_free)(void*, void*) = nullptr;
+  void* alloc_user = nullptr;
   std::string err;
   ncclComm_t comm = nullptr;
   // peer transport (env->transport = 1): exchange windows, flag window, barrier bookkeeping
@@ -228,12 +233,20 @@ struct DevGuard {
   }
 };
 
+// NVTX range (host timeline of a profiler: per pass launch, per solve / Newton iteration / PCG
+// loop); header-only NVTX v3, a no-op unless a tool is attached
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
+
 // ---------------------------------------------------------------- profiling helpers
 struct ProfScope {
   dbfft_ctx ctx;
   int id;
   int i0 = -1;
-  ProfScope(dbfft_ctx c, int k) : ctx(c), id(k) {
+  Nvtx range;
+  ProfScope(dbfft_ctx c, int k) : ctx(c), id(k), range(kProfNames[k]) {
     ctx->nlaunch += 1;
     if (!ctx->prof) return;
     if (ctx->ev_next + 2 > ctx->ev_pool.size()) {
@@ -709,8 +722,23 @@ __global__ void k_identity9(double* F9, long long n) {
 
 template <typename T>
 dbfft_status dalloc(dbfft_ctx ctx, T** p, size_t count) {
-  CK(cudaMalloc((void**)p, sizeof(T) * std::max<size_t>(count, 1)));
+  const size_t bytes = sizeof(T) * std::max<size_t>(count, 1);
+  if (ctx->dev_alloc) {
+    *p = static_cast<T*>(ctx->dev_alloc(bytes, ctx->alloc_user));
+    if (!*p) {
+      ctx->err = "env allocator returned NULL for " + std::to_string(bytes) + " bytes";
+      return DBFFT_E_OOM;
+    }
+    return DBFFT_OK;
+  }
+  CK(cudaMalloc((void**)p, bytes));
   return DBFFT_OK;
+}
+
+void dfree(dbfft_ctx ctx, void* p) {
+  if (!p) return;
+  if (ctx->dev_free) ctx->dev_free(p, ctx->alloc_user);
+  else cudaFree(p);
 }
 
 // W_n[k] = exp(-2 pi i k / n), k < n, from long double (0.5 ulp), followed for powers of two by the
@@ -991,6 +1019,7 @@ dbfft_status pcg_iterate(dbfft_ctx ctx, const dbfft_opts& o, bool macro, int nb)
     dbfft_status st = DBFFT_OK;
     if (!lg.exec || lg.gen != ctx->gen) st = build_loop_graph(ctx, macro, nb, &lg);
     if (st == DBFFT_OK) {
+      Nvtx range("pcg_while_graph");
       CK(cudaGraphLaunch(lg.exec, ctx->stream));
       CK(cudaMemcpyAsync(ctx->h_cg, ctx->slabs[0].cg, sizeof(CgDev), cudaMemcpyDeviceToHost, ctx->stream));
       CK(cudaStreamSynchronize(ctx->stream));
@@ -1033,6 +1062,7 @@ dbfft_status pcg_iterate(dbfft_ctx ctx, const dbfft_opts& o, bool macro, int nb)
 }
 
 dbfft_status pcg(dbfft_ctx ctx, const dbfft_opts& o, int* iters_out) {
+  Nvtx range("pcg");
   const int nb = cg_blocks();
   const bool macro = ctx->h_cg->macro != 0;
   for (Slab& s : ctx->slabs) {
@@ -1071,6 +1101,7 @@ dbfft_status pcg(dbfft_ctx ctx, const dbfft_opts& o, int* iters_out) {
       return DBFFT_E_NOT_CONVERGED;
     }
     // true-residual confirmation (R7): r = b - A x
+    Nvtx range_tr("pcg_true_residual");
     ApplyOut ao;
     CKS(apply_K_slabs(ctx, &Slab::x, &Slab::q, macro, &CgDev::xe, &ao));
     for (size_t k = 0; k < ctx->slabs.size(); ++k) {
@@ -1380,6 +1411,7 @@ dbfft_status solve_linear(dbfft_ctx ctx, const double* target, const uint8_t* ma
 // ---------------------------------------------------------------- Newton
 // constitutive pass: state += grad(du) + dF ; P, K ; b = F(div P) ; returns <P>, max|d|
 dbfft_status constitutive(dbfft_ctx ctx, bool has_in, const double* dF_host, double dt, double* meanP, double* maxd) {
+  Nvtx range("constitutive_update");
   const bool fin = ctx->kin == 9;
   CKS(upload_e(ctx, dF_host));
   for (Slab& s : ctx->slabs) CK(cudaMemsetAsync(s.bad, 0x7f, sizeof(int), ctx->stream));
@@ -1451,6 +1483,7 @@ dbfft_status solve_newton(dbfft_ctx ctx, const double* target, const uint8_t* ma
   double last = 0.0;
   bool conv = false;
   while (st == DBFFT_OK) {
+    Nvtx range("newton_iteration");
     // preconditioner refresh policy ("computed at the beginning of the increment ... can be
     // recomputed once in a while"; "computed with the initial tangent stiffness")
     if (o.precond_refresh == 2) {
@@ -1523,16 +1556,16 @@ dbfft_status solve_newton(dbfft_ctx ctx, const double* target, const uint8_t* ma
   return DBFFT_OK;
 }
 
-void free_slab(Slab& s, bool peer) {
+void free_slab(dbfft_ctx ctx, Slab& s) {
   void* ptrs[] = {s.x, s.r, s.p, s.q, s.b, s.u, s.u_c, s.WA, s.WB, s.phase, s.ptable, s.F, s.F_c, s.epsp_c, s.epsp_t, s.tan,
                   s.cg, s.part_x, s.part_cg, s.part_misc, s.loc, s.e_dev, s.bad, s.counts, s.tmp_real};
-  for (void* p : ptrs)
-    if (p) cudaFree(p);
-  if (!peer && s.WR && s.WR != s.WA) cudaFree(s.WR);
+  for (void* p : ptrs) dfree(ctx, p);
+  if (!ctx->peer && s.WR && s.WR != s.WA) dfree(ctx, s.WR);
 }
 
 void free_all(dbfft_ctx ctx) {
-  for (Slab& s : ctx->slabs) free_slab(s, ctx->peer);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);  // an external allocator may reuse the memory at once
+  for (Slab& s : ctx->slabs) free_slab(ctx, s);
   peer_free(&ctx->pb1);
   peer_free(&ctx->pb2);
   peer_free(&ctx->pbf);
@@ -1540,8 +1573,7 @@ void free_all(dbfft_ctx ctx) {
     for (int k = 0; k < 4; ++k)
       if (lg[k].exec) cudaGraphExecDestroy(lg[k].exec);
   void* ptrs[] = {ctx->xix, ctx->xiy, ctx->xiz, ctx->tw1, ctx->tw2, ctx->tw3, ctx->loc_ptrs, ctx->trace_dev, ctx->prec_dev};
-  for (void* p : ptrs)
-    if (p) cudaFree(p);
+  for (void* p : ptrs) dfree(ctx, p);
   if (ctx->h_cg) cudaFreeHost(ctx->h_cg);
   if (ctx->h_red) cudaFreeHost(ctx->h_red);
   if (ctx->h_bad) cudaFreeHost(ctx->h_bad);
@@ -1550,13 +1582,12 @@ void free_all(dbfft_ctx ctx) {
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
 }
 
-void free_state(Slab& s) {
+void free_state(dbfft_ctx ctx, Slab& s) {
   double** ptrs[] = {&s.F, &s.F_c, &s.epsp_c, &s.epsp_t, &s.tan};
-  for (double** p : ptrs)
-    if (*p) {
-      cudaFree(*p);
-      *p = nullptr;
-    }
+  for (double** p : ptrs) {
+    dfree(ctx, *p);
+    *p = nullptr;
+  }
 }
 
 dbfft_status ensure_tmp(dbfft_ctx ctx, Slab& s) {
@@ -1776,6 +1807,16 @@ dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinemat
   ctx->loopback = (P > 1 && loopback) ? 1 : 0;
   ctx->rank = ctx->loopback ? 0 : rank;
   ctx->peer = (P > 1 && env && env->transport == DBFFT_TRANSPORT_PEER) ? 1 : 0;
+  if (env && (env->dev_alloc != nullptr) != (env->dev_free != nullptr)) {
+    g_create_error = "env: dev_alloc and dev_free must be given together";
+    delete ctx;
+    return DBFFT_E_INVALID_ARG;
+  }
+  if (env) {
+    ctx->dev_alloc = env->dev_alloc;
+    ctx->dev_free = env->dev_free;
+    ctx->alloc_user = env->alloc_user;
+  }
   memset(ctx->prof_ms, 0, sizeof(ctx->prof_ms));
   memset(ctx->prof_n, 0, sizeof(ctx->prof_n));
   for (int a = 0; a < 9; ++a) ctx->Fbar[a] = ctx->Fbar_c[a] = 0.0;
@@ -2046,11 +2087,12 @@ dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t o
     if (!sl.phase && (s = dalloc(ctx, &sl.phase, sl.Nloc)) != DBFFT_OK) return s;
     const long long off = ctx->loopback ? (long long)sl.z0 * plane : 0;
     CK(cudaMemcpyAsync(sl.phase, phase_id + off, sizeof(uint16_t) * sl.Nloc, kind, ctx->stream));
-    if (sl.ptable) cudaFree(sl.ptable);
+    CK(cudaStreamSynchronize(ctx->stream));  // kernels still reading the old table / counts
+    dfree(ctx, sl.ptable);
     sl.ptable = nullptr;
     if ((s = dalloc(ctx, &sl.ptable, pt.size())) != DBFFT_OK) return s;
     CK(cudaMemcpyAsync(sl.ptable, pt.data(), sizeof(double) * pt.size(), cudaMemcpyHostToDevice, ctx->stream));
-    if (sl.counts) cudaFree(sl.counts);
+    dfree(ctx, sl.counts);
     sl.counts = nullptr;
     if ((s = dalloc(ctx, &sl.counts, n_phases)) != DBFFT_OK) return s;
     CK(cudaMemsetAsync(sl.counts, 0, sizeof(double) * n_phases, ctx->stream));
@@ -2080,7 +2122,7 @@ dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t o
   ctx->family = fam;
   ++ctx->gen;  // buffers baked into captured PCG loops change below
   for (Slab& sl : ctx->slabs) {
-    free_state(sl);
+    free_state(ctx, sl);
     CK(cudaMemsetAsync(sl.u, 0, sizeof(cplx) * 3 * sl.Hs, ctx->stream));
     CK(cudaMemsetAsync(sl.u_c, 0, sizeof(cplx) * 3 * sl.Hs, ctx->stream));
   }
@@ -2236,6 +2278,7 @@ dbfft_status dbfft_solve_increment(dbfft_ctx ctx, const double target[9], const 
     CKS(dalloc(ctx, &ctx->trace_dev, 2 * (size_t)ctx->trace_cap));
   }
   ctx->trace_n = 0;
+  Nvtx range("dbfft_solve_increment");
   auto t0 = std::chrono::steady_clock::now();
   if (report) {
     memset(report, 0, sizeof(*report));
@@ -2440,6 +2483,31 @@ dbfft_status dbfft_get_field(dbfft_ctx ctx, int32_t which, void* out, int32_t ou
     case DBFFT_FIELD_STRESS:
       CKS(field_to_tmp(ctx, which));
       return gather_real(ctx, &Slab::tmp_real, 9, (double*)out, out_on_device);
+    case DBFFT_FIELD_TANGENT: {
+      // the full 3x3x3x3 tangent of the current state, built per voxel from what apply_K reads,
+      // in chunks through a device scratch of 81 x chunk doubles
+      const int mode = ctx->family == FAM_LINEAR ? 3 : ctx->family == FAM_J2 ? 2 : (ctx->tmode ? 1 : 0);
+      const long long plane = (long long)ctx->n1 * ctx->n2;
+      const long long Ndst = ctx->loopback ? ctx->N : ctx->slabs[0].Nloc;
+      const long long chunk = std::min<long long>(ctx->slabs[0].Nloc, 1LL << 20);
+      double* scratch = nullptr;
+      CKS(dalloc(ctx, &scratch, 81 * (size_t)chunk));
+      cudaError_t e = cudaSuccess;
+      for (Slab& s : ctx->slabs) {
+        const long long off = ctx->loopback ? (long long)s.z0 * plane : 0;
+        for (long long v0 = 0; v0 < s.Nloc && e == cudaSuccess; v0 += chunk) {
+          const long long nv = std::min(chunk, s.Nloc - v0);
+          e = launch_tangent81(mode, xgeom(ctx, s, nullptr, nullptr), v0, nv, scratch, ctx->stream);
+          if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync((double*)out + off + v0, sizeof(double) * Ndst, scratch, sizeof(double) * nv,
+                                  sizeof(double) * nv, 81, k, ctx->stream);
+          if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);  // the scratch is reused
+        }
+      }
+      dfree(ctx, scratch);
+      CK(e);
+      return DBFFT_OK;
+    }
     default:
       ctx->err = "get_field: unknown field";
       return DBFFT_E_INVALID_ARG;

@@ -1188,6 +1188,59 @@ __global__ void __launch_bounds__(256) k_mean_tangent(XGeom g, double* partials)
   }
 }
 
+// per-voxel tangent as a full 3x3x3x3 array (DBFFT_FIELD_TANGENT): out[(9 a + b) nv + (v - v0)],
+// a = 3i + j, b = 3k + l, for voxels v0 <= v < v0 + nv.  MODE 0: stored 45-entry upper triangle
+// (finite); 1: compact neo-Hookean (F^-1, c1); 2: compact J2 (theta, thetabar, n); 3: linear phase
+// stiffness (Voigt 6x6 of tensor components, ptable)
+template <int MODE>
+__global__ void __launch_bounds__(256) k_tangent81(XGeom g, long long v0, long long nv, double* __restrict__ out) {
+  const int vo[9] = {0, 5, 4, 5, 1, 3, 4, 3, 2};  // row-major entry -> Voigt index
+  for (long long e = (long long)blockIdx.x * 256 + threadIdx.x; e < nv; e += (long long)gridDim.x * 256) {
+    const long long v = v0 + e;
+    double* o = out + e;
+    if (MODE == 0 || MODE == 1) {
+      double K45[45];
+      if (MODE == 0) {
+#pragma unroll
+        for (int k = 0; k < 45; ++k) K45[k] = g.tan[(long long)k * g.nvox + v];
+      } else {
+        double Fi[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) Fi[k] = g.tan[(long long)k * g.nvox + v];
+        const int ph = g.phase[v];
+        const double mu = g.ptable[36 * ph], lam = g.ptable[36 * ph + 1] - 2.0 * mu / 3.0;
+        nh_tangent45(Fi, g.tan[9 * g.nvox + v], mu, lam, K45);
+      }
+#pragma unroll
+      for (int a = 0; a < 9; ++a)
+#pragma unroll
+        for (int b = 0; b < 9; ++b) o[(long long)(9 * a + b) * nv] = K45[sym9(a, b)];
+    } else if (MODE == 2) {
+      // C_alg = kappa 1 x 1 + 2 mu theta I_dev - 2 mu thetabar n x n   (R16, j2_update)
+      double tc[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) tc[k] = g.tan[(long long)k * g.nvox + v];
+      double kappa, mu;
+      j2_moduli(g.ptable + 36 * g.phase[v], &kappa, &mu);
+#pragma unroll
+      for (int a = 0; a < 9; ++a)
+#pragma unroll
+        for (int b = 0; b < 9; ++b) {
+          const int i = a / 3, j = a % 3, k = b / 3, l = b % 3;
+          const double idev = 0.5 * ((i == k && j == l) + (i == l && j == k)) - ((i == j && k == l) ? 1.0 / 3.0 : 0.0);
+          o[(long long)(9 * a + b) * nv] = ((i == j && k == l) ? kappa : 0.0) + 2.0 * mu * tc[0] * idev -
+                                          2.0 * mu * tc[1] * tc[2 + vo[a]] * tc[2 + vo[b]];
+        }
+    } else {
+      const double* C = g.ptable + 36 * g.phase[v];
+#pragma unroll
+      for (int a = 0; a < 9; ++a)
+#pragma unroll
+        for (int b = 0; b < 9; ++b) o[(long long)(9 * a + b) * nv] = C[6 * vo[a] + vo[b]];
+    }
+  }
+}
+
 // ------------------------------------------------------------------------------------------------
 // Column passes, TMA pipeline.  Persistent, one CTA per SM:
 // warp 8 (one elected lane) streams 32 KB tiles — KC = 2048/N kx-columns x N positions of ONE
@@ -1842,6 +1895,17 @@ int x_grid(int kind, int N1, long long nlines) {
   (void)kind;
   (void)N1;
   return (int)std::min<long long>(nlines, 32LL * num_sms());  // <= 32 resident CTAs per SM
+}
+
+cudaError_t launch_tangent81(int mode, const XGeom& g, long long v0, long long nv, double* out, cudaStream_t s) {
+  const int grid = (int)std::min<long long>((nv + 255) / 256, 8LL * num_sms());
+  switch (mode) {
+    case 0: k_tangent81<0><<<grid, 256, 0, s>>>(g, v0, nv, out); break;
+    case 1: k_tangent81<1><<<grid, 256, 0, s>>>(g, v0, nv, out); break;
+    case 2: k_tangent81<2><<<grid, 256, 0, s>>>(g, v0, nv, out); break;
+    default: k_tangent81<3><<<grid, 256, 0, s>>>(g, v0, nv, out); break;
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_mean_tangent(int mode, const XGeom& g, double* partials, int nblk, cudaStream_t s) {

@@ -117,5 +117,8 @@ int x_grid(int kind, int N1, long long nlines);
 // streaming multiprocessors of the current device (cached per device)
 int num_sms();
 int col_grid(int N, long long ncols);
+// per-voxel tangent, full 81 entries [81][nv] of voxels v0 .. v0+nv (mode 0: stored 45, 1: compact
+// neo-Hookean, 2: compact J2, 3: linear phase table)
+cudaError_t launch_tangent81(int mode, const XGeom& g, long long v0, long long nv, double* out, cudaStream_t s);
 // mean tangent partials (mode 0: full 45, 1: compact neo-Hookean -> 45, 2: compact J2 -> 21)
 cudaError_t launch_mean_tangent(int mode, const XGeom& g, double* partials, int nblk, cudaStream_t s);

@@ -12,10 +12,35 @@ LIB_PATH = os.path.join(HERE, "libdbfft.so")
 # ---------------------------------------------------------------------------- C types
 
 
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p)
+
+
 class Env(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
                 ("cuda_stream", ctypes.c_void_p), ("device", ctypes.c_int32), ("loopback", ctypes.c_int32),
-                ("transport", ctypes.c_int32)]
+                ("transport", ctypes.c_int32), ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN),
+                ("alloc_user", ctypes.c_void_p)]
+
+
+def torch_allocator(device):
+    """dbfft_env allocator hooks backed by torch's CUDA caching allocator (the ctx's buffers show up
+    in torch.cuda.memory_allocated and are recycled by torch after close())."""
+    import torch
+
+    def alloc(nbytes, _user):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), device)
+        except Exception:  # noqa: BLE001  (out of memory -> NULL -> DBFFT_E_OOM)
+            return None
+
+    def free(ptr, _user):
+        try:
+            torch.cuda.caching_allocator_delete(ptr)
+        except Exception:  # noqa: BLE001  (interpreter shutdown)
+            pass
+
+    return ALLOC_FN(alloc), FREE_FN(free)
 
 TRANSPORTS = {"nccl": 0, "peer": 1}
 
@@ -39,7 +64,7 @@ class Report(ctypes.Structure):
 
 
 MAT_ISO, MAT_CUBIC, MAT_NEOHOOKE, MAT_J2, MAT_SVK = 1, 2, 3, 4, 5
-FIELD_U, FIELD_STRAIN, FIELD_STRESS, FIELD_U_HAT = 0, 1, 2, 3
+FIELD_U, FIELD_STRAIN, FIELD_STRESS, FIELD_U_HAT, FIELD_TANGENT = 0, 1, 2, 3, 4
 STATUS = {0: "OK", 1: "E_INVALID_GRID", 2: "E_INVALID_ARG", 3: "E_STATE", 4: "E_CUDA", 5: "E_NCCL", 6: "E_OOM",
           7: "E_NOT_CONVERGED", 8: "E_BREAKDOWN", 9: "E_MATERIAL"}
 
@@ -154,11 +179,13 @@ class DBFFT:
     """One DBFFT context on one CUDA device (include/dbfft.h)."""
 
     def __init__(self, n, L=(1.0, 1.0, 1.0), kinematics="small", device=0, stream=None,
-                 world=1, rank=0, loopback=False, process_group=None, transport="nccl"):
+                 world=1, rank=0, loopback=False, process_group=None, transport="nccl", allocator="torch"):
         """world > 1: slab decomposition (include/dbfft.h "Distribution").  loopback=True keeps
         all `world` virtual ranks in this process; otherwise NCCL, with the unique id broadcast
         over `process_group` (torch.distributed, any backend).  transport: "nccl" (all-to-all
-        exchanges) or "peer" (passes store into the peers' receive buffers, dbfft_env.transport)."""
+        exchanges) or "peer" (passes store into the peers' receive buffers, dbfft_env.transport).
+        allocator: "torch" (the ctx's device memory from torch's caching allocator, dbfft_env
+        dev_alloc / dev_free) or "cuda" (cudaMalloc)."""
         import torch
         self.torch = torch
         self.lib = load_library()
@@ -171,8 +198,15 @@ class DBFFT:
         self._nccl_id = None
         if self.world > 1 and not self.loopback:
             self._nccl_id = nccl_unique_id_broadcast(self.rank, process_group)
+        if allocator == "torch":
+            self._alloc = torch_allocator(device)   # kept alive as long as the ctx
+        elif allocator == "cuda":
+            self._alloc = (ALLOC_FN(), FREE_FN())
+        else:
+            raise ValueError(allocator)
         env = Env(self.rank, self.world, ctypes.cast(self._nccl_id, ctypes.c_void_p) if self._nccl_id else None,
-                  ctypes.c_void_p(self.stream.cuda_stream), device, int(self.loopback), TRANSPORTS[transport])
+                  ctypes.c_void_p(self.stream.cuda_stream), device, int(self.loopback), TRANSPORTS[transport],
+                  self._alloc[0], self._alloc[1], None)
         h = ctypes.c_void_p()
         st = self.lib.dbfft_create((ctypes.c_int32 * 3)(*self.n), (ctypes.c_double * 3)(*L), self.kin,
                                    ctypes.byref(env), ctypes.byref(h))
@@ -327,7 +361,7 @@ class DBFFT:
             n3 //= self.world  # NCCL slab mode: this rank's z-slab
         N = n1 * n2 * n3
         if out is not None:
-            ncomp = 3 if which == FIELD_U else 9
+            ncomp = {FIELD_U: 3, FIELD_TANGENT: 81}.get(which, 9)
             if which == FIELD_U_HAT or not isinstance(out, np.ndarray) or out.dtype != np.float64 \
                     or out.size != ncomp * N or not out.flags["C_CONTIGUOUS"]:
                 raise ValueError("get_field(out=): a C-contiguous float64 host array of the field's size")
@@ -337,7 +371,7 @@ class DBFFT:
             out = self.empty_spectral()
             self._check(self.lib.dbfft_get_field(self.h, which, _dptr(out), 1))
             return out
-        ncomp = 3 if which == FIELD_U else 9
+        ncomp = {FIELD_U: 3, FIELD_TANGENT: 81}.get(which, 9)
         if on_device:
             out = self.torch.empty((ncomp, n3, n2, n1), dtype=self.torch.float64, device=self.device)
             self._check(self.lib.dbfft_get_field(self.h, which, _dptr(out), 1))
@@ -349,6 +383,8 @@ class DBFFT:
         self._check(self.lib.dbfft_get_field(self.h, which, out.ctypes.data_as(ctypes.c_void_p), 0))
         if ncomp == 9:
             out = out.reshape(3, 3, n3, n2, n1)
+        elif ncomp == 81:
+            out = out.reshape(3, 3, 3, 3, n3, n2, n1)
         return out
 
     # ------------------------------------------------------------------ residual monitors
