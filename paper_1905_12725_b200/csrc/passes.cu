@@ -75,6 +75,9 @@ int num_sms() {
 #ifndef DBF_X_STAGE_IN
 #define DBF_X_STAGE_IN 1
 #endif
+#ifndef DBF_X_PREFETCH
+#define DBF_X_PREFETCH 1  // pass_X: bulk L2 prefetch of the next line group's per-voxel tangent rows
+#endif
 #ifndef DBF_X_PACK
 #define DBF_X_PACK 0  // 1: finite-strain apply kinds pair the 9 fields of two lines into 9 FFT jobs (B200 256^3: 0.990 -> 1.058 ms, slower)
 #endif
@@ -595,12 +598,12 @@ DBF_DEV void j2_moduli(const double* prm, double* kappa, double* mu) {
 // the 1/(2N)-scaled P)
 template <int KIND>
 DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* red, const double* tp, long long ts, int ph,
-                     double& xd) {
+                     double& xd, const double* se) {
   if (KIND == X_K_SMALL_PHASE || KIND == X_RHS_SMALL_PHASE || KIND == X_K_J2) {
     double e6[6];
 #pragma unroll
     for (int I = 0; I < 6; ++I)
-      e6[I] = (KIND == X_RHS_SMALL_PHASE ? 0.0 : G[I]) + (g.e ? __ldg(g.e + c_row9_of_voigt[I]) : 0.0);
+      e6[I] = (KIND == X_RHS_SMALL_PHASE ? 0.0 : G[I]) + (se ? se[c_row9_of_voigt[I]] : 0.0);
     double s[6];
     if (KIND == X_K_J2) {
       double tc[8];
@@ -625,7 +628,7 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
 #pragma unroll
     for (int k = 0; k < 45; ++k) K[k] = ld_stream(tp + k * ts);
 #pragma unroll
-    for (int a = 0; a < 9; ++a) e9[a] = G[a] + (g.e ? __ldg(g.e + a) : 0.0);
+    for (int a = 0; a < 9; ++a) e9[a] = G[a] + (se ? se[a] : 0.0);
 #pragma unroll
     for (int a = 0; a < 9; ++a) {
       double acc = 0.0;
@@ -642,7 +645,7 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
     const double c1 = tp[9 * ts];
     const double mu = __ldg(g.ptable + 36 * ph), lam = __ldg(g.ptable + 36 * ph + 1) - 2.0 * mu / 3.0;
 #pragma unroll
-    for (int a = 0; a < 9; ++a) e9[a] = G[a] + (g.e ? __ldg(g.e + a) : 0.0);
+    for (int a = 0; a < 9; ++a) e9[a] = G[a] + (se ? se[a] : 0.0);
     nh_apply(Fi, c1 * g.oscale, mu * g.oscale, lam * g.oscale, e9, P);  // P x 1/(2N): exact for powers of 2
 #pragma unroll
     for (int a = 0; a < 9; ++a) xd += G[a] * P[a];
@@ -651,7 +654,7 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
     double mx = 0.0;
 #pragma unroll
     for (int a = 0; a < 9; ++a) {
-      const double d = (g.has_in ? G[a] : 0.0) + __ldg(g.e + a);
+      const double d = (g.has_in ? G[a] : 0.0) + se[a];
       mx = fmax(mx, fabs(d));
       F[a] = g.F[(long long)a * g.nvox + v] + d;
       g.F[(long long)a * g.nvox + v] = F[a];
@@ -696,7 +699,7 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
     double mx = 0.0;
 #pragma unroll
     for (int I = 0; I < 6; ++I) {
-      const double d = (g.has_in ? G[I] : 0.0) + __ldg(g.e + c_row9_of_voigt[I]);
+      const double d = (g.has_in ? G[I] : 0.0) + se[c_row9_of_voigt[I]];
       mx = fmax(mx, fabs(d));
       eps[I] = g.F[(long long)I * g.nvox + v] + d;
       g.F[(long long)I * g.nvox + v] = eps[I];
@@ -843,6 +846,18 @@ struct XCfg {
                                : (THREADS <= 192) ? DBF_X_MINB : 2;
 };
 
+// per-voxel tangent arrays an apply kind reads in its voxel loop from global memory (L2-prefetched
+// one line group ahead)
+template <int KIND>
+struct XPref {
+  static constexpr int NTAN = DBF_X_PREFETCH ? ((KIND == X_K_FIN_NH) ? (DBF_X_STAGE_TAN_NH ? 0 : 10)
+                                              : (KIND == X_K_J2) ? (DBF_X_STAGE_TAN_J2 ? 0 : 8)
+                                              : (KIND == X_K_FIN_TAN) ? 45 : 0) : 0;
+};
+DBF_DEV void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // ---- bulk async copy (TMA engine) + mbarrier helpers ------------------------------------------
 DBF_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 DBF_DEV void mbar_init(uint64_t* bar, int count) {
@@ -937,9 +952,11 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
   // apply kinds: <sigma> / <dP> from the k = 0 outputs of the R2C (one owner thread per field)
   constexpr bool DCRED = XDcRed<KIND>::value;
   __shared__ double s_dc[DCRED ? LPAR : 1][10];  // per line slot of the CTA: one owner thread per entry
+  __shared__ double s_e[9];  // the macro block (read by every voxel; one load per CTA, not per voxel)
   if (DCRED)
     for (int i = t; i < 10 * LPAR; i += CF::THREADS) s_dc[i / 10][i % 10] = 0.0;
-  if (DCRED) __syncthreads();
+  if (g.e && t < 9) s_e[t] = g.e[t];
+  __syncthreads();
   double xdot = 0.0;  // apply kinds: sum (G + e) : sigma over the CTA's voxels
   double red[T::NRED > 0 ? T::NRED : 1];
 #pragma unroll
@@ -961,6 +978,14 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
 
   for (long long grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
     const long long linea = grp * LPAR + la, lineb = grp * LPAR + lb;
+    // per-voxel data read in the voxel loop straight from global memory: the next group's rows
+    // go to L2 now (bulk prefetch), so the voxel loop's loads hit L2 instead of HBM
+    if (XPref<KIND>::NTAN > 0 && t == 0 && grp + gridDim.x < ngroups) {
+      const long long v1 = (grp + gridDim.x) * LPAR * N1;
+      const uint32_t bytes = (uint32_t)(sizeof(double) * N1 * min((long long)LPAR, g.nlines - (grp + gridDim.x) * LPAR));
+#pragma unroll 1
+      for (int k = 0; k < XPref<KIND>::NTAN; ++k) prefetch_l2(g.tan + (long long)k * g.nvox + v1, bytes);
+    }
     const bool va = linea < g.nlines, vb = lineb < g.nlines;
     const long long nxt = grp + gridDim.x;
     // ------------------------------------------------------------ inverse (C2R) of pairs
@@ -1039,7 +1064,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
         ts = g.nvox;
         ph = (KIND == X_K_FIN_TAN || KIND == X_REAL_OUT) ? 0 : (int)__ldg(g.phase + v);
       }
-      x_voxel<KIND>(g, v, G, P, red, tp, ts, ph, xdot);
+      x_voxel<KIND>(g, v, G, P, red, tp, ts, ph, xdot, g.e ? s_e : nullptr);
 #pragma unroll
       for (int f = 0; f < T::COUT; ++f) real[(l2 * CS + f) * N1 + x] = P[f];
     }

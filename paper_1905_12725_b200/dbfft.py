@@ -185,7 +185,7 @@ class DBFFT:
         over `process_group` (torch.distributed, any backend).  transport: "nccl" (all-to-all
         exchanges) or "peer" (passes store into the peers' receive buffers, dbfft_env.transport).
         allocator: "torch" (the ctx's device memory from torch's caching allocator, dbfft_env
-        dev_alloc / dev_free) or "cuda" (cudaMalloc)."""
+        dev_alloc / dev_free), "cuda" (cudaMalloc) or a tuple (alloc(nbytes) -> ptr, free(ptr))."""
         import torch
         self.torch = torch
         self.lib = load_library()
@@ -198,7 +198,10 @@ class DBFFT:
         self._nccl_id = None
         if self.world > 1 and not self.loopback:
             self._nccl_id = nccl_unique_id_broadcast(self.rank, process_group)
-        if allocator == "torch":
+        if isinstance(allocator, tuple):  # (alloc(nbytes) -> device pointer, free(ptr)) Python callables
+            fa, ff = allocator
+            self._alloc = (ALLOC_FN(lambda nbytes, _u: fa(int(nbytes))), FREE_FN(lambda ptr, _u: ff(ptr)))
+        elif allocator == "torch":
             self._alloc = torch_allocator(device)   # kept alive as long as the ctx
         elif allocator == "cuda":
             self._alloc = (ALLOC_FN(), FREE_FN())
