@@ -1149,10 +1149,11 @@ ColGeom geom_F3_update(dbfft_ctx ctx, Slab& s) {
 
 bool pcg_fused(dbfft_ctx ctx) {
   const char* e = getenv("DBFFT_FUSED_UPDATE");
-  // finite strain only: small strain's F3S program leaves no ring slot for r, and the variant
-  // that loads r straight from global memory ran slower than F3 + k_cg_update (c5 512^3: 8.6 vs
-  // 6.2 ms per iteration)
-  if ((e && e[0] == '0') || ctx->kin != 9) return false;
+  // opt-in (DBFFT_FUSED_UPDATE=1): once the plain F3 took the stage twiddle table it ran faster
+  // unfused (B200 c4 256^3, 2 steps: F3 + k_cg_update 79 + 56 ms vs the fused F3 154 ms; value
+  // 5.03e9 vs 4.99e9).  Finite strain only: small strain's F3S program leaves no ring slot for r,
+  // and a variant reading r straight from global memory was slower (c5 512^3: 8.6 vs 6.2 ms).
+  if (!(e && e[0] == '1') || ctx->kin != 9) return false;
   for (Slab& s : ctx->slabs)
     if (!col_upd_supported(ctx->n3, geom_F3_update(ctx, s))) return false;
   return true;

@@ -84,6 +84,9 @@ int num_sms() {
 #ifndef DBF_COL_MINB
 #define DBF_COL_MINB 4
 #endif
+#ifndef DBF_UPD_TAB
+#define DBF_UPD_TAB 0  // the fused F3 + residual update with the stage table (and a 2-slot ring to fit)
+#endif
 #ifndef DBF_COL_TAB512
 #define DBF_COL_TAB512 0  // stage-table twiddles in the N = 512 TMA column passes too
 #endif
@@ -1119,7 +1122,9 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
           if (stb) g.out[fb * g.fs_out + lineb * g.kxp + k] = B;
         }
       }
-      __syncthreads();  // slots are reused by the next group
+      // no barrier here: a job's R2C and the next group's C2R touch only the job's own two slots
+      // (their reals and FFT exchange), the voxel loop and the real-field kinds that read every
+      // slot sit behind the unconditional barrier after the C2R
     }
   }
 
@@ -1403,7 +1408,7 @@ template <int N, int KIND, bool DOT, int R, bool UPD = false>
 __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __grid_constant__ TmaMaps maps, ColGeom g, ColTiles tl) {
   typedef ColOp<KIND> Op;
   typedef TmaCfg<N> CF;
-  constexpr bool TAB = ColTab<N, KIND>::value;
+  constexpr bool TAB = ColTab<N, KIND>::value && (!UPD || DBF_UPD_TAB);
   if (g.cg_stop0 && (*g.cg_stop0 | *g.cg_stop1)) return;  // PCG stopped (UPD: r stays as it is)
   constexpr int KC = CF::KC, TPC = CF::TPC;
   constexpr int S = UPD ? 3 : 2;  // staging buffers (UPD: r_0, r_1 of a tile stay readable until r_2)
@@ -1759,14 +1764,15 @@ struct ColRing {  // ring depth: 3 slots; small-strain F3 (two-term outputs from
 // in shared memory, so that everything fits 227 KB
 template <int N, int KIND, bool DOT, bool UPD>
 struct ColRingL {
-  static constexpr int R = UPD ? 2 : (KIND == COL_F3S && ColTab<N, KIND>::value) ? 3 : ColRing<KIND, DOT>::R;
+  static constexpr bool TAB = ColTab<N, KIND>::value && (!UPD || DBF_UPD_TAB);
+  static constexpr int R = UPD ? (TAB ? 2 : 3) : (KIND == COL_F3S && TAB) ? 3 : ColRing<KIND, DOT>::R;
 };
 
 template <int N, int KIND, bool DOT, bool UPD = false>
 static cudaError_t launch_col_tma_k(const TmaMaps& maps, const ColGeom& g, const ColTiles& tl, cudaStream_t s, int* grid_out) {
   constexpr int R = ColRingL<N, KIND, DOT, UPD>::R;
   constexpr size_t smem = (size_t)(R + (UPD ? 3 : 2) + 1) * TmaCfg<N>::TILE + 2 * R * sizeof(uint64_t) +
-                          (ColTab<N, KIND>::value ? sizeof(cplx) * N : 0) + 1024;
+                          (ColRingL<N, KIND, DOT, UPD>::TAB ? sizeof(cplx) * N : 0) + 1024;
   static DevOnce once;
   cudaError_t e = dev_once(once, [](int&) {
     if (col_prog_span(kColProgHost[2 * KIND + (DOT ? 1 : 0)]) > R) return cudaErrorInvalidConfiguration;
