@@ -268,6 +268,17 @@ const char* dbfft_profile_name(int32_t kernel_id);
 dbfft_status dbfft_launch_count(dbfft_ctx ctx, int64_t* count);
 int32_t dbfft_profile_count(void);
 
+/* Per-increment dump / resume of the committed state (host blob, layout private to this library
+ * version, with a header checked on restore): the fluctuation spectrum u~_hat, the macro strain /
+ * F, the per-voxel committed state (F or eps, and the J2 plastic strain) and the increment count
+ * (preconditioner policy 3).  dbfft_checkpoint: buf NULL -> *bytes = size needed; else copies
+ * (DBFFT_E_INVALID_ARG if *bytes is too small).  dbfft_restore: into a ctx of the same grid,
+ * kinematics, material family and decomposition, after dbfft_set_phases with the same
+ * microstructure; the next dbfft_solve_increment continues exactly where the dumped ctx would.
+ * Loopback: all slabs; NCCL: this rank's slab.  (sync) */
+dbfft_status dbfft_checkpoint(dbfft_ctx ctx, void* buf, size_t* bytes);
+dbfft_status dbfft_restore(dbfft_ctx ctx, const void* buf, size_t bytes);
+
 /* One-line JSON description of ctx (host): device and SM count, world / rank / loopback, the
  * transport of the two all-to-alls ("none" | "nccl" | "peer"), whether an NCCL communicator is
  * live, and how the last PCG loop ran ("device-side WHILE graph", host-polled graph rounds or

@@ -2598,6 +2598,118 @@ dbfft_status dbfft_incompatibility(dbfft_ctx ctx, const double* field, int32_t o
   return incompat_max(ctx, out);
 }
 
+// ---------------------------------------------------------------- checkpoint / resume
+namespace {
+struct CkptHeader {
+  char magic[8];  // "DBFFTCK1"
+  int32_t n[3], kin, family, P, rank, nph, tmode, pad;
+  int64_t n_incr;
+  double Fbar_c[9];
+};
+
+size_t ckpt_bytes(dbfft_ctx ctx) {
+  size_t b = sizeof(CkptHeader);
+  for (const Slab& s : ctx->slabs) {
+    b += sizeof(cplx) * 3 * (size_t)s.Hs;
+    if (ctx->family == FAM_NEOHOOKE || ctx->family == FAM_J2) b += sizeof(double) * state_fields(ctx) * (size_t)s.Nloc;
+    if (ctx->family == FAM_J2) b += sizeof(double) * 6 * (size_t)s.Nloc;
+  }
+  return b;
+}
+}  // namespace
+
+dbfft_status dbfft_checkpoint(dbfft_ctx ctx, void* buf, size_t* bytes) {
+  if (!ctx || !bytes) return DBFFT_E_INVALID_ARG;
+  DevGuard dev_guard(ctx->device);
+  if (ctx->family == FAM_NONE) {
+    ctx->err = "checkpoint before set_phases";
+    return DBFFT_E_STATE;
+  }
+  const size_t need = ckpt_bytes(ctx);
+  if (!buf) {
+    *bytes = need;
+    return DBFFT_OK;
+  }
+  if (*bytes < need) {
+    ctx->err = "checkpoint: buffer of " + std::to_string(*bytes) + " bytes, need " + std::to_string(need);
+    *bytes = need;
+    return DBFFT_E_INVALID_ARG;
+  }
+  *bytes = need;
+  CkptHeader h;
+  memset(&h, 0, sizeof(h));
+  memcpy(h.magic, "DBFFTCK1", 8);
+  h.n[0] = ctx->n1; h.n[1] = ctx->n2; h.n[2] = ctx->n3;
+  h.kin = ctx->kin; h.family = ctx->family; h.P = ctx->P; h.rank = ctx->rank; h.nph = ctx->nph; h.tmode = ctx->tmode;
+  h.n_incr = ctx->n_incr;
+  memcpy(h.Fbar_c, ctx->Fbar_c, sizeof(h.Fbar_c));
+  char* o = static_cast<char*>(buf);
+  memcpy(o, &h, sizeof(h));
+  o += sizeof(h);
+  const int nf = state_fields(ctx);
+  for (Slab& s : ctx->slabs) {
+    CK(cudaMemcpyAsync(o, s.u_c, sizeof(cplx) * 3 * s.Hs, cudaMemcpyDeviceToHost, ctx->stream));
+    o += sizeof(cplx) * 3 * s.Hs;
+    if (ctx->family == FAM_NEOHOOKE || ctx->family == FAM_J2) {
+      CK(cudaMemcpyAsync(o, s.F_c, sizeof(double) * nf * s.Nloc, cudaMemcpyDeviceToHost, ctx->stream));
+      o += sizeof(double) * nf * s.Nloc;
+    }
+    if (ctx->family == FAM_J2) {
+      CK(cudaMemcpyAsync(o, s.epsp_c, sizeof(double) * 6 * s.Nloc, cudaMemcpyDeviceToHost, ctx->stream));
+      o += sizeof(double) * 6 * s.Nloc;
+    }
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return DBFFT_OK;
+}
+
+dbfft_status dbfft_restore(dbfft_ctx ctx, const void* buf, size_t bytes) {
+  if (!ctx || !buf) return DBFFT_E_INVALID_ARG;
+  DevGuard dev_guard(ctx->device);
+  if (ctx->family == FAM_NONE) {
+    ctx->err = "restore before set_phases";
+    return DBFFT_E_STATE;
+  }
+  CkptHeader h;
+  if (bytes < sizeof(h)) {
+    ctx->err = "restore: truncated checkpoint";
+    return DBFFT_E_INVALID_ARG;
+  }
+  memcpy(&h, buf, sizeof(h));
+  if (memcmp(h.magic, "DBFFTCK1", 8) != 0 || h.n[0] != ctx->n1 || h.n[1] != ctx->n2 || h.n[2] != ctx->n3 || h.kin != ctx->kin ||
+      h.family != ctx->family || h.P != ctx->P || h.rank != ctx->rank || h.nph != ctx->nph || bytes != ckpt_bytes(ctx)) {
+    ctx->err = "restore: checkpoint of another grid / kinematics / material family / decomposition, or wrong size";
+    return DBFFT_E_INVALID_ARG;
+  }
+  const char* o = static_cast<const char*>(buf) + sizeof(h);
+  const int nf = state_fields(ctx);
+  for (Slab& s : ctx->slabs) {
+    CK(cudaMemcpyAsync(s.u_c, o, sizeof(cplx) * 3 * s.Hs, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(s.u, s.u_c, sizeof(cplx) * 3 * s.Hs, cudaMemcpyDeviceToDevice, ctx->stream));
+    o += sizeof(cplx) * 3 * s.Hs;
+    if (ctx->family == FAM_NEOHOOKE || ctx->family == FAM_J2) {
+      CK(cudaMemcpyAsync(s.F_c, o, sizeof(double) * nf * s.Nloc, cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(s.F, s.F_c, sizeof(double) * nf * s.Nloc, cudaMemcpyDeviceToDevice, ctx->stream));
+      o += sizeof(double) * nf * s.Nloc;
+    }
+    if (ctx->family == FAM_J2) {
+      CK(cudaMemcpyAsync(s.epsp_c, o, sizeof(double) * 6 * s.Nloc, cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(s.epsp_t, s.epsp_c, sizeof(double) * 6 * s.Nloc, cudaMemcpyDeviceToDevice, ctx->stream));
+      o += sizeof(double) * 6 * s.Nloc;
+    }
+  }
+  CK(cudaStreamSynchronize(ctx->stream));  // the blob may be freed on return
+  memcpy(ctx->Fbar_c, h.Fbar_c, sizeof(h.Fbar_c));
+  memcpy(ctx->Fbar, h.Fbar_c, sizeof(h.Fbar_c));
+  ctx->n_incr = h.n_incr;
+  if (ctx->family != FAM_LINEAR) {  // tangent (and M) of the restored committed state, as after a commit
+    double zero[9] = {0}, mp[9], mx;
+    CKS(constitutive(ctx, false, zero, 1.0, mp, &mx));
+    CKS(refresh_mean_tangent(ctx));
+  }
+  return DBFFT_OK;
+}
+
 dbfft_status dbfft_get_trace(dbfft_ctx ctx, double* out, int32_t cap, int32_t* n) {
   if (!ctx || !n || (cap > 0 && !out)) return DBFFT_E_INVALID_ARG;
   DevGuard dev_guard(ctx->device);

@@ -74,7 +74,8 @@ EXPORTS = ["dbfft_create", "dbfft_destroy", "dbfft_last_error", "dbfft_spectral_
            "dbfft_solve_increment", "dbfft_get_field", "dbfft_profile_enable", "dbfft_profile_read",
            "dbfft_profile_name", "dbfft_profile_count", "dbfft_launch_count", "dbfft_nccl_unique_id",
            "dbfft_residuals", "dbfft_incompatibility", "dbfft_get_trace", "dbfft_fd_allgather",
-           "dbfft_peer_probe_open", "dbfft_peer_probe_check", "dbfft_peer_probe_close", "dbfft_info"]
+           "dbfft_peer_probe_open", "dbfft_peer_probe_check", "dbfft_peer_probe_close", "dbfft_info", "dbfft_checkpoint",
+           "dbfft_restore"]
 
 _lib = None
 
@@ -127,6 +128,8 @@ def load_library(path=None):
     lib.dbfft_incompatibility.argtypes = [P, P, I32, ctypes.POINTER(D)]
     lib.dbfft_get_trace.argtypes = [P, ctypes.POINTER(D), I32, ctypes.POINTER(I32)]
     lib.dbfft_info.argtypes = [P, ctypes.c_char_p, I32]
+    lib.dbfft_checkpoint.argtypes = [P, P, ctypes.POINTER(ctypes.c_size_t)]
+    lib.dbfft_restore.argtypes = [P, P, ctypes.c_size_t]
     for fn in EXPORTS:
         getattr(lib, fn).restype = getattr(lib, fn).restype if fn in (
             "dbfft_last_error", "dbfft_default_opts", "dbfft_profile_name", "dbfft_profile_count") else ctypes.c_int
@@ -414,6 +417,20 @@ class DBFFT:
         out = ctypes.c_double()
         self._check(self.lib.dbfft_incompatibility(self.h, f.ctypes.data_as(ctypes.c_void_p), 0, ctypes.byref(out)))
         return out.value
+
+    # ------------------------------------------------------------------ checkpoint / resume
+    def checkpoint(self):
+        """The committed state as bytes (dbfft_checkpoint)."""
+        n = ctypes.c_size_t(0)
+        self._check(self.lib.dbfft_checkpoint(self.h, None, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value)
+        self._check(self.lib.dbfft_checkpoint(self.h, buf, ctypes.byref(n)))
+        return buf.raw[: n.value]
+
+    def restore(self, blob):
+        """Install a checkpoint (after set_phases with the same microstructure)."""
+        buf = ctypes.create_string_buffer(bytes(blob), len(blob))
+        self._check(self.lib.dbfft_restore(self.h, buf, len(blob)))
 
     # ------------------------------------------------------------------ profiling
     def info(self):

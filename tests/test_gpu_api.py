@@ -144,3 +144,33 @@ def test_not_converged_is_a_status(dbf):
     assert np.allclose(ctx.get_field(dbf.FIELD_U_HAT).abs().cpu().numpy(), 0.0)
     rep = ctx.solve_increment(L["target"], L["mask"])
     assert rep["converged"]
+
+
+@pytest.mark.parametrize("which", ["finite", "j2", "linear_loopback"])
+def test_checkpoint_restore_resumes_exactly(dbf, which):
+    """dbfft_checkpoint after two increments; a fresh ctx restored from it runs the third increment
+    bit-identically to the original ctx (same Newton / PCG counts, fields, macro values)."""
+    if which == "finite":
+        cfg, kin, kw = configs.c4(n=16, radius_vox=2), "finite", {}
+    elif which == "j2":
+        cfg, kin, kw = configs.c5(n=16, grains=4, increments=3), "small", {}
+    else:
+        cfg, kin, kw = configs.c2(n=32, radius_vox=3), "small", dict(world=2, loopback=True)
+        cfg["loads"] = [dict(target=t * cfg["loads"][0]["target"], mask=cfg["loads"][0]["mask"]) for t in (1, 2, 3)]
+    loads = cfg["loads"][:3]
+    a = dbf.DBFFT(cfg["n"], kinematics=kin, **kw)
+    a.set_phases(cfg["phase"], cfg["materials"])
+    for L in loads[:2]:
+        a.solve_increment(L["target"], L["mask"], dt=1.0)
+    blob = a.checkpoint()
+    ra = a.solve_increment(loads[2]["target"], loads[2]["mask"], dt=1.0)
+    b = dbf.DBFFT(cfg["n"], kinematics=kin, **kw)
+    b.set_phases(cfg["phase"], cfg["materials"])
+    b.restore(blob)
+    rb = b.solve_increment(loads[2]["target"], loads[2]["mask"], dt=1.0)
+    assert (ra["cg_iters"], ra["newton_iters"]) == (rb["cg_iters"], rb["newton_iters"])
+    assert np.array_equal(ra["macro_stress"], rb["macro_stress"])
+    for f in (dbf.FIELD_STRAIN, dbf.FIELD_STRESS, dbf.FIELD_U):
+        assert np.array_equal(a.get_field(f), b.get_field(f))
+    with pytest.raises(dbf.DBFFTError):
+        b.restore(blob[:-8])
