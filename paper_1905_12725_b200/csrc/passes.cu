@@ -722,6 +722,16 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
   }
 }
 
+// Real slots of pass_X: field c (line-major: c = l CS + f) at position x; the two fields of a pair
+// (c = 2q, 2q + 1) are interleaved, so a pair job's reals are one complex array (its FFT's own
+// input / output, 16-byte accesses) and a voxel reads a line's fields as CS/2 16-byte loads
+// (ILV = false: field-major slots c N1 + x, the layout the 6-field kinds keep — interleaving
+// raised their register pressure into spills, 256^3 small pass_X 0.759 -> 0.780 ms)
+template <int N1, bool ILV = true>
+DBF_DEV int x_slot(int c, int x) {
+  return ILV ? (((c >> 1) * N1 + x) << 1) + (c & 1) : c * N1 + x;
+}
+
 // XOR swizzle inside 8-element groups: conflict-free radix-8 scatter/gather, no padding, so
 // the exchange buffer of a field pair is exactly the pair's two real slots (in place).
 struct IdxSwz {
@@ -841,6 +851,7 @@ struct XCfg {
   // pass_X 1.099 -> 0.990 ms); the 6-field small-strain kinds measured a little slower with it
   static constexpr bool TAB = (N1 & 1) == 0 && C == 9;
   static constexpr size_t ST_TW = TAB ? sizeof(cplx) * N1 : 0;
+  static constexpr bool ILV = C == 9;  // pair-interleaved real slots (x_slot)
   static constexpr size_t SMEM = SLOTS + ST_IN + ST_TAN + ST_PH + 16 + ST_TW;  // + 2 mbarriers
   static constexpr int MINB = PACK ? (THREADS <= 160 ? DBF_X_MINB_NOTAN : THREADS <= 320 ? 2 : 1)
                                : ((KIND == X_K_J2 && !DBF_X_STAGE_TAN_J2) || (KIND == X_K_FIN_NH && !DBF_X_STAGE_TAN_NH))
@@ -1019,8 +1030,12 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
 #pragma unroll
       for (int s = 0; s < PX; ++s) {
         const int m = gq + s * TPJ;
-        real[ca * N1 + m] = a[s].x;
-        real[cb * N1 + m] = a[s].y;
+        if (CF::ILV) {
+          cx[jbase + m] = a[s];  // the pair's reals interleaved (fa, fb) at position m
+        } else {
+          real[ca * N1 + m] = a[s].x;
+          real[cb * N1 + m] = a[s].y;
+        }
       }
     }
     __syncthreads();
@@ -1030,7 +1045,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
         const int l2 = vv / N1, x = vv % N1;
         const long long ln = grp * LPAR + l2;
         if (ln >= g.nlines) continue;
-        for (int f = 0; f < nf_real; ++f) g.real_out[(long long)f * g.nvox + ln * N1 + x] = real[(l2 * CS + f) * N1 + x];
+        for (int f = 0; f < nf_real; ++f) g.real_out[(long long)f * g.nvox + ln * N1 + x] = real[x_slot<N1, CF::ILV>(l2 * CS + f, x)];
       }
       __syncthreads();
       continue;
@@ -1040,7 +1055,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
         const int l2 = vv / N1, x = vv % N1;
         const long long ln = grp * LPAR + l2;
         for (int f = 0; f < CS; ++f)
-          real[(l2 * CS + f) * N1 + x] =
+          real[x_slot<N1, CF::ILV>(l2 * CS + f, x)] =
               (ln < g.nlines && f < nf_real) ? g.oscale * __ldg(g.real_in + (long long)g.real_map[f] * g.nvox + ln * N1 + x) : 0.0;
       }
     }
@@ -1051,9 +1066,19 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
       const int l2 = vv / N1, x = vv % N1;
       const long long ln = grp * LPAR + l2;
       if (ln >= g.nlines) continue;
-      double G[C], P[C];
+      double G[CS], P[CS];
+      if constexpr (CS % 2 == 0 && C == 9) {  // a line's pairs: one 16-byte load per field pair
+                                             // (the 6-field kinds spilled with it: scalar)
 #pragma unroll
-      for (int f = 0; f < C; ++f) G[f] = (f < T::CIN && do_in) ? real[(l2 * CS + f) * N1 + x] : 0.0;
+        for (int q = 0; q < CS / 2; ++q) {
+          const cplx v2 = cx[(l2 * (CS / 2) + q) * N1 + x];
+          G[2 * q] = (2 * q < T::CIN && do_in) ? v2.x : 0.0;
+          G[2 * q + 1] = (2 * q + 1 < T::CIN && do_in) ? v2.y : 0.0;
+        }
+      } else {
+#pragma unroll
+        for (int f = 0; f < CS; ++f) G[f] = (f < T::CIN && do_in) ? real[x_slot<N1, CF::ILV>(l2 * CS + f, x)] : 0.0;
+      }
       const long long v = ln * N1 + x;
       const double* tp;
       long long ts;
@@ -1068,8 +1093,14 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
         ph = (KIND == X_K_FIN_TAN || KIND == X_REAL_OUT) ? 0 : (int)__ldg(g.phase + v);
       }
       x_voxel<KIND>(g, v, G, P, red, tp, ts, ph, xdot, g.e ? s_e : nullptr);
+      if constexpr (CS % 2 == 0 && C == 9) {
 #pragma unroll
-      for (int f = 0; f < T::COUT; ++f) real[(l2 * CS + f) * N1 + x] = P[f];
+        for (int q = 0; q < CS / 2; ++q)
+          if (2 * q < T::COUT) cx[(l2 * (CS / 2) + q) * N1 + x] = make_double2(P[2 * q], 2 * q + 1 < T::COUT ? P[2 * q + 1] : 0.0);
+      } else {
+#pragma unroll
+        for (int f = 0; f < T::COUT; ++f) real[x_slot<N1, CF::ILV>(l2 * CS + f, x)] = P[f];
+      }
     }
     __syncthreads();
     if (SIN && STAGE_TAN && t == 0 && nxt < ngroups) {
@@ -1084,9 +1115,8 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
 #pragma unroll
       for (int s = 0; s < PX; ++s) {
         const int m = gq + s * TPJ;
-        const double ra = (fa < COUT) ? real[ca * N1 + m] : 0.0;
-        const double rb = (fb < COUT) ? real[cb * N1 + m] : 0.0;
-        a[s] = make_double2(ra, rb);
+        const cplx v2 = CF::ILV ? cx[jbase + m] : make_double2(real[ca * N1 + m], real[cb * N1 + m]);
+        a[s] = make_double2(fa < COUT ? v2.x : 0.0, fb < COUT ? v2.y : 0.0);
       }
       x_fft<N1, PX, false, CF::TAB>(a, cx, gq, jbase, twx, job);
       constexpr bool SHFL = (PX == 8 && TPJ <= 32);
