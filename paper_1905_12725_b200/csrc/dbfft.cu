@@ -117,6 +117,8 @@ struct Slab {
   cplx *WS1 = nullptr, *WS2 = nullptr, *WR2 = nullptr;
   uint16_t* phase = nullptr;
   double* ptable = nullptr;
+  size_t cap_ptable = 0, cap_counts = 0;  // capacities (doubles): set_phases reuses what fits
+  int state_nf = 0, state_nk = 0;          // state / tangent fields allocated (0: none)
   double *F = nullptr, *F_c = nullptr, *epsp_c = nullptr, *epsp_t = nullptr, *tan = nullptr;
   CgDev* cg = nullptr;
   double *part_x = nullptr, *part_cg = nullptr, *part_misc = nullptr;
@@ -2020,6 +2022,17 @@ dbfft_status dbfft_spectral_layout(dbfft_ctx ctx, int64_t shape[4], int64_t stri
   return DBFFT_OK;
 }
 
+// captured PCG loops bake buffer pointers in: rebuild them only if set_phases moved one
+static void bump_gen_if_moved(dbfft_ctx ctx, const std::vector<const void*>& before) {
+  size_t i = 0;
+  bool moved = false;
+  for (Slab& sl : ctx->slabs)
+    for (const void* q : {(const void*)sl.phase, (const void*)sl.ptable, (const void*)sl.counts, (const void*)sl.F,
+                          (const void*)sl.F_c, (const void*)sl.tan, (const void*)sl.epsp_c, (const void*)sl.epsp_t})
+      moved |= (i < before.size() ? before[i++] : nullptr) != q;
+  if (moved) ++ctx->gen;
+}
+
 dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t on_device, int32_t n_phases, const dbfft_material* table) {
   if (!ctx) return DBFFT_E_INVALID_ARG;
   DevGuard dev_guard(ctx->device);
@@ -2084,18 +2097,31 @@ dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t o
   dbfft_status s;
   const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   const long long plane = (long long)ctx->n1 * ctx->n2;
+  // buffers are reused when they fit (pointers stable: the captured PCG loop graphs stay valid,
+  // e.g. for a new load walk on the same grid); `gen` moves only if a pointer changed
+  std::vector<const void*> before;
+  for (Slab& sl : ctx->slabs)
+    for (const void* q : {(const void*)sl.phase, (const void*)sl.ptable, (const void*)sl.counts, (const void*)sl.F,
+                          (const void*)sl.F_c, (const void*)sl.tan, (const void*)sl.epsp_c, (const void*)sl.epsp_t})
+      before.push_back(q);
+  CK(cudaStreamSynchronize(ctx->stream));  // kernels still reading the old table / counts
   for (Slab& sl : ctx->slabs) {
     if (!sl.phase && (s = dalloc(ctx, &sl.phase, sl.Nloc)) != DBFFT_OK) return s;
     const long long off = ctx->loopback ? (long long)sl.z0 * plane : 0;
     CK(cudaMemcpyAsync(sl.phase, phase_id + off, sizeof(uint16_t) * sl.Nloc, kind, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));  // kernels still reading the old table / counts
-    dfree(ctx, sl.ptable);
-    sl.ptable = nullptr;
-    if ((s = dalloc(ctx, &sl.ptable, pt.size())) != DBFFT_OK) return s;
+    if (sl.cap_ptable < pt.size()) {
+      dfree(ctx, sl.ptable);
+      sl.ptable = nullptr;
+      if ((s = dalloc(ctx, &sl.ptable, pt.size())) != DBFFT_OK) return s;
+      sl.cap_ptable = pt.size();
+    }
     CK(cudaMemcpyAsync(sl.ptable, pt.data(), sizeof(double) * pt.size(), cudaMemcpyHostToDevice, ctx->stream));
-    dfree(ctx, sl.counts);
-    sl.counts = nullptr;
-    if ((s = dalloc(ctx, &sl.counts, n_phases)) != DBFFT_OK) return s;
+    if (sl.cap_counts < (size_t)n_phases) {
+      dfree(ctx, sl.counts);
+      sl.counts = nullptr;
+      if ((s = dalloc(ctx, &sl.counts, n_phases)) != DBFFT_OK) return s;
+      sl.cap_counts = n_phases;
+    }
     CK(cudaMemsetAsync(sl.counts, 0, sizeof(double) * n_phases, ctx->stream));
     CK(cudaMemsetAsync(sl.bad, 0, sizeof(int), ctx->stream));
     CK(launch_phase_hist(sl.phase, sl.Nloc, sl.counts, n_phases, sl.bad, ctx->stream));
@@ -2121,34 +2147,48 @@ dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t o
   ctx->h_ptable = pt;
   ctx->nph = n_phases;
   ctx->family = fam;
-  ++ctx->gen;  // buffers baked into captured PCG loops change below
-  for (Slab& sl : ctx->slabs) {
-    free_state(ctx, sl);
-    CK(cudaMemsetAsync(sl.u, 0, sizeof(cplx) * 3 * sl.Hs, ctx->stream));
-    CK(cudaMemsetAsync(sl.u_c, 0, sizeof(cplx) * 3 * sl.Hs, ctx->stream));
+  {
+    // per-voxel state of the new family: kept when the same fields are allocated already
+    const char* tm = getenv("DBFFT_TANGENT");
+    ctx->tmode = ((tm && strcmp(tm, "full") == 0) || has_svk) ? 0 : 1;
+    const int nf = fam == FAM_NEOHOOKE ? 9 : fam == FAM_J2 ? 6 : 0;
+    const int nk = fam == FAM_NEOHOOKE ? (ctx->tmode ? 10 : 45) : fam == FAM_J2 ? 8 : 0;
+    for (Slab& sl : ctx->slabs) {
+      if (sl.state_nf != nf || sl.state_nk != nk || (fam == FAM_J2) != (sl.epsp_c != nullptr)) {
+        free_state(ctx, sl);
+        sl.state_nf = sl.state_nk = 0;
+      }
+      CK(cudaMemsetAsync(sl.u, 0, sizeof(cplx) * 3 * sl.Hs, ctx->stream));
+      CK(cudaMemsetAsync(sl.u_c, 0, sizeof(cplx) * 3 * sl.Hs, ctx->stream));
+    }
   }
   for (int a = 0; a < 9; ++a) ctx->Fbar[a] = ctx->Fbar_c[a] = (fam == FAM_NEOHOOKE && a % 4 == 0) ? 1.0 : 0.0;
   ctx->h_counts = cnt;
   ctx->n_incr = 0;
   if (fam == FAM_LINEAR) {
+    bump_gen_if_moved(ctx, before);
     CKS(linear_reference(ctx, 0));
   } else {
-    const int nf = fam == FAM_NEOHOOKE ? 9 : 6;
-    const char* tm = getenv("DBFFT_TANGENT");
     // the matrix-free compact tangent is neo-Hookean's; SVK phases store the 45-entry tangent
-    ctx->tmode = ((tm && strcmp(tm, "full") == 0) || has_svk) ? 0 : 1;
+    const int nf = fam == FAM_NEOHOOKE ? 9 : 6;
     const int nk = fam == FAM_NEOHOOKE ? (ctx->tmode ? 10 : 45) : 8;
     for (Slab& sl : ctx->slabs) {
-      if ((s = dalloc(ctx, &sl.F, (size_t)nf * sl.Nloc)) != DBFFT_OK) return s;
-      if ((s = dalloc(ctx, &sl.F_c, (size_t)nf * sl.Nloc)) != DBFFT_OK) return s;
-      if ((s = dalloc(ctx, &sl.tan, (size_t)nk * sl.Nloc)) != DBFFT_OK) return s;
+      if (!sl.state_nf) {
+        if ((s = dalloc(ctx, &sl.F, (size_t)nf * sl.Nloc)) != DBFFT_OK) return s;
+        if ((s = dalloc(ctx, &sl.F_c, (size_t)nf * sl.Nloc)) != DBFFT_OK) return s;
+        if ((s = dalloc(ctx, &sl.tan, (size_t)nk * sl.Nloc)) != DBFFT_OK) return s;
+        if (fam == FAM_J2) {
+          if ((s = dalloc(ctx, &sl.epsp_c, (size_t)6 * sl.Nloc)) != DBFFT_OK) return s;
+          if ((s = dalloc(ctx, &sl.epsp_t, (size_t)6 * sl.Nloc)) != DBFFT_OK) return s;
+        }
+        sl.state_nf = nf;
+        sl.state_nk = nk;
+      }
       if (fam == FAM_NEOHOOKE) {
         k_identity9<<<1024, 256, 0, ctx->stream>>>(sl.F_c, sl.Nloc);
         CK(cudaGetLastError());
       } else {
         CK(cudaMemsetAsync(sl.F_c, 0, sizeof(double) * nf * sl.Nloc, ctx->stream));
-        if ((s = dalloc(ctx, &sl.epsp_c, (size_t)6 * sl.Nloc)) != DBFFT_OK) return s;
-        if ((s = dalloc(ctx, &sl.epsp_t, (size_t)6 * sl.Nloc)) != DBFFT_OK) return s;
         CK(cudaMemsetAsync(sl.epsp_c, 0, sizeof(double) * 6 * sl.Nloc, ctx->stream));
         CK(cudaMemsetAsync(sl.epsp_t, 0, sizeof(double) * 6 * sl.Nloc, ctx->stream));
       }
@@ -2156,6 +2196,7 @@ dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t o
     }
     // tangent at the undeformed state (so apply_K / precond are usable before a solve)
     double zero[9] = {0}, mp[9], mx;
+    bump_gen_if_moved(ctx, before);
     s = constitutive(ctx, false, zero, 1.0, mp, &mx);
     if (s != DBFFT_OK) return s;
     s = refresh_mean_tangent(ctx);

@@ -1,6 +1,6 @@
 """Time-to-solution of the BASELINE configs c1..c5 on one GPU (solve only; setup separate).
 
-usage: python tools/run_configs.py [c1 c2 c3 c4 c5] [--incs K]   -> one JSON line per config"""
+usage: python tools/run_configs.py [c1 c2 c3 c4 c5] [--incs K] [--noprof] [--warm]  -> one JSON line per config"""
 import json
 import os
 import sys
@@ -32,24 +32,36 @@ for name in names:
     loads = cfg["loads"][: incs or len(cfg["loads"])]
     if "--noprof" not in sys.argv:  # the per-kernel profiler disables the CUDA-graph PCG rounds
         ctx.profile(True)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(ctx.stream)
-    iters = newton = 0
-    reps = []
-    for L in loads:
-        rep = ctx.solve_increment(L["target"], L["mask"], dt=cfg["dt"], check_every=8)
-        iters += rep["cg_iters"]
-        newton += rep["newton_iters"]
-        reps.append(rep)
-    ev1.record(ctx.stream)
-    torch.cuda.synchronize()
-    t = ev0.elapsed_time(ev1) / 1e3
+
+    def walk():
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(ctx.stream)
+        iters = newton = 0
+        reps = []
+        for L in loads:
+            rep = ctx.solve_increment(L["target"], L["mask"], dt=cfg["dt"], check_every=8)
+            iters += rep["cg_iters"]
+            newton += rep["newton_iters"]
+            reps.append(rep)
+        ev1.record(ctx.stream)
+        torch.cuda.synchronize()
+        return ev0.elapsed_time(ev1) / 1e3, iters, newton, reps
+
+    # cold: the first walk builds the device-side PCG loop graphs; warm: the same walk again after
+    # set_phases (buffers and graphs reused), what a repeated / batched analysis pays
+    t, iters, newton, reps = walk()
+    t_warm = None
+    if "--warm" in sys.argv:
+        ctx.set_phases(cfg["phase"], cfg["materials"])
+        t_warm = walk()[0]
     prof = ctx.profile_read()
     last = reps[-1]
     ctx.profile(False)
     res = ctx.residuals(loads[-1]["target"], loads[-1]["mask"])  # P:270-290 monitors, final state
     print(json.dumps({"config": name, "grid": list(n), "increments": len(loads), "cg_iters": iters,
-                      "newton_iters": newton, "time_to_solution_s": t, "setup_s": t_setup, "gen_s": t_gen,
+                      "newton_iters": newton, "time_to_solution_s": t, "time_to_solution_warm_s": t_warm,
+                      "ms_per_cg_iter_warm": (1e3 * t_warm / max(iters, 1)) if t_warm else None,
+                      "setup_s": t_setup, "gen_s": t_gen,
                       "voxel_iter_per_s": N * iters / t,
                       "ms_per_cg_iter": 1e3 * t / max(iters, 1),
                       "macro_strain": np.round(last["macro_strain"], 10).tolist(),
