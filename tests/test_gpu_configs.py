@@ -175,3 +175,21 @@ def test_c4_operator_full_size(dbf):
     assert rel(got, g["f"]) <= 1e-12
     # the sample is representative: its norm against the full output norm
     assert np.linalg.norm(g["f"]) > 1e-3 * float(g["f_norm"])
+
+
+def test_c4_first_increment_full_size(dbf):
+    """c4 as configured at 256^3: the first load increment (F_zz = 1.01, P_xx = P_yy = 0 mixed
+    control, Newton-PCG with the neo-Hookean tangent) against the oracle's Newton: same Newton
+    count, macro F / P 1e-9, sampled F and P fields 1e-8."""
+    g = gold("c4inc")
+    cfg = configs.c4()
+    ctx = dbf.DBFFT(cfg["n"], kinematics="finite")
+    ctx.set_phases(cfg["phase"], cfg["materials"])
+    L = cfg["loads"][0]
+    rep = ctx.solve_increment(L["target"], L["mask"])
+    assert rep["converged"] and rep["newton_iters"] == int(g["newton"])
+    assert rel(rep["macro_stress"], g["mean_P"]) <= 1e-9
+    assert rel(rep["macro_strain"], g["mean_F"]) <= 1e-9
+    vs = g["voxels"]
+    assert rel(ctx.get_field(dbf.FIELD_STRAIN).reshape(9, -1)[:, vs], g["F"]) <= 1e-8
+    assert rel(ctx.get_field(dbf.FIELD_STRESS).reshape(9, -1)[:, vs], g["P"]) <= 1e-8
