@@ -2078,6 +2078,12 @@ dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t o
           return DBFFT_E_INVALID_ARG;
         }
         for (int a = 0; a < 5; ++a) d[a] = m.p[a];
+        {  // shear and bulk moduli for the kernels (passes.cu j2_moduli / j2_update)
+          const double E = m.p[0], nu = m.p[1];
+          const double lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+          d[5] = E / (2.0 * (1.0 + nu));
+          d[6] = lam + 2.0 * d[5] / 3.0;
+        }
         f = FAM_J2;
         break;
       default:

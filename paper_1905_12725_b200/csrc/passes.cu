@@ -441,14 +441,20 @@ DBF_DEV double ld_stream(const double* p) {
   return v;
 }
 
-// small-strain contraction: sigma_I = sum_J C[I][J] gamma_J, gamma = (e0,e1,e2,2e3,2e4,2e5)
+// small-strain contraction: sigma_I = sum_J C[I][J] gamma_J, gamma = (e0,e1,e2,2e3,2e4,2e5); the
+// stiffness is symmetric, so its 21 upper-triangle entries are loaded (not 36)
 DBF_DEV void voigt_contract_full(const double* __restrict__ C36, const double* e, double* s) {
   const double g[6] = {e[0], e[1], e[2], 2.0 * e[3], 2.0 * e[4], 2.0 * e[5]};
+  double c[6][6];
+#pragma unroll
+  for (int I = 0; I < 6; ++I)
+#pragma unroll
+    for (int J = I; J < 6; ++J) c[I][J] = c[J][I] = __ldg(C36 + 6 * I + J);
 #pragma unroll
   for (int I = 0; I < 6; ++I) {
     double acc = 0.0;
 #pragma unroll
-    for (int J = 0; J < 6; ++J) acc = fma(__ldg(C36 + 6 * I + J), g[J], acc);
+    for (int J = 0; J < 6; ++J) acc = fma(c[I][J], g[J], acc);
     s[I] = acc;
   }
 }
@@ -519,10 +525,8 @@ DBF_DEV void nh_apply(const double* Fi, double c1, double mu, double lam, const 
 //   C_alg = kappa 1x1 + 2 mu theta I_dev - 2 mu thetabar n x n.
 DBF_DEV void j2_update(const double* eps, const double* epsp, const double* prm, double dt,
                        double* sig, double* tc /*8: theta, thetabar, n[6]*/, double* epsp_new) {
-  const double E = prm[0], nu = prm[1], sy = prm[2], nexp = prm[3], edot0 = prm[4];
-  const double lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
-  const double mu = E / (2.0 * (1.0 + nu));
-  const double kappa = lam + 2.0 * mu / 3.0;
+  const double sy = prm[2], nexp = prm[3], edot0 = prm[4];
+  const double mu = prm[5], kappa = prm[6];  // per-phase moduli from set_phases (no divisions here)
   double ee[6];
 #pragma unroll
   for (int I = 0; I < 6; ++I) ee[I] = eps[I] - epsp[I];
@@ -584,14 +588,16 @@ DBF_DEV void j2_apply(const double* tc, double kappa, double mu, const double* e
   const double ne = tc[2] * e[0] + tc[3] * e[1] + tc[4] * e[2] + 2.0 * (tc[5] * e[3] + tc[6] * e[4] + tc[7] * e[5]);
   const double a = 2.0 * mu * tc[0], b = 2.0 * mu * tc[1] * ne;
 #pragma unroll
+  // (tr / 3 kept as a division: a hoisted tr * (1/3) made ptxas spill 184 bytes in the J2 pass_X)
   for (int I = 0; I < 6; ++I) s[I] = a * (e[I] - (I < 3 ? tr / 3.0 : 0.0)) - b * tc[2 + I] + (I < 3 ? kappa * tr : 0.0);
 }
 
+// shear and bulk moduli of a J2 phase: computed once per phase on the host (set_phases:
+// lam = E nu / ((1 + nu)(1 - 2 nu)), mu = E / (2 (1 + nu)), kappa = lam + 2 mu / 3), not three
+// fp64 divisions per voxel
 DBF_DEV void j2_moduli(const double* prm, double* kappa, double* mu) {
-  const double E = prm[0], nu = prm[1];
-  const double lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
-  *mu = E / (2.0 * (1.0 + nu));
-  *kappa = lam + 2.0 * (*mu) / 3.0;
+  *mu = __ldg(prm + 5);
+  *kappa = __ldg(prm + 6);
 }
 
 // Per-voxel material data of the apply kinds come either from global memory (tp = tan + v,
