@@ -187,6 +187,8 @@ def gpu_arm(args):
             mode = f"replicas x{world}"
     slab = mode.startswith("slab")
     ctx.set_phases(phase, cfg["materials"])
+    # every rank logs its communicator view (device, rank / world, transport, NCCL comm) on stderr
+    print(f"[dbfft rank {rank}/{world}] " + json.dumps(ctx.info()), file=sys.stderr, flush=True)
     loads = cfg["loads"]
     state = {"k": 0}
 

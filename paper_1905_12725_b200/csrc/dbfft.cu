@@ -1016,6 +1016,14 @@ dbfft_status pcg_iterate(dbfft_ctx ctx, const dbfft_opts& o, bool macro, int nb)
   const bool graphs = !ctx->prof && !(genv && genv[0] == '0');
   const int key = loop_key(ctx, macro);
   const int it0 = ctx->h_cg->iters;
+  // NCCL mode: a plain captured graph replayed per host-polled round is NCCL's supported graph
+  // usage; collectives inside a WHILE body (replayed a data-dependent number of times within one
+  // launch) are opt-in (DBFFT_NCCL_WHILE=1) until they have run on a multi-GPU node
+  const char* nw = getenv("DBFFT_NCCL_WHILE");
+  if (ctx->comm && !(nw && nw[0] == '1') && ctx->loop_fail == 0) {
+    ctx->loop_fail = 1;
+    ctx->loop_note = "NCCL mode: host-polled graph rounds (DBFFT_NCCL_WHILE=1 tries the WHILE graph)";
+  }
   if (graphs && ctx->loop_fail == 0) {
     dbfft_ctx_s::LoopGraph& lg = ctx->loop[key];
     dbfft_status st = DBFFT_OK;
@@ -1050,7 +1058,7 @@ dbfft_status pcg_iterate(dbfft_ctx ctx, const dbfft_opts& o, bool macro, int nb)
       if (st == DBFFT_OK) {
         CK(cudaGraphLaunch(lg.exec, ctx->stream));
         ctx->nlaunch += lg.body_launches;
-        if (ctx->loop_fail == 0) ctx->loop_note = "host-polled graph rounds";
+        if (ctx->loop_fail == 0 || ctx->loop_note.empty()) ctx->loop_note = "host-polled graph rounds";
         continue;
       }
       ctx->loop_fail = 2;
