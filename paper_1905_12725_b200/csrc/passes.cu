@@ -1024,13 +1024,6 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
         // Y_k = A_k + i B_k (k <= N/2);  conj(A_{N-k}) + i conj(B_{N-k}) otherwise
         a[s] = lo ? make_double2(A.x - B.y, A.y + B.x) : make_double2(A.x + B.y, B.x - A.y);
       }
-      if (SSP) {
-        __syncthreads();  // everyone has read the input stage
-        if (t == 0 && nxt < ngroups) {
-          fence_proxy_async();
-          x_issue_in<N1, KIND>(g, nxt, st_in, &bars[0]);
-        }
-      }
       x_fft<N1, PX, true, CF::TAB>(a, cx, gq, jbase, twx, job);
       x_jobsync<N1, PX>(job);  // the job's exchange reads are done before its slots become reals
 #pragma unroll
@@ -1045,6 +1038,12 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
       }
     }
     __syncthreads();
+    // everyone has read the input stage (before its C2R): refill it with the next group's
+    // spectra here, behind the barrier the voxel loop needs anyway (no barrier of its own)
+    if (SSP && do_in && t == 0 && nxt < ngroups) {
+      fence_proxy_async();
+      x_issue_in<N1, KIND>(g, nxt, st_in, &bars[0]);
+    }
 
     if (KIND == X_REAL_OUT) {
       for (int vv = t; vv < LPAR * N1; vv += CF::THREADS) {
