@@ -2070,6 +2070,7 @@ dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t o
         d[0] = m.p[0];
         d[1] = m.p[1];
         d[2] = 0.0;  // model flag: neo-Hookean
+        d[3] = m.p[1] - 2.0 * m.p[0] / 3.0;  // lam = kappa - 2 mu / 3 (R14), once per phase
         f = FAM_NEOHOOKE;
         break;
       case DBFFT_MAT_SVK:

@@ -652,7 +652,8 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
 #pragma unroll
     for (int k = 0; k < 9; ++k) Fi[k] = tp[k * ts];
     const double c1 = tp[9 * ts];
-    const double mu = __ldg(g.ptable + 36 * ph), lam = __ldg(g.ptable + 36 * ph + 1) - 2.0 * mu / 3.0;
+    // lam = kappa - 2 mu / 3 per phase from set_phases (ptable[3]): no fp64 division per voxel
+    const double mu = __ldg(g.ptable + 36 * ph), lam = __ldg(g.ptable + 36 * ph + 3);
 #pragma unroll
     for (int a = 0; a < 9; ++a) e9[a] = G[a] + (se ? se[a] : 0.0);
     nh_apply(Fi, c1 * g.oscale, mu * g.oscale, lam * g.oscale, e9, P);  // P x 1/(2N): exact for powers of 2
@@ -1218,7 +1219,7 @@ __global__ void __launch_bounds__(256) k_mean_tangent(XGeom g, double* partials)
       for (int k = 0; k < 9; ++k) Fi[k] = __ldg(g.tan + (long long)k * g.nvox + v);
       const double c1 = __ldg(g.tan + 9 * g.nvox + v);
       const int ph = __ldg(g.phase + v);
-      const double mu = __ldg(g.ptable + 36 * ph), lam = __ldg(g.ptable + 36 * ph + 1) - 2.0 * mu / 3.0;
+      const double mu = __ldg(g.ptable + 36 * ph), lam = __ldg(g.ptable + 36 * ph + 3);
       nh_tangent45(Fi, c1, mu, lam, K45);
 #pragma unroll
       for (int k = 0; k < 45; ++k) acc[k] += K45[k];
@@ -1273,7 +1274,7 @@ __global__ void __launch_bounds__(256) k_tangent81(XGeom g, long long v0, long l
 #pragma unroll
         for (int k = 0; k < 9; ++k) Fi[k] = g.tan[(long long)k * g.nvox + v];
         const int ph = g.phase[v];
-        const double mu = g.ptable[36 * ph], lam = g.ptable[36 * ph + 1] - 2.0 * mu / 3.0;
+        const double mu = g.ptable[36 * ph], lam = g.ptable[36 * ph + 3];
         nh_tangent45(Fi, g.tan[9 * g.nvox + v], mu, lam, K45);
       }
 #pragma unroll
