@@ -78,6 +78,9 @@ int num_sms() {
 #ifndef DBF_X_PREFETCH
 #define DBF_X_PREFETCH 1  // pass_X: bulk L2 prefetch of the next line group's per-voxel tangent rows
 #endif
+#ifndef DBF_X_TPIPE
+#define DBF_X_TPIPE 0  // 1: software-pipelined tangent loads across voxels (spilled: 256^3 0.911 -> 1.015 ms)
+#endif
 #ifndef DBF_X_PACK
 #define DBF_X_PACK 0  // 1: finite-strain apply kinds pair the 9 fields of two lines into 9 FFT jobs (B200 256^3: 0.990 -> 1.058 ms, slower)
 #endif
@@ -607,7 +610,7 @@ DBF_DEV void j2_moduli(const double* prm, double* kappa, double* mu) {
 // the 1/(2N)-scaled P)
 template <int KIND>
 DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* red, const double* tp, long long ts, int ph,
-                     double& xd, const double* se) {
+                     double& xd, const double* se, const double* tpre = nullptr) {
   if (KIND == X_K_SMALL_PHASE || KIND == X_RHS_SMALL_PHASE || KIND == X_K_J2) {
     double e6[6];
 #pragma unroll
@@ -650,8 +653,8 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
   } else if (KIND == X_K_FIN_NH) {
     double Fi[9], e9[9];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) Fi[k] = tp[k * ts];
-    const double c1 = tp[9 * ts];
+    for (int k = 0; k < 9; ++k) Fi[k] = tpre ? tpre[k] : tp[k * ts];
+    const double c1 = tpre ? tpre[9] : tp[9 * ts];
     // lam = kappa - 2 mu / 3 per phase from set_phases (ptable[3]): no fp64 division per voxel
     const double mu = __ldg(g.ptable + 36 * ph), lam = __ldg(g.ptable + 36 * ph + 3);
 #pragma unroll
@@ -860,7 +863,10 @@ struct XCfg {
   static constexpr size_t ST_TW = TAB ? sizeof(cplx) * N1 : 0;
   static constexpr bool ILV = C == 9;  // pair-interleaved real slots (x_slot)
   static constexpr size_t SMEM = SLOTS + ST_IN + ST_TAN + ST_PH + 16 + ST_TW;  // + 2 mbarriers
+  // (CTAs of more than 256 threads — the 9-field kinds at n1 = 512 — take 2 per SM: at 4 their
+  // 320 threads were capped at 48 registers and spilled 424 bytes)
   static constexpr int MINB = PACK ? (THREADS <= 160 ? DBF_X_MINB_NOTAN : THREADS <= 320 ? 2 : 1)
+                               : (THREADS > 256) ? 2
                                : ((KIND == X_K_J2 && !DBF_X_STAGE_TAN_J2) || (KIND == X_K_FIN_NH && !DBF_X_STAGE_TAN_NH))
                                    ? DBF_X_MINB_NOTAN
                                : (KIND == X_CONST_FIN || KIND == X_CONST_J2) ? DBF_X_MINB_CONST
@@ -1068,10 +1074,29 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
 
     // ------------------------------------------------------------ per-voxel operation
     if (SIN && STAGE_TAN) mbar_wait(&bars[1], it & 1);
+    // neo-Hookean apply: the next voxel's tangent row is loaded while this voxel computes
+    constexpr bool TPIPE = DBF_X_TPIPE && KIND == X_K_FIN_NH && S::NTAN == 0;
+    double tnext[TPIPE ? 10 : 1];
+    if (TPIPE && t < LPAR * N1) {
+      const long long v0 = (grp * LPAR) * N1 + t;
+      if (v0 < g.nvox)
+#pragma unroll
+        for (int k = 0; k < 10; ++k) tnext[TPIPE ? k : 0] = __ldg(g.tan + (long long)k * g.nvox + v0);
+    }
     for (int vv = t; KIND != X_REAL_IN && vv < LPAR * N1; vv += CF::THREADS) {
       const int l2 = vv / N1, x = vv % N1;
       const long long ln = grp * LPAR + l2;
       if (ln >= g.nlines) continue;
+      double tcur[TPIPE ? 10 : 1];
+      if (TPIPE) {
+#pragma unroll
+        for (int k = 0; k < 10; ++k) tcur[TPIPE ? k : 0] = tnext[TPIPE ? k : 0];
+        const int vn = vv + CF::THREADS;
+        const long long v1 = (grp * LPAR) * N1 + vn;
+        if (vn < LPAR * N1 && v1 < g.nvox)
+#pragma unroll
+          for (int k = 0; k < 10; ++k) tnext[TPIPE ? k : 0] = __ldg(g.tan + (long long)k * g.nvox + v1);
+      }
       double G[CS], P[CS];
       if constexpr (CS % 2 == 0 && C == 9) {  // a line's pairs: one 16-byte load per field pair
                                              // (the 6-field kinds spilled with it: scalar)
@@ -1098,7 +1123,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
         ts = g.nvox;
         ph = (KIND == X_K_FIN_TAN || KIND == X_REAL_OUT) ? 0 : (int)__ldg(g.phase + v);
       }
-      x_voxel<KIND>(g, v, G, P, red, tp, ts, ph, xdot, g.e ? s_e : nullptr);
+      x_voxel<KIND>(g, v, G, P, red, tp, ts, ph, xdot, g.e ? s_e : nullptr, TPIPE ? tcur : nullptr);
       if constexpr (CS % 2 == 0 && C == 9) {
 #pragma unroll
         for (int q = 0; q < CS / 2; ++q)
