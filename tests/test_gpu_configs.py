@@ -193,3 +193,79 @@ def test_c4_first_increment_full_size(dbf):
     vs = g["voxels"]
     assert rel(ctx.get_field(dbf.FIELD_STRAIN).reshape(9, -1)[:, vs], g["F"]) <= 1e-8
     assert rel(ctx.get_field(dbf.FIELD_STRESS).reshape(9, -1)[:, vs], g["P"]) <= 1e-8
+
+
+# ------------------------------------------------------------------ c5 at 512^3 (single operations)
+
+def _half_xi(n):
+    fx = O.axis_frequencies(n[0], 1.0)[: n[0] // 2 + 1]
+    fy = O.axis_frequencies(n[1], 1.0)
+    fz = O.axis_frequencies(n[2], 1.0)
+    X, Z, Y = np.broadcast_arrays(fx[None, None, :], fz[None, :, None], fy[:, None, None])
+    return np.stack([X, Y, Z])  # [a][ky][kz][kx]
+
+
+@pytest.fixture(scope="module")
+def c5_ctx(dbf):
+    """c5 as configured (512^3, 2000 grains, lognormal yield stresses) — built once."""
+    cfg = configs.c5()
+    ctx = dbf.DBFFT(cfg["n"], kinematics="small")
+    ctx.set_phases(cfg["phase"], cfg["materials"])
+    return cfg, ctx
+
+
+def test_c5_operator_full_size_elastic_closed_form(dbf, c5_ctx):
+    """c5 at 512^3 in its undeformed state: every grain has the same E, nu (only the yield stress
+    differs), so the J2 tangent is the homogeneous elastic stiffness and the operator is diagonal in
+    Fourier space, f(xi) = (xi . C . xi) u(xi) (P3) — checked at all 67M half-spectrum points."""
+    cfg, ctx = c5_ctx
+    n = cfg["n"]
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn((3, n[2], n[1], n[0]), dtype=torch.float64, device="cuda", generator=g)
+    u = (torch.fft.rfftn(x, dim=(1, 2, 3)) / x[0].numel()).permute(0, 2, 1, 3).contiguous()
+    del x
+    f = ctx.apply_K(u).cpu().numpy()
+    un = u.cpu().numpy()
+    del u
+    XI = _half_xi(n)
+    C = O.isotropic_stiffness(cfg["materials"][0]["E"], cfg["materials"][0]["nu"])
+    ref = np.einsum("ik...,k...->i...", np.einsum("ijkl,j...,l...->ik...", C, XI, XI), un)
+    assert rel(f, ref) <= 1e-12
+
+
+def test_c5_operator_full_size_plastic_hermitian(dbf, c5_ctx):
+    """c5 at 512^3 at a heterogeneous plastic state (eval_state at eps = 2e-3 uniaxial + noise:
+    plastic and elastic voxels, per-grain yield stresses): the operator is symmetric,
+    <Kv, w> = <v, Kw> to 1e-12, positive, and exactly zero on the null set Z — properties that hold
+    at any size (the oracle cannot hold the 512^3 3x3x3x3 tangent field)."""
+    cfg, ctx = c5_ctx
+    n = cfg["n"]
+    g = torch.Generator(device="cuda").manual_seed(6)
+    eps = 5e-4 * torch.randn((3, 3, n[2], n[1], n[0]), dtype=torch.float64, device="cuda", generator=g)
+    eps = 0.5 * (eps + eps.transpose(0, 1))
+    for i, d in enumerate((-1e-3, -1e-3, 2e-3)):
+        eps[i, i] += d
+    ctx.eval_state(eps.reshape(9, n[2], n[1], n[0]).contiguous(), dt=1.0)
+    del eps
+
+    def rnd():
+        x = torch.randn((3, n[2], n[1], n[0]), dtype=torch.float64, device="cuda", generator=g)
+        return (torch.fft.rfftn(x, dim=(1, 2, 3)) / x[0].numel()).permute(0, 2, 1, 3).contiguous()
+
+    def dot(a, b):
+        wgt = torch.full((n[0] // 2 + 1,), 2.0, dtype=torch.float64, device="cuda")
+        wgt[0] = 1.0
+        wgt[-1] = 1.0
+        return float(((a.conj() * b).real * wgt).sum())
+
+    v = rnd()
+    Kv = ctx.apply_K(v)
+    w = rnd()
+    Kw = ctx.apply_K(w)
+    a, b = dot(Kv, w), dot(v, Kw)
+    assert abs(a - b) <= 1e-12 * abs(a)
+    assert dot(Kv, v) > 0
+    for ky in (0, n[1] // 2):
+        for kz in (0, n[2] // 2):
+            for kx in (0, n[0] // 2):
+                assert float(Kv[:, ky, kz, kx].abs().max()) == 0.0
