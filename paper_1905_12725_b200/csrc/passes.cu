@@ -435,7 +435,10 @@ DBF_DEV int sym9(int i, int j) {
 }
 
 // Voigt index (xx,yy,zz,yz,xz,xy) -> row-major 3x3 entry
-__device__ __constant__ int c_row9_of_voigt[6] = {0, 4, 8, 5, 2, 1};
+// (a compile-time function: with the loops unrolled every index folds to a constant, so the
+// per-thread accumulators red[] stay in registers — a __constant__ table index put red[] in local
+// memory: 28 % of the J2 pass_X stall samples at 512^3)
+DBF_DEV constexpr int row9_of_voigt(int I) { return I == 0 ? 0 : I == 1 ? 4 : I == 2 ? 8 : I == 3 ? 5 : I == 4 ? 2 : 1; }
 
 // streaming load of per-voxel data (read once per launch: do not allocate in L1)
 DBF_DEV double ld_stream(const double* p) {
@@ -615,7 +618,7 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
     double e6[6];
 #pragma unroll
     for (int I = 0; I < 6; ++I)
-      e6[I] = (KIND == X_RHS_SMALL_PHASE ? 0.0 : G[I]) + (se ? se[c_row9_of_voigt[I]] : 0.0);
+      e6[I] = (KIND == X_RHS_SMALL_PHASE ? 0.0 : G[I]) + (se ? se[row9_of_voigt(I)] : 0.0);
     double s[6];
     if (KIND == X_K_J2) {
       double tc[8];
@@ -633,7 +636,8 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
 #pragma unroll
     for (int I = 0; I < 6; ++I) {
       P[I] = sg * s[I];
-      red[c_row9_of_voigt[I]] += s[I];
+      // the apply kinds read <sigma> off the R2C's k = 0 outputs instead (XDcRed)
+      if (KIND == X_RHS_SMALL_PHASE) red[row9_of_voigt(I)] += s[I];
     }
   } else if (KIND == X_K_FIN_TAN) {
     double e9[9], K[45];
@@ -712,7 +716,7 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
     double mx = 0.0;
 #pragma unroll
     for (int I = 0; I < 6; ++I) {
-      const double d = (g.has_in ? G[I] : 0.0) + se[c_row9_of_voigt[I]];
+      const double d = (g.has_in ? G[I] : 0.0) + se[row9_of_voigt(I)];
       mx = fmax(mx, fabs(d));
       eps[I] = g.F[(long long)I * g.nvox + v] + d;
       g.F[(long long)I * g.nvox + v] = eps[I];
@@ -726,7 +730,7 @@ DBF_DEV void x_voxel(const XGeom& g, long long v, double* G, double* P, double* 
     for (int I = 0; I < 6; ++I) {
       g.epsp_t[(long long)I * g.nvox + v] = epn[I];
       P[I] = -g.oscale * s[I];
-      red[c_row9_of_voigt[I]] += s[I];
+      red[row9_of_voigt(I)] += s[I];
     }
     red[9] = fmax(red[9], mx);
   }
