@@ -860,13 +860,18 @@ struct XCfg {
   static constexpr bool STG_SPEC = STG && DBF_X_STAGE_SPEC;
   static constexpr size_t ST_IN = STG_SPEC ? sizeof(cplx) * LPAR * T::CIN * N1H : 0;
   static constexpr size_t ST_TAN = STG ? sizeof(double) * LPAR * S::NTAN * N1 : 0;
-  static constexpr size_t ST_PH = (STG && S::PH) ? ((sizeof(uint16_t) * LPAR * N1 + 15) & ~size_t(15)) : 0;
+  // PH2: only phase ids staged (no tangent rows): two buffers, group g+1's copy issued when group g
+  // starts (a whole group of lead time instead of the R2C + C2R)
+  // (6-field kinds only: the 9-field neo-Hookean pass measured 0.5 % slower with it)
+  static constexpr bool PH2 = STG && S::PH && S::NTAN == 0 && C != 9;
+  static constexpr size_t ST_PH1 = (STG && S::PH) ? ((sizeof(uint16_t) * LPAR * N1 + 15) & ~size_t(15)) : 0;
+  static constexpr size_t ST_PH = PH2 ? 2 * ST_PH1 : ST_PH1;
   // stage-ordered twiddles (N1 - 1) in shared memory for the 9-field kinds (B200 256^3 finite
   // pass_X 1.099 -> 0.990 ms); the 6-field small-strain kinds measured a little slower with it
   static constexpr bool TAB = (N1 & 1) == 0 && C == 9;
   static constexpr size_t ST_TW = TAB ? sizeof(cplx) * N1 : 0;
   static constexpr bool ILV = C == 9;  // pair-interleaved real slots (x_slot)
-  static constexpr size_t SMEM = SLOTS + ST_IN + ST_TAN + ST_PH + 16 + ST_TW;  // + 2 mbarriers
+  static constexpr size_t SMEM = SLOTS + ST_IN + ST_TAN + ST_PH + 32 + ST_TW;  // + 3 mbarriers (+ pad)
   // (CTAs of more than 256 threads — the 9-field kinds at n1 = 512 — take 2 per SM: at 4 their
   // 320 threads were capped at 48 registers and spilled 424 bytes)
   static constexpr int MINB = PACK ? (THREADS <= 160 ? DBF_X_MINB_NOTAN : THREADS <= 320 ? 2 : 1)
@@ -962,7 +967,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
   double* st_tan = reinterpret_cast<double*>(sb + CF::SLOTS + CF::ST_IN);
   uint16_t* st_ph = reinterpret_cast<uint16_t*>(sb + CF::SLOTS + CF::ST_IN + CF::ST_TAN);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sb + CF::SLOTS + CF::ST_IN + CF::ST_TAN + CF::ST_PH);
-  cplx* stab = reinterpret_cast<cplx*>(bars + 2);
+  cplx* stab = reinterpret_cast<cplx*>(bars + 4);
   // odd lengths keep the plain W_N table (mixed-radix fft_odd); CF::TAB kinds the stage table
   const cplx* twx = CF::TAB ? stab : g.tw;
   if constexpr (CF::TAB) {
@@ -997,6 +1002,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
     if (t == 0) {
       mbar_init(&bars[0], 1);
       mbar_init(&bars[1], 1);
+      mbar_init(&bars[2], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -1008,6 +1014,14 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
   uint32_t it = 0;
 
   for (long long grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
+    // PH2: this group's phase ids are in buffer it & 1 (barrier 1 + (it & 1)); the next group's go
+    // to the other buffer now — its last reader, group it - 1, finished its voxel loop
+    uint16_t* ph_cur = CF::PH2 ? st_ph + (it & 1) * (CF::ST_PH1 / sizeof(uint16_t)) : st_ph;
+    if (CF::PH2 && t == 0 && grp + gridDim.x < ngroups) {
+      fence_proxy_async();  // the buffer's generic-proxy reads (group it - 1) before the async write
+      x_issue_tan<N1, KIND>(g, grp + gridDim.x, st_tan, st_ph + ((it + 1) & 1) * (CF::ST_PH1 / sizeof(uint16_t)),
+                            &bars[1 + ((it + 1) & 1)]);
+    }
     const long long linea = grp * LPAR + la, lineb = grp * LPAR + lb;
     // per-voxel data read in the voxel loop straight from global memory: the next group's rows
     // go to L2 now (bulk prefetch), so the voxel loop's loads hit L2 instead of HBM
@@ -1077,7 +1091,10 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
     }
 
     // ------------------------------------------------------------ per-voxel operation
-    if (SIN && STAGE_TAN) mbar_wait(&bars[1], it & 1);
+    if (SIN && STAGE_TAN) {
+      if (CF::PH2) mbar_wait(&bars[1 + (it & 1)], (it >> 1) & 1);
+      else mbar_wait(&bars[1], it & 1);
+    }
     // neo-Hookean apply: the next voxel's tangent row is loaded while this voxel computes
     constexpr bool TPIPE = DBF_X_TPIPE && KIND == X_K_FIN_NH && S::NTAN == 0;
     double tnext[TPIPE ? 10 : 1];
@@ -1121,7 +1138,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
       if (SIN && STAGE_TAN) {
         tp = (S::NTAN > 0) ? st_tan + vv : (g.tan ? g.tan + v : nullptr);
         ts = (S::NTAN > 0) ? (long long)LPAR * N1 : g.nvox;
-        ph = S::PH ? (int)st_ph[vv] : 0;
+        ph = S::PH ? (int)ph_cur[vv] : 0;
       } else {
         tp = g.tan ? g.tan + v : nullptr;
         ts = g.nvox;
@@ -1138,7 +1155,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
       }
     }
     __syncthreads();
-    if (SIN && STAGE_TAN && t == 0 && nxt < ngroups) {
+    if (SIN && STAGE_TAN && !CF::PH2 && t == 0 && nxt < ngroups) {
       fence_proxy_async();
       x_issue_tan<N1, KIND>(g, nxt, st_tan, st_ph, &bars[1]);
     }
