@@ -49,8 +49,14 @@ int num_sms() {
 #ifndef DBF_X_MINB
 #define DBF_X_MINB 3
 #endif
-#ifndef DBF_X_P
-#define DBF_X_P 8      // pass_X FFT points per thread: 8 (radix-8, CTA exchange) or 16 (radix-16, warp-local)
+#ifndef DBF_X_P16_256
+#define DBF_X_P16_256 0x11  // pass_X kinds (bit = XKind) that run radix-16 FFTs (16 points per thread) at N1 <= 256
+#endif
+#ifndef DBF_X_MINB_J2P16
+#define DBF_X_MINB_J2P16 3  // CTAs per SM of the radix-16 J2 apply kind
+#endif
+#ifndef DBF_X_P16_512
+#define DBF_X_P16_512 0x11  // ... at N1 = 512
 #endif
 #ifndef DBF_X_LRAW
 #define DBF_X_LRAW 192  // target threads per pass_X CTA (lines per CTA = DBF_X_LRAW / threads per line)
@@ -843,7 +849,11 @@ struct XCfg {
   // of 512 voxels over 288 threads idles less than 256 voxels over 160)
   static constexpr bool PACK = DBF_X_PACK && (C & 1) && (N1 & 1) == 0 && (KIND == X_K_FIN_NH || KIND == X_K_FIN_TAN);
   static constexpr int CS = PACK ? C : (C + 1) & ~1;  // real slots per line
-  static constexpr int PX = (N1 & 1) ? PtsPerThread<N1>::value : (N1 >= 16) ? DBF_X_P : 8;   // FFT points per thread
+  // FFT points per thread: radix-16 stages with warp-local exchanges (16) for the kinds in the
+  // P16 masks (bit = kind; N1 <= 256 and N1 = 512 separately), else radix-8 (8)
+  static constexpr unsigned P16M = (N1 <= 256) ? DBF_X_P16_256 : DBF_X_P16_512;
+  static constexpr bool P16 = (N1 & 1) == 0 && N1 >= 32 && KIND < 32 && ((P16M >> KIND) & 1u);
+  static constexpr int PX = (N1 & 1) ? PtsPerThread<N1>::value : P16 ? 16 : 8;
   static constexpr int TPJ = N1 / PX;              // threads per pair FFT (divides 32: warp-local)
   static constexpr int NP = CS / 2;
   static constexpr int PERLINE = TPJ * NP;
@@ -868,7 +878,7 @@ struct XCfg {
   static constexpr size_t ST_PH = PH2 ? 2 * ST_PH1 : ST_PH1;
   // stage-ordered twiddles (N1 - 1) in shared memory for the 9-field kinds (B200 256^3 finite
   // pass_X 1.099 -> 0.990 ms); the 6-field small-strain kinds measured a little slower with it
-  static constexpr bool TAB = (N1 & 1) == 0 && C == 9;
+  static constexpr bool TAB = (N1 & 1) == 0 && C == 9 && PX == 8;  // (the table is the radix-8 plan's)
   static constexpr size_t ST_TW = TAB ? sizeof(cplx) * N1 : 0;
   static constexpr bool ILV = C == 9;  // pair-interleaved real slots (x_slot)
   static constexpr size_t SMEM = SLOTS + ST_IN + ST_TAN + ST_PH + 32 + ST_TW;  // + 3 mbarriers (+ pad)
@@ -876,6 +886,7 @@ struct XCfg {
   // 320 threads were capped at 48 registers and spilled 424 bytes)
   static constexpr int MINB = PACK ? (THREADS <= 160 ? DBF_X_MINB_NOTAN : THREADS <= 320 ? 2 : 1)
                                : (THREADS > 256) ? 2
+                               : (KIND == X_K_J2 && P16) ? DBF_X_MINB_J2P16
                                : ((KIND == X_K_J2 && !DBF_X_STAGE_TAN_J2) || (KIND == X_K_FIN_NH && !DBF_X_STAGE_TAN_NH))
                                    ? DBF_X_MINB_NOTAN
                                : (KIND == X_CONST_FIN || KIND == X_CONST_J2) ? DBF_X_MINB_CONST
