@@ -174,13 +174,17 @@ def gpu_arm(args):
     phase = cfg["phase"]
     if world > 1 and not args.replicas:
         # no fallback: a slab context that cannot be built (NCCL, peer windows) fails the run
+        py = max(1, args.pencil_rows)
         ctx = dbfft.DBFFT(n, kinematics="finite", device=local, stream=stream, world=world, rank=rank,
-                          transport=args.transport)
-        nzl = n[2] // world
-        phase = np.ascontiguousarray(cfg["phase"][rank * nzl:(rank + 1) * nzl])
-        mode = (f"slab x{world} (z-slabs / ky-slabs, " +
-                ("passes store into peer memory (VMM windows) + NCCL all-reduce)" if args.transport == "peer"
-                 else "NCCL all-to-all + all-reduce)"))
+                          transport=args.transport, pencil_rows=py)
+        phase = rank_block(cfg["phase"], rank, world, py)
+        pz = world // py
+        if py > 1:
+            mode = f"slab-pencils {py}x{pz} (2-D pencils, NCCL all-to-all in row / column groups + all-reduce)"
+        else:
+            mode = (f"slab x{world} (z-slabs / ky-slabs, " +
+                    ("passes store into peer memory (VMM windows) + NCCL all-reduce)" if args.transport == "peer"
+                     else "NCCL all-to-all + all-reduce)"))
     else:
         ctx = dbfft.DBFFT(n, kinematics="finite", device=local, stream=stream)
         if world > 1:
@@ -479,6 +483,16 @@ def reference_arm(args):
                       "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
 
 
+def rank_block(field, rank, world, py=1):
+    """This rank's real-space block [z][y][x] of a global field (include/dbfft.h: rank = b Py + a
+    owns z in [b n3/Pz, ...) x y in [a n2/Py, ...), all x; Py = 1: z-slabs)."""
+    pz = world // py
+    n3, n2 = field.shape[-3], field.shape[-2]
+    nzl, nyr = n3 // pz, n2 // py
+    a, b = rank % py, rank // py
+    return np.ascontiguousarray(field[..., b * nzl:(b + 1) * nzl, a * nyr:(a + 1) * nyr, :])
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -492,6 +506,8 @@ def main():
     ap.add_argument("--cpu-n", type=int, default=256, help="grid of the oracle baseline (c4 at 256^3)")
     ap.add_argument("--profile-steps", type=int, default=2, help="steps of the separate per-kernel profiled pass")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of slabs")
+    ap.add_argument("--pencil-rows", type=int, default=1,
+                    help="N > 1: 2-D pencil decomposition on a Py x (N / Py) grid (default 1: z-slabs)")
     ap.add_argument("--transport", choices=("nccl", "peer"), default="nccl",
                     help="N > 1 slabs: NCCL all-to-all exchanges, or passes storing into peer memory")
     args = ap.parse_args()

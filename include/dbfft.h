@@ -91,6 +91,16 @@ typedef struct {
   void* (*dev_alloc)(size_t bytes, void* alloc_user);
   void (*dev_free)(void* ptr, void* alloc_user);
   void* alloc_user;
+  /* Decomposition: 0 or 1 = z-slabs (above).  Py > 1 (a power of two,
+   * Py <= n1/2, Py | n2): 2-D pencils on a Py x Pz grid, Pz = world / Py (Pz | n2, Pz | n3),
+   * rank = b Py + a.  Rank (a, b) owns real z in [b n3/Pz, ...) x y in [a n2/Py, ...) (all x;
+   * local real fields [c][n3/Pz][n2/Py][x]) and spectral ky in [b n2/Pz, ...) x kx in
+   * [a kxm, (a+1) kxm) with kxm = n1/(2 Py), plus the Nyquist kx = n1/2 on a = Py - 1 (local
+   * spectral vectors [3][n2/Pz][kz][kxm + 1]; column kxm is padding, kept 0, on a < Py - 1).
+   * Per operator application 4 exchanges instead of 2: within the column group (same a) around
+   * the z passes as for slabs, and within the row group (same b) after the y-inverse and after
+   * the x pass (the x-line layout gathers / scatters the kx blocks).  NCCL transport only. */
+  int32_t pencil_rows;
 } dbfft_env;
 enum { DBFFT_TRANSPORT_NCCL = 0, DBFFT_TRANSPORT_PEER = 1 };
 

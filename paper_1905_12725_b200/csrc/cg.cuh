@@ -29,8 +29,9 @@ struct PrecQ { double Q[36]; };
 struct SpecGeom {
   int n1h, n2, n3;
   long long Hs;         // points per component
-  Freq fq;              // xy already offset to the local ky slab
+  Freq fq;              // xy already offset to the local ky slab (xx to the local kx block)
   int n1;
+  int kx0;              // global kx of local column 0 (pencil decomposition; else 0)
 };
 
 cudaError_t launch_precond(const SpecGeom& g, const PrecQ* q, const cplx* r, cplx* z, cudaStream_t s);
@@ -71,7 +72,7 @@ DBF_DEV Pt point(const SpecGeom& g, long long i) {
   p.xx = __ldg(g.fq.xx + kx);
   p.xy = __ldg(g.fq.xy + ky);
   p.xz = __ldg(g.fq.xz + kz);
-  p.w = (kx == 0 || 2 * kx == g.n1) ? 1.0 : 2.0;
+  p.w = (kx + g.kx0 == 0 || 2 * (kx + g.kx0) == g.n1) ? 1.0 : 2.0;
   p.null = (p.xx == 0.0 && p.xy == 0.0 && p.xz == 0.0);
   return p;
 }

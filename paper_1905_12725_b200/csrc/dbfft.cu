@@ -103,7 +103,12 @@ bool is_pow2_in(int n) { return (n >= 8 && n <= 512 && (n & (n - 1)) == 0) || n 
 // one rank's share of the problem
 struct Slab {
   int rank = 0;
+  // spectral block: ky in [ky0, ky0 + nyl), all kz, local kx columns [0, nkx) = global kx0 + c;
+  // real block: z in [z0, z0 + nzl), y in [y0, y0 + nyr), all x.  Pencil grid position (pa, pb),
+  // rank = pb Py + pa (z-slabs: Py = 1, pa = 0, pb = rank, nyr = n2, kx0 = 0)
   int nyl = 0, nzl = 0, ky0 = 0, z0 = 0;
+  int pa = 0, pb = 0, nyr = 0, y0 = 0, kx0 = 0;
+  long long fsB = 0;      // field stride of the x-line layout B inside one kx chunk: nzl * nyr * kxp
   long long Hs = 0;       // complex points per field (= n1h * nyl * n3 = n1h * n2 * nzl)
   long long Hsp = 0;      // the same with the padded kx pitch of the intermediate layouts (kxp)
   long long Nloc = 0;     // voxels in the z-slab
@@ -111,6 +116,9 @@ struct Slab {
   const double* xiy = nullptr;  // xi_y of the local ky slab (offset into the global table)
   cplx *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *b = nullptr, *u = nullptr, *u_c = nullptr;
   cplx *WA = nullptr, *WR = nullptr, *WB = nullptr;  // send, receive (== WA when P == 1), y-pass buffers
+  // x-line layout B: the y-inverse and x passes store into WBX, the x and y-forward passes read WB.
+  // Pencils (Py > 1) exchange WBX -> WB within the row group after each; slabs: WBX == WB.
+  cplx* WBX = nullptr;
   // exchange targets: the I1-type passes store into WS1, their readers take WR; the F2-type into
   // WS2, read from WR2.  NCCL transport: WS1 = WS2 = WA, WR2 = WR.  Peer transport: WS1 / WS2 are
   // windows onto every rank's WR / WR2 (peer.cuh), WA stays local scratch.
@@ -136,6 +144,10 @@ struct dbfft_ctx_s {
   int kin;  // 6 or 9
   long long N;  // global voxels
   int P = 1, rank = 0, loopback = 0;
+  // decomposition: Py x Pz rank grid (SURVEY 8(f3) pencils; Py = 1: z-slabs / ky-slabs).  Local
+  // spectral kx columns nkx: n1/2 + 1 (Py = 1), else kxm + 1 (kxm = n1 / (2 Py) columns + the
+  // Nyquist on the last row rank, a zero padding column on the others)
+  int Py = 1, Pz = 1, nkx = 0, kxm = 0;
   int device;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -286,100 +298,114 @@ void prof_flush(dbfft_ctx ctx) {
 // ---------------------------------------------------------------- geometry builders
 SpecGeom spec(dbfft_ctx ctx, const Slab& s) {
   SpecGeom g;
-  g.n1h = ctx->n1h;
+  g.n1h = ctx->nkx;
   g.n2 = s.nyl;
   g.n3 = ctx->n3;
   g.Hs = s.Hs;
-  g.fq = Freq{ctx->xix, s.xiy, ctx->xiz};
+  g.fq = Freq{ctx->xix + s.kx0, s.xiy, ctx->xiz};
   g.n1 = ctx->n1;
+  g.kx0 = s.kx0;
   return g;
 }
 
-ColGeom colbase(dbfft_ctx ctx, const cplx* in, cplx* out) {
+ColGeom colbase(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out) {
   ColGeom g;
   memset(&g, 0, sizeof(g));
   g.in = in;
   g.out = out;
-  g.n1h = ctx->n1h;
+  g.n1h = ctx->nkx;  // local kx columns
   g.n1 = ctx->n1;
+  g.kx0 = s.kx0;
   return g;
 }
 
-// layouts (complex elements, per slab; P = 1 reduces every one of them to the plain layouts):
-//   S  spectral  [f][kyl][kz][kx]                     fs = Hs   (kx dense: the API layout)
-//   X1 I1 -> I2  [rank][f][kyl][zl][kx]  (sender: rank = destination, receiver: rank = source)
-//   B  y-pass    [f][zl][y][kx]                       fs = Hsp
-//   X2 F2 -> F3  [rank][f][kyl][zl][kx]
-// X1, B, X2 rows have the padded kx pitch kxp; chunk sizes nf * nyl * nzl * kxp.
-// chunk stride of the rank-chunked exchange layouts [rank][f][ky_loc][z_loc][kx]: dense, or the
-// granularity-padded chunk of the peer windows
+// layouts (complex elements, per rank; P = 1 reduces every one of them to the plain layouts):
+//   S  spectral  [f][kyl][kz][kxl]                      fs = Hs   (kx dense, nkx: the API layout)
+//   X1 I1 -> I2  [b'][f][kyl][zl][kxl]  (sender: b' = destination column rank, receiver: source)
+//   B  y <-> x   [a'][f][zl][yr][kxl]   (pencils: a' = destination / source row rank, chunk
+//                                        nf fsB; slabs: one chunk [f][zl][y][kx], fs = Hsp)
+//   X2 F2 -> F3  [b'][f][kyl][zl][kxl]
+// X1, B, X2 rows have the padded kx pitch kxp; X1 / X2 chunk sizes nf * nyl * nzl * kxp.
+// chunk stride of the rank-chunked exchange layouts X1 / X2: dense, or the granularity-padded
+// chunk of the peer windows
 long long xpcs(dbfft_ctx ctx, const Slab& s, int nf) {
   return ctx->peer ? ctx->xpcs : (long long)nf * s.nyl * s.nzl * ctx->kxp;
 }
+// chunk stride of the B layout for nf fields (pencils; unused with one chunk)
+long long bpcs(dbfft_ctx ctx, const Slab& s, int nf) { return ctx->Py > 1 ? (long long)nf * s.fsB : 0; }
 
 ColGeom geom_I1(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf) {
-  ColGeom g = colbase(ctx, in, out);
-  const long long n1h = ctx->n1h;
+  ColGeom g = colbase(ctx, s, in, out);
+  const long long nkx = ctx->nkx;
   const long long kxp = ctx->kxp;
-  g.in_fs = s.Hs; g.in_os = (long long)ctx->n3 * n1h; g.in_ps = n1h; g.in_psh = ilog2(ctx->n3); g.in_pcs = 0;
+  g.in_fs = s.Hs; g.in_os = (long long)ctx->n3 * nkx; g.in_ps = nkx; g.in_psh = ilog2(ctx->n3); g.in_pcs = 0;
   g.out_fs = (long long)s.nyl * s.nzl * kxp; g.out_os = (long long)s.nzl * kxp; g.out_ps = kxp;
   g.out_psh = ilog2(s.nzl); g.out_pcs = xpcs(ctx, s, nf);
-  g.ncols = (long long)s.nyl * n1h;
+  g.ncols = (long long)s.nyl * nkx;
   g.tw = ctx->tw3;
   g.fpos = ctx->xiz;
-  g.fq = Freq{ctx->xix, s.xiy, ctx->xiz};
+  g.fq = Freq{ctx->xix + s.kx0, s.xiy, ctx->xiz};
   g.n_xy = s.nyl;
   return g;
 }
-ColGeom geom_I2(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_in) {
-  ColGeom g = colbase(ctx, in, out);
-  const long long n1h = ctx->n1h;
+// nf_out: fields the pass writes (the B layout's chunk stride)
+ColGeom geom_I2(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_in, int nf_out) {
+  ColGeom g = colbase(ctx, s, in, out);
+  const long long nkx = ctx->nkx;
   const long long kxp = ctx->kxp;
   g.in_fs = (long long)s.nyl * s.nzl * kxp; g.in_os = kxp; g.in_ps = (long long)s.nzl * kxp;
   g.in_psh = ilog2(s.nyl); g.in_pcs = xpcs(ctx, s, nf_in);
-  g.out_fs = s.Hsp; g.out_os = (long long)ctx->n2 * kxp; g.out_ps = kxp; g.out_psh = ilog2(ctx->n2); g.out_pcs = 0;
-  g.ncols = (long long)s.nzl * n1h;
+  g.out_fs = s.fsB; g.out_os = (long long)s.nyr * kxp; g.out_ps = kxp; g.out_psh = ilog2(s.nyr); g.out_pcs = bpcs(ctx, s, nf_out);
+  g.ncols = (long long)s.nzl * nkx;
   g.tw = ctx->tw2;
   g.fpos = ctx->xiy;
-  g.fq = Freq{ctx->xix, ctx->xiy, ctx->xiz};
+  g.fq = Freq{ctx->xix + s.kx0, ctx->xiy, ctx->xiz};
   g.n_xy = ctx->n2;
   return g;
 }
-ColGeom geom_F2(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_out) {
-  ColGeom g = colbase(ctx, in, out);
-  const long long n1h = ctx->n1h;
+// nf_in: fields in the B layout (its chunk stride)
+ColGeom geom_F2(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_out, int nf_in) {
+  ColGeom g = colbase(ctx, s, in, out);
+  const long long nkx = ctx->nkx;
   const long long kxp = ctx->kxp;
-  g.in_fs = s.Hsp; g.in_os = (long long)ctx->n2 * kxp; g.in_ps = kxp; g.in_psh = ilog2(ctx->n2); g.in_pcs = 0;
+  g.in_fs = s.fsB; g.in_os = (long long)s.nyr * kxp; g.in_ps = kxp; g.in_psh = ilog2(s.nyr); g.in_pcs = bpcs(ctx, s, nf_in);
   g.out_fs = (long long)s.nyl * s.nzl * kxp; g.out_os = kxp; g.out_ps = (long long)s.nzl * kxp;
   g.out_psh = ilog2(s.nyl); g.out_pcs = xpcs(ctx, s, nf_out);
-  g.ncols = (long long)s.nzl * n1h;
+  g.ncols = (long long)s.nzl * nkx;
   g.tw = ctx->tw2;
   g.fpos = ctx->xiy;
-  g.fq = Freq{ctx->xix, ctx->xiy, ctx->xiz};
+  g.fq = Freq{ctx->xix + s.kx0, ctx->xiy, ctx->xiz};
   g.n_xy = ctx->n2;
   return g;
 }
 ColGeom geom_F3(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_in) {
-  ColGeom g = colbase(ctx, in, out);
-  const long long n1h = ctx->n1h;
+  ColGeom g = colbase(ctx, s, in, out);
+  const long long nkx = ctx->nkx;
   const long long kxp = ctx->kxp;
   g.in_fs = (long long)s.nyl * s.nzl * kxp; g.in_os = (long long)s.nzl * kxp; g.in_ps = kxp;
   g.in_psh = ilog2(s.nzl); g.in_pcs = xpcs(ctx, s, nf_in);
-  g.out_fs = s.Hs; g.out_os = (long long)ctx->n3 * n1h; g.out_ps = n1h; g.out_psh = ilog2(ctx->n3); g.out_pcs = 0;
-  g.ncols = (long long)s.nyl * n1h;
+  g.out_fs = s.Hs; g.out_os = (long long)ctx->n3 * nkx; g.out_ps = nkx; g.out_psh = ilog2(ctx->n3); g.out_pcs = 0;
+  g.ncols = (long long)s.nyl * nkx;
   g.tw = ctx->tw3;
   g.fpos = ctx->xiz;
-  g.fq = Freq{ctx->xix, s.xiy, ctx->xiz};
+  g.fq = Freq{ctx->xix + s.kx0, s.xiy, ctx->xiz};
   g.n_xy = s.nyl;
   return g;
 }
 
-XGeom xgeom(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out) {
+// nf_in / nf_out: fields of the B-layout input / output (pencils: their kx-chunk strides)
+XGeom xgeom(dbfft_ctx ctx, const Slab& s, const cplx* in, cplx* out, int nf_in = 9, int nf_out = 9) {
   XGeom g;
   memset(&g, 0, sizeof(g));
   g.in = in;
   g.out = out;
-  g.fs_in = g.fs_out = s.Hsp;
+  g.fs_in = g.fs_out = s.fsB;
+  if (ctx->Py > 1) {
+    g.kch = ctx->kxm;
+    g.npy = ctx->Py;
+    g.kpcs_in = bpcs(ctx, s, nf_in);
+    g.kpcs_out = bpcs(ctx, s, nf_out);
+  }
   g.n1h = ctx->n1h;
   g.kxp = ctx->kxp;
   g.n1 = ctx->n1;
@@ -439,10 +465,16 @@ dbfft_status run_x(dbfft_ctx ctx, int kind, int prof_id, const XGeom& g, int* gr
   return DBFFT_OK;
 }
 
+long long global_voxel(dbfft_ctx ctx, const Slab& s, long long v);
+
 // ---------------------------------------------------------------- collectives
-// all-to-all of equal chunks: slab r sends WA[d*chunk] to rank d, which stores it at WR[r*chunk]
+// rank of pencil-grid position (a, b) (z-slabs: a = 0, rank = b)
+int grank(dbfft_ctx ctx, int a, int b) { return b * ctx->Py + a; }
+
+// all-to-all of equal chunks within the column group (ranks with the same a): (a, b) sends
+// WA[d*chunk] to (a, d), which stores it at WR[b*chunk] (z-slabs: all ranks, b = rank)
 dbfft_status exchange(dbfft_ctx ctx, long long chunk) {
-  if (ctx->P == 1) return DBFFT_OK;
+  if (ctx->Pz == 1) return DBFFT_OK;
   if (ctx->peer) {  // the pass already stored into the peers' receive buffers: wait until all have
     if (ctx->loopback) return DBFFT_OK;  // one stream orders the virtual ranks
     return peer_barrier(ctx);
@@ -450,24 +482,53 @@ dbfft_status exchange(dbfft_ctx ctx, long long chunk) {
   ProfScope ps(ctx, PK_XCHG);
   const size_t bytes = sizeof(cplx) * chunk;
   if (ctx->loopback) {
-    for (int r = 0; r < ctx->P; ++r)
-      for (int d = 0; d < ctx->P; ++d)
-        CK(cudaMemcpyAsync(ctx->slabs[d].WR + (long long)r * chunk, ctx->slabs[r].WA + (long long)d * chunk, bytes,
+    for (Slab& s : ctx->slabs)
+      for (int d = 0; d < ctx->Pz; ++d)
+        CK(cudaMemcpyAsync(ctx->slabs[grank(ctx, s.pa, d)].WR + (long long)s.pb * chunk, s.WA + (long long)d * chunk, bytes,
                            cudaMemcpyDeviceToDevice, ctx->stream));
     return DBFFT_OK;
   }
   Slab& s = ctx->slabs[0];
-  CK(cudaMemcpyAsync(s.WR + (long long)ctx->rank * chunk, s.WA + (long long)ctx->rank * chunk, bytes, cudaMemcpyDeviceToDevice,
-                     ctx->stream));
+  CK(cudaMemcpyAsync(s.WR + (long long)s.pb * chunk, s.WA + (long long)s.pb * chunk, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
   CKN(g_nccl.GroupStart());
-  for (int d = 0; d < ctx->P; ++d) {
-    if (d == ctx->rank) continue;
-    CKN(g_nccl.Send(s.WA + (long long)d * chunk, 2 * chunk, ncclFloat64, d, ctx->comm, ctx->stream));
-    CKN(g_nccl.Recv(s.WR + (long long)d * chunk, 2 * chunk, ncclFloat64, d, ctx->comm, ctx->stream));
+  for (int d = 0; d < ctx->Pz; ++d) {
+    if (d == s.pb) continue;
+    const int peer = grank(ctx, s.pa, d);
+    CKN(g_nccl.Send(s.WA + (long long)d * chunk, 2 * chunk, ncclFloat64, peer, ctx->comm, ctx->stream));
+    CKN(g_nccl.Recv(s.WR + (long long)d * chunk, 2 * chunk, ncclFloat64, peer, ctx->comm, ctx->stream));
   }
   CKN(g_nccl.GroupEnd());
   return DBFFT_OK;
 }
+
+// pencils: all-to-all of the x-line layout B within the row group (ranks with the same b): (a, b)
+// sends WBX[d*chunk] (nf fields of kx block d) to (d, b), which stores it at WB[a*chunk] — after
+// the y-inverse pass (kx blocks -> full x lines) and after the x pass (back).  No-op for slabs.
+dbfft_status xchg_row(dbfft_ctx ctx, int nf) {
+  if (ctx->Py == 1) return DBFFT_OK;
+  ProfScope ps(ctx, PK_XCHG);
+  const long long chunk = (long long)nf * ctx->slabs[0].fsB;
+  const size_t bytes = sizeof(cplx) * chunk;
+  if (ctx->loopback) {
+    for (Slab& s : ctx->slabs)
+      for (int d = 0; d < ctx->Py; ++d)
+        CK(cudaMemcpyAsync(ctx->slabs[grank(ctx, d, s.pb)].WB + (long long)s.pa * chunk, s.WBX + (long long)d * chunk, bytes,
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+    return DBFFT_OK;
+  }
+  Slab& s = ctx->slabs[0];
+  CK(cudaMemcpyAsync(s.WB + (long long)s.pa * chunk, s.WBX + (long long)s.pa * chunk, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  CKN(g_nccl.GroupStart());
+  for (int d = 0; d < ctx->Py; ++d) {
+    if (d == s.pa) continue;
+    const int peer = grank(ctx, d, s.pb);
+    CKN(g_nccl.Send(s.WBX + (long long)d * chunk, 2 * chunk, ncclFloat64, peer, ctx->comm, ctx->stream));
+    CKN(g_nccl.Recv(s.WB + (long long)d * chunk, 2 * chunk, ncclFloat64, peer, ctx->comm, ctx->stream));
+  }
+  CKN(g_nccl.GroupEnd());
+  return DBFFT_OK;
+}
+int nf_B(dbfft_ctx ctx) { return ctx->kin == 9 ? 9 : 6; }  // fields of the operator's x-line layout
 
 // all-reduce of slab.loc[off .. off+k) over ranks (sum or max)
 dbfft_status allreduce(dbfft_ctx ctx, int off, int k, bool is_max) {
@@ -823,24 +884,27 @@ dbfft_status apply_K_slabs(dbfft_ctx ctx, cplx* Slab::*u, cplx* Slab::*f, bool u
     CKS(run_col(ctx, fin ? COL_I1F : COL_I1S, PK_I1, g, ctx->n3));
   }
   CKS(exchange(ctx, (long long)nf1 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->kxp));
+  const int nfb = nf_B(ctx);
   for (Slab& s : ctx->slabs) {
-    ColGeom g = geom_I2(ctx, s, s.WR, s.WB, nf1);
+    ColGeom g = geom_I2(ctx, s, s.WR, s.WBX, nf1, nfb);
     if (guard) guard_geom(g, s);
     CKS(run_col(ctx, fin ? COL_I2F : COL_I2S, PK_I2, g, ctx->n2));
   }
+  CKS(xchg_row(ctx, nfb));
   if (ao) ao->grid_x.assign(ctx->slabs.size(), 0);
   for (size_t k = 0; k < ctx->slabs.size(); ++k) {
     Slab& s = ctx->slabs[k];
-    XGeom gx = xgeom(ctx, s, s.WB, s.WB);
+    XGeom gx = xgeom(ctx, s, s.WB, s.WBX, nfb, nfb);
     gx.e = use_e ? (const double*)(s.cg->*e_member) : nullptr;
     if (guard) guard_geom(gx, s);
     int gridx = 0;
     CKS(run_x(ctx, xkind, PK_X, gx, &gridx));
     if (ao) ao->grid_x[k] = gridx;
   }
+  CKS(xchg_row(ctx, nfb));
   if (front_only) return DBFFT_OK;  // the caller runs the forward tail (PCG: F3 fused with r -= alpha q)
   for (Slab& s : ctx->slabs) {
-    ColGeom g = geom_F2(ctx, s, s.WB, s.WS2, 6);
+    ColGeom g = geom_F2(ctx, s, s.WB, s.WS2, 6, nfb);
     if (guard) guard_geom(g, s);
     CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, g, ctx->n2));
   }
@@ -856,7 +920,8 @@ dbfft_status apply_K_slabs(dbfft_ctx ctx, cplx* Slab::*u, cplx* Slab::*f, bool u
 // forward tail of the rhs: WB holds -sigma spectra (from an X pass) -> F2 -> F3 -> b
 dbfft_status forward_tail(dbfft_ctx ctx) {
   const bool fin = ctx->kin == 9;
-  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, geom_F2(ctx, s, s.WB, s.WS2, 6), ctx->n2));
+  CKS(xchg_row(ctx, nf_B(ctx)));  // the X pass before it stored into WBX
+  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, geom_F2(ctx, s, s.WB, s.WS2, 6, nf_B(ctx)), ctx->n2));
   CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->kxp));
   for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_F3, geom_F3(ctx, s, s.WR2, s.b, 6), ctx->n3));
   return DBFFT_OK;
@@ -1196,7 +1261,7 @@ dbfft_status pcg_iteration_fused(dbfft_ctx ctx, bool macro, int nb, cudaGraphCon
     CK(launch_fin_alpha(s.cg, s.loc, ctx->stream));
   }
   for (Slab& s : ctx->slabs) {
-    ColGeom g = geom_F2(ctx, s, s.WB, s.WS2, 6);
+    ColGeom g = geom_F2(ctx, s, s.WB, s.WS2, 6, nf_B(ctx));
     guard_geom(g, s);
     CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, g, ctx->n2));
   }
@@ -1384,7 +1449,7 @@ dbfft_status solve_linear(dbfft_ctx ctx, const double* target, const uint8_t* ma
   std::vector<int> grids(ctx->slabs.size());
   for (size_t k = 0; k < ctx->slabs.size(); ++k) {
     Slab& s = ctx->slabs[k];
-    XGeom gx = xgeom(ctx, s, nullptr, s.WB);
+    XGeom gx = xgeom(ctx, s, nullptr, s.WBX, 6, 6);
     gx.e = s.e_dev;
     CKS(run_x(ctx, X_RHS_SMALL_PHASE, PK_XCONST, gx, &grids[k]));
   }
@@ -1430,12 +1495,14 @@ dbfft_status constitutive(dbfft_ctx ctx, bool has_in, const double* dF_host, dou
     const int nf1 = nf_I1(ctx);
     for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_I1F : COL_I1S, PK_I1, geom_I1(ctx, s, s.x, s.WS1, nf1), ctx->n3));
     CKS(exchange(ctx, (long long)nf1 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->kxp));
-    for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_I2F : COL_I2S, PK_I2, geom_I2(ctx, s, s.WR, s.WB, nf1), ctx->n2));
+    for (Slab& s : ctx->slabs)
+      CKS(run_col(ctx, fin ? COL_I2F : COL_I2S, PK_I2, geom_I2(ctx, s, s.WR, s.WBX, nf1, nf_B(ctx)), ctx->n2));
+    CKS(xchg_row(ctx, nf_B(ctx)));
   }
   std::vector<int> grids(ctx->slabs.size());
   for (size_t k = 0; k < ctx->slabs.size(); ++k) {
     Slab& s = ctx->slabs[k];
-    XGeom gx = xgeom(ctx, s, s.WB, s.WB);
+    XGeom gx = xgeom(ctx, s, s.WB, s.WBX, nf_B(ctx), nf_B(ctx));
     gx.e = s.e_dev;
     gx.has_in = has_in ? 1 : 0;
     gx.dt = dt;
@@ -1450,7 +1517,7 @@ dbfft_status constitutive(dbfft_ctx ctx, bool has_in, const double* dF_host, dou
   int bad = 0x7f7f7f7f;
   for (Slab& s : ctx->slabs) {
     CK(cudaMemcpy(ctx->h_bad, s.bad, sizeof(int), cudaMemcpyDeviceToHost));
-    if (*ctx->h_bad != 0x7f7f7f7f && bad == 0x7f7f7f7f) bad = *ctx->h_bad + (int)(s.z0 * (long long)ctx->n1 * ctx->n2);
+    if (*ctx->h_bad != 0x7f7f7f7f && bad == 0x7f7f7f7f) bad = (int)global_voxel(ctx, s, *ctx->h_bad);
   }
   if (bad != 0x7f7f7f7f) {
     *ctx->h_bad = bad;
@@ -1572,6 +1639,7 @@ void free_slab(dbfft_ctx ctx, Slab& s) {
                   s.cg, s.part_x, s.part_cg, s.part_misc, s.loc, s.e_dev, s.bad, s.counts, s.tmp_real};
   for (void* p : ptrs) dfree(ctx, p);
   if (!ctx->peer && s.WR && s.WR != s.WA) dfree(ctx, s.WR);
+  if (s.WBX && s.WBX != s.WB) dfree(ctx, s.WBX);
 }
 
 void free_all(dbfft_ctx ctx) {
@@ -1606,17 +1674,30 @@ dbfft_status ensure_tmp(dbfft_ctx ctx, Slab& s) {
   return DBFFT_OK;
 }
 
+// A rank's real block [zl][yr][x] (nzl rows of nyr n1 contiguous elements) <-> its place in a
+// global [z][y][x] array at (z0, y0, 0) (loopback API); z-slabs: one contiguous block
+cudaError_t real_block_copy(dbfft_ctx ctx, const Slab& s, void* dst, const void* src, size_t esz, bool to_global, cudaMemcpyKind kind) {
+  const size_t row = esz * (size_t)s.nyr * ctx->n1, plane = esz * (size_t)ctx->n1 * ctx->n2;
+  const size_t goff = esz * ((size_t)s.z0 * ctx->n1 * ctx->n2 + (size_t)s.y0 * ctx->n1);
+  if (to_global) return cudaMemcpy2DAsync((char*)dst + goff, plane, src, row, row, s.nzl, kind, ctx->stream);
+  return cudaMemcpy2DAsync(dst, row, (const char*)src + goff, plane, row, s.nzl, kind, ctx->stream);
+}
+// global voxel index of the rank's local voxel v (line-major [zl][yr][x])
+long long global_voxel(dbfft_ctx ctx, const Slab& s, long long v) {
+  const long long rowv = (long long)s.nyr * ctx->n1;
+  return ((long long)s.z0 + v / rowv) * ctx->n1 * ctx->n2 + (long long)s.y0 * ctx->n1 + v % rowv;
+}
+
 // Real fields: the loopback API exposes global [c][z][y][x] arrays; with NCCL each rank passes
-// its own z-slab [c][zl][y][x].
+// its own block [c][zl][yr][x] (z-slabs: [c][zl][y][x]).
 dbfft_status scatter_real(dbfft_ctx ctx, const double* src, int on_device, int ncomp, const int* comp_map, double* Slab::*dst) {
   const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-  const long long plane = (long long)ctx->n1 * ctx->n2;
   const long long Nsrc = ctx->loopback ? ctx->N : ctx->slabs[0].Nloc;
   for (Slab& s : ctx->slabs) {
-    const long long off = ctx->loopback ? (long long)s.z0 * plane : 0;
     for (int c = 0; c < ncomp; ++c) {
       const int sc = comp_map ? comp_map[c] : c;
-      CK(cudaMemcpyAsync(s.*dst + (long long)c * s.Nloc, src + (long long)sc * Nsrc + off, sizeof(double) * s.Nloc, kind, ctx->stream));
+      if (ctx->loopback) CK(real_block_copy(ctx, s, s.*dst + (long long)c * s.Nloc, src + (long long)sc * Nsrc, sizeof(double), false, kind));
+      else CK(cudaMemcpyAsync(s.*dst + (long long)c * s.Nloc, src + (long long)sc * Nsrc, sizeof(double) * s.Nloc, kind, ctx->stream));
     }
   }
   CK(cudaStreamSynchronize(ctx->stream));
@@ -1625,18 +1706,23 @@ dbfft_status scatter_real(dbfft_ctx ctx, const double* src, int on_device, int n
 
 dbfft_status gather_real(dbfft_ctx ctx, double* Slab::*srcm, int ncomp, double* out, int out_on_device) {
   const cudaMemcpyKind kind = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-  const long long plane = (long long)ctx->n1 * ctx->n2;
   const long long Ndst = ctx->loopback ? ctx->N : ctx->slabs[0].Nloc;
   for (Slab& s : ctx->slabs) {
-    const long long off = ctx->loopback ? (long long)s.z0 * plane : 0;
-    for (int c = 0; c < ncomp; ++c)
-      CK(cudaMemcpyAsync(out + (long long)c * Ndst + off, s.*srcm + (long long)c * s.Nloc, sizeof(double) * s.Nloc, kind, ctx->stream));
+    for (int c = 0; c < ncomp; ++c) {
+      if (ctx->loopback) CK(real_block_copy(ctx, s, out + (long long)c * Ndst, s.*srcm + (long long)c * s.Nloc, sizeof(double), true, kind));
+      else CK(cudaMemcpyAsync(out + (long long)c * Ndst, s.*srcm + (long long)c * s.Nloc, sizeof(double) * s.Nloc, kind, ctx->stream));
+    }
   }
   CK(cudaStreamSynchronize(ctx->stream));
   return DBFFT_OK;
 }
 
-// spectral vectors [3][ky][kz][kx]: loopback API vectors are global, slabs own ky ranges
+// spectral vectors [3][ky][kz][kx]: loopback API vectors are global [3][n2][n3][n1/2+1], a rank
+// owns ky in [ky0, ky0 + nyl) and (pencils) the kx columns [kx0, kx0 + kxm) plus the Nyquist on
+// the last row rank; its local layout [3][nyl][n3][nkx] keeps the padding column at zero
+long long spec_cols(dbfft_ctx ctx, const Slab& s) {
+  return ctx->Py == 1 ? ctx->n1h : ctx->kxm + (s.pa == ctx->Py - 1 ? 1 : 0);
+}
 dbfft_status spec_in(dbfft_ctx ctx, const cplx* src, cplx* Slab::*dst) {
   const long long Hs_glob = (long long)ctx->n1h * ctx->n2 * ctx->n3;
   for (Slab& s : ctx->slabs) {
@@ -1644,9 +1730,11 @@ dbfft_status spec_in(dbfft_ctx ctx, const cplx* src, cplx* Slab::*dst) {
       CK(cudaMemcpyAsync(s.*dst, src, sizeof(cplx) * 3 * s.Hs, cudaMemcpyDeviceToDevice, ctx->stream));
       continue;
     }
+    if (ctx->Py > 1) CK(cudaMemsetAsync(s.*dst, 0, sizeof(cplx) * 3 * s.Hs, ctx->stream));
     for (int c = 0; c < 3; ++c)
-      CK(cudaMemcpyAsync(s.*dst + c * s.Hs, src + c * Hs_glob + (long long)s.ky0 * ctx->n3 * ctx->n1h, sizeof(cplx) * s.Hs,
-                         cudaMemcpyDeviceToDevice, ctx->stream));
+      CK(cudaMemcpy2DAsync(s.*dst + c * s.Hs, sizeof(cplx) * ctx->nkx, src + c * Hs_glob + (long long)s.ky0 * ctx->n3 * ctx->n1h + s.kx0,
+                           sizeof(cplx) * ctx->n1h, sizeof(cplx) * spec_cols(ctx, s), (size_t)s.nyl * ctx->n3,
+                           cudaMemcpyDeviceToDevice, ctx->stream));
   }
   return DBFFT_OK;
 }
@@ -1658,8 +1746,9 @@ dbfft_status spec_out(dbfft_ctx ctx, cplx* Slab::*srcm, cplx* dst, cudaMemcpyKin
       continue;
     }
     for (int c = 0; c < 3; ++c)
-      CK(cudaMemcpyAsync(dst + c * Hs_glob + (long long)s.ky0 * ctx->n3 * ctx->n1h, s.*srcm + c * s.Hs, sizeof(cplx) * s.Hs, kind,
-                         ctx->stream));
+      CK(cudaMemcpy2DAsync(dst + c * Hs_glob + (long long)s.ky0 * ctx->n3 * ctx->n1h + s.kx0, sizeof(cplx) * ctx->n1h,
+                           s.*srcm + c * s.Hs, sizeof(cplx) * ctx->nkx, sizeof(cplx) * spec_cols(ctx, s), (size_t)s.nyl * ctx->n3,
+                           kind, ctx->stream));
   }
   CK(cudaStreamSynchronize(ctx->stream));
   return DBFFT_OK;
@@ -1672,12 +1761,14 @@ dbfft_status alloc_slab(dbfft_ctx ctx, Slab& s) {
   CK(cudaMemset(s.u, 0, sizeof(cplx) * v3));
   CK(cudaMemset(s.u_c, 0, sizeof(cplx) * v3));
   CKS(dalloc(ctx, &s.WA, (size_t)6 * s.Hsp));
-  if (ctx->P == 1) s.WR = s.WA;
+  if (ctx->Pz == 1) s.WR = s.WA;
   else if (!ctx->peer) CKS(dalloc(ctx, &s.WR, (size_t)6 * s.Hsp));
   // peer transport: WR / WR2 / WS1 / WS2 are mapped by build_peer once all slabs exist
   s.WS1 = s.WS2 = s.WA;
   s.WR2 = s.WR;
   CKS(dalloc(ctx, &s.WB, (size_t)ctx->kin * s.Hsp));
+  if (ctx->Py > 1) CKS(dalloc(ctx, &s.WBX, (size_t)ctx->kin * s.Hsp));
+  else s.WBX = s.WB;
   CKS(dalloc(ctx, &s.cg, 1));
   int gx = 0;
   for (int k = 0; k < X_REAL_OUT; ++k) gx = std::max(gx, x_grid(k, ctx->n1, s.nlines));
@@ -1790,9 +1881,19 @@ dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinemat
   const int P = env ? std::max(1, env->world) : 1;
   const int rank = env ? env->rank : 0;
   const int loopback = env ? env->loopback : 0;
-  if ((P & (P - 1)) != 0 || n[1] % P != 0 || n[2] % P != 0 || rank < 0 || rank >= P) {
-    g_create_error = "world must be a power of two dividing n2 and n3 (S:48), 0 <= rank < world";
+  const int Py = (env && env->pencil_rows > 1) ? env->pencil_rows : 1;
+  const int Pz = P / Py;
+  if ((P & (P - 1)) != 0 || (Py & (Py - 1)) != 0 || Py > P || n[1] % Pz != 0 || n[2] % Pz != 0 || rank < 0 || rank >= P) {
+    g_create_error = "world and pencil_rows must be powers of two, world / pencil_rows dividing n2 and n3 (S:48), 0 <= rank < world";
     return DBFFT_E_INVALID_GRID;
+  }
+  if (Py > 1 && (!is_pow2_in(n[0]) || (n[0] & (n[0] - 1)) != 0 || n[0] / 2 < Py || n[1] % Py != 0)) {
+    g_create_error = "pencil_rows > 1: n1 a power of two with n1/2 >= pencil_rows, pencil_rows dividing n2";
+    return DBFFT_E_INVALID_GRID;
+  }
+  if (Py > 1 && env && env->transport == DBFFT_TRANSPORT_PEER) {
+    g_create_error = "pencil_rows > 1 runs on the NCCL transport (the peer windows are built for z-slabs)";
+    return DBFFT_E_INVALID_ARG;
   }
   if (P > 1 && !loopback && !env->nccl_id) {
     g_create_error = "world > 1 needs env->nccl_id (dbfft_nccl_unique_id on rank 0, broadcast) or env->loopback";
@@ -1809,7 +1910,11 @@ dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinemat
     // did not (256^3 finite apply_K 2.732 ms either way; 512^3 F2 2.88 -> 3.20 ms), so the
     // default is the dense pitch; the full GPU suite passes with either.
     const char* e = getenv("DBFFT_KX_PAD");
-    ctx->kxp = (e && e[0] == '1') ? (ctx->n1h + 7) / 8 * 8 : ctx->n1h;
+    ctx->Py = Py;
+    ctx->Pz = Pz;
+    ctx->kxm = Py > 1 ? n[0] / (2 * Py) : 0;
+    ctx->nkx = Py > 1 ? ctx->kxm + 1 : ctx->n1h;
+    ctx->kxp = (e && e[0] == '1') ? (ctx->nkx + 7) / 8 * 8 : ctx->nkx;
   }
   for (int a = 0; a < 3; ++a) ctx->L[a] = L[a];
   ctx->kin = kinematics;
@@ -1874,14 +1979,20 @@ dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinemat
   for (int k = 0; k < nslab; ++k) {
     Slab& sl = ctx->slabs[k];
     sl.rank = ctx->loopback ? k : rank;
-    sl.nyl = n[1] / P;
-    sl.nzl = n[2] / P;
-    sl.ky0 = sl.rank * sl.nyl;
-    sl.z0 = sl.rank * sl.nzl;
-    sl.Hs = (long long)ctx->n1h * sl.nyl * n[2];
+    sl.pa = sl.rank % Py;  // pencil grid position, rank = b Py + a
+    sl.pb = sl.rank / Py;
+    sl.nyl = n[1] / Pz;
+    sl.nzl = n[2] / Pz;
+    sl.ky0 = sl.pb * sl.nyl;
+    sl.z0 = sl.pb * sl.nzl;
+    sl.nyr = n[1] / Py;
+    sl.y0 = sl.pa * sl.nyr;
+    sl.kx0 = sl.pa * ctx->kxm;
+    sl.Hs = (long long)ctx->nkx * sl.nyl * n[2];
     sl.Hsp = (long long)ctx->kxp * sl.nyl * n[2];
-    sl.Nloc = (long long)n[0] * n[1] * sl.nzl;
-    sl.nlines = (long long)n[1] * sl.nzl;
+    sl.fsB = (long long)sl.nzl * sl.nyr * ctx->kxp;
+    sl.Nloc = (long long)n[0] * sl.nyr * sl.nzl;
+    sl.nlines = (long long)sl.nyr * sl.nzl;
     sl.xiy = ctx->xiy + sl.ky0;
     if ((s = alloc_slab(ctx, sl)) != DBFFT_OK) return fail(s);
   }
@@ -2019,14 +2130,15 @@ dbfft_status dbfft_destroy(dbfft_ctx ctx) {
 dbfft_status dbfft_spectral_layout(dbfft_ctx ctx, int64_t shape[4], int64_t strides[4]) {
   if (!ctx || !shape || !strides) return DBFFT_E_INVALID_ARG;
   const int nyl = ctx->loopback ? ctx->n2 : ctx->slabs[0].nyl;  // loopback API vectors are global
+  const int nkx = ctx->loopback ? ctx->n1h : ctx->nkx;          // NCCL pencils: the local kx block
   shape[0] = 3;
   shape[1] = nyl;
   shape[2] = ctx->n3;
-  shape[3] = ctx->n1h;
+  shape[3] = nkx;
   strides[3] = 1;
-  strides[2] = ctx->n1h;
-  strides[1] = (int64_t)ctx->n3 * ctx->n1h;
-  strides[0] = (int64_t)nyl * ctx->n3 * ctx->n1h;
+  strides[2] = nkx;
+  strides[1] = (int64_t)ctx->n3 * nkx;
+  strides[0] = (int64_t)nyl * ctx->n3 * nkx;
   return DBFFT_OK;
 }
 
@@ -2111,7 +2223,6 @@ dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t o
   }
   dbfft_status s;
   const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-  const long long plane = (long long)ctx->n1 * ctx->n2;
   // buffers are reused when they fit (pointers stable: the captured PCG loop graphs stay valid,
   // e.g. for a new load walk on the same grid); `gen` moves only if a pointer changed
   std::vector<const void*> before;
@@ -2122,8 +2233,8 @@ dbfft_status dbfft_set_phases(dbfft_ctx ctx, const uint16_t* phase_id, int32_t o
   CK(cudaStreamSynchronize(ctx->stream));  // kernels still reading the old table / counts
   for (Slab& sl : ctx->slabs) {
     if (!sl.phase && (s = dalloc(ctx, &sl.phase, sl.Nloc)) != DBFFT_OK) return s;
-    const long long off = ctx->loopback ? (long long)sl.z0 * plane : 0;
-    CK(cudaMemcpyAsync(sl.phase, phase_id + off, sizeof(uint16_t) * sl.Nloc, kind, ctx->stream));
+    if (ctx->loopback) CK(real_block_copy(ctx, sl, sl.phase, phase_id, sizeof(uint16_t), false, kind));
+    else CK(cudaMemcpyAsync(sl.phase, phase_id, sizeof(uint16_t) * sl.Nloc, kind, ctx->stream));
     if (sl.cap_ptable < pt.size()) {
       dfree(ctx, sl.ptable);
       sl.ptable = nullptr;
@@ -2378,10 +2489,11 @@ dbfft_status field_to_tmp(dbfft_ctx ctx, int which) {
   CKS(upload_e(ctx, ctx->Fbar_c));
   for (Slab& s : ctx->slabs) CKS(run_col(ctx, COL_I1S, PK_OTHER, geom_I1(ctx, s, s.u_c, s.WS1, 5), ctx->n3));
   CKS(exchange(ctx, (long long)5 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->kxp));
+  for (Slab& s : ctx->slabs) CKS(run_col(ctx, COL_I2S, PK_OTHER, geom_I2(ctx, s, s.WR, s.WBX, 5, 6), ctx->n2));
+  CKS(xchg_row(ctx, 6));
   for (Slab& s : ctx->slabs) {
-    CKS(run_col(ctx, COL_I2S, PK_OTHER, geom_I2(ctx, s, s.WR, s.WB, 5), ctx->n2));
     double* tmp6 = reinterpret_cast<double*>(s.WA);  // 6 real fields fit in WA (6 complex fields)
-    XGeom gx = xgeom(ctx, s, s.WB, nullptr);
+    XGeom gx = xgeom(ctx, s, s.WB, nullptr, 6, 6);
     gx.real_out = tmp6;
     CKS(run_x(ctx, X_REAL_OUT + 6, PK_OTHER, gx, nullptr));
     ProfScope ps(ctx, PK_OTHER);
@@ -2427,12 +2539,13 @@ dbfft_status incompat_max(dbfft_ctx ctx, double* result) {
   const long long chunk = (long long)nf * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->kxp;
   for (int row = 0; row < nrow; ++row) {
     for (Slab& s : ctx->slabs) {
-      XGeom gx = xgeom(ctx, s, nullptr, s.WB);
+      XGeom gx = xgeom(ctx, s, nullptr, s.WBX, nf, nf);
       gx.real_in = s.tmp_real;
       for (int f = 0; f < nf; ++f) gx.real_map[f] = fin ? 3 * row + f : kRowMajorVoigt[f];
       CKS(run_x(ctx, X_REAL_IN + nf, PK_OTHER, gx, nullptr));
-      CKS(run_col(ctx, fin ? COL_YF3 : COL_YF6, PK_OTHER, geom_F2(ctx, s, s.WB, s.WS2, nf), ctx->n2));
     }
+    CKS(xchg_row(ctx, nf));
+    for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_YF3 : COL_YF6, PK_OTHER, geom_F2(ctx, s, s.WB, s.WS2, nf, nf), ctx->n2));
     CKS(exchange(ctx, chunk));
     for (Slab& s : ctx->slabs) {
       CKS(run_col(ctx, fin ? COL_ZF3 : COL_ZF6, PK_OTHER, geom_F3(ctx, s, s.WR2, s.WB, nf), ctx->n3));
@@ -2441,11 +2554,12 @@ dbfft_status incompat_max(dbfft_ctx ctx, double* result) {
     }
     for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_ZI3 : COL_ZI6, PK_OTHER, geom_I1(ctx, s, s.WB, s.WS1, nf), ctx->n3));
     CKS(exchange(ctx, chunk));
+    for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_YI3 : COL_YI6, PK_OTHER, geom_I2(ctx, s, s.WR, s.WBX, nf, nf), ctx->n2));
+    CKS(xchg_row(ctx, nf));
     for (size_t k = 0; k < ctx->slabs.size(); ++k) {
       Slab& s = ctx->slabs[k];
-      CKS(run_col(ctx, fin ? COL_YI3 : COL_YI6, PK_OTHER, geom_I2(ctx, s, s.WR, s.WB, nf), ctx->n2));
       double* out = reinterpret_cast<double*>(s.WA);
-      XGeom gx = xgeom(ctx, s, s.WB, nullptr);
+      XGeom gx = xgeom(ctx, s, s.WB, nullptr, nf, nf);
       gx.real_out = out;
       CKS(run_x(ctx, X_REAL_OUT + nf, PK_OTHER, gx, nullptr));
       {
@@ -2480,13 +2594,14 @@ dbfft_status div_norm(dbfft_ctx ctx, double* norm, double* mean9) {
     mean9[a] /= (double)ctx->N;
   }
   for (Slab& s : ctx->slabs) {
-    XGeom gx = xgeom(ctx, s, nullptr, s.WB);
+    XGeom gx = xgeom(ctx, s, nullptr, s.WBX, nf, nf);
     gx.real_in = s.tmp_real;
     for (int f = 0; f < nf; ++f) gx.real_map[f] = fin ? f : kRowMajorVoigt[f];
     CKS(run_x(ctx, X_REAL_IN + nf, PK_OTHER, gx, nullptr));
   }
+  CKS(xchg_row(ctx, nf));
   // the operator's forward tail: f = -i xi . sigma_hat (positive form, R3) into q
-  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_OTHER, geom_F2(ctx, s, s.WB, s.WS2, 6), ctx->n2));
+  for (Slab& s : ctx->slabs) CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_OTHER, geom_F2(ctx, s, s.WB, s.WS2, 6, nf), ctx->n2));
   CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->kxp));
   for (size_t k = 0; k < ctx->slabs.size(); ++k) {
     Slab& s = ctx->slabs[k];
@@ -2528,9 +2643,10 @@ dbfft_status dbfft_get_field(dbfft_ctx ctx, int32_t which, void* out, int32_t ou
     case DBFFT_FIELD_U: {
       for (Slab& s : ctx->slabs) CKS(run_col(ctx, COL_ZI3, PK_OTHER, geom_I1(ctx, s, s.u_c, s.WS1, 3), ctx->n3));
       CKS(exchange(ctx, (long long)3 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->kxp));
+      for (Slab& s : ctx->slabs) CKS(run_col(ctx, COL_YI3, PK_OTHER, geom_I2(ctx, s, s.WR, s.WBX, 3, 3), ctx->n2));
+      CKS(xchg_row(ctx, 3));
       for (Slab& s : ctx->slabs) {
-        CKS(run_col(ctx, COL_YI3, PK_OTHER, geom_I2(ctx, s, s.WR, s.WB, 3), ctx->n2));
-        XGeom gx = xgeom(ctx, s, s.WB, nullptr);
+        XGeom gx = xgeom(ctx, s, s.WB, nullptr, 3, 3);
         gx.real_out = s.tmp_real;
         CKS(run_x(ctx, X_REAL_OUT + 3, PK_OTHER, gx, nullptr));
       }
@@ -2544,15 +2660,16 @@ dbfft_status dbfft_get_field(dbfft_ctx ctx, int32_t which, void* out, int32_t ou
       // the full 3x3x3x3 tangent of the current state, built per voxel from what apply_K reads,
       // in chunks through a device scratch of 81 x chunk doubles
       const int mode = ctx->family == FAM_LINEAR ? 3 : ctx->family == FAM_J2 ? 2 : (ctx->tmode ? 1 : 0);
-      const long long plane = (long long)ctx->n1 * ctx->n2;
       const long long Ndst = ctx->loopback ? ctx->N : ctx->slabs[0].Nloc;
-      const long long chunk = std::min<long long>(ctx->slabs[0].Nloc, 1LL << 20);
+      // (loopback pencils: one [yr][x] plane block per chunk, contiguous in the global array)
+      const long long chunk = (ctx->loopback && ctx->Py > 1) ? (long long)ctx->slabs[0].nyr * ctx->n1
+                                                             : std::min<long long>(ctx->slabs[0].Nloc, 1LL << 20);
       double* scratch = nullptr;
       CKS(dalloc(ctx, &scratch, 81 * (size_t)chunk));
       cudaError_t e = cudaSuccess;
       for (Slab& s : ctx->slabs) {
-        const long long off = ctx->loopback ? (long long)s.z0 * plane : 0;
         for (long long v0 = 0; v0 < s.Nloc && e == cudaSuccess; v0 += chunk) {
+          const long long off = ctx->loopback ? global_voxel(ctx, s, v0) - v0 : 0;
           const long long nv = std::min(chunk, s.Nloc - v0);
           e = launch_tangent81(mode, xgeom(ctx, s, nullptr, nullptr), v0, nv, scratch, ctx->stream);
           if (e == cudaSuccess)
@@ -2606,7 +2723,9 @@ dbfft_status dbfft_info(dbfft_ctx ctx, char* buf, int32_t cap) {
   const char* tr = ctx->P == 1 ? "none" : ctx->peer ? "peer" : "nccl";
   std::string j = "{\"device\": " + std::to_string(ctx->device) + ", \"sms\": " + std::to_string(num_sms()) +
                   ", \"world\": " + std::to_string(ctx->P) + ", \"rank\": " + std::to_string(ctx->rank) +
-                  ", \"loopback\": " + std::to_string(ctx->loopback) + ", \"transport\": \"" + tr +
+                  ", \"loopback\": " + std::to_string(ctx->loopback) + ", \"decomposition\": \"" +
+                  (ctx->Py > 1 ? "pencils " + std::to_string(ctx->Py) + "x" + std::to_string(ctx->Pz) : std::string("z-slabs")) +
+                  "\", \"transport\": \"" + tr +
                   "\", \"nccl_comm\": " + (ctx->comm ? "true" : "false") + ", \"pcg_loop\": \"" + ctx->loop_note + "\"}";
   for (char& c : j)
     if (c == '\n') c = ' ';

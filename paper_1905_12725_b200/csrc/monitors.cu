@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(MB) k_specnorm2(SpecGeom g, const cplx* __rest
   double s = 0.0;
   for (long long i = (long long)blockIdx.x * MB + threadIdx.x; i < g.Hs; i += (long long)gridDim.x * MB) {
     const int kx = (int)(i % g.n1h);
-    const double w = (kx == 0 || 2 * kx == g.n1) ? 1.0 : 2.0;
+    const double w = (kx + g.kx0 == 0 || 2 * (kx + g.kx0) == g.n1) ? 1.0 : 2.0;
     for (int f = 0; f < nf; ++f) {
       const cplx a = v[f * g.Hs + i];
       s += w * (a.x * a.x + a.y * a.y);

@@ -929,6 +929,14 @@ DBF_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
 }
 DBF_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// pencil decomposition: offset of line kx k (0..n1/2) in the kx-chunked layout of XGeom.kch
+// (chunk c = min(k / kch, npy - 1): the Nyquist sits in slot kch of the last chunk)
+DBF_DEV long long x_koff(const XGeom& g, int k, long long pcs) {
+  if (g.kch == 0) return k;
+  const int c = min(k / g.kch, g.npy - 1);
+  return (long long)c * pcs + (k - c * g.kch);
+}
+
 // issue the stage copies of line group `grp` (one elected thread)
 template <int N1, int KIND>
 DBF_DEV void x_issue_in(const XGeom& g, long long grp, cplx* st_in, uint64_t* bar) {
@@ -939,7 +947,16 @@ DBF_DEV void x_issue_in(const XGeom& g, long long grp, cplx* st_in, uint64_t* ba
   const uint32_t row = sizeof(cplx) * CF::N1H;
   mbar_expect_tx(bar, row * CIN * nl);
   for (int l = 0; l < nl; ++l)
-    for (int f = 0; f < CIN; ++f) bulk_g2s(st_in + (l * CIN + f) * CF::N1H, g.in + f * g.fs_in + (l0 + l) * g.kxp, row, bar);
+    for (int f = 0; f < CIN; ++f) {
+      cplx* dst = st_in + (l * CIN + f) * CF::N1H;
+      const cplx* src = g.in + f * g.fs_in + (l0 + l) * g.kxp;
+      if (g.kch == 0) {
+        bulk_g2s(dst, src, row, bar);
+      } else {  // pencil: one copy per kx chunk (the last one carries the Nyquist)
+        for (int c = 0; c < g.npy; ++c)
+          bulk_g2s(dst + c * g.kch, src + c * g.kpcs_in, (uint32_t)sizeof(cplx) * (g.kch + (c == g.npy - 1 ? 1 : 0)), bar);
+      }
+    }
 }
 template <int N1, int KIND>
 DBF_DEV void x_issue_tan(const XGeom& g, long long grp, double* st_tan, uint16_t* st_ph, uint64_t* bar) {
@@ -1054,8 +1071,8 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
         const bool lo = x_lo<N1, PX, TPJ>(s, gq);
         const int kk = lo ? k : N1 - k;
         cplx A = make_double2(0, 0), B = make_double2(0, 0);
-        if (va && fa < cin) A = SSP ? st_in[(la * T::CIN + fa) * CF::N1H + kk] : __ldg(g.in + fa * g.fs_in + linea * g.kxp + kk);
-        if (vb && fb < cin) B = SSP ? st_in[(lb * T::CIN + fb) * CF::N1H + kk] : __ldg(g.in + fb * g.fs_in + lineb * g.kxp + kk);
+        if (va && fa < cin) A = SSP ? st_in[(la * T::CIN + fa) * CF::N1H + kk] : __ldg(g.in + fa * g.fs_in + linea * g.kxp + x_koff(g, kk, g.kpcs_in));
+        if (vb && fb < cin) B = SSP ? st_in[(lb * T::CIN + fb) * CF::N1H + kk] : __ldg(g.in + fb * g.fs_in + lineb * g.kxp + x_koff(g, kk, g.kpcs_in));
         if (kk == 0 || 2 * kk == N1) { A.y = 0.0; B.y = 0.0; }  // Hermitian part (C2R)
         // Y_k = A_k + i B_k (k <= N/2);  conj(A_{N-k}) + i conj(B_{N-k}) otherwise
         a[s] = lo ? make_double2(A.x - B.y, A.y + B.x) : make_double2(A.x + B.y, B.x - A.y);
@@ -1211,8 +1228,14 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
             if (sta) s_dc[DCRED ? la : 0][x_red_slot<KIND>(fa)] += dcs * A.x;
             if (stb && fb < COUT) s_dc[DCRED ? lb : 0][x_red_slot<KIND>(fb)] += dcs * B.x;
           }
-          if (sta) g.out[fa * g.fs_out + linea * g.kxp + k] = A;
-          if (stb) g.out[fb * g.fs_out + lineb * g.kxp + k] = B;
+          const long long ko = x_koff(g, k, g.kpcs_out);
+          if (sta) g.out[fa * g.fs_out + linea * g.kxp + ko] = A;
+          if (stb) g.out[fb * g.fs_out + lineb * g.kxp + ko] = B;
+          if (g.kch > 0 && 2 * k == N1)  // pencil: the padding slot kch of the other kx chunks stays 0
+            for (int c = 0; c + 1 < g.npy; ++c) {
+              if (sta) g.out[c * g.kpcs_out + fa * g.fs_out + linea * g.kxp + g.kch] = make_double2(0.0, 0.0);
+              if (stb) g.out[c * g.kpcs_out + fb * g.fs_out + lineb * g.kxp + g.kch] = make_double2(0.0, 0.0);
+            }
         }
       }
       // no barrier here: a job's R2C and the next group's C2R touch only the job's own two slots
@@ -1586,7 +1609,7 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
     const int outer = tail ? (tile - tl.n_main) * KC + c : tile / tl.nkb;
     const bool valid = outer < tl.n_outer;
     at.set_col(valid ? outer : 0, tail ? g.n1h - 1 : (tile % tl.nkb) * KC + c);
-    const double wdot = (at.kx == 0 || 2 * at.kx == g.n1) ? 1.0 : 2.0;
+    const double wdot = (at.kx + g.kx0 == 0 || 2 * (at.kx + g.kx0) == g.n1) ? 1.0 : 2.0;
     const uint32_t sbase = it * nl;
     int released = 0;
     constexpr int NACC = (KIND == COL_F3S) ? 2 : 1;  // pending two-term outputs

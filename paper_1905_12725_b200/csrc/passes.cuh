@@ -37,6 +37,7 @@ struct ColGeom {
   const int* cg_stop1;   // CgDev.breakdown
   const double* precq;   // preconditioner coefficients (prec_apply; 36 doubles, device)
   int n_xy;          // length of fq.xy (guards the per-column xi_y(outer) lookup of y passes)
+  int kx0;           // global kx of local column 0 (pencil decomposition: the rank's kx block; else 0)
 };
 
 // Column pass kinds
@@ -105,6 +106,11 @@ struct XGeom {
   int tmode;              // X_CONST_FIN: 0 = store the 45-entry tangent, 1 = compact (F^-1, c1)
   const int* stop0;       // PCG loop early exit (CgDev.converged / .breakdown), null: always run
   const int* stop1;
+  // pencil decomposition (kch > 0): a line's kx arrive in npy chunks of kch columns (+ the Nyquist
+  // in slot kch of the last chunk; slot kch of the others is padding, written 0), chunk c at
+  // in + c * kpcs_in (out + c * kpcs_out); kch = 0: one contiguous row of n1h
+  int kch, npy;
+  long long kpcs_in, kpcs_out;
 };
 
 // host launchers (passes.cu)

@@ -20,7 +20,7 @@ class Env(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
                 ("cuda_stream", ctypes.c_void_p), ("device", ctypes.c_int32), ("loopback", ctypes.c_int32),
                 ("transport", ctypes.c_int32), ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN),
-                ("alloc_user", ctypes.c_void_p)]
+                ("alloc_user", ctypes.c_void_p), ("pencil_rows", ctypes.c_int32)]
 
 
 def torch_allocator(device):
@@ -182,13 +182,16 @@ class DBFFT:
     """One DBFFT context on one CUDA device (include/dbfft.h)."""
 
     def __init__(self, n, L=(1.0, 1.0, 1.0), kinematics="small", device=0, stream=None,
-                 world=1, rank=0, loopback=False, process_group=None, transport="nccl", allocator="torch"):
+                 world=1, rank=0, loopback=False, process_group=None, transport="nccl", allocator="torch",
+                 pencil_rows=1):
         """world > 1: slab decomposition (include/dbfft.h "Distribution").  loopback=True keeps
         all `world` virtual ranks in this process; otherwise NCCL, with the unique id broadcast
         over `process_group` (torch.distributed, any backend).  transport: "nccl" (all-to-all
         exchanges) or "peer" (passes store into the peers' receive buffers, dbfft_env.transport).
         allocator: "torch" (the ctx's device memory from torch's caching allocator, dbfft_env
-        dev_alloc / dev_free), "cuda" (cudaMalloc) or a tuple (alloc(nbytes) -> ptr, free(ptr))."""
+        dev_alloc / dev_free), "cuda" (cudaMalloc) or a tuple (alloc(nbytes) -> ptr, free(ptr)).
+        pencil_rows = Py > 1: 2-D pencil decomposition on a Py x (world / Py) rank grid
+        (dbfft_env.pencil_rows), else z-slabs."""
         import torch
         self.torch = torch
         self.lib = load_library()
@@ -198,6 +201,8 @@ class DBFFT:
         torch.cuda.set_device(self.device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         self.world, self.rank, self.loopback = int(world), int(rank), bool(loopback)
+        self.py = max(1, int(pencil_rows))
+        self.pz = self.world // self.py
         self._nccl_id = None
         if self.world > 1 and not self.loopback:
             self._nccl_id = nccl_unique_id_broadcast(self.rank, process_group)
@@ -212,7 +217,7 @@ class DBFFT:
             raise ValueError(allocator)
         env = Env(self.rank, self.world, ctypes.cast(self._nccl_id, ctypes.c_void_p) if self._nccl_id else None,
                   ctypes.c_void_p(self.stream.cuda_stream), device, int(self.loopback), TRANSPORTS[transport],
-                  self._alloc[0], self._alloc[1], None)
+                  self._alloc[0], self._alloc[1], None, self.py)
         h = ctypes.c_void_p()
         st = self.lib.dbfft_create((ctypes.c_int32 * 3)(*self.n), (ctypes.c_double * 3)(*L), self.kin,
                                    ctypes.byref(env), ctypes.byref(h))
@@ -243,7 +248,8 @@ class DBFFT:
     def _nloc(self):
         n1, n2, n3 = self.n
         if self.world > 1 and not self.loopback:
-            n3 //= self.world  # NCCL slab mode: this rank's z-slab
+            n3 //= self.pz  # NCCL mode: this rank's block [n3/Pz][n2/Py][n1] (z-slabs: Py = 1)
+            n2 //= self.py
         return n1 * n2 * n3
 
     def set_phases(self, phase, materials):
@@ -364,7 +370,8 @@ class DBFFT:
         float64 host array of the field's size, e.g. a reused pinned buffer) receives it instead."""
         n1, n2, n3 = self.n
         if self.world > 1 and not self.loopback:
-            n3 //= self.world  # NCCL slab mode: this rank's z-slab
+            n3 //= self.pz  # NCCL mode: this rank's block [n3/Pz][n2/Py][n1] (z-slabs: Py = 1)
+            n2 //= self.py
         N = n1 * n2 * n3
         if out is not None:
             ncomp = {FIELD_U: 3, FIELD_TANGENT: 81}.get(which, 9)

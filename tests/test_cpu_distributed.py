@@ -1,5 +1,6 @@
 """Multi-process host logic on CPU (gloo, world_size 2): the NCCL unique-id bootstrap of the
-binding and the bench's max-over-ranks / sum-over-ranks aggregation."""
+binding, the bench's max-over-ranks / sum-over-ranks aggregation, and each rank's real-space block
+of the global microstructure for z-slabs and 2-D pencils (include/dbfft.h: rank = b Py + a)."""
 import os
 import socket
 
@@ -25,7 +26,12 @@ def _worker(rank, world, port, q):
         buf = dbfft.nccl_unique_id_broadcast(rank)
         import bench
         t, it = bench.aggregate_over_ranks(1.0 + rank, 10 * (rank + 1), device="cpu")
-        q.put((rank, bytes(buf.raw), t, it))
+        import numpy as np
+        g = np.arange(8 * 4 * 6).reshape(8, 4, 6)  # [z][y][x]
+        blocks = {py: bench.rank_block(g, rank, world, py) for py in (1, 2)}
+        allb = [None] * world
+        dist.all_gather_object(allb, blocks)  # every rank sees every block
+        q.put((rank, bytes(buf.raw), t, it, allb))
     finally:
         dist.destroy_process_group()
 
@@ -46,3 +52,9 @@ def test_gloo_bootstrap_and_aggregation():
     assert res[0][1] == res[1][1] and len(res[0][1]) == 128 and any(res[0][1])
     for r in res:
         assert r[2] == 2.0 and r[3] == 30  # max time, summed iterations
+    import numpy as np
+    g = np.arange(8 * 4 * 6).reshape(8, 4, 6)
+    allb = res[0][4]
+    # z-slabs: rank r owns z in [4 r, 4 r + 4); pencils 2 x 1 (Pz = 1): rank a owns y in [2 a, 2 a + 2)
+    assert np.array_equal(np.concatenate([allb[0][1], allb[1][1]], axis=0), g)
+    assert np.array_equal(np.concatenate([allb[0][2], allb[1][2]], axis=1), g)

@@ -86,3 +86,21 @@ def test_synth_determinism_and_geometry():
     assert np.allclose(np.linalg.det(R), 1.0)
     ph, seeds = ms.voronoi((16, 16, 16), 10, 3)
     assert set(np.unique(ph)) <= set(range(10))
+
+
+def test_env_struct_matches_header():
+    """The binding's ctypes dbfft_env mirrors include/dbfft.h field by field, in order (a mismatch
+    would hand the library garbage for e.g. the allocator hooks or pencil_rows)."""
+    from paper_1905_12725_b200 import dbfft
+    src = open(os.path.join(ROOT, "include", "dbfft.h")).read()
+    body = re.search(r"typedef struct \{(.*?)\} dbfft_env;", src, re.S).group(1)
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    names = []
+    for decl in body.split(";"):
+        decl = decl.strip()
+        if not decl:
+            continue
+        m = re.search(r"\(\*\s*(\w+)\)", decl)
+        names += [m.group(1)] if m else re.findall(r"(\w+)\s*(?:,|$)", decl)
+    assert names == [f[0] for f in dbfft.Env._fields_]
+    assert "pencil_rows" in names
