@@ -39,7 +39,8 @@
  *    only its own slab (spectral vectors [3][n2/P][kz][kx]; real fields [c][n3/P][y][x]).
  *    Loopback mode (env->loopback = 1): all P virtual ranks live in this process on one device
  *    and exchange through device copies (tests the distributed data path on one GPU); API
- *    arrays are then the global ones.
+ *    arrays are then the global ones.  env->pencil_rows > 1 selects 2-D pencils instead of
+ *    z-slabs (dbfft_env below: local blocks, padding column, exchanges).
  */
 #ifndef DBFFT_H
 #define DBFFT_H

@@ -1905,16 +1905,20 @@ dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinemat
   ctx->n3 = n[2];
   ctx->n1h = n[0] / 2 + 1;
   {
-    // DBFFT_KX_PAD=1: 128-byte aligned rows (n1h rounded up to 8) in the intermediate layouts.
-    // The strided-tile membench gained 6 % from it (4.65 -> 4.93 TB/s at 256^3) but the passes
-    // did not (256^3 finite apply_K 2.732 ms either way; 512^3 F2 2.88 -> 3.20 ms), so the
-    // default is the dense pitch; the full GPU suite passes with either.
+    // 128-byte aligned rows (the local kx count rounded up to 8) in the intermediate layouts
+    // X1, B, X2: a dense 129-column row starts 16 bytes off the 128-byte grid, so a 128-byte TMA
+    // row touches 5 DRAM sectors (ncu: column-pass reads 8-12 % above the algorithmic bytes).
+    // B200 (tools/ab_promo_pad.sh): 256^3 finite apply_K 2.319 -> 2.301 ms (I1 0.271 -> 0.260,
+    // I2 0.426 -> 0.420), small 1.892 -> 1.876, 128^3 0.365 -> 0.362; but at n1 = 512 the
+    // direct-store y-forward pass slows (2.90 -> 3.22 ms), so the default pads for n1 <= 256.
+    // DBFFT_KX_PAD=1 / =0 forces either (the full GPU suite passes with both).
     const char* e = getenv("DBFFT_KX_PAD");
+    const bool pad = e ? e[0] == '1' : n[0] <= 256;
     ctx->Py = Py;
     ctx->Pz = Pz;
     ctx->kxm = Py > 1 ? n[0] / (2 * Py) : 0;
     ctx->nkx = Py > 1 ? ctx->kxm + 1 : ctx->n1h;
-    ctx->kxp = (e && e[0] == '1') ? (ctx->nkx + 7) / 8 * 8 : ctx->nkx;
+    ctx->kxp = pad ? (ctx->nkx + 7) / 8 * 8 : ctx->nkx;
   }
   for (int a = 0; a < 3; ++a) ctx->L[a] = L[a];
   ctx->kin = kinematics;

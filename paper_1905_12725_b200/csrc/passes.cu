@@ -61,6 +61,9 @@ int num_sms() {
 #ifndef DBF_X_LRAW
 #define DBF_X_LRAW 192  // target threads per pass_X CTA (lines per CTA = DBF_X_LRAW / threads per line)
 #endif
+#ifndef DBF_X_LRAW9
+#define DBF_X_LRAW9 DBF_X_LRAW  // the same for the 9-field (finite-strain) kinds
+#endif
 #ifndef DBF_X_STAGE_SPEC
 #define DBF_X_STAGE_SPEC 1  // pass_X: stage the input spectra too (else only the per-voxel data)
 #endif
@@ -858,7 +861,7 @@ struct XCfg {
   static constexpr int NP = CS / 2;
   static constexpr int PERLINE = TPJ * NP;
   // PACK: 64/TPJ lines (at least 2) so that the CTA is whole warps (the untangle shuffles)
-  static constexpr int LRAW = PACK ? (TPJ >= 32 ? 2 : 64 / TPJ) : DBF_X_LRAW / PERLINE;
+  static constexpr int LRAW = PACK ? (TPJ >= 32 ? 2 : 64 / TPJ) : (C == 9 ? DBF_X_LRAW9 : DBF_X_LRAW) / PERLINE;
   static constexpr int LPAR = LRAW >= 64 ? 64 : LRAW >= 32 ? 32 : LRAW >= 16 ? 16 : LRAW >= 8 ? 8 : LRAW >= 4 ? 4 : LRAW >= 2 ? 2 : 1;
   static constexpr int NJOB = PACK ? LPAR * C / 2 : LPAR * NP;  // pair FFT jobs per line group
   static constexpr int THREADS = NJOB * TPJ;
