@@ -55,6 +55,7 @@ DBF_DEV void block_store(double (&v)[NV], double* partials) {
 }
 
 __global__ void __launch_bounds__(BLK, MINB) k_precond(SpecGeom g, const PrecQ* __restrict__ q, const cplx* __restrict__ r, cplx* __restrict__ z) {
+  DBF_PDL_ENTRY();
   __shared__ PrecQ Q;
   load_prec(Q, q);
   for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < g.Hs; i += (long long)gridDim.x * BLK) {
@@ -70,6 +71,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_precond(SpecGeom g, const PrecQ* 
 
 // p = M r ; partials (<r, p>, <r, r>)
 __global__ void __launch_bounds__(BLK, MINB) k_cg_init(SpecGeom g, const PrecQ* __restrict__ q, const cplx* __restrict__ r, cplx* __restrict__ pv, double* partials) {
+  DBF_PDL_ENTRY();
   __shared__ PrecQ Q;
   load_prec(Q, q);
   double acc[2] = {0.0, 0.0};
@@ -93,6 +95,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_cg_init(SpecGeom g, const PrecQ* 
 // direction kernel, which reads p anyway: 3 vector transfers here instead of 6)
 __global__ void __launch_bounds__(BLK, MINB) k_cg_update(SpecGeom g, const PrecQ* __restrict__ pq, const CgDev* __restrict__ cg, cplx* __restrict__ r,
                                                    const cplx* __restrict__ qv, double* partials) {
+  DBF_PDL_ENTRY();
   if (cg->converged | cg->breakdown) return;
   __shared__ PrecQ Q;
   load_prec(Q, pq);
@@ -158,6 +161,7 @@ DBF_DEV void cg_direction_body(const SpecGeom& g, const PrecQ& Q, double alpha, 
 
 __global__ void __launch_bounds__(BLK, 2) k_cg_direction(SpecGeom g, const PrecQ* __restrict__ q, const CgDev* __restrict__ cg, cplx* __restrict__ x,
                                                       cplx* __restrict__ pv, const cplx* __restrict__ r) {
+  DBF_PDL_ENTRY();
   if (cg->breakdown) return;
   __shared__ PrecQ Q;
   load_prec(Q, q);
@@ -170,6 +174,7 @@ __global__ void __launch_bounds__(BLK, 2) k_cg_direction(SpecGeom g, const PrecQ
 // end of a PCG iteration; inside the device-side loop (a CUDA graph WHILE node) it also decides
 // whether the body runs again
 __global__ void k_fin_x(CgDev* cg, cudaGraphConditionalHandle cond, int set_cond) {
+  DBF_PDL_ENTRY();
   if (threadIdx.x != 0) return;
   cg->xphase = 0;
   if (set_cond) cudaGraphSetConditional(cond, (cg->converged | cg->breakdown) ? 0u : 1u);
@@ -177,12 +182,14 @@ __global__ void k_fin_x(CgDev* cg, cudaGraphConditionalHandle cond, int set_cond
 
 // entry of the device-side loop: run the body only if PCG has not stopped yet
 __global__ void k_loop_cond(const CgDev* cg, cudaGraphConditionalHandle cond) {
+  DBF_PDL_ENTRY();
   if (threadIdx.x == 0) cudaGraphSetConditional(cond, (cg->converged | cg->breakdown) ? 0u : 1u);
 }
 
 // r = b - Ax ; partial <r, r>
 __global__ void __launch_bounds__(BLK, MINB) k_true_residual(SpecGeom g, const cplx* __restrict__ b, const cplx* __restrict__ ax,
                                                        cplx* __restrict__ r, double* partials) {
+  DBF_PDL_ENTRY();
   double acc[1] = {0.0};
   for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < g.Hs; i += (long long)gridDim.x * BLK) {
     Pt p = point(g, i);
@@ -199,6 +206,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_true_residual(SpecGeom g, const c
 }
 
 __global__ void __launch_bounds__(BLK, MINB) k_axpy(SpecGeom g, cplx* __restrict__ y, const cplx* __restrict__ x, double a) {
+  DBF_PDL_ENTRY();
   for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < 3 * g.Hs; i += (long long)gridDim.x * BLK) {
     cplx xv = __ldg(x + i), yv = y[i];
     y[i] = make_double2(fma(a, xv.x, yv.x), fma(a, xv.y, yv.y));
@@ -244,6 +252,7 @@ DBF_DEV double norm9(const double* m) {
 
 // loc = [<r,z>_u, <r,r>_u]
 __global__ void k_fin_init(CgDev* cg, const double* loc) {
+  DBF_PDL_ENTRY();
   if (threadIdx.x != 0) return;
   for (int a = 0; a < 9; ++a) {
     double z = 0.0;
@@ -271,6 +280,7 @@ __global__ void k_fin_init(CgDev* cg, const double* loc) {
 
 // loc = [<p,q>_u, sum sigma(p) (9)]
 __global__ void k_fin_alpha(CgDev* cg, const double* loc) {
+  DBF_PDL_ENTRY();
   if (threadIdx.x != 0) return;
   if (cg->converged | cg->breakdown) return;
   for (int a = 0; a < 9; ++a) cg->dc[a] = loc[1 + a] * cg->inv_n;
@@ -304,6 +314,7 @@ __global__ void k_fin_alpha(CgDev* cg, const double* loc) {
 
 // loc = [<r,z>_u, <r,r>_u]
 __global__ void k_fin_beta(CgDev* cg, const double* loc) {
+  DBF_PDL_ENTRY();
   if (threadIdx.x != 0) return;
   if (cg->converged | cg->breakdown) return;
   double rze = 0.0, ree = 0.0;
@@ -338,6 +349,7 @@ __global__ void k_fin_beta(CgDev* cg, const double* loc) {
 
 // true residual: r = b - Ax already formed.  loc = [<r,r>_u, sum sigma(x) (9)]
 __global__ void k_fin_true(CgDev* cg, const double* loc) {
+  DBF_PDL_ENTRY();
   if (threadIdx.x != 0) return;
   for (int a = 0; a < 9; ++a) cg->dc[a] = loc[1 + a] * cg->inv_n;
   if (cg->sym) sym9(cg->dc);
@@ -357,6 +369,7 @@ __global__ void k_fin_true(CgDev* cg, const double* loc) {
 // loopback all-reduce over P virtual ranks of one process: v[r][off + j] <- op_r v[r][off + j]
 // (v: the slabs' loc buffers, a device array uploaded once at creation)
 __global__ void k_allreduce_lb(double* const* v, int off, int P, int k, int is_max) {
+  DBF_PDL_ENTRY();
   for (int j = threadIdx.x; j < k; j += blockDim.x) {
     double s = v[0][off + j];
     for (int r = 1; r < P; ++r) s = is_max ? fmax(s, v[r][off + j]) : s + v[r][off + j];
@@ -365,6 +378,7 @@ __global__ void k_allreduce_lb(double* const* v, int off, int P, int k, int is_m
 }
 
 __global__ void __launch_bounds__(BLK) k_reduce(const double* partials, int nblk, int nred, double* out, int max_slot) {
+  DBF_PDL_ENTRY();
   __shared__ double s[64];
   cta_reduce(partials, nblk, nred, s, max_slot);
   if (threadIdx.x < nred) out[threadIdx.x] = s[threadIdx.x];
@@ -400,61 +414,47 @@ __global__ void k_fill(double* p, long long n, double v) {
 int cg_blocks() { return nblk(); }
 
 cudaError_t launch_precond(const SpecGeom& g, const PrecQ* q, const cplx* r, cplx* z, cudaStream_t s) {
-  k_precond<<<nblk(), BLK, 0, s>>>(g, q, r, z);
-  return cudaGetLastError();
+  return launch_k(k_precond, nblk(), BLK, 0, s, g, q, r, z);
 }
 cudaError_t launch_cg_init(const SpecGeom& g, const PrecQ* q, const cplx* r, cplx* p, double* partials, int nblk, cudaStream_t s) {
-  k_cg_init<<<nblk, BLK, 0, s>>>(g, q, r, p, partials);
-  return cudaGetLastError();
+  return launch_k(k_cg_init, nblk, BLK, 0, s, g, q, r, p, partials);
 }
 cudaError_t launch_cg_update(const SpecGeom& g, const PrecQ* q, CgDev* cg, cplx* r, const cplx* qv,
                              double* partials, int nblk, cudaStream_t s) {
-  k_cg_update<<<nblk, BLK, 0, s>>>(g, q, cg, r, qv, partials);
-  return cudaGetLastError();
+  return launch_k(k_cg_update, nblk, BLK, 0, s, g, q, cg, r, qv, partials);
 }
 cudaError_t launch_cg_direction(const SpecGeom& g, const PrecQ* q, const CgDev* cg, cplx* x, cplx* p, const cplx* r, cudaStream_t s) {
-  k_cg_direction<<<nblk_dir(), BLK, 0, s>>>(g, q, cg, x, p, r);
-  return cudaGetLastError();
+  return launch_k(k_cg_direction, nblk_dir(), BLK, 0, s, g, q, cg, x, p, r);
 }
 cudaError_t launch_fin_x(CgDev* cg, cudaStream_t s, cudaGraphConditionalHandle cond, int set_cond) {
-  k_fin_x<<<1, 32, 0, s>>>(cg, cond, set_cond);
-  return cudaGetLastError();
+  return launch_k(k_fin_x, 1, 32, 0, s, cg, cond, set_cond);
 }
 cudaError_t launch_loop_cond(const CgDev* cg, cudaGraphConditionalHandle cond, cudaStream_t s) {
-  k_loop_cond<<<1, 32, 0, s>>>(cg, cond);
-  return cudaGetLastError();
+  return launch_k(k_loop_cond, 1, 32, 0, s, cg, cond);
 }
 cudaError_t launch_fin_init(CgDev* cg, const double* loc, cudaStream_t s) {
-  k_fin_init<<<1, 32, 0, s>>>(cg, loc);
-  return cudaGetLastError();
+  return launch_k(k_fin_init, 1, 32, 0, s, cg, loc);
 }
 cudaError_t launch_fin_alpha(CgDev* cg, const double* loc, cudaStream_t s) {
-  k_fin_alpha<<<1, 32, 0, s>>>(cg, loc);
-  return cudaGetLastError();
+  return launch_k(k_fin_alpha, 1, 32, 0, s, cg, loc);
 }
 cudaError_t launch_fin_beta(CgDev* cg, const double* loc, cudaStream_t s) {
-  k_fin_beta<<<1, 32, 0, s>>>(cg, loc);
-  return cudaGetLastError();
+  return launch_k(k_fin_beta, 1, 32, 0, s, cg, loc);
 }
 cudaError_t launch_true_residual(const SpecGeom& g, const cplx* b, const cplx* Ax, cplx* r, double* partials, int nblk, cudaStream_t s) {
-  k_true_residual<<<nblk, BLK, 0, s>>>(g, b, Ax, r, partials);
-  return cudaGetLastError();
+  return launch_k(k_true_residual, nblk, BLK, 0, s, g, b, Ax, r, partials);
 }
 cudaError_t launch_fin_true(CgDev* cg, const double* loc, cudaStream_t s) {
-  k_fin_true<<<1, 32, 0, s>>>(cg, loc);
-  return cudaGetLastError();
+  return launch_k(k_fin_true, 1, 32, 0, s, cg, loc);
 }
 cudaError_t launch_allreduce_lb(double* const* v, int off, int P, int k, int is_max, cudaStream_t s) {
-  k_allreduce_lb<<<1, 64, 0, s>>>(v, off, P, k, is_max);
-  return cudaGetLastError();
+  return launch_k(k_allreduce_lb, 1, 64, 0, s, v, off, P, k, is_max);
 }
 cudaError_t launch_axpy(const SpecGeom& g, cplx* y, const cplx* x, double a, cudaStream_t s) {
-  k_axpy<<<nblk(), BLK, 0, s>>>(g, y, x, a);
-  return cudaGetLastError();
+  return launch_k(k_axpy, nblk(), BLK, 0, s, g, y, x, a);
 }
 cudaError_t launch_reduce(const double* partials, int nblk, int nred, double* out, cudaStream_t s, int max_slot) {
-  k_reduce<<<1, BLK, 0, s>>>(partials, nblk, nred, out, max_slot);
-  return cudaGetLastError();
+  return launch_k(k_reduce, 1, BLK, 0, s, partials, nblk, nred, out, max_slot);
 }
 cudaError_t launch_phase_hist(const uint16_t* ph, long long nvox, double* counts, int nphase, int* bad, cudaStream_t s) {
   k_phase_hist<<<nblk(), BLK, 0, s>>>(ph, nvox, counts, nphase, bad);

@@ -16,6 +16,39 @@
 
 typedef double2 cplx;
 
+// Programmatic dependent launch (PDL, sm_90+): a kernel launched with launch_k() may be scheduled
+// while its stream predecessor drains (launch latency and prologue overlap the predecessor's
+// tail).  Every such kernel starts with DBF_PDL_ENTRY(): it lets its own successor launch early
+// and waits — before touching any global data and in every CTA, so that its completion implies
+// its predecessors' — until the predecessor grid has completed and its writes are visible.
+DBF_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+DBF_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#define DBF_PDL_ENTRY() \
+  do {                  \
+    pdl_trigger();      \
+    pdl_wait();         \
+  } while (0)
+
+bool pdl_enabled();  // DBFFT_PDL=1 (default off, see passes.cu)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  if (!pdl_enabled()) {
+    k<<<grid, block, smem, s>>>(args...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 DBF_DEV cplx cmk(double r, double i) { return make_double2(r, i); }
 DBF_DEV cplx cadd(cplx a, cplx b) { return make_double2(a.x + b.x, a.y + b.y); }
 DBF_DEV cplx csub(cplx a, cplx b) { return make_double2(a.x - b.x, a.y - b.y); }

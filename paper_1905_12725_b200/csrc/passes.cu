@@ -39,6 +39,18 @@ cudaError_t dev_once(DevOnce& o, F init, int* val = nullptr) {
 }
 }  // namespace
 
+// opt-in (DBFFT_PDL=1): measured on B200 (tools/ab_pdl.sh, back to back) it shortened the small
+// solves (c1 0.135 -> 0.133, c2 0.121 -> 0.119 ms per PCG iteration) but slowed c3 (0.419 -> 0.433)
+// and the c4 bench (5.07e9 -> 4.89e9): the early-scheduled dependent CTAs cost more in the
+// predecessor's tail than the launch latency they hide
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DBFFT_PDL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 int num_sms() {
   static DevOnce once;
   int n = 0;
@@ -51,6 +63,18 @@ int num_sms() {
 #endif
 #ifndef DBF_X_P16_256
 #define DBF_X_P16_256 0x11  // pass_X kinds (bit = XKind) that run radix-16 FFTs (16 points per thread) at N1 <= 256
+#endif
+#ifndef DBF_XWS
+#define DBF_XWS 0  // 1: warp-specialised pass_X for the neo-Hookean apply kind at N1 = 256
+#endif
+#ifndef DBF_XWS_NV
+#define DBF_XWS_NV 2  // its voxel warps per CTA
+#endif
+#ifndef DBF_XWS_MINB
+#define DBF_XWS_MINB 3
+#endif
+#ifndef DBF_XWS_MAXREG
+#define DBF_XWS_MAXREG 0  // > 0: register cap instead of the CTAs-per-SM bound
 #endif
 #ifndef DBF_X_MINB_J2P16
 #define DBF_X_MINB_J2P16 3  // CTAs per SM of the radix-16 J2 apply kind
@@ -352,6 +376,7 @@ struct ColPref {
 
 template <int N, int KIND>
 __global__ void __launch_bounds__(256, ColCfg<N>::ODD ? 1 : ColPref<KIND>::MINB) col_pass_kernel(ColGeom g) {
+  DBF_PDL_ENTRY();
   if (g.cg_stop0 && (*g.cg_stop0 | *g.cg_stop1)) return;  // PCG stopped: nothing to compute
   typedef ColOp<KIND> Op;
   typedef ColCfg<N> CF;
@@ -926,6 +951,9 @@ DBF_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try(bar, parity)) {
   }
 }
+DBF_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 DBF_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
@@ -984,6 +1012,7 @@ DBF_DEV void x_issue_tan(const XGeom& g, long long grp, double* st_tan, uint16_t
 // bulk async copies (cp.async.bulk -> TMA engine, mbarrier completion) while group i computes.
 template <int N1, int KIND>
 __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB) x_pass_kernel(XGeom g, int nf_real) {
+  DBF_PDL_ENTRY();
   if (g.stop0 && (*g.stop0 | *g.stop1)) return;  // PCG stopped: nothing to compute
   typedef XCfg<N1, KIND> CF;
   typedef XTraits<KIND> T;
@@ -1285,6 +1314,193 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
   }
 }
 
+
+// ------------------------------------------------------------------------------------------------
+// Warp-specialised pass_X (neo-Hookean apply kind, N1 = 256: one warp per field-pair FFT job).
+// NFW = 5 FFT warps and NVW voxel warps per CTA, one line at a time, two slot buffers: while the
+// voxel warps contract line i in buffer i&1, the FFT warps C2R line i+1 into the other buffer and
+// then R2C line i once the voxel warps signal it — the hand-offs are mbarriers (FULL[b]: C2R done,
+// DONE[b]: voxel op done), so neither role waits at a CTA barrier (the line-group design stalls
+// ~20 % of its samples after its two __syncthreads per line).  The input spectra of the next line
+// are bulk-copied into one stage buffer right after the FFT warps have read the current one (a
+// named barrier of the FFT warps only); per-voxel tangent rows are L2-prefetched one line ahead.
+// ------------------------------------------------------------------------------------------------
+template <int N1>
+struct XwsCfg {
+  typedef XCfg<N1, X_K_FIN_NH> CF;
+  static constexpr int NFW = CF::NP;  // pair jobs of a line (TPJ = 32: one warp each)
+  static constexpr int NVW = DBF_XWS_NV;
+  static constexpr int THREADS = (NFW + NVW) * 32;
+  static constexpr int CS = CF::CS, N1H = CF::N1H;
+  static constexpr size_t SLOTS = sizeof(double) * 2 * CS * N1;
+  static constexpr size_t ST_IN = sizeof(cplx) * 9 * N1H;
+  static constexpr size_t SMEM = SLOTS + ST_IN + sizeof(cplx) * N1 + 8 * sizeof(uint64_t);
+  static_assert(CF::TPJ == 32 && CF::LPAR == 1 && CF::ILV && CF::TAB, "warp-specialised pass_X: N1 = 256 layout");
+};
+
+template <int N1>
+#if DBF_XWS_MAXREG > 0
+__global__ void __maxnreg__(DBF_XWS_MAXREG) x_pass_ws_kernel(XGeom g) {
+#else
+__global__ void __launch_bounds__(XwsCfg<N1>::THREADS, DBF_XWS_MINB) x_pass_ws_kernel(XGeom g) {
+#endif
+  if (g.stop0 && (*g.stop0 | *g.stop1)) return;  // PCG stopped: nothing to compute
+  constexpr int KIND = X_K_FIN_NH;
+  typedef XwsCfg<N1> W;
+  typedef typename W::CF CF;
+  constexpr int CS = W::CS, PX = CF::PX, TPJ = CF::TPJ, NFW = W::NFW, NVW = W::NVW;
+  extern __shared__ __align__(16) double real[];
+  unsigned char* sb = reinterpret_cast<unsigned char*>(real);
+  cplx* st_in = reinterpret_cast<cplx*>(sb + W::SLOTS);
+  cplx* stab = reinterpret_cast<cplx*>(sb + W::SLOTS + W::ST_IN);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sb + W::SLOTS + W::ST_IN + sizeof(cplx) * N1);
+  uint64_t* bstage = bars;      // input stage filled
+  uint64_t* bfull = bars + 1;   // [2] C2R of the buffer's line done (NFW arrivals)
+  uint64_t* bdone = bars + 3;   // [2] voxel op of the buffer's line done (NVW arrivals)
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  __shared__ double s_dc[10];
+  __shared__ double s_e[9];
+  for (int i = t; i < N1 - 1; i += W::THREADS) stab[i] = __ldg(g.tw + N1 + i);
+  if (t < 10) s_dc[t] = 0.0;
+  if (g.e && t < 9) s_e[t] = g.e[t];
+  const long long nmine = (g.nlines > (long long)blockIdx.x) ? (g.nlines - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (t == 0) {
+    mbar_init(bstage, 1);
+    mbar_init(&bfull[0], NFW);
+    mbar_init(&bfull[1], NFW);
+    mbar_init(&bdone[0], NVW);
+    mbar_init(&bdone[1], NVW);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (t == 0 && nmine > 0) x_issue_in<N1, KIND>(g, blockIdx.x, st_in, bstage);
+  double xdot = 0.0;
+  double red[10];
+#pragma unroll
+  for (int r = 0; r < 10; ++r) red[r] = 0.0;
+
+  if (warp < NFW) {
+    // ------------------------------------------------------------------ FFT warps
+    const int job = warp, gq = lane;
+    const int fa = 2 * job, fb = 2 * job + 1;
+    const int jbase = (fa * N1) / 2;
+    auto c2r = [&](long long i) {  // line i of this CTA -> buffer i & 1
+      const long long line = blockIdx.x + i * gridDim.x;
+      cplx* cx = reinterpret_cast<cplx*>(real + (i & 1) * CS * N1);
+      mbar_wait(bstage, (uint32_t)(i & 1));
+      cplx a[PX];
+#pragma unroll
+      for (int s = 0; s < PX; ++s) {
+        const int k = gq + s * TPJ;
+        const bool lo = x_lo<N1, PX, TPJ>(s, gq);
+        const int kk = lo ? k : N1 - k;
+        cplx A = st_in[fa * W::N1H + kk];
+        cplx B = (fb < 9) ? st_in[fb * W::N1H + kk] : make_double2(0, 0);
+        if (kk == 0 || 2 * kk == N1) { A.y = 0.0; B.y = 0.0; }
+        a[s] = lo ? make_double2(A.x - B.y, A.y + B.x) : make_double2(A.x + B.y, B.x - A.y);
+      }
+      // every FFT warp has its inputs in registers: the stage takes the next line's spectra now
+      asm volatile("bar.sync 1, %0;" ::"n"(NFW * 32) : "memory");
+      if (t == 0 && i + 1 < nmine) {
+        fence_proxy_async();
+        x_issue_in<N1, KIND>(g, line + gridDim.x, st_in, bstage);
+      }
+      x_fft<N1, PX, true, true>(a, cx, gq, jbase, stab, job);
+      __syncwarp();
+#pragma unroll
+      for (int s = 0; s < PX; ++s) cx[jbase + gq + s * TPJ] = a[s];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bfull[i & 1]);
+    };
+    auto r2c = [&](long long i) {
+      const long long line = blockIdx.x + i * gridDim.x;
+      cplx* cx = reinterpret_cast<cplx*>(real + (i & 1) * CS * N1);
+      mbar_wait(&bdone[i & 1], (uint32_t)((i >> 1) & 1));
+      cplx a[PX];
+#pragma unroll
+      for (int s = 0; s < PX; ++s) {
+        const cplx v2 = cx[jbase + gq + s * TPJ];
+        a[s] = make_double2(v2.x, fb < 9 ? v2.y : 0.0);
+      }
+      x_fft<N1, PX, false, true>(a, cx, gq, jbase, stab, job);
+      cplx zn[PX];
+      x_partner<TPJ>(a, zn, gq);
+#pragma unroll
+      for (int s = 0; s < PX; ++s) {
+        const int k = gq + s * TPJ;
+        if (!x_lo<N1, PX, TPJ>(s, gq)) continue;
+        const cplx Z = a[s], Zn = zn[s];
+        const cplx A = make_double2(Z.x + Zn.x, Z.y - Zn.y);
+        const cplx B = make_double2(Z.y + Zn.y, Zn.x - Z.x);
+        if (s == 0 && gq == 0) {  // k = 0: the line sums of the pair (<dP>)
+          const double dcs = 0.5 / g.oscale;
+          s_dc[fa] += dcs * A.x;
+          if (fb < 9) s_dc[fb] += dcs * B.x;
+        }
+        const long long ko = x_koff(g, k, g.kpcs_out);
+        g.out[fa * g.fs_out + line * g.kxp + ko] = A;
+        if (fb < 9) g.out[fb * g.fs_out + line * g.kxp + ko] = B;
+        if (g.kch > 0 && 2 * k == N1)
+          for (int c = 0; c + 1 < g.npy; ++c) {
+            g.out[c * g.kpcs_out + fa * g.fs_out + line * g.kxp + g.kch] = make_double2(0.0, 0.0);
+            if (fb < 9) g.out[c * g.kpcs_out + fb * g.fs_out + line * g.kxp + g.kch] = make_double2(0.0, 0.0);
+          }
+      }
+      __syncwarp();  // the job's slots are read (exchange + untangle) before the next C2R writes them
+    };
+    if (nmine > 0) c2r(0);
+    for (long long i = 0; i < nmine; ++i) {
+      if (i + 1 < nmine) c2r(i + 1);
+      r2c(i);
+    }
+  } else {
+    // ------------------------------------------------------------------ voxel warps
+    const int vt = t - NFW * 32;
+    for (long long i = 0; i < nmine; ++i) {
+      const long long line = blockIdx.x + i * gridDim.x;
+      if (vt == 0 && i + 1 < nmine) {  // the next line's tangent rows and phase ids -> L2
+        const long long v1 = (line + gridDim.x) * N1;
+#pragma unroll 1
+        for (int k = 0; k < 10; ++k) prefetch_l2(g.tan + (long long)k * g.nvox + v1, sizeof(double) * N1);
+        prefetch_l2(g.phase + v1, sizeof(uint16_t) * N1);
+      }
+      const cplx* cx = reinterpret_cast<const cplx*>(real + (i & 1) * CS * N1);
+      double* rw = real + (i & 1) * CS * N1;
+      mbar_wait(&bfull[i & 1], (uint32_t)((i >> 1) & 1));
+      for (int x = vt; x < N1; x += NVW * 32) {
+        double G[CS], P[CS];
+#pragma unroll
+        for (int q = 0; q < CS / 2; ++q) {
+          const cplx v2 = cx[q * N1 + x];
+          G[2 * q] = v2.x;
+          G[2 * q + 1] = (2 * q + 1 < 9) ? v2.y : 0.0;
+        }
+        const long long v = line * N1 + x;
+        const int ph = (int)__ldg(g.phase + v);
+        x_voxel<KIND>(g, v, G, P, red, g.tan + v, g.nvox, ph, xdot, g.e ? s_e : nullptr);
+#pragma unroll
+        for (int q = 0; q < CS / 2; ++q)
+          reinterpret_cast<cplx*>(rw)[q * N1 + x] = make_double2(P[2 * q], 2 * q + 1 < 9 ? P[2 * q + 1] : 0.0);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bdone[i & 1]);
+    }
+  }
+  // block reductions in a fixed order (deterministic)
+  __shared__ double sred[W::THREADS / 32];
+  __syncthreads();
+  double v = warp_sum(xdot);
+  if (lane == 0) sred[warp] = v;
+  __syncthreads();
+  if (t < 9) {
+    g.partials[(long long)blockIdx.x * g.nred + t] = s_dc[t];
+  } else if (t == 9) {
+    double s = 0.0;
+    for (int w = 0; w < W::THREADS / 32; ++w) s += sred[w];
+    g.partials[(long long)blockIdx.x * g.nred + 9] = s / g.oscale;  // FIN_NH summed the 1/(2N)-scaled P
+  }
+}
+
 // mean tangent from the stored per-voxel tangent -> partials[block][nk]
 template <int MODE>  // 0: full 45 (finite), 1: compact NH (finite, 45 out), 2: compact J2 (21 out)
 __global__ void __launch_bounds__(256) k_mean_tangent(XGeom g, double* partials) {
@@ -1514,9 +1730,6 @@ DBF_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "mem
 template <int K>
 DBF_DEV void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(K) : "memory"); }
 DBF_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-DBF_DEV void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 DBF_DEV void cons_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 struct TmaMaps {
@@ -1525,6 +1738,7 @@ struct TmaMaps {
 
 template <int N, int KIND, bool DOT, int R, bool UPD = false>
 __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __grid_constant__ TmaMaps maps, ColGeom g, ColTiles tl) {
+  DBF_PDL_ENTRY();
   typedef ColOp<KIND> Op;
   typedef TmaCfg<N> CF;
   constexpr bool TAB = ColTab<N, KIND>::value && (!UPD || DBF_UPD_TAB);
@@ -1759,8 +1973,7 @@ static cudaError_t launch_col_k(const ColGeom& g, cudaStream_t s) {
     return cudaFuncSetAttribute(col_pass_kernel<N, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   });
   if (e != cudaSuccess) return e;
-  col_pass_kernel<N, KIND><<<col_grid(N, g.ncols), ColCfg<N>::THREADS, smem, s>>>(g);
-  return cudaGetLastError();
+  return launch_k(col_pass_kernel<N, KIND>, col_grid(N, g.ncols), ColCfg<N>::THREADS, smem, s, g);
 }
 
 template <int N>
@@ -1900,8 +2113,7 @@ static cudaError_t launch_col_tma_k(const TmaMaps& maps, const ColGeom& g, const
   if (e != cudaSuccess) return e;
   const int grid = std::min(tl.n_tiles, num_sms());
   if (grid_out) *grid_out = grid;
-  col_tma_kernel<N, KIND, DOT, R, UPD><<<grid, TmaCfg<N>::THREADS, smem, s>>>(maps, g, tl);
-  return cudaGetLastError();
+  return launch_k(col_tma_kernel<N, KIND, DOT, R, UPD>, grid, TmaCfg<N>::THREADS, smem, s, maps, g, tl);
 }
 
 // returns cudaErrorNotSupported when this geometry must take the register-pipelined kernel
@@ -2001,8 +2213,7 @@ static cudaError_t launch_x_k(const XGeom& g, cudaStream_t s, int* grid_out, int
   // never more CTAs than partial slots were allocated for (x_grid)
   const int grid = (int)std::min<long long>(std::min<long long>(ngroups, max_grid), x_grid(KIND, N1, g.nlines));
   if (grid_out) *grid_out = grid;
-  x_pass_kernel<N1, KIND><<<grid, CF::THREADS, CF::SMEM, s>>>(g, nf_real);
-  return cudaGetLastError();
+  return launch_k(x_pass_kernel<N1, KIND>, grid, CF::THREADS, CF::SMEM, s, g, nf_real);
 }
 
 template <int N1>
@@ -2023,7 +2234,31 @@ static cudaError_t launch_x_n(int kind, const XGeom& g, cudaStream_t s, int* gri
 }
 
 // kind X_REAL_OUT + nf selects a real-output transform of nf fields (1..9)
+template <int N1>
+static cudaError_t launch_x_ws(const XGeom& g, cudaStream_t s, int* grid_out) {
+  typedef XwsCfg<N1> W;
+  static DevOnce once;
+  int max_grid = 0;
+  cudaError_t e = dev_once(
+      once,
+      [](int& mg) {
+        cudaError_t e2 = cudaFuncSetAttribute(x_pass_ws_kernel<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W::SMEM);
+        if (e2 != cudaSuccess) return e2;
+        int nb = 0;
+        e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, x_pass_ws_kernel<N1>, W::THREADS, W::SMEM);
+        mg = std::max(1, nb) * num_sms();
+        return e2;
+      },
+      &max_grid);
+  if (e != cudaSuccess) return e;
+  const int grid = (int)std::min<long long>(std::min<long long>(g.nlines, max_grid), x_grid(X_K_FIN_NH, N1, g.nlines));
+  if (grid_out) *grid_out = grid;
+  x_pass_ws_kernel<N1><<<grid, W::THREADS, W::SMEM, s>>>(g);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_x(int kind, int N1, const XGeom& g, cudaStream_t s, int* grid_out) {
+  if (DBF_XWS && kind == X_K_FIN_NH && N1 == 256 && g.in && g.out) return launch_x_ws<256>(g, s, grid_out);
   switch (N1) {
     case 8: return launch_x_n<8>(kind, g, s, grid_out);
     case 16: return launch_x_n<16>(kind, g, s, grid_out);
