@@ -41,7 +41,9 @@ H = (n // 2 + 1) * n * n
 N = n ** 3
 c = 9 if kin == "finite" else 6
 fields = {"pass_I1": 3 + 6, "pass_I2": 6 + c, "pass_X": 2 * c, "pass_F2": c + 6, "pass_F3": 6 + 3}
-mat = 82 * N if kin == "finite" else 2 * N
+# per-voxel material bytes: compact neo-Hookean (F^-1, c1) + phase id; J2 compact tangent (theta,
+# thetabar, n) + phase id; linear: phase id only
+mat = 82 * N if kin == "finite" else 66 * N if kin == "j2" else 2 * N
 res = {}
 for k, (ms, cnt) in prof.items():
     if cnt == 0:
