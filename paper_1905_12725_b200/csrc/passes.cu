@@ -85,6 +85,10 @@ int num_sms() {
 #ifndef DBF_X_LRAW
 #define DBF_X_LRAW 192  // target threads per pass_X CTA (lines per CTA = DBF_X_LRAW / threads per line)
 #endif
+#ifndef DBF_X_LRAW16
+#define DBF_X_LRAW16 96  // the radix-16 kinds: 2 lines (96 threads) per CTA, ~50 KB shared memory, 4 CTAs/SM
+                         // (256^3 small 0.618 -> 0.550 ms, 128^3 0.098 -> 0.084 against 4 lines / 192)
+#endif
 #ifndef DBF_X_LRAW9
 #define DBF_X_LRAW9 DBF_X_LRAW  // the same for the 9-field (finite-strain) kinds
 #endif
@@ -886,7 +890,7 @@ struct XCfg {
   static constexpr int NP = CS / 2;
   static constexpr int PERLINE = TPJ * NP;
   // PACK: 64/TPJ lines (at least 2) so that the CTA is whole warps (the untangle shuffles)
-  static constexpr int LRAW = PACK ? (TPJ >= 32 ? 2 : 64 / TPJ) : (C == 9 ? DBF_X_LRAW9 : DBF_X_LRAW) / PERLINE;
+  static constexpr int LRAW = PACK ? (TPJ >= 32 ? 2 : 64 / TPJ) : (C == 9 ? DBF_X_LRAW9 : P16 ? DBF_X_LRAW16 : DBF_X_LRAW) / PERLINE;
   static constexpr int LPAR = LRAW >= 64 ? 64 : LRAW >= 32 ? 32 : LRAW >= 16 ? 16 : LRAW >= 8 ? 8 : LRAW >= 4 ? 4 : LRAW >= 2 ? 2 : 1;
   static constexpr int NJOB = PACK ? LPAR * C / 2 : LPAR * NP;  // pair FFT jobs per line group
   static constexpr int THREADS = NJOB * TPJ;
@@ -2009,6 +2013,10 @@ static cudaError_t launch_col_n(int kind, const ColGeom& g, cudaStream_t s) {
 #ifndef DBF_RING2_SMALL
 #define DBF_RING2_SMALL 0  // 2-deep ring for the small-strain I1 / F2 too (slower: 256^3 I1S 0.319 -> 0.381 ms)
 #endif
+#ifndef DBF_RING2_FIN
+#define DBF_RING2_FIN 1  // 2-deep ring for the finite-strain I1 (F2F went back to 3 with the 128-byte
+                         // pitch: 256^3 0.447 -> 0.433 ms; I1F 0.257 with 2 vs 0.271 with 3)
+#endif
 #ifndef DBF_REG512_MASK
 #define DBF_REG512_MASK 0  // bit k: column kind k at N = 512 takes the register-pipelined kernel
 #endif
@@ -2085,10 +2093,10 @@ static int col_prog_span(const TProg& p) {
 template <int KIND, bool DOT>
 struct ColRing {  // ring depth: 3 slots; small-strain F3 (two-term outputs from 6 inputs) takes 4
   // (B200: 512^3 3.35 -> 3.26 ms, 256^3 0.400 -> 0.392 ms; R = 4 everywhere was slower overall);
-  // the finite-strain I1 and F2 run faster with 2 (256^3: I1 0.319 -> 0.300 ms, F2 0.530 -> 0.522;
-  // I2 was slower with 2)
+  // the finite-strain I1 runs faster with 2 (256^3: 0.319 -> 0.300 ms; I2 was slower with 2, and F2
+  // too once the intermediate rows were 128-byte aligned)
   static constexpr int R = (KIND == COL_F3S) ? 4
-                           : (KIND == COL_I1F || KIND == COL_F2F || (DBF_RING2_SMALL && (KIND == COL_I1S || KIND == COL_F2S))) ? 2
+                           : ((DBF_RING2_FIN && KIND == COL_I1F) || (DBF_RING2_SMALL && (KIND == COL_I1S || KIND == COL_F2S))) ? 2
                            : DBF_COL_R;
 };
 // ring depth of a launch: the fused F3 + residual update (3 staging buffers) takes 2 slots — its
