@@ -85,6 +85,12 @@ int num_sms() {
 #ifndef DBF_X_LRAW
 #define DBF_X_LRAW 192  // target threads per pass_X CTA (lines per CTA = DBF_X_LRAW / threads per line)
 #endif
+#ifndef DBF_X_LRAWJ2
+#define DBF_X_LRAWJ2 DBF_X_LRAW  // the J2 apply kind
+#endif
+#ifndef DBF_X_MINB_NOTAN_J2
+#define DBF_X_MINB_NOTAN_J2 DBF_X_MINB_NOTAN
+#endif
 #ifndef DBF_X_LRAW16
 #define DBF_X_LRAW16 96  // the radix-16 kinds: 2 lines (96 threads) per CTA, ~50 KB shared memory, 4 CTAs/SM
                          // (256^3 small 0.618 -> 0.550 ms, 128^3 0.098 -> 0.084 against 4 lines / 192)
@@ -890,7 +896,7 @@ struct XCfg {
   static constexpr int NP = CS / 2;
   static constexpr int PERLINE = TPJ * NP;
   // PACK: 64/TPJ lines (at least 2) so that the CTA is whole warps (the untangle shuffles)
-  static constexpr int LRAW = PACK ? (TPJ >= 32 ? 2 : 64 / TPJ) : (C == 9 ? DBF_X_LRAW9 : P16 ? DBF_X_LRAW16 : DBF_X_LRAW) / PERLINE;
+  static constexpr int LRAW = PACK ? (TPJ >= 32 ? 2 : 64 / TPJ) : (C == 9 ? DBF_X_LRAW9 : P16 ? DBF_X_LRAW16 : KIND == X_K_J2 ? DBF_X_LRAWJ2 : DBF_X_LRAW) / PERLINE;
   static constexpr int LPAR = LRAW >= 64 ? 64 : LRAW >= 32 ? 32 : LRAW >= 16 ? 16 : LRAW >= 8 ? 8 : LRAW >= 4 ? 4 : LRAW >= 2 ? 2 : 1;
   static constexpr int NJOB = PACK ? LPAR * C / 2 : LPAR * NP;  // pair FFT jobs per line group
   static constexpr int THREADS = NJOB * TPJ;
@@ -919,8 +925,8 @@ struct XCfg {
   static constexpr int MINB = PACK ? (THREADS <= 160 ? DBF_X_MINB_NOTAN : THREADS <= 320 ? 2 : 1)
                                : (THREADS > 256) ? 2
                                : (KIND == X_K_J2 && P16) ? DBF_X_MINB_J2P16
-                               : ((KIND == X_K_J2 && !DBF_X_STAGE_TAN_J2) || (KIND == X_K_FIN_NH && !DBF_X_STAGE_TAN_NH))
-                                   ? DBF_X_MINB_NOTAN
+                               : (KIND == X_K_J2 && !DBF_X_STAGE_TAN_J2) ? DBF_X_MINB_NOTAN_J2
+                               : (KIND == X_K_FIN_NH && !DBF_X_STAGE_TAN_NH) ? DBF_X_MINB_NOTAN
                                : (KIND == X_CONST_FIN || KIND == X_CONST_J2) ? DBF_X_MINB_CONST
                                : (THREADS <= 192) ? DBF_X_MINB : 2;
 };
