@@ -121,6 +121,9 @@ int num_sms() {
 #ifndef DBF_X_PREFETCH
 #define DBF_X_PREFETCH 1  // pass_X: bulk L2 prefetch of the next line group's per-voxel tangent rows
 #endif
+#ifndef DBF_X_TBATCH
+#define DBF_X_TBATCH 0  // neo-Hookean apply: both voxels' tangent rows loaded before either contraction
+#endif
 #ifndef DBF_X_TPIPE
 #define DBF_X_TPIPE 0  // 1: software-pipelined tangent loads across voxels (spilled: 256^3 0.911 -> 1.015 ms)
 #endif
@@ -1166,6 +1169,39 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
       else mbar_wait(&bars[1], it & 1);
     }
     // neo-Hookean apply: the next voxel's tangent row is loaded while this voxel computes
+    // TBATCH (neo-Hookean apply, at most 2 voxels per thread and group): the tangent rows of both of
+    // the thread's voxels are loaded before either is contracted, so their L2 latencies overlap
+    constexpr bool TBATCH = DBF_X_TBATCH && KIND == X_K_FIN_NH && S::NTAN == 0 && LPAR * N1 <= 2 * CF::THREADS;
+    if constexpr (TBATCH) {
+      double tq[2][10];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int vv = t + r * CF::THREADS;
+        const long long v = (grp * LPAR) * N1 + vv;
+        if (vv < LPAR * N1 && v < g.nvox)
+#pragma unroll
+          for (int k = 0; k < 10; ++k) tq[r][k] = __ldg(g.tan + (long long)k * g.nvox + v);
+      }
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int vv = t + r * CF::THREADS;
+        const int l2 = vv / N1, x = vv % N1;
+        const long long ln = grp * LPAR + l2;
+        if (vv >= LPAR * N1 || ln >= g.nlines) continue;
+        double G[CS], P[CS];
+#pragma unroll
+        for (int q = 0; q < CS / 2; ++q) {
+          const cplx v2 = cx[(l2 * (CS / 2) + q) * N1 + x];
+          G[2 * q] = v2.x;
+          G[2 * q + 1] = (2 * q + 1 < T::CIN) ? v2.y : 0.0;
+        }
+        const long long v = ln * N1 + x;
+        x_voxel<KIND>(g, v, G, P, red, nullptr, 0, S::PH ? (int)ph_cur[vv] : (int)__ldg(g.phase + v), xdot, g.e ? s_e : nullptr, tq[r]);
+#pragma unroll
+        for (int q = 0; q < CS / 2; ++q)
+          if (2 * q < T::COUT) cx[(l2 * (CS / 2) + q) * N1 + x] = make_double2(P[2 * q], 2 * q + 1 < T::COUT ? P[2 * q + 1] : 0.0);
+      }
+    }
     constexpr bool TPIPE = DBF_X_TPIPE && KIND == X_K_FIN_NH && S::NTAN == 0;
     double tnext[TPIPE ? 10 : 1];
     if (TPIPE && t < LPAR * N1) {
@@ -1174,7 +1210,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
 #pragma unroll
         for (int k = 0; k < 10; ++k) tnext[TPIPE ? k : 0] = __ldg(g.tan + (long long)k * g.nvox + v0);
     }
-    for (int vv = t; KIND != X_REAL_IN && vv < LPAR * N1; vv += CF::THREADS) {
+    for (int vv = t; KIND != X_REAL_IN && !TBATCH && vv < LPAR * N1; vv += CF::THREADS) {
       const int l2 = vv / N1, x = vv % N1;
       const long long ln = grp * LPAR + l2;
       if (ln >= g.nlines) continue;
