@@ -215,24 +215,30 @@ __global__ void __launch_bounds__(BLK, MINB) k_axpy(SpecGeom g, cplx* __restrict
 
 // ---- single-CTA finalizers ---------------------------------------------------------------------
 // sum partials[j*nred + k] over j for k < nred into out[k] (slot max_slot, if >= 0, is a max)
+// out[k] = sum (or max, k = max_slot) over the nblk CTA partials of slot k (nred <= 64), in a fixed
+// order: thread-strided partial sums, warp shuffles, then the 8 warp results — one CTA barrier for
+// all slots (a tree of 8 barriers per slot took ~10 us for the 10 slots of the x pass)
 DBF_DEV void cta_reduce(const double* partials, int nblk, int nred, double* out, int max_slot) {
-  __shared__ double red[BLK];
+  __shared__ double red[BLK / 32][64];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int k = 0; k < nred; ++k) {
     const bool is_max = (k == max_slot);
     double s = 0.0;
     for (int j = threadIdx.x; j < nblk; j += BLK) {
-      double v = partials[(long long)j * nred + k];
+      const double v = partials[(long long)j * nred + k];
       s = is_max ? fmax(s, v) : s + v;
     }
-    red[threadIdx.x] = s;
-    __syncthreads();
-    for (int w = BLK / 2; w > 0; w >>= 1) {
-      if (threadIdx.x < w) red[threadIdx.x] = is_max ? fmax(red[threadIdx.x], red[threadIdx.x + w]) : red[threadIdx.x] + red[threadIdx.x + w];
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) out[k] = red[0];
-    __syncthreads();
+    s = is_max ? warp_max(s) : warp_sum(s);
+    if (lane == 0) red[w][k] = s;
   }
+  __syncthreads();
+  if (threadIdx.x < nred) {
+    const bool is_max = ((int)threadIdx.x == max_slot);
+    double s = 0.0;
+    for (int q = 0; q < BLK / 32; ++q) s = is_max ? fmax(s, red[q][threadIdx.x]) : s + red[q][threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+  __syncthreads();
 }
 
 DBF_DEV void sym9(double* m) {  // small strain: only 6 Voigt slots were accumulated
@@ -279,9 +285,7 @@ __global__ void k_fin_init(CgDev* cg, const double* loc) {
 }
 
 // loc = [<p,q>_u, sum sigma(p) (9)]
-__global__ void k_fin_alpha(CgDev* cg, const double* loc) {
-  DBF_PDL_ENTRY();
-  if (threadIdx.x != 0) return;
+DBF_DEV void fin_alpha_dev(CgDev* cg, const double* loc) {
   if (cg->converged | cg->breakdown) return;
   for (int a = 0; a < 9; ++a) cg->dc[a] = loc[1 + a] * cg->inv_n;
   if (cg->sym) sym9(cg->dc);
@@ -311,11 +315,13 @@ __global__ void k_fin_alpha(CgDev* cg, const double* loc) {
     cg->ze[a] = z;
   }
 }
+__global__ void k_fin_alpha(CgDev* cg, const double* loc) {
+  DBF_PDL_ENTRY();
+  if (threadIdx.x == 0) fin_alpha_dev(cg, loc);
+}
 
 // loc = [<r,z>_u, <r,r>_u]
-__global__ void k_fin_beta(CgDev* cg, const double* loc) {
-  DBF_PDL_ENTRY();
-  if (threadIdx.x != 0) return;
+DBF_DEV void fin_beta_dev(CgDev* cg, const double* loc) {
   if (cg->converged | cg->breakdown) return;
   double rze = 0.0, ree = 0.0;
   for (int a = 0; a < 9; ++a) {
@@ -345,6 +351,10 @@ __global__ void k_fin_beta(CgDev* cg, const double* loc) {
   cg->rz = rz_new;
   for (int a = 0; a < 9; ++a) cg->pe[a] = cg->ze[a] + beta * cg->pe[a];
   if (cg->iters >= cg->max_iter) cg->converged = 2;  // exhausted
+}
+__global__ void k_fin_beta(CgDev* cg, const double* loc) {
+  DBF_PDL_ENTRY();
+  if (threadIdx.x == 0) fin_beta_dev(cg, loc);
 }
 
 // true residual: r = b - Ax already formed.  loc = [<r,r>_u, sum sigma(x) (9)]
@@ -382,6 +392,23 @@ __global__ void __launch_bounds__(BLK) k_reduce(const double* partials, int nblk
   __shared__ double s[64];
   cta_reduce(partials, nblk, nred, s, max_slot);
   if (threadIdx.x < nred) out[threadIdx.x] = s[threadIdx.x];
+}
+// one rank: the CTA reduction and the finalizer that consumes it in one launch (loc as for the pair)
+__global__ void __launch_bounds__(BLK) k_reduce_alpha(const double* partials, int nblk, double* loc, CgDev* cg) {
+  DBF_PDL_ENTRY();
+  __shared__ double s[64];
+  cta_reduce(partials, nblk, 10, s, -1);
+  if (threadIdx.x < 10) loc[1 + threadIdx.x] = s[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x == 0) fin_alpha_dev(cg, loc);
+}
+__global__ void __launch_bounds__(BLK) k_reduce_beta(const double* partials, int nblk, double* loc, CgDev* cg) {
+  DBF_PDL_ENTRY();
+  __shared__ double s[64];
+  cta_reduce(partials, nblk, 2, s, -1);
+  if (threadIdx.x < 2) loc[threadIdx.x] = s[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x == 0) fin_beta_dev(cg, loc);
 }
 
 // phase counts: per-CTA shared-memory histogram (integer atomics), one global add per phase and
@@ -452,6 +479,12 @@ cudaError_t launch_allreduce_lb(double* const* v, int off, int P, int k, int is_
 }
 cudaError_t launch_axpy(const SpecGeom& g, cplx* y, const cplx* x, double a, cudaStream_t s) {
   return launch_k(k_axpy, nblk(), BLK, 0, s, g, y, x, a);
+}
+cudaError_t launch_reduce_alpha(const double* partials, int nblk, double* loc, CgDev* cg, cudaStream_t s) {
+  return launch_k(k_reduce_alpha, 1, BLK, 0, s, partials, nblk, loc, cg);
+}
+cudaError_t launch_reduce_beta(const double* partials, int nblk, double* loc, CgDev* cg, cudaStream_t s) {
+  return launch_k(k_reduce_beta, 1, BLK, 0, s, partials, nblk, loc, cg);
 }
 cudaError_t launch_reduce(const double* partials, int nblk, int nred, double* out, cudaStream_t s, int max_slot) {
   return launch_k(k_reduce, 1, BLK, 0, s, partials, nblk, nred, out, max_slot);

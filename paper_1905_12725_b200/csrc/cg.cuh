@@ -46,6 +46,9 @@ cudaError_t launch_loop_cond(const CgDev* cg, cudaGraphConditionalHandle cond, c
 cudaError_t launch_fin_init(CgDev* cg, const double* loc, cudaStream_t s);
 cudaError_t launch_fin_alpha(CgDev* cg, const double* loc, cudaStream_t s);
 cudaError_t launch_fin_beta(CgDev* cg, const double* loc, cudaStream_t s);
+// one rank: CTA partials -> loc (x-pass slots 1..10 / CG slots 0..1) and the finalizer in one launch
+cudaError_t launch_reduce_alpha(const double* partials, int nblk, double* loc, CgDev* cg, cudaStream_t s);
+cudaError_t launch_reduce_beta(const double* partials, int nblk, double* loc, CgDev* cg, cudaStream_t s);
 cudaError_t launch_true_residual(const SpecGeom& g, const cplx* b, const cplx* Ax, cplx* r, double* partials, int nblk, cudaStream_t s);
 cudaError_t launch_fin_true(CgDev* cg, const double* loc, cudaStream_t s);
 cudaError_t launch_allreduce_lb(double* const* v, int off, int P, int k, int is_max, cudaStream_t s);

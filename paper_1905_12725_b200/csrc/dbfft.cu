@@ -1234,6 +1234,28 @@ bool pcg_fused(dbfft_ctx ctx) {
   return true;
 }
 
+// CTA partials of the x pass (alpha: slots 1..10 of loc) or of the residual update (beta: slots
+// 0..1) -> loc, all-reduce over ranks, finalizer.  One rank: reduction and finalizer in one launch.
+dbfft_status reduce_fin(dbfft_ctx ctx, const std::vector<int>& nblk, bool alpha) {
+  if (ctx->P == 1) {
+    Slab& s = ctx->slabs[0];
+    ProfScope ps(ctx, PK_FIN);
+    CK(alpha ? launch_reduce_alpha(s.part_x, nblk[0], s.loc, s.cg, ctx->stream)
+             : launch_reduce_beta(s.part_cg, nblk[0], s.loc, s.cg, ctx->stream));
+    return DBFFT_OK;
+  }
+  for (size_t j = 0; j < ctx->slabs.size(); ++j) {
+    Slab& s = ctx->slabs[j];
+    CKS(alpha ? reduce_to(ctx, s, s.part_x, nblk[j], 10, 1) : reduce_to(ctx, s, s.part_cg, nblk[j], 2, 0));
+  }
+  CKS(alpha ? allreduce(ctx, 1, 10, false) : allreduce(ctx, 0, 2, false));
+  for (Slab& s : ctx->slabs) {
+    ProfScope ps(ctx, PK_FIN);
+    CK(alpha ? launch_fin_alpha(s.cg, s.loc, ctx->stream) : launch_fin_beta(s.cg, s.loc, ctx->stream));
+  }
+  return DBFFT_OK;
+}
+
 // end of an iteration: x += alpha p owed by the direction kernel is settled; slab 0's k_fin_x
 // decides whether the device-side loop runs again (all slabs hold the same reduced scalars)
 dbfft_status fin_x_all(dbfft_ctx ctx, cudaGraphConditionalHandle cond) {
@@ -1251,15 +1273,7 @@ dbfft_status pcg_iteration_fused(dbfft_ctx ctx, bool macro, int nb, cudaGraphCon
   const bool fin = ctx->kin == 9;
   ApplyOut ao;
   CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, macro, &CgDev::pe, &ao, true, true));
-  for (size_t j = 0; j < ctx->slabs.size(); ++j) {
-    Slab& s = ctx->slabs[j];
-    CKS(reduce_to(ctx, s, s.part_x, ao.grid_x[j], 10, 1));
-  }
-  CKS(allreduce(ctx, 1, 10, false));
-  for (Slab& s : ctx->slabs) {
-    ProfScope ps(ctx, PK_FIN);
-    CK(launch_fin_alpha(s.cg, s.loc, ctx->stream));
-  }
+  CKS(reduce_fin(ctx, ao.grid_x, true));
   for (Slab& s : ctx->slabs) {
     ColGeom g = geom_F2(ctx, s, s.WB, s.WS2, 6, nf_B(ctx));
     guard_geom(g, s);
@@ -1270,14 +1284,9 @@ dbfft_status pcg_iteration_fused(dbfft_ctx ctx, bool macro, int nb, cudaGraphCon
   for (size_t j = 0; j < ctx->slabs.size(); ++j) {
     Slab& s = ctx->slabs[j];
     CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_F3, geom_F3_update(ctx, s), ctx->n3, &g3[j]));
-    CKS(reduce_to(ctx, s, s.part_cg, g3[j], 2, 0));
   }
-  CKS(allreduce(ctx, 0, 2, false));
+  CKS(reduce_fin(ctx, g3, false));
   for (Slab& s : ctx->slabs) {
-    {
-      ProfScope ps(ctx, PK_FIN);
-      CK(launch_fin_beta(s.cg, s.loc, ctx->stream));
-    }
     {
       ProfScope ps(ctx, PK_CGDIR);
       CK(launch_cg_direction(spec(ctx, s), ctx->prec_dev, s.cg, s.x, s.p, s.r, ctx->stream));
@@ -1296,28 +1305,13 @@ dbfft_status pcg_body(dbfft_ctx ctx, int every, bool macro, int nb, cudaGraphCon
     // <p, A p> comes from the X pass (slot 9: sum (grad p + p_e) : sigma, Parseval), so F3 does
     // not re-read p
     CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, macro, &CgDev::pe, &ao, false, true));
-    for (size_t j = 0; j < ctx->slabs.size(); ++j) {
-      Slab& s = ctx->slabs[j];
-      CKS(reduce_to(ctx, s, s.part_x, ao.grid_x[j], 10, 1));
-    }
-    CKS(allreduce(ctx, 1, 10, false));
+    CKS(reduce_fin(ctx, ao.grid_x, true));
     for (Slab& s : ctx->slabs) {
-      {
-        ProfScope ps(ctx, PK_FIN);
-        CK(launch_fin_alpha(s.cg, s.loc, ctx->stream));
-      }
-      {
-        ProfScope ps(ctx, PK_CGUPD);
-        CK(launch_cg_update(spec(ctx, s), ctx->prec_dev, s.cg, s.r, s.q, s.part_cg, nb, ctx->stream));
-      }
-      CKS(reduce_to(ctx, s, s.part_cg, nb, 2, 0));
+      ProfScope ps(ctx, PK_CGUPD);
+      CK(launch_cg_update(spec(ctx, s), ctx->prec_dev, s.cg, s.r, s.q, s.part_cg, nb, ctx->stream));
     }
-    CKS(allreduce(ctx, 0, 2, false));
+    CKS(reduce_fin(ctx, std::vector<int>(ctx->slabs.size(), nb), false));
     for (Slab& s : ctx->slabs) {
-      {
-        ProfScope ps(ctx, PK_FIN);
-        CK(launch_fin_beta(s.cg, s.loc, ctx->stream));
-      }
       {
         ProfScope ps(ctx, PK_CGDIR);
         CK(launch_cg_direction(spec(ctx, s), ctx->prec_dev, s.cg, s.x, s.p, s.r, ctx->stream));
