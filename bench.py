@@ -143,6 +143,25 @@ def bytes_apply_K(n, variant, kin=9):
     return 16 * (66 if kin == 9 else 52) * H + TANGENT_BYTES[variant] * N
 
 
+def pcg_iteration_roofline(n, variant, t, iters, world, slab, peak):
+    """SURVEY 8(d) "% HBM roofline of the full PCG iteration": the timed region's time per PCG
+    iteration (Newton-step work — constitutive updates, true residuals — included) against
+    B_iter = B_op + B_cg, the survey's per-axis model (full tangent, 480 H of CG vectors) at 8 TB/s,
+    and against this schedule's algorithmic bytes (compact tangent; CG: 8 vector transfers of 48 H)
+    at the measured copy peak.  Slabs: per GPU, the global bytes / world."""
+    if not iters:
+        return None
+    n1, n2, n3 = n
+    H = (n1 // 2 + 1) * n2 * n3
+    t_it = t / (iters if slab or world == 1 else iters / world)  # one iteration of one problem
+    share = world if slab else 1
+    b_model = (bytes_apply_K(n, "full") + 480 * H) / share
+    b_alg = (bytes_apply_K(n, variant) + 8 * 48 * H) / share
+    return {"ms": t_it * 1e3, "survey_model_bytes": b_model, "survey_model_ms_8TBps": b_model / 8e12 * 1e3,
+            "frac_of_survey_model": b_model / 8e12 / t_it, "algorithmic_bytes": b_alg,
+            "achieved_GBps": b_alg / t_it / 1e9, "frac": b_alg / t_it / 1e9 / peak if peak else None}
+
+
 def aggregate_over_ranks(t_local, iters, device="cuda"):
     """(max over ranks of the timed region, sum over ranks of the PCG iterations)."""
     import torch
@@ -327,7 +346,8 @@ def gpu_arm(args):
                             "algorithmic_bytes": bytes_apply_K(n, variant), "avg_ms": op_ms / n_op,
                             "achieved_GBps": op_gbs, "frac": (op_gbs / peak) if op_gbs else None,
                             "survey_model_ms_8TBps": t_model,
-                            "frac_of_survey_model": t_model / (op_ms / n_op / 1e3)}}
+                            "frac_of_survey_model": t_model / (op_ms / n_op / 1e3)},
+                "pcg_iteration": pcg_iteration_roofline(n, variant, t_max, tot_iters, world, slab, peak)}
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
            "scaling": "strong" if slab else "weak",
