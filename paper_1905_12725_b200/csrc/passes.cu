@@ -121,6 +121,9 @@ int num_sms() {
 #ifndef DBF_X_PREFETCH
 #define DBF_X_PREFETCH 1  // pass_X: bulk L2 prefetch of the next line group's per-voxel tangent rows
 #endif
+#ifndef DBF_X_L1PF
+#define DBF_X_L1PF 0  // 1: neo-Hookean apply prefetches its line's tangent rows to L1 (CCTL.E.PF1) while the C2R runs (256^3: 0.926 -> 0.928 ms, no gain)
+#endif
 #ifndef DBF_X_TBATCH
 #define DBF_X_TBATCH 0  // neo-Hookean apply: both voxels' tangent rows loaded before either contraction
 #endif
@@ -942,6 +945,7 @@ struct XPref {
                                               : (KIND == X_K_J2) ? (DBF_X_STAGE_TAN_J2 ? 0 : 8)
                                               : (KIND == X_K_FIN_TAN) ? 45 : 0) : 0;
 };
+DBF_DEV void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p) : "memory"); }
 DBF_DEV void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
@@ -1103,6 +1107,14 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
       const uint32_t bytes = (uint32_t)(sizeof(double) * N1 * min((long long)LPAR, g.nlines - (grp + gridDim.x) * LPAR));
 #pragma unroll 1
       for (int k = 0; k < XPref<KIND>::NTAN; ++k) prefetch_l2(g.tan + (long long)k * g.nvox + v1, bytes);
+    }
+    // this group's rows (L2-resident since the previous group's prefetch) go on to L1 while the C2R
+    // runs: the voxel loop's 10 loads per voxel then wait for an L1 hit, not an L2 round trip
+    if constexpr (DBF_X_L1PF && KIND == X_K_FIN_NH && S::NTAN == 0 && LPAR == 1 && (N1 % 16) == 0) {
+      constexpr int LPR = N1 / 16;  // 128-byte lines per tangent row of one voxel line
+      const long long v0 = grp * N1;
+      for (int i = t; i < 10 * LPR; i += CF::THREADS) prefetch_l1(g.tan + (long long)(i / LPR) * g.nvox + v0 + (i % LPR) * 16);
+      if (!S::PH && t < (N1 + 63) / 64) prefetch_l1(g.phase + v0 + t * 64);
     }
     const bool va = linea < g.nlines, vb = lineb < g.nlines;
     const long long nxt = grp + gridDim.x;
