@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_cg_init(SpecGeom g, const PrecQ* 
 // direction kernel, which reads p anyway: 3 vector transfers here instead of 6)
 __global__ void __launch_bounds__(BLK, MINB) k_cg_update(SpecGeom g, const PrecQ* __restrict__ pq, const CgDev* __restrict__ cg, cplx* __restrict__ r,
                                                    const cplx* __restrict__ qv, double* partials) {
-  DBF_PDL_ENTRY();
+  DBF_PDL_ENTRY_BIG();
   if (cg->converged | cg->breakdown) return;
   __shared__ PrecQ Q;
   load_prec(Q, pq);
@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_cg_update(SpecGeom g, const PrecQ
       acc[1] += p.w * cdot(rv[c], rv[c]);
     }
   }
+  DBF_PDL_EXIT();
   block_store<2>(acc, partials);
 }
 
@@ -161,7 +162,7 @@ DBF_DEV void cg_direction_body(const SpecGeom& g, const PrecQ& Q, double alpha, 
 
 __global__ void __launch_bounds__(BLK, 2) k_cg_direction(SpecGeom g, const PrecQ* __restrict__ q, const CgDev* __restrict__ cg, cplx* __restrict__ x,
                                                       cplx* __restrict__ pv, const cplx* __restrict__ r) {
-  DBF_PDL_ENTRY();
+  DBF_PDL_ENTRY_BIG();
   if (cg->breakdown) return;
   __shared__ PrecQ Q;
   load_prec(Q, q);

@@ -28,6 +28,21 @@ DBF_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
     pdl_trigger();      \
     pdl_wait();         \
   } while (0)
+// DBF_PDL_LATE=1: the big kernels (passes, k_cg_update, k_cg_direction) let their successor launch
+// only once a CTA has finished its main loop (DBF_PDL_EXIT), so that the successor's CTAs take
+// an SM as this grid drains instead of queueing behind it from the start.
+#ifndef DBF_PDL_LATE
+#define DBF_PDL_LATE 0
+#endif
+#define DBF_PDL_ENTRY_BIG()            \
+  do {                                 \
+    if (!DBF_PDL_LATE) pdl_trigger();  \
+    pdl_wait();                        \
+  } while (0)
+#define DBF_PDL_EXIT()               \
+  do {                               \
+    if (DBF_PDL_LATE) pdl_trigger(); \
+  } while (0)
 
 bool pdl_enabled();  // DBFFT_PDL=1 (default off, see passes.cu)
 template <typename... KArgs, typename... Args>

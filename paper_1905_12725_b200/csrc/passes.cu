@@ -392,7 +392,7 @@ struct ColPref {
 
 template <int N, int KIND>
 __global__ void __launch_bounds__(256, ColCfg<N>::ODD ? 1 : ColPref<KIND>::MINB) col_pass_kernel(ColGeom g) {
-  DBF_PDL_ENTRY();
+  DBF_PDL_ENTRY_BIG();
   if (g.cg_stop0 && (*g.cg_stop0 | *g.cg_stop1)) return;  // PCG stopped: nothing to compute
   typedef ColOp<KIND> Op;
   typedef ColCfg<N> CF;
@@ -1029,7 +1029,7 @@ DBF_DEV void x_issue_tan(const XGeom& g, long long grp, double* st_tan, uint16_t
 // bulk async copies (cp.async.bulk -> TMA engine, mbarrier completion) while group i computes.
 template <int N1, int KIND>
 __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB) x_pass_kernel(XGeom g, int nf_real) {
-  DBF_PDL_ENTRY();
+  DBF_PDL_ENTRY_BIG();
   if (g.stop0 && (*g.stop0 | *g.stop1)) return;  // PCG stopped: nothing to compute
   typedef XCfg<N1, KIND> CF;
   typedef XTraits<KIND> T;
@@ -1353,6 +1353,7 @@ __global__ void __launch_bounds__(XCfg<N1, KIND>::THREADS, XCfg<N1, KIND>::MINB)
       for (int w = 0; w < (FULLW ? nw : CF::THREADS); ++w) s = is_max ? fmax(s, sred[w]) : s + sred[w];
     return s;
   };
+  DBF_PDL_EXIT();
   if (DCRED) {
     const double xs = block_red(xdot, false);
     if (t < T::NRED) {
@@ -1796,11 +1797,11 @@ struct TmaMaps {
 
 template <int N, int KIND, bool DOT, int R, bool UPD = false>
 __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __grid_constant__ TmaMaps maps, ColGeom g, ColTiles tl) {
-  DBF_PDL_ENTRY();
+  if (!DBF_PDL_LATE) DBF_PDL_ENTRY_BIG();
   typedef ColOp<KIND> Op;
   typedef TmaCfg<N> CF;
   constexpr bool TAB = ColTab<N, KIND>::value && (!UPD || DBF_UPD_TAB);
-  if (g.cg_stop0 && (*g.cg_stop0 | *g.cg_stop1)) return;  // PCG stopped (UPD: r stays as it is)
+  if (!DBF_PDL_LATE && g.cg_stop0 && (*g.cg_stop0 | *g.cg_stop1)) return;  // PCG stopped (UPD: r stays as it is)
   constexpr int KC = CF::KC, TPC = CF::TPC;
   constexpr int S = UPD ? 3 : 2;  // staging buffers (UPD: r_0, r_1 of a tile stay readable until r_2)
   extern __shared__ __align__(1024) unsigned char tsm[];
@@ -1826,6 +1827,10 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
   if (TAB)
     for (int i = t; i < N - 1; i += CF::THREADS) stab[i] = __ldg(g.tw + N + i);
   __syncthreads();
+  if (DBF_PDL_LATE) {  // the prologue above touched only constant tables: wait for the predecessor here
+    DBF_PDL_ENTRY_BIG();
+    if (g.cg_stop0 && (*g.cg_stop0 | *g.cg_stop1)) return;
+  }
   const int nl = pg.nl;
 
   if (warp == CF::CONS / 32) {
@@ -1978,6 +1983,7 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
       }
     }
   }
+  DBF_PDL_EXIT();
   if (t == 0) bulk_wait_all();
   if (UPD) {
     __shared__ double red2[8][2];
