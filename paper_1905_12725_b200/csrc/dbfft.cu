@@ -1039,7 +1039,11 @@ dbfft_status build_loop_graph(dbfft_ctx ctx, bool macro, int nb, dbfft_ctx_s::Lo
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   CK(cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   const long long nl0 = ctx->nlaunch;
-  const dbfft_status bst = pcg_body(ctx, 1, macro, nb, h);
+  // DBFFT_LOOP_UNROLL=k: k PCG iterations per evaluation of the WHILE condition (after convergence
+  // the rest of a body exits pass by pass, as in the host-polled rounds); default 1
+  int unroll = 1;
+  if (const char* ue = getenv("DBFFT_LOOP_UNROLL")) unroll = std::min(8, std::max(1, atoi(ue)));
+  const dbfft_status bst = pcg_body(ctx, unroll, macro, nb, h);
   if (bst != DBFFT_OK) {
     abort_capture(ctx);
     return bst;
