@@ -161,15 +161,38 @@ DBF_DEV void cg_direction_body(const SpecGeom& g, const PrecQ& Q, double alpha, 
 }
 
 __global__ void __launch_bounds__(BLK, 2) k_cg_direction(SpecGeom g, const PrecQ* __restrict__ q, const CgDev* __restrict__ cg, cplx* __restrict__ x,
-                                                      cplx* __restrict__ pv, const cplx* __restrict__ r) {
+                                                      cplx* __restrict__ pv, const cplx* __restrict__ r, int x_done) {
   DBF_PDL_ENTRY_BIG();
   if (cg->breakdown) return;
   __shared__ PrecQ Q;
   load_prec(Q, q);
-  const bool do_x = cg->xphase != 0, do_p = cg->converged == 0;
+  const bool do_x = cg->xphase != 0 && !x_done, do_p = cg->converged == 0;
   if (do_x && do_p) cg_direction_body<true, true>(g, Q, cg->alpha, cg->beta, x, pv, r);
   else if (do_p) cg_direction_body<false, true>(g, Q, cg->alpha, cg->beta, x, pv, r);
   else if (do_x) cg_direction_body<true, false>(g, Q, cg->alpha, cg->beta, x, pv, r);
+}
+
+// x += alpha p on a side stream, beside the forward passes of the same iteration (DBFFT_XOVERLAP=1):
+// alpha is final since k_fin_alpha and p stays as it is until the direction kernel, which then runs
+// with x_done = 1 (3 vector transfers instead of 5).  Same fma as cg_direction_body.
+__global__ void __launch_bounds__(BLK, 2) k_cg_xupdate(SpecGeom g, const CgDev* __restrict__ cg, cplx* __restrict__ x, const cplx* __restrict__ pv) {
+  DBF_PDL_ENTRY();
+  if (cg->breakdown | (cg->xphase == 0)) return;
+  const double alpha = cg->alpha;
+  for (long long i = (long long)blockIdx.x * BLK + threadIdx.x; i < g.Hs; i += (long long)gridDim.x * BLK) {
+    cplx pj[3], xj[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      pj[c] = __ldg(pv + c * g.Hs + i);
+      xj[c] = x[c * g.Hs + i];
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      xj[c].x = fma(alpha, pj[c].x, xj[c].x);
+      xj[c].y = fma(alpha, pj[c].y, xj[c].y);
+      x[c * g.Hs + i] = xj[c];
+    }
+  }
 }
 
 // end of a PCG iteration; inside the device-side loop (a CUDA graph WHILE node) it also decides
@@ -451,8 +474,12 @@ cudaError_t launch_cg_update(const SpecGeom& g, const PrecQ* q, CgDev* cg, cplx*
                              double* partials, int nblk, cudaStream_t s) {
   return launch_k(k_cg_update, nblk, BLK, 0, s, g, q, cg, r, qv, partials);
 }
-cudaError_t launch_cg_direction(const SpecGeom& g, const PrecQ* q, const CgDev* cg, cplx* x, cplx* p, const cplx* r, cudaStream_t s) {
-  return launch_k(k_cg_direction, nblk_dir(), BLK, 0, s, g, q, cg, x, p, r);
+cudaError_t launch_cg_direction(const SpecGeom& g, const PrecQ* q, const CgDev* cg, cplx* x, cplx* p, const cplx* r, cudaStream_t s,
+                                int x_done) {
+  return launch_k(k_cg_direction, nblk_dir(), BLK, 0, s, g, q, cg, x, p, r, x_done);
+}
+cudaError_t launch_cg_xupdate(const SpecGeom& g, const CgDev* cg, cplx* x, const cplx* p, int ctas_per_sm, cudaStream_t s) {
+  return launch_k(k_cg_xupdate, ctas_per_sm * num_sms(), BLK, 0, s, g, cg, x, p);
 }
 cudaError_t launch_fin_x(CgDev* cg, cudaStream_t s, cudaGraphConditionalHandle cond, int set_cond) {
   return launch_k(k_fin_x, 1, 32, 0, s, cg, cond, set_cond);

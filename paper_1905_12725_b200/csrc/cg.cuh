@@ -38,7 +38,9 @@ cudaError_t launch_precond(const SpecGeom& g, const PrecQ* q, const cplx* r, cpl
 cudaError_t launch_cg_init(const SpecGeom& g, const PrecQ* q, const cplx* r, cplx* p, double* partials, int nblk, cudaStream_t s);
 cudaError_t launch_cg_update(const SpecGeom& g, const PrecQ* q, CgDev* cg, cplx* r, const cplx* qv,
                              double* partials, int nblk, cudaStream_t s);
-cudaError_t launch_cg_direction(const SpecGeom& g, const PrecQ* q, const CgDev* cg, cplx* x, cplx* p, const cplx* r, cudaStream_t s);
+cudaError_t launch_cg_direction(const SpecGeom& g, const PrecQ* q, const CgDev* cg, cplx* x, cplx* p, const cplx* r, cudaStream_t s,
+                                int x_done = 0);
+cudaError_t launch_cg_xupdate(const SpecGeom& g, const CgDev* cg, cplx* x, const cplx* p, int ctas_per_sm, cudaStream_t s);
 // cond/set_cond: inside the device-side PCG loop (CUDA graph WHILE node) k_fin_x also sets the
 // loop condition to "not converged and no breakdown"
 cudaError_t launch_fin_x(CgDev* cg, cudaStream_t s, cudaGraphConditionalHandle cond = 0, int set_cond = 0);

@@ -151,6 +151,11 @@ struct dbfft_ctx_s {
   int device;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  // DBFFT_XOVERLAP=k (k CTAs per SM): x += alpha p runs on `side`, forked after alpha and joined
+  // before the direction kernel (pcg_body)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int xoverlap = 0;
   // device allocations: the caller's allocator (e.g. torch's caching allocator) or cudaMalloc
   void* (*dev_alloc)(size_t, void*) = nullptr;
   void (*dev_free)(void*, void*) = nullptr;
@@ -1308,17 +1313,44 @@ dbfft_status pcg_body(dbfft_ctx ctx, int every, bool macro, int nb, cudaGraphCon
     ApplyOut ao;
     // <p, A p> comes from the X pass (slot 9: sum (grad p + p_e) : sigma, Parseval), so F3 does
     // not re-read p
-    CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, macro, &CgDev::pe, &ao, false, true));
-    CKS(reduce_fin(ctx, ao.grid_x, true));
+    if (ctx->xoverlap) {
+      // alpha right after the X pass; x += alpha p on the side stream beside F2 / F3 / the residual
+      // update (joined before the direction kernel, which alone writes p)
+      CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, macro, &CgDev::pe, &ao, true, true));
+      CKS(reduce_fin(ctx, ao.grid_x, true));
+      CK(cudaEventRecord(ctx->ev_fork, ctx->stream));
+      CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+      for (Slab& s : ctx->slabs) {
+        ctx->nlaunch += 1;
+        CK(launch_cg_xupdate(spec(ctx, s), s.cg, s.x, s.p, ctx->xoverlap, ctx->side));
+      }
+      CK(cudaEventRecord(ctx->ev_join, ctx->side));
+      const bool fin = ctx->kin == 9;
+      for (Slab& s : ctx->slabs) {
+        ColGeom g = geom_F2(ctx, s, s.WB, s.WS2, 6, nf_B(ctx));
+        guard_geom(g, s);
+        CKS(run_col(ctx, fin ? COL_F2F : COL_F2S, PK_F2, g, ctx->n2));
+      }
+      CKS(exchange(ctx, (long long)6 * ctx->slabs[0].nyl * ctx->slabs[0].nzl * ctx->kxp));
+      for (Slab& s : ctx->slabs) {
+        ColGeom g = geom_F3(ctx, s, s.WR2, s.q, 6);
+        guard_geom(g, s);
+        CKS(run_col(ctx, fin ? COL_F3F : COL_F3S, PK_F3, g, ctx->n3));
+      }
+    } else {
+      CKS(apply_K_slabs(ctx, &Slab::p, &Slab::q, macro, &CgDev::pe, &ao, false, true));
+      CKS(reduce_fin(ctx, ao.grid_x, true));
+    }
     for (Slab& s : ctx->slabs) {
       ProfScope ps(ctx, PK_CGUPD);
       CK(launch_cg_update(spec(ctx, s), ctx->prec_dev, s.cg, s.r, s.q, s.part_cg, nb, ctx->stream));
     }
     CKS(reduce_fin(ctx, std::vector<int>(ctx->slabs.size(), nb), false));
+    if (ctx->xoverlap) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
     for (Slab& s : ctx->slabs) {
       {
         ProfScope ps(ctx, PK_CGDIR);
-        CK(launch_cg_direction(spec(ctx, s), ctx->prec_dev, s.cg, s.x, s.p, s.r, ctx->stream));
+        CK(launch_cg_direction(spec(ctx, s), ctx->prec_dev, s.cg, s.x, s.p, s.r, ctx->stream, ctx->xoverlap ? 1 : 0));
       }
     }
     CKS(fin_x_all(ctx, cond));
@@ -1656,6 +1688,9 @@ void free_all(dbfft_ctx ctx) {
   if (ctx->h_bad) cudaFreeHost(ctx->h_bad);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
 }
 
@@ -1963,6 +1998,15 @@ dbfft_status dbfft_create(const int32_t n[3], const double L[3], int32_t kinemat
       return fail(DBFFT_E_CUDA);
     }
     ctx->own_stream = true;
+  }
+  if (const char* xo = getenv("DBFFT_XOVERLAP")) {
+    ctx->xoverlap = std::min(4, std::max(0, atoi(xo)));
+    if (ctx->xoverlap && (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+                          cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+                          cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess)) {
+      ctx->err = "DBFFT_XOVERLAP: side stream / events could not be created";
+      return fail(DBFFT_E_CUDA);
+    }
   }
   dbfft_status s;
   std::vector<double> hx = axis_xi(ctx->n1, L[0], ctx->n1h), hy = axis_xi(ctx->n2, L[1], ctx->n2), hz = axis_xi(ctx->n3, L[2], ctx->n3);
