@@ -136,6 +136,11 @@ int num_sms() {
 #ifndef DBF_COL_MINB
 #define DBF_COL_MINB 4
 #endif
+// (the 168-register cap of these 288-thread kernels is the hardware's: 9 warps put 3 on one SM
+// sub-partition of 16 K registers; __maxnreg__(208) fails to launch)
+#ifndef DBF_COL_XINPLACE
+#define DBF_COL_XINPLACE 0  // 1: TMA column passes run their FFT exchanges inside the output tile's own staging slots (no 32 KB exchange buffer, 60 KB of L1 instead of 28): parity green, 4-10 % slower (256^3 finite I1 0.257 -> 0.282, F2 0.432 -> 0.471 ms)
+#endif
 #ifndef DBF_UPD_TAB
 #define DBF_UPD_TAB 0  // the fused F3 + residual update with the stage table (and a 2-slot ring to fit)
 #endif
@@ -1775,6 +1780,25 @@ struct SyncCol {
 // tail tile: [KC][N] unswizzled
 template <int N>
 DBF_DEV int tma_toff(int pos, int c) { return c * N + pos; }
+// FFT exchange index inside a staging tile: column c keeps to its own 16-byte slots of the tile
+// layout (so a warp never touches another column's), positions XOR-swizzled as in IdxSwz — the
+// slot's bank group depends on pos & 7 only, in both layouts, so scatter and gather stay
+// conflict-free
+template <int N>
+struct IdxTile {
+  int cb, sh, sw, sm;  // per tile and column: base, log2 row pitch, swizzle term and mask (tail tiles: 0)
+  DBF_DEV IdxTile(int c, bool tail) {
+    constexpr int SW = TmaCfg<N>::SW;
+    cb = tail ? c * N : (c / SW) * (N * SW);
+    sh = tail ? 0 : (SW == 8 ? 3 : 2);
+    sw = tail ? 0 : c % SW;
+    sm = tail ? 0 : SW - 1;
+  }
+  DBF_DEV int operator()(int pos) const {
+    const int p = pos ^ ((pos >> 3) & 7);
+    return cb + (p << sh) + (sw ^ ((TmaCfg<N>::SW == 8 ? p : (p >> 1)) & sm));
+  }
+};
 
 DBF_DEV void tma_load5(void* dst, const CUtensorMap* m, int c0, int c1, int c2, int c3, int c4, uint64_t* bar) {
   asm volatile(
@@ -1808,10 +1832,14 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
   // 1024-byte alignment of the ring (128B swizzle atoms)
   // (offset arithmetic on the shared array keeps the shared address space: LDS/STS, not LD/ST)
   unsigned char* base = tsm + ((1024u - (smem_u32(tsm) & 1023u)) & 1023u);
+  // XIN: the exchanges of a term run inside the staging buffer its output goes to (free since the
+  // barrier of the previous output: the store two outputs back has been read), so there is no
+  // separate exchange buffer; the fused update reads earlier staging buffers and keeps one
+  constexpr bool XIN = DBF_COL_XINPLACE && !UPD;
   cplx* ring = reinterpret_cast<cplx*>(base);
   cplx* stg = reinterpret_cast<cplx*>(base + R * CF::TILE);
   cplx* xb = reinterpret_cast<cplx*>(base + (R + S) * CF::TILE);
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + (R + S + 1) * CF::TILE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + (R + S + (XIN ? 0 : 1)) * CF::TILE);
   uint64_t* empty = full + R;
   cplx* stab = reinterpret_cast<cplx*>(empty + R);  // stage-ordered twiddles (N - 1), copied once
   const TProg& pg = c_prog[2 * KIND + (DOT ? 1 : 0)];
@@ -1918,7 +1946,17 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
         const cplx v1 = (lb >= 0) ? sbp[o] : v0;
         a[s] = Op::pre(at, j, v0, v1);
       }
-      if constexpr (TPC <= 32) fft_cta<N, Op::INV, IdxSwz, SyncWarp, TAB>(a, xcol, gq, IdxSwz{0}, TAB ? stab : g.tw, SyncWarp{});
+      cplx* so = stg + (nout % S) * (CF::TILE / 16);
+      if constexpr (XIN) {
+        const IdxTile<N> ix(c, tail);
+        if constexpr (TPC <= 32) {
+          fft_cta<N, Op::INV, IdxTile<N>, SyncWarp, TAB>(a, so, gq, ix, TAB ? stab : g.tw, SyncWarp{});
+          SyncWarp{}();  // the column's last gathers are done before its outputs overwrite the slots
+        } else {
+          fft_cta<N, Op::INV, IdxTile<N>, SyncCol, TAB>(a, so, gq, ix, TAB ? stab : g.tw, SyncCol{2 + c, TPC});
+          SyncCol{2 + c, TPC}();
+        }
+      } else if constexpr (TPC <= 32) fft_cta<N, Op::INV, IdxSwz, SyncWarp, TAB>(a, xcol, gq, IdxSwz{0}, TAB ? stab : g.tw, SyncWarp{});
       else fft_cta<N, Op::INV, IdxSwz, SyncCol, TAB>(a, xcol, gq, IdxSwz{0}, TAB ? stab : g.tw, SyncCol{2 + c, TPC});
       const int ai = pg.acc[k];
       const int ld = pg.ldot[k];
@@ -1928,7 +1966,6 @@ __global__ void __launch_bounds__(TmaCfg<N>::THREADS, 1) col_tma_kernel(const __
         mbar_wait(&full[qd % R], (qd / R) & 1);
         sd = ring + (qd % R) * (CF::TILE / 16);
       }
-      cplx* so = stg + (nout % S) * (CF::TILE / 16);
 #pragma unroll
       for (int s = 0; s < 8; ++s) {
         at.pos = gq + s * TPC;
@@ -2171,7 +2208,7 @@ struct ColRingL {
 template <int N, int KIND, bool DOT, bool UPD = false>
 static cudaError_t launch_col_tma_k(const TmaMaps& maps, const ColGeom& g, const ColTiles& tl, cudaStream_t s, int* grid_out) {
   constexpr int R = ColRingL<N, KIND, DOT, UPD>::R;
-  constexpr size_t smem = (size_t)(R + (UPD ? 3 : 2) + 1) * TmaCfg<N>::TILE + 2 * R * sizeof(uint64_t) +
+  constexpr size_t smem = (size_t)(R + (UPD ? 3 : 2) + ((DBF_COL_XINPLACE && !UPD) ? 0 : 1)) * TmaCfg<N>::TILE + 2 * R * sizeof(uint64_t) +
                           (ColRingL<N, KIND, DOT, UPD>::TAB ? sizeof(cplx) * N : 0) + 1024;
   static DevOnce once;
   cudaError_t e = dev_once(once, [](int&) {
